@@ -1,0 +1,433 @@
+/*
+ * oracle/frob_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously-correct CPU oracle for Frobenius inversion of complex
+ * matrices (Dai, Lim & Ye, arXiv 2208.01239).  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load this library.  It
+ * shares no code, header, table or helper with the CUDA path in
+ * paper_2208_01239_b200/csrc, and the CUDA path never calls it.
+ *
+ * Everything is IEEE fp64, row-major, planar (real part and imaginary part in two
+ * separate n*n arrays, leading dimension n).  Compiled with -ffp-contract=off so
+ * every multiply and add rounds separately; OpenMP only splits independent rows or
+ * columns, so the rounding order of every entry is fixed and independent of the
+ * thread count.
+ *
+ * Paper passages followed (P:Lxxx = line of the paper's LaTeX source):
+ *   or_dgetrf        Alg 3 line 1 "compute LU factorization of A = LU", partial
+ *                    pivoting, first index of max |a_ik| (LAPACK idamax convention).
+ *   or_dtrtri_upper  Alg 3 line 2 "compute U^{-1}" by column substitutions
+ *                    ("inverting a triangular matrix can be done by a sequence of ...
+ *                    substitutions", proof of Thm 5.1).
+ *   or_dgetri_solve  Alg 3 line 3 "solve for X from XL = U^{-1}", then the column
+ *                    interchanges that undo P (A = P^T L U  =>  A^{-1} = U^{-1} L^{-1} P).
+ *   or_dinv          Alg 3 = the real inversion inv_{n,R} used twice by Alg 1.
+ *   or_dgemm         m_{n,R}: C = A B, plain triple loop, k ascending.
+ *   or_frob_inv      Alg 1 "Frobenius inversion I" with tau = 1 (f = x^2+1,
+ *                    P:L123): S1 branch returns J - iK, S2 branch returns K - iJ.  The
+ *                    numerical branch choice (the paper's S1/S2 are algebraic)
+ *                    follows DESIGN.md reading R1.
+ *   or_zinv_gj       The plain definition: complex Gauss-Jordan inverse with partial
+ *                    pivoting on |re|+|im| (the object Lemma 4.1, reaches exactly).
+ *   or_zinv_lu       Alg 3 applied over C (the paper's comparator).
+ */
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORACLE_EPS 1.1102230246251565e-16 /* u = 2^-53, unit roundoff of fp64 */
+
+/* ------------------------------------------------------------------ real */
+
+/* LU with partial pivoting, in place.  On return a holds L (strict lower, unit
+ * diagonal implied) and U (upper); ipiv[k] = row swapped with row k at step k
+ * (0-based, LAPACK order).  Returns 0 or the 1-based index of the first exactly
+ * zero pivot (elimination of that column is skipped, as LAPACK does). */
+int or_dgetrf(int n, double *a, int *ipiv)
+{
+    int info = 0;
+    for (int k = 0; k < n; ++k) {
+        int p = k;
+        double best = fabs(a[(size_t)k * n + k]);
+        for (int i = k + 1; i < n; ++i) {
+            double v = fabs(a[(size_t)i * n + k]);
+            if (v > best) { best = v; p = i; }
+        }
+        ipiv[k] = p;
+        if (p != k) {
+            for (int j = 0; j < n; ++j) {
+                double t = a[(size_t)k * n + j];
+                a[(size_t)k * n + j] = a[(size_t)p * n + j];
+                a[(size_t)p * n + j] = t;
+            }
+        }
+        double piv = a[(size_t)k * n + k];
+        if (piv == 0.0) { if (!info) info = k + 1; continue; }
+        #pragma omp parallel for schedule(static) if (n - k > 256)
+        for (int i = k + 1; i < n; ++i) {
+            double l = a[(size_t)i * n + k] / piv;
+            a[(size_t)i * n + k] = l;
+            for (int j = k + 1; j < n; ++j)
+                a[(size_t)i * n + j] = a[(size_t)i * n + j] - l * a[(size_t)k * n + j];
+        }
+    }
+    return info;
+}
+
+/* X = U^{-1} for the upper triangle U of lu (out of place, X full n*n with zeros
+ * below the diagonal).  Column j solves U x = e_j by back substitution. */
+int or_dtrtri_upper(int n, const double *lu, double *x)
+{
+    for (int j = 0; j < n; ++j)
+        if (lu[(size_t)j * n + j] == 0.0) return j + 1;
+    double *xt = (double *)malloc(sizeof(double) * (size_t)n * n); /* xt[j*n+i] = X[i][j] */
+    #pragma omp parallel for schedule(dynamic, 8) if (n > 128)
+    for (int j = 0; j < n; ++j) {
+        double *col = xt + (size_t)j * n;
+        for (int i = j + 1; i < n; ++i) col[i] = 0.0;
+        col[j] = 1.0 / lu[(size_t)j * n + j];
+        for (int i = j - 1; i >= 0; --i) {
+            double s = 0.0;
+            for (int k = i + 1; k <= j; ++k) s = s + lu[(size_t)i * n + k] * col[k];
+            col[i] = -s / lu[(size_t)i * n + i];
+        }
+    }
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) x[(size_t)i * n + j] = xt[(size_t)j * n + i];
+    free(xt);
+    return 0;
+}
+
+/* Solve X L = W for X (L = unit lower triangle of lu), column j from n-1 down to 0:
+ * X[:,j] = W[:,j] - sum_{k>j} X[:,k] L[k][j].  Rows are independent. */
+void or_dgetri_solve(int n, const double *lu, const double *w, double *x)
+{
+    double *lt = (double *)malloc(sizeof(double) * (size_t)n * n); /* lt[j*n+k] = L[k][j] */
+    for (int k = 0; k < n; ++k)
+        for (int j = 0; j < n; ++j) lt[(size_t)j * n + k] = lu[(size_t)k * n + j];
+    #pragma omp parallel for schedule(static) if (n > 128)
+    for (int i = 0; i < n; ++i) {
+        double *xi = x + (size_t)i * n;
+        const double *wi = w + (size_t)i * n;
+        for (int j = n - 1; j >= 0; --j) {
+            double s = 0.0;
+            const double *lj = lt + (size_t)j * n;
+            for (int k = j + 1; k < n; ++k) s = s + xi[k] * lj[k];
+            xi[j] = wi[j] - s;
+        }
+    }
+    free(lt);
+}
+
+/* A^{-1} = X P: undo the row interchanges as column interchanges, last first. */
+void or_col_unswap(int n, double *x, const int *ipiv)
+{
+    for (int k = n - 1; k >= 0; --k) {
+        int p = ipiv[k];
+        if (p == k) continue;
+        for (int i = 0; i < n; ++i) {
+            double t = x[(size_t)i * n + k];
+            x[(size_t)i * n + k] = x[(size_t)i * n + p];
+            x[(size_t)i * n + p] = t;
+        }
+    }
+}
+
+static double max_abs(size_t cnt, const double *v)
+{
+    double m = 0.0;
+    for (size_t i = 0; i < cnt; ++i) { double t = fabs(v[i]); if (t > m) m = t; }
+    return m;
+}
+
+/* Pivot diagnostics of an LU: rho = max|u_ii| / min|u_ii| and the singularity test
+ * |u_kk| < 100*n*u*max_i|u_ii| (reading R2); xmax is unused (kept for the
+ * ABI of the helper). */
+static void pivot_diag(int n, const double *lu, double xmax, double *rho, int *singular_col)
+{
+    double mx = 0.0, mn = INFINITY;
+    int sc = 0;
+    (void)xmax;
+    for (int i = 0; i < n; ++i) {
+        double d = fabs(lu[(size_t)i * n + i]);
+        if (d > mx) mx = d;
+        if (d < mn) mn = d;
+    }
+    double thr = 100.0 * (double)n * ORACLE_EPS * mx;
+    for (int i = 0; i < n; ++i) {
+        double d = fabs(lu[(size_t)i * n + i]);
+        if (!(d >= thr) || d == 0.0) { sc = i + 1; break; }
+    }
+    *rho = (mn > 0.0) ? mx / mn : INFINITY;
+    *singular_col = sc;
+}
+
+/* Alg 3: A^{-1} via LU.  ainv receives the inverse.  Returns 0 or 1-based singular
+ * pivot column; *rho receives the pivot ratio. */
+int or_dinv(int n, const double *a, double *ainv, double *rho)
+{
+    double *lu = (double *)malloc(sizeof(double) * (size_t)n * n);
+    double *w = (double *)malloc(sizeof(double) * (size_t)n * n);
+    int *ipiv = (int *)malloc(sizeof(int) * (size_t)(n > 0 ? n : 1));
+    memcpy(lu, a, sizeof(double) * (size_t)n * n);
+    or_dgetrf(n, lu, ipiv);
+    int sc;
+    double r;
+    pivot_diag(n, lu, max_abs((size_t)n * n, a), &r, &sc);
+    if (rho) *rho = r;
+    int info = sc;
+    if (!info) {
+        or_dtrtri_upper(n, lu, w);
+        or_dgetri_solve(n, lu, w, ainv);
+        or_col_unswap(n, ainv, ipiv);
+    }
+    free(lu); free(w); free(ipiv);
+    return info;
+}
+
+/* C = A B (m x k times k x n); C[i][j] = sum_{k ascending} A[i][k] B[k][j]. */
+void or_dgemm(int m, int n, int k, const double *a, const double *b, double *c)
+{
+    #pragma omp parallel for schedule(static) if ((long)m * n * k > 2000000L)
+    for (int i = 0; i < m; ++i) {
+        double *ci = c + (size_t)i * n;
+        for (int j = 0; j < n; ++j) ci[j] = 0.0;
+        for (int q = 0; q < k; ++q) {
+            double aiq = a[(size_t)i * k + q];
+            const double *bq = b + (size_t)q * n;
+            for (int j = 0; j < n; ++j) ci[j] = ci[j] + aiq * bq[j];
+        }
+    }
+}
+
+/* Factor X only to obtain (rho, singular column): used by the AUTO branch rule. */
+static void lu_probe(int n, const double *x, double *rho, int *sc)
+{
+    double *lu = (double *)malloc(sizeof(double) * (size_t)n * n);
+    int *ipiv = (int *)malloc(sizeof(int) * (size_t)(n > 0 ? n : 1));
+    memcpy(lu, x, sizeof(double) * (size_t)n * n);
+    or_dgetrf(n, lu, ipiv);
+    pivot_diag(n, lu, max_abs((size_t)n * n, x), rho, sc);
+    free(lu); free(ipiv);
+}
+
+/* Alg 1 with tau = 1.
+ *   branch: 0 = AUTO (R1), 1 = S1 (X=A, Y=B), 2 = S2 (X=B, Y=A).
+ *   tau_sw: AUTO switch threshold on the pivot ratio rho_A.
+ * Returns 0 ok, 1 singular (out[0] = 1-based column), 2 both parts singular.
+ * out[0]=info, out[1]=branch used (1|2); rho[0]=rho_A, rho[1]=rho_B (NaN if not factored). */
+int or_frob_inv(int n, const double *A, const double *B, double *Xre, double *Xim,
+                int branch, double tau_sw, int *out, double *rho)
+{
+    double rho_a = NAN, rho_b = NAN;
+    int sc_a = 0, sc_b = 0;
+    int use = branch;
+    if (branch == 0) {
+        lu_probe(n, A, &rho_a, &sc_a);
+        if (sc_a || rho_a > tau_sw) {
+            lu_probe(n, B, &rho_b, &sc_b);
+            if (sc_a && sc_b) { out[0] = 0; out[1] = 0; rho[0] = rho_a; rho[1] = rho_b; return 2; }
+            if (sc_a) use = 2;
+            else if (sc_b) use = 1;
+            else use = (rho_b < rho_a) ? 2 : 1;
+        } else {
+            use = 1;
+        }
+    }
+    rho[0] = rho_a; rho[1] = rho_b;
+    out[1] = use;
+    const double *X = (use == 1) ? A : B;   /* line 2 / line 4 of Alg 1 */
+    const double *Y = (use == 1) ? B : A;
+    size_t nn = (size_t)n * n;
+    double *Xinv = (double *)malloc(sizeof(double) * nn);
+    double *F = (double *)malloc(sizeof(double) * nn);
+    double *G = (double *)malloc(sizeof(double) * nn);
+    double *J = (double *)malloc(sizeof(double) * nn);
+    double *K = (double *)malloc(sizeof(double) * nn);
+    double rx;
+    int info = or_dinv(n, X, Xinv, &rx);          /* compute X^{-1}                 */
+    if (use == 1 && branch != 0) rho[0] = rx;
+    if (use == 2 && branch != 0) rho[1] = rx;
+    if (info) { out[0] = info; goto done; }
+    or_dgemm(n, n, n, Xinv, Y, F);                 /* compute X^{-1} Y               */
+    or_dgemm(n, n, n, Y, F, G);                    /* compute Y X^{-1} Y             */
+    for (size_t i = 0; i < nn; ++i) G[i] = X[i] + G[i]; /* tau1 X + tau2 Y X^{-1} Y    */
+    info = or_dinv(n, G, J, NULL);                 /* J = (tau1 X + tau2 Y X^-1 Y)^-1 */
+    if (info) { out[0] = info; goto done; }
+    or_dgemm(n, n, n, F, J, K);                    /* K = X^{-1} Y J                 */
+    if (use == 1) {                                /* return J - iK                  */
+        for (size_t i = 0; i < nn; ++i) { Xre[i] = J[i]; Xim[i] = -K[i]; }
+    } else {                                       /* return K - iJ                  */
+        for (size_t i = 0; i < nn; ++i) { Xre[i] = K[i]; Xim[i] = -J[i]; }
+    }
+    out[0] = 0;
+done:
+    free(Xinv); free(F); free(G); free(J); free(K);
+    return info ? 1 : 0;
+}
+
+/* --------------------------------------------------------------- complex */
+
+static double cabs1(double re, double im) { return fabs(re) + fabs(im); }
+
+/* Complex Gauss-Jordan inverse with partial pivoting (first max of |re|+|im|), in
+ * place on (re, im).  Returns 0 or the 1-based column of an exactly zero pivot. */
+int or_zinv_gj(int n, double *re, double *im)
+{
+    int *piv = (int *)malloc(sizeof(int) * (size_t)(n > 0 ? n : 1));
+    int info = 0;
+    for (int k = 0; k < n && !info; ++k) {
+        int p = k;
+        double best = cabs1(re[(size_t)k * n + k], im[(size_t)k * n + k]);
+        for (int i = k + 1; i < n; ++i) {
+            double v = cabs1(re[(size_t)i * n + k], im[(size_t)i * n + k]);
+            if (v > best) { best = v; p = i; }
+        }
+        piv[k] = p;
+        if (best == 0.0) { info = k + 1; break; }
+        if (p != k) {
+            for (int j = 0; j < n; ++j) {
+                double t = re[(size_t)k * n + j]; re[(size_t)k * n + j] = re[(size_t)p * n + j]; re[(size_t)p * n + j] = t;
+                t = im[(size_t)k * n + j]; im[(size_t)k * n + j] = im[(size_t)p * n + j]; im[(size_t)p * n + j] = t;
+            }
+        }
+        /* 1/p = conj(p) / |p|^2 */
+        double pr = re[(size_t)k * n + k], pi = im[(size_t)k * n + k];
+        double den = pr * pr + pi * pi;
+        double ir = pr / den, ii = -pi / den;
+        re[(size_t)k * n + k] = 1.0; im[(size_t)k * n + k] = 0.0;
+        for (int j = 0; j < n; ++j) {
+            double xr = re[(size_t)k * n + j], xi = im[(size_t)k * n + j];
+            re[(size_t)k * n + j] = xr * ir - xi * ii;
+            im[(size_t)k * n + j] = xr * ii + xi * ir;
+        }
+        #pragma omp parallel for schedule(static) if (n > 256)
+        for (int i = 0; i < n; ++i) {
+            if (i == k) continue;
+            double fr = re[(size_t)i * n + k], fi = im[(size_t)i * n + k];
+            re[(size_t)i * n + k] = 0.0; im[(size_t)i * n + k] = 0.0;
+            if (fr == 0.0 && fi == 0.0) continue;
+            for (int j = 0; j < n; ++j) {
+                double xr = re[(size_t)k * n + j], xi = im[(size_t)k * n + j];
+                re[(size_t)i * n + j] = re[(size_t)i * n + j] - (fr * xr - fi * xi);
+                im[(size_t)i * n + j] = im[(size_t)i * n + j] - (fr * xi + fi * xr);
+            }
+        }
+    }
+    if (!info) {
+        for (int k = n - 1; k >= 0; --k) {
+            int p = piv[k];
+            if (p == k) continue;
+            for (int i = 0; i < n; ++i) {
+                double t = re[(size_t)i * n + k]; re[(size_t)i * n + k] = re[(size_t)i * n + p]; re[(size_t)i * n + p] = t;
+                t = im[(size_t)i * n + k]; im[(size_t)i * n + k] = im[(size_t)i * n + p]; im[(size_t)i * n + p] = t;
+            }
+        }
+    }
+    free(piv);
+    return info;
+}
+
+/* Alg 3 over C (the comparator): complex LU with partial pivoting (|re|+|im|), U^{-1}
+ * by column substitution, solve X L = U^{-1}, undo interchanges.  Out of place.
+ * Returns 0 or 1-based zero-pivot column. */
+int or_zinv_lu(int n, const double *zr, const double *zi, double *xr, double *xi)
+{
+    size_t nn = (size_t)n * n;
+    double *ar = (double *)malloc(sizeof(double) * nn), *ai = (double *)malloc(sizeof(double) * nn);
+    double *wr = (double *)malloc(sizeof(double) * nn), *wi = (double *)malloc(sizeof(double) * nn);
+    int *ipiv = (int *)malloc(sizeof(int) * (size_t)(n > 0 ? n : 1));
+    memcpy(ar, zr, sizeof(double) * nn);
+    memcpy(ai, zi, sizeof(double) * nn);
+    int info = 0;
+    /* line 1: LU */
+    for (int k = 0; k < n; ++k) {
+        int p = k;
+        double best = cabs1(ar[(size_t)k * n + k], ai[(size_t)k * n + k]);
+        for (int i = k + 1; i < n; ++i) {
+            double v = cabs1(ar[(size_t)i * n + k], ai[(size_t)i * n + k]);
+            if (v > best) { best = v; p = i; }
+        }
+        ipiv[k] = p;
+        if (p != k) {
+            for (int j = 0; j < n; ++j) {
+                double t = ar[(size_t)k * n + j]; ar[(size_t)k * n + j] = ar[(size_t)p * n + j]; ar[(size_t)p * n + j] = t;
+                t = ai[(size_t)k * n + j]; ai[(size_t)k * n + j] = ai[(size_t)p * n + j]; ai[(size_t)p * n + j] = t;
+            }
+        }
+        double pr = ar[(size_t)k * n + k], pi = ai[(size_t)k * n + k];
+        if (pr == 0.0 && pi == 0.0) { if (!info) info = k + 1; continue; }
+        double den = pr * pr + pi * pi;
+        double ir = pr / den, ii = -pi / den;
+        #pragma omp parallel for schedule(static) if (n - k > 256)
+        for (int i = k + 1; i < n; ++i) {
+            double vr = ar[(size_t)i * n + k], vi = ai[(size_t)i * n + k];
+            double lr = vr * ir - vi * ii, li = vr * ii + vi * ir;
+            ar[(size_t)i * n + k] = lr; ai[(size_t)i * n + k] = li;
+            for (int j = k + 1; j < n; ++j) {
+                double ur = ar[(size_t)k * n + j], ui = ai[(size_t)k * n + j];
+                ar[(size_t)i * n + j] = ar[(size_t)i * n + j] - (lr * ur - li * ui);
+                ai[(size_t)i * n + j] = ai[(size_t)i * n + j] - (lr * ui + li * ur);
+            }
+        }
+    }
+    if (info) goto done;
+    /* line 2: W = U^{-1}, column j by back substitution */
+    #pragma omp parallel for schedule(dynamic, 8) if (n > 128)
+    for (int j = 0; j < n; ++j) {
+        for (int i = j + 1; i < n; ++i) { wr[(size_t)i * n + j] = 0.0; wi[(size_t)i * n + j] = 0.0; }
+        double ur = ar[(size_t)j * n + j], ui = ai[(size_t)j * n + j];
+        double den = ur * ur + ui * ui;
+        wr[(size_t)j * n + j] = ur / den; wi[(size_t)j * n + j] = -ui / den;
+        for (int i = j - 1; i >= 0; --i) {
+            double sr = 0.0, si = 0.0;
+            for (int k = i + 1; k <= j; ++k) {
+                double a_r = ar[(size_t)i * n + k], a_i = ai[(size_t)i * n + k];
+                double b_r = wr[(size_t)k * n + j], b_i = wi[(size_t)k * n + j];
+                sr = sr + (a_r * b_r - a_i * b_i);
+                si = si + (a_r * b_i + a_i * b_r);
+            }
+            double dr = ar[(size_t)i * n + i], di = ai[(size_t)i * n + i];
+            double dd = dr * dr + di * di;
+            /* -s / d = -s * conj(d) / |d|^2 */
+            wr[(size_t)i * n + j] = -(sr * dr + si * di) / dd;
+            wi[(size_t)i * n + j] = -(si * dr - sr * di) / dd;
+        }
+    }
+    /* line 3: solve X L = W, rows independent, column j from n-1 down */
+    #pragma omp parallel for schedule(static) if (n > 128)
+    for (int i = 0; i < n; ++i) {
+        for (int j = n - 1; j >= 0; --j) {
+            double sr = 0.0, si = 0.0;
+            for (int k = j + 1; k < n; ++k) {
+                double x_r = xr[(size_t)i * n + k], x_i = xi[(size_t)i * n + k];
+                double l_r = ar[(size_t)k * n + j], l_i = ai[(size_t)k * n + j];
+                sr = sr + (x_r * l_r - x_i * l_i);
+                si = si + (x_r * l_i + x_i * l_r);
+            }
+            xr[(size_t)i * n + j] = wr[(size_t)i * n + j] - sr;
+            xi[(size_t)i * n + j] = wi[(size_t)i * n + j] - si;
+        }
+    }
+    for (int k = n - 1; k >= 0; --k) {
+        int p = ipiv[k];
+        if (p == k) continue;
+        for (int i = 0; i < n; ++i) {
+            double t = xr[(size_t)i * n + k]; xr[(size_t)i * n + k] = xr[(size_t)i * n + p]; xr[(size_t)i * n + p] = t;
+            t = xi[(size_t)i * n + k]; xi[(size_t)i * n + k] = xi[(size_t)i * n + p]; xi[(size_t)i * n + p] = t;
+        }
+    }
+done:
+    free(ar); free(ai); free(wr); free(wi); free(ipiv);
+    return info;
+}
+
+int or_num_threads(void)
+{
+#ifdef _OPENMP
+    extern int omp_get_max_threads(void);
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}

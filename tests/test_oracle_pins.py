@@ -1,0 +1,312 @@
+"""Pins for the CPU oracle (oracle/): it is checked against things other than itself.
+
+- exact rational brute force over Q(i) (tests/golden/exact_inverses.json, written by
+  tests/golden/make_golden.py from oracle/exact.py),
+- closed forms (n=1 reduction P:L218, 2x2 adjugate, diagonal, unitary inputs,
+  SPEC trivial cases in tests/golden/closed_forms.json),
+- structural special cases (B=0, A=0, both parts singular),
+- invariants (P A = L U, Z X = I, two-branch agreement, branch-B rotation),
+- LAPACK (numpy) as an independent library reference for the real kernels.
+A plausible slip (dropped term, wrong sign, transposed operand, wrong branch output
+order, wrong pivot un-swap) fails at least one of these.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import exact
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+U = 2.0 ** -53
+
+
+def _dec(m):
+    from fractions import Fraction
+    return np.array([[complex(float(Fraction(a)), float(Fraction(b))) for a, b in r] for r in m])
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def _cm(rows):
+    return np.array([[complex(a, b) for a, b in r] for r in rows])
+
+
+# ------------------------------------------------------------------ exact brute force
+@pytest.mark.parametrize("case", _gold("exact_inverses.json")["cases"],
+                         ids=lambda c: f"n{c['n']}")
+def test_exact_golden(case):
+    z = np.array(case["re"], float) + 1j * np.array(case["im"], float)
+    ref = _dec(case["inv"])
+    kap = np.linalg.cond(z)
+    tol = 50 * case["n"] * U * kap * max(1.0, kap)
+    x, info = oracle.zinv_gj(z)
+    assert info == 0
+    assert oracle.rel_fro(x, ref) <= tol
+    xl, info = oracle.zinv_lu(z)
+    assert info == 0 and oracle.rel_fro(xl, ref) <= tol
+    for br in ("a", "b"):
+        if case["frob_" + br] is None:
+            continue
+        # Lemma 4.1 in exact arithmetic: Alg 1 equals the exact inverse exactly.
+        assert case["frob_" + br] == case["inv"]
+        xf, st, inf = oracle.frob_inv(z, br)
+        if st == 0:
+            kx = np.linalg.cond(z.real if br == "a" else z.imag)
+            assert oracle.rel_fro(xf, ref) <= 100 * case["n"] * U * kap * kx * kx + tol
+
+
+def test_exact_alg1_matches_definition_random():
+    """Alg 1 over Q(i), both branches, equals Gauss-Jordan over Q(i) (fresh draws)."""
+    rng = np.random.default_rng(7)
+    for n in (2, 3, 4):
+        re = rng.integers(-3, 4, size=(n, n))
+        im = rng.integers(-3, 4, size=(n, n))
+        z = exact.from_ints(re.tolist(), im.tolist())
+        try:
+            zi = exact.inv_exact(z)
+            fa = exact.frobenius_exact(z, "a")
+            fb = exact.frobenius_exact(z, "b")
+        except ZeroDivisionError:
+            continue
+        assert fa == zi and fb == zi
+
+
+# ------------------------------------------------------------------ closed forms
+def test_closed_forms_golden():
+    g = _gold("closed_forms.json")
+    for c in g["complex_inverse"]:
+        z, ref = _cm(c["z"]), _cm(c["inv"])
+        for fn in (lambda q: oracle.zinv_gj(q)[0], lambda q: oracle.zinv_lu(q)[0],
+                   lambda q: oracle.frob_inv(q)[0]):
+            np.testing.assert_allclose(fn(z), ref, rtol=0, atol=1e-15, err_msg=c["cite"])
+    for c in g["upper_triangular_inverse"]:
+        x, info = oracle.dtrtri_upper(np.array(c["u"], float))
+        np.testing.assert_allclose(x, np.array(c["inv"]), rtol=1e-15, atol=0)
+
+
+def test_n1_reduction_all_branches():
+    """for n = 1, Alg 1 is the scalar (a+ib)^{-1} = (a-ib)/(a^2+b^2)."""
+    for a, b in [(3.0, 4.0), (-1.5, 0.25), (1e-3, 7.0), (2.0, -2.0)]:
+        ref = complex(a, -b) / (a * a + b * b)
+        z = np.array([[complex(a, b)]])
+        for br in ("a", "b", "auto"):
+            x, st, _ = oracle.frob_inv(z, br)
+            assert st == 0
+            assert abs(x[0, 0] - ref) <= 4 * U * abs(ref)
+
+
+def test_2x2_adjugate():
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        z = rng.standard_normal((2, 2)) + 1j * rng.standard_normal((2, 2))
+        det = z[0, 0] * z[1, 1] - z[0, 1] * z[1, 0]
+        ref = np.array([[z[1, 1], -z[0, 1]], [-z[1, 0], z[0, 0]]]) / det
+        kap = np.linalg.cond(z)
+        for x in (oracle.zinv_gj(z)[0], oracle.zinv_lu(z)[0], oracle.frob_inv(z, "auto")[0]):
+            assert oracle.rel_fro(x, ref) <= 1e-13 * kap * kap
+
+
+def test_diagonal():
+    d = np.array([1 + 2j, -3 + 0.5j, 0.25 - 4j, 5 + 5j, -2 - 1j])
+    z = np.diag(d)
+    ref = np.diag(1 / d)
+    for x in (oracle.zinv_gj(z)[0], oracle.zinv_lu(z)[0], oracle.frob_inv(z, "a")[0],
+              oracle.frob_inv(z, "b")[0]):
+        np.testing.assert_allclose(x, ref, rtol=4e-16 * 8, atol=0)
+
+
+def test_unitary_phase():
+    """Z = Q e^{i theta} with Q real orthogonal: Z^{-1} = e^{-i theta} Q^T (both A, B invertible)."""
+    n = 16
+    q, _ = np.linalg.qr(np.random.default_rng(1).standard_normal((n, n)))
+    for th in (0.3, 1.1, 2.5):
+        z = q * np.exp(1j * th)
+        ref = np.exp(-1j * th) * q.T
+        for br in ("a", "b", "auto"):
+            x, st, _ = oracle.frob_inv(z, br)
+            assert st == 0
+            assert oracle.rel_fro(x, ref) <= 1e-13 / min(abs(math.cos(th)), abs(math.sin(th))) ** 2
+        assert oracle.rel_fro(oracle.zinv_gj(z)[0], ref) <= 1e-14
+
+
+# ------------------------------------------------------------------ special structure
+def test_b_zero_is_real_inverse_bitwise():
+    a, _ = synth.gauss_pair(24, seed=5)
+    z = a + 0j
+    x, st, info = oracle.frob_inv(z, "auto")
+    ainv, i2, _ = oracle.dinv(a)
+    assert st == 0 and info["branch_used"] == 1
+    assert np.array_equal(x.real, ainv)
+    assert not np.any(x.imag)
+
+
+def test_a_zero_takes_branch_b():
+    _, b = synth.gauss_pair(24, seed=6)
+    z = 1j * b
+    x, st, info = oracle.frob_inv(z, "auto")
+    binv, _, _ = oracle.dinv(b)
+    assert st == 0 and info["branch_used"] == 2
+    assert not np.any(x.real)
+    assert np.array_equal(x.imag, -binv)
+
+
+def test_both_parts_singular_dft():
+    z = synth.dft_unitary(8)
+    _, st, _ = oracle.frob_inv(z, "auto")
+    assert st == 2
+    x, info = oracle.zinv_gj(z)
+    assert info == 0 and oracle.rel_fro(x, z.conj().T) <= 1e-14
+
+
+def test_branch_b_is_rotated_branch_a():
+    """S2 output (K - iJ) equals -i * S1-Alg1 applied to (B, -A) bitwise."""
+    z = synth.shifted_complex(20, seed=11, shift=6.0)
+    xb, st, _ = oracle.frob_inv(z, "b")
+    xa_rot, st2, _ = oracle.frob_inv(z.imag - 1j * z.real, "a")
+    assert st == 0 and st2 == 0
+    assert np.array_equal(xb, -1j * xa_rot)
+
+
+# ------------------------------------------------------------------ real kernels
+def test_dgetrf_reconstruction_and_lapack_pivots():
+    a, _ = synth.gauss_pair(40, seed=2, shift=0.0)
+    lu, ipiv, info = oracle.dgetrf(a)
+    assert info == 0
+    n = a.shape[0]
+    l = np.tril(lu, -1) + np.eye(n)
+    u = np.triu(lu)
+    pa = a.copy()
+    for k in range(n):
+        pa[[k, ipiv[k]]] = pa[[ipiv[k], k]]
+    assert np.abs(pa - l @ u).max() <= 10 * n * U * np.abs(a).max() * 4
+    assert np.abs(l).max() <= 1.0
+    import scipy.linalg as sla
+    lu2, piv2 = sla.lu_factor(a)
+    assert np.array_equal(piv2, ipiv)
+    np.testing.assert_allclose(lu, lu2, rtol=0, atol=1e-12)
+
+
+def test_dgetrf_swap_example():
+    lu, ipiv, info = oracle.dgetrf(np.array([[0.0, 1.0], [1.0, 0.0]]))
+    assert list(ipiv) == [1, 1] and np.array_equal(lu, np.eye(2))
+
+
+def test_dinv_3x3_adjugate_and_lapack():
+    m = np.array([[4.0, -2.0, 1.0], [3.0, 6.0, -4.0], [2.0, 1.0, 8.0]])
+    c = np.zeros((3, 3))
+    for i in range(3):
+        for j in range(3):
+            minor = np.delete(np.delete(m, i, 0), j, 1)
+            c[i, j] = (-1) ** (i + j) * (minor[0, 0] * minor[1, 1] - minor[0, 1] * minor[1, 0])
+    det = float(np.dot(m[0], c[0]))
+    adj = c.T / det
+    x, info, rho = oracle.dinv(m)
+    assert info == 0
+    np.testing.assert_allclose(x, adj, rtol=1e-14, atol=1e-16)
+    a, _ = synth.gauss_pair(50, seed=4)
+    np.testing.assert_allclose(oracle.dinv(a)[0], np.linalg.inv(a), rtol=0, atol=1e-13)
+
+
+def test_dgetri_solve_and_trtri():
+    a, _ = synth.gauss_pair(30, seed=9)
+    lu, ipiv, _ = oracle.dgetrf(a)
+    w, info = oracle.dtrtri_upper(lu)
+    assert info == 0
+    np.testing.assert_allclose(w @ np.triu(lu), np.eye(30), atol=1e-13)
+    assert not np.any(np.tril(w, -1))
+    x = oracle.dgetri_solve(lu, w)
+    l = np.tril(lu, -1) + np.eye(30)
+    np.testing.assert_allclose(x @ l, w, atol=1e-13)
+
+
+def test_dgemm_exact_integers():
+    rng = np.random.default_rng(0)
+    a = rng.integers(-50, 50, size=(13, 17)).astype(float)
+    b = rng.integers(-50, 50, size=(17, 11)).astype(float)
+    ref = (a.astype(np.int64) @ b.astype(np.int64)).astype(float)
+    assert np.array_equal(oracle.dgemm(a, b), ref)
+
+
+# ------------------------------------------------------------------ whole-method invariants
+@pytest.mark.parametrize("n", [33, 64, 130])
+def test_frob_vs_definition_config_style(n):
+    z = synth.shifted_complex(n, seed=n, shift=8.0)
+    xg, info = oracle.zinv_gj(z)
+    assert info == 0
+    for br in ("a", "b", "auto"):
+        xf, st, _ = oracle.frob_inv(z, br)
+        assert st == 0
+        assert oracle.rel_fro(xf, xg) <= 1e-10
+        assert oracle.residual_fro(z, xf) <= 1e-11 * n
+    xl, info = oracle.zinv_lu(z)
+    assert oracle.rel_fro(xl, xg) <= 1e-12
+    np.testing.assert_allclose(xg, np.linalg.inv(z), rtol=0, atol=1e-12 * np.abs(xg).max())
+
+
+def test_auto_switch_on_bad_a():
+    """A nearly singular (rho_A huge) -> AUTO takes branch B (R1)."""
+    n = 12
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((n, n))
+    a[:, 0] = a[:, 1] * (1 + 1e-9)
+    b = rng.standard_normal((n, n)) + 4 * np.eye(n)
+    x, st, info = oracle.frob_inv(a + 1j * b, "auto")
+    assert st == 0 and info["branch_used"] == 2 and info["rho_a"] > oracle.TAU_SWITCH
+    assert oracle.rel_fro(x, np.linalg.inv(a + 1j * b)) <= 1e-9
+
+
+def test_paper_accuracy_generator_residuals():
+    """P:L1076-1077 kappa=10 generator; Frobenius residuals stay within 50x of complex LU."""
+    n = 64
+    a = synth.hadamard_kappa(n, 10.0, seed=1)
+    b = synth.hadamard_kappa(n, 10.0, seed=2)
+    z = a + 1j * b
+    xf, st, _ = oracle.frob_inv(z)
+    xl, _ = oracle.zinv_lu(z)
+    rf = max(oracle.res_lr(z, xf))
+    rl = max(oracle.res_lr(z, xl))
+    assert st == 0 and rf <= max(50 * rl, 1e-14)
+
+
+# ------------------------------------------------------------------ Newton drivers
+def test_sign_closed_forms():
+    g = _gold("closed_forms.json")
+    for c in g["sign"]:
+        for m in ("frobenius", "zlu"):
+            s, it, _ = oracle.sign_newton(np.array(c["z"], complex), method=m)
+            np.testing.assert_allclose(s, np.array(c["s"], complex), atol=1e-15)
+    for c in g["polar"]:
+        u, h, it, _ = oracle.polar_newton(np.array(c["a"], complex))
+        np.testing.assert_allclose(u, np.array(c["u"]), atol=1e-15)
+        np.testing.assert_allclose(h, np.array(c["h"]), atol=1e-15)
+
+
+def test_sign_newton_config4_small():
+    z, s, lam, sinv = synth.sign_instance(48, seed=0)
+    ref = (s * np.sign(lam.real)[None, :]) @ sinv
+    for m in ("frobenius", "zlu"):
+        x, it, d = oracle.sign_newton(z, tol=1e-12, max_iter=50, method=m)
+        assert it < 50 and d[-1] < 1e-12
+        assert oracle.rel_fro(x, ref) <= 1e-12
+        assert np.abs(x @ x - np.eye(48)).max() <= 1e-11
+        assert np.abs(x @ z - z @ x).max() <= 1e-10 * np.abs(z).max()
+
+
+def test_polar_planted():
+    n = 24
+    rng = np.random.default_rng(2)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    c = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    h0 = c.conj().T @ c + n * np.eye(n)
+    a = q @ h0
+    u, h, it, _ = oracle.polar_newton(a, tol=1e-13)
+    assert oracle.rel_fro(u, q) <= 1e-12 and oracle.rel_fro(h, h0) <= 1e-12
+    assert np.abs(u.conj().T @ u - np.eye(n)).max() <= 1e-13
