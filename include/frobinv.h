@@ -1,0 +1,178 @@
+/*
+ * frobinv.h -- C ABI of the B200-native Frobenius inversion library (libfrobinv.so).
+ *
+ * Method: Dai, Lim & Ye, "Inverting a complex matrix", arXiv 2208.01239.
+ *   Lemma 4.1 / Alg 1:  for Z = A + iB with A, B real n x n,
+ *     S1 (A invertible):  Z^{-1} = (A + B A^{-1} B)^{-1} - i A^{-1} B (A + B A^{-1} B)^{-1}
+ *     S2 (B invertible):  Z^{-1} = B^{-1} A (A B^{-1} A + B)^{-1} - i (A B^{-1} A + B)^{-1}
+ *   computed with two real inversions (Alg 3: LU with partial pivoting,
+ *   U^{-1}, solve X L = U^{-1}) and three real GEMMs.
+ *
+ * Conventions shared by every entry point
+ *   - Matrices are dense, ROW-MAJOR.  Complex matrices are interleaved complex128
+ *     (re, im pairs of IEEE fp64; the layout of torch.complex128 and cuDoubleComplex);
+ *     a leading dimension `ld*` counts complex elements per row (>= n).  Real matrices
+ *     are fp64 with a leading dimension in doubles.
+ *   - All matrix / workspace pointers are DEVICE pointers owned by the caller (except
+ *     the *_host entry points and the host_* out-parameters, which are host memory).
+ *     The library never allocates device memory and keeps no global state: calls are
+ *     re-entrant given distinct workspaces.
+ *   - `stream` is a cudaStream_t passed as void*; NULL means the legacy default
+ *     stream.  Work is enqueued asynchronously on it.  The only host synchronisations
+ *     are (a) FROB_BRANCH_AUTO in frob_inv (one 32-byte device->host read of the pivot
+ *     diagnostics of LU(A)), (b) a non-NULL host_info / host-side outputs, (c) the
+ *     Newton drivers (one 16-byte read of delta_t per iteration), (d) *_host entries.
+ *   - Outputs must not alias inputs (X != Z, S != Z, ...): FROB_ERR_INVALID_ARG.
+ *   - Singular pivots: a pivot u_kk of an LU is "singular" when
+ *       |u_kk| < 100 * n * 2^-53 * max_i |u_ii|        (reading R2);
+ *     info = 1-based column k+1 of the first such pivot (LAPACK-style).
+ *   - Errors are returned as frob_status; CUDA launch/runtime failures give
+ *     FROB_ERR_CUDA (query frob_last_cuda_error()).
+ */
+#ifndef FROBINV_H
+#define FROBINV_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    FROB_OK = 0,
+    FROB_ERR_SINGULAR = 1,       /* chosen branch (or the inner M) has a singular pivot; info = column */
+    FROB_ERR_BOTH_SINGULAR = 2,  /* AUTO: neither A nor B usable (Z outside S1 u S2) */
+    FROB_ERR_NOT_CONVERGED = 3,  /* Newton driver hit max_iter; the last iterate is returned */
+    FROB_ERR_INVALID_ARG = 4,
+    FROB_ERR_NONFINITE = 5,      /* NaN/Inf in the input */
+    FROB_ERR_WORKSPACE = 6,      /* ws NULL or ws_bytes below the *_workspace_bytes query */
+    FROB_ERR_CUDA = 7
+} frob_status;
+
+typedef enum {
+    FROB_BRANCH_AUTO = 0, /* S1 unless LU(A) is singular or its pivot ratio exceeds 256; then the
+                             branch whose LU has the smaller pivot ratio (reading R1)   */
+    FROB_BRANCH_A = 1,    /* S1: X = A, Y = B (Alg 1 line 2)                                      */
+    FROB_BRANCH_B = 2     /* S2: X = B, Y = A (Alg 1 line 4)                                      */
+} frob_branch;
+
+typedef enum { FROB_INV_FROBENIUS = 0, FROB_INV_ZLU = 1 } frob_inv_method;
+
+typedef struct {
+    int info;          /* 0 or the 1-based singular pivot column                         */
+    int branch_used;   /* 1 = S1, 2 = S2, 0 = none                                       */
+    double rho_a;      /* max|u_ii|/min|u_ii| of LU(A) (NaN if A was not factored)       */
+    double rho_b;      /* same for LU(B)                                                 */
+    double rho_m;      /* same for LU(M), M = X + Y X^{-1} Y                              */
+} frob_info;
+
+/* ---------------------------------------------------------------- single matrix */
+
+/* Bytes of device workspace frob_inv needs for order n (256-byte aligned pointer). */
+size_t frob_inv_workspace_bytes(int n);
+
+/* Z^{-1} by Frobenius inversion (Alg 1; steps SURVEY.md 8(a) a0-a7).
+ *   n      order (>= 1)
+ *   Z      device, n x n complex128 row-major, leading dim ldz (complex elements)
+ *   X      device output, n x n complex128, leading dim ldx; must not overlap Z
+ *   branch frob_branch
+ *   ws     device workspace of at least frob_inv_workspace_bytes(n) bytes
+ *   host_info  nullable; if non-NULL the call synchronises `stream` and fills it.
+ * Returns FROB_OK, or an error status (X is then unspecified). */
+frob_status frob_inv(int n, const double *Z, long long ldz, double *X, long long ldx,
+                     int branch, void *ws, size_t ws_bytes, void *stream, frob_info *host_info);
+
+/* Same computation with HOST input/output buffers (pinned memory recommended): copies
+ * Z host->device, runs frob_inv, copies X device->host, synchronises.  Z_host/X_host
+ * are dense (ld = n).  ws must hold frob_inv_host_workspace_bytes(n) bytes. */
+size_t frob_inv_host_workspace_bytes(int n);
+frob_status frob_inv_host(int n, const double *Z_host, double *X_host, int branch,
+                          void *ws, size_t ws_bytes, void *stream, frob_info *host_info);
+
+/* Complex-LU inversion: Alg 3 over C (the paper's comparator `X\eye(n)`,
+ * P:L1057): complex LU with partial pivoting on |re|+|im|, U^{-1}, X = U^{-1} L^{-1},
+ * column interchanges.  Same layout/ownership rules as frob_inv.
+ * host_info: nullable host int receiving info (forces a synchronisation). */
+size_t zinv_lu_workspace_bytes(int n);
+frob_status zinv_lu(int n, const double *Z, long long ldz, double *X, long long ldx,
+                    void *ws, size_t ws_bytes, void *stream, int *host_info);
+
+/* ---------------------------------------------------------------- batched small n */
+
+/* One CTA per matrix for n <= 64 (registers/shared memory), a resident
+ * shared-memory pipeline per matrix for 64 < n <= 128.  Z and X hold `batch`
+ * n x n complex128 matrices, dense (ld = n), matrix b at Z + 2*b*strideZ doubles
+ * (strideZ in complex elements, >= n*n).
+ *   d_info         device int[batch]: 0 or 1-based singular column per matrix
+ *   d_branch_used  device uint8[batch]: 1 (S1) or 2 (S2) per matrix (nullable)
+ * No host synchronisation; per-matrix failures are reported only in d_info.
+ * FROB_BRANCH_AUTO applies reading R1 per matrix (lazy: B is factored only if LU(A)
+ * fails the pivot-ratio test). */
+size_t frob_inv_batched_workspace_bytes(int n, int batch);
+frob_status frob_inv_batched(int n, int batch, const double *Z, long long strideZ,
+                             double *X, long long strideX, int branch, int *d_info,
+                             unsigned char *d_branch_used, void *ws, size_t ws_bytes,
+                             void *stream);
+
+size_t zinv_lu_batched_workspace_bytes(int n, int batch);
+frob_status zinv_lu_batched(int n, int batch, const double *Z, long long strideZ,
+                            double *X, long long strideX, int *d_info, void *ws,
+                            size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------- Newton drivers */
+
+/* Matrix sign by Newton X_{t+1} = (X_t + X_t^{-1})/2, X_0 = Z.
+ * Stops when delta_t = ||X_{t+1} - X_t||_F / ||X_{t+1}||_F < tol or after max_iter
+ * steps (BASELINE config 4; reading R6); at least one step.
+ *   Z, S        device n x n complex128 (ld = n); S receives sign(Z); S != Z
+ *   method      frob_inv_method used for X_t^{-1}
+ *   host_iters, host_final_delta   host out (required)
+ *   host_trace  nullable host double[max_iter] receiving delta_t per step
+ * Returns FROB_OK, FROB_ERR_NOT_CONVERGED (S = last iterate) or an inversion error. */
+size_t frob_newton_workspace_bytes(int n, int method);
+frob_status frob_sign_newton(int n, const double *Z, double *S, double tol, int max_iter,
+                             int method, void *ws, size_t ws_bytes, void *stream,
+                             int *host_iters, double *host_final_delta, double *host_trace);
+
+/* Polar decomposition A = U H by Newton X_{t+1} = (X_t + X_t^{-*})/2, X_0 = A
+ * (P:L1231-1233); H = (U^H A + (U^H A)^H)/2 (reading R7).  Same stopping
+ * rule and outputs as frob_sign_newton; U, H device n x n complex128 (ld = n). */
+frob_status frob_polar_newton(int n, const double *A, double *U, double *H, double tol,
+                              int max_iter, int method, void *ws, size_t ws_bytes,
+                              void *stream, int *host_iters, double *host_final_delta,
+                              double *host_trace);
+
+/* ---------------------------------------------------------------- real building blocks
+ * Exposed so the paper's threshold quantities T_inv and T_mult (Thm 5.1)
+ * can be measured on the very kernels the Frobenius path uses. */
+
+/* C = alpha * A B + beta * C; A m x k, B k x n, C m x n, all fp64 row-major. */
+frob_status frob_dgemm(int m, int n, int k, double alpha, const double *A, long long lda,
+                       const double *B, long long ldb, double beta, double *C, long long ldc,
+                       void *stream);
+
+/* Real inversion Alg 3: Ainv = A^{-1}, fp64 n x n row-major.
+ * host_info nullable (info + pivot ratio via rho_a). */
+size_t frob_dinv_workspace_bytes(int n);
+frob_status frob_dinv(int n, const double *A, long long lda, double *Ainv, long long ldainv,
+                      void *ws, size_t ws_bytes, void *stream, frob_info *host_info);
+
+/* LU with partial pivoting in place (Alg 3 line 1): on return A holds L\U of P A
+ * and perm[i] = original row index of row i of P A (device int[n]).  Needs
+ * frob_dgetrf_workspace_bytes(n). */
+size_t frob_dgetrf_workspace_bytes(int n);
+frob_status frob_dgetrf(int n, double *A, long long lda, int *perm, void *ws, size_t ws_bytes,
+                        void *stream, frob_info *host_info);
+
+/* ---------------------------------------------------------------- misc */
+const char *frob_status_string(int status);
+const char *frob_last_cuda_error(void);
+int frob_version(void);
+/* Diagnostics: number of CUDA kernels this process has launched through the library
+ * (monotonic; used by bench.py to report gpu_launches). */
+unsigned long long frob_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FROBINV_H */

@@ -1,0 +1,11 @@
+"""B200-native Frobenius inversion of complex matrices (arXiv 2208.01239).
+
+The product is the C-ABI CUDA library ``libfrobinv.so`` (include/frobinv.h); this
+package only builds it (``build.py``) and binds it (``frobinv.py``).
+"""
+from .frobinv import (  # noqa: F401
+    FrobError, dgemm, dgetrf, dinv, inv, inv_batched, inv_host, load, polar, sign, zinv, zinv_batched,
+)
+
+__all__ = ["inv", "inv_batched", "inv_host", "zinv", "zinv_batched", "sign", "polar", "dgemm", "dinv",
+           "dgetrf", "load", "FrobError"]

@@ -1,0 +1,401 @@
+// batched.cu -- batched small-n Frobenius inversion and complex-LU comparator:
+// one CTA per matrix, everything resident on chip (BASELINE config 3; config 1).
+//
+// Per matrix (Alg 1):
+//   load Z (interleaved, coalesced) -> planar A, B in shared memory
+//   X^{-1} by a register-resident Gauss-Jordan sweep with partial pivoting
+//       (each thread owns a 4x4 block; no row swaps: the pivot order is recorded and
+//        undone when the inverse is written back -- "exchange" form of GJ)
+//   branch check (reading R1) on the sweep pivots (= the U diagonal of LU with
+//       partial pivoting); lazy: B is swept only when A fails
+//   C = X^{-1} Y,  M = X + Y C,  Re = M^{-1} (sweep),  Im = -C Re
+//       the three GEMMs run on the FP64 tensor cores (DMMA m8n8k4) from shared memory
+//   store X interleaved (branch S1: Re - i(-Im) ... see the epilogue)
+// The real inversion used here is Gauss-Jordan, which computes the same inverse as
+// Alg 3 (2n^3 flops) with n sequential steps instead of 3n ("batched path").
+#include <climits>
+#include <cmath>
+#include "common.cuh"
+#include "../../include/frobinv.h"
+
+namespace frob {
+
+template <int N>
+struct BCfg {
+    static constexpr int TPR = N / 4;            // threads per row of 4x4 blocks
+    static constexpr int THREADS = TPR * TPR;
+    static constexpr int S = N + 4;              // padded smem row stride (doubles)
+    static constexpr int WARPS = THREADS / 32;
+};
+
+// shared state of the sweep (double-buffered by step parity)
+template <typename T, int N>
+struct SweepShared {
+    T colk[2][N];
+    T rowp[2][N];
+    double candv[2][N / 4];
+    int candi[2][N / 4];
+    int pivrow[N];
+    int pos[N];
+    double pmag_k[N];
+};
+
+// Gauss-Jordan sweep on the register blocks a[4][4] (rows r0.., cols c0..) over the
+// leading n x n part of an N x N matrix (padding = identity).  On return the
+// inverse, scattered: A^{-1}[pos[i]][pivrow[j]] = a(i, j).  Returns pivot stats.
+template <typename T, int N>
+FROB_DEV void gj_sweep(T (&a)[4][4], int n, SweepShared<T, N> &sh, double &pmax, double &pmin) {
+    using C = BCfg<N>;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int ti = tid / C::TPR, tj = tid % C::TPR;
+    const int r0 = ti * 4, c0 = tj * 4;
+    unsigned long long used0 = 0, used1 = 0;  // rows already used as pivots (N <= 128)
+    pmax = 0.0;
+    pmin = INFINITY;
+    for (int k = 0; k < n; ++k) {
+        const int par = k & 1;
+        if (tj == (k >> 2)) {
+            const int cc = k & 3;
+            double bv = -1.0;
+            int bi = INT_MAX;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int r = r0 + q;
+                sh.colk[par][r] = a[q][cc];
+                const bool u = (r < 64) ? ((used0 >> r) & 1ull) : ((used1 >> (r - 64)) & 1ull);
+                if (r < n && !u) {
+                    const double v = pkey(a[q][cc]);
+                    if (better(v, r, bv, bi)) { bv = v; bi = r; }
+                }
+            }
+            sh.candv[par][ti] = bv;
+            sh.candi[par][ti] = bi;
+        }
+        __syncthreads();
+        ArgMax m = warp_argmax(lane < C::TPR ? sh.candv[par][lane] : -1.0,
+                               lane < C::TPR ? sh.candi[par][lane] : INT_MAX);
+        const int p = m.i;
+        const T piv = sh.colk[par][p];
+        const double mag = pmag(piv);
+        pmax = fmax(pmax, mag);
+        pmin = fmin(pmin, mag);
+        const T ip = is_zero(piv) ? zero_of(T()) : recip(piv);
+        if (p < 64) used0 |= 1ull << p; else used1 |= 1ull << (p - 64);
+        if (tid == 0) { sh.pivrow[k] = p; sh.pmag_k[k] = mag; }
+        if (ti == (p >> 2)) {
+            const int q = p & 3;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) sh.rowp[par][c0 + c] = (c0 + c == k) ? ip : mul(a[q][c], ip);
+        }
+        __syncthreads();
+        T rp[4], ck[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) rp[c] = sh.rowp[par][c0 + c];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ck[q] = sh.colk[par][r0 + q];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (r0 + q == p) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) a[q][c] = rp[c];
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    a[q][c] = (c0 + c == k) ? neg(mul(ck[q], rp[c])) : msub(a[q][c], ck[q], rp[c]);
+            }
+        }
+    }
+    __syncthreads();
+    for (int k = tid; k < N; k += C::THREADS) {
+        if (k >= n) sh.pivrow[k] = k;
+    }
+    __syncthreads();
+    for (int k = tid; k < N; k += C::THREADS) sh.pos[sh.pivrow[k]] = k;
+    __syncthreads();
+}
+
+// write the sweep result as the inverse into smem buffer M (stride S)
+template <typename T, int N>
+FROB_DEV void sweep_store(const T (&a)[4][4], const SweepShared<T, N> &sh, T *M) {
+    using C = BCfg<N>;
+    const int tid = threadIdx.x;
+    const int r0 = (tid / C::TPR) * 4, c0 = (tid % C::TPR) * 4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int orow = sh.pos[r0 + q];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) M[orow * C::S + sh.pivrow[c0 + c]] = a[q][c];
+    }
+}
+
+// load register blocks from smem matrix (stride S); rows/cols >= n get identity padding
+template <typename T, int N>
+FROB_DEV void load_blocks(T (&a)[4][4], const T *M, int n) {
+    using C = BCfg<N>;
+    const int tid = threadIdx.x;
+    const int r0 = (tid / C::TPR) * 4, c0 = (tid % C::TPR) * 4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int i = r0 + q, j = c0 + c;
+            a[q][c] = (i < n && j < n) ? M[i * C::S + j] : ((i == j) ? one_of(T()) : zero_of(T()));
+        }
+}
+
+// first 1-based pivot column with |u_kk| < 100 n u max (reading R2), 0 if none
+template <typename T, int N>
+FROB_DEV int sweep_info(const SweepShared<T, N> &sh, int n, double pmax) {
+    const double thr = 100.0 * n * 1.1102230246251565e-16 * pmax;
+    for (int k = 0; k < n; ++k)
+        if (!(sh.pmag_k[k] >= thr) || sh.pmag_k[k] == 0.0) return k + 1;
+    return 0;
+}
+
+// ----------------------------------------------------------------- in-CTA DMMA GEMM
+// acc = X * Y over the N x N smem operands (stride S). Warp tiling per N.
+template <int N> struct WT;
+template <> struct WT<32> { static constexpr int WGM = 2, WGN = 1, MT = 2, NT = 4; };
+template <> struct WT<64> { static constexpr int WGM = 2, WGN = 4, MT = 4, NT = 2; };
+
+template <int N>
+FROB_DEV void cta_mma(const double *Xs, const double *Ys, int kmax, double (&acc)[WT<N>::MT][WT<N>::NT][2]) {
+    using C = BCfg<N>;
+    using W = WT<N>;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm0 = (warp / W::WGN) * (W::MT * 8), wn0 = (warp % W::WGN) * (W::NT * 8);
+#pragma unroll
+    for (int i = 0; i < W::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < W::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int kk = 0; kk < kmax; kk += 4) {
+        double a[W::MT], b[W::NT];
+#pragma unroll
+        for (int i = 0; i < W::MT; ++i) a[i] = Xs[(wm0 + i * 8 + g) * C::S + kk + t];
+#pragma unroll
+        for (int j = 0; j < W::NT; ++j) b[j] = Ys[(kk + t) * C::S + wn0 + j * 8 + g];
+#pragma unroll
+        for (int i = 0; i < W::MT; ++i)
+#pragma unroll
+            for (int j = 0; j < W::NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+}
+
+template <int N, typename F>
+FROB_DEV void cta_mma_foreach(const double (&acc)[WT<N>::MT][WT<N>::NT][2], F f) {
+    using W = WT<N>;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm0 = (warp / W::WGN) * (W::MT * 8), wn0 = (warp % W::WGN) * (W::NT * 8);
+#pragma unroll
+    for (int i = 0; i < W::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < W::NT; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) f(wm0 + i * 8 + g, wn0 + j * 8 + 2 * t + e, acc[i][j][e]);
+}
+
+// ----------------------------------------------------------------- Frobenius kernel
+template <int N>
+struct FrobSmem {
+    double buf[3][N * BCfg<N>::S];
+    SweepShared<double, N> sw;
+};
+
+template <int N>
+__global__ void __launch_bounds__(BCfg<N>::THREADS)
+frob_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__restrict__ X, long long sX,
+                    int n, int branch, int *__restrict__ info, unsigned char *__restrict__ bused) {
+    using C = BCfg<N>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    FrobSmem<N> &sm = *reinterpret_cast<FrobSmem<N> *>(smem_raw);
+    const int tid = threadIdx.x;
+    const long long b = blockIdx.x;
+    const double2 *Zb = Z + b * sZ;
+    double2 *Xb = X + b * sX;
+    double *As = sm.buf[0], *Bs = sm.buf[1], *Ws = sm.buf[2];
+
+    // a0: coalesced interleaved load -> planar A, B (zero padded)
+    for (int idx = tid; idx < N * N; idx += C::THREADS) {
+        const int i = idx / N, j = idx - i * N;
+        double2 z = make_double2(0.0, 0.0);
+        if (i < n && j < n) z = Zb[i * n + j];
+        As[i * C::S + j] = z.x;
+        Bs[i * C::S + j] = z.y;
+    }
+    __syncthreads();
+
+    double a[4][4];
+    double pmax, pmin;
+    int use = (branch == FROB_BRANCH_B) ? 2 : 1;
+    load_blocks<double, N>(a, use == 1 ? As : Bs, n);
+    gj_sweep<double, N>(a, n, sm.sw, pmax, pmin);
+    int inf_x = sweep_info<double, N>(sm.sw, n, pmax);
+    sweep_store<double, N>(a, sm.sw, Ws);
+    if (branch == FROB_BRANCH_AUTO) {
+        const double rho_a = (pmin > 0.0) ? pmax / pmin : INFINITY;
+        if (inf_x != 0 || !(rho_a <= 256.0)) {
+            // lazy switch: sweep B too and keep the branch with the smaller pivot ratio
+            __syncthreads();
+            load_blocks<double, N>(a, Bs, n);
+            double qmax, qmin;
+            gj_sweep<double, N>(a, n, sm.sw, qmax, qmin);
+            const int inf_b = sweep_info<double, N>(sm.sw, n, qmax);
+            const double rho_b = (qmin > 0.0) ? qmax / qmin : INFINITY;
+            if (inf_b == 0 && (inf_x != 0 || rho_b < rho_a)) {
+                use = 2;
+                inf_x = 0;
+                __syncthreads();
+                sweep_store<double, N>(a, sm.sw, Ws);
+            } else if (inf_b != 0 && inf_x != 0) {
+                inf_x = -1;  // both singular
+            }
+        }
+    }
+    __syncthreads();
+    double *Xs = (use == 1) ? As : Bs;   // X of Alg 1
+    double *Ys = (use == 1) ? Bs : As;   // Y of Alg 1 (S2: Y = -A via sgn)
+    const double sgn = (use == 1) ? 1.0 : -1.0;
+
+    // a3: C = X^{-1} (sgn Y)  -> Ws (after everyone has read X^{-1})
+    double acc[WT<N>::MT][WT<N>::NT][2];
+    cta_mma<N>(Ws, Ys, N, acc);
+    __syncthreads();
+    cta_mma_foreach<N>(acc, [&](int i, int j, double v) { Ws[i * C::S + j] = sgn * v; });
+    __syncthreads();
+    // a4: M = X + (sgn Y) C  -> Xs
+    cta_mma<N>(Ys, Ws, N, acc);
+    __syncthreads();
+    cta_mma_foreach<N>(acc, [&](int i, int j, double v) {
+        Xs[i * C::S + j] = (i < n && j < n) ? fma(sgn, v, Xs[i * C::S + j]) : 0.0;
+    });
+    __syncthreads();
+    // a5: Re = M^{-1} -> Ys
+    load_blocks<double, N>(a, Xs, n);
+    gj_sweep<double, N>(a, n, sm.sw, pmax, pmin);
+    const int inf_m = sweep_info<double, N>(sm.sw, n, pmax);
+    sweep_store<double, N>(a, sm.sw, Ys);
+    __syncthreads();
+    // a6/a7: Im = -C Re, interleaved store
+    cta_mma<N>(Ws, Ys, N, acc);
+    cta_mma_foreach<N>(acc, [&](int i, int j, double v) {
+        if (i < n && j < n) {
+            const double re = Ys[i * C::S + j];
+            Xb[i * n + j] = (use == 1) ? make_double2(re, -v) : make_double2(-v, -re);
+        }
+    });
+    if (tid == 0) {
+        info[b] = (inf_x < 0) ? 1 : (inf_x ? inf_x : inf_m);
+        if (bused) bused[b] = (inf_x < 0) ? 0 : (unsigned char)use;
+    }
+}
+
+// ----------------------------------------------------------------- complex-LU comparator
+// Complex Gauss-Jordan sweep with partial pivoting on |re|+|im| (same pivots as complex
+// LU with partial pivoting); inverse written straight to the output.
+template <int N>
+struct ZSmem {
+    double2 buf[N * BCfg<N>::S];
+    SweepShared<double2, N> sw;
+};
+
+template <int N>
+__global__ void __launch_bounds__(BCfg<N>::THREADS)
+zinv_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__restrict__ X, long long sX,
+                    int n, int *__restrict__ info) {
+    using C = BCfg<N>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ZSmem<N> &sm = *reinterpret_cast<ZSmem<N> *>(smem_raw);
+    const int tid = threadIdx.x;
+    const long long b = blockIdx.x;
+    const double2 *Zb = Z + b * sZ;
+    double2 *Xb = X + b * sX;
+    for (int idx = tid; idx < N * N; idx += C::THREADS) {
+        const int i = idx / N, j = idx - i * N;
+        sm.buf[i * C::S + j] = (i < n && j < n) ? Zb[i * n + j] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    double2 a[4][4];
+    double pmax, pmin;
+    load_blocks<double2, N>(a, sm.buf, n);
+    gj_sweep<double2, N>(a, n, sm.sw, pmax, pmin);
+    const int inf = sweep_info<double2, N>(sm.sw, n, pmax);
+    sweep_store<double2, N>(a, sm.sw, sm.buf);
+    __syncthreads();
+    for (int idx = tid; idx < n * n; idx += C::THREADS) {
+        const int i = idx / n, j = idx - i * n;
+        Xb[i * n + j] = sm.buf[i * C::S + j];
+    }
+    if (tid == 0) info[b] = inf;
+}
+
+template <typename K>
+static cudaError_t set_smem(K kern, size_t bytes) {
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+}  // namespace frob
+
+using namespace frob;
+
+extern "C" {
+
+size_t frob_inv_batched_workspace_bytes(int n, int batch) { (void)n; (void)batch; return 0; }
+size_t zinv_lu_batched_workspace_bytes(int n, int batch) { (void)n; (void)batch; return 0; }
+
+frob_status frob_inv_batched(int n, int batch, const double *Z, long long strideZ, double *X,
+                             long long strideX, int branch, int *d_info, unsigned char *d_branch_used,
+                             void *ws, size_t ws_bytes, void *stream) {
+    (void)ws; (void)ws_bytes;
+    if (n < 1 || n > 64 || batch < 0 || !d_info || strideZ < (long long)n * n || strideX < (long long)n * n ||
+        branch < 0 || branch > 2)
+        return FROB_ERR_INVALID_ARG;
+    if (batch == 0) return FROB_OK;
+    if (!Z || !X) return FROB_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    const double2 *Zc = reinterpret_cast<const double2 *>(Z);
+    double2 *Xc = reinterpret_cast<double2 *>(X);
+    cudaError_t e;
+    if (n <= 32) {
+        const size_t smem = sizeof(FrobSmem<32>);
+        if ((e = set_smem(frob_batched_kernel<32>, smem)) != cudaSuccess) return FROB_ERR_CUDA;
+        count_launch();
+        frob_batched_kernel<32><<<batch, BCfg<32>::THREADS, smem, s>>>(Zc, strideZ, Xc, strideX, n, branch,
+                                                                       d_info, d_branch_used);
+    } else {
+        const size_t smem = sizeof(FrobSmem<64>);
+        if ((e = set_smem(frob_batched_kernel<64>, smem)) != cudaSuccess) return FROB_ERR_CUDA;
+        count_launch();
+        frob_batched_kernel<64><<<batch, BCfg<64>::THREADS, smem, s>>>(Zc, strideZ, Xc, strideX, n, branch,
+                                                                       d_info, d_branch_used);
+    }
+    return cudaGetLastError() == cudaSuccess ? FROB_OK : FROB_ERR_CUDA;
+}
+
+frob_status zinv_lu_batched(int n, int batch, const double *Z, long long strideZ, double *X,
+                            long long strideX, int *d_info, void *ws, size_t ws_bytes, void *stream) {
+    (void)ws; (void)ws_bytes;
+    if (n < 1 || n > 64 || batch < 0 || !d_info || strideZ < (long long)n * n || strideX < (long long)n * n)
+        return FROB_ERR_INVALID_ARG;
+    if (batch == 0) return FROB_OK;
+    if (!Z || !X) return FROB_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    const double2 *Zc = reinterpret_cast<const double2 *>(Z);
+    double2 *Xc = reinterpret_cast<double2 *>(X);
+    cudaError_t e;
+    if (n <= 32) {
+        const size_t smem = sizeof(ZSmem<32>);
+        if ((e = set_smem(zinv_batched_kernel<32>, smem)) != cudaSuccess) return FROB_ERR_CUDA;
+        count_launch();
+        zinv_batched_kernel<32><<<batch, BCfg<32>::THREADS, smem, s>>>(Zc, strideZ, Xc, strideX, n, d_info);
+    } else {
+        const size_t smem = sizeof(ZSmem<64>);
+        if ((e = set_smem(zinv_batched_kernel<64>, smem)) != cudaSuccess) return FROB_ERR_CUDA;
+        count_launch();
+        zinv_batched_kernel<64><<<batch, BCfg<64>::THREADS, smem, s>>>(Zc, strideZ, Xc, strideX, n, d_info);
+    }
+    return cudaGetLastError() == cudaSuccess ? FROB_OK : FROB_ERR_CUDA;
+}
+
+}  // extern "C"

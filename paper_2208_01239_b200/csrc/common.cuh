@@ -1,0 +1,107 @@
+// common.cuh -- shared device helpers of the CUDA path (sm_100a).
+// Element types: double (real) and double2 (complex, .x = re, .y = im).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstddef>
+
+#define FROB_DEV __device__ __forceinline__
+
+namespace frob {
+
+// process-wide count of kernel launches issued by the library (frob_launch_count())
+unsigned long long &launch_counter();
+inline void count_launch(unsigned long long k = 1) { __atomic_fetch_add(&launch_counter(), k, __ATOMIC_RELAXED); }
+
+// ------------------------------------------------------------------ element ops
+FROB_DEV double zero_of(double) { return 0.0; }
+FROB_DEV double2 zero_of(double2) { return make_double2(0.0, 0.0); }
+FROB_DEV double one_of(double) { return 1.0; }
+FROB_DEV double2 one_of(double2) { return make_double2(1.0, 0.0); }
+
+// pivot magnitude: |x| for real, |re|+|im| for complex (LAPACK idamax / izamax)
+FROB_DEV double pmag(double v) { return fabs(v); }
+FROB_DEV double pmag(double2 v) { return fabs(v.x) + fabs(v.y); }
+// pivot-search key: NaN counts as +inf so a pivot always exists (the non-finite
+// result is then reported through the nonfinite flag instead of faulting)
+template <typename T>
+FROB_DEV double pkey(T v) {
+    const double m = pmag(v);
+    return (m != m) ? INFINITY : m;
+}
+FROB_DEV bool is_zero(double v) { return v == 0.0; }
+FROB_DEV bool is_zero(double2 v) { return v.x == 0.0 && v.y == 0.0; }
+
+FROB_DEV double mul(double a, double b) { return a * b; }
+FROB_DEV double2 mul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// c - a*b
+FROB_DEV double msub(double c, double a, double b) { return fma(-a, b, c); }
+FROB_DEV double2 msub(double2 c, double2 a, double2 b) {
+    return make_double2(fma(-a.x, b.x, fma(a.y, b.y, c.x)), fma(-a.x, b.y, fma(-a.y, b.x, c.y)));
+}
+// c + a*b
+FROB_DEV double madd(double c, double a, double b) { return fma(a, b, c); }
+FROB_DEV double2 madd(double2 c, double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
+FROB_DEV double add(double a, double b) { return a + b; }
+FROB_DEV double2 add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+FROB_DEV double neg(double a) { return -a; }
+FROB_DEV double2 neg(double2 a) { return make_double2(-a.x, -a.y); }
+FROB_DEV double recip(double a) { return 1.0 / a; }
+FROB_DEV double2 recip(double2 a) {
+    // 1/(x+iy) = (x - iy)/(x^2+y^2), scaled to avoid overflow/underflow of x^2+y^2
+    double s = fmax(fabs(a.x), fabs(a.y));
+    double xs = a.x / s, ys = a.y / s;
+    double d = s * (xs * xs + ys * ys);
+    return make_double2(xs / d, -ys / d);
+}
+FROB_DEV double scal(double a, double s) { return a * s; }
+FROB_DEV double2 scal(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+FROB_DEV bool finite_of(double v) { return isfinite(v); }
+FROB_DEV bool finite_of(double2 v) { return isfinite(v.x) && isfinite(v.y); }
+
+FROB_DEV double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+FROB_DEV double2 shfl(double2 v, int src) {
+    return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+// argmax key: larger magnitude wins; ties -> smaller row index (first max)
+struct ArgMax {
+    double v;
+    int i;
+};
+FROB_DEV bool better(double v1, int i1, double v2, int i2) {
+    return (v1 > v2) || (v1 == v2 && i1 < i2);
+}
+FROB_DEV ArgMax warp_argmax(double v, int i) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        double v2 = __shfl_xor_sync(0xffffffffu, v, off);
+        int i2 = __shfl_xor_sync(0xffffffffu, i, off);
+        if (better(v2, i2, v, i)) { v = v2; i = i2; }
+    }
+    return ArgMax{v, i};
+}
+
+// ------------------------------------------------------------------ FP64 tensor core
+// mma.sync m8n8k4 f64 (SASS DMMA.8x8x4).  Fragments (g = lane>>2, t = lane&3):
+//   a = A[g][t], b = B[t][g], c0 = C[g][2t], c1 = C[g][2t+1].
+FROB_DEV void dmma(double &c0, double &c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// ------------------------------------------------------------------ cp.async
+FROB_DEV void cp_async16(void *smem, const void *gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+FROB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+FROB_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+}  // namespace frob

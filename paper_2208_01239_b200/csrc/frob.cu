@@ -1,0 +1,620 @@
+// frob.cu -- single-matrix Frobenius inversion (Alg 1), the complex-LU
+// comparator (Alg 3 over C), real inversion / GEMM / LU entry points, and the Newton
+// drivers.  Host orchestration only; every arithmetic step runs in the kernels of
+// gemm.cuh / lu.cu / this file.
+#include <cstdio>
+#include <cstring>
+#include <cmath>
+#include <climits>
+#include "lu.cuh"
+#include "../../include/frobinv.h"
+
+namespace frob {
+
+static thread_local char g_last_cuda[256] = "";
+
+unsigned long long &launch_counter() {
+    static unsigned long long c = 0;
+    return c;
+}
+
+static frob_status cuda_fail(cudaError_t e) {
+    snprintf(g_last_cuda, sizeof(g_last_cuda), "%s", cudaGetErrorString(e));
+    return FROB_ERR_CUDA;
+}
+#define FROB_CUDA(x)                                   \
+    do {                                               \
+        cudaError_t _e = (x);                          \
+        if (_e != cudaSuccess) return cuda_fail(_e);   \
+    } while (0)
+
+static long long ld_of(int n) { return ((long long)n + 7) / 8 * 8; }
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+// Bump allocator over the caller's workspace.
+struct Carve {
+    unsigned char *base;
+    size_t off, cap;
+    template <typename T>
+    T *take(size_t count) {
+        T *p = reinterpret_cast<T *>(base ? base + off : nullptr);
+        off += align256(count * sizeof(T));
+        return p;
+    }
+};
+
+// ---------------------------------------------------------------------- elementwise
+// a0: split interleaved Z (ldz) into planar A, B (ld) and a copy of the branch matrix
+__global__ void split_kernel(const double2 *__restrict__ Z, long long ldz, int n, double *__restrict__ A,
+                             double *__restrict__ B, double *__restrict__ W, int wsel, long long ld,
+                             int *__restrict__ nonfinite) {
+    const long long total = (long long)n * n;
+    int bad = 0;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / n), j = (int)(idx - (long long)i * n);
+        const double2 z = Z[(long long)i * ldz + j];
+        bad |= !(isfinite(z.x) && isfinite(z.y));
+        const long long o = (long long)i * ld + j;
+        A[o] = z.x;
+        B[o] = z.y;
+        if (W) W[o] = (wsel == 2) ? z.y : z.x;
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
+}
+
+template <typename T>
+__global__ void copy2d_kernel(const T *__restrict__ src, long long lds, T *__restrict__ dst, long long ldd,
+                              int n, int *__restrict__ nonfinite) {
+    const long long total = (long long)n * n;
+    int bad = 0;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / n), j = (int)(idx - (long long)i * n);
+        const T v = src[(long long)i * lds + j];
+        if (nonfinite) bad |= !finite_of(v);
+        dst[(long long)i * ldd + j] = v;
+    }
+    if (nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
+}
+
+static int ew_blocks(long long total) {
+    return (int)std::min<long long>((total + 255) / 256, 148LL * 8);
+}
+
+// ---------------------------------------------------------------------- workspace
+struct FrobWs {
+    double *A, *B, *W1, *W2, *W3, *W4, *W5;
+    double *diag;
+    int *perm_x, *perm_b, *perm_m, *mv;
+    LuStats *stats;   // [0] A, [1] B, [2] M
+    int *flags;       // [0] nonfinite
+    size_t bytes;
+};
+
+static FrobWs carve_frob(void *ws, int n) {
+    const long long ld = ld_of(n);
+    Carve c{reinterpret_cast<unsigned char *>(ws), 0, 0};
+    FrobWs w{};
+    w.A = c.take<double>((size_t)n * ld);
+    w.B = c.take<double>((size_t)n * ld);
+    w.W1 = c.take<double>((size_t)n * ld);
+    w.W2 = c.take<double>((size_t)n * ld);
+    w.W3 = c.take<double>((size_t)n * ld);
+    w.W4 = c.take<double>((size_t)n * ld);
+    w.W5 = c.take<double>((size_t)n * ld);
+    w.diag = c.take<double>((size_t)n);
+    w.perm_x = c.take<int>((size_t)n);
+    w.perm_b = c.take<int>((size_t)n);
+    w.perm_m = c.take<int>((size_t)n);
+    w.mv = c.take<int>(MV_INTS);
+    w.stats = c.take<LuStats>(3);
+    w.flags = c.take<int>(4);
+    w.bytes = c.off;
+    return w;
+}
+
+struct ZluWs {
+    double2 *W, *U, *L, *diag;
+    int *perm, *mv;
+    LuStats *stats;
+    int *flags;
+    size_t bytes;
+};
+
+static ZluWs carve_zlu(void *ws, int n) {
+    const long long ld = ld_of(n);
+    Carve c{reinterpret_cast<unsigned char *>(ws), 0, 0};
+    ZluWs w{};
+    w.W = c.take<double2>((size_t)n * ld);
+    w.U = c.take<double2>((size_t)n * ld);
+    w.L = c.take<double2>((size_t)n * ld);
+    w.diag = c.take<double2>((size_t)n);
+    w.perm = c.take<int>((size_t)n);
+    w.mv = c.take<int>(MV_INTS);
+    w.stats = c.take<LuStats>(1);
+    w.flags = c.take<int>(4);
+    w.bytes = c.off;
+    return w;
+}
+
+static bool overlap(const void *a, size_t na, const void *b, size_t nb) {
+    const char *x = (const char *)a, *y = (const char *)b;
+    return x < y + nb && y < x + na;
+}
+
+// ---------------------------------------------------------------------- frob_inv
+static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *X, long long ldx,
+                                 int branch, void *ws, size_t ws_bytes, cudaStream_t s,
+                                 frob_info *host_info) {
+    if (n < 1 || !Z || !X || ldz < n || ldx < n || branch < 0 || branch > 2) return FROB_ERR_INVALID_ARG;
+    if (overlap(Z, (size_t)((n - 1) * ldz + n) * 16, X, (size_t)((n - 1) * ldx + n) * 16))
+        return FROB_ERR_INVALID_ARG;
+    FrobWs w = carve_frob(nullptr, n);
+    if (!ws || ws_bytes < w.bytes) return FROB_ERR_WORKSPACE;
+    w = carve_frob(ws, n);
+    const long long ld = ld_of(n);
+    const double2 *Zc = reinterpret_cast<const double2 *>(Z);
+
+    FROB_CUDA(cudaMemsetAsync(w.flags, 0, 4 * sizeof(int), s));
+    // a0: ingest
+    count_launch();
+    split_kernel<<<ew_blocks((long long)n * n), 256, 0, s>>>(Zc, ldz, n, w.A, w.B, w.W1,
+                                                             branch == FROB_BRANCH_B ? 2 : 1, ld, w.flags);
+    FROB_CUDA(cudaGetLastError());
+
+    // a1: LU of the branch matrix (A unless forced B)
+    int use = (branch == FROB_BRANCH_B) ? 2 : 1;
+    int *perm = w.perm_x;
+    double *Xlu = w.W1;
+    FROB_CUDA(getrf<double>(n, Xlu, ld, perm, w.mv, w.diag, &w.stats[use == 1 ? 0 : 1], s));
+
+    LuStats hs[3];
+    for (auto &h : hs) { h.rho = NAN; h.umax = 0; h.info = 0; h.nonfinite = 0; }
+    int hflags = 0;
+    if (branch == FROB_BRANCH_AUTO) {
+        // a1': branch check (reading R1) -- one small device->host read
+        FROB_CUDA(cudaMemcpyAsync(&hs[0], &w.stats[0], sizeof(LuStats), cudaMemcpyDeviceToHost, s));
+        FROB_CUDA(cudaMemcpyAsync(&hflags, w.flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+        FROB_CUDA(cudaStreamSynchronize(s));
+        if (hflags) {
+            if (host_info) { host_info->info = 0; host_info->branch_used = 0; }
+            return FROB_ERR_NONFINITE;
+        }
+        if (hs[0].info != 0 || !(hs[0].rho <= 256.0)) {
+            count_launch();
+            copy2d_kernel<double><<<ew_blocks((long long)n * n), 256, 0, s>>>(w.B, ld, w.W5, ld, n, nullptr);
+            FROB_CUDA(cudaGetLastError());
+            FROB_CUDA(getrf<double>(n, w.W5, ld, w.perm_b, w.mv, w.diag, &w.stats[1], s));
+            FROB_CUDA(cudaMemcpyAsync(&hs[1], &w.stats[1], sizeof(LuStats), cudaMemcpyDeviceToHost, s));
+            FROB_CUDA(cudaStreamSynchronize(s));
+            const bool sa = hs[0].info != 0, sb = hs[1].info != 0;
+            if (sa && sb) {
+                if (host_info) {
+                    host_info->info = hs[0].info; host_info->branch_used = 0;
+                    host_info->rho_a = hs[0].rho; host_info->rho_b = hs[1].rho; host_info->rho_m = NAN;
+                }
+                return FROB_ERR_BOTH_SINGULAR;
+            }
+            if (sa || (!sb && hs[1].rho < hs[0].rho)) {
+                use = 2;
+                perm = w.perm_b;
+                Xlu = w.W5;
+            }
+        }
+    }
+    const double *Xm = (use == 1) ? w.A : w.B;   // X of Alg 1
+    const double *Ym = (use == 1) ? w.B : w.A;   // Y of Alg 1 (S2 uses Y = -A via sgn)
+    const double sgn = (use == 1) ? 1.0 : -1.0;
+
+    // a2: Xinv' = U^{-1} L^{-1}  (X^{-1} = Xinv' P)
+    FROB_CUDA(inv_from_lu<double>(n, Xlu, ld, w.W2, w.W3, w.W4, ld, nullptr, s));
+    // a3: C = X^{-1} Y = Xinv' (P Y)   [B-row gather]
+    {
+        auto p = gemm_params<double>(n, n, n, sgn, w.W4, ld, Ym, ld, 0.0, nullptr, ld, w.W2, ld);
+        p.browmap = perm;
+        FROB_CUDA(gemm_launch<double>(p, 1, s));
+    }
+    // a4: M = X + Y C
+    {
+        auto p = gemm_params<double>(n, n, n, sgn, Ym, ld, w.W2, ld, 1.0, Xm, ld, w.W3, ld);
+        FROB_CUDA(gemm_launch<double>(p, 1, s));
+    }
+    // a5: Re' = M^{-1} (un-permuted)
+    FROB_CUDA(getrf<double>(n, w.W3, ld, w.perm_m, w.mv, w.diag, &w.stats[2], s));
+    double *Re = (use == 1) ? w.A : w.B;  // X buffer is free now
+    FROB_CUDA(inv_from_lu<double>(n, w.W3, ld, w.W1, w.W4, Re, ld, nullptr, s));
+    // a6/a7: Im' = -C Re', fused with the column interchanges and the interleaved store
+    {
+        auto p = gemm_params<double>(n, n, n, -1.0, w.W2, ld, Re, ld, 0.0, Re, ld, X, ldx);
+        p.epi = (use == 1) ? EPI_FROB_A : EPI_FROB_B;
+        p.colperm = w.perm_m;
+        FROB_CUDA(gemm_launch<double>(p, 1, s));
+    }
+    if (host_info) {
+        FROB_CUDA(cudaMemcpyAsync(hs, w.stats, 3 * sizeof(LuStats), cudaMemcpyDeviceToHost, s));
+        FROB_CUDA(cudaMemcpyAsync(&hflags, w.flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+        FROB_CUDA(cudaStreamSynchronize(s));
+        host_info->branch_used = use;
+        host_info->rho_a = (use == 1 || branch == FROB_BRANCH_AUTO) ? hs[0].rho : NAN;
+        host_info->rho_b = (use == 2 || (branch == FROB_BRANCH_AUTO && !std::isnan(hs[1].rho))) ? hs[1].rho : NAN;
+        host_info->rho_m = hs[2].rho;
+        const int ix = (use == 1) ? hs[0].info : hs[1].info;
+        host_info->info = ix ? ix : hs[2].info;
+        if (hflags) return FROB_ERR_NONFINITE;
+        if (host_info->info) return FROB_ERR_SINGULAR;
+    }
+    return FROB_OK;
+}
+
+// ---------------------------------------------------------------------- zinv_lu
+static frob_status zinv_lu_impl(int n, const double *Z, long long ldz, double *X, long long ldx,
+                                void *ws, size_t ws_bytes, cudaStream_t s, int *host_info) {
+    if (n < 1 || !Z || !X || ldz < n || ldx < n) return FROB_ERR_INVALID_ARG;
+    if (overlap(Z, (size_t)((n - 1) * ldz + n) * 16, X, (size_t)((n - 1) * ldx + n) * 16))
+        return FROB_ERR_INVALID_ARG;
+    ZluWs w = carve_zlu(nullptr, n);
+    if (!ws || ws_bytes < w.bytes) return FROB_ERR_WORKSPACE;
+    w = carve_zlu(ws, n);
+    const long long ld = ld_of(n);
+    FROB_CUDA(cudaMemsetAsync(w.flags, 0, 4 * sizeof(int), s));
+    count_launch();
+    copy2d_kernel<double2><<<ew_blocks((long long)n * n), 256, 0, s>>>(
+        reinterpret_cast<const double2 *>(Z), ldz, w.W, ld, n, w.flags);
+    FROB_CUDA(cudaGetLastError());
+    FROB_CUDA(getrf<double2>(n, w.W, ld, w.perm, w.mv, w.diag, w.stats, s));
+    FROB_CUDA(inv_from_lu<double2>(n, w.W, ld, w.U, w.L, reinterpret_cast<double2 *>(X), ldx, w.perm, s));
+    if (host_info) {
+        LuStats hs;
+        int hf = 0;
+        FROB_CUDA(cudaMemcpyAsync(&hs, w.stats, sizeof(LuStats), cudaMemcpyDeviceToHost, s));
+        FROB_CUDA(cudaMemcpyAsync(&hf, w.flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+        FROB_CUDA(cudaStreamSynchronize(s));
+        *host_info = hs.info;
+        if (hf) return FROB_ERR_NONFINITE;
+        if (hs.info) return FROB_ERR_SINGULAR;
+    }
+    return FROB_OK;
+}
+
+// ---------------------------------------------------------------------- real inverse
+struct DinvWs {
+    double *W, *U, *L, *diag;
+    int *perm, *mv;
+    LuStats *stats;
+    size_t bytes;
+};
+static DinvWs carve_dinv(void *ws, int n) {
+    const long long ld = ld_of(n);
+    Carve c{reinterpret_cast<unsigned char *>(ws), 0, 0};
+    DinvWs w{};
+    w.W = c.take<double>((size_t)n * ld);
+    w.U = c.take<double>((size_t)n * ld);
+    w.L = c.take<double>((size_t)n * ld);
+    w.diag = c.take<double>((size_t)n);
+    w.perm = c.take<int>((size_t)n);
+    w.mv = c.take<int>(MV_INTS);
+    w.stats = c.take<LuStats>(1);
+    w.bytes = c.off;
+    return w;
+}
+
+// ---------------------------------------------------------------------- Newton
+// X <- (X + Y^op)/2 where Y^op = Y (sign) or conj(Y)^T (polar); per-block partial sums
+// of |Xnew - Xold|^2 and |Xnew|^2 (deterministic two-pass reduction).
+template <bool POLAR>
+__global__ void __launch_bounds__(256) newton_update_kernel(double2 *__restrict__ X, const double2 *__restrict__ Y,
+                                                            int n, double *__restrict__ partial) {
+    __shared__ double2 tile[32][33];
+    __shared__ double rs[8][2];
+    const int tiles = (n + 31) / 32;
+    double s_d = 0.0, s_x = 0.0;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    for (int tb = blockIdx.x; tb < tiles * tiles; tb += gridDim.x) {
+        const int bi = tb / tiles, bj = tb - bi * tiles;
+        if (POLAR) {
+            // load Y block (bj, bi) transposed
+            __syncthreads();
+            for (int r = ty; r < 32; r += 8) {
+                const int gi = bj * 32 + r, gj = bi * 32 + tx;
+                if (gi < n && gj < n) tile[r][tx] = Y[(long long)gi * n + gj];
+            }
+            __syncthreads();
+        }
+        for (int r = ty; r < 32; r += 8) {
+            const int gi = bi * 32 + r, gj = bj * 32 + tx;
+            if (gi >= n || gj >= n) continue;
+            double2 y;
+            if (POLAR) {
+                const double2 t = tile[tx][r];
+                y = make_double2(t.x, -t.y);
+            } else {
+                y = Y[(long long)gi * n + gj];
+            }
+            const double2 x = X[(long long)gi * n + gj];
+            const double2 xn = make_double2(0.5 * (x.x + y.x), 0.5 * (x.y + y.y));
+            const double dx = xn.x - x.x, dy = xn.y - x.y;
+            s_d = fma(dx, dx, fma(dy, dy, s_d));
+            s_x = fma(xn.x, xn.x, fma(xn.y, xn.y, s_x));
+            X[(long long)gi * n + gj] = xn;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s_d += __shfl_xor_sync(0xffffffffu, s_d, o);
+        s_x += __shfl_xor_sync(0xffffffffu, s_x, o);
+    }
+    if (tx == 0) { rs[ty][0] = s_d; rs[ty][1] = s_x; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0, b = 0;
+        for (int i = 0; i < 8; ++i) { a += rs[i][0]; b += rs[i][1]; }
+        partial[2 * blockIdx.x] = a;
+        partial[2 * blockIdx.x + 1] = b;
+    }
+}
+
+__global__ void reduce_pairs_kernel(const double *__restrict__ partial, int nb, double *__restrict__ out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double a = 0, b = 0;
+        for (int i = 0; i < nb; ++i) { a += partial[2 * i]; b += partial[2 * i + 1]; }
+        out[0] = a;
+        out[1] = b;
+    }
+}
+
+// H = (W + W^H)/2
+__global__ void herm_sym_kernel(const double2 *__restrict__ W, double2 *__restrict__ H, int n) {
+    const long long total = (long long)n * n;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / n), j = (int)(idx - (long long)i * n);
+        const double2 a = W[(long long)i * n + j], b = W[(long long)j * n + i];
+        H[idx] = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+    }
+}
+// V = U^H
+__global__ void conj_transpose_kernel(const double2 *__restrict__ U, double2 *__restrict__ V, int n) {
+    const long long total = (long long)n * n;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / n), j = (int)(idx - (long long)i * n);
+        const double2 a = U[(long long)j * n + i];
+        V[idx] = make_double2(a.x, -a.y);
+    }
+}
+
+constexpr int NEWTON_BLOCKS = 296;
+
+static size_t inv_ws_bytes(int n, int method) {
+    return method == FROB_INV_ZLU ? carve_zlu(nullptr, n).bytes : carve_frob(nullptr, n).bytes;
+}
+
+static size_t newton_ws_bytes(int n, int method) {
+    return align256(inv_ws_bytes(n, method)) + align256((size_t)n * n * 16) * 2 +
+           align256(NEWTON_BLOCKS * 2 * sizeof(double)) + align256(2 * sizeof(double));
+}
+
+static frob_status newton_impl(bool polar, int n, const double *Z, double *S, double *Hout, double tol,
+                               int max_iter, int method, void *ws, size_t ws_bytes, cudaStream_t s,
+                               int *iters, double *final_delta, double *trace) {
+    if (n < 1 || !Z || !S || max_iter < 1 || !(tol > 0) || !iters || !final_delta ||
+        (method != FROB_INV_FROBENIUS && method != FROB_INV_ZLU) || (polar && !Hout))
+        return FROB_ERR_INVALID_ARG;
+    if (overlap(Z, (size_t)n * n * 16, S, (size_t)n * n * 16)) return FROB_ERR_INVALID_ARG;
+    if (!ws || ws_bytes < newton_ws_bytes(n, method)) return FROB_ERR_WORKSPACE;
+    unsigned char *b = reinterpret_cast<unsigned char *>(ws);
+    const size_t ib = align256(inv_ws_bytes(n, method));
+    void *iws = b;
+    double *Yinv = reinterpret_cast<double *>(b + ib);
+    double *Tmp = reinterpret_cast<double *>(b + ib + align256((size_t)n * n * 16));
+    double *partial = reinterpret_cast<double *>(b + ib + 2 * align256((size_t)n * n * 16));
+    double *sums = partial + align256(NEWTON_BLOCKS * 2 * sizeof(double)) / sizeof(double);
+
+    FROB_CUDA(cudaMemcpyAsync(S, Z, (size_t)n * n * 16, cudaMemcpyDeviceToDevice, s));
+    const int tiles = (n + 31) / 32;
+    const int nb = std::min(NEWTON_BLOCKS, tiles * tiles);
+    double delta = INFINITY;
+    int it = 0;
+    frob_status st = FROB_OK;
+    for (it = 0; it < max_iter;) {
+        if (method == FROB_INV_ZLU) st = zinv_lu_impl(n, S, n, Yinv, n, iws, ib, s, nullptr);
+        else st = frob_inv_impl(n, S, n, Yinv, n, FROB_BRANCH_AUTO, iws, ib, s, nullptr);
+        if (st != FROB_OK) return st;
+        count_launch();
+        if (polar)
+            newton_update_kernel<true><<<nb, 256, 0, s>>>(reinterpret_cast<double2 *>(S),
+                                                           reinterpret_cast<const double2 *>(Yinv), n, partial);
+        else
+            newton_update_kernel<false><<<nb, 256, 0, s>>>(reinterpret_cast<double2 *>(S),
+                                                            reinterpret_cast<const double2 *>(Yinv), n, partial);
+        FROB_CUDA(cudaGetLastError());
+        count_launch();
+        reduce_pairs_kernel<<<1, 32, 0, s>>>(partial, nb, sums);
+        FROB_CUDA(cudaGetLastError());
+        double h[2];
+        FROB_CUDA(cudaMemcpyAsync(h, sums, sizeof(h), cudaMemcpyDeviceToHost, s));
+        FROB_CUDA(cudaStreamSynchronize(s));
+        delta = std::sqrt(h[0]) / std::sqrt(h[1]);
+        if (trace) trace[it] = delta;
+        ++it;
+        if (delta < tol) break;
+    }
+    *iters = it;
+    *final_delta = delta;
+    if (polar) {
+        // H = (U^H A + (U^H A)^H) / 2
+        const double2 *U2 = reinterpret_cast<const double2 *>(S);
+        count_launch();
+        conj_transpose_kernel<<<ew_blocks((long long)n * n), 256, 0, s>>>(U2, reinterpret_cast<double2 *>(Yinv), n);
+        FROB_CUDA(cudaGetLastError());
+        auto p = gemm_params<double2>(n, n, n, 1.0, reinterpret_cast<const double2 *>(Yinv), n,
+                                      reinterpret_cast<const double2 *>(Z), n, 0.0, nullptr, n,
+                                      reinterpret_cast<double2 *>(Tmp), n);
+        FROB_CUDA(gemm_launch<double2>(p, 1, s));
+        count_launch();
+        herm_sym_kernel<<<ew_blocks((long long)n * n), 256, 0, s>>>(reinterpret_cast<const double2 *>(Tmp),
+                                                                     reinterpret_cast<double2 *>(Hout), n);
+        FROB_CUDA(cudaGetLastError());
+        FROB_CUDA(cudaStreamSynchronize(s));
+    }
+    return (delta < tol) ? FROB_OK : FROB_ERR_NOT_CONVERGED;
+}
+
+}  // namespace frob
+
+// =====================================================================================
+// C ABI
+// =====================================================================================
+using namespace frob;
+
+extern "C" {
+
+size_t frob_inv_workspace_bytes(int n) { return n < 1 ? 0 : carve_frob(nullptr, n).bytes; }
+
+frob_status frob_inv(int n, const double *Z, long long ldz, double *X, long long ldx, int branch,
+                     void *ws, size_t ws_bytes, void *stream, frob_info *host_info) {
+    return frob_inv_impl(n, Z, ldz, X, ldx, branch, ws, ws_bytes, (cudaStream_t)stream, host_info);
+}
+
+size_t frob_inv_host_workspace_bytes(int n) {
+    return n < 1 ? 0 : align256(frob_inv_workspace_bytes(n)) + 2 * align256((size_t)n * n * 16);
+}
+
+frob_status frob_inv_host(int n, const double *Z_host, double *X_host, int branch, void *ws,
+                          size_t ws_bytes, void *stream, frob_info *host_info) {
+    if (n < 1 || !Z_host || !X_host) return FROB_ERR_INVALID_ARG;
+    if (!ws || ws_bytes < frob_inv_host_workspace_bytes(n)) return FROB_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned char *b = reinterpret_cast<unsigned char *>(ws);
+    const size_t ib = align256(frob_inv_workspace_bytes(n));
+    double *Zd = reinterpret_cast<double *>(b + ib);
+    double *Xd = reinterpret_cast<double *>(b + ib + align256((size_t)n * n * 16));
+    FROB_CUDA(cudaMemcpyAsync(Zd, Z_host, (size_t)n * n * 16, cudaMemcpyHostToDevice, s));
+    frob_status st = frob_inv_impl(n, Zd, n, Xd, n, branch, ws, ib, s, host_info);
+    if (st != FROB_OK) return st;
+    FROB_CUDA(cudaMemcpyAsync(X_host, Xd, (size_t)n * n * 16, cudaMemcpyDeviceToHost, s));
+    FROB_CUDA(cudaStreamSynchronize(s));
+    return FROB_OK;
+}
+
+size_t zinv_lu_workspace_bytes(int n) { return n < 1 ? 0 : carve_zlu(nullptr, n).bytes; }
+
+frob_status zinv_lu(int n, const double *Z, long long ldz, double *X, long long ldx, void *ws,
+                    size_t ws_bytes, void *stream, int *host_info) {
+    return zinv_lu_impl(n, Z, ldz, X, ldx, ws, ws_bytes, (cudaStream_t)stream, host_info);
+}
+
+size_t frob_newton_workspace_bytes(int n, int method) { return n < 1 ? 0 : newton_ws_bytes(n, method); }
+
+frob_status frob_sign_newton(int n, const double *Z, double *S, double tol, int max_iter, int method,
+                             void *ws, size_t ws_bytes, void *stream, int *host_iters,
+                             double *host_final_delta, double *host_trace) {
+    return newton_impl(false, n, Z, S, nullptr, tol, max_iter, method, ws, ws_bytes, (cudaStream_t)stream,
+                       host_iters, host_final_delta, host_trace);
+}
+
+frob_status frob_polar_newton(int n, const double *A, double *U, double *H, double tol, int max_iter,
+                              int method, void *ws, size_t ws_bytes, void *stream, int *host_iters,
+                              double *host_final_delta, double *host_trace) {
+    if (H && (overlap(H, (size_t)n * n * 16, A, (size_t)n * n * 16) ||
+              overlap(H, (size_t)n * n * 16, U, (size_t)n * n * 16)))
+        return FROB_ERR_INVALID_ARG;
+    return newton_impl(true, n, A, U, H, tol, max_iter, method, ws, ws_bytes, (cudaStream_t)stream,
+                       host_iters, host_final_delta, host_trace);
+}
+
+frob_status frob_dgemm(int m, int n, int k, double alpha, const double *A, long long lda, const double *B,
+                       long long ldb, double beta, double *C, long long ldc, void *stream) {
+    if (m < 0 || n < 0 || k < 0 || (m > 0 && n > 0 && (!C || ldc < n)) || (k > 0 && (!A || !B || lda < k || ldb < n)))
+        return FROB_ERR_INVALID_ARG;
+    auto p = gemm_params<double>(m, n, k, alpha, A, lda, B, ldb, beta, beta != 0.0 ? C : nullptr, ldc, C, ldc);
+    FROB_CUDA(gemm_launch<double>(p, 1, (cudaStream_t)stream));
+    return FROB_OK;
+}
+
+size_t frob_dinv_workspace_bytes(int n) { return n < 1 ? 0 : carve_dinv(nullptr, n).bytes; }
+
+frob_status frob_dinv(int n, const double *A, long long lda, double *Ainv, long long ldainv, void *ws,
+                      size_t ws_bytes, void *stream, frob_info *host_info) {
+    if (n < 1 || !A || !Ainv || lda < n || ldainv < n) return FROB_ERR_INVALID_ARG;
+    if (overlap(A, (size_t)((n - 1) * lda + n) * 8, Ainv, (size_t)((n - 1) * ldainv + n) * 8))
+        return FROB_ERR_INVALID_ARG;
+    DinvWs w = carve_dinv(nullptr, n);
+    if (!ws || ws_bytes < w.bytes) return FROB_ERR_WORKSPACE;
+    w = carve_dinv(ws, n);
+    cudaStream_t s = (cudaStream_t)stream;
+    const long long ld = ld_of(n);
+    count_launch();
+    copy2d_kernel<double><<<ew_blocks((long long)n * n), 256, 0, s>>>(A, lda, w.W, ld, n, nullptr);
+    FROB_CUDA(cudaGetLastError());
+    FROB_CUDA(getrf<double>(n, w.W, ld, w.perm, w.mv, w.diag, w.stats, s));
+    FROB_CUDA(inv_from_lu<double>(n, w.W, ld, w.U, w.L, Ainv, ldainv, w.perm, s));
+    if (host_info) {
+        LuStats hs;
+        FROB_CUDA(cudaMemcpyAsync(&hs, w.stats, sizeof(hs), cudaMemcpyDeviceToHost, s));
+        FROB_CUDA(cudaStreamSynchronize(s));
+        host_info->info = hs.info;
+        host_info->branch_used = 0;
+        host_info->rho_a = hs.rho;
+        host_info->rho_b = NAN;
+        host_info->rho_m = NAN;
+        if (hs.info) return FROB_ERR_SINGULAR;
+    }
+    return FROB_OK;
+}
+
+size_t frob_dgetrf_workspace_bytes(int n) {
+    if (n < 1) return 0;
+    Carve c{nullptr, 0, 0};
+    c.take<double>((size_t)n);
+    c.take<int>(MV_INTS);
+    c.take<LuStats>(1);
+    return c.off;
+}
+
+frob_status frob_dgetrf(int n, double *A, long long lda, int *perm, void *ws, size_t ws_bytes, void *stream,
+                        frob_info *host_info) {
+    if (n < 1 || !A || !perm || lda < n) return FROB_ERR_INVALID_ARG;
+    if (!ws || ws_bytes < frob_dgetrf_workspace_bytes(n)) return FROB_ERR_WORKSPACE;
+    Carve c{reinterpret_cast<unsigned char *>(ws), 0, 0};
+    double *diag = c.take<double>((size_t)n);
+    int *mv = c.take<int>(MV_INTS);
+    LuStats *st = c.take<LuStats>(1);
+    cudaStream_t s = (cudaStream_t)stream;
+    FROB_CUDA(getrf<double>(n, A, lda, perm, mv, diag, st, s));
+    if (host_info) {
+        LuStats hs;
+        FROB_CUDA(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+        FROB_CUDA(cudaStreamSynchronize(s));
+        host_info->info = hs.info;
+        host_info->branch_used = 0;
+        host_info->rho_a = hs.rho;
+        host_info->rho_b = NAN;
+        host_info->rho_m = NAN;
+        if (hs.info) return FROB_ERR_SINGULAR;
+    }
+    return FROB_OK;
+}
+
+const char *frob_status_string(int status) {
+    switch (status) {
+        case FROB_OK: return "ok";
+        case FROB_ERR_SINGULAR: return "singular pivot";
+        case FROB_ERR_BOTH_SINGULAR: return "both real and imaginary parts singular";
+        case FROB_ERR_NOT_CONVERGED: return "Newton iteration did not converge";
+        case FROB_ERR_INVALID_ARG: return "invalid argument";
+        case FROB_ERR_NONFINITE: return "non-finite input";
+        case FROB_ERR_WORKSPACE: return "workspace too small";
+        case FROB_ERR_CUDA: return "CUDA error";
+        default: return "unknown status";
+    }
+}
+
+const char *frob_last_cuda_error(void) { return g_last_cuda; }
+
+unsigned long long frob_launch_count(void) { return frob::launch_counter(); }
+
+int frob_version(void) { return 1; }
+
+}  // extern "C"

@@ -1,0 +1,228 @@
+// gemm.cuh -- FP64 tensor-core (DMMA) GEMM engine for the Frobenius path.
+//
+//   C = alpha * op_A * op_B + beta * D          (row-major, fp64 or complex fp64)
+//
+// Used for: LU trailing updates (Alg 3 line 1), the triangular-inverse recursion and
+// the product U^{-1} L^{-1} (Alg 3 lines 2-3), and the three Frobenius GEMMs
+// C = X^{-1} Y, M = X + Y C, Im = -C Re (Alg 1).
+//
+// Design (B200 / sm_100a): FP64 has no tcgen05 kind, so the tensor path is the
+// warp-level DMMA (mma.sync.m8n8k4.f64).  Operands are staged global -> shared memory
+// with a multi-stage cp.async (LDGSTS) pipeline; each warp owns a register tile of
+// 8x8 accumulators.  Shared-memory row strides are padded (real: +4 doubles, complex:
+// +4 / +2 elements) so every fragment load is bank-conflict free.
+// Extras fused into the kernel:
+//   - triangular operands: per-tile k-range restriction (skips all-zero blocks),
+//   - B row gather (rows of P*B without materialising it),
+//   - output column scatter (the column interchanges of A^{-1} = X P),
+//   - the final Frobenius epilogue: X[i][perm[j]] = (Re'[i][j], -(C Re')[i][j]) written
+//     interleaved (branch S1), or (Im', -Re') for branch S2.
+#pragma once
+#include "common.cuh"
+
+namespace frob {
+
+enum { TRI_NONE = 0, TRI_UPPER = 1, TRI_LOWER = 2 };
+enum { EPI_STORE = 0, EPI_FROB_A = 1, EPI_FROB_B = 2 };
+
+template <typename T>
+struct GemmParams {
+    int M, N, K;
+    const T *A; long long lda, sA;
+    const T *B; long long ldb, sB;
+    T *C; long long ldc, sC;         // EPI_FROB_*: C is reinterpreted as double2 (interleaved out)
+    const T *D; long long ldd, sD;   // beta input (may alias C) / Re' for EPI_FROB_*
+    double alpha, beta;
+    const int *browmap;              // nullable: row k of B is B[browmap[k]]
+    const int *colperm;              // nullable: output column j goes to colperm[j]
+    int triA, triB, epi;
+};
+
+template <typename T> struct GemmCfg;
+template <> struct GemmCfg<double> {
+    static constexpr int BM = 64, BN = 64, BK = 16, WGM = 2, WGN = 2, STAGES = 3;
+    static constexpr int PADA = 4, PADB = 4;
+};
+template <> struct GemmCfg<double2> {
+    static constexpr int BM = 64, BN = 64, BK = 8, WGM = 2, WGN = 4, STAGES = 3;
+    static constexpr int PADA = 4, PADB = 2;
+};
+
+template <typename T>
+constexpr size_t gemm_smem_bytes() {
+    using C = GemmCfg<T>;
+    return (size_t)C::STAGES * ((size_t)C::BM * (C::BK + C::PADA) + (size_t)C::BK * (C::BN + C::PADB)) * sizeof(T);
+}
+
+// ---------------------------------------------------------------- MMA micro-kernels
+template <int MT, int NT>
+FROB_DEV void mma_tile(double (&acc)[MT][NT][2], const double (&a)[MT], const double (&b)[NT]) {
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+}
+// complex: acc[..][0..1] real part, acc[..][2..3] imaginary part
+template <int MT, int NT>
+FROB_DEV void mma_tile(double (&acc)[MT][NT][4], const double2 (&a)[MT], const double2 (&b)[NT]) {
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+        double nai = -a[i].y;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            dmma(acc[i][j][0], acc[i][j][1], a[i].x, b[j].x);
+            dmma(acc[i][j][0], acc[i][j][1], nai, b[j].y);
+            dmma(acc[i][j][2], acc[i][j][3], a[i].x, b[j].y);
+            dmma(acc[i][j][2], acc[i][j][3], a[i].y, b[j].x);
+        }
+    }
+}
+
+template <typename T> struct AccW { static constexpr int V = 2; };
+template <> struct AccW<double2> { static constexpr int V = 4; };
+
+FROB_DEV double acc_val(const double (&c)[2], int e) { return c[e]; }
+FROB_DEV double2 acc_val(const double (&c)[4], int e) { return make_double2(c[e], c[2 + e]); }
+
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(GemmCfg<T>::WGM * GemmCfg<T>::WGN * 32)
+gemm_kernel(GemmParams<T> p) {
+    using Cf = GemmCfg<T>;
+    constexpr int BM = Cf::BM, BN = Cf::BN, BK = Cf::BK, STAGES = Cf::STAGES;
+    constexpr int NTH = Cf::WGM * Cf::WGN * 32;
+    constexpr int WM = BM / Cf::WGM, WN = BN / Cf::WGN, MT = WM / 8, NT = WN / 8;
+    constexpr int E = 16 / sizeof(T);
+    constexpr int SA = BK + Cf::PADA, SB = BN + Cf::PADB;
+    constexpr int V = AccW<T>::V;
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T *As = reinterpret_cast<T *>(smem_raw);
+    T *Bs = As + STAGES * BM * SA;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm0 = (warp / Cf::WGN) * WM, wn0 = (warp % Cf::WGN) * WN;
+    const long long bz = blockIdx.z;
+    const T *__restrict__ A = p.A + bz * p.sA;
+    const T *__restrict__ B = p.B + bz * p.sB;
+    const int M = p.M, N = p.N, K = p.K;
+    const int row0 = blockIdx.y * BM, col0 = blockIdx.x * BN;
+
+    int kb = 0, ke = K;
+    if (p.triA == TRI_UPPER) kb = max(kb, row0);
+    else if (p.triA == TRI_LOWER) ke = min(ke, row0 + BM);
+    if (p.triB == TRI_UPPER) ke = min(ke, col0 + BN);
+    else if (p.triB == TRI_LOWER) kb = max(kb, col0);
+    kb = (kb / BK) * BK;
+    const int nk = (ke > kb) ? (ke - kb + BK - 1) / BK : 0;
+
+    double acc[MT][NT][V];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int e = 0; e < V; ++e) acc[i][j][e] = 0.0;
+
+    auto load_stage = [&](int s, int kt) {
+        const int k0 = kb + kt * BK;
+        T *as = As + s * BM * SA;
+        T *bs = Bs + s * BK * SB;
+        constexpr int ACH = BM * BK / E;
+#pragma unroll 2
+        for (int c = tid; c < ACH; c += NTH) {
+            const int r = c / (BK / E), cc = (c % (BK / E)) * E;
+            const int gr = row0 + r, gk = k0 + cc;
+            T *dst = as + r * SA + cc;
+            if (VEC && gr < M && gk + E <= K) {
+                cp_async16(dst, A + (long long)gr * p.lda + gk);
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e)
+                    dst[e] = (gr < M && gk + e < K) ? A[(long long)gr * p.lda + gk + e] : zero_of(T());
+            }
+        }
+        constexpr int BCH = BK * BN / E;
+#pragma unroll 2
+        for (int c = tid; c < BCH; c += NTH) {
+            const int r = c / (BN / E), cc = (c % (BN / E)) * E;
+            const int gk = k0 + r, gc = col0 + cc;
+            T *dst = bs + r * SB + cc;
+            if (gk < K) {
+                const long long brow = p.browmap ? (long long)p.browmap[gk] : (long long)gk;
+                const T *src = B + brow * p.ldb + gc;
+                if (VEC && gc + E <= N) {
+                    cp_async16(dst, src);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) dst[e] = (gc + e < N) ? src[e] : zero_of(T());
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) dst[e] = zero_of(T());
+            }
+        }
+    };
+
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < nk) load_stage(s, s);
+        cp_async_commit();
+    }
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        {
+            const int nx = kt + STAGES - 1;
+            if (nx < nk) load_stage(nx % STAGES, nx);
+            cp_async_commit();
+        }
+        const T *as = As + (kt % STAGES) * BM * SA;
+        const T *bs = Bs + (kt % STAGES) * BK * SB;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            T a[MT], b[NT];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) a[i] = as[(wm0 + i * 8 + g) * SA + kk + t];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) b[j] = bs[(kk + t) * SB + wn0 + j * 8 + g];
+            mma_tile<MT, NT>(acc, a, b);
+        }
+    }
+    cp_async_wait<0>();
+
+    // ------------------------------------------------------------ epilogue
+    const T *__restrict__ D = p.D ? p.D + bz * p.sD : nullptr;
+    T *__restrict__ Cp = p.C + bz * p.sC;
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+        const int row = row0 + wm0 + i * 8 + g;
+        if (row >= M) continue;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = col0 + wn0 + j * 8 + 2 * t + e;
+                if (col >= N) continue;
+                T v = scal(acc_val(acc[i][j], e), p.alpha);
+                const int oc = p.colperm ? p.colperm[col] : col;
+                if constexpr (sizeof(T) == 8) {
+                    if (p.epi != EPI_STORE) {
+                        const double d = D[(long long)row * p.ldd + col];
+                        double2 *X = reinterpret_cast<double2 *>(Cp);
+                        X[(long long)row * p.ldc + oc] =
+                            (p.epi == EPI_FROB_A) ? make_double2(d, v) : make_double2(v, -d);
+                        continue;
+                    }
+                }
+                if (p.beta != 0.0) {
+                    const T d = D[(long long)row * p.ldd + col];
+                    v = add(v, scal(d, p.beta));
+                }
+                Cp[(long long)row * p.ldc + oc] = v;
+            }
+        }
+    }
+}
+
+}  // namespace frob

@@ -1,0 +1,58 @@
+// lu.cuh -- blocked LU with partial pivoting (Alg 3 line 1) and the explicit
+// inverse from the LU factors (Alg 3 lines 2-3), for real (double) and
+// complex (double2) matrices, row-major.
+//
+// Panel: one thread-block CLUSTER owns the m x PW panel in shared memory (rows split
+// across the CTAs).  Per column: each thread scans its rows, warp-shuffle argmax,
+// block argmax through shared memory, cluster argmax through DSMEM (one cluster
+// barrier per column), then every CTA applies the rank-1 update to its rows.  Rows are
+// never moved during the panel ("physical rows" + done flags); at the end each row is
+// written straight to its final position and the row movement list is emitted for the
+// rest of the matrix.
+#pragma once
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace frob {
+
+// device-side pivot diagnostics of one LU (filled by lu_stats_kernel)
+struct LuStats {
+    double rho;      // max|u_ii| / min|u_ii|
+    double umax;     // max|u_ii|
+    int info;        // 0 or 1-based first singular pivot column (reading R2)
+    int nonfinite;   // 1 if any pivot is NaN/Inf
+};
+
+// Row movement produced by one panel: rows src[q] -> dst[q] (global indices), q < cnt.
+// Layout in an int buffer: [cnt, dst[0..2PWMAX), src[0..2PWMAX)].
+constexpr int PW_MAX = 32;
+constexpr int MV_INTS = 1 + 4 * PW_MAX;
+
+template <typename T>
+cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuStats *stats,
+                  cudaStream_t s);
+
+// From an LU in `lu` (ld): Xinv = U^{-1} L^{-1} (un-permuted: A^{-1} = Xinv P).
+// Work buffers U, L (n x ld each) are overwritten; `lu` may be used as the
+// recursion scratch (it is destroyed) when lu_is_scratch.
+template <typename T>
+cudaError_t inv_from_lu(int n, T *lu, long long ld, T *U, T *L, T *out, long long ldo,
+                        const int *colperm, cudaStream_t s);
+
+template <typename T>
+cudaError_t gemm_launch(const GemmParams<T> &p, int batch, cudaStream_t s);
+
+template <typename T>
+GemmParams<T> gemm_params(int M, int N, int K, double alpha, const T *A, long long lda,
+                          const T *B, long long ldb, double beta, const T *D, long long ldd,
+                          T *C, long long ldc) {
+    GemmParams<T> p{};
+    p.M = M; p.N = N; p.K = K;
+    p.A = A; p.lda = lda; p.B = B; p.ldb = ldb;
+    p.C = C; p.ldc = ldc; p.D = D; p.ldd = ldd;
+    p.alpha = alpha; p.beta = beta;
+    p.triA = TRI_NONE; p.triB = TRI_NONE; p.epi = EPI_STORE;
+    return p;
+}
+
+}  // namespace frob

@@ -1,0 +1,287 @@
+"""Thin Python binding of libfrobinv.so (include/frobinv.h) -- argument marshalling only.
+
+Every step of the method runs in the CUDA kernels behind the C ABI; this module only
+allocates torch tensors for outputs / workspaces, passes device pointers and the
+current CUDA stream, and maps status codes to exceptions.  There is no CPU fallback:
+if the library is missing or no CUDA device is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfrobinv.so")
+
+STATUS = {0: "ok", 1: "singular", 2: "both_singular", 3: "not_converged", 4: "invalid_arg",
+          5: "nonfinite", 6: "workspace", 7: "cuda"}
+BRANCH = {"auto": 0, "a": 1, "b": 2}
+METHOD = {"frobenius": 0, "frob": 0, "zlu": 1}
+
+# header declarations (name -> (restype, argtypes)); tests check every one is exported
+_vp, _dp, _ip = ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)
+_ll, _i, _sz, _d = ctypes.c_longlong, ctypes.c_int, ctypes.c_size_t, ctypes.c_double
+
+
+class FrobInfo(ctypes.Structure):
+    _fields_ = [("info", ctypes.c_int), ("branch_used", ctypes.c_int), ("rho_a", ctypes.c_double),
+                ("rho_b", ctypes.c_double), ("rho_m", ctypes.c_double)]
+
+    def as_dict(self):
+        return {"info": self.info, "branch_used": self.branch_used, "rho_a": self.rho_a,
+                "rho_b": self.rho_b, "rho_m": self.rho_m}
+
+
+_FIP = ctypes.POINTER(FrobInfo)
+SIGNATURES = {
+    "frob_inv_workspace_bytes": (_sz, [_i]),
+    "frob_inv": (_i, [_i, _vp, _ll, _vp, _ll, _i, _vp, _sz, _vp, _FIP]),
+    "frob_inv_host_workspace_bytes": (_sz, [_i]),
+    "frob_inv_host": (_i, [_i, _vp, _vp, _i, _vp, _sz, _vp, _FIP]),
+    "zinv_lu_workspace_bytes": (_sz, [_i]),
+    "zinv_lu": (_i, [_i, _vp, _ll, _vp, _ll, _vp, _sz, _vp, _ip]),
+    "frob_inv_batched_workspace_bytes": (_sz, [_i, _i]),
+    "frob_inv_batched": (_i, [_i, _i, _vp, _ll, _vp, _ll, _i, _vp, _vp, _vp, _sz, _vp]),
+    "zinv_lu_batched_workspace_bytes": (_sz, [_i, _i]),
+    "zinv_lu_batched": (_i, [_i, _i, _vp, _ll, _vp, _ll, _vp, _vp, _sz, _vp]),
+    "frob_newton_workspace_bytes": (_sz, [_i, _i]),
+    "frob_sign_newton": (_i, [_i, _vp, _vp, _d, _i, _i, _vp, _sz, _vp, _ip, _dp, _dp]),
+    "frob_polar_newton": (_i, [_i, _vp, _vp, _vp, _d, _i, _i, _vp, _sz, _vp, _ip, _dp, _dp]),
+    "frob_dgemm": (_i, [_i, _i, _i, _d, _vp, _ll, _vp, _ll, _d, _vp, _ll, _vp]),
+    "frob_dinv_workspace_bytes": (_sz, [_i]),
+    "frob_dinv": (_i, [_i, _vp, _ll, _vp, _ll, _vp, _sz, _vp, _FIP]),
+    "frob_dgetrf_workspace_bytes": (_sz, [_i]),
+    "frob_dgetrf": (_i, [_i, _vp, _ll, _vp, _vp, _sz, _vp, _FIP]),
+    "frob_status_string": (ctypes.c_char_p, [_i]),
+    "frob_last_cuda_error": (ctypes.c_char_p, []),
+    "frob_version": (_i, []),
+    "frob_launch_count": (ctypes.c_ulonglong, []),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class FrobError(RuntimeError):
+    def __init__(self, fn, status, info=None):
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        self.info = info
+        msg = f"{fn}: {self.name}"
+        if status == 7 and _lib is not None:
+            msg += " (" + _lib.frob_last_cuda_error().decode() + ")"
+        if info is not None:
+            msg += f" info={info}"
+        super().__init__(msg)
+
+
+def load(path: str = LIB_PATH):
+    """Load libfrobinv.so (raises if it has not been built)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(path):
+                raise ImportError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+            L = ctypes.CDLL(path)
+            for name, (res, args) in SIGNATURES.items():
+                f = getattr(L, name)
+                f.restype = res
+                f.argtypes = args
+            _lib = L
+    return _lib
+
+
+def launch_count() -> int:
+    """Kernels launched through the library so far in this process."""
+    return int(load().frob_launch_count())
+
+
+def _need_cuda(t: torch.Tensor, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+_ws_cache: dict = {}
+
+
+def workspace(nbytes: int, device) -> torch.Tensor:
+    """Cached device workspace (uint8) of at least nbytes on `device`."""
+    key = (torch.device(device).index, torch.cuda.current_stream(device).cuda_stream)
+    t = _ws_cache.get(key)
+    if t is None or t.numel() < nbytes:
+        t = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+        _ws_cache[key] = t
+    return t
+
+
+def _p(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _check(fn, st, info=None):
+    if st != 0:
+        raise FrobError(fn, st, info)
+
+
+# ----------------------------------------------------------------------------- single matrix
+def inv(z: torch.Tensor, branch: str = "auto", out: torch.Tensor | None = None, info: bool = False):
+    """Z^{-1} by Frobenius inversion (Alg 1).  z: (n, n) complex128 CUDA tensor."""
+    L = load()
+    _need_cuda(z, "z")
+    assert z.dtype == torch.complex128 and z.dim() == 2 and z.shape[0] == z.shape[1]
+    z = z if z.stride(1) == 1 else z.contiguous()
+    n = z.shape[0]
+    x = out if out is not None else torch.empty((n, n), dtype=torch.complex128, device=z.device)
+    ws = workspace(L.frob_inv_workspace_bytes(n), z.device)
+    fi = FrobInfo()
+    st = L.frob_inv(n, _p(z), z.stride(0), _p(x), x.stride(0), BRANCH[branch], _p(ws), ws.numel(),
+                    _stream(), ctypes.byref(fi) if info else None)
+    _check("frob_inv", st, fi.as_dict() if info else None)
+    return (x, fi.as_dict()) if info else x
+
+
+def inv_host(z_host: torch.Tensor, x_host: torch.Tensor | None = None, branch: str = "auto",
+             device="cuda"):
+    """End-to-end call with HOST buffers (pinned recommended): H2D, invert, D2H."""
+    L = load()
+    assert z_host.dtype == torch.complex128 and not z_host.is_cuda and z_host.is_contiguous()
+    n = z_host.shape[0]
+    x_host = x_host if x_host is not None else torch.empty_like(z_host)
+    ws = workspace(L.frob_inv_host_workspace_bytes(n), device)
+    st = L.frob_inv_host(n, _p(z_host), _p(x_host), BRANCH[branch], _p(ws), ws.numel(), _stream(), None)
+    _check("frob_inv_host", st)
+    return x_host
+
+
+def zinv(z: torch.Tensor, out: torch.Tensor | None = None):
+    """Complex-LU inversion (Alg 3 over C), the comparator."""
+    L = load()
+    _need_cuda(z, "z")
+    assert z.dtype == torch.complex128 and z.dim() == 2
+    z = z if z.stride(1) == 1 else z.contiguous()
+    n = z.shape[0]
+    x = out if out is not None else torch.empty((n, n), dtype=torch.complex128, device=z.device)
+    ws = workspace(L.zinv_lu_workspace_bytes(n), z.device)
+    st = L.zinv_lu(n, _p(z), z.stride(0), _p(x), x.stride(0), _p(ws), ws.numel(), _stream(), None)
+    _check("zinv_lu", st)
+    return x
+
+
+# ----------------------------------------------------------------------------- batched
+def inv_batched(z: torch.Tensor, branch: str = "auto", out: torch.Tensor | None = None):
+    """Batched Frobenius inversion, z: (batch, n, n) complex128 contiguous, n <= 64.
+    Returns (X, info int32[batch], branch_used uint8[batch])."""
+    L = load()
+    _need_cuda(z, "z")
+    assert z.dtype == torch.complex128 and z.dim() == 3 and z.is_contiguous()
+    b, n, _ = z.shape
+    x = out if out is not None else torch.empty_like(z)
+    info = torch.empty(b, dtype=torch.int32, device=z.device)
+    bu = torch.empty(b, dtype=torch.uint8, device=z.device)
+    st = L.frob_inv_batched(n, b, _p(z), n * n, _p(x), n * n, BRANCH[branch], _p(info), _p(bu), None, 0,
+                            _stream())
+    _check("frob_inv_batched", st)
+    return x, info, bu
+
+
+def zinv_batched(z: torch.Tensor, out: torch.Tensor | None = None):
+    L = load()
+    _need_cuda(z, "z")
+    assert z.dtype == torch.complex128 and z.dim() == 3 and z.is_contiguous()
+    b, n, _ = z.shape
+    x = out if out is not None else torch.empty_like(z)
+    info = torch.empty(b, dtype=torch.int32, device=z.device)
+    st = L.zinv_lu_batched(n, b, _p(z), n * n, _p(x), n * n, _p(info), None, 0, _stream())
+    _check("zinv_lu_batched", st)
+    return x, info
+
+
+# ----------------------------------------------------------------------------- Newton drivers
+def sign(z: torch.Tensor, tol: float = 1e-12, max_iter: int = 50, method: str = "frobenius",
+         trace: bool = False):
+    """Matrix sign by Newton.  Returns (S, iters, final_delta[, deltas])."""
+    L = load()
+    _need_cuda(z, "z")
+    z = z.contiguous()
+    n = z.shape[0]
+    s = torch.empty_like(z)
+    ws = workspace(L.frob_newton_workspace_bytes(n, METHOD[method]), z.device)
+    it = ctypes.c_int(0)
+    fd = ctypes.c_double(0.0)
+    tr = (ctypes.c_double * max_iter)()
+    st = L.frob_sign_newton(n, _p(z), _p(s), tol, max_iter, METHOD[method], _p(ws), ws.numel(), _stream(),
+                            ctypes.byref(it), ctypes.byref(fd), tr)
+    if st not in (0, 3):
+        _check("frob_sign_newton", st)
+    out = (s, it.value, fd.value)
+    return out + ([tr[i] for i in range(it.value)],) if trace else out
+
+
+def polar(a: torch.Tensor, tol: float = 1e-12, max_iter: int = 50, method: str = "frobenius"):
+    """Polar decomposition A = U H by Newton.  Returns (U, H, iters, final_delta)."""
+    L = load()
+    _need_cuda(a, "a")
+    a = a.contiguous()
+    n = a.shape[0]
+    u = torch.empty_like(a)
+    h = torch.empty_like(a)
+    ws = workspace(L.frob_newton_workspace_bytes(n, METHOD[method]), a.device)
+    it = ctypes.c_int(0)
+    fd = ctypes.c_double(0.0)
+    st = L.frob_polar_newton(n, _p(a), _p(u), _p(h), tol, max_iter, METHOD[method], _p(ws), ws.numel(),
+                             _stream(), ctypes.byref(it), ctypes.byref(fd), None)
+    if st not in (0, 3):
+        _check("frob_polar_newton", st)
+    return u, h, it.value, fd.value
+
+
+# ----------------------------------------------------------------------------- real blocks
+def dgemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor | None = None, alpha: float = 1.0,
+          beta: float = 0.0):
+    L = load()
+    _need_cuda(a, "a")
+    m, k = a.shape
+    k2, n = b.shape
+    assert k == k2 and a.dtype == b.dtype == torch.float64
+    if c is None:
+        c = torch.empty((m, n), dtype=torch.float64, device=a.device)
+        beta = 0.0
+    st = L.frob_dgemm(m, n, k, alpha, _p(a), a.stride(0), _p(b), b.stride(0), beta, _p(c), c.stride(0),
+                      _stream())
+    _check("frob_dgemm", st)
+    return c
+
+
+def dinv(a: torch.Tensor, out: torch.Tensor | None = None, info: bool = False):
+    L = load()
+    _need_cuda(a, "a")
+    n = a.shape[0]
+    x = out if out is not None else torch.empty_like(a)
+    ws = workspace(L.frob_dinv_workspace_bytes(n), a.device)
+    fi = FrobInfo()
+    st = L.frob_dinv(n, _p(a), a.stride(0), _p(x), x.stride(0), _p(ws), ws.numel(), _stream(),
+                     ctypes.byref(fi) if info else None)
+    _check("frob_dinv", st, fi.as_dict() if info else None)
+    return (x, fi.as_dict()) if info else x
+
+
+def dgetrf(a: torch.Tensor):
+    """In-place LU of a copy: returns (LU, perm) with (P A)[i] = A[perm[i]]."""
+    L = load()
+    _need_cuda(a, "a")
+    lu = a.clone()
+    n = a.shape[0]
+    perm = torch.empty(n, dtype=torch.int32, device=a.device)
+    ws = workspace(L.frob_dgetrf_workspace_bytes(n), a.device)
+    fi = FrobInfo()
+    st = L.frob_dgetrf(n, _p(lu), lu.stride(0), _p(perm), _p(ws), ws.numel(), _stream(), ctypes.byref(fi))
+    if st not in (0, 1):
+        _check("frob_dgetrf", st)
+    return lu, perm, fi.as_dict()

@@ -1,0 +1,258 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Tolerances (BASELINE north_star):
+  ||X_gpu - X_oracle||_F / ||X_oracle||_F <= 1e-10   and   ||Z X_gpu - I||_F <= 1e-11 n
+for kappa_2(Z) <= 1e4.  GEMM / LU building blocks are checked tighter (rounding order
+differs only through FMA and blocking).  Bitwise invariants: conj(Z) -> conj(X),
+2Z -> X/2, B = 0 -> real inverse, repeat-run determinism.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+fb = pytest.importorskip("paper_2208_01239_b200")
+
+REL = 1e-10
+DEV = "cuda"
+
+
+def _t(z):
+    return torch.from_numpy(np.ascontiguousarray(z)).to(DEV)
+
+
+def _np(t):
+    return t.cpu().numpy()
+
+
+def _resid(z, x):
+    # independent library GEMM (torch complex128 matmul), not our kernels
+    zt, xt = _t(z), _t(x)
+    e = zt @ xt - torch.eye(z.shape[0], dtype=torch.complex128, device=DEV)
+    return float(torch.linalg.norm(e))
+
+
+def _check_inverse(z, x, ref=None, rel=REL):
+    n = z.shape[0]
+    if ref is None:
+        ref, info = oracle.zinv_gj(z)
+        assert info == 0
+    r = oracle.rel_fro(x, ref)
+    res = _resid(z, x)
+    assert r <= rel, f"rel {r:.3e}"
+    assert res <= 1e-11 * n, f"residual {res:.3e}"
+    return r, res
+
+
+# ------------------------------------------------------------------ building blocks
+@pytest.mark.parametrize("mnk", [(1, 1, 1), (7, 5, 3), (37, 53, 29), (64, 64, 64), (130, 70, 200),
+                                 (257, 129, 65), (512, 512, 512)])
+def test_dgemm(mnk):
+    m, n, k = mnk
+    rng = np.random.default_rng(m * 7 + n)
+    a = rng.standard_normal((m, k))
+    b = rng.standard_normal((k, n))
+    c0 = rng.standard_normal((m, n))
+    ref = oracle.dgemm(a, b)
+    c = _np(fb.dgemm(_t(a), _t(b)))
+    assert np.abs(c - ref).max() <= 1e-14 * k * np.abs(a).max() * np.abs(b).max() + 1e-300
+    ct = _t(c0)
+    fb.dgemm(_t(a), _t(b), ct, alpha=-0.5, beta=2.0)
+    np.testing.assert_allclose(_np(ct), 2.0 * c0 - 0.5 * ref, rtol=0, atol=1e-13 * k)
+
+
+def test_dgemm_exact_integers():
+    rng = np.random.default_rng(1)
+    a = rng.integers(-64, 64, size=(200, 300)).astype(float)
+    b = rng.integers(-64, 64, size=(300, 150)).astype(float)
+    assert np.array_equal(_np(fb.dgemm(_t(a), _t(b))), oracle.dgemm(a, b))
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 33, 100, 257, 1000])
+def test_dgetrf_reconstruction(n):
+    a, _ = synth.gauss_pair(n, seed=n, shift=0.0)
+    lu, perm, info = fb.dgetrf(_t(a))
+    lu, perm = _np(lu), _np(perm)
+    assert sorted(perm.tolist()) == list(range(n))
+    l = np.tril(lu, -1) + np.eye(n)
+    u = np.triu(lu)
+    assert np.abs(l).max() <= 1.0 + 1e-15  # partial pivoting: |l_ij| <= 1
+    err = np.abs(a[perm] - l @ u).max()
+    assert err <= 20 * n * 2.0 ** -53 * np.abs(a).max() * max(1.0, np.abs(u).max() / np.abs(a).max())
+    # same pivots as the oracle (LAPACK order) when no near-ties: compare U diagonals
+    lo, ipiv, _ = oracle.dgetrf(a)
+    np.testing.assert_allclose(np.abs(np.diag(u)), np.abs(np.diag(lo)), rtol=1e-9)
+
+
+@pytest.mark.parametrize("n", [1, 7, 64, 100, 255, 512])
+def test_dinv(n):
+    a, _ = synth.gauss_pair(n, seed=n + 1, shift=math.sqrt(n))
+    ref, info, _ = oracle.dinv(a)
+    x = _np(fb.dinv(_t(a)))
+    assert oracle.rel_fro(x, ref) <= 1e-12 * max(1.0, np.linalg.cond(a))
+
+
+# ------------------------------------------------------------------ frob_inv (single)
+@pytest.mark.parametrize("n", [1, 2, 3, 17, 64, 100, 256, 513])
+@pytest.mark.parametrize("branch", ["auto", "a", "b"])
+def test_frob_inv_small(n, branch):
+    z = synth.shifted_complex(n, seed=100 + n, shift=math.sqrt(n) + 2.0)
+    if branch == "b":
+        z = z.imag * 0.5 + 1j * (z.real)  # make B the well-conditioned part
+    x, info = fb.inv(_t(z), branch=branch, info=True)
+    _check_inverse(z, _np(x))
+    if branch != "auto":
+        assert info["branch_used"] == (1 if branch == "a" else 2)
+
+
+def test_config1_all_paths():
+    """BASELINE config 1: n=64, both branches, AUTO, complex LU, batched kernel."""
+    z = synth.config1()
+    ref, _ = oracle.zinv_gj(z)
+    for br in ("auto", "a", "b"):
+        _check_inverse(z, _np(fb.inv(_t(z), branch=br)), ref)
+        xb, inf, bu = fb.inv_batched(_t(z[None]), branch=br)
+        assert int(inf[0]) == 0
+        _check_inverse(z, _np(xb)[0], ref)
+    _check_inverse(z, _np(fb.zinv(_t(z))), ref)
+    xz, inf = fb.zinv_batched(_t(z[None]))
+    _check_inverse(z, _np(xz)[0], ref)
+
+
+def test_config2_full_size():
+    """BASELINE config 2: n=1024 at full size, in the launch configuration bench.py times."""
+    z = synth.config2(1024)
+    ref, _ = oracle.zinv_gj(z)
+    x, info = fb.inv(_t(z), info=True)
+    _check_inverse(z, _np(x), ref)
+    assert info["branch_used"] == 1 and info["info"] == 0
+    _check_inverse(z, _np(fb.zinv(_t(z))), ref)
+    # the oracle's Frobenius (Alg 1 literally) agrees too
+    xo, st, _ = oracle.frob_inv(z)
+    assert oracle.rel_fro(_np(x), xo) <= REL
+
+
+@pytest.mark.parametrize("n", [1, 5, 31, 64, 129, 300])
+def test_zinv_lu(n):
+    z = synth.shifted_complex(n, seed=7 * n, shift=3.0 + math.sqrt(n))
+    _check_inverse(z, _np(fb.zinv(_t(z))))
+
+
+# ------------------------------------------------------------------ bitwise invariants
+def test_bitwise_invariants():
+    z = synth.shifted_complex(200, seed=3, shift=16.0)
+    x = _np(fb.inv(_t(z), branch="a"))
+    x2 = _np(fb.inv(_t(z), branch="a"))
+    assert np.array_equal(x, x2), "repeat-run determinism"
+    xc = _np(fb.inv(_t(np.conj(z)), branch="a"))
+    assert np.array_equal(xc, np.conj(x)), "conj(Z) -> conj(X)"
+    xs = _np(fb.inv(_t(2.0 * z), branch="a"))
+    assert np.array_equal(xs, x / 2.0), "2Z -> X/2"
+
+
+def test_b_zero_and_a_zero():
+    a, b = synth.gauss_pair(96, seed=4, shift=10.0)
+    x, info = fb.inv(_t(a + 0j), info=True)
+    x = _np(x)
+    assert info["branch_used"] == 1
+    assert not np.any(x.imag)
+    assert np.array_equal(x.real, _np(fb.dinv(_t(a))))
+    y, info = fb.inv(_t(1j * a), info=True)
+    y = _np(y)
+    assert info["branch_used"] == 2
+    assert not np.any(y.real)
+    np.testing.assert_allclose(y.imag, -x.real, rtol=0, atol=0)
+
+
+def test_auto_switches_and_both_singular():
+    n = 48
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((n, n))
+    a[:, 0] = a[:, 1] * (1 + 1e-9)
+    b = rng.standard_normal((n, n)) + 6 * np.eye(n)
+    z = a + 1j * b
+    x, info = fb.inv(_t(z), info=True)
+    assert info["branch_used"] == 2 and info["rho_a"] > 256
+    _check_inverse(z, _np(x), rel=1e-8)
+    with pytest.raises(fb.FrobError) as e:
+        fb.inv(_t(synth.dft_unitary(16)))
+    assert e.value.name == "both_singular"
+    xb, inf, bu = fb.inv_batched(_t(np.stack([z, synth.dft_unitary(n)])))
+    assert int(bu[0]) == 2 and int(inf[0]) == 0
+    assert int(bu[1]) == 0 and int(inf[1]) != 0
+
+
+def test_nonfinite_and_invalid():
+    z = synth.shifted_complex(32, seed=1)
+    z[3, 4] = np.nan
+    with pytest.raises(fb.FrobError) as e:
+        fb.inv(_t(z))
+    assert e.value.name == "nonfinite"
+    zt = _t(synth.shifted_complex(32, seed=1))
+    with pytest.raises(fb.FrobError) as e:
+        fb.inv(zt, out=zt)
+    assert e.value.name == "invalid_arg"
+
+
+# ------------------------------------------------------------------ batched
+@pytest.mark.parametrize("n", [1, 2, 17, 32, 50, 64])
+@pytest.mark.parametrize("branch", ["auto", "a"])
+def test_batched(n, branch):
+    cnt = 40
+    z = synth.batch(n, cnt, seed=9, shift=8.0)
+    x, inf, bu = fb.inv_batched(_t(z), branch=branch)
+    x, inf = _np(x), _np(inf)
+    xz, infz = fb.zinv_batched(_t(z))
+    xz = _np(xz)
+    for i in range(cnt):
+        ref, _ = oracle.zinv_gj(z[i])
+        assert inf[i] == 0
+        _check_inverse(z[i], x[i], ref)
+        _check_inverse(z[i], xz[i], ref)
+
+
+def test_batched_config3_n32_sample():
+    """Config 3 (n=32 half) at full batch: every output checked via residual, a sample vs oracle."""
+    z = synth.batch(32, 65536, seed=0)
+    x, inf, bu = fb.inv_batched(_t(z))
+    assert int(inf.abs().sum()) == 0
+    zt = _t(z)
+    e = torch.matmul(zt, x) - torch.eye(32, dtype=torch.complex128, device=DEV)
+    res = torch.linalg.norm(e, dim=(1, 2))
+    assert float(res.max()) <= 1e-11 * 32
+    xs = _np(x[::4096])
+    for k, i in enumerate(range(0, 65536, 4096)):
+        ref, _ = oracle.zinv_gj(z[i])
+        assert oracle.rel_fro(xs[k], ref) <= REL
+
+
+# ------------------------------------------------------------------ Newton drivers
+def test_sign_small_and_closed_form():
+    z, s, lam, sinv = synth.sign_instance(64, seed=0)
+    ref = (s * np.sign(lam.real)[None, :]) @ sinv
+    for m in ("frobenius", "zlu"):
+        st, it, d = fb.sign(_t(z), tol=1e-12, max_iter=50, method=m)
+        st = _np(st)
+        assert d < 1e-12 and it < 50
+        assert oracle.rel_fro(st, ref) <= 1e-11
+        so, ito, _ = oracle.sign_newton(z, method=m)
+        assert oracle.rel_fro(st, so) <= 1e-11
+        assert abs(it - ito) <= 1
+
+
+def test_polar_small():
+    n = 40
+    rng = np.random.default_rng(2)
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    c = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    h0 = c.conj().T @ c + n * np.eye(n)
+    a = q @ h0
+    u, h, it, d = fb.polar(_t(a), tol=1e-13)
+    u, h = _np(u), _np(h)
+    assert oracle.rel_fro(u, q) <= 1e-11 and oracle.rel_fro(h, h0) <= 1e-11
