@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstddef>
+#include <climits>
 
 #define FROB_DEV __device__ __forceinline__
 
@@ -84,6 +85,36 @@ FROB_DEV ArgMax warp_argmax(double v, int i) {
         if (better(v2, i2, v, i)) { v = v2; i = i2; }
     }
     return ArgMax{v, i};
+}
+
+// Exact warp argmax with redux.sync on the IEEE bit pattern of a non-negative key
+// (monotone as an unsigned integer): max of the high word, then of the low word among
+// the lanes holding that high word, then min index among the lanes holding both.
+// Same result as warp_argmax (first max); three REDUX instead of five shuffle rounds.
+FROB_DEV unsigned redux_max(unsigned v) {
+    unsigned r;
+    asm volatile("redux.sync.max.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+    return r;
+}
+FROB_DEV unsigned redux_min(unsigned v) {
+    unsigned r;
+    asm volatile("redux.sync.min.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+    return r;
+}
+// key must be >= 0 (or -1.0 for "no candidate", mapped below every real key)
+FROB_DEV ArgMax warp_argmax_redux(double key, int idx) {
+    const unsigned long long kb = (key < 0.0) ? 0ull : (unsigned long long)__double_as_longlong(key) + 1ull;
+    const unsigned hi = (unsigned)(kb >> 32), lo = (unsigned)kb;
+    const unsigned mh = redux_max(hi);
+    const unsigned ml = redux_max(hi == mh ? lo : 0u);
+    const bool cand = (hi == mh) && (lo == ml);
+    const unsigned mi = redux_min(cand ? (unsigned)idx : 0xffffffffu);
+    const unsigned long long mk = ((unsigned long long)mh << 32) | ml;
+    ArgMax r;
+    r.v = (mk == 0ull) ? -1.0 : __longlong_as_double((long long)(mk - 1ull));
+    r.i = (int)mi;
+    if (mk == 0ull) r.i = INT_MAX;
+    return r;
 }
 
 // ------------------------------------------------------------------ FP64 tensor core

@@ -192,8 +192,63 @@ gemm_kernel(GemmParams<T> p) {
     cp_async_wait<0>();
 
     // ------------------------------------------------------------ epilogue
+    // All reads of D (which may alias C) and of colperm are issued before any store so
+    // the memory latency is paid once, not once per element.
     const T *__restrict__ D = p.D ? p.D + bz * p.sD : nullptr;
-    T *__restrict__ Cp = p.C + bz * p.sC;
+    T *Cp = p.C + bz * p.sC;
+    if constexpr (sizeof(T) == 8) {
+        // fast path: interior tile, plain store, 16-byte aligned rows -> vector D/C access
+        const bool interior = (row0 + BM <= M) && (col0 + BN <= N) && p.epi == EPI_STORE && !p.colperm &&
+                              ((p.ldc & 1) == 0) && (!D || (p.ldd & 1) == 0) &&
+                              ((reinterpret_cast<uintptr_t>(Cp) & 15) == 0) &&
+                              (!D || (reinterpret_cast<uintptr_t>(D) & 15) == 0);
+        if (interior) {
+            const double alpha = p.alpha, beta = p.beta;
+            double2 dv2[MT][NT];
+            if (beta != 0.0) {
+#pragma unroll
+                for (int i = 0; i < MT; ++i)
+#pragma unroll
+                    for (int j = 0; j < NT; ++j)
+                        dv2[i][j] = *reinterpret_cast<const double2 *>(
+                            D + (long long)(row0 + wm0 + i * 8 + g) * p.ldd + col0 + wn0 + j * 8 + 2 * t);
+            }
+#pragma unroll
+            for (int i = 0; i < MT; ++i)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    double2 v = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
+                    if (beta != 0.0) {
+                        v.x = fma(beta, dv2[i][j].x, v.x);
+                        v.y = fma(beta, dv2[i][j].y, v.y);
+                    }
+                    *reinterpret_cast<double2 *>(Cp + (long long)(row0 + wm0 + i * 8 + g) * p.ldc + col0 + wn0 +
+                                                 j * 8 + 2 * t) = v;
+                }
+            return;
+        }
+    }
+    const bool needD = (p.epi != EPI_STORE) || (p.beta != 0.0);
+    T dv[MT][NT][2];
+    int oc[NT][2];
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int col = col0 + wn0 + j * 8 + 2 * t + e;
+            oc[j][e] = (p.colperm && col < N) ? p.colperm[col] : col;
+        }
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+        const int row = row0 + wm0 + i * 8 + g;
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int col = col0 + wn0 + j * 8 + 2 * t + e;
+                dv[i][j][e] = (needD && row < M && col < N) ? D[(long long)row * p.ldd + col] : zero_of(T());
+            }
+    }
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
         const int row = row0 + wm0 + i * 8 + g;
@@ -205,21 +260,17 @@ gemm_kernel(GemmParams<T> p) {
                 const int col = col0 + wn0 + j * 8 + 2 * t + e;
                 if (col >= N) continue;
                 T v = scal(acc_val(acc[i][j], e), p.alpha);
-                const int oc = p.colperm ? p.colperm[col] : col;
                 if constexpr (sizeof(T) == 8) {
                     if (p.epi != EPI_STORE) {
-                        const double d = D[(long long)row * p.ldd + col];
+                        const double d = dv[i][j][e];
                         double2 *X = reinterpret_cast<double2 *>(Cp);
-                        X[(long long)row * p.ldc + oc] =
+                        X[(long long)row * p.ldc + oc[j][e]] =
                             (p.epi == EPI_FROB_A) ? make_double2(d, v) : make_double2(v, -d);
                         continue;
                     }
                 }
-                if (p.beta != 0.0) {
-                    const T d = D[(long long)row * p.ldd + col];
-                    v = add(v, scal(d, p.beta));
-                }
-                Cp[(long long)row * p.ldc + oc] = v;
+                if (p.beta != 0.0) v = add(v, scal(dv[i][j][e], p.beta));
+                Cp[(long long)row * p.ldc + oc[j][e]] = v;
             }
         }
     }

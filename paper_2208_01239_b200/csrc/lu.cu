@@ -3,6 +3,8 @@
 #include <cooperative_groups.h>
 #include <climits>
 #include <cstdio>
+#include <utility>
+#include <type_traits>
 #include "lu.cuh"
 
 namespace cg = cooperative_groups;
@@ -45,132 +47,319 @@ template cudaError_t gemm_launch<double>(const GemmParams<double> &, int, cudaSt
 template cudaError_t gemm_launch<double2>(const GemmParams<double2> &, int, cudaStream_t);
 
 // =====================================================================================
-// Panel factorisation (cluster, DSMEM argmax)
+// Panel factorisation: rows in REGISTERS, one CTA (or a thread-block cluster with DSMEM)
 // =====================================================================================
-constexpr int PANEL_THREADS = 256;
-constexpr int PANEL_WARPS = PANEL_THREADS / 32;
+// Thread t of cluster rank c owns panel rows rbeg + t + q*PANEL_T (q < R), rbeg = c*R*PANEL_T,
+// all PW columns in registers.  The column loop is a compact runtime loop (a fully
+// unrolled panel overflows the instruction cache); register indices stay static by
+// ROTATING each row one slot per column: slot 0 always holds the current column, slots
+// 1..PW-1-j the columns to its right, and the finished column (multiplier, or U entry for
+// pivot rows) is rotated into slot PW-1.  Per column j:
+//   local argmax (slot 0) -> warp-shuffle argmax; the winning lane publishes its whole row
+//   next to the candidate -> ONE __syncthreads -> block argmax in every warp
+//   [cluster: CTA winner + row to DSMEM, ONE cluster barrier, cluster argmax]
+//   -> pivot row read with vector shared loads -> rank-1 update of own rows -> rotate.
+// Rows never move during the panel; at the end each row is written to its final
+// position and the row movement for the other columns is emitted.
+constexpr int PANEL_T = 256;
+constexpr int PANEL_W = PANEL_T / 32;
 
 template <typename T, int PW>
-struct PanelShared {
-    // fixed part (after the row tile and per-row ints)
-    double wred_v[2][PANEL_WARPS];
-    int wred_i[2][PANEL_WARPS];
-    double pub_v[2];
-    int pub_i[2];
-    T pubrow[2][PW];
-    T wpiv[PANEL_WARPS][PW];
-    int pivrows[PW];
-    T pvals[PW];
-    int vac[PW];
-    unsigned evmask;
-};
-
-template <typename T, int PW>
-static size_t panel_smem_bytes(int rpc) {
-    size_t tile = (size_t)rpc * (PW + 1) * sizeof(T);
-    size_t ints = (size_t)rpc * sizeof(int);
-    size_t off = (tile + ints + 15) & ~(size_t)15;
-    return off + sizeof(PanelShared<T, PW>);
+FROB_DEV void store_row(T *dst, const T (&r)[PW]) {
+    if constexpr (sizeof(T) == 8) {
+#pragma unroll
+        for (int c = 0; c < PW; c += 2)
+            *reinterpret_cast<double2 *>(dst + c) = make_double2(r[c], r[c + 1]);
+    } else {
+#pragma unroll
+        for (int c = 0; c < PW; ++c) dst[c] = r[c];
+    }
 }
 
-// P: panel top-left (row k0, col k0); m = n - k0 panel rows; w <= PW columns.
+template <typename T, int PW, int R>
+FROB_DEV void store_row_sel(T *dst, const T (&a)[R][PW], int q) {
+    switch (q) {
+        case 0: store_row<T, PW>(dst, a[0]); break;
+        case 1: if constexpr (R > 1) store_row<T, PW>(dst, a[1]); break;
+        case 2: if constexpr (R > 2) store_row<T, PW>(dst, a[2]); break;
+        default: if constexpr (R > 3) store_row<T, PW>(dst, a[R - 1]); break;
+    }
+}
+
 template <typename T, int PW>
-__global__ void __launch_bounds__(PANEL_THREADS)
-lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int rpc, int CS, int k0,
-                int *__restrict__ mv, T *__restrict__ diag) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T *tile = reinterpret_cast<T *>(smem_raw);
-    int *rowpiv = reinterpret_cast<int *>(smem_raw + (size_t)rpc * (PW + 1) * sizeof(T));
-    size_t off = ((size_t)rpc * (PW + 1) * sizeof(T) + (size_t)rpc * sizeof(int) + 15) & ~(size_t)15;
-    PanelShared<T, PW> &sh = *reinterpret_cast<PanelShared<T, PW> *>(smem_raw + off);
-    constexpr int TS = PW + 1;
+FROB_DEV void load_row(T (&u)[PW], const T *src) {
+    if constexpr (sizeof(T) == 8) {
+#pragma unroll
+        for (int c = 0; c < PW; c += 2) {
+            const double2 v = *reinterpret_cast<const double2 *>(src + c);
+            u[c] = v.x;
+            u[c + 1] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < PW; ++c) u[c] = src[c];
+    }
+}
+
+constexpr int PANEL_UNROLL = 4;
+
+#ifdef FROB_PANEL_TRACE
+__device__ long long g_panel_trace[64];
+#define PTRACE(i) do { if (threadIdx.x == 0 && blockIdx.x == 0) g_panel_trace[i] = clock64(); } while (0)
+#define PTRACEJ(j, i) do { if ((j) == 5) PTRACE(i); } while (0)
+#else
+#define PTRACE(i) do { } while (0)
+#define PTRACEJ(j, i) do { } while (0)
+#endif
+
+// Coalesced staging of 256-row chunks of the panel through shared memory (row stride
+// 18 doubles = 144 B: 16-byte aligned and conflict-free for per-thread 128-bit row access).
+constexpr int STG_STRIDE = 18;
+
+template <typename T, int PW, int R, bool CLUSTER>
+__global__ void __launch_bounds__(PANEL_T)
+lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, int *__restrict__ mv,
+                T *__restrict__ diag) {
+    constexpr int RW = PW * sizeof(T) / 8;  // row width in doubles (16)
+    static_assert(RW == 16, "panel rows are 128 bytes");
+    static_assert(PW % PANEL_UNROLL == 0, "PW must be a multiple of the unroll");
+    extern __shared__ __align__(16) double stg[];  // R * PANEL_T rows x STG_STRIDE doubles
+    __shared__ int sdst[R * PANEL_T];
+    __shared__ double wv[2][PANEL_W];
+    __shared__ int wi[2][PANEL_W];
+    __shared__ __align__(16) T wrow[2][PANEL_W][PW];  // each warp's candidate row (zero-padded)
+    __shared__ T wip[2][PANEL_W];                     // and the reciprocal of its pivot value
+    __shared__ __align__(16) T upiv[PANEL_W][PW];     // warp-private copy (cluster path)
+    __shared__ T upiv_ip[PANEL_W];
+    __shared__ T pubip[2];
+    __shared__ double pubv[2];
+    __shared__ int pubi[2];
+    __shared__ __align__(16) T pubrow[2][PW];
+    __shared__ int pivrows[PW];
+    __shared__ T pvals[PW];
+    __shared__ int vac[PW];
+    __shared__ unsigned evm;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int crank = 0;
-    if (CS > 1) crank = (int)cg::this_cluster().block_rank();
-    const int rbeg = crank * rpc;
-    const int nrows = max(0, min(rpc, m - rbeg));
+    if constexpr (CLUSTER) crank = (int)cg::this_cluster().block_rank();
+    constexpr int RPC = R * PANEL_T;
+    const int rbeg = crank * RPC;
+    const long long ldd = lda * (long long)(sizeof(T) / 8);  // leading dim in doubles
+    double *Pd = reinterpret_cast<double *>(P);
+    const int wd = w * (int)(sizeof(T) / 8);                 // live doubles per row
+    const bool vec = ((reinterpret_cast<uintptr_t>(Pd) & 15) == 0) && ((ldd & 1) == 0);
 
-    for (int idx = tid; idx < nrows * w; idx += PANEL_THREADS) {
-        const int r = idx / w, c = idx - r * w;
-        tile[r * TS + c] = P[(long long)(rbeg + r) * lda + c];
-    }
-    for (int r = tid; r < nrows; r += PANEL_THREADS) rowpiv[r] = -1;
-    __syncthreads();
-
-    for (int j = 0; j < w; ++j) {
-        const int par = j & 1;
-        double bv = -1.0;
-        int bi = INT_MAX;
-        for (int r = tid; r < nrows; r += PANEL_THREADS) {
-            if (rowpiv[r] < 0) {
-                const double v = pkey(tile[r * TS + j]);
-                if (better(v, rbeg + r, bv, bi)) { bv = v; bi = rbeg + r; }
-            }
+    PTRACE(0);
+    T a[R][PW];
+    int grow[R], pidx[R];
+    unsigned done = 0;
+    // coalesced cp.async of all R*256 rows (8 threads per 128-byte row) into shared memory
+#pragma unroll 4
+    for (int idx = tid; idx < RPC * 8; idx += PANEL_T) {
+        const int r = idx >> 3, c2 = (idx & 7) * 2;
+        double *d = &stg[r * STG_STRIDE + c2];
+        const int g = rbeg + r;
+        if (vec && g < m && c2 + 1 < wd) {
+            cp_async16(d, Pd + (long long)g * ldd + c2);
+        } else if (g < m && c2 + 1 < wd) {
+            d[0] = Pd[(long long)g * ldd + c2];
+            d[1] = Pd[(long long)g * ldd + c2 + 1];
+        } else {
+            d[0] = (g < m && c2 < wd) ? Pd[(long long)g * ldd + c2] : 0.0;
+            d[1] = 0.0;
         }
-        ArgMax wa = warp_argmax(bv, bi);
-        if (lane == 0) { sh.wred_v[par][warp] = wa.v; sh.wred_i[par][warp] = wa.i; }
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+        grow[q] = rbeg + q * PANEL_T + tid;
+        pidx[q] = -1;
+        if (grow[q] >= m) done |= 1u << q;
+        const double *row = &stg[(q * PANEL_T + tid) * STG_STRIDE];
+        double t[16];
+#pragma unroll
+        for (int c = 0; c < 16; c += 2) {
+            const double2 v = *reinterpret_cast<const double2 *>(row + c);
+            t[c] = v.x;
+            t[c + 1] = v.y;
+        }
+#pragma unroll
+        for (int c = 0; c < PW; ++c) {
+            if constexpr (sizeof(T) == 8) a[q][c] = t[c];
+            else a[q][c] = make_double2(t[2 * c], t[2 * c + 1]);
+        }
+    }
+    PTRACE(1);
+
+    // ---------------------------------------------------------------- column pipeline
+    // publish(j, S): candidate of column j (current slot S) -- local argmax, warp argmax
+    // (redux), candidate to wv/wi, the warp winner's row (zero-padded: rotated slot c is
+    // live iff (c-S) mod PW < PW-j) and its reciprocal (computed speculatively by every
+    // lane for its own candidate, overlapping the redux) to wrow[j&1][warp].
+    // finish(j, S): barrier, block argmax (+ cluster argmax), pivot row, then the update
+    // of the NEXT column's slot first, publish(j+1), and only then the other slots.
+    int qb_next = 0;
+    double bv_next = -1.0;
+    int bi_next = INT_MAX;
+    auto local_cand = [&](auto Sc) {
+        constexpr int S = decltype(Sc)::value % PW;
+        bv_next = -1.0;
+        bi_next = INT_MAX;
+        qb_next = 0;
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+            if (!((done >> q) & 1u)) {
+                const double v = pkey(a[q][S]);
+                if (better(v, grow[q], bv_next, bi_next)) { bv_next = v; bi_next = grow[q]; qb_next = q; }
+            }
+    };
+    auto publish = [&](const int j, auto Sc) {
+        // Sc may be PANEL_UNROLL (first column after the next rotation): the row is then
+        // stored already rotated so that it matches the frame the consumer will use.
+        constexpr int V = decltype(Sc)::value;
+        constexpr int S = V % PW;
+        constexpr int K = (V >= PANEL_UNROLL) ? PANEL_UNROLL : 0;
+        constexpr int SN = V - K;  // slot of column j after the rotation
+        const int par = j & 1;
+        T myp = zero_of(T());
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+            if (q == qb_next) myp = a[q][S];
+        const T myip = is_zero(myp) ? zero_of(T()) : recip(myp);  // speculative
+        const ArgMax wa = warp_argmax_redux(bv_next, bi_next);
+        if (lane == 0) { wv[par][warp] = wa.v; wi[par][warp] = wa.i; }
+        if (bi_next == wa.i && bi_next != INT_MAX) {
+#pragma unroll
+            for (int q = 0; q < R; ++q)
+                if (q == qb_next) {
+                    T r[PW];
+#pragma unroll
+                    for (int c = 0; c < PW; ++c)
+                        r[c] = (((c - SN + PW) % PW) < PW - j) ? a[q][(c + K) % PW] : zero_of(T());
+                    store_row<T, PW>(wrow[par][warp], r);
+                    wip[par][warp] = myip;
+                }
+        }
+    };
+    auto finish = [&](const int j, auto Sc) {
+        constexpr int S = decltype(Sc)::value % PW;
+        constexpr int S1 = (decltype(Sc)::value + 1) % PW;
+        const int par = j & 1;
         __syncthreads();
-        ArgMax ca = warp_argmax(lane < PANEL_WARPS ? sh.wred_v[par][lane] : -1.0,
-                                lane < PANEL_WARPS ? sh.wred_i[par][lane] : INT_MAX);
+        const ArgMax ca = warp_argmax_redux(lane < PANEL_W ? wv[par][lane] : -1.0,
+                                            lane < PANEL_W ? wi[par][lane] : INT_MAX);
+        const int cw = (ca.i == INT_MAX) ? 0 : ((ca.i - rbeg) % PANEL_T) >> 5;  // warp holding the CTA winner
         int gp;
-        T pv = zero_of(T());
-        if (CS == 1) {
+        T u[PW];
+        T ip;
+        if constexpr (!CLUSTER) {
             gp = ca.i;
-            if (lane < w) pv = tile[(gp - rbeg) * TS + lane];
+            load_row<T, PW>(u, wrow[par][cw]);
+            ip = wip[par][cw];
         } else {
             cg::cluster_group cl = cg::this_cluster();
             if (warp == 0) {
-                if (lane == 0) { sh.pub_v[par] = ca.v; sh.pub_i[par] = ca.i; }
-                if (lane < w && ca.i != INT_MAX) sh.pubrow[par][lane] = tile[(ca.i - rbeg) * TS + lane];
+                if (lane == 0) { pubv[par] = ca.v; pubi[par] = ca.i; pubip[par] = wip[par][cw]; }
+                if (lane < PW) pubrow[par][lane] = wrow[par][cw][lane];
             }
             cl.sync();
             double qv = -1.0;
             int qi = INT_MAX;
             if (lane < CS) {
-                qv = *cl.map_shared_rank(&sh.pub_v[par], lane);
-                qi = *cl.map_shared_rank(&sh.pub_i[par], lane);
+                qv = *cl.map_shared_rank(&pubv[par], lane);
+                qi = *cl.map_shared_rank(&pubi[par], lane);
             }
-            ArgMax ga = warp_argmax(qv, qi);
+            const ArgMax ga = warp_argmax_redux(qv, qi);
             gp = ga.i;
-            const int owner = gp / rpc;
-            if (lane < w) pv = *cl.map_shared_rank(&sh.pubrow[par][lane], owner);
+            const int owner = gp / RPC;
+            if (lane < PW) upiv[warp][lane] = *cl.map_shared_rank(&pubrow[par][lane], owner);
+            if (lane == 0) upiv_ip[warp] = *cl.map_shared_rank(&pubip[par], owner);
+            __syncwarp();
+            load_row<T, PW>(u, upiv[warp]);
+            ip = upiv_ip[warp];
+            __syncwarp();
         }
-        if (lane < PW) sh.wpiv[warp][lane] = pv;
-        __syncwarp();
-        const T piv = sh.wpiv[warp][j];
+        const T piv = u[S];
         const bool zp = is_zero(piv);
-        const T ip = zp ? zero_of(T()) : recip(piv);
-        if (tid == 0) { sh.pivrows[j] = gp; sh.pvals[j] = piv; }
-        for (int r = tid; r < nrows; r += PANEL_THREADS) {
-            if (rowpiv[r] >= 0) continue;
-            if (rbeg + r == gp) { rowpiv[r] = j; continue; }
-            if (zp) continue;
-            T *row = tile + r * TS;
-            const T l = mul(row[j], ip);
-            row[j] = l;
-            for (int c = j + 1; c < w; ++c) row[c] = msub(row[c], l, sh.wpiv[warp][c]);
+        if (tid == 0) { pivrows[j] = gp; pvals[j] = piv; }
+        T l[R];
+        bool act[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const bool live = !((done >> q) & 1u);
+            if (live && grow[q] == gp) { done |= 1u << q; pidx[q] = j; }
+            act[q] = live && grow[q] != gp && !zp;
+            l[q] = act[q] ? mul(a[q][S], ip) : a[q][S];
+            if (act[q] && S1 != S) a[q][S1] = msub(a[q][S1], l[q], u[S1]);
         }
+        if (j + 1 < w) {
+            local_cand(std::integral_constant<int, decltype(Sc)::value + 1>{});
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            if (act[q]) {
+#pragma unroll
+                for (int c = 0; c < PW; ++c)
+                    if (c != S && c != S1) a[q][c] = msub(a[q][c], l[q], u[c]);
+            }
+            a[q][S] = l[q];
+        }
+        if (j + 1 < w) publish(j + 1, std::integral_constant<int, decltype(Sc)::value + 1>{});
+        PTRACE(2 + j);
+    };
+    auto rotate = [&](auto Kc) {
+        constexpr int K = decltype(Kc)::value;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            T t[PW];
+#pragma unroll
+            for (int c = 0; c < PW; ++c) t[c] = a[q][(c + K) % PW];
+#pragma unroll
+            for (int c = 0; c < PW; ++c) a[q][c] = t[c];
+        }
+    };
+
+    local_cand(std::integral_constant<int, 0>{});
+    publish(0, std::integral_constant<int, 0>{});
+    int j = 0;
+#pragma unroll 1
+    for (; j + PANEL_UNROLL <= w; j += PANEL_UNROLL) {
+        finish(j + 0, std::integral_constant<int, 0>{});
+        finish(j + 1, std::integral_constant<int, 1>{});
+        finish(j + 2, std::integral_constant<int, 2>{});
+        finish(j + 3, std::integral_constant<int, 3>{});
+        rotate(std::integral_constant<int, PANEL_UNROLL>{});
     }
+    // tail (w % 4 columns, last panel only), then restore the original slot order
+    const int jt = j;
+    if (j < w) { finish(j, std::integral_constant<int, 0>{}); ++j; }
+    if (j < w) { finish(j, std::integral_constant<int, 1>{}); ++j; }
+    if (j < w) { finish(j, std::integral_constant<int, 2>{}); ++j; }
+    const int rem = (PW - jt) % PW;  // slots still to rotate so that slot c holds column c
+#pragma unroll 1
+    for (int r = 0; r < rem; ++r) rotate(std::integral_constant<int, 1>{});
     __syncthreads();
+    PTRACE(40);
 
     // final positions: pivot j -> row j; evicted rows (< w, not pivots) fill the rows
     // vacated by pivots that came from below (>= w), in pivot order.
     if (warp == 0) {
         bool rp = false;
         if (lane < w)
-            for (int q = 0; q < w; ++q) rp |= (sh.pivrows[q] == lane);
+            for (int q = 0; q < w; ++q) rp |= (pivrows[q] == lane);
         const unsigned pivmask = __ballot_sync(0xffffffffu, rp);
         const unsigned wmask = (w >= 32) ? 0xffffffffu : ((1u << w) - 1u);
         const unsigned evmask = wmask & ~pivmask;
-        const int gpj = lane < w ? sh.pivrows[lane] : -1;
+        const int gpj = lane < w ? pivrows[lane] : -1;
         const bool isv = lane < w && gpj >= w;
         const unsigned vb = __ballot_sync(0xffffffffu, isv);
-        if (isv) sh.vac[__popc(vb & ((1u << lane) - 1u))] = gpj;
-        if (lane == 0) sh.evmask = evmask;
+        if (isv) vac[__popc(vb & ((1u << lane) - 1u))] = gpj;
+        if (lane == 0) evm = evmask;
         __syncwarp();
         if (crank == 0) {
-            // movement list for the other columns (global row indices)
             const bool moved = lane < w && gpj != lane;
             const unsigned mb = __ballot_sync(0xffffffffu, moved);
             const int nm = __popc(mb);
@@ -182,44 +371,83 @@ lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int rpc, int CS,
             const bool ev = (evmask >> lane) & 1u;
             if (ev) {
                 const int q = nm + __popc(evmask & ((1u << lane) - 1u));
-                mv[1 + q] = k0 + sh.vac[__popc(evmask & ((1u << lane) - 1u))];
+                mv[1 + q] = k0 + vac[__popc(evmask & ((1u << lane) - 1u))];
                 mv[1 + 2 * PW_MAX + q] = k0 + lane;
             }
             if (lane == 0) mv[0] = nm + __popc(evmask);
-            if (lane < w) diag[k0 + lane] = sh.pvals[lane];
+            if (lane < w) diag[k0 + lane] = pvals[lane];
         }
     }
     __syncthreads();
-    for (int r = tid; r < nrows; r += PANEL_THREADS) {
-        const int g = rbeg + r;
-        int dst;
-        if (rowpiv[r] >= 0) dst = rowpiv[r];
-        else if (g < w) dst = sh.vac[__popc(sh.evmask & ((1u << g) - 1u))];
-        else dst = g;
-        rowpiv[r] = dst;
+    // write back through the staging buffer, coalesced, each row to its final position
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+        const int g = grow[q];
+        int dst = g;
+        if (pidx[q] >= 0) dst = pidx[q];
+        else if (g < w) dst = vac[__popc(evm & ((1u << g) - 1u))];
+        sdst[q * PANEL_T + tid] = (g < m) ? dst : -1;
+        double t[16];
+#pragma unroll
+        for (int c = 0; c < PW; ++c) {
+            if constexpr (sizeof(T) == 8) t[c] = a[q][c];
+            else { t[2 * c] = a[q][c].x; t[2 * c + 1] = a[q][c].y; }
+        }
+        double *row = &stg[(q * PANEL_T + tid) * STG_STRIDE];
+#pragma unroll
+        for (int c = 0; c < 16; c += 2) *reinterpret_cast<double2 *>(row + c) = make_double2(t[c], t[c + 1]);
     }
     __syncthreads();
-    for (int idx = tid; idx < nrows * w; idx += PANEL_THREADS) {
-        const int r = idx / w, c = idx - r * w;
-        P[(long long)rowpiv[r] * lda + c] = tile[r * TS + c];
+#pragma unroll 4
+    for (int idx = tid; idx < RPC * 8; idx += PANEL_T) {
+        const int r = idx >> 3, c2 = (idx & 7) * 2;
+        const int d = sdst[r];
+        if (d < 0 || c2 >= wd) continue;
+        double *out = Pd + (long long)d * ldd + c2;
+        const double2 v = *reinterpret_cast<const double2 *>(&stg[r * STG_STRIDE + c2]);
+        if (c2 + 1 < wd) {
+            if (vec) *reinterpret_cast<double2 *>(out) = v;
+            else { out[0] = v.x; out[1] = v.y; }
+        } else {
+            out[0] = v.x;
+        }
     }
+    PTRACE(41);
+    if constexpr (CLUSTER) cg::this_cluster().sync();  // no CTA leaves while its smem may still be read
 }
 
 // =====================================================================================
 // Row movement on the other columns + U12 = L11^{-1} A12 (unit lower forward solve)
 // =====================================================================================
-constexpr int SWP_COLS = 64;
+constexpr int SWP_COLS = 32;
 
+// One thread per column outside the panel.  Rows k0..k0+w-1 of column c are gathered
+// straight from their source rows (srcrow), the other moved rows (evicted -> vacated)
+// are copied; for c right of the panel the gathered top rows then get
+// U12 = L11^{-1} A12 (unit lower forward substitution in registers).  Every load of a
+// column is issued before its first store.
 template <typename T, int PW>
 __global__ void __launch_bounds__(SWP_COLS)
-lu_swap_trsm_kernel(T *__restrict__ A, long long lda, int n, int k0, int w,
-                    const int *__restrict__ mv, int *__restrict__ perm) {
+lu_swap_trsm_kernel(T *__restrict__ A, long long lda, int n, int k0, int w, const int *__restrict__ mv,
+                    int *__restrict__ perm) {
     __shared__ T Ls[PW][PW + 1];
-    __shared__ T buf[2 * PW][SWP_COLS];
+    __shared__ int srcrow[PW];
+    __shared__ int xdst[PW], xsrc[PW];  // moves with destination outside the top w rows
+    __shared__ int nx_s;
     __shared__ int ptmp[2 * PW];
     const int tid = threadIdx.x;
     const int cnt = mv[0];
     const int *dst = mv + 1, *src = mv + 1 + 2 * PW_MAX;
+    if (tid == 0) {
+        for (int i = 0; i < w; ++i) srcrow[i] = k0 + i;
+        int nx = 0;
+        for (int q = 0; q < cnt; ++q) {
+            const int d = dst[q];
+            if (d < k0 + w) srcrow[d - k0] = src[q];
+            else { xdst[nx] = d; xsrc[nx] = src[q]; ++nx; }
+        }
+        nx_s = nx;
+    }
     if (blockIdx.x == 0) {
         for (int q = tid; q < cnt; q += SWP_COLS) ptmp[q] = perm[src[q]];
         __syncthreads();
@@ -233,24 +461,29 @@ lu_swap_trsm_kernel(T *__restrict__ A, long long lda, int n, int k0, int w,
     const int v = blockIdx.x * SWP_COLS + tid;
     if (v >= n - w) return;
     const int c = (v < k0) ? v : v + w;
-    for (int q = 0; q < cnt; ++q) buf[q][tid] = A[(long long)src[q] * lda + c];
-    for (int q = 0; q < cnt; ++q) A[(long long)dst[q] * lda + c] = buf[q][tid];
-    if (c < k0 + w) return;
-    T x[PW];
+    const int nx = nx_s;
+    T x[PW], y[PW];
 #pragma unroll
-    for (int i = 0; i < PW; ++i) x[i] = (i < w) ? A[(long long)(k0 + i) * lda + c] : zero_of(T());
+    for (int i = 0; i < PW; ++i) x[i] = (i < w) ? A[(long long)srcrow[i] * lda + c] : zero_of(T());
 #pragma unroll
-    for (int i = 1; i < PW; ++i) {
-        if (i < w) {
-            T acc = x[i];
+    for (int i = 0; i < PW; ++i) y[i] = (i < nx) ? A[(long long)xsrc[i] * lda + c] : zero_of(T());
+    if (c >= k0 + w) {
 #pragma unroll
-            for (int q = 0; q < i; ++q) acc = msub(acc, Ls[i][q], x[q]);
-            x[i] = acc;
+        for (int i = 1; i < PW; ++i) {
+            if (i < w) {
+                T acc = x[i];
+#pragma unroll
+                for (int q = 0; q < i; ++q) acc = msub(acc, Ls[i][q], x[q]);
+                x[i] = acc;
+            }
         }
     }
 #pragma unroll
     for (int i = 0; i < PW; ++i)
         if (i < w) A[(long long)(k0 + i) * lda + c] = x[i];
+#pragma unroll
+    for (int i = 0; i < PW; ++i)
+        if (i < nx) A[(long long)xdst[i] * lda + c] = y[i];
 }
 
 // =====================================================================================
@@ -324,31 +557,39 @@ __global__ void iota_kernel(int *p, int n) {
 // =====================================================================================
 // getrf driver
 // =====================================================================================
-template <typename T, int PW>
-static cudaError_t launch_panel(T *P, long long lda, int m, int w, int k0, int *mv, T *diag,
-                                cudaStream_t s) {
-    // rows per CTA so that the tile fits in ~200 KB of shared memory
-    const size_t row_bytes = (size_t)(PW + 1) * sizeof(T) + sizeof(int);
-    const int maxrows = (int)((200 * 1024 - sizeof(PanelShared<T, PW>) - 64) / row_bytes);
-    int CS = (m + maxrows - 1) / maxrows;
-    if (CS < 1) CS = 1;
-    int rpc = (m + CS - 1) / CS;
-    const size_t smem = panel_smem_bytes<T, PW>(rpc);
-    auto kern = lu_panel_kernel<T, PW>;
+// panel width: 16 real / 8 complex columns (16 doubles per row in registers)
+template <typename T> struct PanelW { static constexpr int PW = 16; };
+template <> struct PanelW<double2> { static constexpr int PW = 8; };
+constexpr int PANEL_MAX_CS = 16;
+
+template <typename T, int PW, int R>
+static cudaError_t launch_panel_r(T *P, long long lda, int m, int w, int k0, int *mv, T *diag, int CS,
+                                  cudaStream_t s) {
+    const size_t smem = (size_t)R * PANEL_T * STG_STRIDE * sizeof(double);
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !attr_set[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaError_t e = cudaFuncSetAttribute(lu_panel_kernel<T, PW, R, false>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        e = cudaFuncSetAttribute(lu_panel_kernel<T, PW, R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(lu_panel_kernel<T, PW, R, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         attr_set[dev] = true;
     }
+    if (CS == 1) {
+        count_launch();
+        lu_panel_kernel<T, PW, R, false><<<1, PANEL_T, smem, s>>>(P, lda, m, w, 1, k0, mv, diag);
+        return cudaGetLastError();
+    }
+    auto kern = lu_panel_kernel<T, PW, R, true>;
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute attr[1];
     cfg.gridDim = dim3(CS, 1, 1);
-    cfg.blockDim = dim3(PANEL_THREADS, 1, 1);
+    cfg.blockDim = dim3(PANEL_T, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -356,23 +597,17 @@ static cudaError_t launch_panel(T *P, long long lda, int m, int w, int k0, int *
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = (CS > 1) ? 1 : 0;
+    cfg.numAttrs = 1;
     count_launch();
-    return cudaLaunchKernelEx(&cfg, kern, P, lda, m, w, rpc, CS, k0, mv, diag);
+    return cudaLaunchKernelEx(&cfg, kern, P, lda, m, w, CS, k0, mv, diag);
 }
 
-// Largest panel width whose cluster stays <= 16 CTAs.
-template <typename T>
-static int choose_pw(int n) {
-    const int rows32 = (int)((200 * 1024 - 2048) / ((32 + 1) * sizeof(T) + 4));
-    const int rows16 = (int)((200 * 1024 - 2048) / ((16 + 1) * sizeof(T) + 4));
-    if (sizeof(T) == 8) {
-        if ((n + rows32 - 1) / rows32 <= 8) return 32;
-        if ((n + rows16 - 1) / rows16 <= 16) return 16;
-        return 8;
-    }
-    if ((n + rows16 - 1) / rows16 <= 8) return 16;
-    return 8;
+template <typename T, int PW>
+static cudaError_t launch_panel(T *P, long long lda, int m, int w, int k0, int *mv, T *diag, cudaStream_t s) {
+    if (m <= PANEL_T) return launch_panel_r<T, PW, 1>(P, lda, m, w, k0, mv, diag, 1, s);
+    if (m <= 2 * PANEL_T) return launch_panel_r<T, PW, 2>(P, lda, m, w, k0, mv, diag, 1, s);
+    const int CS = (m + 4 * PANEL_T - 1) / (4 * PANEL_T);
+    return launch_panel_r<T, PW, 4>(P, lda, m, w, k0, mv, diag, CS, s);
 }
 
 template <typename T, int PW>
@@ -406,15 +641,7 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
     iota_kernel<<<(n + 255) / 256, 256, 0, s>>>(perm, n);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const int pw = choose_pw<T>(n);
-    if constexpr (sizeof(T) == 8) {
-        if (pw == 32) e = getrf_pw<T, 32>(n, A, lda, perm, mv, diag, s);
-        else if (pw == 16) e = getrf_pw<T, 16>(n, A, lda, perm, mv, diag, s);
-        else e = getrf_pw<T, 8>(n, A, lda, perm, mv, diag, s);
-    } else {
-        if (pw == 16) e = getrf_pw<T, 16>(n, A, lda, perm, mv, diag, s);
-        else e = getrf_pw<T, 8>(n, A, lda, perm, mv, diag, s);
-    }
+    e = getrf_pw<T, PanelW<T>::PW>(n, A, lda, perm, mv, diag, s);
     if (e != cudaSuccess) return e;
     if (stats) {
         count_launch();

@@ -1,0 +1,76 @@
+// panel_probe.cu -- cycle-level probe of the LU kernels (debug tool, not the product).
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DFROB_PANEL_TRACE -o tools/panel_probe tools/panel_probe.cu
+#include "../paper_2208_01239_b200/csrc/lu.cu"
+#include <vector>
+#include <random>
+using namespace frob;
+unsigned long long &frob::launch_counter() { static unsigned long long c = 0; return c; }
+
+int main(int argc, char **argv) {
+    int n = argc > 1 ? atoi(argv[1]) : 1024;
+    long long ld = n;
+    std::vector<double> h((size_t)n * n);
+    std::mt19937_64 g(1);
+    std::normal_distribution<double> nd;
+    for (auto &x : h) x = nd(g);
+    for (int i = 0; i < n; ++i) h[(size_t)i * n + i] += 32.0;
+    double *A, *diag;
+    int *perm, *mv;
+    cudaMalloc(&A, h.size() * 8);
+    cudaMalloc(&diag, n * 8);
+    cudaMalloc(&perm, n * 4);
+    cudaMalloc(&mv, MV_INTS * 4);
+    cudaMemcpy(A, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    // 1) one panel at k0 = 0 (m = n), traced
+    for (int rep = 0; rep < 3; ++rep) {
+        cudaMemcpy(A, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+        cudaEventRecord(e0);
+        launch_panel<double, 16>(A, ld, n, 16, 0, mv, diag, 0);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        long long tr[64];
+        cudaMemcpyFromSymbol(tr, g_panel_trace, sizeof(tr));
+        printf("panel m=%d: %.2f us | load %lld | cols:", n, ms * 1e3, tr[1] - tr[0]);
+        for (int j = 0; j < 16; ++j) printf(" %lld", tr[2 + j] - (j ? tr[1 + j] : tr[1]));
+        printf(" | tail %lld | store %lld\n", tr[40] - tr[17], tr[41] - tr[40]);
+        printf("   col5: wargmax %lld, lane0 store %lld, bar %lld, bargmax %lld, owner+bar2+load %lld, recip %lld, update %lld\n",
+               tr[51] - tr[50], tr[52] - tr[51], tr[53] - tr[52], tr[54] - tr[53], tr[55] - tr[54], tr[56] - tr[55], tr[7] - tr[56]);
+    }
+    // 2) kernel-only timings of the LU pieces
+    cudaMemcpy(A, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+    iota_kernel<<<(n + 255) / 256, 256>>>(perm, n);
+    float ms;
+    cudaEventRecord(e0);
+    for (int r = 0; r < 20; ++r) launch_panel<double, 16>(A, ld, n, 16, 0, mv, diag, 0);
+    cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+    printf("panel x20 avg %.2f us\n", ms * 1e3 / 20);
+    cudaEventRecord(e0);
+    for (int r = 0; r < 20; ++r) lu_swap_trsm_kernel<double, 16><<<(n - 16 + SWP_COLS - 1) / SWP_COLS, SWP_COLS>>>(A, ld, n, 0, 16, mv, perm);
+    cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+    printf("swap_trsm x20 avg %.2f us\n", ms * 1e3 / 20);
+    auto p = gemm_params<double>(n - 16, n - 16, 16, -1.0, A + 16 * ld, ld, A + 16, ld, 1.0, A + 16 * ld + 16, ld, A + 16 * ld + 16, ld);
+    cudaEventRecord(e0);
+    for (int r = 0; r < 20; ++r) gemm_launch<double>(p, 1, 0);
+    cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+    printf("trailing gemm K=16 x20 avg %.2f us\n", ms * 1e3 / 20);
+    auto q = gemm_params<double>(n, n, n, 1.0, A, ld, A, ld, 0.0, nullptr, ld, A + 0, ld);
+    double *C; cudaMalloc(&C, h.size() * 8); q.C = C;
+    cudaEventRecord(e0);
+    for (int r = 0; r < 10; ++r) gemm_launch<double>(q, 1, 0);
+    cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+    printf("gemm nnn x10 avg %.2f us = %.2f TF\n", ms * 1e3 / 10, 2.0 * n * n * (double)n / (ms / 10 * 1e-3) / 1e12);
+    // full getrf
+    LuStats *st; cudaMalloc(&st, sizeof(LuStats));
+    for (int r = 0; r < 2; ++r) {
+        cudaMemcpy(A, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+        cudaEventRecord(e0);
+        getrf<double>(n, A, ld, perm, mv, diag, st, 0);
+        cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+        printf("getrf n=%d: %.1f us (%lld launches so far)\n", n, ms * 1e3, launch_counter());
+    }
+    printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}
