@@ -20,60 +20,78 @@
 
 namespace frob {
 
+// Register-block geometry: N x N matrix, each thread owns a BR x BC block.
+template <int N, int BR = 4, int BC = 4>
+struct Geo {
+    static constexpr int RT = N / BR;          // thread rows (<= 32: one warp reduces a column)
+    static constexpr int CT = N / BC;          // thread columns
+    static constexpr int THREADS = RT * CT;
+    static constexpr int S = N + 4;            // padded smem row stride
+    static_assert(RT <= 32, "column candidates must fit one warp");
+};
 template <int N>
 struct BCfg {
-    static constexpr int TPR = N / 4;            // threads per row of 4x4 blocks
-    static constexpr int THREADS = TPR * TPR;
-    static constexpr int S = N + 4;              // padded smem row stride (doubles)
-    static constexpr int WARPS = THREADS / 32;
+    static constexpr int S = N + 4;
+    static constexpr int THREADS = Geo<N>::THREADS;
 };
+
+// static-index select from a small register array (avoids local-memory indexing)
+template <typename T, int K>
+FROB_DEV T sel_k(const T (&v)[K], int idx) {
+    T r = v[0];
+#pragma unroll
+    for (int i = 1; i < K; ++i)
+        if (idx == i) r = v[i];
+    return r;
+}
 
 // shared state of the sweep (double-buffered by step parity)
 template <typename T, int N>
 struct SweepShared {
     T colk[2][N];
     T rowp[2][N];
-    double candv[2][N / 4];
-    int candi[2][N / 4];
+    unsigned long long candk[2][32];
+    int candi[2][32];
     int pivrow[N];
     int pos[N];
     double pmag_k[N];
 };
 
-// Gauss-Jordan sweep on the register blocks a[4][4] (rows r0.., cols c0..) over the
-// leading n x n part of an N x N matrix (padding = identity).  On return the
-// inverse, scattered: A^{-1}[pos[i]][pivrow[j]] = a(i, j).  Returns pivot stats.
-template <typename T, int N>
-FROB_DEV void gj_sweep(T (&a)[4][4], int n, SweepShared<T, N> &sh, double &pmax, double &pmin) {
-    using C = BCfg<N>;
+// Gauss-Jordan sweep (exchange form, partial pivoting) on the register blocks a[BR][BC]
+// over the leading n x n part of an N x N matrix (padding = identity).  On return the
+// inverse, scattered: A^{-1}[pos[i]][pivrow[j]] = a(i, j).
+template <typename T, int N, int BR, int BC>
+FROB_DEV void gj_sweep(T (&a)[BR][BC], int n, SweepShared<T, N> &sh, double &pmax, double &pmin) {
+    using G = Geo<N, BR, BC>;
     const int tid = threadIdx.x, lane = tid & 31;
-    const int ti = tid / C::TPR, tj = tid % C::TPR;
-    const int r0 = ti * 4, c0 = tj * 4;
+    const int ti = tid / G::CT, tj = tid % G::CT;
+    const int r0 = ti * BR, c0 = tj * BC;
     unsigned long long used0 = 0, used1 = 0;  // rows already used as pivots (N <= 128)
     pmax = 0.0;
     pmin = INFINITY;
     for (int k = 0; k < n; ++k) {
         const int par = k & 1;
-        if (tj == (k >> 2)) {
-            const int cc = k & 3;
-            double bv = -1.0;
+        if (tj == k / BC) {
+            const int cc = k % BC;
+            unsigned long long bk = 0;
             int bi = INT_MAX;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < BR; ++q) {
                 const int r = r0 + q;
-                sh.colk[par][r] = a[q][cc];
+                const T v = sel_k<T, BC>(a[q], cc);
+                sh.colk[par][r] = v;
                 const bool u = (r < 64) ? ((used0 >> r) & 1ull) : ((used1 >> (r - 64)) & 1ull);
                 if (r < n && !u) {
-                    const double v = pkey(a[q][cc]);
-                    if (better(v, r, bv, bi)) { bv = v; bi = r; }
+                    const unsigned long long kk = pkey_bits(v);
+                    if (kk > bk) { bk = kk; bi = r; }
                 }
             }
-            sh.candv[par][ti] = bv;
+            sh.candk[par][ti] = bk;
             sh.candi[par][ti] = bi;
         }
         __syncthreads();
-        ArgMax m = warp_argmax(lane < C::TPR ? sh.candv[par][lane] : -1.0,
-                               lane < C::TPR ? sh.candi[par][lane] : INT_MAX);
+        const ArgMaxK m = warp_argmax_key(lane < G::RT ? sh.candk[par][lane] : 0ull,
+                                          lane < G::RT ? sh.candi[par][lane] : INT_MAX);
         const int p = m.i;
         const T piv = sh.colk[par][p];
         const double mag = pmag(piv);
@@ -82,65 +100,75 @@ FROB_DEV void gj_sweep(T (&a)[4][4], int n, SweepShared<T, N> &sh, double &pmax,
         const T ip = is_zero(piv) ? zero_of(T()) : recip(piv);
         if (p < 64) used0 |= 1ull << p; else used1 |= 1ull << (p - 64);
         if (tid == 0) { sh.pivrow[k] = p; sh.pmag_k[k] = mag; }
-        if (ti == (p >> 2)) {
-            const int q = p & 3;
+        if (ti == p / BR) {
+            const int q = p % BR;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) sh.rowp[par][c0 + c] = (c0 + c == k) ? ip : mul(a[q][c], ip);
+            for (int c = 0; c < BC; ++c) {
+                T v = a[0][c];
+#pragma unroll
+                for (int qq = 1; qq < BR; ++qq)
+                    if (q == qq) v = a[qq][c];
+                sh.rowp[par][c0 + c] = (c0 + c == k) ? ip : mul(v, ip);
+            }
         }
         __syncthreads();
-        T rp[4], ck[4];
+        T rp[BC], ck[BR];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) rp[c] = sh.rowp[par][c0 + c];
+        for (int c = 0; c < BC; ++c) rp[c] = sh.rowp[par][c0 + c];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) ck[q] = sh.colk[par][r0 + q];
+        for (int q = 0; q < BR; ++q) ck[q] = sh.colk[par][r0 + q];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < BR; ++q) {
             if (r0 + q == p) {
 #pragma unroll
-                for (int c = 0; c < 4; ++c) a[q][c] = rp[c];
+                for (int c = 0; c < BC; ++c) a[q][c] = rp[c];
             } else {
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
+                for (int c = 0; c < BC; ++c)
                     a[q][c] = (c0 + c == k) ? neg(mul(ck[q], rp[c])) : msub(a[q][c], ck[q], rp[c]);
             }
         }
     }
     __syncthreads();
-    for (int k = tid; k < N; k += C::THREADS) {
+    for (int k = tid; k < N; k += G::THREADS)
         if (k >= n) sh.pivrow[k] = k;
-    }
     __syncthreads();
-    for (int k = tid; k < N; k += C::THREADS) sh.pos[sh.pivrow[k]] = k;
+    for (int k = tid; k < N; k += G::THREADS) sh.pos[sh.pivrow[k]] = k;
     __syncthreads();
 }
 
-// write the sweep result as the inverse into smem buffer M (stride S)
-template <typename T, int N>
-FROB_DEV void sweep_store(const T (&a)[4][4], const SweepShared<T, N> &sh, T *M) {
-    using C = BCfg<N>;
+// write the sweep result as the inverse into a row-major matrix M (stride ldm)
+template <typename T, int N, int BR, int BC>
+FROB_DEV void sweep_store(const T (&a)[BR][BC], const SweepShared<T, N> &sh, T *M, int ldm) {
+    using G = Geo<N, BR, BC>;
     const int tid = threadIdx.x;
-    const int r0 = (tid / C::TPR) * 4, c0 = (tid % C::TPR) * 4;
+    const int r0 = (tid / G::CT) * BR, c0 = (tid % G::CT) * BC;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < BR; ++q) {
         const int orow = sh.pos[r0 + q];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) M[orow * C::S + sh.pivrow[c0 + c]] = a[q][c];
+        for (int c = 0; c < BC; ++c) M[orow * ldm + sh.pivrow[c0 + c]] = a[q][c];
     }
 }
 
-// load register blocks from smem matrix (stride S); rows/cols >= n get identity padding
+// load register blocks through an accessor f(i, j) (only called for i, j < n);
+// rows/cols >= n get identity padding
+template <typename T, int N, int BR, int BC, typename F>
+FROB_DEV void load_blocks_f(T (&a)[BR][BC], int n, F f) {
+    using G = Geo<N, BR, BC>;
+    const int tid = threadIdx.x;
+    const int r0 = (tid / G::CT) * BR, c0 = (tid % G::CT) * BC;
+#pragma unroll
+    for (int q = 0; q < BR; ++q)
+#pragma unroll
+        for (int c = 0; c < BC; ++c) {
+            const int i = r0 + q, j = c0 + c;
+            a[q][c] = (i < n && j < n) ? f(i, j) : ((i == j) ? one_of(T()) : zero_of(T()));
+        }
+}
 template <typename T, int N>
 FROB_DEV void load_blocks(T (&a)[4][4], const T *M, int n) {
-    using C = BCfg<N>;
-    const int tid = threadIdx.x;
-    const int r0 = (tid / C::TPR) * 4, c0 = (tid % C::TPR) * 4;
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const int i = r0 + q, j = c0 + c;
-            a[q][c] = (i < n && j < n) ? M[i * C::S + j] : ((i == j) ? one_of(T()) : zero_of(T()));
-        }
+    load_blocks_f<T, N, 4, 4>(a, n, [&](int i, int j) { return M[i * BCfg<N>::S + j]; });
 }
 
 // first 1-based pivot column with |u_kk| < 100 n u max (reading R2), 0 if none
@@ -157,6 +185,33 @@ FROB_DEV int sweep_info(const SweepShared<T, N> &sh, int n, double pmax) {
 template <int N> struct WT;
 template <> struct WT<32> { static constexpr int WGM = 2, WGN = 1, MT = 2, NT = 4; };
 template <> struct WT<64> { static constexpr int WGM = 2, WGN = 4, MT = 4, NT = 2; };
+template <> struct WT<128> { static constexpr int WGM = 2, WGN = 8, MT = 4, NT = 2; };  // per 64-row half
+
+// acc = op_A * op_B over an N x N x N product with operands given by accessors
+// fa(row, k) and fb(k, col) (shared or global memory; DMMA fragments loaded directly).
+template <int N, typename FA, typename FB>
+FROB_DEV void cta_mma_f(FA fa, FB fb, double (&acc)[WT<N>::MT][WT<N>::NT][2], int row_off = 0) {
+    using W = WT<N>;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm0 = row_off + (warp / W::WGN) * (W::MT * 8), wn0 = (warp % W::WGN) * (W::NT * 8);
+#pragma unroll
+    for (int i = 0; i < W::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < W::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 2
+    for (int kk = 0; kk < N; kk += 4) {
+        double a[W::MT], b[W::NT];
+#pragma unroll
+        for (int i = 0; i < W::MT; ++i) a[i] = fa(wm0 + i * 8 + g, kk + t);
+#pragma unroll
+        for (int j = 0; j < W::NT; ++j) b[j] = fb(kk + t, wn0 + j * 8 + g);
+#pragma unroll
+        for (int i = 0; i < W::MT; ++i)
+#pragma unroll
+            for (int j = 0; j < W::NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+}
 
 template <int N>
 FROB_DEV void cta_mma(const double *Xs, const double *Ys, int kmax, double (&acc)[WT<N>::MT][WT<N>::NT][2]) {
@@ -183,11 +238,11 @@ FROB_DEV void cta_mma(const double *Xs, const double *Ys, int kmax, double (&acc
 }
 
 template <int N, typename F>
-FROB_DEV void cta_mma_foreach(const double (&acc)[WT<N>::MT][WT<N>::NT][2], F f) {
+FROB_DEV void cta_mma_foreach(const double (&acc)[WT<N>::MT][WT<N>::NT][2], F f, int row_off = 0) {
     using W = WT<N>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const int wm0 = (warp / W::WGN) * (W::MT * 8), wn0 = (warp % W::WGN) * (W::NT * 8);
+    const int wm0 = row_off + (warp / W::WGN) * (W::MT * 8), wn0 = (warp % W::WGN) * (W::NT * 8);
 #pragma unroll
     for (int i = 0; i < W::MT; ++i)
 #pragma unroll
@@ -230,9 +285,9 @@ frob_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__rest
     double pmax, pmin;
     int use = (branch == FROB_BRANCH_B) ? 2 : 1;
     load_blocks<double, N>(a, use == 1 ? As : Bs, n);
-    gj_sweep<double, N>(a, n, sm.sw, pmax, pmin);
+    gj_sweep<double, N, 4, 4>(a, n, sm.sw, pmax, pmin);
     int inf_x = sweep_info<double, N>(sm.sw, n, pmax);
-    sweep_store<double, N>(a, sm.sw, Ws);
+    sweep_store<double, N, 4, 4>(a, sm.sw, Ws, C::S);
     if (branch == FROB_BRANCH_AUTO) {
         const double rho_a = (pmin > 0.0) ? pmax / pmin : INFINITY;
         if (inf_x != 0 || !(rho_a <= 256.0)) {
@@ -240,14 +295,14 @@ frob_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__rest
             __syncthreads();
             load_blocks<double, N>(a, Bs, n);
             double qmax, qmin;
-            gj_sweep<double, N>(a, n, sm.sw, qmax, qmin);
+            gj_sweep<double, N, 4, 4>(a, n, sm.sw, qmax, qmin);
             const int inf_b = sweep_info<double, N>(sm.sw, n, qmax);
             const double rho_b = (qmin > 0.0) ? qmax / qmin : INFINITY;
             if (inf_b == 0 && (inf_x != 0 || rho_b < rho_a)) {
                 use = 2;
                 inf_x = 0;
                 __syncthreads();
-                sweep_store<double, N>(a, sm.sw, Ws);
+                sweep_store<double, N, 4, 4>(a, sm.sw, Ws, C::S);
             } else if (inf_b != 0 && inf_x != 0) {
                 inf_x = -1;  // both singular
             }
@@ -273,9 +328,9 @@ frob_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__rest
     __syncthreads();
     // a5: Re = M^{-1} -> Ys
     load_blocks<double, N>(a, Xs, n);
-    gj_sweep<double, N>(a, n, sm.sw, pmax, pmin);
+    gj_sweep<double, N, 4, 4>(a, n, sm.sw, pmax, pmin);
     const int inf_m = sweep_info<double, N>(sm.sw, n, pmax);
-    sweep_store<double, N>(a, sm.sw, Ys);
+    sweep_store<double, N, 4, 4>(a, sm.sw, Ys, C::S);
     __syncthreads();
     // a6/a7: Im = -C Re, interleaved store
     cta_mma<N>(Ws, Ys, N, acc);
@@ -285,6 +340,103 @@ frob_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__rest
             Xb[i * n + j] = (use == 1) ? make_double2(re, -v) : make_double2(-v, -re);
         }
     });
+    if (tid == 0) {
+        info[b] = (inf_x < 0) ? 1 : (inf_x ? inf_x : inf_m);
+        if (bused) bused[b] = (inf_x < 0) ? 0 : (unsigned char)use;
+    }
+}
+
+// ----------------------------------------------------------------- Frobenius, 64 < n <= 128
+// 512 threads, 4x8 register blocks for the sweeps; one 135 KB shared buffer (X^{-1}, then
+// M, then Re); C = X^{-1} Y lives in the first half of the OUTPUT matrix (planar n x n
+// doubles) until the final epilogue overwrites it with the interleaved result.
+struct Frob128Smem {
+    double S[128 * 132];
+    SweepShared<double, 128> sw;
+};
+
+__global__ void __launch_bounds__(512)
+frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__restrict__ X, long long sX, int n,
+                       int branch, int *__restrict__ info, unsigned char *__restrict__ bused) {
+    constexpr int N = 128, SS = 132;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Frob128Smem &sm = *reinterpret_cast<Frob128Smem *>(smem_raw);
+    double *S = sm.S;
+    const int tid = threadIdx.x;
+    const long long b = blockIdx.x;
+    const double2 *Zb = Z + b * sZ;
+    double2 *Xb = X + b * sX;
+    // scratch: planar C (n x n) in the SECOND half of the output matrix, so the final
+    // epilogue for rows < 64 (bytes [0, 1024 n)) never clobbers C rows >= 64 (n >= 64)
+    double *Cg = reinterpret_cast<double *>(Xb) + (long long)n * n;
+
+    double a[4][8];
+    double pmax, pmin;
+    int use = (branch == FROB_BRANCH_B) ? 2 : 1;
+    if (use == 1) load_blocks_f<double, N, 4, 8>(a, n, [&](int i, int j) { return Zb[i * n + j].x; });
+    else load_blocks_f<double, N, 4, 8>(a, n, [&](int i, int j) { return Zb[i * n + j].y; });
+    gj_sweep<double, N, 4, 8>(a, n, sm.sw, pmax, pmin);
+    int inf_x = sweep_info<double, N>(sm.sw, n, pmax);
+    sweep_store<double, N, 4, 8>(a, sm.sw, S, SS);
+    if (branch == FROB_BRANCH_AUTO) {
+        const double rho_a = (pmin > 0.0) ? pmax / pmin : INFINITY;
+        if (inf_x != 0 || !(rho_a <= 256.0)) {
+            __syncthreads();
+            load_blocks_f<double, N, 4, 8>(a, n, [&](int i, int j) { return Zb[i * n + j].y; });
+            double qmax, qmin;
+            gj_sweep<double, N, 4, 8>(a, n, sm.sw, qmax, qmin);
+            const int inf_b = sweep_info<double, N>(sm.sw, n, qmax);
+            const double rho_b = (qmin > 0.0) ? qmax / qmin : INFINITY;
+            if (inf_b == 0 && (inf_x != 0 || rho_b < rho_a)) {
+                use = 2;
+                inf_x = 0;
+                __syncthreads();
+                sweep_store<double, N, 4, 8>(a, sm.sw, S, SS);
+            } else if (inf_b != 0 && inf_x != 0) {
+                inf_x = -1;
+            }
+        }
+    }
+    __syncthreads();
+    const double sgn = (use == 1) ? 1.0 : -1.0;
+    const bool ya = (use == 2);  // Y = A (imag part otherwise)
+    auto Yv = [&](int i, int j) { return (i < n && j < n) ? sgn * (ya ? Zb[i * n + j].x : Zb[i * n + j].y) : 0.0; };
+    auto Xv = [&](int i, int j) { return ya ? Zb[i * n + j].y : Zb[i * n + j].x; };
+    double acc[WT<N>::MT][WT<N>::NT][2];
+    // a3: C = X^{-1} (sgn Y) -> Cg   (two 64-row halves to bound register use)
+    for (int h = 0; h < 2; ++h) {
+        cta_mma_f<N>([&](int r, int k) { return S[r * SS + k]; }, Yv, acc, 64 * h);
+        cta_mma_foreach<N>(acc, [&](int i, int j, double v) {
+            if (i < n && j < n) Cg[i * n + j] = v;
+        }, 64 * h);
+    }
+    __syncthreads();
+    // a4: M = X + (sgn Y) C -> S
+    for (int h = 0; h < 2; ++h) {
+        cta_mma_f<N>(Yv, [&](int k, int c) { return (k < n && c < n) ? Cg[k * n + c] : 0.0; }, acc, 64 * h);
+        cta_mma_foreach<N>(acc, [&](int i, int j, double v) { S[i * SS + j] = (i < n && j < n) ? Xv(i, j) + v : 0.0; },
+                           64 * h);
+    }
+    __syncthreads();
+    // a5: Re = M^{-1} -> S
+    load_blocks_f<double, N, 4, 8>(a, n, [&](int i, int j) { return S[i * SS + j]; });
+    gj_sweep<double, N, 4, 8>(a, n, sm.sw, pmax, pmin);
+    const int inf_m = sweep_info<double, N>(sm.sw, n, pmax);
+    sweep_store<double, N, 4, 8>(a, sm.sw, S, SS);
+    __syncthreads();
+    // a6/a7: Im = -C Re, interleaved store (after every warp has finished reading Cg)
+    auto out = [&](int i, int j, double v) {
+        if (i < n && j < n) {
+            const double re = S[i * SS + j];
+            Xb[i * n + j] = (use == 1) ? make_double2(re, -v) : make_double2(-v, -re);
+        }
+    };
+    for (int h = 0; h < 2; ++h) {
+        cta_mma_f<N>([&](int r, int k) { return (r < n && k < n) ? Cg[r * n + k] : 0.0; },
+                     [&](int k, int c) { return S[k * SS + c]; }, acc, 64 * h);
+        __syncthreads();  // every warp has read the C rows of this half
+        cta_mma_foreach<N>(acc, out, 64 * h);
+    }
     if (tid == 0) {
         info[b] = (inf_x < 0) ? 1 : (inf_x ? inf_x : inf_m);
         if (bused) bused[b] = (inf_x < 0) ? 0 : (unsigned char)use;
@@ -319,9 +471,9 @@ zinv_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__rest
     double2 a[4][4];
     double pmax, pmin;
     load_blocks<double2, N>(a, sm.buf, n);
-    gj_sweep<double2, N>(a, n, sm.sw, pmax, pmin);
+    gj_sweep<double2, N, 4, 4>(a, n, sm.sw, pmax, pmin);
     const int inf = sweep_info<double2, N>(sm.sw, n, pmax);
-    sweep_store<double2, N>(a, sm.sw, sm.buf);
+    sweep_store<double2, N, 4, 4>(a, sm.sw, sm.buf, C::S);
     __syncthreads();
     for (int idx = tid; idx < n * n; idx += C::THREADS) {
         const int i = idx / n, j = idx - i * n;
@@ -348,7 +500,7 @@ frob_status frob_inv_batched(int n, int batch, const double *Z, long long stride
                              long long strideX, int branch, int *d_info, unsigned char *d_branch_used,
                              void *ws, size_t ws_bytes, void *stream) {
     (void)ws; (void)ws_bytes;
-    if (n < 1 || n > 64 || batch < 0 || !d_info || strideZ < (long long)n * n || strideX < (long long)n * n ||
+    if (n < 1 || n > 128 || batch < 0 || !d_info || strideZ < (long long)n * n || strideX < (long long)n * n ||
         branch < 0 || branch > 2)
         return FROB_ERR_INVALID_ARG;
     if (batch == 0) return FROB_OK;
@@ -363,12 +515,18 @@ frob_status frob_inv_batched(int n, int batch, const double *Z, long long stride
         count_launch();
         frob_batched_kernel<32><<<batch, BCfg<32>::THREADS, smem, s>>>(Zc, strideZ, Xc, strideX, n, branch,
                                                                        d_info, d_branch_used);
-    } else {
+    } else if (n <= 64) {
         const size_t smem = sizeof(FrobSmem<64>);
         if ((e = set_smem(frob_batched_kernel<64>, smem)) != cudaSuccess) return FROB_ERR_CUDA;
         count_launch();
         frob_batched_kernel<64><<<batch, BCfg<64>::THREADS, smem, s>>>(Zc, strideZ, Xc, strideX, n, branch,
                                                                        d_info, d_branch_used);
+    } else {
+        const size_t smem = sizeof(Frob128Smem);
+        if ((e = set_smem(frob_batched128_kernel, smem)) != cudaSuccess) return FROB_ERR_CUDA;
+        count_launch();
+        frob_batched128_kernel<<<batch, 512, smem, s>>>(Zc, strideZ, Xc, strideX, n, branch, d_info,
+                                                         d_branch_used);
     }
     return cudaGetLastError() == cudaSuccess ? FROB_OK : FROB_ERR_CUDA;
 }

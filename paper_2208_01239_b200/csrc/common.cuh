@@ -101,6 +101,32 @@ FROB_DEV unsigned redux_min(unsigned v) {
     asm volatile("redux.sync.min.u32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
     return r;
 }
+// Integer pivot keys: 1 + the IEEE bit pattern of |v| (monotone in |v|; NaN patterns sort
+// above +inf, i.e. NaN counts as the largest magnitude), 0 = no candidate.  Real only;
+// complex keys (|re|+|im|) go through the double path.
+FROB_DEV unsigned long long pkey_bits(double v) {
+    return ((unsigned long long)__double_as_longlong(v) & 0x7fffffffffffffffull) + 1ull;
+}
+FROB_DEV unsigned long long pkey_bits(double2 v) {
+    const double m = fabs(v.x) + fabs(v.y);
+    return (m != m) ? 0x7ff8000000000001ull : (unsigned long long)__double_as_longlong(m) + 1ull;
+}
+struct ArgMaxK {
+    unsigned long long k;
+    int i;
+};
+// first max over (key, -idx) within the warp, 3 x REDUX
+FROB_DEV ArgMaxK warp_argmax_key(unsigned long long kb, int idx) {
+    const unsigned hi = (unsigned)(kb >> 32), lo = (unsigned)kb;
+    const unsigned mh = redux_max(hi);
+    const unsigned ml = redux_max(hi == mh ? lo : 0u);
+    const bool cand = (hi == mh) && (lo == ml);
+    const unsigned mi = redux_min(cand ? (unsigned)idx : 0xffffffffu);
+    ArgMaxK r;
+    r.k = ((unsigned long long)mh << 32) | ml;
+    r.i = (r.k == 0ull) ? INT_MAX : (int)mi;
+    return r;
+}
 // key must be >= 0 (or -1.0 for "no candidate", mapped below every real key)
 FROB_DEV ArgMax warp_argmax_redux(double key, int idx) {
     const unsigned long long kb = (key < 0.0) ? 0ull : (unsigned long long)__double_as_longlong(key) + 1ull;

@@ -125,14 +125,14 @@ lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, 
     static_assert(PW % PANEL_UNROLL == 0, "PW must be a multiple of the unroll");
     extern __shared__ __align__(16) double stg[];  // R * PANEL_T rows x STG_STRIDE doubles
     __shared__ int sdst[R * PANEL_T];
-    __shared__ double wv[2][PANEL_W];
+    __shared__ unsigned long long wv[2][PANEL_W];
     __shared__ int wi[2][PANEL_W];
     __shared__ __align__(16) T wrow[2][PANEL_W][PW];  // each warp's candidate row (zero-padded)
     __shared__ T wip[2][PANEL_W];                     // and the reciprocal of its pivot value
     __shared__ __align__(16) T upiv[PANEL_W][PW];     // warp-private copy (cluster path)
     __shared__ T upiv_ip[PANEL_W];
     __shared__ T pubip[2];
-    __shared__ double pubv[2];
+    __shared__ unsigned long long pubv[2];
     __shared__ int pubi[2];
     __shared__ __align__(16) T pubrow[2][PW];
     __shared__ int pivrows[PW];
@@ -202,35 +202,33 @@ lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, 
     // finish(j, S): barrier, block argmax (+ cluster argmax), pivot row, then the update
     // of the NEXT column's slot first, publish(j+1), and only then the other slots.
     int qb_next = 0;
-    double bv_next = -1.0;
+    unsigned long long bv_next = 0;
     int bi_next = INT_MAX;
+    T myip = zero_of(T());
     auto local_cand = [&](auto Sc) {
         constexpr int S = decltype(Sc)::value % PW;
-        bv_next = -1.0;
+        bv_next = 0;
         bi_next = INT_MAX;
         qb_next = 0;
+        T myp = zero_of(T());
 #pragma unroll
         for (int q = 0; q < R; ++q)
             if (!((done >> q) & 1u)) {
-                const double v = pkey(a[q][S]);
-                if (better(v, grow[q], bv_next, bi_next)) { bv_next = v; bi_next = grow[q]; qb_next = q; }
+                const unsigned long long k = pkey_bits(a[q][S]);
+                if (k > bv_next) { bv_next = k; bi_next = grow[q]; qb_next = q; myp = a[q][S]; }
             }
+        // speculative reciprocal of this lane's candidate (used if it wins)
+        myip = is_zero(myp) ? zero_of(T()) : recip(myp);
     };
     auto publish = [&](const int j, auto Sc) {
         // Sc may be PANEL_UNROLL (first column after the next rotation): the row is then
         // stored already rotated so that it matches the frame the consumer will use.
         constexpr int V = decltype(Sc)::value;
-        constexpr int S = V % PW;
         constexpr int K = (V >= PANEL_UNROLL) ? PANEL_UNROLL : 0;
         constexpr int SN = V - K;  // slot of column j after the rotation
         const int par = j & 1;
-        T myp = zero_of(T());
-#pragma unroll
-        for (int q = 0; q < R; ++q)
-            if (q == qb_next) myp = a[q][S];
-        const T myip = is_zero(myp) ? zero_of(T()) : recip(myp);  // speculative
-        const ArgMax wa = warp_argmax_redux(bv_next, bi_next);
-        if (lane == 0) { wv[par][warp] = wa.v; wi[par][warp] = wa.i; }
+        const ArgMaxK wa = warp_argmax_key(bv_next, bi_next);
+        if (lane == 0) { wv[par][warp] = wa.k; wi[par][warp] = wa.i; }
         if (bi_next == wa.i && bi_next != INT_MAX) {
 #pragma unroll
             for (int q = 0; q < R; ++q)
@@ -248,9 +246,12 @@ lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, 
         constexpr int S = decltype(Sc)::value % PW;
         constexpr int S1 = (decltype(Sc)::value + 1) % PW;
         const int par = j & 1;
+        PTRACEJ(j, 50);
         __syncthreads();
-        const ArgMax ca = warp_argmax_redux(lane < PANEL_W ? wv[par][lane] : -1.0,
-                                            lane < PANEL_W ? wi[par][lane] : INT_MAX);
+        PTRACEJ(j, 51);
+        const ArgMaxK ca = warp_argmax_key(lane < PANEL_W ? wv[par][lane] : 0ull,
+                                           lane < PANEL_W ? wi[par][lane] : INT_MAX);
+        PTRACEJ(j, 52);
         const int cw = (ca.i == INT_MAX) ? 0 : ((ca.i - rbeg) % PANEL_T) >> 5;  // warp holding the CTA winner
         int gp;
         T u[PW];
@@ -262,17 +263,17 @@ lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, 
         } else {
             cg::cluster_group cl = cg::this_cluster();
             if (warp == 0) {
-                if (lane == 0) { pubv[par] = ca.v; pubi[par] = ca.i; pubip[par] = wip[par][cw]; }
+                if (lane == 0) { pubv[par] = ca.k; pubi[par] = ca.i; pubip[par] = wip[par][cw]; }
                 if (lane < PW) pubrow[par][lane] = wrow[par][cw][lane];
             }
             cl.sync();
-            double qv = -1.0;
+            unsigned long long qv = 0;
             int qi = INT_MAX;
             if (lane < CS) {
                 qv = *cl.map_shared_rank(&pubv[par], lane);
                 qi = *cl.map_shared_rank(&pubi[par], lane);
             }
-            const ArgMax ga = warp_argmax_redux(qv, qi);
+            const ArgMaxK ga = warp_argmax_key(qv, qi);
             gp = ga.i;
             const int owner = gp / RPC;
             if (lane < PW) upiv[warp][lane] = *cl.map_shared_rank(&pubrow[par][lane], owner);
@@ -284,6 +285,7 @@ lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, 
         }
         const T piv = u[S];
         const bool zp = is_zero(piv);
+        PTRACEJ(j, 53);
         if (tid == 0) { pivrows[j] = gp; pvals[j] = piv; }
         T l[R];
         bool act[R];
@@ -298,6 +300,7 @@ lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, 
         if (j + 1 < w) {
             local_cand(std::integral_constant<int, decltype(Sc)::value + 1>{});
         }
+        PTRACEJ(j, 54);
 #pragma unroll
         for (int q = 0; q < R; ++q) {
             if (act[q]) {
@@ -307,6 +310,7 @@ lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, 
             }
             a[q][S] = l[q];
         }
+        PTRACEJ(j, 55);
         if (j + 1 < w) publish(j + 1, std::integral_constant<int, decltype(Sc)::value + 1>{});
         PTRACE(2 + j);
     };

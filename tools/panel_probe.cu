@@ -3,6 +3,7 @@
 #include "../paper_2208_01239_b200/csrc/lu.cu"
 #include <vector>
 #include <random>
+#include <algorithm>
 using namespace frob;
 unsigned long long &frob::launch_counter() { static unsigned long long c = 0; return c; }
 
@@ -36,8 +37,26 @@ int main(int argc, char **argv) {
         printf("panel m=%d: %.2f us | load %lld | cols:", n, ms * 1e3, tr[1] - tr[0]);
         for (int j = 0; j < 16; ++j) printf(" %lld", tr[2 + j] - (j ? tr[1 + j] : tr[1]));
         printf(" | tail %lld | store %lld\n", tr[40] - tr[17], tr[41] - tr[40]);
-        printf("   col5: wargmax %lld, lane0 store %lld, bar %lld, bargmax %lld, owner+bar2+load %lld, recip %lld, update %lld\n",
-               tr[51] - tr[50], tr[52] - tr[51], tr[53] - tr[52], tr[54] - tr[53], tr[55] - tr[54], tr[56] - tr[55], tr[7] - tr[56]);
+        printf("   col5: pre-bar %lld, bar %lld, bargmax %lld, u-load %lld, next-slot+cand %lld, rest-update %lld, publish %lld\n", tr[50] - tr[6], tr[51] - tr[50], tr[52] - tr[51], tr[53] - tr[52], tr[54] - tr[53], tr[55] - tr[54], tr[7] - tr[55]);
+    }
+    // 1b) cluster variants for the same panel
+    {
+        auto tp = [&](const char *nm, auto fn) {
+            float ms2;
+            for (int r = 0; r < 3; ++r) fn();
+            cudaEventRecord(e0);
+            for (int r = 0; r < 20; ++r) fn();
+            cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms2, e0, e1);
+            printf("  %-28s %.2f us  (%s)\n", nm, ms2 * 1e3 / 20, cudaGetErrorString(cudaGetLastError()));
+        };
+        if (n <= 1024) tp("R4 CS1", [&] { launch_panel_r<double, 16, 4>(A, ld, n, 16, 0, mv, diag, 1, 0); });
+        if (n <= 1024) tp("R2 CS2", [&] { launch_panel_r<double, 16, 2>(A, ld, n, 16, 0, mv, diag, 2, 0); });
+        if (n <= 1024) tp("R1 CS4", [&] { launch_panel_r<double, 16, 1>(A, ld, n, 16, 0, mv, diag, 4, 0); });
+        if (n <= 512) tp("R1 CS2", [&] { launch_panel_r<double, 16, 1>(A, ld, n, 16, 0, mv, diag, 2, 0); });
+        if (n <= 2048) tp("R1 CS8", [&] { launch_panel_r<double, 16, 1>(A, ld, n, 16, 0, mv, diag, (n + 255) / 256, 0); });
+        if (n > 1024) tp("R4 CSn", [&] { launch_panel_r<double, 16, 4>(A, ld, n, 16, 0, mv, diag, (n + 1023) / 1024, 0); });
+        if (n > 1024 && n <= 8192) tp("R2 CSn", [&] { launch_panel_r<double, 16, 2>(A, ld, n, 16, 0, mv, diag, (n + 511) / 512, 0); });
+        if (n > 1024 && n <= 4096) tp("R1 CSn", [&] { launch_panel_r<double, 16, 1>(A, ld, n, 16, 0, mv, diag, (n + 255) / 256, 0); });
     }
     // 2) kernel-only timings of the LU pieces
     cudaMemcpy(A, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
@@ -70,6 +89,40 @@ int main(int argc, char **argv) {
         getrf<double>(n, A, ld, perm, mv, diag, st, 0);
         cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
         printf("getrf n=%d: %.1f us (%lld launches so far)\n", n, ms * 1e3, launch_counter());
+    }
+    {
+        double *U, *L, *O;
+        cudaMalloc(&U, h.size() * 8); cudaMalloc(&L, h.size() * 8); cudaMalloc(&O, h.size() * 8);
+        for (int r = 0; r < 3; ++r) {
+            getrf<double>(n, A, ld, perm, mv, diag, st, 0);
+            cudaEventRecord(e0);
+            inv_from_lu<double>(n, A, ld, U, L, O, ld, perm, 0);
+            cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+            printf("inv_from_lu n=%d: %.1f us\n", n, ms * 1e3);
+        }
+        // pieces
+        long long total = (long long)n * n;
+        cudaEventRecord(e0);
+        extract_ul_kernel<double><<<(int)std::min<long long>((total + 255) / 256, 148LL * 16), 256>>>(A, ld, n, U, L);
+        cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+        printf("  extract %.1f us\n", ms * 1e3);
+        cudaEventRecord(e0);
+        tri_leaf_kernel<double><<<dim3((n + TRI_LEAF - 1) / TRI_LEAF, 2), TRI_LEAF>>>(U, L, ld, n);
+        cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+        printf("  leaf %.1f us\n", ms * 1e3);
+        for (int sz = TRI_LEAF; sz < n; sz *= 2) {
+            const int full = n / (2 * sz);
+            cudaEventRecord(e0);
+            tri_level<double>(U, L, A, ld, sz, 0, sz, full, 0);
+            cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+            printf("  level s=%d (x%d) %.1f us\n", sz, full, ms * 1e3);
+        }
+        auto pp = gemm_params<double>(n, n, n, 1.0, U, ld, L, ld, 0.0, nullptr, ld, O, ld);
+        pp.triA = TRI_UPPER; pp.triB = TRI_LOWER; pp.colperm = perm;
+        cudaEventRecord(e0);
+        gemm_launch<double>(pp, 1, 0);
+        cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+        printf("  product %.1f us\n", ms * 1e3);
     }
     printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
