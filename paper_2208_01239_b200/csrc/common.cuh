@@ -59,6 +59,18 @@ FROB_DEV double2 recip(double2 a) {
     double d = s * (xs * xs + ys * ys);
     return make_double2(xs / d, -ys / d);
 }
+// Branch-free reciprocal for the LU critical path: MUFU approximation + two Newton steps
+// (error ~1 ulp; not correctly rounded, like LAPACK's multiply-by-reciprocal scaling).
+// Inputs with |x| > 2^1021 flush to 0 (ftz); pivots that large do not occur here.
+FROB_DEV double frcp(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+FROB_DEV double frcp(double2 x) { return 0.0; }  // unused overload guard
 FROB_DEV double scal(double a, double s) { return a * s; }
 FROB_DEV double2 scal(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
 FROB_DEV bool finite_of(double v) { return isfinite(v); }
@@ -150,6 +162,30 @@ FROB_DEV void dmma(double &c0, double &c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1)
                  : "d"(a), "d"(b));
+}
+
+// ------------------------------------------------------------------ programmatic dependent launch
+// Kernels of the LU chain are launched with programmatic stream serialization: each one
+// lets its successor launch immediately and waits for its predecessor's results before
+// touching memory (both are no-ops without the launch attribute).
+FROB_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+FROB_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    count_launch();
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
 // ------------------------------------------------------------------ cp.async

@@ -85,7 +85,7 @@ static int ew_blocks(long long total) {
 // ---------------------------------------------------------------------- workspace
 struct FrobWs {
     double *A, *B, *W1, *W2, *W3, *W4, *W5;
-    double *diag;
+    double *diag, *work;
     int *perm_x, *perm_b, *perm_m, *mv;
     LuStats *stats;   // [0] A, [1] B, [2] M
     int *flags;       // [0] nonfinite
@@ -104,10 +104,11 @@ static FrobWs carve_frob(void *ws, int n) {
     w.W4 = c.take<double>((size_t)n * ld);
     w.W5 = c.take<double>((size_t)n * ld);
     w.diag = c.take<double>((size_t)n);
+    w.work = c.take<double>(getrf_work_elems<double>(n));
     w.perm_x = c.take<int>((size_t)n);
     w.perm_b = c.take<int>((size_t)n);
     w.perm_m = c.take<int>((size_t)n);
-    w.mv = c.take<int>(MV_INTS);
+    w.mv = c.take<int>(lu_mv_ints(n));
     w.stats = c.take<LuStats>(3);
     w.flags = c.take<int>(4);
     w.bytes = c.off;
@@ -115,7 +116,7 @@ static FrobWs carve_frob(void *ws, int n) {
 }
 
 struct ZluWs {
-    double2 *W, *U, *L, *diag;
+    double2 *W, *U, *L, *diag, *work;
     int *perm, *mv;
     LuStats *stats;
     int *flags;
@@ -130,8 +131,9 @@ static ZluWs carve_zlu(void *ws, int n) {
     w.U = c.take<double2>((size_t)n * ld);
     w.L = c.take<double2>((size_t)n * ld);
     w.diag = c.take<double2>((size_t)n);
+    w.work = c.take<double2>(getrf_work_elems<double2>(n));
     w.perm = c.take<int>((size_t)n);
-    w.mv = c.take<int>(MV_INTS);
+    w.mv = c.take<int>(lu_mv_ints(n));
     w.stats = c.take<LuStats>(1);
     w.flags = c.take<int>(4);
     w.bytes = c.off;
@@ -167,7 +169,7 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
     int use = (branch == FROB_BRANCH_B) ? 2 : 1;
     int *perm = w.perm_x;
     double *Xlu = w.W1;
-    FROB_CUDA(getrf<double>(n, Xlu, ld, perm, w.mv, w.diag, &w.stats[use == 1 ? 0 : 1], s));
+    FROB_CUDA(getrf<double>(n, Xlu, ld, perm, w.mv, w.diag, &w.stats[use == 1 ? 0 : 1], w.work, s));
 
     LuStats hs[3];
     for (auto &h : hs) { h.rho = NAN; h.umax = 0; h.info = 0; h.nonfinite = 0; }
@@ -185,7 +187,7 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
             count_launch();
             copy2d_kernel<double><<<ew_blocks((long long)n * n), 256, 0, s>>>(w.B, ld, w.W5, ld, n, nullptr);
             FROB_CUDA(cudaGetLastError());
-            FROB_CUDA(getrf<double>(n, w.W5, ld, w.perm_b, w.mv, w.diag, &w.stats[1], s));
+            FROB_CUDA(getrf<double>(n, w.W5, ld, w.perm_b, w.mv, w.diag, &w.stats[1], w.work, s));
             FROB_CUDA(cudaMemcpyAsync(&hs[1], &w.stats[1], sizeof(LuStats), cudaMemcpyDeviceToHost, s));
             FROB_CUDA(cudaStreamSynchronize(s));
             const bool sa = hs[0].info != 0, sb = hs[1].info != 0;
@@ -221,7 +223,7 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
         FROB_CUDA(gemm_launch<double>(p, 1, s));
     }
     // a5: Re' = M^{-1} (un-permuted)
-    FROB_CUDA(getrf<double>(n, w.W3, ld, w.perm_m, w.mv, w.diag, &w.stats[2], s));
+    FROB_CUDA(getrf<double>(n, w.W3, ld, w.perm_m, w.mv, w.diag, &w.stats[2], w.work, s));
     double *Re = (use == 1) ? w.A : w.B;  // X buffer is free now
     FROB_CUDA(inv_from_lu<double>(n, w.W3, ld, w.W1, w.W4, Re, ld, nullptr, s));
     // a6/a7: Im' = -C Re', fused with the column interchanges and the interleaved store
@@ -262,7 +264,7 @@ static frob_status zinv_lu_impl(int n, const double *Z, long long ldz, double *X
     copy2d_kernel<double2><<<ew_blocks((long long)n * n), 256, 0, s>>>(
         reinterpret_cast<const double2 *>(Z), ldz, w.W, ld, n, w.flags);
     FROB_CUDA(cudaGetLastError());
-    FROB_CUDA(getrf<double2>(n, w.W, ld, w.perm, w.mv, w.diag, w.stats, s));
+    FROB_CUDA(getrf<double2>(n, w.W, ld, w.perm, w.mv, w.diag, w.stats, w.work, s));
     FROB_CUDA(inv_from_lu<double2>(n, w.W, ld, w.U, w.L, reinterpret_cast<double2 *>(X), ldx, w.perm, s));
     if (host_info) {
         LuStats hs;
@@ -279,7 +281,7 @@ static frob_status zinv_lu_impl(int n, const double *Z, long long ldz, double *X
 
 // ---------------------------------------------------------------------- real inverse
 struct DinvWs {
-    double *W, *U, *L, *diag;
+    double *W, *U, *L, *diag, *work;
     int *perm, *mv;
     LuStats *stats;
     size_t bytes;
@@ -292,8 +294,9 @@ static DinvWs carve_dinv(void *ws, int n) {
     w.U = c.take<double>((size_t)n * ld);
     w.L = c.take<double>((size_t)n * ld);
     w.diag = c.take<double>((size_t)n);
+    w.work = c.take<double>(getrf_work_elems<double>(n));
     w.perm = c.take<int>((size_t)n);
-    w.mv = c.take<int>(MV_INTS);
+    w.mv = c.take<int>(lu_mv_ints(n));
     w.stats = c.take<LuStats>(1);
     w.bytes = c.off;
     return w;
@@ -548,7 +551,7 @@ frob_status frob_dinv(int n, const double *A, long long lda, double *Ainv, long 
     count_launch();
     copy2d_kernel<double><<<ew_blocks((long long)n * n), 256, 0, s>>>(A, lda, w.W, ld, n, nullptr);
     FROB_CUDA(cudaGetLastError());
-    FROB_CUDA(getrf<double>(n, w.W, ld, w.perm, w.mv, w.diag, w.stats, s));
+    FROB_CUDA(getrf<double>(n, w.W, ld, w.perm, w.mv, w.diag, w.stats, w.work, s));
     FROB_CUDA(inv_from_lu<double>(n, w.W, ld, w.U, w.L, Ainv, ldainv, w.perm, s));
     if (host_info) {
         LuStats hs;
@@ -568,7 +571,8 @@ size_t frob_dgetrf_workspace_bytes(int n) {
     if (n < 1) return 0;
     Carve c{nullptr, 0, 0};
     c.take<double>((size_t)n);
-    c.take<int>(MV_INTS);
+    c.take<double>(getrf_work_elems<double>(n));
+    c.take<int>(lu_mv_ints(n));
     c.take<LuStats>(1);
     return c.off;
 }
@@ -579,10 +583,11 @@ frob_status frob_dgetrf(int n, double *A, long long lda, int *perm, void *ws, si
     if (!ws || ws_bytes < frob_dgetrf_workspace_bytes(n)) return FROB_ERR_WORKSPACE;
     Carve c{reinterpret_cast<unsigned char *>(ws), 0, 0};
     double *diag = c.take<double>((size_t)n);
-    int *mv = c.take<int>(MV_INTS);
+    double *work = c.take<double>(getrf_work_elems<double>(n));
+    int *mv = c.take<int>(lu_mv_ints(n));
     LuStats *st = c.take<LuStats>(1);
     cudaStream_t s = (cudaStream_t)stream;
-    FROB_CUDA(getrf<double>(n, A, lda, perm, mv, diag, st, s));
+    FROB_CUDA(getrf<double>(n, A, lda, perm, mv, diag, st, work, s));
     if (host_info) {
         LuStats hs;
         FROB_CUDA(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));

@@ -98,6 +98,8 @@ gemm_kernel(GemmParams<T> p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T *As = reinterpret_cast<T *>(smem_raw);
     T *Bs = As + STAGES * BM * SA;
+    pdl_trigger();
+    pdl_wait();
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;

@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <utility>
 #include <type_traits>
+#include <mutex>
 #include "lu.cuh"
 
 namespace cg = cooperative_groups;
@@ -28,9 +29,7 @@ static cudaError_t gemm_launch_impl(const GemmParams<T> &p, int batch, cudaStrea
         attr_set[dev] = true;
     }
     dim3 grid((p.N + Cf::BN - 1) / Cf::BN, (p.M + Cf::BM - 1) / Cf::BM, batch);
-    count_launch();
-    gemm_kernel<T, VEC><<<grid, Cf::WGM * Cf::WGN * 32, smem, s>>>(p);
-    return cudaGetLastError();
+    return launch_pdl(gemm_kernel<T, VEC>, grid, dim3(Cf::WGM * Cf::WGN * 32), smem, s, p);
 }
 
 static bool aligned16(const void *ptr) { return ((uintptr_t)ptr & 15u) == 0; }
@@ -120,6 +119,8 @@ template <typename T, int PW, int R, bool CLUSTER>
 __global__ void __launch_bounds__(PANEL_T)
 lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, int *__restrict__ mv,
                 T *__restrict__ diag) {
+    pdl_trigger();
+    pdl_wait();
     constexpr int RW = PW * sizeof(T) / 8;  // row width in doubles (16)
     static_assert(RW == 16, "panel rows are 128 bytes");
     static_assert(PW % PANEL_UNROLL == 0, "PW must be a multiple of the unroll");
@@ -150,6 +151,8 @@ lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, 
     const int wd = w * (int)(sizeof(T) / 8);                 // live doubles per row
     const bool vec = ((reinterpret_cast<uintptr_t>(Pd) & 15) == 0) && ((ldd & 1) == 0);
 
+    T *stgT = reinterpret_cast<T *>(stg);
+    constexpr int STG_T = STG_STRIDE * 8 / (int)sizeof(T);  // row stride of the L buffer in T
     PTRACE(0);
     T a[R][PW];
     int grow[R], pidx[R];
@@ -218,7 +221,8 @@ lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, 
                 if (k > bv_next) { bv_next = k; bi_next = grow[q]; qb_next = q; myp = a[q][S]; }
             }
         // speculative reciprocal of this lane's candidate (used if it wins)
-        myip = is_zero(myp) ? zero_of(T()) : recip(myp);
+        if constexpr (sizeof(T) == 8) myip = is_zero(myp) ? zero_of(T()) : frcp(myp);
+        else myip = is_zero(myp) ? zero_of(T()) : recip(myp);
     };
     auto publish = [&](const int j, auto Sc) {
         // Sc may be PANEL_UNROLL (first column after the next rotation): the row is then
@@ -236,7 +240,7 @@ lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, 
                     T r[PW];
 #pragma unroll
                     for (int c = 0; c < PW; ++c)
-                        r[c] = (((c - SN + PW) % PW) < PW - j) ? a[q][(c + K) % PW] : zero_of(T());
+                        r[c] = a[q][(c + K) % PW];  // finished slots are already zero
                     store_row<T, PW>(wrow[par][warp], r);
                     wip[par][warp] = myip;
                 }
@@ -308,7 +312,12 @@ lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, 
                 for (int c = 0; c < PW; ++c)
                     if (c != S && c != S1) a[q][c] = msub(a[q][c], l[q], u[c]);
             }
-            a[q][S] = l[q];
+            // multiplier of a live non-pivot row -> L buffer; its register slot becomes 0 so a
+            // published pivot row never carries finished columns (no masking needed)
+            if (!((done >> q) & 1u)) {
+                stgT[(q * PANEL_T + tid) * STG_T + j] = l[q];
+                a[q][S] = zero_of(T());
+            }
         }
         PTRACEJ(j, 55);
         if (j + 1 < w) publish(j + 1, std::integral_constant<int, decltype(Sc)::value + 1>{});
@@ -391,15 +400,13 @@ lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, 
         if (pidx[q] >= 0) dst = pidx[q];
         else if (g < w) dst = vac[__popc(evm & ((1u << g) - 1u))];
         sdst[q * PANEL_T + tid] = (g < m) ? dst : -1;
-        double t[16];
+        // columns before the row's pivot step hold L multipliers (already in the buffer);
+        // a pivot row keeps its U part (columns >= its step) in registers
+        const int jp = (pidx[q] >= 0) ? pidx[q] : PW;
+        T *row = stgT + (q * PANEL_T + tid) * STG_T;
 #pragma unroll
-        for (int c = 0; c < PW; ++c) {
-            if constexpr (sizeof(T) == 8) t[c] = a[q][c];
-            else { t[2 * c] = a[q][c].x; t[2 * c + 1] = a[q][c].y; }
-        }
-        double *row = &stg[(q * PANEL_T + tid) * STG_STRIDE];
-#pragma unroll
-        for (int c = 0; c < 16; c += 2) *reinterpret_cast<double2 *>(row + c) = make_double2(t[c], t[c + 1]);
+        for (int c = 0; c < PW; ++c)
+            if (c >= jp) row[c] = a[q][c];
     }
     __syncthreads();
 #pragma unroll 4
@@ -432,8 +439,10 @@ constexpr int SWP_COLS = 32;
 // column is issued before its first store.
 template <typename T, int PW>
 __global__ void __launch_bounds__(SWP_COLS)
-lu_swap_trsm_kernel(T *__restrict__ A, long long lda, int n, int k0, int w, const int *__restrict__ mv,
+lu_swap_trsm_kernel(T *__restrict__ A, long long lda, int cb, int ce, int k0, int w, const int *__restrict__ mv,
                     int *__restrict__ perm) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ T Ls[PW][PW + 1];
     __shared__ int srcrow[PW];
     __shared__ int xdst[PW], xsrc[PW];  // moves with destination outside the top w rows
@@ -452,7 +461,7 @@ lu_swap_trsm_kernel(T *__restrict__ A, long long lda, int n, int k0, int w, cons
         }
         nx_s = nx;
     }
-    if (blockIdx.x == 0) {
+    if (perm && blockIdx.x == 0) {
         for (int q = tid; q < cnt; q += SWP_COLS) ptmp[q] = perm[src[q]];
         __syncthreads();
         for (int q = tid; q < cnt; q += SWP_COLS) perm[dst[q]] = ptmp[q];
@@ -463,8 +472,8 @@ lu_swap_trsm_kernel(T *__restrict__ A, long long lda, int n, int k0, int w, cons
     }
     __syncthreads();
     const int v = blockIdx.x * SWP_COLS + tid;
-    if (v >= n - w) return;
-    const int c = (v < k0) ? v : v + w;
+    if (v >= ce - cb - w) return;
+    const int c = (cb + v < k0) ? cb + v : cb + v + w;
     const int nx = nx_s;
     T x[PW], y[PW];
 #pragma unroll
@@ -490,11 +499,68 @@ lu_swap_trsm_kernel(T *__restrict__ A, long long lda, int n, int k0, int w, cons
         if (i < nx) A[(long long)xdst[i] * lda + c] = y[i];
 }
 
+// Apply nlists consecutive panel row movements (lists at mv0 + l*MV_INTS) to the columns
+// [ca0, ca1) and [cb0, cb1): one thread per column, lists in order, every load of a list
+// before its stores.
+constexpr int SWM_COLS = 64;
+template <typename T, int PW>
+__global__ void __launch_bounds__(SWM_COLS)
+lu_swap_multi_kernel(T *__restrict__ A, long long lda, int ca0, int ca1, int cb0, int cb1,
+                     const int *__restrict__ mv0, int nlists) {
+    pdl_trigger();
+    pdl_wait();
+    const int v = blockIdx.x * SWM_COLS + threadIdx.x;
+    const int na = ca1 - ca0;
+    if (v >= na + (cb1 - cb0)) return;
+    const int c = (v < na) ? ca0 + v : cb0 + (v - na);
+    for (int l = 0; l < nlists; ++l) {
+        const int *mv = mv0 + (long long)l * MV_INTS;
+        const int cnt = mv[0];
+        const int *dst = mv + 1, *src = mv + 1 + 2 * PW_MAX;
+        T val[2 * PW];
+#pragma unroll
+        for (int q = 0; q < 2 * PW; ++q)
+            if (q < cnt) val[q] = A[(long long)src[q] * lda + c];
+#pragma unroll
+        for (int q = 0; q < 2 * PW; ++q)
+            if (q < cnt) A[(long long)dst[q] * lda + c] = val[q];
+    }
+}
+
+template <typename T>
+__global__ void copy_block_kernel(const T *__restrict__ src, long long lds, T *__restrict__ dst, long long ldd,
+                                  int rows, int cols) {
+    pdl_trigger();
+    pdl_wait();
+    const long long total = (long long)rows * cols;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / cols), j = (int)(idx - (long long)i * cols);
+        dst[(long long)i * ldd + j] = src[(long long)i * lds + j];
+    }
+}
+
+// Linv = (unit lower triangle of the W x W block at L, ld) extracted with unit diagonal
+template <typename T>
+__global__ void extract_unit_lower_kernel(const T *__restrict__ L, long long ld, int W, T *__restrict__ Li,
+                                          long long ldi) {
+    pdl_trigger();
+    pdl_wait();
+    const long long total = (long long)W * W;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / W), j = (int)(idx - (long long)i * W);
+        Li[(long long)i * ldi + j] = (j < i) ? L[(long long)i * ld + j] : ((i == j) ? one_of(T()) : zero_of(T()));
+    }
+}
+
 // =====================================================================================
 // Pivot diagnostics (reading R2): rho, singular column, non-finite
 // =====================================================================================
 template <typename T>
 __global__ void __launch_bounds__(1024) lu_stats_kernel(const T *__restrict__ diag, int n, LuStats *st) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ double smax[32], smin[32];
     __shared__ int snf[32], sidx[32];
     __shared__ double thr_s;
@@ -554,6 +620,8 @@ __global__ void __launch_bounds__(1024) lu_stats_kernel(const T *__restrict__ di
 }
 
 __global__ void iota_kernel(int *p, int n) {
+    pdl_trigger();
+    pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = i;
 }
@@ -585,13 +653,12 @@ static cudaError_t launch_panel_r(T *P, long long lda, int m, int w, int k0, int
         attr_set[dev] = true;
     }
     if (CS == 1) {
-        count_launch();
-        lu_panel_kernel<T, PW, R, false><<<1, PANEL_T, smem, s>>>(P, lda, m, w, 1, k0, mv, diag);
-        return cudaGetLastError();
+        return launch_pdl(lu_panel_kernel<T, PW, R, false>, dim3(1), dim3(PANEL_T), smem, s, P, lda, m, w, 1, k0,
+                          mv, diag);
     }
     auto kern = lu_panel_kernel<T, PW, R, true>;
     cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     cfg.gridDim = dim3(CS, 1, 1);
     cfg.blockDim = dim3(PANEL_T, 1, 1);
     cfg.dynamicSmemBytes = smem;
@@ -600,8 +667,10 @@ static cudaError_t launch_panel_r(T *P, long long lda, int m, int w, int k0, int
     attr[0].val.clusterDim.x = CS;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     count_launch();
     return cudaLaunchKernelEx(&cfg, kern, P, lda, m, w, CS, k0, mv, diag);
 }
@@ -613,49 +682,6 @@ static cudaError_t launch_panel(T *P, long long lda, int m, int w, int k0, int *
     const int CS = (m + 4 * PANEL_T - 1) / (4 * PANEL_T);
     return launch_panel_r<T, PW, 4>(P, lda, m, w, k0, mv, diag, CS, s);
 }
-
-template <typename T, int PW>
-static cudaError_t getrf_pw(int n, T *A, long long lda, int *perm, int *mv, T *diag, cudaStream_t s) {
-    cudaError_t e;
-    for (int k0 = 0; k0 < n; k0 += PW) {
-        const int w = min(PW, n - k0), m = n - k0;
-        e = launch_panel<T, PW>(A + (long long)k0 * lda + k0, lda, m, w, k0, mv, diag, s);
-        if (e != cudaSuccess) return e;
-        const int ncols = n - w;
-        const int nb = max(1, (ncols + SWP_COLS - 1) / SWP_COLS);
-        count_launch();
-        lu_swap_trsm_kernel<T, PW><<<nb, SWP_COLS, 0, s>>>(A, lda, n, k0, w, mv, perm);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        const int rest = n - k0 - w;
-        if (rest > 0) {
-            T *a21 = A + (long long)(k0 + w) * lda + k0;
-            T *a12 = A + (long long)k0 * lda + k0 + w;
-            T *a22 = A + (long long)(k0 + w) * lda + k0 + w;
-            auto p = gemm_params<T>(rest, rest, w, -1.0, a21, lda, a12, lda, 1.0, a22, lda, a22, lda);
-            if ((e = gemm_launch<T>(p, 1, s)) != cudaSuccess) return e;
-        }
-    }
-    return cudaSuccess;
-}
-
-template <typename T>
-cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuStats *stats,
-                  cudaStream_t s) {
-    count_launch();
-    iota_kernel<<<(n + 255) / 256, 256, 0, s>>>(perm, n);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    e = getrf_pw<T, PanelW<T>::PW>(n, A, lda, perm, mv, diag, s);
-    if (e != cudaSuccess) return e;
-    if (stats) {
-        count_launch();
-        lu_stats_kernel<T><<<1, 1024, 0, s>>>(diag, n, stats);
-        e = cudaGetLastError();
-    }
-    return e;
-}
-template cudaError_t getrf<double>(int, double *, long long, int *, int *, double *, LuStats *, cudaStream_t);
-template cudaError_t getrf<double2>(int, double2 *, long long, int *, int *, double2 *, LuStats *, cudaStream_t);
 
 // =====================================================================================
 // Triangular inverses: U^{-1} (non-unit upper) and L^{-1} (unit lower)
@@ -680,12 +706,14 @@ __global__ void extract_ul_kernel(const T *__restrict__ lu, long long ld, int n,
 // blockIdx.y == 0: invert upper diagonal blocks of U in place; == 1: unit-lower blocks of L
 template <typename T>
 __global__ void __launch_bounds__(TRI_LEAF) tri_leaf_kernel(T *__restrict__ U, T *__restrict__ L,
-                                                            long long ld, int n) {
+                                                            long long ld, int n, int lower_only = 0) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ T S[TRI_LEAF][TRI_LEAF + 1];
     __shared__ T X[TRI_LEAF][TRI_LEAF + 1];
     const int b0 = blockIdx.x * TRI_LEAF;
     const int sz = min(TRI_LEAF, n - b0);
-    const bool upper = (blockIdx.y == 0);
+    const bool upper = (blockIdx.y == 0) && !lower_only;
     T *M = upper ? U : L;
     const int tid = threadIdx.x;
     for (int i = 0; i < sz; ++i)
@@ -722,11 +750,11 @@ __global__ void __launch_bounds__(TRI_LEAF) tri_leaf_kernel(T *__restrict__ U, T
 // One recursion level of size s: blocks [o, o+s) x [o+s, o+s+s2) for o = p*2s.
 template <typename T>
 static cudaError_t tri_level(T *U, T *L, T *tmp, long long ld, int s, int o, int s2, int batch,
-                             cudaStream_t st) {
+                             cudaStream_t st, bool do_upper = true) {
     const long long stride = 2LL * s * (ld + 1);
     cudaError_t e;
     // upper: W = U12 * inv(U22);  U12 <- -inv(U11) * W
-    {
+    if (do_upper) {
         auto p = gemm_params<T>(s, s2, s2, 1.0, U + (long long)o * ld + o + s, ld,
                                 U + (long long)(o + s) * ld + o + s, ld, 0.0, nullptr, ld,
                                 tmp + (long long)o * ld + o + s, ld);
@@ -786,5 +814,187 @@ cudaError_t inv_from_lu(int n, T *lu, long long ld, T *U, T *L, T *out, long lon
 }
 template cudaError_t inv_from_lu<double>(int, double *, long long, double *, double *, double *, long long, const int *, cudaStream_t);
 template cudaError_t inv_from_lu<double2>(int, double2 *, long long, double2 *, double2 *, double2 *, long long, const int *, cudaStream_t);
+
+
+// =====================================================================================
+// getrf: two-level blocked right-looking LU with look-ahead
+// =====================================================================================
+// Outer blocks of LU_NB columns; inside a block, PW-column register panels with narrow
+// swap/TRSM/GEMM updates restricted to the block.  After a block, its row movements,
+// U12 = L11^{-1} A12 (L11^{-1} by the triangular recursion, so the TRSM is a K = LU_NB
+// GEMM) and the K = LU_NB trailing GEMM are applied: first to the NEXT block's columns on
+// the caller's stream (look-ahead), and for all other columns on an internal auxiliary
+// stream, where they overlap the next block's panel chain.
+// below this order the single-level LU (full-width K = PW trailing updates) is faster
+constexpr int LU_TWO_LEVEL_MIN = 2048;
+
+struct AuxCtx {
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev[4];
+    bool ok = false;
+    std::mutex mu;
+};
+static AuxCtx &aux_ctx(cudaError_t &err) {
+    static AuxCtx ctx[64];
+    static std::mutex gmu;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    AuxCtx &c = ctx[dev & 63];
+    std::lock_guard<std::mutex> g(gmu);
+    err = cudaSuccess;
+    if (!c.ok) {
+        err = cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking);
+        for (auto &e : c.ev)
+            if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        c.ok = (err == cudaSuccess);
+    }
+    return c;
+}
+
+static long long ld8(int n) { return ((long long)n + 7) / 8 * 8; }
+
+template <typename T>
+size_t getrf_work_elems(int n) {
+    if (n <= LU_NB) return 1;
+    return 3 * (size_t)LU_NB * LU_NB + 2 * (size_t)LU_NB * ld8(n);
+}
+template size_t getrf_work_elems<double>(int);
+template size_t getrf_work_elems<double2>(int);
+
+size_t lu_mv_ints(int n) { return ((size_t)(n + 7) / 8 + 1) * MV_INTS; }
+
+static int ew_grid(long long total) {
+    long long nb = (total + 255) / 256;
+    return (int)(nb < 148LL * 8 ? nb : 148LL * 8);
+}
+
+// one panel step restricted to the column range [cb, ce) (the panel lies inside it)
+template <typename T, int PW>
+static cudaError_t panel_step(int n, T *A, long long lda, int cb, int ce, int k0, int *perm, int *list, T *diag,
+                              cudaStream_t s) {
+    cudaError_t e;
+    const int w = min(PW, ce - k0), m = n - k0;
+    if ((e = launch_panel<T, PW>(A + (long long)k0 * lda + k0, lda, m, w, k0, list, diag, s)) != cudaSuccess) return e;
+    const int ncols = ce - cb - w;
+    if ((e = launch_pdl(lu_swap_trsm_kernel<T, PW>, dim3(max(1, (ncols + SWP_COLS - 1) / SWP_COLS)), dim3(SWP_COLS),
+                        0, s, A, lda, cb, ce, k0, w, list, perm)) != cudaSuccess)
+        return e;
+    const int rest = ce - k0 - w;
+    if (rest > 0 && m - w > 0) {
+        T *a21 = A + (long long)(k0 + w) * lda + k0;
+        T *a12 = A + (long long)k0 * lda + k0 + w;
+        T *a22 = A + (long long)(k0 + w) * lda + k0 + w;
+        auto p = gemm_params<T>(m - w, rest, w, -1.0, a21, lda, a12, lda, 1.0, a22, lda, a22, lda);
+        if ((e = gemm_launch<T>(p, 1, s)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+// outer update of columns [c0, c1) by block (K0, W): U12 = Linv * A12 -> Tb, A22 -= L21 * Tb, A12 <- Tb
+template <typename T>
+static cudaError_t outer_update(int n, T *A, long long lda, int K0, int W, int c0, int c1, const T *Linv, T *Tb,
+                                long long ldT, cudaStream_t s) {
+    cudaError_t e;
+    const int nc = c1 - c0;
+    if (nc <= 0) return cudaSuccess;
+    auto p = gemm_params<T>(W, nc, W, 1.0, Linv, LU_NB, A + (long long)K0 * lda + c0, lda, 0.0, nullptr, ldT,
+                            Tb + c0, ldT);
+    p.triA = TRI_LOWER;
+    if ((e = gemm_launch<T>(p, 1, s)) != cudaSuccess) return e;
+    const int mr = n - K0 - W;
+    if (mr > 0) {
+        T *c = A + (long long)(K0 + W) * lda + c0;
+        auto q = gemm_params<T>(mr, nc, W, -1.0, A + (long long)(K0 + W) * lda + K0, lda, Tb + c0, ldT, 1.0, c, lda,
+                                c, lda);
+        if ((e = gemm_launch<T>(q, 1, s)) != cudaSuccess) return e;
+    }
+    return launch_pdl(copy_block_kernel<T>, dim3(ew_grid((long long)W * nc)), dim3(256), 0, s, Tb + c0, ldT,
+                      A + (long long)K0 * lda + c0, lda, W, nc);
+}
+
+template <typename T>
+cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuStats *stats, T *work,
+                  cudaStream_t s) {
+    constexpr int PW = PanelW<T>::PW;
+    cudaError_t e = launch_pdl(iota_kernel, dim3((n + 255) / 256), dim3(256), 0, s, perm, n);
+    if (e != cudaSuccess) return e;
+    if (n < LU_TWO_LEVEL_MIN || !work) {
+        for (int k0 = 0; k0 < n; k0 += PW)
+            if ((e = panel_step<T, PW>(n, A, lda, 0, n, k0, perm, mv + (long long)(k0 / PW) * MV_INTS, diag, s)) !=
+                cudaSuccess)
+                return e;
+    } else {
+        AuxCtx &ax = aux_ctx(e);
+        if (e != cudaSuccess) return e;
+        std::lock_guard<std::mutex> guard(ax.mu);
+        const long long ldT = ld8(n);
+        T *Linv[2] = {work, work + (size_t)LU_NB * LU_NB};
+        T *tmp = work + 2 * (size_t)LU_NB * LU_NB;
+        T *Tb[2] = {tmp + (size_t)LU_NB * LU_NB, tmp + (size_t)LU_NB * LU_NB + (size_t)LU_NB * ldT};
+        cudaEvent_t evL = ax.ev[0], evR[2] = {ax.ev[1], ax.ev[2]}, evJ = ax.ev[3];
+        int t = 0;
+        for (int K0 = 0; K0 < n; K0 += LU_NB, ++t) {
+            const int W = min(LU_NB, n - K0);
+            for (int k0 = K0; k0 < K0 + W; k0 += PW)
+                if ((e = panel_step<T, PW>(n, A, lda, K0, K0 + W, k0, perm, mv + (long long)(k0 / PW) * MV_INTS,
+                                           diag, s)) != cudaSuccess)
+                    return e;
+            const int cn0 = K0 + W, cn1 = min(n, K0 + 2 * W);
+            const int nl = (W + PW - 1) / PW;
+            const int *lists = mv + (long long)(K0 / PW) * MV_INTS;
+            T *Li = Linv[t & 1];
+            if (cn0 < n) {
+                // L11^{-1} (W x W unit lower) by the triangular recursion
+                if ((e = launch_pdl(extract_unit_lower_kernel<T>, dim3(ew_grid((long long)W * W)), dim3(256), 0, s,
+                                    A + (long long)K0 * lda + K0, lda, W, Li, (long long)LU_NB)) != cudaSuccess)
+                    return e;
+                if ((e = launch_pdl(tri_leaf_kernel<T>, dim3((W + TRI_LEAF - 1) / TRI_LEAF, 1), dim3(TRI_LEAF), 0, s,
+                                    Li, Li, (long long)LU_NB, W, 1)) != cudaSuccess)
+                    return e;
+                for (int sz = TRI_LEAF; sz < W; sz *= 2) {
+                    const int full = W / (2 * sz);
+                    if (full > 0 && (e = tri_level<T>(Li, Li, tmp, LU_NB, sz, 0, sz, full, s, false)) != cudaSuccess)
+                        return e;
+                    const int o = full * 2 * sz;
+                    if (o + sz < W && (e = tri_level<T>(Li, Li, tmp, LU_NB, sz, o, W - o - sz, 1, s, false)) !=
+                                          cudaSuccess)
+                        return e;
+                }
+            }
+            if ((e = cudaEventRecord(evL, s)) != cudaSuccess) return e;
+            // ---- auxiliary stream: left columns + columns beyond the look-ahead block
+            if ((e = cudaStreamWaitEvent(ax.st, evL, 0)) != cudaSuccess) return e;
+            {
+                const int ncol = K0 + (n - cn1);
+                if (ncol > 0) {
+                    if ((e = launch_pdl(lu_swap_multi_kernel<T, PW>, dim3((ncol + SWM_COLS - 1) / SWM_COLS),
+                                        dim3(SWM_COLS), 0, ax.st, A, lda, 0, K0, cn1, n, lists, nl)) != cudaSuccess)
+                        return e;
+                }
+                if (cn1 < n && (e = outer_update<T>(n, A, lda, K0, W, cn1, n, Li, Tb[t & 1], ldT, ax.st)) != cudaSuccess)
+                    return e;
+            }
+            if ((e = cudaEventRecord(evR[t & 1], ax.st)) != cudaSuccess) return e;
+            // ---- caller's stream: look-ahead block [cn0, cn1)
+            if (cn0 < n) {
+                if (t > 0 && (e = cudaStreamWaitEvent(s, evR[(t - 1) & 1], 0)) != cudaSuccess) return e;
+                if ((e = launch_pdl(lu_swap_multi_kernel<T, PW>, dim3((cn1 - cn0 + SWM_COLS - 1) / SWM_COLS),
+                                    dim3(SWM_COLS), 0, s, A, lda, cn0, cn1, 0, 0, lists, nl)) != cudaSuccess)
+                    return e;
+                if ((e = outer_update<T>(n, A, lda, K0, W, cn0, cn1, Li, Tb[t & 1], ldT, s)) != cudaSuccess) return e;
+            }
+        }
+        // join the auxiliary stream
+        if ((e = cudaEventRecord(evJ, ax.st)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(s, evJ, 0)) != cudaSuccess) return e;
+    }
+    if (stats) {
+        e = launch_pdl(lu_stats_kernel<T>, dim3(1), dim3(1024), 0, s, diag, n, stats);
+    }
+    return e;
+}
+template cudaError_t getrf<double>(int, double *, long long, int *, int *, double *, LuStats *, double *, cudaStream_t);
+template cudaError_t getrf<double2>(int, double2 *, long long, int *, int *, double2 *, LuStats *, double2 *,
+                                    cudaStream_t);
 
 }  // namespace frob

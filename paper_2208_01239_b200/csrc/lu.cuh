@@ -28,8 +28,16 @@ struct LuStats {
 constexpr int PW_MAX = 32;
 constexpr int MV_INTS = 1 + 4 * PW_MAX;
 
+// Outer block width of the two-level LU.
+constexpr int LU_NB = 128;
+// ints needed for the per-panel row-movement lists (mv) of an order-n LU
+size_t lu_mv_ints(int n);
+// elements of T workspace for the outer update (L11^{-1} x2, recursion scratch, U12 x2)
 template <typename T>
-cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuStats *stats,
+size_t getrf_work_elems(int n);
+
+template <typename T>
+cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuStats *stats, T *work,
                   cudaStream_t s);
 
 // From an LU in `lu` (ld): Xinv = U^{-1} L^{-1} (un-permuted: A^{-1} = Xinv P).

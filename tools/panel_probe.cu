@@ -20,7 +20,8 @@ int main(int argc, char **argv) {
     cudaMalloc(&A, h.size() * 8);
     cudaMalloc(&diag, n * 8);
     cudaMalloc(&perm, n * 4);
-    cudaMalloc(&mv, MV_INTS * 4);
+    cudaMalloc(&mv, lu_mv_ints(n) * 4);
+    double *work; cudaMalloc(&work, getrf_work_elems<double>(n) * 8);
     cudaMemcpy(A, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -67,7 +68,7 @@ int main(int argc, char **argv) {
     cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
     printf("panel x20 avg %.2f us\n", ms * 1e3 / 20);
     cudaEventRecord(e0);
-    for (int r = 0; r < 20; ++r) lu_swap_trsm_kernel<double, 16><<<(n - 16 + SWP_COLS - 1) / SWP_COLS, SWP_COLS>>>(A, ld, n, 0, 16, mv, perm);
+    for (int r = 0; r < 20; ++r) lu_swap_trsm_kernel<double, 16><<<(n - 16 + SWP_COLS - 1) / SWP_COLS, SWP_COLS>>>(A, ld, 0, n, 0, 16, mv, perm);
     cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
     printf("swap_trsm x20 avg %.2f us\n", ms * 1e3 / 20);
     auto p = gemm_params<double>(n - 16, n - 16, 16, -1.0, A + 16 * ld, ld, A + 16, ld, 1.0, A + 16 * ld + 16, ld, A + 16 * ld + 16, ld);
@@ -86,7 +87,7 @@ int main(int argc, char **argv) {
     for (int r = 0; r < 2; ++r) {
         cudaMemcpy(A, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
         cudaEventRecord(e0);
-        getrf<double>(n, A, ld, perm, mv, diag, st, 0);
+        getrf<double>(n, A, ld, perm, mv, diag, st, work, 0);
         cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
         printf("getrf n=%d: %.1f us (%lld launches so far)\n", n, ms * 1e3, launch_counter());
     }
@@ -94,7 +95,7 @@ int main(int argc, char **argv) {
         double *U, *L, *O;
         cudaMalloc(&U, h.size() * 8); cudaMalloc(&L, h.size() * 8); cudaMalloc(&O, h.size() * 8);
         for (int r = 0; r < 3; ++r) {
-            getrf<double>(n, A, ld, perm, mv, diag, st, 0);
+            getrf<double>(n, A, ld, perm, mv, diag, st, work, 0);
             cudaEventRecord(e0);
             inv_from_lu<double>(n, A, ld, U, L, O, ld, perm, 0);
             cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
