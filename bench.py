@@ -3,19 +3,23 @@
 
 Default workload (N=1): BASELINE config 2 -- one complex n=1024 FP64 matrix,
 A = G1 + sqrt(n) I, B = G2, inverted by Frobenius inversion (Alg 1) through
-the C ABI (frob_inv, AUTO branch).  One "step" = one full inversion (all SURVEY 8(a)
-rows a0-a7).  Inputs (16 MiB) are smaller than L2, so L2 is flushed (256 MiB write)
-between timed steps, outside the CUDA-event pairs.
+the C ABI (frob_inv, AUTO branch).  One "step" = one full inversion (all SURVEY 8(a) rows
+a0-a7).  Inputs (16 MiB) are smaller than L2, so L2 is flushed (256 MiB write) between
+timed steps, outside the CUDA-event pairs.
 
-Also reported on the same line: the in-house complex-LU comparator (zinv_lu) on the
-same input, the paper's threshold quantities T_inv, T_mult (Thm 5.1), the
-roofline of the dominant kernel, the CPU oracle baseline and an end-to-end number with
-host buffers.
+Other workloads (--config): 3 = batched 65536 x n=32 + 16384 x n=128 (one step = both
+sub-batches, sharded across ranks); 4 = matrix sign by Newton, n=2048 (one step = one
+full Newton solve, one instance per rank); 5 = one large matrix (--n, default 4096).
+
+Every line also carries: the in-house complex-LU comparator on the same input, the
+paper's threshold quantities T_inv, T_mult (Thm 5.1), the roofline of the
+GEMM engine, the CPU oracle baseline (rank 0, N=1) and an end-to-end number with host
+buffers.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config 2|5] [--n N]
-Multi-GPU (torchrun): every rank inverts its own instance (seed + rank): independent
-problems, no data-path collective, "scaling": "weak"; timing = max over ranks.
+                  [--config 2|3|4|5] [--n N]
+Multi-GPU (torchrun): independent problems per rank (instances: seed + rank; batches:
+contiguous index shards), no data-path collective, "scaling": "weak"; time = max over ranks.
 """
 from __future__ import annotations
 
@@ -45,18 +49,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[2, 5])
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5])
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
     return ap.parse_args()
-
-
-def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
 
 
 def fp64_peak():
@@ -97,7 +94,7 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
-            time.sleep(0.15)
+            time.sleep(0.25)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
@@ -107,8 +104,8 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4)
                           if len(s) > i + 2 and s[i + 2].lower() == "active"})
@@ -116,69 +113,264 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+# ------------------------------------------------------------------------------- workloads
+class Workload:
+    """One config: device-resident step, host-buffer e2e step, units and flops per step."""
+    label = ""
+    units = 1          # complex inverses per step on this rank
+    flops = 0.0        # algorithmic FP64 flops per step on this rank (Frobenius 10 n^3)
+    flush = True       # inputs smaller than L2 -> flush between timed steps
+    n_ref = 1024       # order used for the comparator / threshold extras
+
+    def step(self):
+        raise NotImplementedError
+
+    def e2e_step(self):
+        raise NotImplementedError
+
+    def bytes_h2d(self):
+        return 0
+
+    def bytes_d2h(self):
+        return 0
+
+    def check(self):
+        return {}
+
+
+class SingleMatrix(Workload):
+    def __init__(self, fb, torch, dev, n, seed, label):
+        import synth
+        self.fb, self.torch, self.dev, self.n = fb, torch, dev, n
+        self.z_np = synth.config2(n, seed=seed)
+        self.z = torch.from_numpy(self.z_np).to(dev)
+        self.x = torch.empty_like(self.z)
+        self.zh = self.z.cpu().pin_memory()
+        self.xh = torch.empty_like(self.zh).pin_memory()
+        self.units = 1
+        self.flops = 10.0 * n ** 3
+        self.flush = 16 * n * n * 2 < 128 * 2 ** 20
+        self.n_ref = n
+        self.label = (f"config{2 if n == 1024 else 5}: single complex FP64 matrix n={n}, "
+                      f"A=G1+sqrt(n)I, B=G2, Frobenius (Alg 1), AUTO branch")
+
+    def step(self):
+        self.fb.inv(self.z, out=self.x)
+
+    def e2e_step(self):
+        self.fb.inv_host(self.zh, self.xh, device=self.dev)
+
+    def bytes_h2d(self):
+        return self.zh.numel() * 16
+
+    def bytes_d2h(self):
+        return self.xh.numel() * 16
+
+    def check(self):
+        t = self.torch
+        self.fb.inv(self.z, out=self.x)
+        r = float(t.linalg.norm(self.z @ self.x - t.eye(self.n, dtype=t.complex128, device=self.dev)))
+        return {"residual_fro": r, "residual_bound": 1e-11 * self.n}
+
+
+class Batched(Workload):
+    """Config 3: 65536 x n=32 and 16384 x n=128, shard of this rank."""
+
+    def __init__(self, fb, torch, dev, rank, world):
+        import synth
+        from paper_2208_01239_b200 import dist as fdist
+        self.fb, self.torch, self.dev = fb, torch, dev
+        self.parts = []
+        for n, total in ((32, 65536), (128, 16384)):
+            b, e = fdist.shard_range(total, rank, world)
+            z = torch.from_numpy(synth.batch(n, e - b, seed=0, start=b)).to(dev)
+            self.parts.append((n, z, torch.empty_like(z)))
+        self.units = sum(p[1].shape[0] for p in self.parts)
+        self.flops = sum(10.0 * p[0] ** 3 * p[1].shape[0] for p in self.parts)
+        self.flush = False
+        self.n_ref = 128
+        self.host = [(p[1].cpu().pin_memory(), torch.empty_like(p[1], device="cpu").pin_memory()) for p in self.parts]
+        self.label = "config3: 65536 x n=32 + 16384 x n=128 complex FP64 (shift 8, seed+index), batched Frobenius, AUTO"
+
+    def step(self):
+        for n, z, x in self.parts:
+            self.fb.inv_batched(z, out=x)
+
+    def e2e_step(self):
+        for (n, z, x), (zh, xh) in zip(self.parts, self.host):
+            z.copy_(zh, non_blocking=True)
+            self.fb.inv_batched(z, out=x)
+            xh.copy_(x, non_blocking=True)
+        self.torch.cuda.current_stream().synchronize()
+
+    def bytes_h2d(self):
+        return sum(h[0].numel() * 16 for h in self.host)
+
+    def bytes_d2h(self):
+        return self.bytes_h2d()
+
+    def check(self):
+        t = self.torch
+        out = {}
+        for n, z, x in self.parts:
+            _, info, bu = self.fb.inv_batched(z, out=x)
+            e = t.matmul(z[:512], x[:512]) - t.eye(n, dtype=t.complex128, device=self.dev)
+            out[f"n{n}"] = {"singular": int((info != 0).sum()), "branch_b": int((bu == 2).sum()),
+                            "residual_fro_max_first512": float(t.linalg.norm(e, dim=(1, 2)).max())}
+        return out
+
+
+class SignNewton(Workload):
+    """Config 4: sign(Z) by Newton, n=2048, one instance per rank."""
+
+    def __init__(self, fb, torch, dev, n, seed):
+        import synth
+        self.fb, self.torch, self.dev, self.n = fb, torch, dev, n
+        z, s, lam, sinv = synth.sign_instance(n, seed=seed)
+        self.ref = torch.from_numpy((s * np.sign(lam.real)[None, :]) @ sinv).to(dev)
+        self.z = torch.from_numpy(z).to(dev)
+        self.zh = self.z.cpu().pin_memory()
+        self.sh = torch.empty_like(self.zh).pin_memory()
+        _, it, _ = fb.sign(self.z, tol=1e-12, max_iter=50)
+        self.iters = it
+        self.units = it             # complex inversions per Newton solve
+        self.flops = 10.0 * n ** 3 * it
+        self.flush = False
+        self.n_ref = n
+        self.label = f"config4: matrix sign by Newton, complex FP64 n={n}, tol 1e-12 (Frobenius inversions)"
+
+    def step(self):
+        self.fb.sign(self.z, tol=1e-12, max_iter=50)
+
+    def e2e_step(self):
+        z = self.zh.to(self.dev, non_blocking=True)
+        s, _, _ = self.fb.sign(z, tol=1e-12, max_iter=50)
+        self.sh.copy_(s)
+
+    def bytes_h2d(self):
+        return self.zh.numel() * 16
+
+    def bytes_d2h(self):
+        return self.sh.numel() * 16
+
+    def check(self):
+        s, it, d = self.fb.sign(self.z, tol=1e-12, max_iter=50)
+        t = self.torch
+        rel = float(t.linalg.norm(s - self.ref) / t.linalg.norm(self.ref))
+        return {"newton_iters": it, "final_delta": d, "rel_err_vs_closed_form": rel}
+
+
 # ------------------------------------------------------------------------------- reference arm
-def run_reference(args, n, ws, rank):
+def run_reference(args, rank):
     """The CPU oracle as the reference arm (tier rule): same metric, config and unit."""
     if rank != 0:
         return
     import oracle
     import synth
-    z = synth.config2(n, seed=0)
+    oracle.build()
+    if args.config in (2, 5):
+        n = args.n or (1024 if args.config == 2 else 4096)
+        z = synth.config2(n, seed=0)
+        work = lambda: oracle.frob_inv(z)  # noqa: E731
+        units, label = 1, f"config{args.config}: single complex FP64 matrix n={n}, Frobenius (Alg 1)"
+        sample = f"{args.steps} oracle frob_inv calls at n={n}"
+    elif args.config == 3:
+        z32 = synth.batch(32, 2048, seed=0)
+        z128 = synth.batch(128, 16, seed=0)
+
+        def work():
+            for m in z32:
+                oracle.frob_inv(m)
+            for m in z128:
+                oracle.frob_inv(m)
+        units, label = 2048 + 16, "config3 sample: 2048 x n=32 + 16 x n=128 (same generator), Frobenius"
+        sample = "per step: 2048 n=32 + 16 n=128 matrices of the config-3 set (bounded sample)"
+    else:
+        z, _, _, _ = synth.sign_instance(512, seed=0)
+        work = lambda: oracle.sign_newton(z, tol=1e-12, max_iter=50)  # noqa: E731
+        units, label = 13, "config4 sample: sign Newton at n=512 (same generator)"
+        sample = "per step: one Newton sign solve at n=512 (bounded sample of config 4)"
     for _ in range(min(args.warmup, 1)):
-        oracle.frob_inv(z)
+        work()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.frob_inv(z)
+        work()
     dt = time.perf_counter() - t0
-    v = args.steps / dt
+    v = units * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (BASELINE config 2 generator, seed 0)",
-        "config": {"workload": f"config{args.config}: single complex FP64 matrix n={n}, Frobenius (Alg 1)",
-                   "n": n, "l2": "cpu"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-                         "sample": f"{args.steps} oracle frob_inv calls at n={n}"},
+        "data": "synthetic (BASELINE generators)", "config": {"workload": label, "l2": "cpu"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def cpu_baseline(args, wl):
+    """Oracle on the box's host cores, bounded sample (~10 s), same unit."""
+    import oracle
+    import synth
+    oracle.build()
+    t0 = time.perf_counter()
+    cnt = 0
+    if isinstance(wl, SingleMatrix):
+        while True:
+            oracle.frob_inv(wl.z_np)
+            cnt += 1
+            if time.perf_counter() - t0 > 10.0 or cnt >= 20:
+                break
+        sample = f"{cnt} oracle frob_inv calls (plain C, OpenMP) on the same n={wl.n} input"
+    elif isinstance(wl, Batched):
+        zs = synth.batch(32, 4096, seed=0)
+        for m in zs:
+            oracle.frob_inv(m)
+            cnt += 1
+            if time.perf_counter() - t0 > 8.0:
+                break
+        sample = f"{cnt} n=32 matrices of the config-3 set (oracle frob_inv); n=128 omitted"
+    else:
+        z, _, _, _ = synth.sign_instance(512, seed=0)
+        _, it, _ = oracle.sign_newton(z, tol=1e-12, max_iter=50)
+        cnt = it
+        sample = f"one Newton sign solve at n=512 ({it} oracle Frobenius inversions; n=2048 too slow)"
+    dt = time.perf_counter() - t0
+    return {"value": cnt / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle", "sample": sample}
+
+
 # ------------------------------------------------------------------------------- our arm
 def main():
     args = parse()
-    ws, rank, local = dist_env()
-    n = args.n or (1024 if args.config == 2 else 4096)
+    from paper_2208_01239_b200 import dist as fdist
+    ws, rank, local = fdist.env()
     if args.impl == "reference":
-        return run_reference(args, n, ws, rank)
+        return run_reference(args, rank)
 
     import torch
     import torch.distributed as dist
 
     import paper_2208_01239_b200 as fb
     from paper_2208_01239_b200 import frobinv as fbi
-    import synth
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=dev)
-    lib = fbi.load()
+    fbi.load()
 
-    z_np = synth.config2(n, seed=rank)           # instance per rank (weak scaling)
-    z = torch.from_numpy(z_np).to(dev)
-    x = torch.empty_like(z)
+    if args.config in (2, 5):
+        wl = SingleMatrix(fb, torch, dev, args.n or (1024 if args.config == 2 else 4096),
+                          fdist.instance_seed(0, rank), "")
+    elif args.config == 3:
+        wl = Batched(fb, torch, dev, rank, ws)
+    else:
+        wl = SignNewton(fb, torch, dev, args.n or 2048, fdist.instance_seed(0, rank))
+
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step_frob():
-        fb.inv(z, out=x)
-
-    def step_zinv():
-        fb.zinv(z, out=x)
-
-    def timed(fn, steps, warmup, flush_l2=True):
+    def timed(fn, steps, warmup, flush_l2):
         for _ in range(warmup):
             fn()
         torch.cuda.synchronize()
@@ -194,100 +386,85 @@ def main():
 
     # ---------------------------------------------------------------- main timed region
     for _ in range(args.warmup):
-        step_frob()
+        wl.step()
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
     l0 = fbi.launch_count()
     with ClockSampler(local) as clk:
-        times = timed(step_frob, args.steps, 0)
+        times = timed(wl.step, args.steps, 0, wl.flush)
     launches = fbi.launch_count() - l0
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    total_ms = sum(times)
-    if ws > 1:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = fdist.max_over_ranks(sum(times), dev)
+    units_all = fdist.sum_over_ranks(wl.units, dev)
     ms_step = total_ms / args.steps
-    value = ws * args.steps / (total_ms / 1e3)
-    flops = 10.0 * n ** 3  # Frobenius literal: 2 T_inv + 3 T_mult = 10 n^3
+    value = units_all * args.steps / (total_ms / 1e3)
+    flops_all = fdist.sum_over_ranks(wl.flops, dev)
     peak, peak_src = fp64_peak()
 
     extras = {}
     if not args.no_extras:
-        # comparator and threshold quantities (Thm 5.1) on the same GPU, same input
-        zt = timed(step_zinv, max(5, args.steps // 2), 2)
-        t_zinv = statistics.median(zt)
-        a = z.real.contiguous()
+        n = wl.n_ref
+        import synth
+        zr = torch.from_numpy(synth.config2(n, seed=rank)).to(dev)
+        xr = torch.empty_like(zr)
+        t_zinv = statistics.median(timed(lambda: fb.zinv(zr, out=xr), 5, 2, True))
+        t_frob = statistics.median(timed(lambda: fb.inv(zr, out=xr), 5, 2, True))
+        a = zr.real.contiguous()
         ainv = torch.empty_like(a)
         cm = torch.empty_like(a)
-        t_inv = statistics.median(timed(lambda: fb.dinv(a, out=ainv), 10, 2))
-        t_mult = statistics.median(timed(lambda: fb.dgemm(a, ainv, cm), 10, 2))
-        t_frob_med = statistics.median(times)
+        t_inv = statistics.median(timed(lambda: fb.dinv(a, out=ainv), 5, 2, True))
+        t_mult = statistics.median(timed(lambda: fb.dgemm(a, ainv, cm), 5, 2, True))
         ratio = t_inv / t_mult
         r_z = t_zinv / t_inv
         lam = 1.0
-        pred = ratio > (2 + lam) / (r_z - 2) if r_z > 2 else False
-        extras = {
-            "frobenius": {"ms_median": t_frob_med, "tflops_alg": flops / t_frob_med / 1e9},
-            "zinv_lu": {"ms_median": t_zinv, "inverses_per_sec": 1e3 / t_zinv,
-                        "tflops_alg": 8.0 * n ** 3 / t_zinv / 1e9},
-            "threshold": {"T_inv_ms": t_inv, "T_mult_ms": t_mult, "ratio_Tinv_Tmult": ratio,
-                          "paper_threshold_lambda_half": 1.25, "paper_threshold_lambda_one": 1.5,
-                          "lambda": lam, "r_z": r_z, "break_even_general": (2 + lam) / (r_z - 2) if r_z > 2 else None,
-                          "predicted_frob_faster": bool(pred), "measured_frob_faster": bool(t_frob_med < t_zinv)},
-            "gemm_tflops_nnn": 2.0 * n ** 3 / t_mult / 1e9,
-        }
-        # roofline of the dominant kernel: the DMMA GEMM engine at the n x n x n shape the
-        # three Frobenius GEMMs use (same kernel, same stream, CUDA events, L2 flushed)
-        extras["roofline"] = {
-            "bound": "tensor", "kernel": "gemm_kernel<double> (DMMA m8n8k4)",
-            "achieved": 2.0 * n ** 3 / t_mult / 1e9, "peak": peak, "unit": "TFLOP/s",
-            "frac": (2.0 * n ** 3 / t_mult / 1e9) / peak, "traffic": None,
-            "peak_source": peak_src,
-        }
-        # end-to-end through the C ABI with pinned host buffers (H2D + compute + D2H)
-        zh = z.cpu().pin_memory()
-        xh = torch.empty_like(zh).pin_memory()
-        e2e_t = timed(lambda: fb.inv_host(zh, xh, device=dev), max(3, args.steps // 2), 1)
-        extras["e2e"] = {"value": ws * 1e3 / statistics.median(e2e_t), "unit": UNIT,
-                         "h2d_bytes_per_step": int(zh.numel() * 16), "d2h_bytes_per_step": int(xh.numel() * 16)}
-
-    # correctness spot check of the timed output (residual, independent torch GEMM)
-    fb.inv(z, out=x)
-    res = float(torch.linalg.norm(z @ x - torch.eye(n, dtype=torch.complex128, device=dev)))
+        extras["comparison_single_n"] = {
+            "n": n, "frobenius_ms": t_frob, "zinv_lu_ms": t_zinv,
+            "frobenius_tflops_alg": 10.0 * n ** 3 / t_frob / 1e9, "zinv_lu_tflops_alg": 8.0 * n ** 3 / t_zinv / 1e9,
+            "frob_over_zinv_time": t_frob / t_zinv}
+        extras["threshold"] = {
+            "n": n, "T_inv_ms": t_inv, "T_mult_ms": t_mult, "ratio_Tinv_Tmult": ratio,
+            "paper_threshold_lambda_half": 1.25, "paper_threshold_lambda_one": 1.5, "lambda": lam, "r_z": r_z,
+            "break_even_general": (2 + lam) / (r_z - 2) if r_z > 2 else None,
+            "predicted_frob_faster": bool(r_z > 2 and ratio > (2 + lam) / (r_z - 2)),
+            "measured_frob_faster": bool(t_frob < t_zinv)}
+        if isinstance(wl, Batched):
+            z32 = wl.parts[0][1]
+            tb_f = statistics.median(timed(lambda: fb.inv_batched(z32), 3, 1, False))
+            tb_z = statistics.median(timed(lambda: fb.zinv_batched(z32), 3, 1, False))
+            extras["batched_n32_comparison"] = {"frob_ms": tb_f, "zinv_lu_ms": tb_z, "count": int(z32.shape[0])}
+        # roofline of the GEMM engine (DMMA) at the n x n x n shape of the three Frobenius GEMMs
+        ach = 2.0 * n ** 3 / t_mult / 1e9
+        extras["roofline"] = {"bound": "tensor", "kernel": "gemm_kernel<double> (DMMA m8n8k4), n x n x n",
+                              "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                              "traffic": None, "peak_source": peak_src}
+        e2e = timed(wl.e2e_step, max(3, args.steps // 2), 1, False)
+        e2e_ms = fdist.max_over_ranks(statistics.median(e2e), dev)
+        extras["e2e"] = {"value": units_all * 1e3 / e2e_ms, "unit": UNIT,
+                         "h2d_bytes_per_step": int(wl.bytes_h2d()), "d2h_bytes_per_step": int(wl.bytes_d2h())}
+    chk = wl.check()
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        import oracle
-        oracle.build()
-        t0 = time.perf_counter()
-        cnt = 0
-        while True:
-            oracle.frob_inv(z_np)
-            cnt += 1
-            if time.perf_counter() - t0 > 10.0 or cnt >= 20:
-                break
-        dt = time.perf_counter() - t0
-        cpu = {"value": cnt / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-               "sample": f"{cnt} oracle frob_inv calls (plain C, OpenMP) on the same n={n} input"}
+        cpu = cpu_baseline(args, wl)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE config 2 generator, seed = rank)",
-            "config": {"workload": f"config{args.config}: single complex FP64 matrix n={n}, Frobenius (Alg 1), AUTO branch",
-                       "n": n, "l2": "flushed (256 MiB write) between timed steps", "parallelism": f"replicas x{ws}"},
-            "tflops_alg": flops / (ms_step * 1e-3) / 1e12,
-            "step_roofline_frac": flops / (ms_step * 1e-3) / 1e12 / peak,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE generators, seed = rank / index)",
+            "config": {"workload": wl.label, "l2": ("flushed (256 MiB write) between timed steps" if wl.flush
+                                                    else "inputs larger than L2 / not flushed"),
+                       "parallelism": f"{ws} rank(s), independent problems"},
+            "tflops_alg": flops_all / (total_ms / args.steps * 1e-3) / 1e12,
+            "step_roofline_frac": flops_all / (total_ms / args.steps * 1e-3) / 1e12 / (peak * ws),
             "gpu_launches": int(launches),
             "gpu_launches_per_step": launches / args.steps,
             "clocks": clk.summary(),
-            "residual_fro": res,
+            "check": chk,
         }
         line.update(extras)
         if cpu:

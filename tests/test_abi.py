@@ -57,9 +57,9 @@ def test_invalid_arguments_rejected_without_gpu(lib):
     assert st == 4  # X aliases Z
     st = lib.frob_inv(8, ctypes.c_void_p(4096), 8, ctypes.c_void_p(1 << 20), 8, 0, None, 0, None, None)
     assert st == 6  # no workspace
-    st = lib.frob_inv_batched(65, 1, ctypes.c_void_p(4096), 65 * 65, ctypes.c_void_p(1 << 20), 65 * 65, 0,
+    st = lib.frob_inv_batched(129, 1, ctypes.c_void_p(4096), 129 * 129, ctypes.c_void_p(1 << 20), 129 * 129, 0,
                               ctypes.c_void_p(8192), None, None, 0, None)
-    assert st == 4  # n > 64 not supported by the batched kernels
+    assert st == 4  # n > 128 not supported by the batched kernels
 
 
 def test_product_has_no_cpu_fallback():
