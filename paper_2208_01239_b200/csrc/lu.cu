@@ -118,7 +118,7 @@ constexpr int STG_STRIDE = 18;
 template <typename T, int PW, int R, bool CLUSTER>
 __global__ void __launch_bounds__(PANEL_T)
 lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, int *__restrict__ mv,
-                T *__restrict__ diag) {
+                T *__restrict__ diag, int cb, int ce, int *__restrict__ perm) {
     pdl_trigger();
     pdl_wait();
     constexpr int RW = PW * sizeof(T) / 8;  // row width in doubles (16)
@@ -130,12 +130,13 @@ lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, 
     __shared__ int wi[2][PANEL_W];
     __shared__ __align__(16) T wrow[2][PANEL_W][PW];  // each warp's candidate row (zero-padded)
     __shared__ T wip[2][PANEL_W];                     // and the reciprocal of its pivot value
-    __shared__ __align__(16) T upiv[PANEL_W][PW];     // warp-private copy (cluster path)
-    __shared__ T upiv_ip[PANEL_W];
-    __shared__ T pubip[2];
-    __shared__ unsigned long long pubv[2];
-    __shared__ int pubi[2];
-    __shared__ __align__(16) T pubrow[2][PW];
+    // cluster exchange (push model): slot [par][rank] written by CTA `rank`
+    constexpr int CSMAX = CLUSTER ? 16 : 1;
+    __shared__ unsigned long long rkey[2][CSMAX];
+    __shared__ int ridx[2][CSMAX];
+    __shared__ T rip[2][CSMAX];
+    __shared__ __align__(16) T rrow[2][CSMAX][PW];
+    __shared__ __align__(8) unsigned long long rbar[2];
     __shared__ int pivrows[PW];
     __shared__ T pvals[PW];
     __shared__ int vac[PW];
@@ -151,6 +152,14 @@ lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, 
     const int wd = w * (int)(sizeof(T) / 8);                 // live doubles per row
     const bool vec = ((reinterpret_cast<uintptr_t>(Pd) & 15) == 0) && ((ldd & 1) == 0);
 
+    if constexpr (CLUSTER) {
+        if (tid == 0) {
+            mbar_init(smem_u32(&rbar[0]), (unsigned)CS);
+            mbar_init(smem_u32(&rbar[1]), (unsigned)CS);
+            mbar_init_fence();
+        }
+        cg::this_cluster().sync();  // every CTA's barriers exist before anyone arrives on them
+    }
     T *stgT = reinterpret_cast<T *>(stg);
     constexpr int STG_T = STG_STRIDE * 8 / (int)sizeof(T);  // row stride of the L buffer in T
     PTRACE(0);
@@ -265,27 +274,25 @@ lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, 
             load_row<T, PW>(u, wrow[par][cw]);
             ip = wip[par][cw];
         } else {
-            cg::cluster_group cl = cg::this_cluster();
-            if (warp == 0) {
-                if (lane == 0) { pubv[par] = ca.k; pubi[par] = ca.i; pubip[par] = wip[par][cw]; }
-                if (lane < PW) pubrow[par][lane] = wrow[par][cw][lane];
+            // push the CTA winner (key, index, reciprocal, row) into every CTA of the cluster,
+            // then one remote mbarrier arrive per target; wait on the local barrier
+            if (warp == 0 && lane < CS) {
+                const unsigned tgt = (unsigned)lane;
+                const T *wr = wrow[par][cw];
+                const unsigned rowa = mapa_u32(smem_u32(&rrow[par][crank][0]), tgt);
+#pragma unroll
+                for (int c = 0; c < PW; ++c) st_cluster(rowa + c * (unsigned)sizeof(T), wr[c]);
+                st_cluster(mapa_u32(smem_u32(&rkey[par][crank]), tgt), ca.k);
+                st_cluster(mapa_u32(smem_u32(&ridx[par][crank]), tgt), ca.i);
+                st_cluster(mapa_u32(smem_u32(&rip[par][crank]), tgt), wip[par][cw]);
+                mbar_remote_arrive(mapa_u32(smem_u32(&rbar[par]), tgt));
             }
-            cl.sync();
-            unsigned long long qv = 0;
-            int qi = INT_MAX;
-            if (lane < CS) {
-                qv = *cl.map_shared_rank(&pubv[par], lane);
-                qi = *cl.map_shared_rank(&pubi[par], lane);
-            }
-            const ArgMaxK ga = warp_argmax_key(qv, qi);
+            mbar_wait_parity(smem_u32(&rbar[par]), (unsigned)((j >> 1) & 1));
+            const ArgMaxK ga = warp_argmax_key(lane < CS ? rkey[par][lane] : 0ull, lane < CS ? ridx[par][lane] : INT_MAX);
             gp = ga.i;
             const int owner = gp / RPC;
-            if (lane < PW) upiv[warp][lane] = *cl.map_shared_rank(&pubrow[par][lane], owner);
-            if (lane == 0) upiv_ip[warp] = *cl.map_shared_rank(&pubip[par], owner);
-            __syncwarp();
-            load_row<T, PW>(u, upiv[warp]);
-            ip = upiv_ip[warp];
-            __syncwarp();
+            load_row<T, PW>(u, rrow[par][owner]);
+            ip = rip[par][owner];
         }
         const T piv = u[S];
         const bool zp = is_zero(piv);
@@ -424,6 +431,71 @@ lu_panel_kernel(T *__restrict__ P, long long lda, int m, int w, int CS, int k0, 
         }
     }
     PTRACE(41);
+    // ---- fused: row movement of this panel + U12 = L11^{-1} A12 on the other columns of
+    // the block [cb, ce) (the two-level LU's inner update), once every CTA's rows are back
+    const int ncol = ce - cb - w;
+    if (ncol > 0) {
+        __shared__ T Ls[PW][PW + 1];
+        __shared__ int srcr[PW], xdst[PW], xsrc[PW];
+        __shared__ int nx_s;
+        if constexpr (CLUSTER) cg::this_cluster().sync();  // release/acquire: the writeback is visible
+        else __syncthreads();
+        T *A = P - (long long)k0 * lda - k0;  // matrix origin
+        if (tid == 0) {
+            int nx = 0;
+            for (int i = 0; i < w; ++i) srcr[i] = k0 + pivrows[i];
+            for (int r = 0; r < w; ++r)
+                if ((evm >> r) & 1u) {
+                    xdst[nx] = k0 + vac[__popc(evm & ((1u << r) - 1u))];
+                    xsrc[nx] = k0 + r;
+                    ++nx;
+                }
+            nx_s = nx;
+        }
+        if (crank == 0 && warp == 0 && perm) {  // perm[dst] = perm[src] for the moved rows
+            int d = -1, v = 0;
+            if (lane < w && pivrows[lane] != lane) { d = k0 + lane; v = perm[k0 + pivrows[lane]]; }
+            int d2 = -1, v2 = 0;
+            if (lane < w && ((evm >> lane) & 1u)) {
+                d2 = k0 + vac[__popc(evm & ((1u << lane) - 1u))];
+                v2 = perm[k0 + lane];
+            }
+            __syncwarp();
+            if (d >= 0) perm[d] = v;
+            if (d2 >= 0) perm[d2] = v2;
+        }
+        for (int idx = tid; idx < w * w; idx += PANEL_T) {
+            const int i = idx / w, q = idx - i * w;
+            Ls[i][q] = A[(long long)(k0 + i) * lda + k0 + q];
+        }
+        __syncthreads();
+        const int nx = nx_s;
+        for (int v = crank * PANEL_T + tid; v < ncol; v += CS * PANEL_T) {
+            const int c = (cb + v < k0) ? cb + v : cb + v + w;
+            T x[PW], y[PW];
+#pragma unroll
+            for (int i = 0; i < PW; ++i) x[i] = (i < w) ? A[(long long)srcr[i] * lda + c] : zero_of(T());
+#pragma unroll
+            for (int i = 0; i < PW; ++i) y[i] = (i < nx) ? A[(long long)xsrc[i] * lda + c] : zero_of(T());
+            if (c >= k0 + w) {
+#pragma unroll
+                for (int i = 1; i < PW; ++i) {
+                    if (i < w) {
+                        T acc = x[i];
+#pragma unroll
+                        for (int q = 0; q < i; ++q) acc = msub(acc, Ls[i][q], x[q]);
+                        x[i] = acc;
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < PW; ++i)
+                if (i < w) A[(long long)(k0 + i) * lda + c] = x[i];
+#pragma unroll
+            for (int i = 0; i < PW; ++i)
+                if (i < nx) A[(long long)xdst[i] * lda + c] = y[i];
+        }
+    }
     if constexpr (CLUSTER) cg::this_cluster().sync();  // no CTA leaves while its smem may still be read
 }
 
@@ -636,7 +708,7 @@ constexpr int PANEL_MAX_CS = 16;
 
 template <typename T, int PW, int R>
 static cudaError_t launch_panel_r(T *P, long long lda, int m, int w, int k0, int *mv, T *diag, int CS,
-                                  cudaStream_t s) {
+                                  cudaStream_t s, int cb = 0, int ce = 0, int *perm = nullptr) {
     const size_t smem = (size_t)R * PANEL_T * STG_STRIDE * sizeof(double);
     static bool attr_set[64] = {false};
     int dev = 0;
@@ -654,7 +726,7 @@ static cudaError_t launch_panel_r(T *P, long long lda, int m, int w, int k0, int
     }
     if (CS == 1) {
         return launch_pdl(lu_panel_kernel<T, PW, R, false>, dim3(1), dim3(PANEL_T), smem, s, P, lda, m, w, 1, k0,
-                          mv, diag);
+                          mv, diag, cb, ce, perm);
     }
     auto kern = lu_panel_kernel<T, PW, R, true>;
     cudaLaunchConfig_t cfg{};
@@ -672,15 +744,21 @@ static cudaError_t launch_panel_r(T *P, long long lda, int m, int w, int k0, int
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     count_launch();
-    return cudaLaunchKernelEx(&cfg, kern, P, lda, m, w, CS, k0, mv, diag);
+    return cudaLaunchKernelEx(&cfg, kern, P, lda, m, w, CS, k0, mv, diag, cb, ce, perm);
 }
 
 template <typename T, int PW>
-static cudaError_t launch_panel(T *P, long long lda, int m, int w, int k0, int *mv, T *diag, cudaStream_t s) {
-    if (m <= PANEL_T) return launch_panel_r<T, PW, 1>(P, lda, m, w, k0, mv, diag, 1, s);
-    if (m <= 2 * PANEL_T) return launch_panel_r<T, PW, 2>(P, lda, m, w, k0, mv, diag, 1, s);
-    const int CS = (m + 4 * PANEL_T - 1) / (4 * PANEL_T);
-    return launch_panel_r<T, PW, 4>(P, lda, m, w, k0, mv, diag, CS, s);
+static cudaError_t launch_panel(T *P, long long lda, int m, int w, int k0, int *mv, T *diag, cudaStream_t s,
+                                int cb = 0, int ce = 0, int *perm = nullptr) {
+    // single CTA up to 1024 rows; beyond, a cluster with as few rows per CTA as 16 CTAs allow
+    // (the push-model exchange makes more, lighter CTAs cheaper per column)
+    if (m <= PANEL_T) return launch_panel_r<T, PW, 1>(P, lda, m, w, k0, mv, diag, 1, s, cb, ce, perm);
+    if (m <= 2 * PANEL_T) return launch_panel_r<T, PW, 2>(P, lda, m, w, k0, mv, diag, 1, s, cb, ce, perm);
+    if (m <= 4 * PANEL_T) return launch_panel_r<T, PW, 4>(P, lda, m, w, k0, mv, diag, 1, s, cb, ce, perm);
+    if (m <= 16 * PANEL_T) return launch_panel_r<T, PW, 1>(P, lda, m, w, k0, mv, diag, (m + PANEL_T - 1) / PANEL_T, s, cb, ce, perm);
+    if (m <= 32 * PANEL_T)
+        return launch_panel_r<T, PW, 2>(P, lda, m, w, k0, mv, diag, (m + 2 * PANEL_T - 1) / (2 * PANEL_T), s, cb, ce, perm);
+    return launch_panel_r<T, PW, 4>(P, lda, m, w, k0, mv, diag, (m + 4 * PANEL_T - 1) / (4 * PANEL_T), s, cb, ce, perm);
 }
 
 // =====================================================================================
@@ -874,11 +952,16 @@ static cudaError_t panel_step(int n, T *A, long long lda, int cb, int ce, int k0
                               cudaStream_t s) {
     cudaError_t e;
     const int w = min(PW, ce - k0), m = n - k0;
-    if ((e = launch_panel<T, PW>(A + (long long)k0 * lda + k0, lda, m, w, k0, list, diag, s)) != cudaSuccess) return e;
-    const int ncols = ce - cb - w;
-    if ((e = launch_pdl(lu_swap_trsm_kernel<T, PW>, dim3(max(1, (ncols + SWP_COLS - 1) / SWP_COLS)), dim3(SWP_COLS),
-                        0, s, A, lda, cb, ce, k0, w, list, perm)) != cudaSuccess)
+    const bool fused = (ce - cb) <= LU_NB;  // inner step of the two-level LU: swap+TRSM fused into the panel
+    if ((e = launch_panel<T, PW>(A + (long long)k0 * lda + k0, lda, m, w, k0, list, diag, s, fused ? cb : 0,
+                                 fused ? ce : 0, fused ? perm : nullptr)) != cudaSuccess)
         return e;
+    const int ncols = ce - cb - w;
+    if (!fused || ncols <= 0) {
+        if ((e = launch_pdl(lu_swap_trsm_kernel<T, PW>, dim3(max(1, (ncols + SWP_COLS - 1) / SWP_COLS)),
+                            dim3(SWP_COLS), 0, s, A, lda, cb, ce, k0, w, list, perm)) != cudaSuccess)
+            return e;
+    }
     const int rest = ce - k0 - w;
     if (rest > 0 && m - w > 0) {
         T *a21 = A + (long long)(k0 + w) * lda + k0;
