@@ -210,7 +210,7 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
     const double sgn = (use == 1) ? 1.0 : -1.0;
 
     // a2: Xinv' = U^{-1} L^{-1}  (X^{-1} = Xinv' P)
-    FROB_CUDA(inv_from_lu<double>(n, Xlu, ld, w.W2, w.W3, w.W4, ld, nullptr, s));
+    FROB_CUDA(inv_from_lu<double>(n, Xlu, ld, w.W2, w.W3, w.W4, ld, nullptr, w.flags + 2, s));
     // a3: C = X^{-1} Y = Xinv' (P Y)   [B-row gather]
     {
         auto p = gemm_params<double>(n, n, n, sgn, w.W4, ld, Ym, ld, 0.0, nullptr, ld, w.W2, ld);
@@ -225,7 +225,7 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
     // a5: Re' = M^{-1} (un-permuted)
     FROB_CUDA(getrf<double>(n, w.W3, ld, w.perm_m, w.mv, w.diag, &w.stats[2], w.work, s));
     double *Re = (use == 1) ? w.A : w.B;  // X buffer is free now
-    FROB_CUDA(inv_from_lu<double>(n, w.W3, ld, w.W1, w.W4, Re, ld, nullptr, s));
+    FROB_CUDA(inv_from_lu<double>(n, w.W3, ld, w.W1, w.W4, Re, ld, nullptr, w.flags + 2, s));
     // a6/a7: Im' = -C Re', fused with the column interchanges and the interleaved store
     {
         auto p = gemm_params<double>(n, n, n, -1.0, w.W2, ld, Re, ld, 0.0, Re, ld, X, ldx);
@@ -265,7 +265,7 @@ static frob_status zinv_lu_impl(int n, const double *Z, long long ldz, double *X
         reinterpret_cast<const double2 *>(Z), ldz, w.W, ld, n, w.flags);
     FROB_CUDA(cudaGetLastError());
     FROB_CUDA(getrf<double2>(n, w.W, ld, w.perm, w.mv, w.diag, w.stats, w.work, s));
-    FROB_CUDA(inv_from_lu<double2>(n, w.W, ld, w.U, w.L, reinterpret_cast<double2 *>(X), ldx, w.perm, s));
+    FROB_CUDA(inv_from_lu<double2>(n, w.W, ld, w.U, w.L, reinterpret_cast<double2 *>(X), ldx, w.perm, w.flags + 2, s));
     if (host_info) {
         LuStats hs;
         int hf = 0;
@@ -284,6 +284,7 @@ struct DinvWs {
     double *W, *U, *L, *diag, *work;
     int *perm, *mv;
     LuStats *stats;
+    int *flags;
     size_t bytes;
 };
 static DinvWs carve_dinv(void *ws, int n) {
@@ -298,6 +299,7 @@ static DinvWs carve_dinv(void *ws, int n) {
     w.perm = c.take<int>((size_t)n);
     w.mv = c.take<int>(lu_mv_ints(n));
     w.stats = c.take<LuStats>(1);
+    w.flags = c.take<int>(4);
     w.bytes = c.off;
     return w;
 }
@@ -552,7 +554,7 @@ frob_status frob_dinv(int n, const double *A, long long lda, double *Ainv, long 
     copy2d_kernel<double><<<ew_blocks((long long)n * n), 256, 0, s>>>(A, lda, w.W, ld, n, nullptr);
     FROB_CUDA(cudaGetLastError());
     FROB_CUDA(getrf<double>(n, w.W, ld, w.perm, w.mv, w.diag, w.stats, w.work, s));
-    FROB_CUDA(inv_from_lu<double>(n, w.W, ld, w.U, w.L, Ainv, ldainv, w.perm, s));
+    FROB_CUDA(inv_from_lu<double>(n, w.W, ld, w.U, w.L, Ainv, ldainv, w.perm, w.flags, s));
     if (host_info) {
         LuStats hs;
         FROB_CUDA(cudaMemcpyAsync(&hs, w.stats, sizeof(hs), cudaMemcpyDeviceToHost, s));

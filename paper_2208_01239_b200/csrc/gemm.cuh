@@ -36,6 +36,15 @@ struct GemmParams {
     const int *browmap;              // nullable: row k of B is B[browmap[k]]
     const int *colperm;              // nullable: output column j goes to colperm[j]
     int triA, triB, epi;
+    int *counter;                    // non-null: persistent CTAs take tiles from this counter,
+                                     // longest k-range first (square triangular products)
+};
+
+// Up to two independent problems in one launch (blockIdx.z < zsplit -> q[0], else q[1]).
+template <typename T>
+struct GemmPair {
+    GemmParams<T> q[2];
+    int zsplit;
 };
 
 template <typename T> struct GemmCfg;
@@ -85,8 +94,7 @@ FROB_DEV double acc_val(const double (&c)[2], int e) { return c[e]; }
 FROB_DEV double2 acc_val(const double (&c)[4], int e) { return make_double2(c[e], c[2 + e]); }
 
 template <typename T, bool VEC>
-__global__ void __launch_bounds__(GemmCfg<T>::WGM * GemmCfg<T>::WGN * 32)
-gemm_kernel(GemmParams<T> p) {
+FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int row0, const int col0, T *As, T *Bs) {
     using Cf = GemmCfg<T>;
     constexpr int BM = Cf::BM, BN = Cf::BN, BK = Cf::BK, STAGES = Cf::STAGES;
     constexpr int NTH = Cf::WGM * Cf::WGN * 32;
@@ -95,20 +103,13 @@ gemm_kernel(GemmParams<T> p) {
     constexpr int SA = BK + Cf::PADA, SB = BN + Cf::PADB;
     constexpr int V = AccW<T>::V;
 
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T *As = reinterpret_cast<T *>(smem_raw);
-    T *Bs = As + STAGES * BM * SA;
-    pdl_trigger();
-    pdl_wait();
-
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int wm0 = (warp / Cf::WGN) * WM, wn0 = (warp % Cf::WGN) * WN;
-    const long long bz = blockIdx.z;
     const T *__restrict__ A = p.A + bz * p.sA;
     const T *__restrict__ B = p.B + bz * p.sB;
     const int M = p.M, N = p.N, K = p.K;
-    const int row0 = blockIdx.y * BM, col0 = blockIdx.x * BN;
+    if (row0 >= M || col0 >= N) return;
 
     int kb = 0, ke = K;
     if (p.triA == TRI_UPPER) kb = max(kb, row0);
@@ -275,6 +276,44 @@ gemm_kernel(GemmParams<T> p) {
                 Cp[(long long)row * p.ldc + oc[j][e]] = v;
             }
         }
+    }
+}
+
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(GemmCfg<T>::WGM * GemmCfg<T>::WGN * 32)
+gemm_kernel(GemmPair<T> pp) {
+    using Cf = GemmCfg<T>;
+    constexpr int SA = Cf::BK + Cf::PADA;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T *As = reinterpret_cast<T *>(smem_raw);
+    T *Bs = As + Cf::STAGES * Cf::BM * SA;
+    pdl_trigger();
+    pdl_wait();
+    const int z = blockIdx.z;
+    const GemmParams<T> &p = (z < pp.zsplit) ? pp.q[0] : pp.q[1];
+    const long long bz = (z < pp.zsplit) ? z : z - pp.zsplit;
+    if (!p.counter) {
+        gemm_tile<T, VEC>(p, bz, blockIdx.y * Cf::BM, blockIdx.x * Cf::BN, As, Bs);
+        return;
+    }
+    // persistent: tiles in order of max(I, J) = 0, 1, ... (longest k-range first for
+    // upper x lower products); t -> d = isqrt(t), r = t - d^2: (d, r) or (r - d - 1, d)
+    __shared__ int tile_s;
+    const int D = (p.M + Cf::BM - 1) / Cf::BM;
+    const int total = D * D;
+    for (;;) {
+        __syncthreads();  // previous tile done with the shared stages
+        if (threadIdx.x == 0) tile_s = atomicAdd(p.counter, 1);
+        __syncthreads();
+        const int tt = tile_s;
+        if (tt >= total) break;
+        int d = (int)sqrtf((float)tt);
+        while (d * d > tt) --d;
+        while ((d + 1) * (d + 1) <= tt) ++d;
+        const int r = tt - d * d;
+        const int I = (r <= d) ? d : r - d - 1;
+        const int J = (r <= d) ? r : d;
+        gemm_tile<T, VEC>(p, bz, I * Cf::BM, J * Cf::BN, As, Bs);
     }
 }
 

@@ -16,7 +16,7 @@ namespace frob {
 // GEMM launcher
 // =====================================================================================
 template <typename T, bool VEC>
-static cudaError_t gemm_launch_impl(const GemmParams<T> &p, int batch, cudaStream_t s) {
+static cudaError_t gemm_launch_impl(const GemmPair<T> &pp, int batch0, int batch1, cudaStream_t s) {
     using Cf = GemmCfg<T>;
     constexpr size_t smem = gemm_smem_bytes<T>();
     static bool attr_set[64] = {false};
@@ -28,19 +28,53 @@ static cudaError_t gemm_launch_impl(const GemmParams<T> &p, int batch, cudaStrea
         if (e != cudaSuccess) return e;
         attr_set[dev] = true;
     }
-    dim3 grid((p.N + Cf::BN - 1) / Cf::BN, (p.M + Cf::BM - 1) / Cf::BM, batch);
-    return launch_pdl(gemm_kernel<T, VEC>, grid, dim3(Cf::WGM * Cf::WGN * 32), smem, s, p);
+    const GemmParams<T> &p0 = pp.q[0];
+    if (p0.counter) {
+        const int D = (p0.M + Cf::BM - 1) / Cf::BM;
+        const int grid = min(D * D, 148 * 3);
+        cudaError_t e = cudaMemsetAsync(p0.counter, 0, sizeof(int), s);
+        if (e != cudaSuccess) return e;
+        return launch_pdl(gemm_kernel<T, VEC>, dim3(grid, 1, 1), dim3(Cf::WGM * Cf::WGN * 32), smem, s, pp);
+    }
+    int M = p0.M, N = p0.N;
+    if (batch1 > 0) {
+        M = max(M, pp.q[1].M);
+        N = max(N, pp.q[1].N);
+    }
+    dim3 grid((N + Cf::BN - 1) / Cf::BN, (M + Cf::BM - 1) / Cf::BM, batch0 + batch1);
+    return launch_pdl(gemm_kernel<T, VEC>, grid, dim3(Cf::WGM * Cf::WGN * 32), smem, s, pp);
 }
 
 static bool aligned16(const void *ptr) { return ((uintptr_t)ptr & 15u) == 0; }
 
 template <typename T>
+static bool gemm_vec_ok(const GemmParams<T> &p, int batch) {
+    constexpr int E = 16 / sizeof(T);
+    return aligned16(p.A) && aligned16(p.B) && (p.lda % E == 0) && (p.ldb % E == 0) &&
+           (batch <= 1 || ((p.sA % E == 0) && (p.sB % E == 0)));
+}
+
+template <typename T>
 cudaError_t gemm_launch(const GemmParams<T> &p, int batch, cudaStream_t s) {
     if (p.M <= 0 || p.N <= 0 || batch <= 0) return cudaSuccess;
-    constexpr int E = 16 / sizeof(T);
-    bool vec = aligned16(p.A) && aligned16(p.B) && (p.lda % E == 0) && (p.ldb % E == 0) &&
-               (batch == 1 || ((p.sA % E == 0) && (p.sB % E == 0)));
-    return vec ? gemm_launch_impl<T, true>(p, batch, s) : gemm_launch_impl<T, false>(p, batch, s);
+    GemmPair<T> pp{};
+    pp.q[0] = p;
+    pp.q[1] = p;
+    pp.zsplit = batch;
+    return gemm_vec_ok(p, batch) ? gemm_launch_impl<T, true>(pp, batch, 0, s) : gemm_launch_impl<T, false>(pp, batch, 0, s);
+}
+
+// two independent problems (each possibly batched) in one launch
+template <typename T>
+cudaError_t gemm_launch2(const GemmParams<T> &p0, int b0, const GemmParams<T> &p1, int b1, cudaStream_t s) {
+    if (p0.M <= 0 || p0.N <= 0 || b0 <= 0) return gemm_launch<T>(p1, b1, s);
+    if (p1.M <= 0 || p1.N <= 0 || b1 <= 0) return gemm_launch<T>(p0, b0, s);
+    GemmPair<T> pp{};
+    pp.q[0] = p0;
+    pp.q[1] = p1;
+    pp.zsplit = b0;
+    const bool vec = gemm_vec_ok(p0, b0) && gemm_vec_ok(p1, b1);
+    return vec ? gemm_launch_impl<T, true>(pp, b0, b1, s) : gemm_launch_impl<T, false>(pp, b0, b1, s);
 }
 template cudaError_t gemm_launch<double>(const GemmParams<double> &, int, cudaStream_t);
 template cudaError_t gemm_launch<double2>(const GemmParams<double2> &, int, cudaStream_t);
@@ -831,38 +865,31 @@ static cudaError_t tri_level(T *U, T *L, T *tmp, long long ld, int s, int o, int
                              cudaStream_t st, bool do_upper = true) {
     const long long stride = 2LL * s * (ld + 1);
     cudaError_t e;
-    // upper: W = U12 * inv(U22);  U12 <- -inv(U11) * W
-    if (do_upper) {
-        auto p = gemm_params<T>(s, s2, s2, 1.0, U + (long long)o * ld + o + s, ld,
-                                U + (long long)(o + s) * ld + o + s, ld, 0.0, nullptr, ld,
-                                tmp + (long long)o * ld + o + s, ld);
-        p.triB = TRI_UPPER; p.sA = p.sB = p.sC = stride; p.sD = 0;
-        if ((e = gemm_launch<T>(p, batch, st)) != cudaSuccess) return e;
-        auto q = gemm_params<T>(s, s2, s, -1.0, U + (long long)o * ld + o, ld,
-                                tmp + (long long)o * ld + o + s, ld, 0.0, nullptr, ld,
-                                U + (long long)o * ld + o + s, ld);
-        q.triA = TRI_UPPER; q.sA = q.sB = q.sC = stride; q.sD = 0;
-        if ((e = gemm_launch<T>(q, batch, st)) != cudaSuccess) return e;
-    }
-    // lower: W = L21 * inv(L11);  L21 <- -inv(L22) * W
-    {
-        auto p = gemm_params<T>(s2, s, s, 1.0, L + (long long)(o + s) * ld + o, ld,
-                                L + (long long)o * ld + o, ld, 0.0, nullptr, ld,
-                                tmp + (long long)(o + s) * ld + o, ld);
-        p.triB = TRI_LOWER; p.sA = p.sB = p.sC = stride; p.sD = 0;
-        if ((e = gemm_launch<T>(p, batch, st)) != cudaSuccess) return e;
-        auto q = gemm_params<T>(s2, s, s2, -1.0, L + (long long)(o + s) * ld + o + s, ld,
-                                tmp + (long long)(o + s) * ld + o, ld, 0.0, nullptr, ld,
-                                L + (long long)(o + s) * ld + o, ld);
-        q.triA = TRI_LOWER; q.sA = q.sB = q.sC = stride; q.sD = 0;
-        if ((e = gemm_launch<T>(q, batch, st)) != cudaSuccess) return e;
-    }
-    return cudaSuccess;
+    // step 1 -- upper: W = U12 * inv(U22);  lower: W = L21 * inv(L11)   (one launch)
+    auto pu = gemm_params<T>(s, s2, s2, 1.0, U + (long long)o * ld + o + s, ld,
+                             U + (long long)(o + s) * ld + o + s, ld, 0.0, nullptr, ld,
+                             tmp + (long long)o * ld + o + s, ld);
+    pu.triB = TRI_UPPER; pu.sA = pu.sB = pu.sC = stride; pu.sD = 0;
+    auto pl = gemm_params<T>(s2, s, s, 1.0, L + (long long)(o + s) * ld + o, ld,
+                             L + (long long)o * ld + o, ld, 0.0, nullptr, ld,
+                             tmp + (long long)(o + s) * ld + o, ld);
+    pl.triB = TRI_LOWER; pl.sA = pl.sB = pl.sC = stride; pl.sD = 0;
+    if ((e = gemm_launch2<T>(pl, batch, pu, do_upper ? batch : 0, st)) != cudaSuccess) return e;
+    // step 2 -- upper: U12 <- -inv(U11) * W;  lower: L21 <- -inv(L22) * W
+    auto qu = gemm_params<T>(s, s2, s, -1.0, U + (long long)o * ld + o, ld,
+                             tmp + (long long)o * ld + o + s, ld, 0.0, nullptr, ld,
+                             U + (long long)o * ld + o + s, ld);
+    qu.triA = TRI_UPPER; qu.sA = qu.sB = qu.sC = stride; qu.sD = 0;
+    auto ql = gemm_params<T>(s2, s, s2, -1.0, L + (long long)(o + s) * ld + o + s, ld,
+                             tmp + (long long)(o + s) * ld + o, ld, 0.0, nullptr, ld,
+                             L + (long long)(o + s) * ld + o, ld);
+    ql.triA = TRI_LOWER; ql.sA = ql.sB = ql.sC = stride; ql.sD = 0;
+    return gemm_launch2<T>(ql, batch, qu, do_upper ? batch : 0, st);
 }
 
 template <typename T>
 cudaError_t inv_from_lu(int n, T *lu, long long ld, T *U, T *L, T *out, long long ldo,
-                        const int *colperm, cudaStream_t s) {
+                        const int *colperm, int *counter, cudaStream_t s) {
     cudaError_t e;
     {
         long long total = (long long)n * n;
@@ -888,10 +915,13 @@ cudaError_t inv_from_lu(int n, T *lu, long long ld, T *U, T *L, T *out, long lon
     p.triA = TRI_UPPER;
     p.triB = TRI_LOWER;
     p.colperm = colperm;
+    // persistent CTAs, longest k-range first (tile (0,0) has k = 0..n): only when the tile
+    // count is comparable to the resident CTAs; larger products balance by themselves
+    p.counter = (n <= 2048) ? counter : nullptr;
     return gemm_launch<T>(p, 1, s);
 }
-template cudaError_t inv_from_lu<double>(int, double *, long long, double *, double *, double *, long long, const int *, cudaStream_t);
-template cudaError_t inv_from_lu<double2>(int, double2 *, long long, double2 *, double2 *, double2 *, long long, const int *, cudaStream_t);
+template cudaError_t inv_from_lu<double>(int, double *, long long, double *, double *, double *, long long, const int *, int *, cudaStream_t);
+template cudaError_t inv_from_lu<double2>(int, double2 *, long long, double2 *, double2 *, double2 *, long long, const int *, int *, cudaStream_t);
 
 
 // =====================================================================================

@@ -43,12 +43,15 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
 // From an LU in `lu` (ld): Xinv = U^{-1} L^{-1} (un-permuted: A^{-1} = Xinv P).
 // Work buffers U, L (n x ld each) are overwritten; `lu` may be used as the
 // recursion scratch (it is destroyed) when lu_is_scratch.
+// counter: device int scratch for the persistent product scheduler (nullable = static grid)
 template <typename T>
 cudaError_t inv_from_lu(int n, T *lu, long long ld, T *U, T *L, T *out, long long ldo,
-                        const int *colperm, cudaStream_t s);
+                        const int *colperm, int *counter, cudaStream_t s);
 
 template <typename T>
 cudaError_t gemm_launch(const GemmParams<T> &p, int batch, cudaStream_t s);
+template <typename T>
+cudaError_t gemm_launch2(const GemmParams<T> &p0, int b0, const GemmParams<T> &p1, int b1, cudaStream_t s);
 
 template <typename T>
 GemmParams<T> gemm_params(int M, int N, int K, double alpha, const T *A, long long lda,

@@ -16,6 +16,8 @@ int main(int argc, char **argv) {
     double *A, *diag, *work, *U, *L, *O;
     int *perm, *mv;
     LuStats *st;
+    int *cnt;
+    cudaMalloc(&cnt, 16);
     cudaMalloc(&A, h.size() * 8); cudaMalloc(&U, h.size() * 8); cudaMalloc(&L, h.size() * 8); cudaMalloc(&O, h.size() * 8);
     cudaMalloc(&diag, n * 8); cudaMalloc(&perm, n * 4); cudaMalloc(&mv, lu_mv_ints(n) * 4);
     cudaMalloc(&work, getrf_work_elems<double>(n) * 8); cudaMalloc(&st, sizeof(LuStats));
@@ -27,7 +29,7 @@ int main(int argc, char **argv) {
         cudaEventRecord(e0);
         getrf<double>(n, A, ld, perm, mv, diag, st, work, 0);
         cudaEventRecord(e1);
-        inv_from_lu<double>(n, A, ld, U, L, O, ld, perm, 0);
+        inv_from_lu<double>(n, A, ld, U, L, O, ld, perm, cnt, 0);
         cudaEventRecord(e2);
         cudaEventSynchronize(e2);
         float ms1, ms2;
