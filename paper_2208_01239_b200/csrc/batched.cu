@@ -66,9 +66,11 @@ FROB_DEV void gj_sweep(T (&a)[BR][BC], int n, SweepShared<T, N> &sh, double &pma
     const int tid = threadIdx.x, lane = tid & 31;
     const int ti = tid / G::CT, tj = tid % G::CT;
     const int r0 = ti * BR, c0 = tj * BC;
-    unsigned long long used0 = 0, used1 = 0;  // rows already used as pivots (N <= 128)
-    pmax = 0.0;
-    pmin = INFINITY;
+    // loop-carried state is kept small (the 1024-thread n = 128 kernel has 64 registers):
+    // used rows live in shared memory (pos[] doubles as the flag array), pivot magnitudes
+    // are reduced after the loop
+    for (int k = tid; k < N; k += G::THREADS) sh.pos[k] = 0;
+    __syncthreads();
     for (int k = 0; k < n; ++k) {
         const int par = k & 1;
         if (tj == k / BC) {
@@ -80,8 +82,7 @@ FROB_DEV void gj_sweep(T (&a)[BR][BC], int n, SweepShared<T, N> &sh, double &pma
                 const int r = r0 + q;
                 const T v = sel_k<T, BC>(a[q], cc);
                 sh.colk[par][r] = v;
-                const bool u = (r < 64) ? ((used0 >> r) & 1ull) : ((used1 >> (r - 64)) & 1ull);
-                if (r < n && !u) {
+                if (r < n && !sh.pos[r]) {
                     const unsigned long long kk = pkey_bits(v);
                     if (kk > bk) { bk = kk; bi = r; }
                 }
@@ -94,12 +95,8 @@ FROB_DEV void gj_sweep(T (&a)[BR][BC], int n, SweepShared<T, N> &sh, double &pma
                                           lane < G::RT ? sh.candi[par][lane] : INT_MAX);
         const int p = m.i;
         const T piv = sh.colk[par][p];
-        const double mag = pmag(piv);
-        pmax = fmax(pmax, mag);
-        pmin = fmin(pmin, mag);
         const T ip = is_zero(piv) ? zero_of(T()) : recip(piv);
-        if (p < 64) used0 |= 1ull << p; else used1 |= 1ull << (p - 64);
-        if (tid == 0) { sh.pivrow[k] = p; sh.pmag_k[k] = mag; }
+        if (tid == 0) { sh.pivrow[k] = p; sh.pmag_k[k] = pmag(piv); sh.pos[p] = 1; }
         if (ti == p / BR) {
             const int q = p % BR;
 #pragma unroll
@@ -130,6 +127,12 @@ FROB_DEV void gj_sweep(T (&a)[BR][BC], int n, SweepShared<T, N> &sh, double &pma
         }
     }
     __syncthreads();
+    pmax = 0.0;
+    pmin = INFINITY;
+    for (int k = 0; k < n; ++k) {
+        pmax = fmax(pmax, sh.pmag_k[k]);
+        pmin = fmin(pmin, sh.pmag_k[k]);
+    }
     for (int k = tid; k < N; k += G::THREADS)
         if (k >= n) sh.pivrow[k] = k;
     __syncthreads();
@@ -185,7 +188,7 @@ FROB_DEV int sweep_info(const SweepShared<T, N> &sh, int n, double pmax) {
 template <int N> struct WT;
 template <> struct WT<32> { static constexpr int WGM = 2, WGN = 1, MT = 2, NT = 4; };
 template <> struct WT<64> { static constexpr int WGM = 2, WGN = 4, MT = 4, NT = 2; };
-template <> struct WT<128> { static constexpr int WGM = 2, WGN = 8, MT = 4, NT = 2; };  // per 64-row half
+template <> struct WT<128> { static constexpr int WGM = 4, WGN = 8, MT = 2, NT = 2; };  // per 64-row half, 32 warps
 
 // acc = op_A * op_B over an N x N x N product with operands given by accessors
 // fa(row, k) and fb(k, col) (shared or global memory; DMMA fragments loaded directly).
@@ -355,7 +358,59 @@ struct Frob128Smem {
     SweepShared<double, 128> sw;
 };
 
-__global__ void __launch_bounds__(512)
+// Steps a3..a7 for a fixed branch (USE = 1: X = A, Y = B; USE = 2: X = B, Y = -A), so the
+// sign of Y is a compile-time property of the operand accessors.
+template <int USE>
+FROB_DEV void frob128_rest(const double2 *__restrict__ Zb, double2 *__restrict__ Xb, int n, double *S, double *Cg,
+                           SweepShared<double, 128> &sw, int &inf_m) {
+    constexpr int N = 128, SS = 132;
+    auto Yv = [&](int i, int j) {
+        if (i >= n || j >= n) return 0.0;
+        return (USE == 1) ? Zb[i * n + j].y : -Zb[i * n + j].x;
+    };
+    auto Xv = [&](int i, int j) { return (USE == 1) ? Zb[i * n + j].x : Zb[i * n + j].y; };
+    double acc[WT<N>::MT][WT<N>::NT][2];
+    // a3: C = X^{-1} Y -> Cg   (two 64-row halves to bound register use)
+    for (int h = 0; h < 2; ++h) {
+        cta_mma_f<N>([&](int r, int k) { return S[r * SS + k]; }, Yv, acc, 64 * h);
+        cta_mma_foreach<N>(acc, [&](int i, int j, double v) {
+            if (i < n && j < n) Cg[i * n + j] = v;
+        }, 64 * h);
+    }
+    __syncthreads();
+    // a4: M = X + Y C -> S
+    for (int h = 0; h < 2; ++h) {
+        cta_mma_f<N>(Yv, [&](int k, int c) { return (k < n && c < n) ? Cg[k * n + c] : 0.0; }, acc, 64 * h);
+        cta_mma_foreach<N>(acc, [&](int i, int j, double v) { S[i * SS + j] = (i < n && j < n) ? Xv(i, j) + v : 0.0; },
+                           64 * h);
+    }
+    __syncthreads();
+    // a5: Re = M^{-1} -> S
+    {
+        double a[4][4];
+        double pmax, pmin;
+        load_blocks_f<double, N, 4, 4>(a, n, [&](int i, int j) { return S[i * SS + j]; });
+        gj_sweep<double, N, 4, 4>(a, n, sw, pmax, pmin);
+        inf_m = sweep_info<double, N>(sw, n, pmax);
+        sweep_store<double, N, 4, 4>(a, sw, S, SS);
+    }
+    __syncthreads();
+    // a6/a7: Im = -C Re, interleaved store (after every warp has finished reading its C rows)
+    auto out = [&](int i, int j, double v) {
+        if (i < n && j < n) {
+            const double re = S[i * SS + j];
+            Xb[i * n + j] = (USE == 1) ? make_double2(re, -v) : make_double2(-v, -re);
+        }
+    };
+    for (int h = 0; h < 2; ++h) {
+        cta_mma_f<N>([&](int r, int k) { return (r < n && k < n) ? Cg[r * n + k] : 0.0; },
+                     [&](int k, int c) { return S[k * SS + c]; }, acc, 64 * h);
+        __syncthreads();
+        cta_mma_foreach<N>(acc, out, 64 * h);
+    }
+}
+
+__global__ void __launch_bounds__(1024)
 frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__restrict__ X, long long sX, int n,
                        int branch, int *__restrict__ info, unsigned char *__restrict__ bused) {
     constexpr int N = 128, SS = 132;
@@ -370,73 +425,40 @@ frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
     // epilogue for rows < 64 (bytes [0, 1024 n)) never clobbers C rows >= 64 (n >= 64)
     double *Cg = reinterpret_cast<double *>(Xb) + (long long)n * n;
 
-    double a[4][8];
-    double pmax, pmin;
     int use = (branch == FROB_BRANCH_B) ? 2 : 1;
-    if (use == 1) load_blocks_f<double, N, 4, 8>(a, n, [&](int i, int j) { return Zb[i * n + j].x; });
-    else load_blocks_f<double, N, 4, 8>(a, n, [&](int i, int j) { return Zb[i * n + j].y; });
-    gj_sweep<double, N, 4, 8>(a, n, sm.sw, pmax, pmin);
-    int inf_x = sweep_info<double, N>(sm.sw, n, pmax);
-    sweep_store<double, N, 4, 8>(a, sm.sw, S, SS);
-    if (branch == FROB_BRANCH_AUTO) {
-        const double rho_a = (pmin > 0.0) ? pmax / pmin : INFINITY;
-        if (inf_x != 0 || !(rho_a <= 256.0)) {
-            __syncthreads();
-            load_blocks_f<double, N, 4, 8>(a, n, [&](int i, int j) { return Zb[i * n + j].y; });
-            double qmax, qmin;
-            gj_sweep<double, N, 4, 8>(a, n, sm.sw, qmax, qmin);
-            const int inf_b = sweep_info<double, N>(sm.sw, n, qmax);
-            const double rho_b = (qmin > 0.0) ? qmax / qmin : INFINITY;
-            if (inf_b == 0 && (inf_x != 0 || rho_b < rho_a)) {
-                use = 2;
-                inf_x = 0;
+    int inf_x;
+    {
+        double a[4][4];
+        double pmax, pmin;
+        if (use == 1) load_blocks_f<double, N, 4, 4>(a, n, [&](int i, int j) { return Zb[i * n + j].x; });
+        else load_blocks_f<double, N, 4, 4>(a, n, [&](int i, int j) { return Zb[i * n + j].y; });
+        gj_sweep<double, N, 4, 4>(a, n, sm.sw, pmax, pmin);
+        inf_x = sweep_info<double, N>(sm.sw, n, pmax);
+        sweep_store<double, N, 4, 4>(a, sm.sw, S, SS);
+        if (branch == FROB_BRANCH_AUTO) {
+            const double rho_a = (pmin > 0.0) ? pmax / pmin : INFINITY;
+            if (inf_x != 0 || !(rho_a <= 256.0)) {
                 __syncthreads();
-                sweep_store<double, N, 4, 8>(a, sm.sw, S, SS);
-            } else if (inf_b != 0 && inf_x != 0) {
-                inf_x = -1;
+                load_blocks_f<double, N, 4, 4>(a, n, [&](int i, int j) { return Zb[i * n + j].y; });
+                double qmax, qmin;
+                gj_sweep<double, N, 4, 4>(a, n, sm.sw, qmax, qmin);
+                const int inf_b = sweep_info<double, N>(sm.sw, n, qmax);
+                const double rho_b = (qmin > 0.0) ? qmax / qmin : INFINITY;
+                if (inf_b == 0 && (inf_x != 0 || rho_b < rho_a)) {
+                    use = 2;
+                    inf_x = 0;
+                    __syncthreads();
+                    sweep_store<double, N, 4, 4>(a, sm.sw, S, SS);
+                } else if (inf_b != 0 && inf_x != 0) {
+                    inf_x = -1;
+                }
             }
         }
     }
     __syncthreads();
-    const double sgn = (use == 1) ? 1.0 : -1.0;
-    const bool ya = (use == 2);  // Y = A (imag part otherwise)
-    auto Yv = [&](int i, int j) { return (i < n && j < n) ? sgn * (ya ? Zb[i * n + j].x : Zb[i * n + j].y) : 0.0; };
-    auto Xv = [&](int i, int j) { return ya ? Zb[i * n + j].y : Zb[i * n + j].x; };
-    double acc[WT<N>::MT][WT<N>::NT][2];
-    // a3: C = X^{-1} (sgn Y) -> Cg   (two 64-row halves to bound register use)
-    for (int h = 0; h < 2; ++h) {
-        cta_mma_f<N>([&](int r, int k) { return S[r * SS + k]; }, Yv, acc, 64 * h);
-        cta_mma_foreach<N>(acc, [&](int i, int j, double v) {
-            if (i < n && j < n) Cg[i * n + j] = v;
-        }, 64 * h);
-    }
-    __syncthreads();
-    // a4: M = X + (sgn Y) C -> S
-    for (int h = 0; h < 2; ++h) {
-        cta_mma_f<N>(Yv, [&](int k, int c) { return (k < n && c < n) ? Cg[k * n + c] : 0.0; }, acc, 64 * h);
-        cta_mma_foreach<N>(acc, [&](int i, int j, double v) { S[i * SS + j] = (i < n && j < n) ? Xv(i, j) + v : 0.0; },
-                           64 * h);
-    }
-    __syncthreads();
-    // a5: Re = M^{-1} -> S
-    load_blocks_f<double, N, 4, 8>(a, n, [&](int i, int j) { return S[i * SS + j]; });
-    gj_sweep<double, N, 4, 8>(a, n, sm.sw, pmax, pmin);
-    const int inf_m = sweep_info<double, N>(sm.sw, n, pmax);
-    sweep_store<double, N, 4, 8>(a, sm.sw, S, SS);
-    __syncthreads();
-    // a6/a7: Im = -C Re, interleaved store (after every warp has finished reading Cg)
-    auto out = [&](int i, int j, double v) {
-        if (i < n && j < n) {
-            const double re = S[i * SS + j];
-            Xb[i * n + j] = (use == 1) ? make_double2(re, -v) : make_double2(-v, -re);
-        }
-    };
-    for (int h = 0; h < 2; ++h) {
-        cta_mma_f<N>([&](int r, int k) { return (r < n && k < n) ? Cg[r * n + k] : 0.0; },
-                     [&](int k, int c) { return S[k * SS + c]; }, acc, 64 * h);
-        __syncthreads();  // every warp has read the C rows of this half
-        cta_mma_foreach<N>(acc, out, 64 * h);
-    }
+    int inf_m = 0;
+    if (use == 1) frob128_rest<1>(Zb, Xb, n, S, Cg, sm.sw, inf_m);
+    else frob128_rest<2>(Zb, Xb, n, S, Cg, sm.sw, inf_m);
     if (tid == 0) {
         info[b] = (inf_x < 0) ? 1 : (inf_x ? inf_x : inf_m);
         if (bused) bused[b] = (inf_x < 0) ? 0 : (unsigned char)use;
@@ -525,7 +547,7 @@ frob_status frob_inv_batched(int n, int batch, const double *Z, long long stride
         const size_t smem = sizeof(Frob128Smem);
         if ((e = set_smem(frob_batched128_kernel, smem)) != cudaSuccess) return FROB_ERR_CUDA;
         count_launch();
-        frob_batched128_kernel<<<batch, 512, smem, s>>>(Zc, strideZ, Xc, strideX, n, branch, d_info,
+        frob_batched128_kernel<<<batch, 1024, smem, s>>>(Zc, strideZ, Xc, strideX, n, branch, d_info,
                                                          d_branch_used);
     }
     return cudaGetLastError() == cudaSuccess ? FROB_OK : FROB_ERR_CUDA;

@@ -40,6 +40,20 @@ int main(int argc, char **argv) {
         printf(" | tail %lld | store %lld\n", tr[40] - tr[17], tr[41] - tr[40]);
         printf("   col5: pre-bar %lld, bar %lld, bargmax %lld, u-load %lld, next-slot+cand %lld, rest-update %lld, publish %lld\n", tr[50] - tr[6], tr[51] - tr[50], tr[52] - tr[51], tr[53] - tr[52], tr[54] - tr[53], tr[55] - tr[54], tr[7] - tr[55]);
     }
+    // 1a) traced cluster panel (R1, CS = n/256)
+    if (n > 1024) {
+        for (int rep = 0; rep < 2; ++rep) {
+            cudaMemcpy(A, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+            launch_panel_r<double, 16, 1>(A, ld, n, 16, 0, mv, diag, (n + 255) / 256, 0);
+            cudaDeviceSynchronize();
+            long long tr[64];
+            cudaMemcpyFromSymbol(tr, g_panel_trace, sizeof(tr));
+            printf("cluster panel: load %lld | cols:", tr[1] - tr[0]);
+            for (int j = 0; j < 16; ++j) printf(" %lld", tr[2 + j] - (j ? tr[1 + j] : tr[1]));
+            printf(" | store %lld\n   col5: bar %lld, bargmax %lld, ->push %lld, push %lld, wait %lld, after-wait->u %lld\n",
+                   tr[41] - tr[40], tr[51] - tr[50], tr[52] - tr[51], tr[60] - tr[52], tr[61] - tr[60], tr[62] - tr[61], tr[53] - tr[62]);
+        }
+    }
     // 1b) cluster variants for the same panel
     {
         auto tp = [&](const char *nm, auto fn) {
@@ -97,7 +111,7 @@ int main(int argc, char **argv) {
         for (int r = 0; r < 3; ++r) {
             getrf<double>(n, A, ld, perm, mv, diag, st, work, 0);
             cudaEventRecord(e0);
-            inv_from_lu<double>(n, A, ld, U, L, O, ld, perm, 0);
+            inv_from_lu<double>(n, A, ld, U, L, O, ld, perm, nullptr, 0);
             cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
             printf("inv_from_lu n=%d: %.1f us\n", n, ms * 1e3);
         }
