@@ -38,6 +38,8 @@ struct GemmParams {
     int triA, triB, epi;
     int *counter;                    // non-null: persistent CTAs take tiles from this counter,
                                      // longest k-range first (square triangular products)
+    int early_trigger;               // set by the launcher: release dependents at entry
+                                     // (single-wave grids) instead of after the main loop
 };
 
 // Up to two independent problems in one launch (blockIdx.z < zsplit -> q[0], else q[1]).
@@ -47,19 +49,26 @@ struct GemmPair {
     int zsplit;
 };
 
-template <typename T> struct GemmCfg;
-template <> struct GemmCfg<double> {
+// BIG = 0: 64 x 64 tiles (4 warps of 32 x 32), several CTAs per SM -- small / medium problems;
+// BIG = 1: 128 x 128 tiles (8 warps of 64 x 32), one CTA per SM, fewer shared loads per DMMA --
+// large problems (>= 2 waves of tiles).
+template <typename T, int BIG = 0> struct GemmCfg;
+template <> struct GemmCfg<double, 0> {
     static constexpr int BM = 64, BN = 64, BK = 16, WGM = 2, WGN = 2, STAGES = 3;
     static constexpr int PADA = 4, PADB = 4;
 };
-template <> struct GemmCfg<double2> {
+template <> struct GemmCfg<double, 1> {
+    static constexpr int BM = 128, BN = 128, BK = 16, WGM = 2, WGN = 4, STAGES = 3;
+    static constexpr int PADA = 4, PADB = 4;
+};
+template <int BIG> struct GemmCfg<double2, BIG> {
     static constexpr int BM = 64, BN = 64, BK = 8, WGM = 2, WGN = 4, STAGES = 3;
     static constexpr int PADA = 4, PADB = 2;
 };
 
-template <typename T>
+template <typename T, int BIG = 0>
 constexpr size_t gemm_smem_bytes() {
-    using C = GemmCfg<T>;
+    using C = GemmCfg<T, BIG>;
     return (size_t)C::STAGES * ((size_t)C::BM * (C::BK + C::PADA) + (size_t)C::BK * (C::BN + C::PADB)) * sizeof(T);
 }
 
@@ -93,9 +102,9 @@ template <> struct AccW<double2> { static constexpr int V = 4; };
 FROB_DEV double acc_val(const double (&c)[2], int e) { return c[e]; }
 FROB_DEV double2 acc_val(const double (&c)[4], int e) { return make_double2(c[e], c[2 + e]); }
 
-template <typename T, bool VEC>
+template <typename T, bool VEC, int BIG>
 FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int row0, const int col0, T *As, T *Bs) {
-    using Cf = GemmCfg<T>;
+    using Cf = GemmCfg<T, BIG>;
     constexpr int BM = Cf::BM, BN = Cf::BN, BK = Cf::BK, STAGES = Cf::STAGES;
     constexpr int NTH = Cf::WGM * Cf::WGN * 32;
     constexpr int WM = BM / Cf::WGM, WN = BN / Cf::WGN, MT = WM / 8, NT = WN / 8;
@@ -193,6 +202,7 @@ FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int ro
         }
     }
     cp_async_wait<0>();
+    if (!p.counter && !p.early_trigger) pdl_trigger();
 
     // ------------------------------------------------------------ epilogue
     // All reads of D (which may alias C) and of colperm are issued before any store so
@@ -207,32 +217,31 @@ FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int ro
                               (!D || (reinterpret_cast<uintptr_t>(D) & 15) == 0);
         if (interior) {
             const double alpha = p.alpha, beta = p.beta;
-            double2 dv2[MT][NT];
-            if (beta != 0.0) {
 #pragma unroll
-                for (int i = 0; i < MT; ++i)
+            for (int i = 0; i < MT; ++i) {
+                // D loads of one row group are issued together, before its stores
+                double2 dv2[NT];
+                if (beta != 0.0) {
 #pragma unroll
                     for (int j = 0; j < NT; ++j)
-                        dv2[i][j] = *reinterpret_cast<const double2 *>(
+                        dv2[j] = *reinterpret_cast<const double2 *>(
                             D + (long long)(row0 + wm0 + i * 8 + g) * p.ldd + col0 + wn0 + j * 8 + 2 * t);
-            }
-#pragma unroll
-            for (int i = 0; i < MT; ++i)
+                }
 #pragma unroll
                 for (int j = 0; j < NT; ++j) {
                     double2 v = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
                     if (beta != 0.0) {
-                        v.x = fma(beta, dv2[i][j].x, v.x);
-                        v.y = fma(beta, dv2[i][j].y, v.y);
+                        v.x = fma(beta, dv2[j].x, v.x);
+                        v.y = fma(beta, dv2[j].y, v.y);
                     }
                     *reinterpret_cast<double2 *>(Cp + (long long)(row0 + wm0 + i * 8 + g) * p.ldc + col0 + wn0 +
                                                  j * 8 + 2 * t) = v;
                 }
+            }
             return;
         }
     }
     const bool needD = (p.epi != EPI_STORE) || (p.beta != 0.0);
-    T dv[MT][NT][2];
     int oc[NT][2];
 #pragma unroll
     for (int j = 0; j < NT; ++j)
@@ -244,18 +253,15 @@ FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int ro
 #pragma unroll
     for (int i = 0; i < MT; ++i) {
         const int row = row0 + wm0 + i * 8 + g;
+        if (row >= M) continue;
+        T dv[NT][2];
 #pragma unroll
         for (int j = 0; j < NT; ++j)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int col = col0 + wn0 + j * 8 + 2 * t + e;
-                dv[i][j][e] = (needD && row < M && col < N) ? D[(long long)row * p.ldd + col] : zero_of(T());
+                dv[j][e] = (needD && col < N) ? D[(long long)row * p.ldd + col] : zero_of(T());
             }
-    }
-#pragma unroll
-    for (int i = 0; i < MT; ++i) {
-        const int row = row0 + wm0 + i * 8 + g;
-        if (row >= M) continue;
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
 #pragma unroll
@@ -265,35 +271,37 @@ FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int ro
                 T v = scal(acc_val(acc[i][j], e), p.alpha);
                 if constexpr (sizeof(T) == 8) {
                     if (p.epi != EPI_STORE) {
-                        const double d = dv[i][j][e];
+                        const double d = dv[j][e];
                         double2 *X = reinterpret_cast<double2 *>(Cp);
                         X[(long long)row * p.ldc + oc[j][e]] =
                             (p.epi == EPI_FROB_A) ? make_double2(d, v) : make_double2(v, -d);
                         continue;
                     }
                 }
-                if (p.beta != 0.0) v = add(v, scal(dv[i][j][e], p.beta));
+                if (p.beta != 0.0) v = add(v, scal(dv[j][e], p.beta));
                 Cp[(long long)row * p.ldc + oc[j][e]] = v;
             }
         }
     }
 }
 
-template <typename T, bool VEC>
-__global__ void __launch_bounds__(GemmCfg<T>::WGM * GemmCfg<T>::WGN * 32)
+template <typename T, bool VEC, int BIG>
+__global__ void __launch_bounds__(GemmCfg<T, BIG>::WGM * GemmCfg<T, BIG>::WGN * 32)
 gemm_kernel(GemmPair<T> pp) {
-    using Cf = GemmCfg<T>;
+    using Cf = GemmCfg<T, BIG>;
     constexpr int SA = Cf::BK + Cf::PADA;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T *As = reinterpret_cast<T *>(smem_raw);
     T *Bs = As + Cf::STAGES * Cf::BM * SA;
-    pdl_trigger();
+    // multi-wave grids release dependents only after the main loop (see gemm_tile): releasing
+    // them at entry lets the next grid's waiting CTAs occupy SM slots this GEMM still needs
+    if (pp.q[0].early_trigger) pdl_trigger();
     pdl_wait();
     const int z = blockIdx.z;
     const GemmParams<T> &p = (z < pp.zsplit) ? pp.q[0] : pp.q[1];
     const long long bz = (z < pp.zsplit) ? z : z - pp.zsplit;
     if (!p.counter) {
-        gemm_tile<T, VEC>(p, bz, blockIdx.y * Cf::BM, blockIdx.x * Cf::BN, As, Bs);
+        gemm_tile<T, VEC, BIG>(p, bz, blockIdx.y * Cf::BM, blockIdx.x * Cf::BN, As, Bs);
         return;
     }
     // persistent: tiles in order of max(I, J) = 0, 1, ... (longest k-range first for
@@ -306,14 +314,14 @@ gemm_kernel(GemmPair<T> pp) {
         if (threadIdx.x == 0) tile_s = atomicAdd(p.counter, 1);
         __syncthreads();
         const int tt = tile_s;
-        if (tt >= total) break;
+        if (tt >= total) { pdl_trigger(); break; }
         int d = (int)sqrtf((float)tt);
         while (d * d > tt) --d;
         while ((d + 1) * (d + 1) <= tt) ++d;
         const int r = tt - d * d;
         const int I = (r <= d) ? d : r - d - 1;
         const int J = (r <= d) ? r : d;
-        gemm_tile<T, VEC>(p, bz, I * Cf::BM, J * Cf::BN, As, Bs);
+        gemm_tile<T, VEC, BIG>(p, bz, I * Cf::BM, J * Cf::BN, As, Bs);
     }
 }
 

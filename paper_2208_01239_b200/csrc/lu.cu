@@ -3,6 +3,7 @@
 #include <cooperative_groups.h>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <utility>
 #include <type_traits>
 #include <mutex>
@@ -15,15 +16,15 @@ namespace frob {
 // =====================================================================================
 // GEMM launcher
 // =====================================================================================
-template <typename T, bool VEC>
-static cudaError_t gemm_launch_impl(const GemmPair<T> &pp, int batch0, int batch1, cudaStream_t s) {
-    using Cf = GemmCfg<T>;
-    constexpr size_t smem = gemm_smem_bytes<T>();
+template <typename T, bool VEC, int BIG>
+static cudaError_t gemm_launch_cfg(const GemmPair<T> &pp, int batch0, int batch1, cudaStream_t s) {
+    using Cf = GemmCfg<T, BIG>;
+    constexpr size_t smem = gemm_smem_bytes<T, BIG>();
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !attr_set[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_kernel<T, VEC>,
+        cudaError_t e = cudaFuncSetAttribute(gemm_kernel<T, VEC, BIG>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr_set[dev] = true;
@@ -34,7 +35,7 @@ static cudaError_t gemm_launch_impl(const GemmPair<T> &pp, int batch0, int batch
         const int grid = min(D * D, 148 * 3);
         cudaError_t e = cudaMemsetAsync(p0.counter, 0, sizeof(int), s);
         if (e != cudaSuccess) return e;
-        return launch_pdl(gemm_kernel<T, VEC>, dim3(grid, 1, 1), dim3(Cf::WGM * Cf::WGN * 32), smem, s, pp);
+        return launch_pdl(gemm_kernel<T, VEC, BIG>, dim3(grid, 1, 1), dim3(Cf::WGM * Cf::WGN * 32), smem, s, pp);
     }
     int M = p0.M, N = p0.N;
     if (batch1 > 0) {
@@ -42,7 +43,29 @@ static cudaError_t gemm_launch_impl(const GemmPair<T> &pp, int batch0, int batch
         N = max(N, pp.q[1].N);
     }
     dim3 grid((N + Cf::BN - 1) / Cf::BN, (M + Cf::BM - 1) / Cf::BM, batch0 + batch1);
-    return launch_pdl(gemm_kernel<T, VEC>, grid, dim3(Cf::WGM * Cf::WGN * 32), smem, s, pp);
+    GemmPair<T> q = pp;
+    const long long ctas = (long long)grid.x * grid.y * grid.z;
+    // policy (tuning aid, env FROB_PDL_GEMM): 0 = release after the main loop, 1 = early for
+    // single-wave grids, 2 = always early; default 0 (measured best)
+    static int policy = [] {
+        const char *v = getenv("FROB_PDL_GEMM");
+        return v ? atoi(v) : 0;
+    }();
+    const bool early = policy == 2 || (policy == 1 && ctas <= 148LL * (BIG ? 1 : 3));
+    q.q[0].early_trigger = q.q[1].early_trigger = early ? 1 : 0;
+    return launch_pdl(gemm_kernel<T, VEC, BIG>, grid, dim3(Cf::WGM * Cf::WGN * 32), smem, s, q);
+}
+
+template <typename T, bool VEC>
+static cudaError_t gemm_launch_impl(const GemmPair<T> &pp, int batch0, int batch1, cudaStream_t s) {
+    // 128 x 128 tiles when they fill >= 2 waves of the 148 SMs (real only)
+    const GemmParams<T> &p0 = pp.q[0];
+    long long tiles = (long long)((p0.M + 127) / 128) * ((p0.N + 127) / 128) * batch0;
+    if (batch1 > 0) tiles += (long long)((pp.q[1].M + 127) / 128) * ((pp.q[1].N + 127) / 128) * batch1;
+    // (measured: the 128 x 128 variant runs one CTA per SM and is slower than 3 x 64 x 64 per SM;
+    //  kept compiled for experiments, not selected)
+    if (sizeof(T) == 8 && !p0.counter && tiles >= (1LL << 40)) return gemm_launch_cfg<T, VEC, 1>(pp, batch0, batch1, s);
+    return gemm_launch_cfg<T, VEC, 0>(pp, batch0, batch1, s);
 }
 
 static bool aligned16(const void *ptr) { return ((uintptr_t)ptr & 15u) == 0; }
