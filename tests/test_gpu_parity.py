@@ -282,3 +282,45 @@ def test_polar_small():
     u, h, it, d = fb.polar(_t(a), tol=1e-13)
     u, h = _np(u), _np(h)
     assert oracle.rel_fro(u, q) <= 1e-11 and oracle.rel_fro(h, h0) <= 1e-11
+
+
+# ------------------------------------------------------------------ full-size configs 4 and 5
+def test_config4_sign_full_size():
+    """BASELINE config 4 at full size (n=2048): Newton sign with Frobenius and with complex LU,
+    against the closed form S sign(Re lambda) S^{-1} built from the generator's own S^{-1}."""
+    z, s, lam, sinv = synth.sign_instance(2048, seed=0)
+    ref = _t((s * np.sign(lam.real)[None, :]) @ sinv)
+    zt = _t(z)
+    eye = torch.eye(2048, dtype=torch.complex128, device=DEV)
+    for m in ("frobenius", "zlu"):
+        st, it, d = fb.sign(zt, tol=1e-12, max_iter=50, method=m)
+        rel = float(torch.linalg.norm(st - ref) / torch.linalg.norm(ref))
+        assert it < 50 and d < 1e-12, (m, it, d)
+        assert rel <= 1e-10, (m, rel)
+        # invariants with independent library GEMMs: S^2 = I, S Z = Z S
+        assert float(torch.linalg.norm(st @ st - eye)) <= 1e-9
+        assert float(torch.linalg.norm(st @ zt - zt @ st) / torch.linalg.norm(zt)) <= 1e-10
+
+
+@pytest.mark.parametrize("n", [4096, 16384])
+def test_config5_large_sampled_columns(n):
+    """BASELINE config 5 generator at large n (in bench.py's launch configuration: frob_inv, AUTO).
+    The oracle cannot afford O(n^3) here, so sampled columns are checked by a property that
+    holds at any size: ||Z x_j - e_j|| computed in fp64 on the host (plain matvec), plus the
+    full residual with an independent library GEMM at n = 4096."""
+    z = synth.config2(n, seed=0)
+    zt = _t(z)
+    x, info = fb.inv(zt, info=True)
+    assert info["info"] == 0
+    rng = np.random.default_rng(n)
+    cols = rng.choice(n, size=6, replace=False)
+    xs = x[:, torch.from_numpy(cols).to(DEV)].cpu().numpy()
+    for k, j in enumerate(cols):
+        r = z @ xs[:, k]
+        r[j] -= 1.0
+        assert np.linalg.norm(r) <= 1e-11 * n, (j, np.linalg.norm(r))
+    if n <= 4096:
+        xz = fb.zinv(zt)
+        res = float(torch.linalg.norm(zt @ x - torch.eye(n, dtype=torch.complex128, device=DEV)))
+        assert res <= 1e-11 * n
+        assert float(torch.linalg.norm(x - xz) / torch.linalg.norm(xz)) <= 1e-9
