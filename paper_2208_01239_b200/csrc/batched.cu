@@ -47,6 +47,16 @@ FROB_DEV T sel_k(const T (&v)[K], int idx) {
 
 // shared state of the sweep (double-buffered by step parity)
 template <typename T, int N>
+struct SweepShared1 {
+    T slot[2][N / 4][N];   // each block-row's candidate row (double-buffered by step parity)
+    unsigned long long candk[2][32];
+    int candi[2][32];
+    int pivrow[N];
+    int pos[N];
+    double pmag_k[N];
+};
+
+template <typename T, int N>
 struct SweepShared {
     T colk[2][N];
     T rowp[2][N];
@@ -140,9 +150,90 @@ FROB_DEV void gj_sweep(T (&a)[BR][BC], int n, SweepShared<T, N> &sh, double &pma
     __syncthreads();
 }
 
-// write the sweep result as the inverse into a row-major matrix M (stride ldm)
+// One barrier per step.  Thread (ti, tj) owns rows ti*BR.., columns tj*BC..; the CT threads
+// of a block-row are consecutive lanes of one warp, so the column-k values of a block-row come
+// by shuffle from the lane owning column block k/BC.  Each block-row publishes its best row
+// for column k (with the candidate) before the barrier; after it, the pivot row is read from
+// the winning block-row's slot, so no second barrier is needed.
 template <typename T, int N, int BR, int BC>
-FROB_DEV void sweep_store(const T (&a)[BR][BC], const SweepShared<T, N> &sh, T *M, int ldm) {
+FROB_DEV void gj_sweep_1bar(T (&a)[BR][BC], int n, SweepShared1<T, N> &sh, double &pmax, double &pmin) {
+    using G = Geo<N, BR, BC>;
+    static_assert(BR == 4, "slot layout assumes 4-row blocks");
+    static_assert((G::CT & (G::CT - 1)) == 0 && G::CT <= 32, "block-rows must be lane groups");
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int ti = tid / G::CT, tj = tid % G::CT;
+    const int r0 = ti * BR, c0 = tj * BC;
+    const int gbase = lane & ~(G::CT - 1);  // first lane of my block-row group
+    unsigned used = 0;                      // my rows already used as pivots
+    for (int k = 0; k < n; ++k) {
+        const int par = k & 1;
+        const int kb = k / BC, kc = k % BC;
+        // column-k values of my block-row (before this step's update)
+        T ck[BR];
+#pragma unroll
+        for (int q = 0; q < BR; ++q) ck[q] = shfl(sel_k<T, BC>(a[q], kc), gbase + kb);
+        unsigned long long bk = 0;
+        int qb = 0;
+#pragma unroll
+        for (int q = 0; q < BR; ++q) {
+            if (r0 + q < n && !((used >> q) & 1u)) {
+                const unsigned long long kk = pkey_bits(ck[q]);
+                if (kk > bk) { bk = kk; qb = q; }
+            }
+        }
+        if (tj == 0) {
+            sh.candk[par][ti] = bk;
+            sh.candi[par][ti] = bk ? r0 + qb : INT_MAX;
+        }
+#pragma unroll
+        for (int c = 0; c < BC; ++c) {
+            T v = a[0][c];
+#pragma unroll
+            for (int q = 1; q < BR; ++q)
+                if (qb == q) v = a[q][c];
+            sh.slot[par][ti][c0 + c] = v;
+        }
+        __syncthreads();
+        const ArgMaxK m = warp_argmax_key(lane < G::RT ? sh.candk[par][lane] : 0ull,
+                                          lane < G::RT ? sh.candi[par][lane] : INT_MAX);
+        const int p = m.i;
+        const int tip = p / BR;
+        const T piv = sh.slot[par][tip][k];
+        const T ip = is_zero(piv) ? zero_of(T()) : recip(piv);
+        if (tid == 0) { sh.pivrow[k] = p; sh.pmag_k[k] = pmag(piv); }
+        if (tip == ti) used |= 1u << (p - r0);
+        T rp[BC];
+#pragma unroll
+        for (int c = 0; c < BC; ++c) rp[c] = (c0 + c == k) ? ip : mul(sh.slot[par][tip][c0 + c], ip);
+#pragma unroll
+        for (int q = 0; q < BR; ++q) {
+            if (r0 + q == p) {
+#pragma unroll
+                for (int c = 0; c < BC; ++c) a[q][c] = rp[c];
+            } else {
+#pragma unroll
+                for (int c = 0; c < BC; ++c)
+                    a[q][c] = (c0 + c == k) ? neg(mul(ck[q], rp[c])) : msub(a[q][c], ck[q], rp[c]);
+            }
+        }
+    }
+    __syncthreads();
+    pmax = 0.0;
+    pmin = INFINITY;
+    for (int k = 0; k < n; ++k) {
+        pmax = fmax(pmax, sh.pmag_k[k]);
+        pmin = fmin(pmin, sh.pmag_k[k]);
+    }
+    for (int k = tid; k < N; k += G::THREADS)
+        if (k >= n) sh.pivrow[k] = k;
+    __syncthreads();
+    for (int k = tid; k < N; k += G::THREADS) sh.pos[sh.pivrow[k]] = k;
+    __syncthreads();
+}
+
+// write the sweep result as the inverse into a row-major matrix M (stride ldm)
+template <typename T, int N, int BR, int BC, typename SH>
+FROB_DEV void sweep_store(const T (&a)[BR][BC], const SH &sh, T *M, int ldm) {
     using G = Geo<N, BR, BC>;
     const int tid = threadIdx.x;
     const int r0 = (tid / G::CT) * BR, c0 = (tid % G::CT) * BC;
@@ -175,8 +266,8 @@ FROB_DEV void load_blocks(T (&a)[4][4], const T *M, int n) {
 }
 
 // first 1-based pivot column with |u_kk| < 100 n u max (reading R2), 0 if none
-template <typename T, int N>
-FROB_DEV int sweep_info(const SweepShared<T, N> &sh, int n, double pmax) {
+template <typename T, int N, typename SH>
+FROB_DEV int sweep_info(const SH &sh, int n, double pmax) {
     const double thr = 100.0 * n * 1.1102230246251565e-16 * pmax;
     for (int k = 0; k < n; ++k)
         if (!(sh.pmag_k[k] >= thr) || sh.pmag_k[k] == 0.0) return k + 1;
@@ -471,7 +562,7 @@ frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
 template <int N>
 struct ZSmem {
     double2 buf[N * BCfg<N>::S];
-    SweepShared<double2, N> sw;
+    SweepShared1<double2, N> sw;
 };
 
 template <int N>
@@ -493,7 +584,7 @@ zinv_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__rest
     double2 a[4][4];
     double pmax, pmin;
     load_blocks<double2, N>(a, sm.buf, n);
-    gj_sweep<double2, N, 4, 4>(a, n, sm.sw, pmax, pmin);
+    gj_sweep_1bar<double2, N, 4, 4>(a, n, sm.sw, pmax, pmin);
     const int inf = sweep_info<double2, N>(sm.sw, n, pmax);
     sweep_store<double2, N, 4, 4>(a, sm.sw, sm.buf, C::S);
     __syncthreads();
