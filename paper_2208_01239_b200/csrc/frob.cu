@@ -84,9 +84,9 @@ static int ew_blocks(long long total) {
 
 // ---------------------------------------------------------------------- workspace
 struct FrobWs {
-    double *A, *B, *W1, *W2, *W3, *W4, *W5;
+    double *A, *B, *W1, *W2, *W3, *W4, *W5, *W6, *W7;  // W6, W7: n <= LU2_MAX_N only
     double *diag, *work;
-    int *perm_x, *perm_b, *perm_m, *mv;
+    int *perm_x, *perm_b, *perm_m, *mv, *iw;
     LuStats *stats;   // [0] A, [1] B, [2] M
     int *flags;       // [0] nonfinite
     size_t bytes;
@@ -103,12 +103,16 @@ static FrobWs carve_frob(void *ws, int n) {
     w.W3 = c.take<double>((size_t)n * ld);
     w.W4 = c.take<double>((size_t)n * ld);
     w.W5 = c.take<double>((size_t)n * ld);
+    const bool small = n <= LU2_MAX_N;
+    w.W6 = small ? c.take<double>((size_t)n * ld) : nullptr;
+    w.W7 = small ? c.take<double>((size_t)n * ld) : nullptr;
     w.diag = c.take<double>((size_t)n);
     w.work = c.take<double>(getrf_work_elems<double>(n));
     w.perm_x = c.take<int>((size_t)n);
     w.perm_b = c.take<int>((size_t)n);
     w.perm_m = c.take<int>((size_t)n);
     w.mv = c.take<int>(lu_mv_ints(n));
+    w.iw = small ? c.take<int>(lu2_int_elems(n)) : nullptr;
     w.stats = c.take<LuStats>(3);
     w.flags = c.take<int>(4);
     w.bytes = c.off;
@@ -116,8 +120,8 @@ static FrobWs carve_frob(void *ws, int n) {
 }
 
 struct ZluWs {
-    double2 *W, *U, *L, *diag, *work;
-    int *perm, *mv;
+    double2 *W, *U, *L, *W2, *diag, *work;  // W2: n <= LU2_MAX_N only
+    int *perm, *mv, *iw;
     LuStats *stats;
     int *flags;
     size_t bytes;
@@ -130,10 +134,13 @@ static ZluWs carve_zlu(void *ws, int n) {
     w.W = c.take<double2>((size_t)n * ld);
     w.U = c.take<double2>((size_t)n * ld);
     w.L = c.take<double2>((size_t)n * ld);
+    const bool small = n <= LU2_MAX_N;
+    w.W2 = small ? c.take<double2>((size_t)n * ld) : nullptr;
     w.diag = c.take<double2>((size_t)n);
     w.work = c.take<double2>(getrf_work_elems<double2>(n));
     w.perm = c.take<int>((size_t)n);
     w.mv = c.take<int>(lu_mv_ints(n));
+    w.iw = small ? c.take<int>(lu2_int_elems(n)) : nullptr;
     w.stats = c.take<LuStats>(1);
     w.flags = c.take<int>(4);
     w.bytes = c.off;
@@ -169,7 +176,12 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
     int use = (branch == FROB_BRANCH_B) ? 2 : 1;
     int *perm = w.perm_x;
     double *Xlu = w.W1;
-    FROB_CUDA(getrf<double>(n, Xlu, ld, perm, w.mv, w.diag, &w.stats[use == 1 ? 0 : 1], w.work, s));
+    // n <= LU2_MAX_N: latency-oriented LU (lu2.cu), factors come out split (U, L)
+    const bool small = n <= LU2_MAX_N;
+    double *Uf = w.W2, *Lf = w.W3;
+    if (small) FROB_CUDA(lu2_factor<double>(n, w.W1, w.W4, ld, w.W2, w.W3, ld, perm, w.iw, w.diag,
+                                            &w.stats[use == 1 ? 0 : 1], s));
+    else FROB_CUDA(getrf<double>(n, Xlu, ld, perm, w.mv, w.diag, &w.stats[use == 1 ? 0 : 1], w.work, s));
 
     LuStats hs[3];
     for (auto &h : hs) { h.rho = NAN; h.umax = 0; h.info = 0; h.nonfinite = 0; }
@@ -187,7 +199,9 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
             count_launch();
             copy2d_kernel<double><<<ew_blocks((long long)n * n), 256, 0, s>>>(w.B, ld, w.W5, ld, n, nullptr);
             FROB_CUDA(cudaGetLastError());
-            FROB_CUDA(getrf<double>(n, w.W5, ld, w.perm_b, w.mv, w.diag, &w.stats[1], w.work, s));
+            if (small) FROB_CUDA(lu2_factor<double>(n, w.W5, w.W4, ld, w.W6, w.W7, ld, w.perm_b, w.iw, w.diag,
+                                                    &w.stats[1], s));
+            else FROB_CUDA(getrf<double>(n, w.W5, ld, w.perm_b, w.mv, w.diag, &w.stats[1], w.work, s));
             FROB_CUDA(cudaMemcpyAsync(&hs[1], &w.stats[1], sizeof(LuStats), cudaMemcpyDeviceToHost, s));
             FROB_CUDA(cudaStreamSynchronize(s));
             const bool sa = hs[0].info != 0, sb = hs[1].info != 0;
@@ -202,6 +216,8 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
                 use = 2;
                 perm = w.perm_b;
                 Xlu = w.W5;
+                Uf = w.W6;
+                Lf = w.W7;
             }
         }
     }
@@ -210,7 +226,8 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
     const double sgn = (use == 1) ? 1.0 : -1.0;
 
     // a2: Xinv' = U^{-1} L^{-1}  (X^{-1} = Xinv' P)
-    FROB_CUDA(inv_from_lu<double>(n, Xlu, ld, w.W2, w.W3, w.W4, ld, nullptr, w.flags + 2, s));
+    if (small) FROB_CUDA(inv_from_ul<double>(n, Uf, Lf, ld, w.W1, w.W4, ld, nullptr, w.flags + 2, s));
+    else FROB_CUDA(inv_from_lu<double>(n, Xlu, ld, w.W2, w.W3, w.W4, ld, nullptr, w.flags + 2, s));
     // a3: C = X^{-1} Y = Xinv' (P Y)   [B-row gather]
     {
         auto p = gemm_params<double>(n, n, n, sgn, w.W4, ld, Ym, ld, 0.0, nullptr, ld, w.W2, ld);
@@ -223,9 +240,14 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
         FROB_CUDA(gemm_launch<double>(p, 1, s));
     }
     // a5: Re' = M^{-1} (un-permuted)
-    FROB_CUDA(getrf<double>(n, w.W3, ld, w.perm_m, w.mv, w.diag, &w.stats[2], w.work, s));
     double *Re = (use == 1) ? w.A : w.B;  // X buffer is free now
-    FROB_CUDA(inv_from_lu<double>(n, w.W3, ld, w.W1, w.W4, Re, ld, nullptr, w.flags + 2, s));
+    if (small) {
+        FROB_CUDA(lu2_factor<double>(n, w.W3, w.W1, ld, w.W4, w.W5, ld, w.perm_m, w.iw, w.diag, &w.stats[2], s));
+        FROB_CUDA(inv_from_ul<double>(n, w.W4, w.W5, ld, w.W3, Re, ld, nullptr, w.flags + 2, s));
+    } else {
+        FROB_CUDA(getrf<double>(n, w.W3, ld, w.perm_m, w.mv, w.diag, &w.stats[2], w.work, s));
+        FROB_CUDA(inv_from_lu<double>(n, w.W3, ld, w.W1, w.W4, Re, ld, nullptr, w.flags + 2, s));
+    }
     // a6/a7: Im' = -C Re', fused with the column interchanges and the interleaved store
     {
         auto p = gemm_params<double>(n, n, n, -1.0, w.W2, ld, Re, ld, 0.0, Re, ld, X, ldx);
@@ -264,8 +286,13 @@ static frob_status zinv_lu_impl(int n, const double *Z, long long ldz, double *X
     copy2d_kernel<double2><<<ew_blocks((long long)n * n), 256, 0, s>>>(
         reinterpret_cast<const double2 *>(Z), ldz, w.W, ld, n, w.flags);
     FROB_CUDA(cudaGetLastError());
-    FROB_CUDA(getrf<double2>(n, w.W, ld, w.perm, w.mv, w.diag, w.stats, w.work, s));
-    FROB_CUDA(inv_from_lu<double2>(n, w.W, ld, w.U, w.L, reinterpret_cast<double2 *>(X), ldx, w.perm, w.flags + 2, s));
+    if (n <= LU2_MAX_N) {
+        FROB_CUDA(lu2_factor<double2>(n, w.W, w.W2, ld, w.U, w.L, ld, w.perm, w.iw, w.diag, w.stats, s));
+        FROB_CUDA(inv_from_ul<double2>(n, w.U, w.L, ld, w.W, reinterpret_cast<double2 *>(X), ldx, w.perm, w.flags + 2, s));
+    } else {
+        FROB_CUDA(getrf<double2>(n, w.W, ld, w.perm, w.mv, w.diag, w.stats, w.work, s));
+        FROB_CUDA(inv_from_lu<double2>(n, w.W, ld, w.U, w.L, reinterpret_cast<double2 *>(X), ldx, w.perm, w.flags + 2, s));
+    }
     if (host_info) {
         LuStats hs;
         int hf = 0;
@@ -281,8 +308,8 @@ static frob_status zinv_lu_impl(int n, const double *Z, long long ldz, double *X
 
 // ---------------------------------------------------------------------- real inverse
 struct DinvWs {
-    double *W, *U, *L, *diag, *work;
-    int *perm, *mv;
+    double *W, *U, *L, *W2, *diag, *work;  // W2: n <= LU2_MAX_N only
+    int *perm, *mv, *iw;
     LuStats *stats;
     int *flags;
     size_t bytes;
@@ -294,10 +321,13 @@ static DinvWs carve_dinv(void *ws, int n) {
     w.W = c.take<double>((size_t)n * ld);
     w.U = c.take<double>((size_t)n * ld);
     w.L = c.take<double>((size_t)n * ld);
+    const bool small = n <= LU2_MAX_N;
+    w.W2 = small ? c.take<double>((size_t)n * ld) : nullptr;
     w.diag = c.take<double>((size_t)n);
     w.work = c.take<double>(getrf_work_elems<double>(n));
     w.perm = c.take<int>((size_t)n);
     w.mv = c.take<int>(lu_mv_ints(n));
+    w.iw = small ? c.take<int>(lu2_int_elems(n)) : nullptr;
     w.stats = c.take<LuStats>(1);
     w.flags = c.take<int>(4);
     w.bytes = c.off;
@@ -553,8 +583,13 @@ frob_status frob_dinv(int n, const double *A, long long lda, double *Ainv, long 
     count_launch();
     copy2d_kernel<double><<<ew_blocks((long long)n * n), 256, 0, s>>>(A, lda, w.W, ld, n, nullptr);
     FROB_CUDA(cudaGetLastError());
-    FROB_CUDA(getrf<double>(n, w.W, ld, w.perm, w.mv, w.diag, w.stats, w.work, s));
-    FROB_CUDA(inv_from_lu<double>(n, w.W, ld, w.U, w.L, Ainv, ldainv, w.perm, w.flags, s));
+    if (n <= LU2_MAX_N) {
+        FROB_CUDA(lu2_factor<double>(n, w.W, w.W2, ld, w.U, w.L, ld, w.perm, w.iw, w.diag, w.stats, s));
+        FROB_CUDA(inv_from_ul<double>(n, w.U, w.L, ld, w.W, Ainv, ldainv, w.perm, w.flags, s));
+    } else {
+        FROB_CUDA(getrf<double>(n, w.W, ld, w.perm, w.mv, w.diag, w.stats, w.work, s));
+        FROB_CUDA(inv_from_lu<double>(n, w.W, ld, w.U, w.L, Ainv, ldainv, w.perm, w.flags, s));
+    }
     if (host_info) {
         LuStats hs;
         FROB_CUDA(cudaMemcpyAsync(&hs, w.stats, sizeof(hs), cudaMemcpyDeviceToHost, s));

@@ -921,10 +921,16 @@ cudaError_t inv_from_lu(int n, T *lu, long long ld, T *U, T *L, T *out, long lon
         extract_ul_kernel<T><<<blocks, 256, 0, s>>>(lu, ld, n, U, L);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    count_launch();
-    tri_leaf_kernel<T><<<dim3((n + TRI_LEAF - 1) / TRI_LEAF, 2), TRI_LEAF, 0, s>>>(U, L, ld, n);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    T *tmp = lu;  // the LU factors are no longer needed
+    return inv_from_ul<T>(n, U, L, ld, lu, out, ldo, colperm, counter, s);  // the LU factors are scratch now
+}
+
+template <typename T>
+cudaError_t inv_from_ul(int n, T *U, T *L, long long ld, T *tmp, T *out, long long ldo, const int *colperm,
+                        int *counter, cudaStream_t s) {
+    cudaError_t e;
+    if ((e = launch_pdl(tri_leaf_kernel<T>, dim3((n + TRI_LEAF - 1) / TRI_LEAF, 2), dim3(TRI_LEAF), 0, s, U, L, ld, n,
+                        0)) != cudaSuccess)
+        return e;
     for (int sz = TRI_LEAF; sz < n; sz *= 2) {
         const int full = n / (2 * sz);
         if (full > 0 && (e = tri_level<T>(U, L, tmp, ld, sz, 0, sz, full, s)) != cudaSuccess) return e;
@@ -943,6 +949,16 @@ cudaError_t inv_from_lu(int n, T *lu, long long ld, T *U, T *L, T *out, long lon
     p.counter = (n <= 2048) ? counter : nullptr;
     return gemm_launch<T>(p, 1, s);
 }
+template cudaError_t inv_from_ul<double>(int, double *, double *, long long, double *, double *, long long, const int *, int *, cudaStream_t);
+template cudaError_t inv_from_ul<double2>(int, double2 *, double2 *, long long, double2 *, double2 *, long long, const int *, int *, cudaStream_t);
+
+template <typename T>
+cudaError_t lu_stats_launch(const T *diag, int n, LuStats *st, cudaStream_t s) {
+    return launch_pdl(lu_stats_kernel<T>, dim3(1), dim3(1024), 0, s, diag, n, st);
+}
+template cudaError_t lu_stats_launch<double>(const double *, int, LuStats *, cudaStream_t);
+template cudaError_t lu_stats_launch<double2>(const double2 *, int, LuStats *, cudaStream_t);
+
 template cudaError_t inv_from_lu<double>(int, double *, long long, double *, double *, double *, long long, const int *, int *, cudaStream_t);
 template cudaError_t inv_from_lu<double2>(int, double2 *, long long, double2 *, double2 *, double2 *, long long, const int *, int *, cudaStream_t);
 

@@ -48,6 +48,21 @@ template <typename T>
 cudaError_t inv_from_lu(int n, T *lu, long long ld, T *U, T *L, T *out, long long ldo,
                         const int *colperm, int *counter, cudaStream_t s);
 
+// Latency-oriented LU for n <= LU2_MAX_N (lu2.cu): B0 holds A on entry and is destroyed,
+// B1 is scratch (n x ld); the factors come out split: U (upper, zeros below), L (unit lower,
+// zeros above), ldo; perm[i] = original row at position i; iw = lu2_int_elems(n) ints.
+constexpr int LU2_MAX_N = 1024;
+size_t lu2_int_elems(int n);
+template <typename T>
+cudaError_t lu2_factor(int n, T *B0, T *B1, long long ld, T *U, T *L, long long ldo, int *perm, int *iw, T *diag,
+                       LuStats *stats, cudaStream_t s);
+template <typename T>
+cudaError_t lu_stats_launch(const T *diag, int n, LuStats *st, cudaStream_t s);
+// Xinv = U^{-1} L^{-1} from split factors (U, L destroyed; scratch n x ld)
+template <typename T>
+cudaError_t inv_from_ul(int n, T *U, T *L, long long ld, T *scratch, T *out, long long ldo, const int *colperm,
+                        int *counter, cudaStream_t s);
+
 template <typename T>
 cudaError_t gemm_launch(const GemmParams<T> &p, int batch, cudaStream_t s);
 template <typename T>
