@@ -3,6 +3,7 @@
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr -o tools/lu2_probe tools/lu2_probe.cu
 #include "../paper_2208_01239_b200/csrc/lu.cu"
 #include "../paper_2208_01239_b200/csrc/lu2.cu"
+#include "../paper_2208_01239_b200/csrc/lu3.cu"
 #include <vector>
 #include <random>
 #include <cmath>
@@ -17,7 +18,7 @@ template <> double re_of(double v) { return v; }
 template <> double re_of(double2 v) { return v.x; }
 
 template <typename T>
-void run(int n, int reps) {
+void run(int n, int reps, bool use3 = false) {
     const bool cplx = sizeof(T) == 16;
     const long long ld = (n + 7) / 8 * 8;
     const int E = sizeof(T) / 8;
@@ -33,7 +34,7 @@ void run(int n, int reps) {
     const size_t bytes = (size_t)n * ld * sizeof(T);
     CK(cudaMalloc(&B0, bytes)); CK(cudaMalloc(&B1, bytes)); CK(cudaMalloc(&U, bytes)); CK(cudaMalloc(&L, bytes));
     CK(cudaMalloc(&O, bytes));
-    CK(cudaMalloc(&diag, n * sizeof(T))); CK(cudaMalloc(&perm, n * 4)); CK(cudaMalloc(&iw, lu2_int_elems(n) * 4));
+    CK(cudaMalloc(&diag, n * sizeof(T))); CK(cudaMalloc(&perm, n * 4)); CK(cudaMalloc(&iw, std::max(lu2_int_elems(n), lu3_int_elems(n)) * 4));
     CK(cudaMalloc(&st, sizeof(LuStats)));
     cudaMemset(B1, 0, bytes);
     cudaEvent_t e0, e1;
@@ -42,7 +43,8 @@ void run(int n, int reps) {
     for (int r = 0; r < reps; ++r) {
         CK(cudaMemcpy(B0, h.data(), bytes, cudaMemcpyHostToDevice));
         cudaEventRecord(e0);
-        CK(lu2_factor<T>(n, B0, B1, ld, U, L, ld, perm, iw, diag, st, 0));
+        if (use3) CK(lu3_factor<T>(n, B0, ld, U, L, perm, iw, diag, st, 0));
+        else CK(lu2_factor<T>(n, B0, B1, ld, U, L, ld, perm, iw, diag, st, 0));
         cudaEventRecord(e1);
         CK(cudaEventSynchronize(e1));
         float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -97,7 +99,8 @@ void run(int n, int reps) {
     CK(cudaMemcpy(B0, h.data(), bytes, cudaMemcpyHostToDevice));
     float bi = 1e30f;
     for (int r = 0; r < reps; ++r) {
-        CK(lu2_factor<T>(n, B0, B1, ld, U, L, ld, perm, iw, diag, st, 0));
+        if (use3) CK(lu3_factor<T>(n, B0, ld, U, L, perm, iw, diag, st, 0));
+        else CK(lu2_factor<T>(n, B0, B1, ld, U, L, ld, perm, iw, diag, st, 0));
         cudaEventRecord(e0);
         CK(inv_from_ul<T>(n, U, L, ld, B0, O, ld, perm, nullptr, 0));
         cudaEventRecord(e1);
@@ -122,8 +125,8 @@ void run(int n, int reps) {
             sr -= (i == j);
             rres += sr * sr + si * si;
         }
-    printf("%s n=%5d  lu2 %8.1f us  getrf %8.1f us  | rel(PA-LU) %.2e  perm %s  maxL %.2f  pivdiff %d | inv_from_ul %7.1f us  rowsample ||XA-I|| %.2e\n",
-           cplx ? "cplx" : "real", n, best * 1e3, best0 * 1e3, std::sqrt(num / den), pok ? "ok" : "BAD", maxl, pdiff,
+    printf("%s %s n=%5d  lu %8.1f us  getrf %8.1f us  | rel(PA-LU) %.2e  perm %s  maxL %.2f  pivdiff %d | inv_from_ul %7.1f us  rowsample ||XA-I|| %.2e\n",
+           use3 ? "LU3" : "LU2", cplx ? "cplx" : "real", n, best * 1e3, best0 * 1e3, std::sqrt(num / den), pok ? "ok" : "BAD", maxl, pdiff,
            bi * 1e3, std::sqrt(rres));
     cudaFree(B0); cudaFree(B1); cudaFree(U); cudaFree(L); cudaFree(O); cudaFree(diag); cudaFree(perm); cudaFree(iw);
     cudaFree(perm0); cudaFree(mv); cudaFree(work); cudaFree(diag0); cudaFree(st);
@@ -191,8 +194,31 @@ void pieces(int n) {
 }
 
 int main(int argc, char **argv) {
-    if (argc > 1) {
+    if (argc > 1 && argv[1][0] == 'p') {
         pieces<double>(1024); pieces<double>(512); pieces<double2>(1024);
+        return 0;
+    }
+    if (argc > 1 && argv[1][0] == 't') {
+#ifdef FROB_L3_TRACE
+        for (int n : {1024}) {
+            long long z[16] = {0};
+            run<double>(n, 1, true);
+            CK(cudaMemcpyToSymbol(g_l3_trace, z, sizeof(z)));
+            run<double>(n, 1, true);
+            long long tr[16];
+            CK(cudaMemcpyFromSymbol(tr, g_l3_trace, sizeof(tr)));
+            const int nb = n / 16;
+            printf("col trace: cand+shfl %lld push %lld wait %lld argmax+row %lld update %lld\n", tr[9] - tr[8], tr[10] - tr[9], tr[11] - tr[10], tr[12] - tr[11], tr[13] - tr[12]);
+            printf("n=%d per step (cycles): wait %lld  lookahead %lld  columns %lld (%lld/col)  publish %lld\n", n, tr[0] / nb,
+                   tr[1] / nb, tr[2] / nb, tr[2] / n, tr[3] / nb);
+        }
+#endif
+        return 0;
+    }
+    if (argc > 1 && argv[1][0] == '3') {
+        int sz3[] = {1, 5, 16, 17, 100, 256, 300, 512, 513, 777, 1000, 1024};
+        for (int n : sz3) run<double>(n, n >= 512 ? 5 : 2, true);
+        for (int n : sz3) run<double2>(n, n >= 512 ? 5 : 2, true);
         return 0;
     }
     int sizes[] = {1, 5, 16, 17, 100, 256, 300, 512, 513, 777, 1024};
