@@ -40,6 +40,9 @@ struct GemmParams {
                                      // longest k-range first (square triangular products)
     int early_trigger;               // set by the launcher: release dependents at entry
                                      // (single-wave grids) instead of after the main loop
+    int ksplit;                      // set by the launcher: > 1 = split-K, each CTA adds its
+                                     // k-chunk's alpha * partial into C (pre-set to beta * D)
+                                     // with fp64 atomics (order of the S adds not fixed)
 };
 
 // Up to two independent problems in one launch (blockIdx.z < zsplit -> q[0], else q[1]).
@@ -100,6 +103,9 @@ template <typename T> struct AccW { static constexpr int V = 2; };
 template <> struct AccW<double2> { static constexpr int V = 4; };
 
 FROB_DEV double acc_val(const double (&c)[2], int e) { return c[e]; }
+FROB_DEV double acc_re(double v) { return v; }
+FROB_DEV double acc_re(double2 v) { return v.x; }
+FROB_DEV double acc_im(double2 v) { return v.y; }
 FROB_DEV double2 acc_val(const double (&c)[4], int e) { return make_double2(c[e], c[2 + e]); }
 
 template <typename T, bool VEC, int BIG>
@@ -126,6 +132,15 @@ FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int ro
     if (p.triB == TRI_UPPER) ke = min(ke, col0 + BN);
     else if (p.triB == TRI_LOWER) kb = max(kb, col0);
     kb = (kb / BK) * BK;
+    if (p.ksplit > 1) {
+        const int tot = (ke > kb) ? (ke - kb + BK - 1) / BK : 0;
+        const int per = (tot + p.ksplit - 1) / p.ksplit;
+        const int c = (int)(blockIdx.z % p.ksplit);
+        const int b2 = kb + c * per * BK;
+        ke = min(ke, b2 + per * BK);
+        kb = b2;
+        if (kb >= ke) { pdl_trigger(); return; }
+    }
     const int nk = (ke > kb) ? (ke - kb + BK - 1) / BK : 0;
 
     double acc[MT][NT][V];
@@ -209,6 +224,30 @@ FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int ro
     // the memory latency is paid once, not once per element.
     const T *__restrict__ D = p.D ? p.D + bz * p.sD : nullptr;
     T *Cp = p.C + bz * p.sC;
+    if (p.ksplit > 1) {
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+            const int row = row0 + wm0 + i * 8 + g;
+            if (row >= M) continue;
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int col = col0 + wn0 + j * 8 + 2 * t + e;
+                    if (col >= N) continue;
+                    const int oc = p.colperm ? p.colperm[col] : col;
+                    const T v = scal(acc_val(acc[i][j], e), p.alpha);
+                    double *dst = reinterpret_cast<double *>(Cp + (long long)row * p.ldc + oc);
+                    if constexpr (sizeof(T) == 8) {
+                        atomicAdd(dst, acc_re(v));
+                    } else {
+                        atomicAdd(dst, acc_re(v));
+                        atomicAdd(dst + 1, acc_im(v));
+                    }
+                }
+        }
+        return;
+    }
     if constexpr (sizeof(T) == 8) {
         // fast path: interior tile, plain store, 16-byte aligned rows -> vector D/C access
         const bool interior = (row0 + BM <= M) && (col0 + BN <= N) && p.epi == EPI_STORE && !p.colperm &&
@@ -297,7 +336,7 @@ gemm_kernel(GemmPair<T> pp) {
     // them at entry lets the next grid's waiting CTAs occupy SM slots this GEMM still needs
     if (pp.q[0].early_trigger) pdl_trigger();
     pdl_wait();
-    const int z = blockIdx.z;
+    const int z = blockIdx.z / max(1, pp.q[0].ksplit);  // ksplit is equal in both problems
     const GemmParams<T> &p = (z < pp.zsplit) ? pp.q[0] : pp.q[1];
     const long long bz = (z < pp.zsplit) ? z : z - pp.zsplit;
     if (!p.counter) {

@@ -7,6 +7,7 @@
 #include <utility>
 #include <type_traits>
 #include <mutex>
+#include <algorithm>
 #include "lu.cuh"
 
 namespace cg = cooperative_groups;
@@ -16,6 +17,34 @@ namespace frob {
 // =====================================================================================
 // GEMM launcher
 // =====================================================================================
+// split-K needs C = beta * D before the atomic adds: beta == 0 (C zeroed here) or D == C with
+// beta == 1 (accumulate in place); no fused epilogues
+template <typename T>
+static bool split_ok(const GemmParams<T> &p) {
+    return !p.counter && (p.beta == 0.0 || (p.beta == 1.0 && p.D == p.C && p.ldd == p.ldc && p.sD == p.sC));
+}
+template <typename T>
+__global__ void zero_block_kernel(T *__restrict__ C, long long ldc, long long sC, int M, int N, int batch,
+                                  const int *__restrict__ colperm) {
+    pdl_trigger();
+    pdl_wait();
+    const long long total = (long long)M * N * batch;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long b = idx / ((long long)M * N);
+        const long long r = idx - b * M * N;
+        const int i = (int)(r / N), j = (int)(r - (long long)i * N);
+        C[b * sC + (long long)i * ldc + (colperm ? colperm[j] : j)] = zero_of(T());
+    }
+}
+template <typename T>
+static cudaError_t zero_for_split(const GemmParams<T> &p, int batch, cudaStream_t s) {
+    if (p.beta != 0.0) return cudaSuccess;  // accumulate in place
+    const long long total = (long long)p.M * p.N * batch;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);
+    return launch_pdl(zero_block_kernel<T>, dim3(blocks), dim3(256), 0, s, p.C, p.ldc, p.sC, p.M, p.N, batch, p.colperm);
+}
+
 template <typename T, bool VEC, int BIG>
 static cudaError_t gemm_launch_cfg(const GemmPair<T> &pp, int batch0, int batch1, cudaStream_t s) {
     using Cf = GemmCfg<T, BIG>;
@@ -44,6 +73,28 @@ static cudaError_t gemm_launch_cfg(const GemmPair<T> &pp, int batch0, int batch1
     }
     dim3 grid((N + Cf::BN - 1) / Cf::BN, (M + Cf::BM - 1) / Cf::BM, batch0 + batch1);
     GemmPair<T> q = pp;
+    // split-K for grids far below the 148 SMs x 3 resident CTAs with long k-ranges: each CTA
+    // adds its k-chunk into C, which is first set to beta * D (here: beta == 0, or D == C)
+    {
+        const long long tiles = (long long)grid.x * grid.y * grid.z;
+        int S = 1;
+        const int K = max(p0.K, batch1 > 0 ? pp.q[1].K : 0);
+        const bool ok = !BIG && p0.epi == EPI_STORE && (batch1 == 0 || pp.q[1].epi == EPI_STORE) &&
+                        split_ok(p0) && (batch1 == 0 || split_ok(pp.q[1]));
+        if (ok && tiles * 2 <= 148LL * 3 && K >= 256) {
+            S = (int)std::min<long long>(8, (148LL * 3) / tiles);
+            S = std::min(S, K / 128);
+        }
+        if (S > 1) {
+            cudaError_t e = zero_for_split(pp.q[0], batch0, s);
+            if (e == cudaSuccess && batch1 > 0) e = zero_for_split(pp.q[1], batch1, s);
+            if (e != cudaSuccess) return e;
+            grid.z *= S;
+            q.q[0].ksplit = q.q[1].ksplit = S;
+        } else {
+            q.q[0].ksplit = q.q[1].ksplit = 1;
+        }
+    }
     const long long ctas = (long long)grid.x * grid.y * grid.z;
     // policy (tuning aid, env FROB_PDL_GEMM): 0 = release after the main loop, 1 = early for
     // single-wave grids, 2 = always early; default 0 (measured best)
