@@ -20,6 +20,7 @@
 #include <utility>
 #include <algorithm>
 #include "lu.cuh"
+#include "tma.cuh"
 
 namespace frob {
 
@@ -84,12 +85,17 @@ FROB_DEV void ld_row_smem(T (&u)[PW], const T *src) {
 // diag[k0 + j] the pivot values.
 template <typename T, int PW, int R>
 __global__ void __launch_bounds__(P2_T, 1)
-lu_panel2_kernel(T *__restrict__ B, long long ld, int n, int k0, int w, int *__restrict__ mv2,
-                 T *__restrict__ diag) {
+lu_panel2_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, long long ld, int n, int k0, int w,
+                 int *__restrict__ mv2, T *__restrict__ diag) {
     pdl_trigger();
+    extern __shared__ __align__(1024) unsigned char stgb[];  // R * P2_T rows x 128 B, 128B-swizzled (TMA)
+    __shared__ __align__(8) unsigned long long tbar;
+    if (threadIdx.x == 0) {
+        mbar_init(smem_u32(&tbar), 1u);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     pdl_wait();
     P2T(0);
-    extern __shared__ __align__(16) double stg[];  // R * P2_T rows x P2_STG doubles
     __shared__ unsigned long long ck[2][P2_WARPS];
     __shared__ int ci[2][P2_WARPS];
     __shared__ __align__(16) T wrow[2][P2_WARPS][PW];
@@ -97,33 +103,22 @@ lu_panel2_kernel(T *__restrict__ B, long long ld, int n, int k0, int w, int *__r
     __shared__ int pivrow[PW];
     __shared__ int vac[PW];
     __shared__ unsigned evm_s;
-    __shared__ int sdst[R * P2_T];
 
     constexpr int RW = PW * (int)(sizeof(T) / 8);  // doubles per row (16)
     static_assert(RW == 16, "panel rows are 128 bytes");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int m = n - k0;
-    const long long ldd = ld * (long long)(sizeof(T) / 8);
-    double *Pd = reinterpret_cast<double *>(B + (long long)k0 * ld + k0);
-    const int wd = w * (int)(sizeof(T) / 8);
-    const bool vec = ((reinterpret_cast<uintptr_t>(Pd) & 15) == 0) && ((ldd & 1) == 0);
 
-    // ---- coalesced load: 8 threads per 128-byte row
-#pragma unroll 4
-    for (int idx = tid; idx < R * P2_T * 8; idx += P2_T) {
-        const int r = idx >> 3, c2 = (idx & 7) * 2;
-        double *d = &stg[r * P2_STG + c2];
-        if (r < m && c2 + 1 < wd) {
-            if (vec) cp_async16(d, Pd + (long long)r * ldd + c2);
-            else { d[0] = Pd[(long long)r * ldd + c2]; d[1] = Pd[(long long)r * ldd + c2 + 1]; }
-        } else {
-            d[0] = (r < m && c2 < wd) ? Pd[(long long)r * ldd + c2] : 0.0;
-            d[1] = 0.0;
-        }
+    // ---- TMA load: boxes of 256 rows x 128 bytes (rows >= n and columns >= n arrive as zeros)
+    const int E = (int)(sizeof(T) / 8);
+    const int nbox = (m + 255) / 256;
+    if (tid == 0) {
+        mbar_arrive_expect_tx(smem_u32(&tbar), (unsigned)(nbox * 256 * 128));
+        for (int b = 0; b < nbox; ++b)
+            tma_load_2d(smem_u32(stgb + b * 256 * 128), &tmap, k0 * E, k0 + 256 * b, smem_u32(&tbar));
     }
-    cp_async_commit();
-    cp_async_wait<0>();
     __syncthreads();
+    mbar_wait_cta(smem_u32(&tbar), 0u);
     T a[R][PW];
     int grow[R], pst[R];
     unsigned live = 0;
@@ -132,13 +127,12 @@ lu_panel2_kernel(T *__restrict__ B, long long ld, int n, int k0, int w, int *__r
         grow[q] = q * P2_T + tid;
         pst[q] = -1;
         if (grow[q] < m) live |= 1u << q;
-        const double *row = &stg[(q * P2_T + tid) * P2_STG];
         double t[16];
 #pragma unroll
-        for (int c = 0; c < 16; c += 2) {
-            const double2 v = *reinterpret_cast<const double2 *>(row + c);
-            t[c] = v.x;
-            t[c + 1] = v.y;
+        for (int c = 0; c < 8; ++c) {
+            const double2 v = *reinterpret_cast<const double2 *>(stgb + swz128(grow[q], c));
+            t[2 * c] = v.x;
+            t[2 * c + 1] = v.y;
         }
 #pragma unroll
         for (int c = 0; c < PW; ++c) {
@@ -146,7 +140,6 @@ lu_panel2_kernel(T *__restrict__ B, long long ld, int n, int k0, int w, int *__r
             else a[q][c] = make_double2(t[2 * c], t[2 * c + 1]);
         }
     }
-
     P2T(1);
     // ---- candidate of column 0 + publish
     auto candidate = [&](auto Jc, unsigned long long &bk, int &bi, int &bq, T &brcp) {
@@ -161,7 +154,11 @@ lu_panel2_kernel(T *__restrict__ B, long long ld, int n, int k0, int w, int *__r
                 const unsigned long long kq = pkey_bits(a[q][J]);
                 if (kq > bk) { bk = kq; bi = grow[q]; bq = q; myp = a[q][J]; }
             }
+#ifdef FROB_P2_SPEC_RCP
         brcp = rcp_spec(myp);
+#else
+        brcp = myp;
+#endif
     };
     auto publish_row = [&](int s, int bq, const T &brcp) {
 #pragma unroll
@@ -207,7 +204,11 @@ lu_panel2_kernel(T *__restrict__ B, long long ld, int n, int k0, int w, int *__r
         const int gi = ba.i;
         const unsigned ww = ((unsigned)gi & (unsigned)(P2_T - 1)) >> 5;
         ld_row_smem<T, PW>(u, wrow[s][ww]);
+#ifdef FROB_P2_SPEC_RCP
         const T rc = wrcp[s][ww];
+#else
+        const T rc = rcp_spec(u[J]);
+#endif
         P2TJ(J, 42);
         if (tid == 0) {
             pivrow[J] = gi;
@@ -309,29 +310,34 @@ lu_panel2_kernel(T *__restrict__ B, long long ld, int n, int k0, int w, int *__r
     }
     __syncthreads();
     const unsigned evm = evm_s;
+    // ---- rows to their final positions in the staging buffer, then TMA box stores
 #pragma unroll
     for (int q = 0; q < R; ++q) {
         const int g = grow[q];
+        if (g >= m) continue;
         int dst = g;
         if (pst[q] >= 0) dst = pst[q];
         else if (g < w) dst = vac[__popc(evm & ((1u << g) - 1u))];
-        sdst[q * P2_T + tid] = (g < m) ? dst : -1;
-        T *row = reinterpret_cast<T *>(&stg[(q * P2_T + tid) * P2_STG]);
-        st_row_smem<T, PW>(row, a[q]);
+        const double *rd = reinterpret_cast<const double *>(a[q]);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<double2 *>(stgb + swz128(dst, c)) = make_double2(rd[2 * c], rd[2 * c + 1]);
     }
     __syncthreads();
+    // coalesced write-back: 8 threads per 128-byte row (measured faster than a TMA box store
+    // followed by its completion wait)
+    {
+        const long long ldd = ld * E;
+        double *P = reinterpret_cast<double *>(B) + (long long)k0 * ldd + (long long)k0 * E;
+        const int wd = w * E;
 #pragma unroll 4
-    for (int idx = tid; idx < R * P2_T * 8; idx += P2_T) {
-        const int r = idx >> 3, c2 = (idx & 7) * 2;
-        const int d = sdst[r];
-        if (d < 0 || c2 >= wd) continue;
-        double *out = Pd + (long long)d * ldd + c2;
-        const double2 v = *reinterpret_cast<const double2 *>(&stg[r * P2_STG + c2]);
-        if (c2 + 1 < wd) {
-            if (vec) *reinterpret_cast<double2 *>(out) = v;
-            else { out[0] = v.x; out[1] = v.y; }
-        } else {
-            out[0] = v.x;
+        for (int idx = tid; idx < m * 8; idx += P2_T) {
+            const int r = idx >> 3, c = idx & 7;
+            if (2 * c >= wd) continue;
+            const double2 v = *reinterpret_cast<const double2 *>(stgb + swz128(r, c));
+            double *out = P + (long long)r * ldd + 2 * c;
+            if (2 * c + 1 < wd) *reinterpret_cast<double2 *>(out) = v;
+            else out[0] = v.x;
         }
     }
     P2T(21);
@@ -538,8 +544,9 @@ size_t lu2_int_elems(int n) {
 }
 
 template <typename T, int PW, int R>
-static cudaError_t launch_panel2(T *B, long long ld, int n, int k0, int w, int *mv2, T *diag, cudaStream_t s) {
-    const size_t smem = (size_t)R * P2_T * P2_STG * sizeof(double);
+static cudaError_t launch_panel2(const CUtensorMap &tm, T *B, long long ld, int n, int k0, int w, int *mv2, T *diag,
+                                 cudaStream_t s) {
+    const size_t smem = (size_t)R * P2_T * 128 + 1024;
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -549,7 +556,7 @@ static cudaError_t launch_panel2(T *B, long long ld, int n, int k0, int w, int *
         if (e != cudaSuccess) return e;
         attr_set[dev] = true;
     }
-    return launch_pdl(lu_panel2_kernel<T, PW, R>, dim3(1), dim3(P2_T), smem, s, B, ld, n, k0, w, mv2, diag);
+    return launch_pdl(lu_panel2_kernel<T, PW, R>, dim3(1), dim3(P2_T), smem, s, tm, B, ld, n, k0, w, mv2, diag);
 }
 
 template <typename T>
@@ -561,15 +568,21 @@ cudaError_t lu2_factor(int n, T *B0, T *B1, long long ld, T *U, T *L, long long 
     int *iperm = iw;
     int *mvb = iw + n;
     int *snap = mvb + (size_t)steps * MV2_INTS;
-    cudaError_t e = launch_pdl(iota2_kernel, dim3((n + 255) / 256), dim3(256), 0, s, perm, iperm, n);
+    // TMA descriptors of the two ping-pong buffers (rows x 16-double boxes, 128B swizzle)
+    const int E = (int)(sizeof(T) / 8);
+    CUtensorMap tm[2];
+    cudaError_t e = tma_map_rows128(&tm[0], B0, n, (long long)n * E, ld * E, 256);
+    if (e == cudaSuccess) e = tma_map_rows128(&tm[1], B1, n, (long long)n * E, ld * E, 256);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(iota2_kernel, dim3((n + 255) / 256), dim3(256), 0, s, perm, iperm, n);
     if (e != cudaSuccess) return e;
     for (int k = 0; k < steps; ++k) {
         const int k0 = k * PW, w = min(PW, n - k0), m = n - k0;
         T *Bk = (k & 1) ? B1 : B0;
         T *Bn = (k & 1) ? B0 : B1;
         int *mv2 = mvb + (size_t)k * MV2_INTS;
-        if (m <= P2_T) e = launch_panel2<T, PW, 1>(Bk, ld, n, k0, w, mv2, diag, s);
-        else e = launch_panel2<T, PW, 2>(Bk, ld, n, k0, w, mv2, diag, s);
+        if (m <= P2_T) e = launch_panel2<T, PW, 1>(tm[k & 1], Bk, ld, n, k0, w, mv2, diag, s);
+        else e = launch_panel2<T, PW, 2>(tm[k & 1], Bk, ld, n, k0, w, mv2, diag, s);
         if (e != cudaSuccess) return e;
         const int rest = n - k0 - w;
         dim3 grid(max(1, (rest + U2_TC - 1) / U2_TC), max(1, (rest + U2_TR - 1) / U2_TR));

@@ -2,6 +2,7 @@
 // blocked getrf (lu.cu).  Debug tool, not the product.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr -o tools/lu2_probe tools/lu2_probe.cu
 #include "../paper_2208_01239_b200/csrc/lu.cu"
+#include "../paper_2208_01239_b200/csrc/tma.cu"
 #include "../paper_2208_01239_b200/csrc/lu2.cu"
 #include "../paper_2208_01239_b200/csrc/lu3.cu"
 #include <vector>
@@ -156,9 +157,11 @@ void pieces(int n) {
         printf("  %s n=%d: %-40s %8.2f us\n", sizeof(T) == 8 ? "real" : "cplx", n, nm, ms * 1e3 / reps);
     };
     // the panel kernel re-factors the same (already factored) panel: timing only
+    CUtensorMap tmap;
+    CK(tma_map_rows128(&tmap, B0, n, (long long)n * (sizeof(T) / 8), ld * (sizeof(T) / 8), 256));
     tm("panel2 (m=n) x20", [&] {
-        if (n <= P2_T) launch_panel2<T, PW, 1>(B0, ld, n, 0, PW, iw, diag, 0);
-        else launch_panel2<T, PW, 2>(B0, ld, n, 0, PW, iw, diag, 0);
+        if (n <= P2_T) launch_panel2<T, PW, 1>(tmap, B0, ld, n, 0, PW, iw, diag, 0);
+        else launch_panel2<T, PW, 2>(tmap, B0, ld, n, 0, PW, iw, diag, 0);
     }, 20);
 #ifdef FROB_P2_TRACE
     {
@@ -172,10 +175,7 @@ void pieces(int n) {
                tr[40] - tr[6], tr[41] - tr[40], tr[42] - tr[41], tr[43] - tr[42], tr[44] - tr[43], tr[45] - tr[44], tr[7] - tr[45]);
     }
 #endif
-    tm("panel2 (m=n) plain launch x20", [&] {
-        const size_t smem = (size_t)2 * P2_T * P2_STG * 8;
-        lu_panel2_kernel<T, PW, 2><<<1, P2_T, smem>>>(B0, ld, n, 0, PW, iw, diag);
-    }, 20);
+
     const int rest = n - PW;
     dim3 grid(max(1, (rest + U2_TC - 1) / U2_TC), max(1, (rest + U2_TR - 1) / U2_TR));
     tm("update2 step 0 x20", [&] {
@@ -183,8 +183,8 @@ void pieces(int n) {
                    (const int *)iw, perm, iperm, (int *)nullptr);
     }, 20);
     tm("panel2+update2 alternating x20", [&] {
-        if (n <= P2_T) launch_panel2<T, PW, 1>(B0, ld, n, 0, PW, iw, diag, 0);
-        else launch_panel2<T, PW, 2>(B0, ld, n, 0, PW, iw, diag, 0);
+        if (n <= P2_T) launch_panel2<T, PW, 1>(tmap, B0, ld, n, 0, PW, iw, diag, 0);
+        else launch_panel2<T, PW, 2>(tmap, B0, ld, n, 0, PW, iw, diag, 0);
         launch_pdl(lu_update2_kernel<T, PW>, grid, dim3(U2_T), 0, (cudaStream_t)0, (const T *)B0, B1, ld, n, 0, PW,
                    (const int *)iw, perm, iperm, (int *)nullptr);
     }, 20);
