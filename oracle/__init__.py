@@ -55,9 +55,11 @@ def lib():
             L.or_dinv.argtypes = [ctypes.c_int, dp, dp, dp]
             L.or_dgemm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, dp, dp, dp]
             L.or_frob_inv.argtypes = [ctypes.c_int, dp, dp, dp, dp, ctypes.c_int, ctypes.c_double, ip, dp]
+            L.or_frob_inv_rand.argtypes = [ctypes.c_int, dp, dp, ctypes.c_double, dp, dp, ctypes.c_double,
+                                           ip, dp]
             L.or_zinv_gj.argtypes = [ctypes.c_int, dp, dp]
             L.or_zinv_lu.argtypes = [ctypes.c_int, dp, dp, dp, dp]
-            for f in ("or_dgetrf", "or_dtrtri_upper", "or_dinv", "or_frob_inv", "or_zinv_gj",
+            for f in ("or_dgetrf", "or_dtrtri_upper", "or_dinv", "or_frob_inv", "or_frob_inv_rand", "or_zinv_gj",
                       "or_zinv_lu", "or_num_threads"):
                 getattr(L, f).restype = ctypes.c_int
             L.or_dgetri_solve.restype = None
@@ -148,6 +150,23 @@ def frob_inv(z, branch: str = "auto", tau: float = TAU_SWITCH):
     x = xr + 1j * xi
     return x, st, {"info": int(out[0]), "branch_used": int(out[1]),
                    "rho_a": float(rho[0]), "rho_b": float(rho[1])}
+
+
+def frob_inv_rand(z, mu: float, tau: float = TAU_SWITCH):
+    """Alg 5 with the random mu given: Z^{-1} = (1 + mu i) (Z (1 + mu i))^{-1}.
+
+    Returns (X complex128, status, info dict) as frob_inv (status of the inner Alg 1 call).
+    """
+    a, b = split(z)
+    n = a.shape[0]
+    xr = np.zeros_like(a)
+    xi = np.zeros_like(a)
+    out = np.zeros(2, dtype=np.int32)
+    rho = np.zeros(2, dtype=np.float64)
+    st = lib().or_frob_inv_rand(n, _p(a), _p(b), float(mu), _p(xr), _p(xi), float(tau),
+                                _p(out, ctypes.c_int), _p(rho))
+    return xr + 1j * xi, st, {"info": int(out[0]), "branch_used": int(out[1]),
+                              "rho_a": float(rho[0]), "rho_b": float(rho[1])}
 
 
 def zinv_gj(z):

@@ -97,6 +97,15 @@ def frobenius_exact(m, branch: str = "a"):
     return [[cadd(kv, cmul(mi, jv)) for jv, kv in zip(jr, kr)] for jr, kr in zip(j, k)]
 
 
+def frobenius_rand_exact(m, mu):
+    """Alg 5 over Q(i) for a rational mu: X = A - mu B, Y = mu A + B,
+    W = Alg 1 (X + iY) (branch S1), return (W1 - mu W2) + i (mu W1 + W2)."""
+    mu = Fr(mu)
+    rot = [[(v[0] - mu * v[1], mu * v[0] + v[1]) for v in r] for r in m]
+    w = frobenius_exact(rot, "a")
+    return [[(v[0] - mu * v[1], mu * v[0] + v[1]) for v in r] for r in w]
+
+
 def to_complex(m):
     import numpy as np
     return np.array([[complex(float(v[0]), float(v[1])) for v in r] for r in m])

@@ -23,6 +23,7 @@
  *                    interchanges that undo P (A = P^T L U  =>  A^{-1} = U^{-1} L^{-1} P).
  *   or_dinv          Alg 3 = the real inversion inv_{n,R} used twice by Alg 1.
  *   or_dgemm         m_{n,R}: C = A B, plain triple loop, k ascending.
+ *   or_frob_inv_rand Alg 5 randomized Frobenius inversion, mu given
  *   or_frob_inv      Alg 1 "Frobenius inversion I" with tau = 1 (f = x^2+1,
  *                    P:L123): S1 branch returns J - iK, S2 branch returns K - iJ.  The
  *                    numerical branch choice (the paper's S1/S2 are algebraic)
@@ -264,6 +265,36 @@ int or_frob_inv(int n, const double *A, const double *B, double *Xre, double *Xi
 done:
     free(Xinv); free(F); free(G); free(J); free(K);
     return info ? 1 : 0;
+}
+
+/* Alg 5 "randomized Frobenius inversion", mu supplied by the caller (line 1 draws
+ * it from [0,1]; random numbers are inputs here).
+ *   line 2: X = A - mu B, Y = mu A + B
+ *   line 3: W = (X + iY)^{-1} by Alg 1 (AUTO branch rule, R1)
+ *   line 4: W1 = Re W, W2 = Im W
+ *   line 5: Z^{-1} = (W1 - mu W2) + i (mu W1 + W2)
+ * Returns the status of the inner Alg 1 call (out / rho as there). */
+int or_frob_inv_rand(int n, const double *A, const double *B, double mu, double *Xre, double *Xim,
+                     double tau_sw, int *out, double *rho)
+{
+    size_t nn = (size_t)n * n;
+    double *X = (double *)malloc(sizeof(double) * nn);
+    double *Y = (double *)malloc(sizeof(double) * nn);
+    double *W1 = (double *)malloc(sizeof(double) * nn);
+    double *W2 = (double *)malloc(sizeof(double) * nn);
+    for (size_t i = 0; i < nn; ++i) {           /* line 2 */
+        X[i] = A[i] - mu * B[i];
+        Y[i] = mu * A[i] + B[i];
+    }
+    int st = or_frob_inv(n, X, Y, W1, W2, 0, tau_sw, out, rho);   /* lines 3-4 */
+    if (st == 0) {
+        for (size_t i = 0; i < nn; ++i) {       /* line 5 */
+            Xre[i] = W1[i] - mu * W2[i];
+            Xim[i] = mu * W1[i] + W2[i];
+        }
+    }
+    free(X); free(Y); free(W1); free(W2);
+    return st;
 }
 
 /* --------------------------------------------------------------- complex */

@@ -175,6 +175,61 @@ def test_branch_b_is_rotated_branch_a():
     assert np.array_equal(xb, -1j * xa_rot)
 
 
+# ------------------------------------------------------------------ Alg 5 (randomized)
+def test_exact_alg5_matches_definition_including_both_singular():
+    """Alg 5 over Q(i) with rational mu equals the exact inverse, also where Alg 1 cannot run:
+    Z = [[1, i], [i, 1]] has A = I but B = [[0,1],[1,0]]; Z = [[1+i, 1-i],[1-i, 1+i]] has A and B
+    both singular (rank 1) while Z is invertible (det = 4i) -- Lemma 5.4."""
+    cases = [([[1, 0], [0, 1]], [[0, 1], [1, 0]]), ([[1, 1], [1, 1]], [[1, -1], [-1, 1]])]
+    rng = np.random.default_rng(5)
+    for n in (3, 4):
+        cases.append((rng.integers(-3, 4, size=(n, n)).tolist(), rng.integers(-3, 4, size=(n, n)).tolist()))
+    from fractions import Fraction
+    for re, im in cases:
+        z = exact.from_ints(re, im)
+        try:
+            zi = exact.inv_exact(z)
+        except ZeroDivisionError:
+            continue
+        for mu in (Fraction(1, 3), Fraction(5, 7)):
+            assert exact.frobenius_rand_exact(z, mu) == zi
+    # the both-singular example really defeats Alg 1 in both branches
+    z = exact.from_ints(cases[1][0], cases[1][1])
+    for br in ("a", "b"):
+        with pytest.raises(ZeroDivisionError):
+            exact.frobenius_exact(z, br)
+
+
+def test_alg5_dft_both_singular_gives_unitary_inverse():
+    """DFT/sqrt(n): A, B singular (AUTO Alg 1 -> status 2) but Alg 5 returns Z^{-1} = Z^H."""
+    z = synth.dft_unitary(16)
+    _, st, _ = oracle.frob_inv(z, "auto")
+    assert st == 2
+    x, st, info = oracle.frob_inv_rand(z, 0.6180339887)
+    assert st == 0
+    assert oracle.rel_fro(x, z.conj().T) <= 1e-13
+
+
+def test_alg5_mu_zero_is_alg1_bitwise():
+    z = synth.shifted_complex(24, seed=3, shift=6.0)
+    x0, st0, _ = oracle.frob_inv(z, "auto")
+    xr, st1, _ = oracle.frob_inv_rand(z, 0.0)
+    assert st0 == 0 and st1 == 0
+    assert np.array_equal(x0, xr)
+
+
+def test_alg5_residual_and_rotation_identity():
+    """Z X = I, and X equals (1 + mu i) times Alg 1 applied to (1 + mu i) Z (line 5)."""
+    z = synth.shifted_complex(40, seed=9, shift=7.0)
+    mu = 0.41
+    x, st, _ = oracle.frob_inv_rand(z, mu)
+    assert st == 0
+    assert oracle.residual_fro(z, x) <= 1e-12 * 40
+    w, st2, _ = oracle.frob_inv((1 + 1j * mu) * z, "auto")
+    assert st2 == 0
+    assert oracle.rel_fro(x, (1 + 1j * mu) * w) <= 1e-14
+
+
 # ------------------------------------------------------------------ real kernels
 def test_dgetrf_reconstruction_and_lapack_pivots():
     a, _ = synth.gauss_pair(40, seed=2, shift=0.0)
