@@ -82,6 +82,17 @@ size_t frob_inv_workspace_bytes(int n);
 frob_status frob_inv(int n, const double *Z, long long ldz, double *X, long long ldx,
                      int branch, void *ws, size_t ws_bytes, void *stream, frob_info *host_info);
 
+/* Randomized Frobenius inversion (Alg 5): X = A - mu B, Y = mu A + B,
+ * W = (X + iY)^{-1} by Alg 1 (AUTO branch rule), Z^{-1} = (W1 - mu W2) + i (mu W1 + W2).
+ * Works for invertible Z whose real and imaginary parts are both singular (Lemma 5.4,
+ * A - mu B is singular for at most n values of mu).  mu in [0, 1] is drawn by the
+ * CALLER (line 1; the Python binding uses a seeded generator); mu outside [0, 1] gives
+ * FROB_ERR_INVALID_ARG.  Workspace, layout, aliasing and errors as frob_inv (host_info
+ * describes the inner Alg 1 call on X + iY).  Cost: frob_inv + 8 n^2, fused into
+ * the ingest and final-epilogue kernels. */
+frob_status frob_inv_rand(int n, const double *Z, long long ldz, double *X, long long ldx, double mu,
+                          void *ws, size_t ws_bytes, void *stream, frob_info *host_info);
+
 /* Same computation with HOST input/output buffers (pinned memory recommended): copies
  * Z host->device, runs frob_inv, copies X device->host, synchronises.  Z_host/X_host
  * are dense (ld = n).  ws must hold frob_inv_host_workspace_bytes(n) bytes. */

@@ -45,15 +45,17 @@ struct Carve {
 
 // ---------------------------------------------------------------------- elementwise
 // a0: split interleaved Z (ldz) into planar A, B (ld) and a copy of the branch matrix
+// mu != 0: Alg 5 line 2 -- the parts of (1 + mu i) Z: X = A - mu B, Y = mu A + B
 __global__ void split_kernel(const double2 *__restrict__ Z, long long ldz, int n, double *__restrict__ A,
                              double *__restrict__ B, double *__restrict__ W, int wsel, long long ld,
-                             int *__restrict__ nonfinite) {
+                             int *__restrict__ nonfinite, double mu) {
     const long long total = (long long)n * n;
     int bad = 0;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
         const int i = (int)(idx / n), j = (int)(idx - (long long)i * n);
-        const double2 z = Z[(long long)i * ldz + j];
+        double2 z = Z[(long long)i * ldz + j];
+        if (mu != 0.0) z = make_double2(z.x - mu * z.y, mu * z.x + z.y);
         bad |= !(isfinite(z.x) && isfinite(z.y));
         const long long o = (long long)i * ld + j;
         A[o] = z.x;
@@ -155,7 +157,7 @@ static bool overlap(const void *a, size_t na, const void *b, size_t nb) {
 // ---------------------------------------------------------------------- frob_inv
 static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *X, long long ldx,
                                  int branch, void *ws, size_t ws_bytes, cudaStream_t s,
-                                 frob_info *host_info) {
+                                 frob_info *host_info, double mu = 0.0) {
     if (n < 1 || !Z || !X || ldz < n || ldx < n || branch < 0 || branch > 2) return FROB_ERR_INVALID_ARG;
     if (overlap(Z, (size_t)((n - 1) * ldz + n) * 16, X, (size_t)((n - 1) * ldx + n) * 16))
         return FROB_ERR_INVALID_ARG;
@@ -169,7 +171,7 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
     // a0: ingest
     count_launch();
     split_kernel<<<ew_blocks((long long)n * n), 256, 0, s>>>(Zc, ldz, n, w.A, w.B, w.W1,
-                                                             branch == FROB_BRANCH_B ? 2 : 1, ld, w.flags);
+                                                             branch == FROB_BRANCH_B ? 2 : 1, ld, w.flags, mu);
     FROB_CUDA(cudaGetLastError());
 
     // a1: LU of the branch matrix (A unless forced B)
@@ -253,6 +255,7 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
         auto p = gemm_params<double>(n, n, n, -1.0, w.W2, ld, Re, ld, 0.0, Re, ld, X, ldx);
         p.epi = (use == 1) ? EPI_FROB_A : EPI_FROB_B;
         p.colperm = w.perm_m;
+        p.mu = mu;  // Alg 5 line 5: Z^{-1} = (1 + mu i) W
         FROB_CUDA(gemm_launch<double>(p, 1, s));
     }
     if (host_info) {
@@ -510,6 +513,12 @@ size_t frob_inv_workspace_bytes(int n) { return n < 1 ? 0 : carve_frob(nullptr, 
 frob_status frob_inv(int n, const double *Z, long long ldz, double *X, long long ldx, int branch,
                      void *ws, size_t ws_bytes, void *stream, frob_info *host_info) {
     return frob_inv_impl(n, Z, ldz, X, ldx, branch, ws, ws_bytes, (cudaStream_t)stream, host_info);
+}
+
+frob_status frob_inv_rand(int n, const double *Z, long long ldz, double *X, long long ldx, double mu, void *ws,
+                          size_t ws_bytes, void *stream, frob_info *host_info) {
+    if (!(mu >= 0.0 && mu <= 1.0)) return FROB_ERR_INVALID_ARG;
+    return frob_inv_impl(n, Z, ldz, X, ldx, FROB_BRANCH_AUTO, ws, ws_bytes, (cudaStream_t)stream, host_info, mu);
 }
 
 size_t frob_inv_host_workspace_bytes(int n) {

@@ -40,6 +40,7 @@ struct GemmParams {
                                      // longest k-range first (square triangular products)
     int early_trigger;               // set by the launcher: release dependents at entry
                                      // (single-wave grids) instead of after the main loop
+    double mu;                       // EPI_FROB_*: output scaled by (1 + mu i) (Alg 5 line 5)
     int ksplit;                      // set by the launcher: > 1 = split-K, each CTA adds its
                                      // k-chunk's alpha * partial into C (pre-set to beta * D)
                                      // with fp64 atomics (order of the S adds not fixed)
@@ -312,8 +313,9 @@ FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int ro
                     if (p.epi != EPI_STORE) {
                         const double d = dv[j][e];
                         double2 *X = reinterpret_cast<double2 *>(Cp);
-                        X[(long long)row * p.ldc + oc[j][e]] =
-                            (p.epi == EPI_FROB_A) ? make_double2(d, v) : make_double2(v, -d);
+                        double2 o = (p.epi == EPI_FROB_A) ? make_double2(d, v) : make_double2(v, -d);
+                        if (p.mu != 0.0) o = make_double2(o.x - p.mu * o.y, p.mu * o.x + o.y);
+                        X[(long long)row * p.ldc + oc[j][e]] = o;
                         continue;
                     }
                 }

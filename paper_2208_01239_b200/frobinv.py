@@ -39,6 +39,7 @@ _FIP = ctypes.POINTER(FrobInfo)
 SIGNATURES = {
     "frob_inv_workspace_bytes": (_sz, [_i]),
     "frob_inv": (_i, [_i, _vp, _ll, _vp, _ll, _i, _vp, _sz, _vp, _FIP]),
+    "frob_inv_rand": (_i, [_i, _vp, _ll, _vp, _ll, _d, _vp, _sz, _vp, _FIP]),
     "frob_inv_host_workspace_bytes": (_sz, [_i]),
     "frob_inv_host": (_i, [_i, _vp, _vp, _i, _vp, _sz, _vp, _FIP]),
     "zinv_lu_workspace_bytes": (_sz, [_i]),
@@ -144,6 +145,30 @@ def inv(z: torch.Tensor, branch: str = "auto", out: torch.Tensor | None = None, 
     st = L.frob_inv(n, _p(z), z.stride(0), _p(x), x.stride(0), BRANCH[branch], _p(ws), ws.numel(),
                     _stream(), ctypes.byref(fi) if info else None)
     _check("frob_inv", st, fi.as_dict() if info else None)
+    return (x, fi.as_dict()) if info else x
+
+
+def draw_mu(seed: int) -> float:
+    """Alg 5 line 1: mu uniform in [0, 1] from a seeded counter-based generator (Philox)."""
+    import numpy as np
+    return float(np.random.Generator(np.random.Philox(key=seed)).random())
+
+
+def inv_rand(z: torch.Tensor, mu: float | None = None, seed: int = 0, out: torch.Tensor | None = None,
+             info: bool = False):
+    """Randomized Frobenius inversion (Alg 5).  mu in [0, 1]; drawn from `seed` if None."""
+    L = load()
+    _need_cuda(z, "z")
+    assert z.dtype == torch.complex128 and z.dim() == 2 and z.shape[0] == z.shape[1]
+    z = z if z.stride(1) == 1 else z.contiguous()
+    n = z.shape[0]
+    mu = draw_mu(seed) if mu is None else float(mu)
+    x = out if out is not None else torch.empty((n, n), dtype=torch.complex128, device=z.device)
+    ws = workspace(L.frob_inv_workspace_bytes(n), z.device)
+    fi = FrobInfo()
+    st = L.frob_inv_rand(n, _p(z), z.stride(0), _p(x), x.stride(0), mu, _p(ws), ws.numel(), _stream(),
+                         ctypes.byref(fi) if info else None)
+    _check("frob_inv_rand", st, fi.as_dict() if info else None)
     return (x, fi.as_dict()) if info else x
 
 

@@ -99,7 +99,7 @@ def test_dinv(n):
 
 
 # ------------------------------------------------------------------ frob_inv (single)
-@pytest.mark.parametrize("n", [1, 2, 3, 17, 64, 100, 256, 513])
+@pytest.mark.parametrize("n", [1, 2, 3, 16, 17, 64, 100, 256, 511, 512, 513, 1000, 1025])
 @pytest.mark.parametrize("branch", ["auto", "a", "b"])
 def test_frob_inv_small(n, branch):
     z = synth.shifted_complex(n, seed=100 + n, shift=math.sqrt(n) + 2.0)
@@ -138,10 +138,41 @@ def test_config2_full_size():
     assert oracle.rel_fro(_np(x), xo) <= REL
 
 
-@pytest.mark.parametrize("n", [1, 5, 31, 64, 129, 300])
+@pytest.mark.parametrize("n", [1, 5, 8, 9, 31, 64, 129, 300, 513, 1000, 1025])
 def test_zinv_lu(n):
     z = synth.shifted_complex(n, seed=7 * n, shift=3.0 + math.sqrt(n))
     _check_inverse(z, _np(fb.zinv(_t(z))))
+
+
+# ------------------------------------------------------------------ Alg 5 (randomized)
+@pytest.mark.parametrize("n", [1, 7, 64, 300, 1024])
+def test_frob_inv_rand_vs_oracle(n):
+    """Alg 5 on the GPU vs the oracle's Alg 5 with the same mu, and vs the definition."""
+    z = synth.shifted_complex(n, seed=500 + n, shift=math.sqrt(n) + 2.0)
+    mu = fb.draw_mu(n)
+    x = _np(fb.inv_rand(_t(z), mu=mu))
+    xo, st, _ = oracle.frob_inv_rand(z, mu)
+    assert st == 0
+    assert oracle.rel_fro(x, xo) <= REL
+    _check_inverse(z, x)
+
+
+def test_frob_inv_rand_both_parts_singular():
+    """DFT/sqrt(n): Alg 1 fails in both branches, Alg 5 returns Z^{-1} = Z^H."""
+    for n in (16, 64, 256):
+        z = synth.dft_unitary(n)
+        with pytest.raises(fb.FrobError):
+            fb.inv(_t(z))
+        x = _np(fb.inv_rand(_t(z), seed=n))
+        _check_inverse(z, x, ref=z.conj().T)
+
+
+def test_frob_inv_rand_mu_zero_and_invalid():
+    z = synth.shifted_complex(80, seed=8, shift=10.0)
+    assert np.array_equal(_np(fb.inv_rand(_t(z), mu=0.0)), _np(fb.inv(_t(z))))
+    with pytest.raises(fb.FrobError) as e:
+        fb.inv_rand(_t(z), mu=1.5)
+    assert e.value.name == "invalid_arg"
 
 
 # ------------------------------------------------------------------ bitwise invariants
