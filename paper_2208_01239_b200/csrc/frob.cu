@@ -157,7 +157,7 @@ static bool overlap(const void *a, size_t na, const void *b, size_t nb) {
 // ---------------------------------------------------------------------- frob_inv
 static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *X, long long ldx,
                                  int branch, void *ws, size_t ws_bytes, cudaStream_t s,
-                                 frob_info *host_info, double mu = 0.0) {
+                                 frob_info *host_info, double mu = 0.0, bool fused = false) {
     if (n < 1 || !Z || !X || ldz < n || ldx < n || branch < 0 || branch > 2) return FROB_ERR_INVALID_ARG;
     if (overlap(Z, (size_t)((n - 1) * ldz + n) * 16, X, (size_t)((n - 1) * ldx + n) * 16))
         return FROB_ERR_INVALID_ARG;
@@ -227,32 +227,51 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
     const double *Ym = (use == 1) ? w.B : w.A;   // Y of Alg 1 (S2 uses Y = -A via sgn)
     const double sgn = (use == 1) ? 1.0 : -1.0;
 
-    // a2: Xinv' = U^{-1} L^{-1}  (X^{-1} = Xinv' P)
-    if (small) FROB_CUDA(inv_from_ul<double>(n, Uf, Lf, ld, w.W1, w.W4, ld, nullptr, w.flags + 2, s));
-    else FROB_CUDA(inv_from_lu<double>(n, Xlu, ld, w.W2, w.W3, w.W4, ld, nullptr, w.flags + 2, s));
-    // a3: C = X^{-1} Y = Xinv' (P Y)   [B-row gather]
-    {
-        auto p = gemm_params<double>(n, n, n, sgn, w.W4, ld, Ym, ld, 0.0, nullptr, ld, w.W2, ld);
+    double *Cb;  // C = X^{-1} Y
+    if (!fused) {
+        // a2: Xinv' = U^{-1} L^{-1}  (X^{-1} = Xinv' P)
+        if (small) FROB_CUDA(inv_from_ul<double>(n, Uf, Lf, ld, w.W1, w.W4, ld, nullptr, w.flags + 2, s));
+        else FROB_CUDA(inv_from_lu<double>(n, Xlu, ld, w.W2, w.W3, w.W4, ld, nullptr, w.flags + 2, s));
+        // a3: C = X^{-1} Y = Xinv' (P Y)   [B-row gather]
+        Cb = w.W2;
+        auto p = gemm_params<double>(n, n, n, sgn, w.W4, ld, Ym, ld, 0.0, nullptr, ld, Cb, ld);
         p.browmap = perm;
         FROB_CUDA(gemm_launch<double>(p, 1, s));
+    } else {
+        // a2+a3 fused (NEXT-1): C = U^{-1} (L^{-1} (P Y)); X^{-1} is never formed
+        if (!small) {
+            FROB_CUDA(extract_ul<double>(n, Xlu, ld, w.W2, w.W3, s));
+            Uf = w.W2;
+            Lf = w.W3;
+        }
+        FROB_CUDA(tri_inverses<double>(n, Uf, Lf, ld, w.W1, s));
+        auto p = gemm_params<double>(n, n, n, sgn, Lf, ld, Ym, ld, 0.0, nullptr, ld, w.W4, ld);
+        p.triA = TRI_LOWER;
+        p.browmap = perm;
+        FROB_CUDA(gemm_launch<double>(p, 1, s));
+        Cb = w.W1;
+        auto q = gemm_params<double>(n, n, n, 1.0, Uf, ld, w.W4, ld, 0.0, nullptr, ld, Cb, ld);
+        q.triA = TRI_UPPER;
+        FROB_CUDA(gemm_launch<double>(q, 1, s));
     }
     // a4: M = X + Y C
     {
-        auto p = gemm_params<double>(n, n, n, sgn, Ym, ld, w.W2, ld, 1.0, Xm, ld, w.W3, ld);
+        auto p = gemm_params<double>(n, n, n, sgn, Ym, ld, Cb, ld, 1.0, Xm, ld, w.W3, ld);
         FROB_CUDA(gemm_launch<double>(p, 1, s));
     }
-    // a5: Re' = M^{-1} (un-permuted)
+    // a5: Re' = M^{-1} (un-permuted); scratch: the two buffers not holding C
     double *Re = (use == 1) ? w.A : w.B;  // X buffer is free now
+    double *Sa = fused ? w.W2 : w.W1;
     if (small) {
-        FROB_CUDA(lu2_factor<double>(n, w.W3, w.W1, ld, w.W4, w.W5, ld, w.perm_m, w.iw, w.diag, &w.stats[2], s));
+        FROB_CUDA(lu2_factor<double>(n, w.W3, Sa, ld, w.W4, w.W5, ld, w.perm_m, w.iw, w.diag, &w.stats[2], s));
         FROB_CUDA(inv_from_ul<double>(n, w.W4, w.W5, ld, w.W3, Re, ld, nullptr, w.flags + 2, s));
     } else {
         FROB_CUDA(getrf<double>(n, w.W3, ld, w.perm_m, w.mv, w.diag, &w.stats[2], w.work, s));
-        FROB_CUDA(inv_from_lu<double>(n, w.W3, ld, w.W1, w.W4, Re, ld, nullptr, w.flags + 2, s));
+        FROB_CUDA(inv_from_lu<double>(n, w.W3, ld, Sa, w.W4, Re, ld, nullptr, w.flags + 2, s));
     }
     // a6/a7: Im' = -C Re', fused with the column interchanges and the interleaved store
     {
-        auto p = gemm_params<double>(n, n, n, -1.0, w.W2, ld, Re, ld, 0.0, Re, ld, X, ldx);
+        auto p = gemm_params<double>(n, n, n, -1.0, Cb, ld, Re, ld, 0.0, Re, ld, X, ldx);
         p.epi = (use == 1) ? EPI_FROB_A : EPI_FROB_B;
         p.colperm = w.perm_m;
         p.mu = mu;  // Alg 5 line 5: Z^{-1} = (1 + mu i) W
@@ -519,6 +538,13 @@ frob_status frob_inv_rand(int n, const double *Z, long long ldz, double *X, long
                           size_t ws_bytes, void *stream, frob_info *host_info) {
     if (!(mu >= 0.0 && mu <= 1.0)) return FROB_ERR_INVALID_ARG;
     return frob_inv_impl(n, Z, ldz, X, ldx, FROB_BRANCH_AUTO, ws, ws_bytes, (cudaStream_t)stream, host_info, mu);
+}
+
+frob_status frob_inv_opts(int n, const double *Z, long long ldz, double *X, long long ldx, int branch, int options,
+                          void *ws, size_t ws_bytes, void *stream, frob_info *host_info) {
+    if (options & ~FROB_OPT_FUSED_FIRST_STEP) return FROB_ERR_INVALID_ARG;
+    return frob_inv_impl(n, Z, ldz, X, ldx, branch, ws, ws_bytes, (cudaStream_t)stream, host_info, 0.0,
+                         (options & FROB_OPT_FUSED_FIRST_STEP) != 0);
 }
 
 size_t frob_inv_host_workspace_bytes(int n) {

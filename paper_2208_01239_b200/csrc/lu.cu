@@ -889,6 +889,17 @@ __global__ void extract_ul_kernel(const T *__restrict__ lu, long long ld, int n,
     }
 }
 
+template <typename T>
+cudaError_t extract_ul(int n, const T *lu, long long ld, T *U, T *L, cudaStream_t s) {
+    const long long total = (long long)n * n;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+    count_launch();
+    extract_ul_kernel<T><<<blocks, 256, 0, s>>>(lu, ld, n, U, L);
+    return cudaGetLastError();
+}
+template cudaError_t extract_ul<double>(int, const double *, long long, double *, double *, cudaStream_t);
+template cudaError_t extract_ul<double2>(int, const double2 *, long long, double2 *, double2 *, cudaStream_t);
+
 // blockIdx.y == 0: invert upper diagonal blocks of U in place; == 1: unit-lower blocks of L
 template <typename T>
 __global__ void __launch_bounds__(TRI_LEAF) tri_leaf_kernel(T *__restrict__ U, T *__restrict__ L,
@@ -975,9 +986,9 @@ cudaError_t inv_from_lu(int n, T *lu, long long ld, T *U, T *L, T *out, long lon
     return inv_from_ul<T>(n, U, L, ld, lu, out, ldo, colperm, counter, s);  // the LU factors are scratch now
 }
 
+// U <- U^{-1}, L <- L^{-1} in place (32 x 32 diagonal inverses + log-depth recursion)
 template <typename T>
-cudaError_t inv_from_ul(int n, T *U, T *L, long long ld, T *tmp, T *out, long long ldo, const int *colperm,
-                        int *counter, cudaStream_t s) {
+cudaError_t tri_inverses(int n, T *U, T *L, long long ld, T *tmp, cudaStream_t s) {
     cudaError_t e;
     if ((e = launch_pdl(tri_leaf_kernel<T>, dim3((n + TRI_LEAF - 1) / TRI_LEAF, 2), dim3(TRI_LEAF), 0, s, U, L, ld, n,
                         0)) != cudaSuccess)
@@ -990,6 +1001,16 @@ cudaError_t inv_from_ul(int n, T *U, T *L, long long ld, T *tmp, T *out, long lo
             if ((e = tri_level<T>(U, L, tmp, ld, sz, o, n - o - sz, 1, s)) != cudaSuccess) return e;
         }
     }
+    return cudaSuccess;
+}
+template cudaError_t tri_inverses<double>(int, double *, double *, long long, double *, cudaStream_t);
+template cudaError_t tri_inverses<double2>(int, double2 *, double2 *, long long, double2 *, cudaStream_t);
+
+template <typename T>
+cudaError_t inv_from_ul(int n, T *U, T *L, long long ld, T *tmp, T *out, long long ldo, const int *colperm,
+                        int *counter, cudaStream_t s) {
+    cudaError_t e;
+    if ((e = tri_inverses<T>(n, U, L, ld, tmp, s)) != cudaSuccess) return e;
     // X = U^{-1} L^{-1}: (upper) x (lower) -> k from max(row0, col0)
     auto p = gemm_params<T>(n, n, n, 1.0, U, ld, L, ld, 0.0, nullptr, ld, out, ldo);
     p.triA = TRI_UPPER;

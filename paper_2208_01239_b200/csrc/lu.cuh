@@ -66,6 +66,12 @@ cudaError_t lu3_factor(int n, T *A, long long ld, T *U, T *L, int *perm, int *iw
                        cudaStream_t s);
 template <typename T>
 cudaError_t lu_stats_launch(const T *diag, int n, LuStats *st, cudaStream_t s);
+// U = triu(lu) (zeros below), L = tril(lu, -1) + I (zeros above)
+template <typename T>
+cudaError_t extract_ul(int n, const T *lu, long long ld, T *U, T *L, cudaStream_t s);
+// U <- U^{-1} (upper), L <- L^{-1} (unit lower) in place; tmp: n x ld scratch
+template <typename T>
+cudaError_t tri_inverses(int n, T *U, T *L, long long ld, T *tmp, cudaStream_t s);
 // Xinv = U^{-1} L^{-1} from split factors (U, L destroyed; scratch n x ld)
 template <typename T>
 cudaError_t inv_from_ul(int n, T *U, T *L, long long ld, T *scratch, T *out, long long ldo, const int *colperm,

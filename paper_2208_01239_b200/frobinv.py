@@ -39,6 +39,7 @@ _FIP = ctypes.POINTER(FrobInfo)
 SIGNATURES = {
     "frob_inv_workspace_bytes": (_sz, [_i]),
     "frob_inv": (_i, [_i, _vp, _ll, _vp, _ll, _i, _vp, _sz, _vp, _FIP]),
+    "frob_inv_opts": (_i, [_i, _vp, _ll, _vp, _ll, _i, _i, _vp, _sz, _vp, _FIP]),
     "frob_inv_rand": (_i, [_i, _vp, _ll, _vp, _ll, _d, _vp, _sz, _vp, _FIP]),
     "frob_inv_host_workspace_bytes": (_sz, [_i]),
     "frob_inv_host": (_i, [_i, _vp, _vp, _i, _vp, _sz, _vp, _FIP]),
@@ -132,8 +133,10 @@ def _check(fn, st, info=None):
 
 
 # ----------------------------------------------------------------------------- single matrix
-def inv(z: torch.Tensor, branch: str = "auto", out: torch.Tensor | None = None, info: bool = False):
-    """Z^{-1} by Frobenius inversion (Alg 1).  z: (n, n) complex128 CUDA tensor."""
+def inv(z: torch.Tensor, branch: str = "auto", out: torch.Tensor | None = None, info: bool = False,
+        fused: bool = False):
+    """Z^{-1} by Frobenius inversion (Alg 1).  z: (n, n) complex128 CUDA tensor.
+    fused=True: NEXT-1 first step C = U^{-1} (L^{-1} (P Y)) (FROB_OPT_FUSED_FIRST_STEP)."""
     L = load()
     _need_cuda(z, "z")
     assert z.dtype == torch.complex128 and z.dim() == 2 and z.shape[0] == z.shape[1]
@@ -142,8 +145,8 @@ def inv(z: torch.Tensor, branch: str = "auto", out: torch.Tensor | None = None, 
     x = out if out is not None else torch.empty((n, n), dtype=torch.complex128, device=z.device)
     ws = workspace(L.frob_inv_workspace_bytes(n), z.device)
     fi = FrobInfo()
-    st = L.frob_inv(n, _p(z), z.stride(0), _p(x), x.stride(0), BRANCH[branch], _p(ws), ws.numel(),
-                    _stream(), ctypes.byref(fi) if info else None)
+    st = L.frob_inv_opts(n, _p(z), z.stride(0), _p(x), x.stride(0), BRANCH[branch], 1 if fused else 0,
+                         _p(ws), ws.numel(), _stream(), ctypes.byref(fi) if info else None)
     _check("frob_inv", st, fi.as_dict() if info else None)
     return (x, fi.as_dict()) if info else x
 

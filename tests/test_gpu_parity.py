@@ -144,6 +144,26 @@ def test_zinv_lu(n):
     _check_inverse(z, _np(fb.zinv(_t(z))))
 
 
+# ------------------------------------------------------------------ NEXT-1 fused first step
+@pytest.mark.parametrize("n", [1, 2, 33, 256, 513, 1024, 2048])
+@pytest.mark.parametrize("branch", ["auto", "b"])
+def test_frob_inv_fused_first_step(n, branch):
+    """C = U^{-1}(L^{-1}(P Y)) instead of X^{-1} Y: same oracle, same bounds; both LU paths."""
+    z = synth.shifted_complex(n, seed=900 + n, shift=math.sqrt(n) + 2.0)
+    if branch == "b":
+        z = z.imag * 0.5 + 1j * z.real
+    x, info = fb.inv(_t(z), branch=branch, info=True, fused=True)
+    x = _np(x)
+    if n <= 1024:
+        _check_inverse(z, x)
+    else:
+        xo, st, _ = oracle.frob_inv(z, branch)
+        assert st == 0 and oracle.rel_fro(x, xo) <= REL
+        assert _resid(z, x) <= 1e-11 * n
+    x_lit = _np(fb.inv(_t(z), branch=branch))
+    assert oracle.rel_fro(x, x_lit) <= 1e-11  # two roundings of the same Alg 1 (kappa ~ 2e3 at n = 2048)
+
+
 # ------------------------------------------------------------------ Alg 5 (randomized)
 @pytest.mark.parametrize("n", [1, 7, 64, 300, 1024])
 def test_frob_inv_rand_vs_oracle(n):
