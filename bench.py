@@ -56,6 +56,16 @@ def parse():
     return ap.parse_args()
 
 
+def fp64_alu_peak():
+    """Measured FP64 DFMA (non-tensor) peak (tools/fp64_peak.cu)."""
+    try:
+        with open(PEAKS_FILE) as f:
+            d = json.load(f)
+        return float(d["dfma_tflops"]), "measured: tools/fp64_peak.cu DFMA register loop, 148 SMs"
+    except Exception:
+        return 37.2, "nominal: 148 SMs x 64 DFMA/clk x 2 x 1.965 GHz"
+
+
 def fp64_peak():
     """Measured FP64 tensor (DMMA) peak on this pool's B200 (tools/fp64_peak.cu)."""
     try:
@@ -436,11 +446,43 @@ def main():
             tb_f = statistics.median(timed(lambda: fb.inv_batched(z32), 3, 1, False))
             tb_z = statistics.median(timed(lambda: fb.zinv_batched(z32), 3, 1, False))
             extras["batched_n32_comparison"] = {"frob_ms": tb_f, "zinv_lu_ms": tb_z, "count": int(z32.shape[0])}
-        # roofline of the GEMM engine (DMMA) at the n x n x n shape of the three Frobenius GEMMs
+        # NEXT-1 (fused first step) and Alg 5 (randomized) on the same input
+        t_fused = statistics.median(timed(lambda: fb.inv(zr, out=xr, fused=True), 5, 2, True))
+        t_rand = statistics.median(timed(lambda: fb.inv_rand(zr, mu=0.5, out=xr), 5, 2, True))
+        extras["comparison_single_n"].update({
+            "frobenius_fused_first_step_ms": t_fused, "frobenius_fused_tflops_alg": (28.0 / 3.0) * n ** 3 / t_fused / 1e9,
+            "frobenius_randomized_ms": t_rand})
+        # GEMM engine (DMMA) at the n x n x n shape of the three Frobenius GEMMs
         ach = 2.0 * n ** 3 / t_mult / 1e9
-        extras["roofline"] = {"bound": "tensor", "kernel": "gemm_kernel<double> (DMMA m8n8k4), n x n x n",
-                              "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                              "traffic": None, "peak_source": peak_src}
+        extras["roofline_gemm"] = {"bound": "tensor", "kernel": "gemm_kernel<double> (DMMA m8n8k4), n x n x n",
+                                   "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                                   "peak_source": peak_src}
+        # dominant kernel of the timed step: a separate instrumented pass (CUDA events recorded by
+        # the library on the stream each kernel is launched on), never inside the timed region
+        fbi.profile_enable(True)
+        pw = timed(wl.step, max(2, min(args.steps, 5)), 1, wl.flush)
+        prof = fbi.profile_read()
+        fbi.profile_enable(False)
+        if prof:
+            name, d = max(prof.items(), key=lambda kv: kv[1]["total_ms"])
+            avg_ms = d["total_ms"] / max(1, d["launches"])
+            ach_k = d["flops"] / max(1, d["launches"]) / (avg_ms * 1e-3) / 1e12
+            tensor = name.startswith("gemm")
+            pk, pk_src = (peak, peak_src) if tensor else fp64_alu_peak()
+            steps_prof = len(pw) + 1
+            extras["roofline"] = {
+                "bound": "tensor" if tensor else "alu", "kernel": name, "achieved": ach_k, "peak": pk,
+                "unit": "TFLOP/s", "frac": ach_k / pk, "traffic": None, "peak_source": pk_src,
+                "flops_per_launch": d["flops"] / max(1, d["launches"]), "avg_launch_ms": avg_ms,
+                "launches_per_step": d["launches"] / steps_prof,
+                "share_of_step": d["total_ms"] / steps_prof / statistics.median(pw),
+                "note": ("FP64 pipe; the LU panel is a latency-bound pivot chain (one pivot search + "
+                         "rank-1 update per column), so its fraction of the FP64 peak is small by nature"
+                         if not tensor else "DMMA tensor pipe")}
+            extras["kernel_profile"] = {k: {"launches_per_step": v["launches"] / steps_prof,
+                                            "ms_per_step": v["total_ms"] / steps_prof,
+                                            "tflops": v["flops"] / (v["total_ms"] * 1e-3) / 1e12 if v["total_ms"] else None}
+                                        for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["total_ms"])}
         e2e = timed(wl.e2e_step, max(3, args.steps // 2), 1, False)
         e2e_ms = fdist.max_over_ranks(statistics.median(e2e), dev)
         extras["e2e"] = {"value": units_all * 1e3 / e2e_ms, "unit": UNIT,

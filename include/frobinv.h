@@ -192,6 +192,16 @@ int frob_version(void);
  * (monotonic; used by bench.py to report gpu_launches). */
 unsigned long long frob_launch_count(void);
 
+/* Optional per-kernel timing for measurement tools (off by default; not thread-safe with
+ * concurrent library calls).  frob_profile_enable(1) clears and starts recording: every
+ * instrumented launch (LU panel, fused LU update, GEMM engine) is bracketed by CUDA events
+ * on the stream it is launched on.  frob_profile_read synchronises the recorded events and
+ * writes {"name": {"launches": L, "total_ms": T}, ...} (JSON, NUL-terminated) into buf;
+ * returns the JSON length (call with buf = NULL to size it) or -1 on a CUDA error.
+ * Instrumented runs are slower (events between launches); time the product separately. */
+void frob_profile_enable(int on);
+int frob_profile_read(char *buf, size_t len);
+
 #ifdef __cplusplus
 }
 #endif

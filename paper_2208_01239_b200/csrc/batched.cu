@@ -626,18 +626,21 @@ frob_status frob_inv_batched(int n, int batch, const double *Z, long long stride
         const size_t smem = sizeof(FrobSmem<32>);
         if ((e = set_smem(frob_batched_kernel<32>, smem)) != cudaSuccess) return FROB_ERR_CUDA;
         count_launch();
+        ProfScope ps("frob_batched<32>", s, 10.0 * n * (double)n * n * batch);
         frob_batched_kernel<32><<<batch, BCfg<32>::THREADS, smem, s>>>(Zc, strideZ, Xc, strideX, n, branch,
                                                                        d_info, d_branch_used);
     } else if (n <= 64) {
         const size_t smem = sizeof(FrobSmem<64>);
         if ((e = set_smem(frob_batched_kernel<64>, smem)) != cudaSuccess) return FROB_ERR_CUDA;
         count_launch();
+        ProfScope ps("frob_batched<64>", s, 10.0 * n * (double)n * n * batch);
         frob_batched_kernel<64><<<batch, BCfg<64>::THREADS, smem, s>>>(Zc, strideZ, Xc, strideX, n, branch,
                                                                        d_info, d_branch_used);
     } else {
         const size_t smem = sizeof(Frob128Smem);
         if ((e = set_smem(frob_batched128_kernel, smem)) != cudaSuccess) return FROB_ERR_CUDA;
         count_launch();
+        ProfScope ps("frob_batched128", s, 10.0 * n * (double)n * n * batch);
         frob_batched128_kernel<<<batch, 1024, smem, s>>>(Zc, strideZ, Xc, strideX, n, branch, d_info,
                                                          d_branch_used);
     }
@@ -659,11 +662,13 @@ frob_status zinv_lu_batched(int n, int batch, const double *Z, long long strideZ
         const size_t smem = sizeof(ZSmem<32>);
         if ((e = set_smem(zinv_batched_kernel<32>, smem)) != cudaSuccess) return FROB_ERR_CUDA;
         count_launch();
+        ProfScope ps("zinv_batched<32>", s, 8.0 * n * (double)n * n * batch);
         zinv_batched_kernel<32><<<batch, BCfg<32>::THREADS, smem, s>>>(Zc, strideZ, Xc, strideX, n, d_info);
     } else {
         const size_t smem = sizeof(ZSmem<64>);
         if ((e = set_smem(zinv_batched_kernel<64>, smem)) != cudaSuccess) return FROB_ERR_CUDA;
         count_launch();
+        ProfScope ps("zinv_batched<64>", s, 8.0 * n * (double)n * n * batch);
         zinv_batched_kernel<64><<<batch, BCfg<64>::THREADS, smem, s>>>(Zc, strideZ, Xc, strideX, n, d_info);
     }
     return cudaGetLastError() == cudaSuccess ? FROB_OK : FROB_ERR_CUDA;

@@ -14,6 +14,23 @@ namespace frob {
 unsigned long long &launch_counter();
 inline void count_launch(unsigned long long k = 1) { __atomic_fetch_add(&launch_counter(), k, __ATOMIC_RELAXED); }
 
+// Optional per-kernel timing (frob_profile_enable): CUDA events recorded on the launching
+// stream around instrumented launches; off by default (then a no-op).
+bool prof_enabled();
+// work: algorithmic flops of the launch (FP64; complex multiply-add = 8 real flops)
+void prof_record(const char *name, cudaStream_t s, bool begin, double work);
+struct ProfScope {
+    const char *name;
+    cudaStream_t s;
+    bool on;
+    ProfScope(const char *nm, cudaStream_t st, double work = 0.0) : name(nm), s(st), on(prof_enabled()) {
+        if (on) prof_record(name, s, true, work);
+    }
+    ~ProfScope() {
+        if (on) prof_record(name, s, false, 0.0);
+    }
+};
+
 // ------------------------------------------------------------------ element ops
 FROB_DEV double zero_of(double) { return 0.0; }
 FROB_DEV double2 zero_of(double2) { return make_double2(0.0, 0.0); }

@@ -6,12 +6,52 @@
 #include <cstring>
 #include <cmath>
 #include <climits>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
 #include "lu.cuh"
 #include "../../include/frobinv.h"
 
 namespace frob {
 
 static thread_local char g_last_cuda[256] = "";
+
+// ---------------------------------------------------------------------- kernel profiler
+struct ProfEv {
+    const char *name;
+    cudaEvent_t a, b;
+    double work;
+};
+static std::mutex g_prof_mu;
+static std::vector<ProfEv> g_prof;
+static bool g_prof_on = false;
+struct ProfOpen {
+    const char *name;
+    cudaEvent_t e;
+    double work;
+};
+static std::vector<ProfOpen> g_prof_open;
+
+bool prof_enabled() { return g_prof_on; }
+void prof_record(const char *name, cudaStream_t s, bool begin, double work) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, s);
+    if (begin) {
+        g_prof_open.push_back({name, e, work});
+    } else {
+        for (size_t i = g_prof_open.size(); i-- > 0;) {
+            if (g_prof_open[i].name == name) {
+                g_prof.push_back({name, g_prof_open[i].e, e, g_prof_open[i].work});
+                g_prof_open.erase(g_prof_open.begin() + (long)i);
+                return;
+            }
+        }
+        cudaEventDestroy(e);
+    }
+}
 
 unsigned long long &launch_counter() {
     static unsigned long long c = 0;
@@ -689,6 +729,44 @@ const char *frob_status_string(int status) {
 }
 
 const char *frob_last_cuda_error(void) { return g_last_cuda; }
+
+void frob_profile_enable(int on) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    for (auto &r : g_prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto &r : g_prof_open) cudaEventDestroy(r.e);
+    g_prof.clear();
+    g_prof_open.clear();
+    g_prof_on = on != 0;
+}
+
+int frob_profile_read(char *buf, size_t len) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    struct Agg { long long cnt = 0; double ms = 0.0, work = 0.0; };
+    std::map<std::string, Agg> agg;
+    for (auto &r : g_prof) {
+        if (cudaEventSynchronize(r.b) != cudaSuccess) return -1;
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) return -1;
+        auto &a = agg[r.name];
+        a.cnt += 1;
+        a.ms += ms;
+        a.work += r.work;
+    }
+    std::string out = "{";
+    bool first = true;
+    for (auto &kv : agg) {
+        char tmp[320];
+        snprintf(tmp, sizeof(tmp), "%s\"%s\": {\"launches\": %lld, \"total_ms\": %.6f, \"flops\": %.6e}",
+                 first ? "" : ", ", kv.first.c_str(), kv.second.cnt, kv.second.ms, kv.second.work);
+        out += tmp;
+        first = false;
+    }
+    out += "}";
+    if (buf && len > 0) {
+        snprintf(buf, len, "%s", out.c_str());
+    }
+    return (int)out.size();
+}
 
 unsigned long long frob_launch_count(void) { return frob::launch_counter(); }
 

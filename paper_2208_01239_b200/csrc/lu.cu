@@ -17,6 +17,18 @@ namespace frob {
 // =====================================================================================
 // GEMM launcher
 // =====================================================================================
+// algorithmic flops of a (paired, batched) launch: 2 M N K, halved per triangular operand
+template <typename T>
+static double gemm_work(const GemmPair<T> &pp, int b0, int b1) {
+    auto one = [](const GemmParams<T> &p) {
+        double f = 2.0 * p.M * (double)p.N * p.K;
+        if (p.triA != TRI_NONE) f *= 0.5;
+        if (p.triB != TRI_NONE) f *= (p.triA != TRI_NONE) ? (2.0 / 3.0) : 0.5;
+        return f * (sizeof(T) == 8 ? 1.0 : 4.0);
+    };
+    return one(pp.q[0]) * b0 + (b1 > 0 ? one(pp.q[1]) * b1 : 0.0);
+}
+
 // split-K needs C = beta * D before the atomic adds: beta == 0 (C zeroed here) or D == C with
 // beta == 1 (accumulate in place); no fused epilogues
 template <typename T>
@@ -64,6 +76,7 @@ static cudaError_t gemm_launch_cfg(const GemmPair<T> &pp, int batch0, int batch1
         const int grid = min(D * D, 148 * 3);
         cudaError_t e = cudaMemsetAsync(p0.counter, 0, sizeof(int), s);
         if (e != cudaSuccess) return e;
+        ProfScope ps(sizeof(T) == 8 ? "gemm<double>" : "gemm<double2>", s, gemm_work(pp, batch0, batch1));
         return launch_pdl(gemm_kernel<T, VEC, BIG>, dim3(grid, 1, 1), dim3(Cf::WGM * Cf::WGN * 32), smem, s, pp);
     }
     int M = p0.M, N = p0.N;
@@ -104,6 +117,7 @@ static cudaError_t gemm_launch_cfg(const GemmPair<T> &pp, int batch0, int batch1
     }();
     const bool early = policy == 2 || (policy == 1 && ctas <= 148LL * (BIG ? 1 : 3));
     q.q[0].early_trigger = q.q[1].early_trigger = early ? 1 : 0;
+    ProfScope ps(sizeof(T) == 8 ? "gemm<double>" : "gemm<double2>", s, gemm_work(pp, batch0, batch1));
     return launch_pdl(gemm_kernel<T, VEC, BIG>, grid, dim3(Cf::WGM * Cf::WGN * 32), smem, s, q);
 }
 
@@ -832,6 +846,9 @@ static cudaError_t launch_panel_r(T *P, long long lda, int m, int w, int k0, int
         if (e != cudaSuccess) return e;
         attr_set[dev] = true;
     }
+    double wk = 0.0;
+    for (int j = 0; j < w; ++j) wk += (double)(m - j - 1) * (1.0 + 2.0 * (w - j - 1));
+    ProfScope ps(sizeof(T) == 8 ? "lu_panel<double>" : "lu_panel<double2>", s, wk * (sizeof(T) == 8 ? 1.0 : 4.0));
     if (CS == 1) {
         return launch_pdl(lu_panel_kernel<T, PW, R, false>, dim3(1), dim3(PANEL_T), smem, s, P, lda, m, w, 1, k0,
                           mv, diag, cb, ce, perm);
@@ -1099,6 +1116,7 @@ static cudaError_t panel_step(int n, T *A, long long lda, int cb, int ce, int k0
         return e;
     const int ncols = ce - cb - w;
     if (!fused || ncols <= 0) {
+        ProfScope ps(sizeof(T) == 8 ? "lu_swap_trsm<double>" : "lu_swap_trsm<double2>", s);
         if ((e = launch_pdl(lu_swap_trsm_kernel<T, PW>, dim3(max(1, (ncols + SWP_COLS - 1) / SWP_COLS)),
                             dim3(SWP_COLS), 0, s, A, lda, cb, ce, k0, w, list, perm)) != cudaSuccess)
             return e;

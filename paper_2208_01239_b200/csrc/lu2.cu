@@ -556,6 +556,10 @@ static cudaError_t launch_panel2(const CUtensorMap &tm, T *B, long long ld, int 
         if (e != cudaSuccess) return e;
         attr_set[dev] = true;
     }
+    // panel flops: column j scales m-j-1 rows and updates their w-j-1 remaining entries
+    double wk = 0.0;
+    for (int j = 0; j < w; ++j) wk += (double)(n - k0 - j - 1) * (1.0 + 2.0 * (w - j - 1));
+    ProfScope ps(sizeof(T) == 8 ? "lu_panel2<double>" : "lu_panel2<double2>", s, wk * (sizeof(T) == 8 ? 1.0 : 4.0));
     return launch_pdl(lu_panel2_kernel<T, PW, R>, dim3(1), dim3(P2_T), smem, s, tm, B, ld, n, k0, w, mv2, diag);
 }
 
@@ -586,6 +590,8 @@ cudaError_t lu2_factor(int n, T *B0, T *B1, long long ld, T *U, T *L, long long 
         if (e != cudaSuccess) return e;
         const int rest = n - k0 - w;
         dim3 grid(max(1, (rest + U2_TC - 1) / U2_TC), max(1, (rest + U2_TR - 1) / U2_TR));
+        const double upd = ((double)(m - w) * 2.0 * w + (double)w * w) * (double)rest;  // GEMM + TRSM
+        ProfScope ps(sizeof(T) == 8 ? "lu_update2<double>" : "lu_update2<double2>", s, upd * (sizeof(T) == 8 ? 1.0 : 4.0));
         e = launch_pdl(lu_update2_kernel<T, PW>, grid, dim3(U2_T), 0, s, (const T *)Bk, Bn, ld, n, k0, w,
                        (const int *)mv2, perm, iperm, k + 1 < steps ? snap + (size_t)k * n : (int *)nullptr);
         if (e != cudaSuccess) return e;

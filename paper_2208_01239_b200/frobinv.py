@@ -57,6 +57,8 @@ SIGNATURES = {
     "frob_dinv": (_i, [_i, _vp, _ll, _vp, _ll, _vp, _sz, _vp, _FIP]),
     "frob_dgetrf_workspace_bytes": (_sz, [_i]),
     "frob_dgetrf": (_i, [_i, _vp, _ll, _vp, _vp, _sz, _vp, _FIP]),
+    "frob_profile_enable": (None, [_i]),
+    "frob_profile_read": (_i, [ctypes.c_char_p, _sz]),
     "frob_status_string": (ctypes.c_char_p, [_i]),
     "frob_last_cuda_error": (ctypes.c_char_p, []),
     "frob_version": (_i, []),
@@ -94,6 +96,23 @@ def load(path: str = LIB_PATH):
                 f.argtypes = args
             _lib = L
     return _lib
+
+
+def profile_enable(on: bool = True):
+    """Per-kernel CUDA-event timing inside the library (measurement passes only)."""
+    load().frob_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """{kernel: {"launches", "total_ms", "flops"}} of the launches since profile_enable."""
+    import json
+    L = load()
+    n = L.frob_profile_read(None, 0)
+    if n < 0:
+        raise RuntimeError("frob_profile_read failed")
+    buf = ctypes.create_string_buffer(n + 1)
+    L.frob_profile_read(buf, n + 1)
+    return json.loads(buf.value.decode())
 
 
 def launch_count() -> int:
