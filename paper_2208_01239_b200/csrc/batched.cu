@@ -67,6 +67,30 @@ struct SweepShared {
     double pmag_k[N];
 };
 
+// after a sweep: pivot magnitude range (warp-parallel), identity for padding, pos[] = inverse
+// of pivrow[]
+template <typename T, int N, int NT, typename SH>
+FROB_DEV void sweep_finish(SH &sh, int n, double &pmax, double &pmin) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    double mx = 0.0, mn = INFINITY;
+    for (int k = lane; k < n; k += 32) {
+        mx = fmax(mx, sh.pmag_k[k]);
+        mn = fmin(mn, sh.pmag_k[k]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    pmax = mx;
+    pmin = mn;
+    for (int k = tid; k < N; k += NT)
+        if (k >= n) sh.pivrow[k] = k;
+    __syncthreads();
+    for (int k = tid; k < N; k += NT) sh.pos[sh.pivrow[k]] = k;
+    __syncthreads();
+}
+
 // Gauss-Jordan sweep (exchange form, partial pivoting) on the register blocks a[BR][BC]
 // over the leading n x n part of an N x N matrix (padding = identity).  On return the
 // inverse, scattered: A^{-1}[pos[i]][pivrow[j]] = a(i, j).
@@ -124,30 +148,31 @@ FROB_DEV void gj_sweep(T (&a)[BR][BC], int n, SweepShared<T, N> &sh, double &pma
         for (int c = 0; c < BC; ++c) rp[c] = sh.rowp[par][c0 + c];
 #pragma unroll
         for (int q = 0; q < BR; ++q) ck[q] = sh.colk[par][r0 + q];
+        // uniform exchange-form update (see gj_sweep_1bar): zero column k first, pivot row last
+        if (tj == k / BC) {
+            const int kc = k % BC;
 #pragma unroll
-        for (int q = 0; q < BR; ++q) {
-            if (r0 + q == p) {
+            for (int c = 0; c < BC; ++c)
+                if (c == kc) {
 #pragma unroll
-                for (int c = 0; c < BC; ++c) a[q][c] = rp[c];
-            } else {
+                    for (int q = 0; q < BR; ++q) a[q][c] = zero_of(T());
+                }
+        }
 #pragma unroll
-                for (int c = 0; c < BC; ++c)
-                    a[q][c] = (c0 + c == k) ? neg(mul(ck[q], rp[c])) : msub(a[q][c], ck[q], rp[c]);
-            }
+        for (int q = 0; q < BR; ++q)
+#pragma unroll
+            for (int c = 0; c < BC; ++c) a[q][c] = msub(a[q][c], ck[q], rp[c]);
+        if (ti == p / BR) {
+#pragma unroll
+            for (int q = 0; q < BR; ++q)
+                if (r0 + q == p) {
+#pragma unroll
+                    for (int c = 0; c < BC; ++c) a[q][c] = rp[c];
+                }
         }
     }
     __syncthreads();
-    pmax = 0.0;
-    pmin = INFINITY;
-    for (int k = 0; k < n; ++k) {
-        pmax = fmax(pmax, sh.pmag_k[k]);
-        pmin = fmin(pmin, sh.pmag_k[k]);
-    }
-    for (int k = tid; k < N; k += G::THREADS)
-        if (k >= n) sh.pivrow[k] = k;
-    __syncthreads();
-    for (int k = tid; k < N; k += G::THREADS) sh.pos[sh.pivrow[k]] = k;
-    __syncthreads();
+    sweep_finish<T, N, G::THREADS>(sh, n, pmax, pmin);
 }
 
 // One barrier per step.  Thread (ti, tj) owns rows ti*BR.., columns tj*BC..; the CT threads
@@ -202,33 +227,36 @@ FROB_DEV void gj_sweep_1bar(T (&a)[BR][BC], int n, SweepShared1<T, N> &sh, doubl
         const T ip = is_zero(piv) ? zero_of(T()) : recip(piv);
         if (tid == 0) { sh.pivrow[k] = p; sh.pmag_k[k] = pmag(piv); }
         if (tip == ti) used |= 1u << (p - r0);
+        // exchange-form update, uniform over the block: the owner of column k first zeroes it
+        // and puts 1/piv into the pivot-row vector, so a - ck * rp gives -ck/piv there; the
+        // pivot row is overwritten with rp afterwards
         T rp[BC];
 #pragma unroll
-        for (int c = 0; c < BC; ++c) rp[c] = (c0 + c == k) ? ip : mul(sh.slot[par][tip][c0 + c], ip);
+        for (int c = 0; c < BC; ++c) rp[c] = mul(sh.slot[par][tip][c0 + c], ip);
+        if (tj == kb) {
 #pragma unroll
-        for (int q = 0; q < BR; ++q) {
-            if (r0 + q == p) {
+            for (int c = 0; c < BC; ++c)
+                if (c == kc) {
+                    rp[c] = ip;
 #pragma unroll
-                for (int c = 0; c < BC; ++c) a[q][c] = rp[c];
-            } else {
+                    for (int q = 0; q < BR; ++q) a[q][c] = zero_of(T());
+                }
+        }
 #pragma unroll
-                for (int c = 0; c < BC; ++c)
-                    a[q][c] = (c0 + c == k) ? neg(mul(ck[q], rp[c])) : msub(a[q][c], ck[q], rp[c]);
-            }
+        for (int q = 0; q < BR; ++q)
+#pragma unroll
+            for (int c = 0; c < BC; ++c) a[q][c] = msub(a[q][c], ck[q], rp[c]);
+        if (ti == tip) {
+#pragma unroll
+            for (int q = 0; q < BR; ++q)
+                if (r0 + q == p) {
+#pragma unroll
+                    for (int c = 0; c < BC; ++c) a[q][c] = rp[c];
+                }
         }
     }
     __syncthreads();
-    pmax = 0.0;
-    pmin = INFINITY;
-    for (int k = 0; k < n; ++k) {
-        pmax = fmax(pmax, sh.pmag_k[k]);
-        pmin = fmin(pmin, sh.pmag_k[k]);
-    }
-    for (int k = tid; k < N; k += G::THREADS)
-        if (k >= n) sh.pivrow[k] = k;
-    __syncthreads();
-    for (int k = tid; k < N; k += G::THREADS) sh.pos[sh.pivrow[k]] = k;
-    __syncthreads();
+    sweep_finish<T, N, G::THREADS>(sh, n, pmax, pmin);
 }
 
 // write the sweep result as the inverse into a row-major matrix M (stride ldm)
@@ -269,9 +297,12 @@ FROB_DEV void load_blocks(T (&a)[4][4], const T *M, int n) {
 template <typename T, int N, typename SH>
 FROB_DEV int sweep_info(const SH &sh, int n, double pmax) {
     const double thr = 100.0 * n * 1.1102230246251565e-16 * pmax;
-    for (int k = 0; k < n; ++k)
-        if (!(sh.pmag_k[k] >= thr) || sh.pmag_k[k] == 0.0) return k + 1;
-    return 0;
+    const int lane = threadIdx.x & 31;
+    int first = INT_MAX;
+    for (int k = lane; k < n; k += 32)
+        if (!(sh.pmag_k[k] >= thr) || sh.pmag_k[k] == 0.0) { first = k; break; }
+    first = (int)redux_min((unsigned)first);
+    return first == INT_MAX ? 0 : first + 1;
 }
 
 // ----------------------------------------------------------------- in-CTA DMMA GEMM
