@@ -15,6 +15,7 @@
 // Alg 3 (2n^3 flops) with n sequential steps instead of 3n ("batched path").
 #include <climits>
 #include <cmath>
+#include <utility>
 #include "common.cuh"
 #include "../../include/frobinv.h"
 
@@ -34,6 +35,15 @@ struct BCfg {
     static constexpr int S = N + 4;
     static constexpr int THREADS = Geo<N>::THREADS;
 };
+
+template <typename F, int... J>
+FROB_DEV void bstatic_for_impl(F &&f, std::integer_sequence<int, J...>) {
+    (f(std::integral_constant<int, J>{}), ...);
+}
+template <int K, typename F>
+FROB_DEV void bstatic_for(F &&f) {
+    bstatic_for_impl(f, std::make_integer_sequence<int, K>{});
+}
 
 // static-index select from a small register array (avoids local-memory indexing)
 template <typename T, int K>
@@ -105,16 +115,19 @@ FROB_DEV void gj_sweep(T (&a)[BR][BC], int n, SweepShared<T, N> &sh, double &pma
     // are reduced after the loop
     for (int k = tid; k < N; k += G::THREADS) sh.pos[k] = 0;
     __syncthreads();
-    for (int k = 0; k < n; ++k) {
+    // one step of the sweep; the column's position inside its register block (KC) is a
+    // compile-time constant (the steps are unrolled by BC), so no register selects on it
+    auto step = [&](const int k, auto KCc) {
+        constexpr int KC = decltype(KCc)::value;
         const int par = k & 1;
-        if (tj == k / BC) {
-            const int cc = k % BC;
+        const bool owner = (tj == k / BC);
+        if (owner) {
             unsigned long long bk = 0;
             int bi = INT_MAX;
 #pragma unroll
             for (int q = 0; q < BR; ++q) {
                 const int r = r0 + q;
-                const T v = sel_k<T, BC>(a[q], cc);
+                const T v = a[q][KC];
                 sh.colk[par][r] = v;
                 if (r < n && !sh.pos[r]) {
                     const unsigned long long kk = pkey_bits(v);
@@ -139,7 +152,7 @@ FROB_DEV void gj_sweep(T (&a)[BR][BC], int n, SweepShared<T, N> &sh, double &pma
 #pragma unroll
                 for (int qq = 1; qq < BR; ++qq)
                     if (q == qq) v = a[qq][c];
-                sh.rowp[par][c0 + c] = (c0 + c == k) ? ip : mul(v, ip);
+                sh.rowp[par][c0 + c] = (owner && c == KC) ? ip : mul(v, ip);
             }
         }
         __syncthreads();
@@ -148,15 +161,11 @@ FROB_DEV void gj_sweep(T (&a)[BR][BC], int n, SweepShared<T, N> &sh, double &pma
         for (int c = 0; c < BC; ++c) rp[c] = sh.rowp[par][c0 + c];
 #pragma unroll
         for (int q = 0; q < BR; ++q) ck[q] = sh.colk[par][r0 + q];
-        // uniform exchange-form update (see gj_sweep_1bar): zero column k first, pivot row last
-        if (tj == k / BC) {
-            const int kc = k % BC;
+        // uniform exchange-form update: the owner of column k zeroes it first (a - ck * rp then
+        // gives -ck / piv there), the pivot row is written last
+        if (owner) {
 #pragma unroll
-            for (int c = 0; c < BC; ++c)
-                if (c == kc) {
-#pragma unroll
-                    for (int q = 0; q < BR; ++q) a[q][c] = zero_of(T());
-                }
+            for (int q = 0; q < BR; ++q) a[q][KC] = zero_of(T());
         }
 #pragma unroll
         for (int q = 0; q < BR; ++q)
@@ -170,6 +179,13 @@ FROB_DEV void gj_sweep(T (&a)[BR][BC], int n, SweepShared<T, N> &sh, double &pma
                     for (int c = 0; c < BC; ++c) a[q][c] = rp[c];
                 }
         }
+    };
+    for (int kb = 0; kb * BC < n; ++kb) {
+        bstatic_for<BC>([&](auto KCc) {
+            constexpr int KC = decltype(KCc)::value;
+            const int k = kb * BC + KC;
+            if (k < n) step(k, KCc);
+        });
     }
     __syncthreads();
     sweep_finish<T, N, G::THREADS>(sh, n, pmax, pmin);
@@ -310,7 +326,7 @@ FROB_DEV int sweep_info(const SH &sh, int n, double pmax) {
 template <int N> struct WT;
 template <> struct WT<32> { static constexpr int WGM = 2, WGN = 1, MT = 2, NT = 4; };
 template <> struct WT<64> { static constexpr int WGM = 2, WGN = 4, MT = 4, NT = 2; };
-template <> struct WT<128> { static constexpr int WGM = 4, WGN = 8, MT = 2, NT = 2; };  // per 64-row half, 32 warps
+template <> struct WT<128> { static constexpr int WGM = 2, WGN = 8, MT = 4, NT = 2; };  // per 64-row half, 16 warps
 
 // acc = op_A * op_B over an N x N x N product with operands given by accessors
 // fa(row, k) and fb(k, col) (shared or global memory; DMMA fragments loaded directly).
@@ -475,6 +491,10 @@ frob_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__rest
 // 512 threads, 4x8 register blocks for the sweeps; one 135 KB shared buffer (X^{-1}, then
 // M, then Re); C = X^{-1} Y lives in the first half of the OUTPUT matrix (planar n x n
 // doubles) until the final epilogue overwrites it with the interleaved result.
+// 512 threads, 4 x 8 register blocks (32 FMAs per thread per sweep step): fewer per-step
+// bookkeeping instructions than 1024 x (4 x 4), more warps to hide latency than 256 x (8 x 8)
+constexpr int R128 = 4, B128 = 8;
+constexpr int T128 = (128 / R128) * (128 / B128);
 struct Frob128Smem {
     double S[128 * 132];
     SweepShared<double, 128> sw;
@@ -509,12 +529,12 @@ FROB_DEV void frob128_rest(const double2 *__restrict__ Zb, double2 *__restrict__
     __syncthreads();
     // a5: Re = M^{-1} -> S
     {
-        double a[4][4];
+        double a[R128][B128];
         double pmax, pmin;
-        load_blocks_f<double, N, 4, 4>(a, n, [&](int i, int j) { return S[i * SS + j]; });
-        gj_sweep<double, N, 4, 4>(a, n, sw, pmax, pmin);
+        load_blocks_f<double, N, R128, B128>(a, n, [&](int i, int j) { return S[i * SS + j]; });
+        gj_sweep<double, N, R128, B128>(a, n, sw, pmax, pmin);
         inf_m = sweep_info<double, N>(sw, n, pmax);
-        sweep_store<double, N, 4, 4>(a, sw, S, SS);
+        sweep_store<double, N, R128, B128>(a, sw, S, SS);
     }
     __syncthreads();
     // a6/a7: Im = -C Re, interleaved store (after every warp has finished reading its C rows)
@@ -532,7 +552,7 @@ FROB_DEV void frob128_rest(const double2 *__restrict__ Zb, double2 *__restrict__
     }
 }
 
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(T128, 1)
 frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__restrict__ X, long long sX, int n,
                        int branch, int *__restrict__ info, unsigned char *__restrict__ bused) {
     constexpr int N = 128, SS = 132;
@@ -550,27 +570,27 @@ frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
     int use = (branch == FROB_BRANCH_B) ? 2 : 1;
     int inf_x;
     {
-        double a[4][4];
+        double a[R128][B128];
         double pmax, pmin;
-        if (use == 1) load_blocks_f<double, N, 4, 4>(a, n, [&](int i, int j) { return Zb[i * n + j].x; });
-        else load_blocks_f<double, N, 4, 4>(a, n, [&](int i, int j) { return Zb[i * n + j].y; });
-        gj_sweep<double, N, 4, 4>(a, n, sm.sw, pmax, pmin);
+        if (use == 1) load_blocks_f<double, N, R128, B128>(a, n, [&](int i, int j) { return Zb[i * n + j].x; });
+        else load_blocks_f<double, N, R128, B128>(a, n, [&](int i, int j) { return Zb[i * n + j].y; });
+        gj_sweep<double, N, R128, B128>(a, n, sm.sw, pmax, pmin);
         inf_x = sweep_info<double, N>(sm.sw, n, pmax);
-        sweep_store<double, N, 4, 4>(a, sm.sw, S, SS);
+        sweep_store<double, N, R128, B128>(a, sm.sw, S, SS);
         if (branch == FROB_BRANCH_AUTO) {
             const double rho_a = (pmin > 0.0) ? pmax / pmin : INFINITY;
             if (inf_x != 0 || !(rho_a <= 256.0)) {
                 __syncthreads();
-                load_blocks_f<double, N, 4, 4>(a, n, [&](int i, int j) { return Zb[i * n + j].y; });
+                load_blocks_f<double, N, R128, B128>(a, n, [&](int i, int j) { return Zb[i * n + j].y; });
                 double qmax, qmin;
-                gj_sweep<double, N, 4, 4>(a, n, sm.sw, qmax, qmin);
+                gj_sweep<double, N, R128, B128>(a, n, sm.sw, qmax, qmin);
                 const int inf_b = sweep_info<double, N>(sm.sw, n, qmax);
                 const double rho_b = (qmin > 0.0) ? qmax / qmin : INFINITY;
                 if (inf_b == 0 && (inf_x != 0 || rho_b < rho_a)) {
                     use = 2;
                     inf_x = 0;
                     __syncthreads();
-                    sweep_store<double, N, 4, 4>(a, sm.sw, S, SS);
+                    sweep_store<double, N, R128, B128>(a, sm.sw, S, SS);
                 } else if (inf_b != 0 && inf_x != 0) {
                     inf_x = -1;
                 }
@@ -672,7 +692,7 @@ frob_status frob_inv_batched(int n, int batch, const double *Z, long long stride
         if ((e = set_smem(frob_batched128_kernel, smem)) != cudaSuccess) return FROB_ERR_CUDA;
         count_launch();
         ProfScope ps("frob_batched128", s, 10.0 * n * (double)n * n * batch);
-        frob_batched128_kernel<<<batch, 1024, smem, s>>>(Zc, strideZ, Xc, strideX, n, branch, d_info,
+        frob_batched128_kernel<<<batch, T128, smem, s>>>(Zc, strideZ, Xc, strideX, n, branch, d_info,
                                                          d_branch_used);
     }
     return cudaGetLastError() == cudaSuccess ? FROB_OK : FROB_ERR_CUDA;
