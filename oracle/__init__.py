@@ -234,6 +234,28 @@ def polar_newton(a, tol: float = 1e-12, max_iter: int = 50, method: str = "frobe
     return x, h, len(deltas), deltas
 
 
+def sylvester_sign(a, b, c, tol: float = 1e-12, max_iter: int = 50, method: str = "frobenius"):
+    """A X + X B = C via the matrix sign function: for sign(A) = I, sign(B) = I,
+    sign([[A, -C], [0, -B]]) = [[I, -2X], [0, -I]].  Newton X_{t+1} = (X_t + X_t^{-1})/2 from
+    X_0 = [[A, -C], [0, -B]] (sign_newton above); X = -S_12 / 2.  Returns (X, iters, deltas)."""
+    a = np.asarray(a, dtype=np.complex128)
+    b = np.asarray(b, dtype=np.complex128)
+    c = np.asarray(c, dtype=np.complex128)
+    m, n = a.shape[0], b.shape[0]
+    t = np.zeros((m + n, m + n), dtype=np.complex128)
+    t[:m, :m] = a
+    t[:m, m:] = -c
+    t[m:, m:] = -b
+    s, it, d = sign_newton(t, tol=tol, max_iter=max_iter, method=method)
+    return -0.5 * s[:m, m:], it, d
+
+
+def lyapunov_sign(a, c, tol: float = 1e-12, max_iter: int = 50, method: str = "frobenius"):
+    """A X + X A^* = C: the Sylvester solver with B = A^*."""
+    a = np.asarray(a, dtype=np.complex128)
+    return sylvester_sign(a, a.conj().T, c, tol, max_iter, method)
+
+
 # --------------------------------------------------------------- metrics
 def max_norm(z) -> float:
     """||A + iB||_max = max(||A||_max, ||B||_max)  (P:L1072-1074)."""

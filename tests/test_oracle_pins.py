@@ -365,3 +365,47 @@ def test_polar_planted():
     u, h, it, _ = oracle.polar_newton(a, tol=1e-13)
     assert oracle.rel_fro(u, q) <= 1e-12 and oracle.rel_fro(h, h0) <= 1e-12
     assert np.abs(u.conj().T @ u - np.eye(n)).max() <= 1e-13
+
+
+# ------------------------------------------------------------------ Sylvester / Lyapunov (NEXT-3)
+def test_sylvester_diagonal_closed_form():
+    """Diagonal A, B: X_ij = C_ij / (a_i + b_j) (textbook closed form)."""
+    rng = np.random.default_rng(21)
+    m, n = 5, 4
+    a = np.diag(1.0 + rng.random(m) + 1j * rng.standard_normal(m))
+    b = np.diag(2.0 + rng.random(n) - 1j * rng.standard_normal(n))
+    c = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
+    x, it, _ = oracle.sylvester_sign(a, b, c)
+    ref = c / (np.diag(a)[:, None] + np.diag(b)[None, :])
+    assert np.abs(x - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_sylvester_vs_kronecker_and_scipy():
+    """Dense A, B with spectra in the right half plane: the sign-based X equals the
+    Kronecker solve vec(X) = (I (x) A + B^T (x) I)^{-1} vec(C) and scipy's Bartels-Stewart."""
+    import scipy.linalg as sla
+    rng = np.random.default_rng(22)
+    m, n = 6, 7
+    a = rng.standard_normal((m, m)) + 1j * rng.standard_normal((m, m)) + 6 * np.eye(m)
+    b = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)) + 6 * np.eye(n)
+    c = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
+    x, it, _ = oracle.sylvester_sign(a, b, c)
+    k = np.kron(np.eye(n), a) + np.kron(b.T, np.eye(m))
+    xk = np.linalg.solve(k, c.reshape(-1, order="F")).reshape((m, n), order="F")
+    assert oracle.rel_fro(x, xk) <= 1e-12
+    assert oracle.rel_fro(x, sla.solve_sylvester(a, b, c)) <= 1e-12
+    assert np.linalg.norm(a @ x + x @ b - c) <= 1e-12 * np.linalg.norm(c)
+    x2, _, _ = oracle.sylvester_sign(a, b, c, method="zlu")
+    assert oracle.rel_fro(x, x2) <= 1e-12
+
+
+def test_lyapunov_hermitian_solution():
+    """A X + X A^* = C with Hermitian C has a Hermitian solution (uniqueness)."""
+    rng = np.random.default_rng(23)
+    n = 8
+    a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)) + 7 * np.eye(n)
+    c = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    c = c + c.conj().T
+    x, _, _ = oracle.lyapunov_sign(a, c)
+    assert np.linalg.norm(x - x.conj().T) <= 1e-12 * np.linalg.norm(x)
+    assert np.linalg.norm(a @ x + x @ a.conj().T - c) <= 1e-12 * np.linalg.norm(c)
