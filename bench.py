@@ -442,10 +442,19 @@ def main():
             "predicted_frob_faster": bool(r_z > 2 and ratio > (2 + lam) / (r_z - 2)),
             "measured_frob_faster": bool(t_frob < t_zinv)}
         if isinstance(wl, Batched):
-            z32 = wl.parts[0][1]
-            tb_f = statistics.median(timed(lambda: fb.inv_batched(z32), 3, 1, False))
-            tb_z = statistics.median(timed(lambda: fb.zinv_batched(z32), 3, 1, False))
-            extras["batched_n32_comparison"] = {"frob_ms": tb_f, "zinv_lu_ms": tb_z, "count": int(z32.shape[0])}
+            # batched Frobenius vs the batched complex Gauss-Jordan comparator (n <= 64): the
+            # config-3 n = 32 shard, and n = 64 from the same generator (crossover evidence)
+            cmp = {}
+            z64 = torch.from_numpy(synth.batch(64, 16384, seed=0)).to(dev)
+            for nn, zz in ((32, wl.parts[0][1]), (64, z64)):
+                tb_f = statistics.median(timed(lambda: fb.inv_batched(zz), 3, 1, False))
+                tb_z = statistics.median(timed(lambda: fb.zinv_batched(zz), 3, 1, False))
+                cnt = int(zz.shape[0])
+                cmp[f"n{nn}"] = {"count": cnt, "frob_ms": tb_f, "zinv_lu_ms": tb_z, "frob_over_zinv_time": tb_f / tb_z,
+                                 "frob_inverses_per_s": cnt / tb_f * 1e3, "zinv_inverses_per_s": cnt / tb_z * 1e3,
+                                 "frob_tflops_alg": 10.0 * nn ** 3 * cnt / tb_f / 1e9,
+                                 "zinv_tflops_alg": 8.0 * nn ** 3 * cnt / tb_z / 1e9}
+            extras["batched_comparison"] = cmp
         # NEXT-1 (fused first step) and Alg 5 (randomized) on the same input
         t_fused = statistics.median(timed(lambda: fb.inv(zr, out=xr, fused=True), 5, 2, True))
         t_rand = statistics.median(timed(lambda: fb.inv_rand(zr, mu=0.5, out=xr), 5, 2, True))

@@ -184,6 +184,25 @@ size_t frob_dgetrf_workspace_bytes(int n);
 frob_status frob_dgetrf(int n, double *A, long long lda, int *perm, void *ws, size_t ws_bytes,
                         void *stream, frob_info *host_info);
 
+/* Sylvester equation A X + X B = C through the matrix sign function:
+ * sign([[A, -C], [0, -B]]) = [[I, -2X], [0, -I]] when sign(A) = I_m and sign(B) = I_n
+ * (spectra in the open right half plane); the sign of the order-(m+n) block matrix is computed
+ * by frob_sign_newton's iteration (each step one inversion by `method`), X = -S_12 / 2.
+ *   A  device m x m, B device n x n, C device m x n, X device m x n output: complex128,
+ *      row-major, dense (ld = number of columns).
+ *   tol, max_iter, method, host_iters, host_final_delta: as frob_sign_newton.
+ * Returns FROB_OK, FROB_ERR_NOT_CONVERGED (X from the last iterate), or an error status.
+ * Synchronises `stream` (the Newton driver reads delta_t every step). */
+size_t frob_sylvester_workspace_bytes(int m, int n, int method);
+frob_status frob_sylvester(int m, int n, const double *A, const double *B, const double *C, double *X,
+                           double tol, int max_iter, int method, void *ws, size_t ws_bytes, void *stream,
+                           int *host_iters, double *host_final_delta);
+/* Lyapunov equation A X + X A^* = C: frob_sylvester with B = A^* (built on the
+ * device).  Workspace: frob_sylvester_workspace_bytes(n, n, method). */
+frob_status frob_lyapunov(int n, const double *A, const double *C, double *X, double tol, int max_iter,
+                          int method, void *ws, size_t ws_bytes, void *stream, int *host_iters,
+                          double *host_final_delta);
+
 /* ---------------------------------------------------------------- misc */
 const char *frob_status_string(int status);
 const char *frob_last_cuda_error(void);

@@ -558,6 +558,70 @@ static frob_status newton_impl(bool polar, int n, const double *Z, double *S, do
     return (delta < tol) ? FROB_OK : FROB_ERR_NOT_CONVERGED;
 }
 
+// ---------------------------------------------------------------------- Sylvester (NEXT-3)
+// T = [[A, -C], [0, -B]] (order m + n) from dense row-major A (m x m), B (n x n), C (m x n);
+// lyap != 0: B = A^H (B pointer ignored)
+__global__ void sylv_assemble_kernel(const double2 *__restrict__ A, const double2 *__restrict__ B,
+                                     const double2 *__restrict__ C, int m, int n, int lyap, double2 *__restrict__ T) {
+    const int N = m + n;
+    const long long total = (long long)N * N;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / N), j = (int)(idx - (long long)i * N);
+        double2 v = make_double2(0.0, 0.0);
+        if (i < m && j < m) v = A[(long long)i * m + j];
+        else if (i < m) { const double2 c = C[(long long)i * n + (j - m)]; v = make_double2(-c.x, -c.y); }
+        else if (j >= m) {
+            const int bi = i - m, bj = j - m;
+            if (lyap) { const double2 a = A[(long long)bj * m + bi]; v = make_double2(-a.x, a.y); }  // -(A^H)
+            else { const double2 b = B[(long long)bi * n + bj]; v = make_double2(-b.x, -b.y); }
+        }
+        T[idx] = v;
+    }
+}
+// X = -S_12 / 2
+__global__ void sylv_extract_kernel(const double2 *__restrict__ S, int m, int n, double2 *__restrict__ X) {
+    const int N = m + n;
+    const long long total = (long long)m * n;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / n), j = (int)(idx - (long long)i * n);
+        const double2 v = S[(long long)i * N + m + j];
+        X[idx] = make_double2(-0.5 * v.x, -0.5 * v.y);
+    }
+}
+
+static size_t sylv_ws_bytes(int m, int n, int method) {
+    const int N = m + n;
+    return align256(newton_ws_bytes(N, method)) + 2 * align256((size_t)N * N * 16);
+}
+
+static frob_status sylvester_impl(int m, int n, const double *A, const double *B, const double *C, double *X,
+                                  int lyap, double tol, int max_iter, int method, void *ws, size_t ws_bytes,
+                                  cudaStream_t s, int *iters, double *final_delta) {
+    if (m < 1 || n < 1 || !A || !C || !X || (!lyap && !B) || !iters || !final_delta) return FROB_ERR_INVALID_ARG;
+    if (lyap && m != n) return FROB_ERR_INVALID_ARG;
+    if (!ws || ws_bytes < sylv_ws_bytes(m, n, method)) return FROB_ERR_WORKSPACE;
+    const int N = m + n;
+    unsigned char *b = reinterpret_cast<unsigned char *>(ws);
+    const size_t nb = align256(newton_ws_bytes(N, method));
+    double2 *T = reinterpret_cast<double2 *>(b + nb);
+    double2 *S = reinterpret_cast<double2 *>(b + nb + align256((size_t)N * N * 16));
+    count_launch();
+    sylv_assemble_kernel<<<ew_blocks((long long)N * N), 256, 0, s>>>(
+        reinterpret_cast<const double2 *>(A), reinterpret_cast<const double2 *>(B), reinterpret_cast<const double2 *>(C),
+        m, n, lyap, T);
+    FROB_CUDA(cudaGetLastError());
+    frob_status st = newton_impl(false, N, reinterpret_cast<const double *>(T), reinterpret_cast<double *>(S), nullptr,
+                                 tol, max_iter, method, ws, nb, s, iters, final_delta, nullptr);
+    if (st != FROB_OK && st != FROB_ERR_NOT_CONVERGED) return st;
+    count_launch();
+    sylv_extract_kernel<<<ew_blocks((long long)m * n), 256, 0, s>>>(S, m, n, reinterpret_cast<double2 *>(X));
+    FROB_CUDA(cudaGetLastError());
+    FROB_CUDA(cudaStreamSynchronize(s));
+    return st;
+}
+
 }  // namespace frob
 
 // =====================================================================================
@@ -632,6 +696,23 @@ frob_status frob_polar_newton(int n, const double *A, double *U, double *H, doub
         return FROB_ERR_INVALID_ARG;
     return newton_impl(true, n, A, U, H, tol, max_iter, method, ws, ws_bytes, (cudaStream_t)stream,
                        host_iters, host_final_delta, host_trace);
+}
+
+size_t frob_sylvester_workspace_bytes(int m, int n, int method) {
+    return (m < 1 || n < 1) ? 0 : sylv_ws_bytes(m, n, method);
+}
+
+frob_status frob_sylvester(int m, int n, const double *A, const double *B, const double *C, double *X, double tol,
+                           int max_iter, int method, void *ws, size_t ws_bytes, void *stream, int *host_iters,
+                           double *host_final_delta) {
+    return sylvester_impl(m, n, A, B, C, X, 0, tol, max_iter, method, ws, ws_bytes, (cudaStream_t)stream, host_iters,
+                          host_final_delta);
+}
+
+frob_status frob_lyapunov(int n, const double *A, const double *C, double *X, double tol, int max_iter, int method,
+                          void *ws, size_t ws_bytes, void *stream, int *host_iters, double *host_final_delta) {
+    return sylvester_impl(n, n, A, nullptr, C, X, 1, tol, max_iter, method, ws, ws_bytes, (cudaStream_t)stream,
+                          host_iters, host_final_delta);
 }
 
 frob_status frob_dgemm(int m, int n, int k, double alpha, const double *A, long long lda, const double *B,

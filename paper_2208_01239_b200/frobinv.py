@@ -52,6 +52,9 @@ SIGNATURES = {
     "frob_newton_workspace_bytes": (_sz, [_i, _i]),
     "frob_sign_newton": (_i, [_i, _vp, _vp, _d, _i, _i, _vp, _sz, _vp, _ip, _dp, _dp]),
     "frob_polar_newton": (_i, [_i, _vp, _vp, _vp, _d, _i, _i, _vp, _sz, _vp, _ip, _dp, _dp]),
+    "frob_sylvester_workspace_bytes": (_sz, [_i, _i, _i]),
+    "frob_sylvester": (_i, [_i, _i, _vp, _vp, _vp, _vp, _d, _i, _i, _vp, _sz, _vp, _ip, _dp]),
+    "frob_lyapunov": (_i, [_i, _vp, _vp, _vp, _d, _i, _i, _vp, _sz, _vp, _ip, _dp]),
     "frob_dgemm": (_i, [_i, _i, _i, _d, _vp, _ll, _vp, _ll, _d, _vp, _ll, _vp]),
     "frob_dinv_workspace_bytes": (_sz, [_i]),
     "frob_dinv": (_i, [_i, _vp, _ll, _vp, _ll, _vp, _sz, _vp, _FIP]),
@@ -290,6 +293,43 @@ def polar(a: torch.Tensor, tol: float = 1e-12, max_iter: int = 50, method: str =
 
 
 # ----------------------------------------------------------------------------- real blocks
+def sylvester(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, tol: float = 1e-12, max_iter: int = 50,
+              method: str = "frobenius"):
+    """A X + X B = C via the sign of [[A, -C], [0, -B]].  Returns (X, iters, delta)."""
+    L = load()
+    for t, nm in ((a, "a"), (b, "b"), (c, "c")):
+        _need_cuda(t, nm)
+        assert t.dtype == torch.complex128
+    a, b, c = a.contiguous(), b.contiguous(), c.contiguous()
+    m, n = a.shape[0], b.shape[0]
+    assert c.shape == (m, n)
+    x = torch.empty((m, n), dtype=torch.complex128, device=a.device)
+    ws = workspace(L.frob_sylvester_workspace_bytes(m, n, METHOD[method]), a.device)
+    it, d = ctypes.c_int(0), ctypes.c_double(0.0)
+    st = L.frob_sylvester(m, n, _p(a), _p(b), _p(c), _p(x), tol, max_iter, METHOD[method], _p(ws), ws.numel(),
+                          _stream(), ctypes.byref(it), ctypes.byref(d))
+    if st not in (0, 3):
+        _check("frob_sylvester", st)
+    return x, it.value, d.value
+
+
+def lyapunov(a: torch.Tensor, c: torch.Tensor, tol: float = 1e-12, max_iter: int = 50, method: str = "frobenius"):
+    """A X + X A^* = C.  Returns (X, iters, delta)."""
+    L = load()
+    _need_cuda(a, "a")
+    _need_cuda(c, "c")
+    a, c = a.contiguous(), c.contiguous()
+    n = a.shape[0]
+    x = torch.empty((n, n), dtype=torch.complex128, device=a.device)
+    ws = workspace(L.frob_sylvester_workspace_bytes(n, n, METHOD[method]), a.device)
+    it, d = ctypes.c_int(0), ctypes.c_double(0.0)
+    st = L.frob_lyapunov(n, _p(a), _p(c), _p(x), tol, max_iter, METHOD[method], _p(ws), ws.numel(), _stream(),
+                         ctypes.byref(it), ctypes.byref(d))
+    if st not in (0, 3):
+        _check("frob_lyapunov", st)
+    return x, it.value, d.value
+
+
 def dgemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor | None = None, alpha: float = 1.0,
           beta: float = 0.0):
     L = load()

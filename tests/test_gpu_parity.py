@@ -375,3 +375,36 @@ def test_config5_large_sampled_columns(n):
         res = float(torch.linalg.norm(zt @ x - torch.eye(n, dtype=torch.complex128, device=DEV)))
         assert res <= 1e-11 * n
         assert float(torch.linalg.norm(x - xz) / torch.linalg.norm(xz)) <= 1e-9
+
+
+# ------------------------------------------------------------------ Sylvester / Lyapunov (NEXT-3)
+@pytest.mark.parametrize("mn", [(1, 1), (5, 3), (40, 24), (96, 96)])
+@pytest.mark.parametrize("method", ["frobenius", "zlu"])
+def test_sylvester_vs_oracle(mn, method):
+    m, n = mn
+    rng = np.random.default_rng(m * 100 + n)
+    # spectra well inside the right half plane (complex Gaussian disc radius ~ sqrt(2 m)):
+    # sign(A) = I, sign(B) = I as the block-sign formula requires
+    a = rng.standard_normal((m, m)) + 1j * rng.standard_normal((m, m)) + (3 + 2 * math.sqrt(2 * m)) * np.eye(m)
+    b = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)) + (3 + 2 * math.sqrt(2 * n)) * np.eye(n)
+    c = rng.standard_normal((m, n)) + 1j * rng.standard_normal((m, n))
+    x, it, d = fb.sylvester(_t(a), _t(b), _t(c), method=method)
+    x = _np(x)
+    xo, ito, _ = oracle.sylvester_sign(a, b, c, method="frobenius" if method == "frobenius" else "zlu")
+    assert oracle.rel_fro(x, xo) <= REL
+    assert np.linalg.norm(a @ x + x @ b - c) <= 1e-11 * np.linalg.norm(c) * max(m, n)
+    assert abs(it - ito) <= 1
+
+
+def test_lyapunov_gpu():
+    n = 64
+    rng = np.random.default_rng(64)
+    a = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)) + (3 + 2 * math.sqrt(2 * n)) * np.eye(n)
+    c = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    c = c + c.conj().T
+    x, it, d = fb.lyapunov(_t(a), _t(c))
+    x = _np(x)
+    xo, _, _ = oracle.lyapunov_sign(a, c)
+    assert oracle.rel_fro(x, xo) <= REL
+    assert np.linalg.norm(a @ x + x @ a.conj().T - c) <= 1e-11 * np.linalg.norm(c) * n
+    assert np.linalg.norm(x - x.conj().T) <= 1e-11 * np.linalg.norm(x)
