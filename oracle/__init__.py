@@ -57,9 +57,13 @@ def lib():
             L.or_frob_inv.argtypes = [ctypes.c_int, dp, dp, dp, dp, ctypes.c_int, ctypes.c_double, ip, dp]
             L.or_frob_inv_rand.argtypes = [ctypes.c_int, dp, dp, ctypes.c_double, dp, dp, ctypes.c_double,
                                            ip, dp]
+            L.or_dpotrf_upper.argtypes = [ctypes.c_int, dp, dp]
+            L.or_hpd_frob_inv.argtypes = [ctypes.c_int, dp, dp, dp, dp, ip]
+            L.or_zhpd_inv_chol.argtypes = [ctypes.c_int, dp, dp, dp, dp]
             L.or_zinv_gj.argtypes = [ctypes.c_int, dp, dp]
             L.or_zinv_lu.argtypes = [ctypes.c_int, dp, dp, dp, dp]
             for f in ("or_dgetrf", "or_dtrtri_upper", "or_dinv", "or_frob_inv", "or_frob_inv_rand", "or_zinv_gj",
+                      "or_dpotrf_upper", "or_hpd_frob_inv", "or_zhpd_inv_chol",
                       "or_zinv_lu", "or_num_threads"):
                 getattr(L, f).restype = ctypes.c_int
             L.or_dgetri_solve.restype = None
@@ -167,6 +171,33 @@ def frob_inv_rand(z, mu: float, tau: float = TAU_SWITCH):
                                 _p(out, ctypes.c_int), _p(rho))
     return xr + 1j * xi, st, {"info": int(out[0]), "branch_used": int(out[1]),
                               "rho_a": float(rho[0]), "rho_b": float(rho[1])}
+
+
+def dpotrf_upper(a):
+    """Alg 10: A = U^T U, U upper.  Returns (U, info)."""
+    a = _f64(a)
+    u = np.zeros_like(a)
+    info = lib().or_dpotrf_upper(a.shape[0], _p(a), _p(u))
+    return u, info
+
+
+def hpd_frob_inv(z):
+    """Alg 6 for Hermitian positive definite Z.  Returns (X, status, col)."""
+    a, b = split(z)
+    xr = np.zeros_like(a)
+    xi = np.zeros_like(a)
+    col = np.zeros(1, dtype=np.int32)
+    st = lib().or_hpd_frob_inv(a.shape[0], _p(a), _p(b), _p(xr), _p(xi), _p(col, ctypes.c_int))
+    return xr + 1j * xi, st, int(col[0])
+
+
+def zhpd_inv_chol(z):
+    """Alg 8 over C: complex Cholesky inversion X = U^{-1} U^{-H}.  Returns (X, info)."""
+    re, im = split(z)
+    xr = np.zeros_like(re)
+    xi = np.zeros_like(im)
+    info = lib().or_zhpd_inv_chol(re.shape[0], _p(re), _p(im), _p(xr), _p(xi))
+    return xr + 1j * xi, info
 
 
 def zinv_gj(z):

@@ -23,6 +23,8 @@
  *                    interchanges that undo P (A = P^T L U  =>  A^{-1} = U^{-1} L^{-1} P).
  *   or_dinv          Alg 3 = the real inversion inv_{n,R} used twice by Alg 1.
  *   or_dgemm         m_{n,R}: C = A B, plain triple loop, k ascending.
+ *   or_dpotrf_upper  Alg 10 Cholesky; or_hpd_frob_inv Alg 6;
+ *   or_zhpd_inv_chol Alg 8 complex Cholesky inversion
  *   or_frob_inv_rand Alg 5 randomized Frobenius inversion, mu given
  *   or_frob_inv      Alg 1 "Frobenius inversion I" with tau = 1 (f = x^2+1,
  *                    P:L123): S1 branch returns J - iK, S2 branch returns K - iJ.  The
@@ -294,6 +296,151 @@ int or_frob_inv_rand(int n, const double *A, const double *B, double mu, double 
         }
     }
     free(X); free(Y); free(W1); free(W2);
+    return st;
+}
+
+/* --------------------------------------------------------------- HPD (Section 6) */
+
+/* Alg 10 "Cholesky decomposition", real case, column by column:
+ *   Z[1:k-1,k] = (Z[1:k-1,1:k-1]^T)^{-1} Z[1:k-1,k]        (forward substitution)
+ *   Z[k,k]     = sqrt(Z[k,k] - Z[1:k-1,k]^T Z[1:k-1,k])
+ * on the upper triangle of a; u (n x n) receives U with A = U^T U (zeros below).
+ * Returns 0, or the 1-based column whose pivot is not positive. */
+int or_dpotrf_upper(int n, const double *a, double *u)
+{
+    size_t nn = (size_t)n * n;
+    for (size_t i = 0; i < nn; ++i) u[i] = 0.0;
+    for (int k = 0; k < n; ++k) {
+        for (int i = 0; i < k; ++i) {                 /* forward substitution with U^T */
+            double s = a[(size_t)i * n + k];
+            for (int q = 0; q < i; ++q) s -= u[(size_t)q * n + i] * u[(size_t)q * n + k];
+            u[(size_t)i * n + k] = s / u[(size_t)i * n + i];
+        }
+        double d = a[(size_t)k * n + k];
+        for (int q = 0; q < k; ++q) d -= u[(size_t)q * n + k] * u[(size_t)q * n + k];
+        if (!(d > 0.0)) return k + 1;
+        u[(size_t)k * n + k] = sqrt(d);
+    }
+    return 0;
+}
+
+/* X = U^{-T} Y for upper U: forward substitution per column of Y (U^T X = Y) */
+static void fwd_ut(int n, const double *u, const double *y, double *x)
+{
+    for (int c = 0; c < n; ++c)
+        for (int i = 0; i < n; ++i) {
+            double s = y[(size_t)i * n + c];
+            for (int q = 0; q < i; ++q) s -= u[(size_t)q * n + i] * x[(size_t)q * n + c];
+            x[(size_t)i * n + c] = s / u[(size_t)i * n + i];
+        }
+}
+/* X = U^{-1} Y for upper U: back substitution per column of Y */
+static void back_u(int n, const double *u, const double *y, double *x)
+{
+    for (int c = 0; c < n; ++c)
+        for (int i = n - 1; i >= 0; --i) {
+            double s = y[(size_t)i * n + c];
+            for (int q = i + 1; q < n; ++q) s -= u[(size_t)i * n + q] * x[(size_t)q * n + c];
+            x[(size_t)i * n + c] = s / u[(size_t)i * n + i];
+        }
+}
+static void transpose(int n, const double *a, double *t)
+{
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) t[(size_t)j * n + i] = a[(size_t)i * n + j];
+}
+
+/* Alg 6 "first variant of Frobenius inversion" for HPD Z = A + iB (Lemma 6.1:
+ * Z is in S1, so X = A, Y = B):
+ *   l.6  X = U^T U            l.7  K1 = (U^T)^{-1} Y      l.8  K2 = U^{-1} K1
+ *   l.9  K3 = K1^T K1         l.10 K4 = X - K3            l.11 K4 = V^T V
+ *   l.12 K5 = V^{-1}          l.13 K6 = K5 K5^T           l.14 K7 = K2 K6
+ *   return K6 - i K7.
+ * Returns 0, or 1 (U) / 2 (V) when a Cholesky pivot is not positive (out_col: column). */
+int or_hpd_frob_inv(int n, const double *A, const double *B, double *Xre, double *Xim, int *out_col)
+{
+    size_t nn = (size_t)n * n;
+    double *U = (double *)malloc(sizeof(double) * nn), *K1 = (double *)malloc(sizeof(double) * nn);
+    double *K2 = (double *)malloc(sizeof(double) * nn), *T = (double *)malloc(sizeof(double) * nn);
+    double *K4 = (double *)malloc(sizeof(double) * nn), *V = (double *)malloc(sizeof(double) * nn);
+    double *K5 = (double *)malloc(sizeof(double) * nn), *K6 = (double *)malloc(sizeof(double) * nn);
+    int st = 0, c;
+    if ((c = or_dpotrf_upper(n, A, U))) { st = 1; *out_col = c; goto done; }      /* l.6  */
+    fwd_ut(n, U, B, K1);                                                           /* l.7  */
+    back_u(n, U, K1, K2);                                                          /* l.8  */
+    transpose(n, K1, T);
+    or_dgemm(n, n, n, T, K1, K4);                                                  /* l.9  */
+    for (size_t i = 0; i < nn; ++i) K4[i] = A[i] - K4[i];                          /* l.10 */
+    if ((c = or_dpotrf_upper(n, K4, V))) { st = 2; *out_col = c; goto done; }      /* l.11 */
+    if (or_dtrtri_upper(n, V, K5)) { st = 2; *out_col = 0; goto done; }           /* l.12 */
+    transpose(n, K5, T);
+    or_dgemm(n, n, n, K5, T, K6);                                                  /* l.13 */
+    or_dgemm(n, n, n, K2, K6, T);                                                  /* l.14 */
+    for (size_t i = 0; i < nn; ++i) { Xre[i] = K6[i]; Xim[i] = -T[i]; }            /* K6 - iK7 */
+    *out_col = 0;
+done:
+    free(U); free(K1); free(K2); free(T); free(K4); free(V); free(K5); free(K6);
+    return st;
+}
+
+/* Alg 8 "first matrix inversion via Cholesky decomposition" over C:
+ * Z = U^H U (Alg 10 with conjugates), K = U^{-1}, X = K K^H.  Returns 0 or the 1-based
+ * column of a non-positive pivot. */
+int or_zhpd_inv_chol(int n, const double *zr, const double *zi, double *xr, double *xi)
+{
+    size_t nn = (size_t)n * n;
+    double *ur = (double *)calloc(nn, sizeof(double)), *ui = (double *)calloc(nn, sizeof(double));
+    double *kr = (double *)calloc(nn, sizeof(double)), *ki = (double *)calloc(nn, sizeof(double));
+    int st = 0;
+    for (int k = 0; k < n && !st; ++k) {
+        for (int i = 0; i < k; ++i) {     /* U[i][k] = (z[i][k] - sum_q conj(U[q][i]) U[q][k]) / U[i][i] */
+            double sr = zr[(size_t)i * n + k], si = zi[(size_t)i * n + k];
+            for (int q = 0; q < i; ++q) {
+                const double ar = ur[(size_t)q * n + i], ai = -ui[(size_t)q * n + i];
+                const double br = ur[(size_t)q * n + k], bi = ui[(size_t)q * n + k];
+                sr -= ar * br - ai * bi;
+                si -= ar * bi + ai * br;
+            }
+            const double d = ur[(size_t)i * n + i];  /* real, positive */
+            ur[(size_t)i * n + k] = sr / d;
+            ui[(size_t)i * n + k] = si / d;
+        }
+        double d = zr[(size_t)k * n + k];
+        for (int q = 0; q < k; ++q)
+            d -= ur[(size_t)q * n + k] * ur[(size_t)q * n + k] + ui[(size_t)q * n + k] * ui[(size_t)q * n + k];
+        if (!(d > 0.0)) { st = k + 1; break; }
+        ur[(size_t)k * n + k] = sqrt(d);
+    }
+    if (!st) {
+        /* K = U^{-1}: column j by back substitution, U K[:, j] = e_j */
+        for (int j = 0; j < n; ++j)
+            for (int i = j; i >= 0; --i) {
+                double sr = (i == j) ? 1.0 : 0.0, si = 0.0;
+                for (int q = i + 1; q <= j; ++q) {
+                    const double ar = ur[(size_t)i * n + q], ai = ui[(size_t)i * n + q];
+                    const double br = kr[(size_t)q * n + j], bi = ki[(size_t)q * n + j];
+                    sr -= ar * br - ai * bi;
+                    si -= ar * bi + ai * br;
+                }
+                const double d = ur[(size_t)i * n + i];
+                kr[(size_t)i * n + j] = sr / d;
+                ki[(size_t)i * n + j] = si / d;
+            }
+        /* X = K K^H */
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j) {
+                double sr = 0.0, si = 0.0;
+                for (int q = 0; q < n; ++q) {
+                    const double ar = kr[(size_t)i * n + q], ai = ki[(size_t)i * n + q];
+                    const double br = kr[(size_t)j * n + q], bi = -ki[(size_t)j * n + q];
+                    sr += ar * br - ai * bi;
+                    si += ar * bi + ai * br;
+                }
+                xr[(size_t)i * n + j] = sr;
+                xi[(size_t)i * n + j] = si;
+            }
+    }
+    free(ur); free(ui); free(kr); free(ki);
     return st;
 }
 

@@ -101,6 +101,15 @@ def sign_instance(n: int, seed: int = 0, index: int = 0):
     return np.ascontiguousarray(z), s, lam, sinv
 
 
+def hpd(n: int, seed: int = 0, delta: float = 0.01) -> np.ndarray:
+    """Hermitian positive definite test matrix in the style of the paper's HPD experiment
+    ((A+iB)(A+iB)^* + 0.01 I): W = (G1 + i G2)/sqrt(n), Z = W W^* + delta I."""
+    g = np.random.Generator(np.random.Philox(key=[seed, 0xB1D]))
+    w = (g.standard_normal((n, n)) + 1j * g.standard_normal((n, n))) / math.sqrt(n)
+    z = w @ w.conj().T + delta * np.eye(n)
+    return 0.5 * (z + z.conj().T)
+
+
 def dft_unitary(n: int) -> np.ndarray:
     """F/sqrt(n): unitary, with singular real and imaginary parts for n > 2."""
     j = np.arange(n)

@@ -409,3 +409,53 @@ def test_lyapunov_hermitian_solution():
     x, _, _ = oracle.lyapunov_sign(a, c)
     assert np.linalg.norm(x - x.conj().T) <= 1e-12 * np.linalg.norm(x)
     assert np.linalg.norm(a @ x + x @ a.conj().T - c) <= 1e-12 * np.linalg.norm(c)
+
+
+# ------------------------------------------------------------------ HPD (NEXT-4)
+def test_dpotrf_vs_lapack_and_reconstruction():
+    z = synth.hpd(40, seed=1)
+    a = z.real.copy()
+    u, info = oracle.dpotrf_upper(a)
+    assert info == 0
+    assert np.all(u[np.tril_indices(40, -1)] == 0.0)
+    np.testing.assert_allclose(u, np.linalg.cholesky(a).T, rtol=1e-12, atol=1e-13)
+    assert np.linalg.norm(u.T @ u - a) <= 1e-14 * np.linalg.norm(a)
+    bad = a.copy()
+    bad[5, 5] = -1.0
+    assert oracle.dpotrf_upper(bad)[1] != 0
+
+
+def test_hpd_2x2_closed_form():
+    """Z = [[a, i b], [-i b, c]] (Hermitian): Z^{-1} = [[c, -i b], [i b, a]] / (a c - b^2)."""
+    a, b, c = 3.0, 1.25, 2.0
+    z = np.array([[a, 1j * b], [-1j * b, c]])
+    ref = np.array([[c, -1j * b], [1j * b, a]]) / (a * c - b * b)
+    for x, st in (oracle.hpd_frob_inv(z)[:2], oracle.zhpd_inv_chol(z)):
+        assert st == 0
+        assert np.abs(x - ref).max() <= 1e-15
+
+
+def test_hpd_variants_vs_definition_and_alg1():
+    """Alg 6 and Alg 8 against complex Gauss-Jordan, LAPACK and the LU-based Alg 1; lemma 6.1:
+    A symmetric positive definite, B skew-symmetric."""
+    for n in (3, 17, 64):
+        z = synth.hpd(n, seed=n)
+        assert np.array_equal(z.real, z.real.T) and np.array_equal(z.imag, -z.imag.T)
+        ref, _ = oracle.zinv_gj(z)
+        x6, st, _ = oracle.hpd_frob_inv(z)
+        x8, st8 = oracle.zhpd_inv_chol(z)
+        x1, st1, _ = oracle.frob_inv(z, "a")
+        assert st == 0 and st8 == 0 and st1 == 0
+        kap = np.linalg.cond(z)
+        for x in (x6, x8, x1):
+            assert oracle.rel_fro(x, ref) <= 1e-15 * kap * kap * n
+            assert oracle.rel_fro(x, np.linalg.inv(z)) <= 1e-15 * kap * kap * n
+        assert np.linalg.norm(x6 - x6.conj().T) <= 1e-12 * np.linalg.norm(x6)
+
+
+def test_hpd_rejects_indefinite():
+    z = synth.hpd(12, seed=3)
+    z[0, 0] = -5.0
+    _, st, col = oracle.hpd_frob_inv(z)
+    assert st == 1 and col == 1
+    assert oracle.zhpd_inv_chol(z)[1] == 1
