@@ -479,9 +479,17 @@ def main():
             tensor = name.startswith("gemm")
             pk, pk_src = (peak, peak_src) if tensor else fp64_alu_peak()
             steps_prof = len(pw) + 1
+            traffic = None
+            try:  # DRAM bytes per launch from this round's committed ncu --set full capture
+                with open(os.path.join(ROOT, "profiles", "r01", "dram_traffic.json")) as f:
+                    tr = json.load(f).get(name)
+                if tr and "batched" not in name:
+                    traffic = tr["bytes_per_launch"]
+            except Exception:
+                pass
             extras["roofline"] = {
                 "bound": "tensor" if tensor else "alu", "kernel": name, "achieved": ach_k, "peak": pk,
-                "unit": "TFLOP/s", "frac": ach_k / pk, "traffic": None, "peak_source": pk_src,
+                "unit": "TFLOP/s", "frac": ach_k / pk, "traffic": traffic, "peak_source": pk_src,
                 "flops_per_launch": d["flops"] / max(1, d["launches"]), "avg_launch_ms": avg_ms,
                 "launches_per_step": d["launches"] / steps_prof,
                 "share_of_step": d["total_ms"] / steps_prof / statistics.median(pw),
