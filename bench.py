@@ -461,6 +461,12 @@ def main():
         extras["comparison_single_n"].update({
             "frobenius_fused_first_step_ms": t_fused, "frobenius_fused_tflops_alg": (28.0 / 3.0) * n ** 3 / t_fused / 1e9,
             "frobenius_randomized_ms": t_rand})
+        # NEXT-4: HPD inversion, Cholesky-based Frobenius variant (Alg 6) vs complex Cholesky (Alg 8)
+        zh = torch.from_numpy(synth.hpd(n, seed=rank)).to(dev)
+        t_h6 = statistics.median(timed(lambda: fb.hpd_inv(zh, out=xr, check=False), 5, 2, True))
+        t_h8 = statistics.median(timed(lambda: fb.zhpd_inv(zh, out=xr, check=False), 5, 2, True))
+        extras["hpd_comparison"] = {"n": n, "frob_hpd_alg6_ms": t_h6, "complex_cholesky_alg8_ms": t_h8,
+                                    "alg6_over_alg8_time": t_h6 / t_h8}
         # GEMM engine (DMMA) at the n x n x n shape of the three Frobenius GEMMs
         ach = 2.0 * n ** 3 / t_mult / 1e9
         extras["roofline_gemm"] = {"bound": "tensor", "kernel": "gemm_kernel<double> (DMMA m8n8k4), n x n x n",

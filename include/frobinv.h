@@ -184,6 +184,23 @@ size_t frob_dgetrf_workspace_bytes(int n);
 frob_status frob_dgetrf(int n, double *A, long long lda, int *perm, void *ws, size_t ws_bytes,
                         void *stream, frob_info *host_info);
 
+/* Hermitian positive definite inversion (paper Section 6).
+ * frob_hpd_inv: Alg 6 "first variant of Frobenius inversion" -- for HPD Z = A + iB
+ *   (Lemma 6.1: A symmetric positive definite, B skew, Z in S1): Cholesky A = U^T U,
+ *   K1 = U^{-T} B, K2 = U^{-1} K1, K4 = A - K1^T K1 = V^T V, K6 = V^{-1} V^{-T}, K7 = K2 K6,
+ *   Z^{-1} = K6 - i K7 (Cholesky blocked right-looking, Alg 10).
+ * zhpd_inv_chol: Alg 8 over C, the comparator: Z = U^H U, X = U^{-1} U^{-H}.
+ *   Z, X: device n x n complex128 (ldz, ldx complex elements), Z is not checked for being
+ *   Hermitian (only its upper triangle is read by the Cholesky factorisations).
+ *   host_info: nullable; if non-NULL the call synchronises and stores 0 or the 1-based column
+ *   of the first non-positive Cholesky pivot (FROB_ERR_SINGULAR: not positive definite). */
+size_t frob_hpd_inv_workspace_bytes(int n);
+frob_status frob_hpd_inv(int n, const double *Z, long long ldz, double *X, long long ldx, void *ws,
+                         size_t ws_bytes, void *stream, int *host_info);
+size_t zhpd_inv_chol_workspace_bytes(int n);
+frob_status zhpd_inv_chol(int n, const double *Z, long long ldz, double *X, long long ldx, void *ws,
+                          size_t ws_bytes, void *stream, int *host_info);
+
 /* Sylvester equation A X + X B = C through the matrix sign function:
  * sign([[A, -C], [0, -B]]) = [[I, -2X], [0, -I]] when sign(A) = I_m and sign(B) = I_n
  * (spectra in the open right half plane); the sign of the order-(m+n) block matrix is computed

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfrobinv.so")
-SOURCES = ["lu.cu", "lu2.cu", "tma.cu", "frob.cu", "batched.cu"]
+SOURCES = ["lu.cu", "lu2.cu", "tma.cu", "frob.cu", "batched.cu", "hpd.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -964,7 +964,7 @@ __global__ void __launch_bounds__(TRI_LEAF) tri_leaf_kernel(T *__restrict__ U, T
 // One recursion level of size s: blocks [o, o+s) x [o+s, o+s+s2) for o = p*2s.
 template <typename T>
 static cudaError_t tri_level(T *U, T *L, T *tmp, long long ld, int s, int o, int s2, int batch,
-                             cudaStream_t st, bool do_upper = true) {
+                             cudaStream_t st, bool do_upper = true, bool do_lower = true) {
     const long long stride = 2LL * s * (ld + 1);
     cudaError_t e;
     // step 1 -- upper: W = U12 * inv(U22);  lower: W = L21 * inv(L11)   (one launch)
@@ -976,7 +976,11 @@ static cudaError_t tri_level(T *U, T *L, T *tmp, long long ld, int s, int o, int
                              L + (long long)o * ld + o, ld, 0.0, nullptr, ld,
                              tmp + (long long)(o + s) * ld + o, ld);
     pl.triB = TRI_LOWER; pl.sA = pl.sB = pl.sC = stride; pl.sD = 0;
-    if ((e = gemm_launch2<T>(pl, batch, pu, do_upper ? batch : 0, st)) != cudaSuccess) return e;
+    if (!do_lower) {
+        if ((e = gemm_launch<T>(pu, batch, st)) != cudaSuccess) return e;
+    } else if ((e = gemm_launch2<T>(pl, batch, pu, do_upper ? batch : 0, st)) != cudaSuccess) {
+        return e;
+    }
     // step 2 -- upper: U12 <- -inv(U11) * W;  lower: L21 <- -inv(L22) * W
     auto qu = gemm_params<T>(s, s2, s, -1.0, U + (long long)o * ld + o, ld,
                              tmp + (long long)o * ld + o + s, ld, 0.0, nullptr, ld,
@@ -986,6 +990,7 @@ static cudaError_t tri_level(T *U, T *L, T *tmp, long long ld, int s, int o, int
                              tmp + (long long)(o + s) * ld + o, ld, 0.0, nullptr, ld,
                              L + (long long)(o + s) * ld + o, ld);
     ql.triA = TRI_LOWER; ql.sA = ql.sB = ql.sC = stride; ql.sD = 0;
+    if (!do_lower) return gemm_launch<T>(qu, batch, st);
     return gemm_launch2<T>(ql, batch, qu, do_upper ? batch : 0, st);
 }
 
@@ -1007,15 +1012,18 @@ cudaError_t inv_from_lu(int n, T *lu, long long ld, T *U, T *L, T *out, long lon
 template <typename T>
 cudaError_t tri_inverses(int n, T *U, T *L, long long ld, T *tmp, cudaStream_t s) {
     cudaError_t e;
-    if ((e = launch_pdl(tri_leaf_kernel<T>, dim3((n + TRI_LEAF - 1) / TRI_LEAF, 2), dim3(TRI_LEAF), 0, s, U, L, ld, n,
-                        0)) != cudaSuccess)
+    const bool lower = L != nullptr;  // L == nullptr: invert the upper triangle U only
+    if ((e = launch_pdl(tri_leaf_kernel<T>, dim3((n + TRI_LEAF - 1) / TRI_LEAF, lower ? 2 : 1), dim3(TRI_LEAF), 0, s,
+                        U, lower ? L : U, ld, n, 0)) != cudaSuccess)
         return e;
     for (int sz = TRI_LEAF; sz < n; sz *= 2) {
         const int full = n / (2 * sz);
-        if (full > 0 && (e = tri_level<T>(U, L, tmp, ld, sz, 0, sz, full, s)) != cudaSuccess) return e;
+        if (full > 0 && (e = tri_level<T>(U, lower ? L : U, tmp, ld, sz, 0, sz, full, s, true, lower)) != cudaSuccess)
+            return e;
         const int o = full * 2 * sz;
         if (o + sz < n) {
-            if ((e = tri_level<T>(U, L, tmp, ld, sz, o, n - o - sz, 1, s)) != cudaSuccess) return e;
+            if ((e = tri_level<T>(U, lower ? L : U, tmp, ld, sz, o, n - o - sz, 1, s, true, lower)) != cudaSuccess)
+                return e;
         }
     }
     return cudaSuccess;

@@ -52,6 +52,10 @@ SIGNATURES = {
     "frob_newton_workspace_bytes": (_sz, [_i, _i]),
     "frob_sign_newton": (_i, [_i, _vp, _vp, _d, _i, _i, _vp, _sz, _vp, _ip, _dp, _dp]),
     "frob_polar_newton": (_i, [_i, _vp, _vp, _vp, _d, _i, _i, _vp, _sz, _vp, _ip, _dp, _dp]),
+    "frob_hpd_inv_workspace_bytes": (_sz, [_i]),
+    "frob_hpd_inv": (_i, [_i, _vp, _ll, _vp, _ll, _vp, _sz, _vp, _ip]),
+    "zhpd_inv_chol_workspace_bytes": (_sz, [_i]),
+    "zhpd_inv_chol": (_i, [_i, _vp, _ll, _vp, _ll, _vp, _sz, _vp, _ip]),
     "frob_sylvester_workspace_bytes": (_sz, [_i, _i, _i]),
     "frob_sylvester": (_i, [_i, _i, _vp, _vp, _vp, _vp, _d, _i, _i, _vp, _sz, _vp, _ip, _dp]),
     "frob_lyapunov": (_i, [_i, _vp, _vp, _vp, _d, _i, _i, _vp, _sz, _vp, _ip, _dp]),
@@ -293,6 +297,31 @@ def polar(a: torch.Tensor, tol: float = 1e-12, max_iter: int = 50, method: str =
 
 
 # ----------------------------------------------------------------------------- real blocks
+def _hpd_call(fn, wsfn, z, out, check):
+    L = load()
+    _need_cuda(z, "z")
+    assert z.dtype == torch.complex128 and z.dim() == 2 and z.shape[0] == z.shape[1]
+    z = z if z.stride(1) == 1 else z.contiguous()
+    n = z.shape[0]
+    x = out if out is not None else torch.empty((n, n), dtype=torch.complex128, device=z.device)
+    ws = workspace(getattr(L, wsfn)(n), z.device)
+    info = ctypes.c_int(0)
+    st = getattr(L, fn)(n, _p(z), z.stride(0), _p(x), x.stride(0), _p(ws), ws.numel(), _stream(),
+                        ctypes.byref(info) if check else None)
+    _check(fn, st, {"info": info.value} if check else None)
+    return x
+
+
+def hpd_inv(z: torch.Tensor, out: torch.Tensor | None = None, check: bool = True):
+    """HPD inversion by the Cholesky-based Frobenius variant (Alg 6)."""
+    return _hpd_call("frob_hpd_inv", "frob_hpd_inv_workspace_bytes", z, out, check)
+
+
+def zhpd_inv(z: torch.Tensor, out: torch.Tensor | None = None, check: bool = True):
+    """HPD inversion by complex Cholesky (Alg 8 over C), the comparator."""
+    return _hpd_call("zhpd_inv_chol", "zhpd_inv_chol_workspace_bytes", z, out, check)
+
+
 def sylvester(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, tol: float = 1e-12, max_iter: int = 50,
               method: str = "frobenius"):
     """A X + X B = C via the sign of [[A, -C], [0, -B]].  Returns (X, iters, delta)."""

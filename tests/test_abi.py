@@ -15,7 +15,7 @@ def _declared():
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     names = re.findall(r"\b([a-z_][a-z0-9_]*)\s*\(", src)
     skip = {"if", "sizeof", "defined"}
-    return sorted({n for n in names if n not in skip and (n.startswith("frob") or n.startswith("zinv"))})
+    return sorted({n for n in names if n not in skip and (n.startswith("frob") or n.startswith("zinv") or n.startswith("zhpd"))})
 
 
 @pytest.fixture(scope="module")

@@ -408,3 +408,29 @@ def test_lyapunov_gpu():
     assert oracle.rel_fro(x, xo) <= REL
     assert np.linalg.norm(a @ x + x @ a.conj().T - c) <= 1e-11 * np.linalg.norm(c) * n
     assert np.linalg.norm(x - x.conj().T) <= 1e-11 * np.linalg.norm(x)
+
+
+# ------------------------------------------------------------------ HPD (NEXT-4)
+@pytest.mark.parametrize("n", [1, 2, 17, 64, 65, 100, 257, 1000])
+def test_hpd_inv_vs_oracle(n):
+    """Alg 6 and Alg 8 on the GPU vs the oracle's Alg 6 / Alg 8 and the definition."""
+    z = synth.hpd(n, seed=n)
+    ref, _ = oracle.zinv_gj(z)
+    x6 = _np(fb.hpd_inv(_t(z)))
+    x8 = _np(fb.zhpd_inv(_t(z)))
+    _check_inverse(z, x6, ref)
+    _check_inverse(z, x8, ref)
+    if n <= 257:
+        xo6, st, _ = oracle.hpd_frob_inv(z)
+        xo8, st8 = oracle.zhpd_inv_chol(z)
+        assert st == 0 and st8 == 0
+        assert oracle.rel_fro(x6, xo6) <= REL and oracle.rel_fro(x8, xo8) <= REL
+
+
+def test_hpd_not_positive_definite():
+    z = synth.hpd(40, seed=4)
+    z[7, 7] = -3.0
+    for f in (fb.hpd_inv, fb.zhpd_inv):
+        with pytest.raises(fb.FrobError) as e:
+            f(_t(z))
+        assert e.value.name == "singular"
