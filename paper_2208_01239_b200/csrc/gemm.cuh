@@ -152,11 +152,54 @@ FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int ro
 #pragma unroll
             for (int e = 0; e < V; ++e) acc[i][j][e] = 0.0;
 
+    // Fast path (interior tile, 16-byte aligned operands): every thread's chunks keep the same
+    // (row, column) offsets in each stage, so their global addresses are computed once and
+    // advanced by a constant per stage; no bounds checks.  The checked path below serves edge
+    // tiles and the ragged last stage (K or a triangular k-range not a multiple of BK).
+    constexpr int ACH = BM * BK / E, BCH = BK * BN / E;
+    constexpr int APT = (ACH + NTH - 1) / NTH, BPT = (BCH + NTH - 1) / NTH;
+    static_assert(ACH % NTH == 0 && BCH % NTH == 0, "whole chunks per thread");
+    const bool fast = VEC && row0 + BM <= M && col0 + BN <= N;
+    const T *asrc[APT];
+    unsigned adst[APT];
+    int boff[BPT], bdst[BPT], brr[BPT];
+    if (fast) {
+#pragma unroll
+        for (int u = 0; u < APT; ++u) {
+            const int c = tid + u * NTH;
+            const int r = c / (BK / E), cc = (c % (BK / E)) * E;
+            asrc[u] = A + (long long)(row0 + r) * p.lda + kb + cc;
+            adst[u] = (unsigned)(r * SA + cc);
+        }
+#pragma unroll
+        for (int u = 0; u < BPT; ++u) {
+            const int c = tid + u * NTH;
+            const int r = c / (BN / E), cc = (c % (BN / E)) * E;
+            brr[u] = r;
+            boff[u] = col0 + cc;
+            bdst[u] = r * SB + cc;
+        }
+    }
     auto load_stage = [&](int s, int kt) {
         const int k0 = kb + kt * BK;
+        if (fast && k0 + BK <= K) {
+            T *as = As + s * BM * SA;
+            T *bs = Bs + s * BK * SB;
+#pragma unroll
+            for (int u = 0; u < APT; ++u) cp_async16(as + adst[u], asrc[u] + kt * BK);
+            if (p.browmap) {
+#pragma unroll
+                for (int u = 0; u < BPT; ++u)
+                    cp_async16(bs + bdst[u], B + (long long)p.browmap[k0 + brr[u]] * p.ldb + boff[u]);
+            } else {
+#pragma unroll
+                for (int u = 0; u < BPT; ++u)
+                    cp_async16(bs + bdst[u], B + (long long)(k0 + brr[u]) * p.ldb + boff[u]);
+            }
+            return;
+        }
         T *as = As + s * BM * SA;
         T *bs = Bs + s * BK * SB;
-        constexpr int ACH = BM * BK / E;
 #pragma unroll 2
         for (int c = tid; c < ACH; c += NTH) {
             const int r = c / (BK / E), cc = (c % (BK / E)) * E;
@@ -170,7 +213,6 @@ FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int ro
                     dst[e] = (gr < M && gk + e < K) ? A[(long long)gr * p.lda + gk + e] : zero_of(T());
             }
         }
-        constexpr int BCH = BK * BN / E;
 #pragma unroll 2
         for (int c = tid; c < BCH; c += NTH) {
             const int r = c / (BN / E), cc = (c % (BN / E)) * E;
