@@ -206,13 +206,15 @@ FROB_DEV void gj_sweep_1bar(T (&a)[BR][BC], int n, SweepShared1<T, N> &sh, doubl
     const int r0 = ti * BR, c0 = tj * BC;
     const int gbase = lane & ~(G::CT - 1);  // first lane of my block-row group
     unsigned used = 0;                      // my rows already used as pivots
-    for (int k = 0; k < n; ++k) {
+    // steps unrolled by BC: the column's position in its register block (KC) is static
+    auto step = [&](const int k, auto KCc) {
+        constexpr int KC = decltype(KCc)::value;
         const int par = k & 1;
-        const int kb = k / BC, kc = k % BC;
+        const int kb = k / BC;
         // column-k values of my block-row (before this step's update)
         T ck[BR];
 #pragma unroll
-        for (int q = 0; q < BR; ++q) ck[q] = shfl(sel_k<T, BC>(a[q], kc), gbase + kb);
+        for (int q = 0; q < BR; ++q) ck[q] = shfl(a[q][KC], gbase + kb);
         unsigned long long bk = 0;
         int qb = 0;
 #pragma unroll
@@ -250,13 +252,9 @@ FROB_DEV void gj_sweep_1bar(T (&a)[BR][BC], int n, SweepShared1<T, N> &sh, doubl
 #pragma unroll
         for (int c = 0; c < BC; ++c) rp[c] = mul(sh.slot[par][tip][c0 + c], ip);
         if (tj == kb) {
+            rp[KC] = ip;
 #pragma unroll
-            for (int c = 0; c < BC; ++c)
-                if (c == kc) {
-                    rp[c] = ip;
-#pragma unroll
-                    for (int q = 0; q < BR; ++q) a[q][c] = zero_of(T());
-                }
+            for (int q = 0; q < BR; ++q) a[q][KC] = zero_of(T());
         }
 #pragma unroll
         for (int q = 0; q < BR; ++q)
@@ -270,6 +268,13 @@ FROB_DEV void gj_sweep_1bar(T (&a)[BR][BC], int n, SweepShared1<T, N> &sh, doubl
                     for (int c = 0; c < BC; ++c) a[q][c] = rp[c];
                 }
         }
+    };
+    for (int kb = 0; kb * BC < n; ++kb) {
+        bstatic_for<BC>([&](auto KCc) {
+            constexpr int KC = decltype(KCc)::value;
+            const int k = kb * BC + KC;
+            if (k < n) step(k, KCc);
+        });
     }
     __syncthreads();
     sweep_finish<T, N, G::THREADS>(sh, n, pmax, pmin);
