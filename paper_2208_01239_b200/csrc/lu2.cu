@@ -28,11 +28,13 @@ constexpr int P2_T = 512;
 constexpr int P2_WARPS = P2_T / 32;
 constexpr int P2_STG = 18;  // staging row stride in doubles (16 + 2: 16-byte aligned, conflict free)
 
-template <typename T> struct Panel2W { static constexpr int PW = 16; };
-template <> struct Panel2W<double2> { static constexpr int PW = 8; };
+// panel width of one step: two 128-byte row halves (32 real / 16 complex columns)
+template <typename T> struct Panel2W { static constexpr int PW = 32, PH = 16; };
+template <> struct Panel2W<double2> { static constexpr int PW = 8, PH = 8; };  // one half: the two-half complex variant spills
 
-// mv2 layout (ints): [0] = number of moves, [1 .. 1+32) dst, [33 .. 65) src (absolute rows)
-constexpr int MV2_INTS = 1 + 2 * 32;
+// mv2 layout (ints): [0] = number of moves, [1, 1 + MV2_MAX) dst, [1 + MV2_MAX, 1 + 2 MV2_MAX) src
+constexpr int MV2_MAX = 64;
+constexpr int MV2_INTS = 1 + 2 * MV2_MAX;
 
 template <typename F, int... J>
 FROB_DEV void static_for_impl(F &&f, std::integer_sequence<int, J...>) {
@@ -80,10 +82,15 @@ FROB_DEV void ld_row_smem(T (&u)[PW], const T *src) {
     }
 }
 
-// Panel of step k0: rows [k0, n) x columns [k0, k0 + w) of B (ld), factored in place.
-// Thread t owns relative rows t + q * P2_T (q < R).  mv2 receives the row moves of the step,
-// diag[k0 + j] the pivot values.
-template <typename T, int PW, int R>
+// Panel of step k0: rows [k0, n) x columns [k0, k0 + w) of B (ld), w <= 2 * PH, factored in
+// place as two PH-column halves (PH = 16 real / 8 complex: 128-byte row halves).  Thread t owns
+// relative rows t + q * P2_T (q < R).  Half 0 is TMA-loaded and moved to registers; half 1 is
+// TMA-loaded into the staging buffer while half 0 is factored, then receives half 0's rank-PH
+// update there (U12 = L11^{-1} X by PH threads), and the two halves swap places: half 1 goes to
+// registers, half 0's factored rows wait in the staging buffer.  Rows never move inside the
+// panel; both halves are written to their final positions at the end.  mv2 receives the row
+// moves of the step, diag[k0 + j] the pivot values.
+template <typename T, int PH, int R, bool TWO>
 __global__ void __launch_bounds__(P2_T, 1)
 lu_panel2_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, long long ld, int n, int k0, int w,
                  int *__restrict__ mv2, T *__restrict__ diag) {
@@ -96,30 +103,56 @@ lu_panel2_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, lo
     }
     pdl_wait();
     P2T(0);
+    constexpr int PW = 2 * PH;                     // panel width in elements
     __shared__ unsigned long long ck[2][P2_WARPS];
     __shared__ int ci[2][P2_WARPS];
-    __shared__ __align__(16) T wrow[2][P2_WARPS][PW];
-    __shared__ T wrcp[2][P2_WARPS];
+    __shared__ __align__(16) T wrow[2][P2_WARPS][PH];
     __shared__ int pivrow[PW];
     __shared__ int vac[PW];
     __shared__ unsigned evm_s;
+    __shared__ T L11s[PH][PH + 1];
+    __shared__ T U12s[PH][PH + 1];
+    __shared__ int sdst[R * P2_T];
 
-    constexpr int RW = PW * (int)(sizeof(T) / 8);  // doubles per row (16)
-    static_assert(RW == 16, "panel rows are 128 bytes");
+    constexpr int RW = PH * (int)(sizeof(T) / 8);  // doubles per row half (16)
+    static_assert(RW == 16, "panel row halves are 128 bytes");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int m = n - k0;
-
-    // ---- TMA load: boxes of 256 rows x 128 bytes (rows >= n and columns >= n arrive as zeros)
     const int E = (int)(sizeof(T) / 8);
     const int nbox = (m + 255) / 256;
-    if (tid == 0) {
+    const bool two = TWO && w > PH;  // TWO = false compiles the second half out (complex: spills)
+    auto tma_half = [&](int h, unsigned parity_unused) {
+        (void)parity_unused;
         mbar_arrive_expect_tx(smem_u32(&tbar), (unsigned)(nbox * 256 * 128));
         for (int b = 0; b < nbox; ++b)
-            tma_load_2d(smem_u32(stgb + b * 256 * 128), &tmap, k0 * E, k0 + 256 * b, smem_u32(&tbar));
-    }
+            tma_load_2d(smem_u32(stgb + b * 256 * 128), &tmap, (k0 + h * PH) * E, k0 + 256 * b, smem_u32(&tbar));
+    };
+    auto row_from_stg = [&](int r, T (&dst)[PH]) {
+        double t[16];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const double2 v = *reinterpret_cast<const double2 *>(stgb + swz128(r, c));
+            t[2 * c] = v.x;
+            t[2 * c + 1] = v.y;
+        }
+#pragma unroll
+        for (int c = 0; c < PH; ++c) {
+            if constexpr (sizeof(T) == 8) dst[c] = t[c];
+            else dst[c] = make_double2(t[2 * c], t[2 * c + 1]);
+        }
+    };
+    auto row_to_stg = [&](int r, const T (&src)[PH]) {
+        const double *rd = reinterpret_cast<const double *>(src);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<double2 *>(stgb + swz128(r, c)) = make_double2(rd[2 * c], rd[2 * c + 1]);
+    };
+
+    // ---- half 0: TMA load -> registers; half 1 then streams into the staging buffer
+    if (tid == 0) tma_half(0, 0u);
     __syncthreads();
     mbar_wait_cta(smem_u32(&tbar), 0u);
-    T a[R][PW];
+    T a[R][PH];
     int grow[R], pst[R];
     unsigned live = 0;
 #pragma unroll
@@ -127,153 +160,194 @@ lu_panel2_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, lo
         grow[q] = q * P2_T + tid;
         pst[q] = -1;
         if (grow[q] < m) live |= 1u << q;
-        double t[16];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            const double2 v = *reinterpret_cast<const double2 *>(stgb + swz128(grow[q], c));
-            t[2 * c] = v.x;
-            t[2 * c + 1] = v.y;
-        }
-#pragma unroll
-        for (int c = 0; c < PW; ++c) {
-            if constexpr (sizeof(T) == 8) a[q][c] = t[c];
-            else a[q][c] = make_double2(t[2 * c], t[2 * c + 1]);
-        }
+        row_from_stg(grow[q], a[q]);
+    }
+    __syncthreads();  // every thread has read its half-0 rows: the staging buffer is free
+    if (two && tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tma_half(1, 1u);
     }
     P2T(1);
-    // ---- candidate of column 0 + publish
-    auto candidate = [&](auto Jc, unsigned long long &bk, int &bi, int &bq, T &brcp) {
+
+    auto candidate = [&](auto Jc, unsigned long long &bk, int &bi, int &bq) {
         constexpr int J = decltype(Jc)::value;
         bk = 0ull;
         bi = INT_MAX;
         bq = 0;
-        T myp = zero_of(T());
 #pragma unroll
         for (int q = 0; q < R; ++q)
             if ((live >> q) & 1u) {
                 const unsigned long long kq = pkey_bits(a[q][J]);
-                if (kq > bk) { bk = kq; bi = grow[q]; bq = q; myp = a[q][J]; }
+                if (kq > bk) { bk = kq; bi = grow[q]; bq = q; }
             }
-#ifdef FROB_P2_SPEC_RCP
-        brcp = rcp_spec(myp);
-#else
-        brcp = myp;
-#endif
     };
-    auto publish_row = [&](int s, int bq, const T &brcp) {
-#pragma unroll
-        for (int q = 0; q < R; ++q)
-            if (q == bq) st_row_smem<T, PW>(wrow[s][warp], a[q]);
-        wrcp[s][warp] = brcp;
-    };
-    {
-        unsigned long long bk; int bi, bq; T brcp;
-        candidate(std::integral_constant<int, 0>{}, bk, bi, bq, brcp);
+    auto publish_first = [&]() {
+        unsigned long long bk; int bi, bq;
+        candidate(std::integral_constant<int, 0>{}, bk, bi, bq);
         const ArgMaxK wa = warp_argmax_key(bk, bi);
         if (lane == 0) { ck[0][warp] = wa.k; ci[0][warp] = wa.i; }
-        if (bi == wa.i && wa.k != 0ull) publish_row(0, bq, brcp);
-    }
+        if (bi == wa.i && wa.k != 0ull) {
+#pragma unroll
+            for (int q = 0; q < R; ++q)
+                if (q == bq) st_row_smem<T, PH>(wrow[0][warp], a[q]);
+        }
+    };
 
-    // ---- column loop (fully unrolled: static register indices)
-    // Software-pipelined: the rank-1 update of pivot J-1 on columns >= J+1 is deferred into
-    // iteration J, right after the barrier, where it overlaps the block argmax; only column J
-    // (needed for the candidate keys) and the published candidate row are updated eagerly.
-    T u[PW];          // pivot row of the current (then previous) column
+    // ---- column loop over one half (fully unrolled: static register indices), JO = offset of
+    // the half.  Software-pipelined: the rank-1 update of pivot J-1 on columns >= J+1 is
+    // deferred into iteration J, right after the barrier; only column J+1 (needed for the
+    // candidate keys) and the published candidate row are updated eagerly.
+    T u[PH];          // pivot row of the current (then previous) column
     T lp[R];          // multipliers of the pending (deferred) update
     unsigned pact = 0;  // rows with a pending update
+    auto run_half = [&](const int JO, const int wh) {
 #pragma unroll
-    for (int c = 0; c < PW; ++c) u[c] = zero_of(T());
+        for (int c = 0; c < PH; ++c) u[c] = zero_of(T());
 #pragma unroll
-    for (int q = 0; q < R; ++q) lp[q] = zero_of(T());
-    auto column = [&](auto Jc) {
-        constexpr int J = decltype(Jc)::value;
-        constexpr int s = J & 1;
-        P2TJ(J, 40);
-        __syncthreads();
-        P2TJ(J, 41);
-        // (a) deferred update of pivot J-1 (columns >= J+1)
-#pragma unroll
-        for (int q = 0; q < R; ++q)
-            if ((pact >> q) & 1u) {
-#pragma unroll
-                for (int c = J + 1; c < PW; ++c) a[q][c] = msub(a[q][c], lp[q], u[c]);
-            }
-        // (b) block argmax over the warp candidates, pivot row + its reciprocal
-        const ArgMaxK ba = warp_argmax_key(lane < P2_WARPS ? ck[s][lane] : 0ull,
-                                           lane < P2_WARPS ? ci[s][lane] : INT_MAX);
-        const int gi = ba.i;
-        const unsigned ww = ((unsigned)gi & (unsigned)(P2_T - 1)) >> 5;
-        ld_row_smem<T, PW>(u, wrow[s][ww]);
-#ifdef FROB_P2_SPEC_RCP
-        const T rc = wrcp[s][ww];
-#else
-        const T rc = rcp_spec(u[J]);
-#endif
-        P2TJ(J, 42);
-        if (tid == 0) {
-            pivrow[J] = gi;
-            diag[k0 + J] = u[J];
-        }
-        // (c) multipliers, eager update of column J+1
-        T l[R];
+        for (int q = 0; q < R; ++q) lp[q] = zero_of(T());
         pact = 0;
+        auto column = [&](auto Jc) {
+            constexpr int J = decltype(Jc)::value;
+            constexpr int s = J & 1;
+            P2TJ(J, 40);
+            __syncthreads();
+            P2TJ(J, 41);
+            // (a) deferred update of pivot J-1 (columns >= J+1)
 #pragma unroll
-        for (int q = 0; q < R; ++q) {
-            const bool lv = (live >> q) & 1u;
-            const bool isp = lv && grow[q] == gi;
-            if (isp) { live &= ~(1u << q); pst[q] = J; }
-            const bool act = lv && !isp;
-            l[q] = act ? mul(a[q][J], rc) : zero_of(T());
-            if (act) {
-                pact |= 1u << q;
-                a[q][J] = l[q];
-                if constexpr (J + 1 < PW) a[q][J + 1] = msub(a[q][J + 1], l[q], u[J + 1]);
+            for (int q = 0; q < R; ++q)
+                if ((pact >> q) & 1u) {
+#pragma unroll
+                    for (int c = J + 1; c < PH; ++c) a[q][c] = msub(a[q][c], lp[q], u[c]);
+                }
+            // (b) block argmax over the warp candidates, pivot row + its reciprocal
+            const ArgMaxK ba = warp_argmax_key(lane < P2_WARPS ? ck[s][lane] : 0ull,
+                                               lane < P2_WARPS ? ci[s][lane] : INT_MAX);
+            const int gi = ba.i;
+            const unsigned ww = ((unsigned)gi & (unsigned)(P2_T - 1)) >> 5;
+            ld_row_smem<T, PH>(u, wrow[s][ww]);
+            const T rc = rcp_spec(u[J]);
+            P2TJ(J, 42);
+            if (tid == 0) {
+                pivrow[JO + J] = gi;
+                diag[k0 + JO + J] = u[J];
             }
-            lp[q] = l[q];
-        }
-        P2TJ(J, 43);
-        if constexpr (J + 1 < PW) {
-            if (J + 1 < w) {
-                // (e) candidate of column J+1, warp argmax
-                unsigned long long bk; int bi, bq; T brcp;
-                candidate(std::integral_constant<int, J + 1>{}, bk, bi, bq, brcp);
-                const ArgMaxK wa = warp_argmax_key(bk, bi);
-                if (lane == 0) { ck[s ^ 1][warp] = wa.k; ci[s ^ 1][warp] = wa.i; }
-                P2TJ(J, 44);
-                // (f) the warp winner publishes its row updated through pivot J
-                if (bi == wa.i && wa.k != 0ull) {
-                    T lw = l[0];
+            // (c) multipliers, eager update of column J+1
+            T l[R];
+            pact = 0;
 #pragma unroll
-                    for (int q = 1; q < R; ++q)
-                        if (q == bq) lw = l[q];
-                    T *dst = wrow[s ^ 1][warp];
-                    auto rowval = [&](const int c) {
-                        T v = a[0][c];
+            for (int q = 0; q < R; ++q) {
+                const bool lv = (live >> q) & 1u;
+                const bool isp = lv && grow[q] == gi;
+                if (isp) { live &= ~(1u << q); pst[q] = JO + J; }
+                const bool act = lv && !isp;
+                l[q] = act ? mul(a[q][J], rc) : zero_of(T());
+                if (act) {
+                    pact |= 1u << q;
+                    a[q][J] = l[q];
+                    if constexpr (J + 1 < PH) a[q][J + 1] = msub(a[q][J + 1], l[q], u[J + 1]);
+                }
+                lp[q] = l[q];
+            }
+            P2TJ(J, 43);
+            if constexpr (J + 1 < PH) {
+                if (J + 1 < wh) {
+                    // (e) candidate of column J+1, warp argmax
+                    unsigned long long bk; int bi, bq;
+                    candidate(std::integral_constant<int, J + 1>{}, bk, bi, bq);
+                    const ArgMaxK wa = warp_argmax_key(bk, bi);
+                    if (lane == 0) { ck[s ^ 1][warp] = wa.k; ci[s ^ 1][warp] = wa.i; }
+                    P2TJ(J, 44);
+                    // (f) the warp winner publishes its row updated through pivot J
+                    if (bi == wa.i && wa.k != 0ull) {
+                        T lw = l[0];
 #pragma unroll
                         for (int q = 1; q < R; ++q)
-                            if (q == bq) v = a[q][c];
-                        return (c >= J + 2) ? msub(v, lw, u[c]) : v;
-                    };
-                    if constexpr (sizeof(T) == 8) {
+                            if (q == bq) lw = l[q];
+                        T *dst = wrow[s ^ 1][warp];
+                        auto rowval = [&](const int c) {
+                            T v = a[0][c];
 #pragma unroll
-                        for (int c = 0; c < PW; c += 2)
-                            *reinterpret_cast<double2 *>(dst + c) = make_double2(rowval(c), rowval(c + 1));
-                    } else {
+                            for (int q = 1; q < R; ++q)
+                                if (q == bq) v = a[q][c];
+                            return (c >= J + 2) ? msub(v, lw, u[c]) : v;
+                        };
+                        if constexpr (sizeof(T) == 8) {
 #pragma unroll
-                        for (int c = 0; c < PW; ++c) dst[c] = rowval(c);
+                            for (int c = 0; c < PH; c += 2)
+                                *reinterpret_cast<double2 *>(dst + c) = make_double2(rowval(c), rowval(c + 1));
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < PH; ++c) dst[c] = rowval(c);
+                        }
                     }
-                    wrcp[s ^ 1][warp] = brcp;
+                    P2TJ(J, 45);
                 }
-                P2TJ(J, 45);
             }
-        }
-        P2T(2 + J);
+            P2T(2 + J);
+        };
+        static_for<PH>([&](auto Jc) {
+            constexpr int Jv = decltype(Jc)::value;
+            if (Jv < wh) column(Jc);
+        });
     };
-    static_for<PW>([&](auto Jc) {
-        constexpr int Jv = decltype(Jc)::value;
-        if (Jv < w) column(Jc);
-    });
+
+    publish_first();
+    run_half(0, min(w, PH));
     __syncthreads();
+
+    if constexpr (TWO) if (two) {
+        // ---- half 1: U12 = L11^{-1} X from half 0's pivot rows, rank-PH update, swap
+        mbar_wait_cta(smem_u32(&tbar), 1u);
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+            if (pst[q] >= 0) {
+                T x[PH];
+                row_from_stg(grow[q], x);
+#pragma unroll
+                for (int c = 0; c < PH; ++c) {
+                    L11s[pst[q]][c] = a[q][c];
+                    U12s[pst[q]][c] = x[c];
+                }
+            }
+        __syncthreads();
+        if (tid < PH) {
+            T x[PH];
+#pragma unroll
+            for (int j = 0; j < PH; ++j) x[j] = U12s[j][tid];
+#pragma unroll
+            for (int q = 0; q < PH; ++q)
+#pragma unroll
+                for (int j = q + 1; j < PH; ++j) x[j] = msub(x[j], L11s[j][q], x[q]);
+#pragma unroll
+            for (int j = 0; j < PH; ++j) U12s[j][tid] = x[j];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const int g = grow[q];
+            if (g >= m) continue;
+            T x[PH];
+            row_from_stg(g, x);
+            if (pst[q] >= 0) {
+#pragma unroll
+                for (int c = 0; c < PH; ++c) x[c] = U12s[pst[q]][c];
+            } else {
+#pragma unroll
+                for (int j = 0; j < PH; ++j) {
+                    const T lj = a[q][j];
+#pragma unroll
+                    for (int c = 0; c < PH; ++c) x[c] = msub(x[c], lj, U12s[j][c]);
+                }
+            }
+            row_to_stg(g, a[q]);  // half 0's factored row waits in the staging buffer
+#pragma unroll
+            for (int c = 0; c < PH; ++c) a[q][c] = x[c];
+        }
+        __syncthreads();
+        publish_first();
+        run_half(PH, w - PH);
+        __syncthreads();
+    }
     P2T(20);
 
     // ---- final positions: pivot j -> j; evicted top rows (< w, not pivots) fill the rows
@@ -298,48 +372,54 @@ lu_panel2_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, lo
         if (moved) {
             const int q = __popc(mb & ((1u << lane) - 1u));
             mv2[1 + q] = k0 + lane;
-            mv2[33 + q] = k0 + pj;
+            mv2[1 + MV2_MAX + q] = k0 + pj;
         }
         const bool ev = (evmask >> lane) & 1u;
         if (ev) {
             const int q = nm + __popc(evmask & ((1u << lane) - 1u));
             mv2[1 + q] = k0 + vac[__popc(evmask & ((1u << lane) - 1u))];
-            mv2[33 + q] = k0 + lane;
+            mv2[1 + MV2_MAX + q] = k0 + lane;
         }
         if (lane == 0) mv2[0] = nm + __popc(evmask);
     }
     __syncthreads();
     const unsigned evm = evm_s;
-    // ---- rows to their final positions in the staging buffer, then TMA box stores
+    int mydst[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) {
         const int g = grow[q];
-        if (g >= m) continue;
         int dst = g;
         if (pst[q] >= 0) dst = pst[q];
         else if (g < w) dst = vac[__popc(evm & ((1u << g) - 1u))];
-        const double *rd = reinterpret_cast<const double *>(a[q]);
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-            *reinterpret_cast<double2 *>(stgb + swz128(dst, c)) = make_double2(rd[2 * c], rd[2 * c + 1]);
+        mydst[q] = dst;
+        if (g < m) sdst[q * P2_T + tid] = dst;
     }
     __syncthreads();
-    // coalesced write-back: 8 threads per 128-byte row (measured faster than a TMA box store
-    // followed by its completion wait)
-    {
-        const long long ldd = ld * E;
-        double *P = reinterpret_cast<double *>(B) + (long long)k0 * ldd + (long long)k0 * E;
-        const int wd = w * E;
+    // coalesced write-back, 8 threads per 128-byte row half
+    const long long ldd = ld * E;
+    double *P = reinterpret_cast<double *>(B) + (long long)k0 * ldd + (long long)k0 * E;
+    auto write_half = [&](int h, bool by_origin) {
+        const int wd = (min(w, (h + 1) * PH) - h * PH) * E;
 #pragma unroll 4
         for (int idx = tid; idx < m * 8; idx += P2_T) {
             const int r = idx >> 3, c = idx & 7;
             if (2 * c >= wd) continue;
+            const int d = by_origin ? sdst[r] : r;
             const double2 v = *reinterpret_cast<const double2 *>(stgb + swz128(r, c));
-            double *out = P + (long long)r * ldd + 2 * c;
+            double *out = P + (long long)d * ldd + h * PH * E + 2 * c;
             if (2 * c + 1 < wd) *reinterpret_cast<double2 *>(out) = v;
             else out[0] = v.x;
         }
+    };
+    if constexpr (TWO) if (two) {
+        write_half(0, true);  // half 0 rows sit at their original positions in the staging buffer
+        __syncthreads();
     }
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+        if (grow[q] < m) row_to_stg(mydst[q], a[q]);
+    __syncthreads();
+    write_half(two ? 1 : 0, false);
     P2T(21);
 }
 
@@ -372,7 +452,7 @@ lu_update2_kernel(const T *__restrict__ Bk, T *__restrict__ Bn, long long ld, in
     pdl_wait();
     constexpr int SP = SPad<T>::P;
     constexpr int E = 16 / (int)sizeof(T);  // elements per 16-byte chunk
-    __shared__ int mdst[32], msrc[32];
+    __shared__ int mdst[MV2_MAX], msrc[MV2_MAX];
     __shared__ int nmv_s;
     __shared__ __align__(16) T L11[PW][PW + SP];
     __shared__ __align__(16) T Us[PW][U2_TC];          // X, then U12 in place
@@ -409,11 +489,11 @@ lu_update2_kernel(const T *__restrict__ Bk, T *__restrict__ Bn, long long ld, in
         }
     }
     // ---- 2. the move list
-    if (tid < 32) {
+    if (tid < MV2_MAX) {
         const int nm = mv2[0];
         if (tid == 0) nmv_s = nm;
         mdst[tid] = tid < nm ? mv2[1 + tid] : -1;
-        msrc[tid] = tid < nm ? mv2[33 + tid] : -1;
+        msrc[tid] = tid < nm ? mv2[1 + MV2_MAX + tid] : -1;
     }
     __syncthreads();
     const int nm = nmv_s;
@@ -543,7 +623,7 @@ size_t lu2_int_elems(int n) {
     return (size_t)n /* iperm */ + steps * MV2_INTS + steps * (size_t)n /* snapshots */;
 }
 
-template <typename T, int PW, int R>
+template <typename T, int PH, int R>
 static cudaError_t launch_panel2(const CUtensorMap &tm, T *B, long long ld, int n, int k0, int w, int *mv2, T *diag,
                                  cudaStream_t s) {
     const size_t smem = (size_t)R * P2_T * 128 + 1024;
@@ -551,7 +631,8 @@ static cudaError_t launch_panel2(const CUtensorMap &tm, T *B, long long ld, int 
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !attr_set[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(lu_panel2_kernel<T, PW, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(lu_panel2_kernel<T, PH, R, (Panel2W<T>::PW > PH)>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
         attr_set[dev] = true;
@@ -560,13 +641,14 @@ static cudaError_t launch_panel2(const CUtensorMap &tm, T *B, long long ld, int 
     double wk = 0.0;
     for (int j = 0; j < w; ++j) wk += (double)(n - k0 - j - 1) * (1.0 + 2.0 * (w - j - 1));
     ProfScope ps(sizeof(T) == 8 ? "lu_panel2<double>" : "lu_panel2<double2>", s, wk * (sizeof(T) == 8 ? 1.0 : 4.0));
-    return launch_pdl(lu_panel2_kernel<T, PW, R>, dim3(1), dim3(P2_T), smem, s, tm, B, ld, n, k0, w, mv2, diag);
+    return launch_pdl(lu_panel2_kernel<T, PH, R, (Panel2W<T>::PW > PH)>, dim3(1), dim3(P2_T), smem, s, tm, B, ld, n,
+                      k0, w, mv2, diag);
 }
 
 template <typename T>
 cudaError_t lu2_factor(int n, T *B0, T *B1, long long ld, T *U, T *L, long long ldo, int *perm, int *iw, T *diag,
                        LuStats *stats, cudaStream_t s) {
-    constexpr int PW = Panel2W<T>::PW;
+    constexpr int PW = Panel2W<T>::PW, PH = Panel2W<T>::PH;
     if (n > LU2_MAX_N) return cudaErrorInvalidValue;
     const int steps = (n + PW - 1) / PW;
     int *iperm = iw;
@@ -585,8 +667,8 @@ cudaError_t lu2_factor(int n, T *B0, T *B1, long long ld, T *U, T *L, long long 
         T *Bk = (k & 1) ? B1 : B0;
         T *Bn = (k & 1) ? B0 : B1;
         int *mv2 = mvb + (size_t)k * MV2_INTS;
-        if (m <= P2_T) e = launch_panel2<T, PW, 1>(tm[k & 1], Bk, ld, n, k0, w, mv2, diag, s);
-        else e = launch_panel2<T, PW, 2>(tm[k & 1], Bk, ld, n, k0, w, mv2, diag, s);
+        if (m <= P2_T) e = launch_panel2<T, PH, 1>(tm[k & 1], Bk, ld, n, k0, w, mv2, diag, s);
+        else e = launch_panel2<T, PH, 2>(tm[k & 1], Bk, ld, n, k0, w, mv2, diag, s);
         if (e != cudaSuccess) return e;
         const int rest = n - k0 - w;
         dim3 grid(max(1, (rest + U2_TC - 1) / U2_TC), max(1, (rest + U2_TR - 1) / U2_TR));

@@ -137,7 +137,7 @@ void run(int n, int reps, bool use3 = false) {
 
 template <typename T>
 void pieces(int n) {
-    constexpr int PW = Panel2W<T>::PW;
+    constexpr int PW = Panel2W<T>::PW, PH = Panel2W<T>::PH;
     const long long ld = (n + 7) / 8 * 8;
     const size_t bytes = (size_t)n * ld * sizeof(T);
     std::vector<double> h(bytes / 8);
@@ -162,8 +162,8 @@ void pieces(int n) {
     CUtensorMap tmap;
     CK(tma_map_rows128(&tmap, B0, n, (long long)n * (sizeof(T) / 8), ld * (sizeof(T) / 8), 256));
     tm("panel2 (m=n) x20", [&] {
-        if (n <= P2_T) launch_panel2<T, PW, 1>(tmap, B0, ld, n, 0, PW, iw, diag, 0);
-        else launch_panel2<T, PW, 2>(tmap, B0, ld, n, 0, PW, iw, diag, 0);
+        if (n <= P2_T) launch_panel2<T, PH, 1>(tmap, B0, ld, n, 0, PW, iw, diag, 0);
+        else launch_panel2<T, PH, 2>(tmap, B0, ld, n, 0, PW, iw, diag, 0);
     }, 20);
 #ifdef FROB_P2_TRACE
     {
@@ -185,8 +185,8 @@ void pieces(int n) {
                    (const int *)iw, perm, iperm, (int *)nullptr);
     }, 20);
     tm("panel2+update2 alternating x20", [&] {
-        if (n <= P2_T) launch_panel2<T, PW, 1>(tmap, B0, ld, n, 0, PW, iw, diag, 0);
-        else launch_panel2<T, PW, 2>(tmap, B0, ld, n, 0, PW, iw, diag, 0);
+        if (n <= P2_T) launch_panel2<T, PH, 1>(tmap, B0, ld, n, 0, PW, iw, diag, 0);
+        else launch_panel2<T, PH, 2>(tmap, B0, ld, n, 0, PW, iw, diag, 0);
         launch_pdl(lu_update2_kernel<T, PW>, grid, dim3(U2_T), 0, (cudaStream_t)0, (const T *)B0, B1, ld, n, 0, PW,
                    (const int *)iw, perm, iperm, (int *)nullptr);
     }, 20);
