@@ -41,6 +41,7 @@ struct GemmParams {
     int early_trigger;               // set by the launcher: release dependents at entry
                                      // (single-wave grids) instead of after the main loop
     double mu;                       // EPI_FROB_*: output scaled by (1 + mu i) (Alg 5 line 5)
+    int force_split;                 // request split-K even above the tile-count threshold
     int ksplit;                      // set by the launcher: > 1 = split-K, each CTA adds its
                                      // k-chunk's alpha * partial into C (pre-set to beta * D)
                                      // with fp64 atomics (order of the S adds not fixed)
