@@ -444,7 +444,7 @@ FROB_DEV void cp_row16(T *dst, const T *src, int nelem) {  // nelem * sizeof(T) 
 }
 
 template <typename T, int PW>
-__global__ void __launch_bounds__(U2_T)
+__global__ void __launch_bounds__(U2_T, 2)
 lu_update2_kernel(const T *__restrict__ Bk, T *__restrict__ Bn, long long ld, int n, int k0, int w,
                   const int *__restrict__ mv2, int *__restrict__ perm, int *__restrict__ iperm,
                   int *__restrict__ snap) {
