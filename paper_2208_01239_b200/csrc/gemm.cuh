@@ -42,9 +42,9 @@ struct GemmParams {
                                      // (single-wave grids) instead of after the main loop
     double mu;                       // EPI_FROB_*: output scaled by (1 + mu i) (Alg 5 line 5)
     int force_split;                 // request split-K even above the tile-count threshold
-    int ksplit;                      // set by the launcher: > 1 = split-K, each CTA adds its
-                                     // k-chunk's alpha * partial into C (pre-set to beta * D)
-                                     // with fp64 atomics (order of the S adds not fixed)
+    int ksplit;                      // set by the launcher: > 1 = split-K over a (1, 1, ksplit)
+                                     // cluster; the partials meet in distributed shared memory
+                                     // and are summed in chunk order (deterministic)
 };
 
 // Up to two independent problems in one launch (blockIdx.z < zsplit -> q[0], else q[1]).
@@ -74,7 +74,10 @@ template <int BIG> struct GemmCfg<double2, BIG> {
 template <typename T, int BIG = 0>
 constexpr size_t gemm_smem_bytes() {
     using C = GemmCfg<T, BIG>;
-    return (size_t)C::STAGES * ((size_t)C::BM * (C::BK + C::PADA) + (size_t)C::BK * (C::BN + C::PADB)) * sizeof(T);
+    // (the split-K cluster reduction reuses the stages for one BM x (BN + pad) partial)
+    const size_t st = (size_t)C::STAGES * ((size_t)C::BM * (C::BK + C::PADA) + (size_t)C::BK * (C::BN + C::PADB)) * sizeof(T);
+    const size_t part = (size_t)C::BM * (C::BN + (sizeof(T) == 8 ? 4 : 0)) * sizeof(T);
+    return st > part ? st : part;
 }
 
 // ---------------------------------------------------------------- MMA micro-kernels
@@ -110,7 +113,42 @@ FROB_DEV double acc_re(double2 v) { return v.x; }
 FROB_DEV double acc_im(double2 v) { return v.y; }
 FROB_DEV double2 acc_val(const double (&c)[4], int e) { return make_double2(c[e], c[2 + e]); }
 
-template <typename T, bool VEC, int BIG>
+// Split-K cluster reduction (see gemm_tile): out of line so that its registers do not add to the
+// main loop's allocation.  P = this CTA's BM x PS partial in shared memory.
+template <typename T, int BM, int BN, int PS, int NTH>
+FROB_DEV void split_reduce(const int S, const int M, const int N, const double alpha, const double beta,
+                                          const T *__restrict__ D, const long long ldd, T *Cp, const long long ldc,
+                                          const int *__restrict__ colperm, const int row0, const int col0,
+                                          const T *P) {
+    cluster_sync_all();
+    const int tid = threadIdx.x;
+    unsigned rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const unsigned pbase = smem_u32(P);
+    constexpr int TILE = BM * BN, SMAX = 8;
+    const int per = (TILE + S - 1) / S;
+    const int lo = (int)rank * per, hi = min(TILE, lo + per);
+    for (int idx = lo + tid; idx < hi; idx += NTH) {
+        // all S remote loads in flight before the adds; summed in rank (= chunk) order
+        const unsigned off = pbase + (unsigned)(((idx / BN) * PS + idx % BN) * sizeof(T));
+        T part[SMAX];
+#pragma unroll
+        for (int q = 0; q < SMAX; ++q)
+            if (q < S) part[q] = ld_cluster(mapa_u32(off, (unsigned)q), T());
+        const int row = row0 + idx / BN, col = col0 + idx % BN;
+        if (row >= M || col >= N) continue;
+        T v = part[0];
+#pragma unroll
+        for (int q = 1; q < SMAX; ++q)
+            if (q < S) v = add(v, part[q]);
+        v = scal(v, alpha);
+        if (beta != 0.0) v = add(v, scal(D[(long long)row * ldd + col], beta));
+        Cp[(long long)row * ldc + (colperm ? colperm[col] : col)] = v;
+    }
+    cluster_sync_all();  // keep this CTA's partial alive until every reader is done
+}
+
+template <typename T, bool VEC, int BIG, bool SPLIT>
 FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int row0, const int col0, T *As, T *Bs) {
     using Cf = GemmCfg<T, BIG>;
     constexpr int BM = Cf::BM, BN = Cf::BN, BK = Cf::BK, STAGES = Cf::STAGES;
@@ -134,14 +172,13 @@ FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int ro
     if (p.triB == TRI_UPPER) ke = min(ke, col0 + BN);
     else if (p.triB == TRI_LOWER) kb = max(kb, col0);
     kb = (kb / BK) * BK;
-    if (p.ksplit > 1) {
+    if (SPLIT) {
         const int tot = (ke > kb) ? (ke - kb + BK - 1) / BK : 0;
         const int per = (tot + p.ksplit - 1) / p.ksplit;
         const int c = (int)(blockIdx.z % p.ksplit);
         const int b2 = kb + c * per * BK;
         ke = min(ke, b2 + per * BK);
-        kb = b2;
-        if (kb >= ke) { pdl_trigger(); return; }
+        kb = b2;  // an empty chunk still joins the cluster reduction (adds zero)
     }
     const int nk = (ke > kb) ? (ke - kb + BK - 1) / BK : 0;
 
@@ -268,28 +305,22 @@ FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int ro
     // the memory latency is paid once, not once per element.
     const T *__restrict__ D = p.D ? p.D + bz * p.sD : nullptr;
     T *Cp = p.C + bz * p.sC;
-    if (p.ksplit > 1) {
+    if constexpr (SPLIT) {
+        // deterministic split-K: the cluster's S CTAs hold the partials of one tile; each writes
+        // its partial to its own shared memory, then reduces 1/S of the tile over all S partials
+        // (read through DSMEM in rank order, so the summation order is fixed) and stores it
+        constexpr int PS = BN + (sizeof(T) == 8 ? 4 : 0);
+        static_assert((size_t)BM * PS * sizeof(T) <= gemm_smem_bytes<T, BIG>(), "partial fits the stages");
+        T *P = As;
+        __syncthreads();  // all warps done with the stage buffers
 #pragma unroll
-        for (int i = 0; i < MT; ++i) {
-            const int row = row0 + wm0 + i * 8 + g;
-            if (row >= M) continue;
+        for (int i = 0; i < MT; ++i)
 #pragma unroll
             for (int j = 0; j < NT; ++j)
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int col = col0 + wn0 + j * 8 + 2 * t + e;
-                    if (col >= N) continue;
-                    const int oc = p.colperm ? p.colperm[col] : col;
-                    const T v = scal(acc_val(acc[i][j], e), p.alpha);
-                    double *dst = reinterpret_cast<double *>(Cp + (long long)row * p.ldc + oc);
-                    if constexpr (sizeof(T) == 8) {
-                        atomicAdd(dst, acc_re(v));
-                    } else {
-                        atomicAdd(dst, acc_re(v));
-                        atomicAdd(dst + 1, acc_im(v));
-                    }
-                }
-        }
+                for (int e = 0; e < 2; ++e)
+                    P[(wm0 + i * 8 + g) * PS + wn0 + j * 8 + 2 * t + e] = acc_val(acc[i][j], e);
+        split_reduce<T, BM, BN, PS, NTH>(p.ksplit, M, N, p.alpha, p.beta, D, p.ldd, Cp, p.ldc, p.colperm, row0, col0, P);
         return;
     }
     if constexpr (sizeof(T) == 8) {
@@ -369,7 +400,9 @@ FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int ro
     }
 }
 
-template <typename T, bool VEC, int BIG>
+// SPLIT: the split-K instantiation (cluster launch, see gemm_tile); a separate kernel so that its
+// reduction code does not raise the register allocation of the plain GEMM
+template <typename T, bool VEC, int BIG, bool SPLIT>
 __global__ void __launch_bounds__(GemmCfg<T, BIG>::WGM * GemmCfg<T, BIG>::WGN * 32)
 gemm_kernel(GemmPair<T> pp) {
     using Cf = GemmCfg<T, BIG>;
@@ -381,11 +414,11 @@ gemm_kernel(GemmPair<T> pp) {
     // them at entry lets the next grid's waiting CTAs occupy SM slots this GEMM still needs
     if (pp.q[0].early_trigger) pdl_trigger();
     pdl_wait();
-    const int z = blockIdx.z / max(1, pp.q[0].ksplit);  // ksplit is equal in both problems
+    const int z = SPLIT ? blockIdx.z / pp.q[0].ksplit : blockIdx.z;  // ksplit is equal in both problems
     const GemmParams<T> &p = (z < pp.zsplit) ? pp.q[0] : pp.q[1];
     const long long bz = (z < pp.zsplit) ? z : z - pp.zsplit;
-    if (!p.counter) {
-        gemm_tile<T, VEC, BIG>(p, bz, blockIdx.y * Cf::BM, blockIdx.x * Cf::BN, As, Bs);
+    if (SPLIT || !p.counter) {
+        gemm_tile<T, VEC, BIG, SPLIT>(p, bz, blockIdx.y * Cf::BM, blockIdx.x * Cf::BN, As, Bs);
         return;
     }
     // persistent: tiles in order of max(I, J) = 0, 1, ... (longest k-range first for
@@ -405,7 +438,7 @@ gemm_kernel(GemmPair<T> pp) {
         const int r = tt - d * d;
         const int I = (r <= d) ? d : r - d - 1;
         const int J = (r <= d) ? r : d;
-        gemm_tile<T, VEC, BIG>(p, bz, I * Cf::BM, J * Cf::BN, As, Bs);
+        gemm_tile<T, VEC, BIG, false>(p, bz, I * Cf::BM, J * Cf::BN, As, Bs);
     }
 }
 

@@ -29,32 +29,10 @@ static double gemm_work(const GemmPair<T> &pp, int b0, int b1) {
     return one(pp.q[0]) * b0 + (b1 > 0 ? one(pp.q[1]) * b1 : 0.0);
 }
 
-// split-K needs C = beta * D before the atomic adds: beta == 0 (C zeroed here) or D == C with
-// beta == 1 (accumulate in place); no fused epilogues
+// split-K (cluster reduction, see gemm_tile) serves plain-store epilogues of non-persistent GEMMs
 template <typename T>
 static bool split_ok(const GemmParams<T> &p) {
-    return !p.counter && (p.beta == 0.0 || (p.beta == 1.0 && p.D == p.C && p.ldd == p.ldc && p.sD == p.sC));
-}
-template <typename T>
-__global__ void zero_block_kernel(T *__restrict__ C, long long ldc, long long sC, int M, int N, int batch,
-                                  const int *__restrict__ colperm) {
-    pdl_trigger();
-    pdl_wait();
-    const long long total = (long long)M * N * batch;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const long long b = idx / ((long long)M * N);
-        const long long r = idx - b * M * N;
-        const int i = (int)(r / N), j = (int)(r - (long long)i * N);
-        C[b * sC + (long long)i * ldc + (colperm ? colperm[j] : j)] = zero_of(T());
-    }
-}
-template <typename T>
-static cudaError_t zero_for_split(const GemmParams<T> &p, int batch, cudaStream_t s) {
-    if (p.beta != 0.0) return cudaSuccess;  // accumulate in place
-    const long long total = (long long)p.M * p.N * batch;
-    const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);
-    return launch_pdl(zero_block_kernel<T>, dim3(blocks), dim3(256), 0, s, p.C, p.ldc, p.sC, p.M, p.N, batch, p.colperm);
+    return !p.counter && p.epi == EPI_STORE;
 }
 
 template <typename T, bool VEC, int BIG>
@@ -65,8 +43,12 @@ static cudaError_t gemm_launch_cfg(const GemmPair<T> &pp, int batch0, int batch1
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !attr_set[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_kernel<T, VEC, BIG>,
+        cudaError_t e = cudaFuncSetAttribute(gemm_kernel<T, VEC, BIG, false>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if constexpr (!BIG)
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(gemm_kernel<T, VEC, BIG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
         if (e != cudaSuccess) return e;
         attr_set[dev] = true;
     }
@@ -77,7 +59,7 @@ static cudaError_t gemm_launch_cfg(const GemmPair<T> &pp, int batch0, int batch1
         cudaError_t e = cudaMemsetAsync(p0.counter, 0, sizeof(int), s);
         if (e != cudaSuccess) return e;
         ProfScope ps(sizeof(T) == 8 ? "gemm<double>" : "gemm<double2>", s, gemm_work(pp, batch0, batch1));
-        return launch_pdl(gemm_kernel<T, VEC, BIG>, dim3(grid, 1, 1), dim3(Cf::WGM * Cf::WGN * 32), smem, s, pp);
+        return launch_pdl(gemm_kernel<T, VEC, BIG, false>, dim3(grid, 1, 1), dim3(Cf::WGM * Cf::WGN * 32), smem, s, pp);
     }
     int M = p0.M, N = p0.N;
     if (batch1 > 0) {
@@ -86,8 +68,8 @@ static cudaError_t gemm_launch_cfg(const GemmPair<T> &pp, int batch0, int batch1
     }
     dim3 grid((N + Cf::BN - 1) / Cf::BN, (M + Cf::BM - 1) / Cf::BM, batch0 + batch1);
     GemmPair<T> q = pp;
-    // split-K for grids far below the 148 SMs x 3 resident CTAs with long k-ranges: each CTA
-    // adds its k-chunk into C, which is first set to beta * D (here: beta == 0, or D == C)
+    // split-K for grids far below the 148 SMs x 3 resident CTAs with long k-ranges: the S
+    // k-chunks of a tile run as one (1, 1, S) cluster and are summed in DSMEM in chunk order
     {
         const long long tiles = (long long)grid.x * grid.y * grid.z;
         int S = 1;
@@ -100,9 +82,6 @@ static cudaError_t gemm_launch_cfg(const GemmPair<T> &pp, int batch0, int batch1
         }
         if (ok && p0.force_split && K >= 512) S = std::max(S, std::min(4, K / 256));
         if (S > 1) {
-            cudaError_t e = zero_for_split(pp.q[0], batch0, s);
-            if (e == cudaSuccess && batch1 > 0) e = zero_for_split(pp.q[1], batch1, s);
-            if (e != cudaSuccess) return e;
             grid.z *= S;
             q.q[0].ksplit = q.q[1].ksplit = S;
         } else {
@@ -119,7 +98,10 @@ static cudaError_t gemm_launch_cfg(const GemmPair<T> &pp, int batch0, int batch1
     const bool early = policy == 2 || (policy == 1 && ctas <= 148LL * (BIG ? 1 : 3));
     q.q[0].early_trigger = q.q[1].early_trigger = early ? 1 : 0;
     ProfScope ps(sizeof(T) == 8 ? "gemm<double>" : "gemm<double2>", s, gemm_work(pp, batch0, batch1));
-    return launch_pdl(gemm_kernel<T, VEC, BIG>, grid, dim3(Cf::WGM * Cf::WGN * 32), smem, s, q);
+    if (!BIG && q.q[0].ksplit > 1)
+        return launch_pdl_cluster_z(gemm_kernel<T, VEC, BIG, !BIG>, grid, dim3(Cf::WGM * Cf::WGN * 32), smem, s,
+                                    q.q[0].ksplit, q);
+    return launch_pdl(gemm_kernel<T, VEC, BIG, false>, grid, dim3(Cf::WGM * Cf::WGN * 32), smem, s, q);
 }
 
 template <typename T, bool VEC>
