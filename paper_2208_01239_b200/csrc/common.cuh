@@ -19,6 +19,13 @@ inline void count_launch(unsigned long long k = 1) { __atomic_fetch_add(&launch_
 bool prof_enabled();
 // work: algorithmic flops of the launch (FP64; complex multiply-add = 8 real flops)
 void prof_record(const char *name, cudaStream_t s, bool begin, double work);
+// role tag for the GEMM launches below it (profiler names; string literals, compared by address)
+extern thread_local const char *g_gemm_tag;
+struct GemmTag {
+    const char *prev;
+    explicit GemmTag(const char *t) : prev(g_gemm_tag) { g_gemm_tag = t; }
+    ~GemmTag() { g_gemm_tag = prev; }
+};
 struct ProfScope {
     const char *name;
     cudaStream_t s;

@@ -34,6 +34,7 @@ struct ProfOpen {
 static std::vector<ProfOpen> g_prof_open;
 
 bool prof_enabled() { return g_prof_on; }
+thread_local const char *g_gemm_tag = nullptr;
 void prof_record(const char *name, cudaStream_t s, bool begin, double work) {
     std::lock_guard<std::mutex> g(g_prof_mu);
     cudaEvent_t e;
@@ -145,7 +146,7 @@ static FrobWs carve_frob(void *ws, int n) {
     w.W3 = c.take<double>((size_t)n * ld);
     w.W4 = c.take<double>((size_t)n * ld);
     w.W5 = c.take<double>((size_t)n * ld);
-    const bool small = n <= LU2_MAX_N;
+    const bool small = n <= lu2_max_n();
     w.W6 = small ? c.take<double>((size_t)n * ld) : nullptr;
     w.W7 = small ? c.take<double>((size_t)n * ld) : nullptr;
     w.diag = c.take<double>((size_t)n);
@@ -176,7 +177,7 @@ static ZluWs carve_zlu(void *ws, int n) {
     w.W = c.take<double2>((size_t)n * ld);
     w.U = c.take<double2>((size_t)n * ld);
     w.L = c.take<double2>((size_t)n * ld);
-    const bool small = n <= LU2_MAX_N;
+    const bool small = n <= lu2_max_n();
     w.W2 = small ? c.take<double2>((size_t)n * ld) : nullptr;
     w.diag = c.take<double2>((size_t)n);
     w.work = c.take<double2>(getrf_work_elems<double2>(n));
@@ -219,7 +220,7 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
     int *perm = w.perm_x;
     double *Xlu = w.W1;
     // n <= LU2_MAX_N: latency-oriented LU (lu2.cu), factors come out split (U, L)
-    const bool small = n <= LU2_MAX_N;
+    const bool small = n <= lu2_max_n();
     double *Uf = w.W2, *Lf = w.W3;
     if (small) FROB_CUDA(lu2_factor<double>(n, w.W1, w.W4, ld, w.W2, w.W3, ld, perm, w.iw, w.diag,
                                             &w.stats[use == 1 ? 0 : 1], s));
@@ -348,7 +349,7 @@ static frob_status zinv_lu_impl(int n, const double *Z, long long ldz, double *X
     copy2d_kernel<double2><<<ew_blocks((long long)n * n), 256, 0, s>>>(
         reinterpret_cast<const double2 *>(Z), ldz, w.W, ld, n, w.flags);
     FROB_CUDA(cudaGetLastError());
-    if (n <= LU2_MAX_N) {
+    if (n <= lu2_max_n()) {
         FROB_CUDA(lu2_factor<double2>(n, w.W, w.W2, ld, w.U, w.L, ld, w.perm, w.iw, w.diag, w.stats, s));
         FROB_CUDA(inv_from_ul<double2>(n, w.U, w.L, ld, w.W, reinterpret_cast<double2 *>(X), ldx, w.perm, w.flags + 2, s));
     } else {
@@ -383,7 +384,7 @@ static DinvWs carve_dinv(void *ws, int n) {
     w.W = c.take<double>((size_t)n * ld);
     w.U = c.take<double>((size_t)n * ld);
     w.L = c.take<double>((size_t)n * ld);
-    const bool small = n <= LU2_MAX_N;
+    const bool small = n <= lu2_max_n();
     w.W2 = small ? c.take<double>((size_t)n * ld) : nullptr;
     w.diag = c.take<double>((size_t)n);
     w.work = c.take<double>(getrf_work_elems<double>(n));
@@ -739,7 +740,7 @@ frob_status frob_dinv(int n, const double *A, long long lda, double *Ainv, long 
     count_launch();
     copy2d_kernel<double><<<ew_blocks((long long)n * n), 256, 0, s>>>(A, lda, w.W, ld, n, nullptr);
     FROB_CUDA(cudaGetLastError());
-    if (n <= LU2_MAX_N) {
+    if (n <= lu2_max_n()) {
         FROB_CUDA(lu2_factor<double>(n, w.W, w.W2, ld, w.U, w.L, ld, w.perm, w.iw, w.diag, w.stats, s));
         FROB_CUDA(inv_from_ul<double>(n, w.U, w.L, ld, w.W, Ainv, ldainv, w.perm, w.flags, s));
     } else {

@@ -9,6 +9,7 @@
 #include <mutex>
 #include <algorithm>
 #include "lu.cuh"
+#include "tma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -58,7 +59,7 @@ static cudaError_t gemm_launch_cfg(const GemmPair<T> &pp, int batch0, int batch1
         const int grid = min(D * D, 148 * 3);
         cudaError_t e = cudaMemsetAsync(p0.counter, 0, sizeof(int), s);
         if (e != cudaSuccess) return e;
-        ProfScope ps(sizeof(T) == 8 ? "gemm<double>" : "gemm<double2>", s, gemm_work(pp, batch0, batch1));
+        ProfScope ps(g_gemm_tag ? g_gemm_tag : sizeof(T) == 8 ? "gemm<double>" : "gemm<double2>", s, gemm_work(pp, batch0, batch1));
         return launch_pdl(gemm_kernel<T, VEC, BIG, false>, dim3(grid, 1, 1), dim3(Cf::WGM * Cf::WGN * 32), smem, s, pp);
     }
     int M = p0.M, N = p0.N;
@@ -97,7 +98,7 @@ static cudaError_t gemm_launch_cfg(const GemmPair<T> &pp, int batch0, int batch1
     }();
     const bool early = policy == 2 || (policy == 1 && ctas <= 148LL * (BIG ? 1 : 3));
     q.q[0].early_trigger = q.q[1].early_trigger = early ? 1 : 0;
-    ProfScope ps(sizeof(T) == 8 ? "gemm<double>" : "gemm<double2>", s, gemm_work(pp, batch0, batch1));
+    ProfScope ps(g_gemm_tag ? g_gemm_tag : sizeof(T) == 8 ? "gemm<double>" : "gemm<double2>", s, gemm_work(pp, batch0, batch1));
     if (!BIG && q.q[0].ksplit > 1)
         return launch_pdl_cluster_z(gemm_kernel<T, VEC, BIG, !BIG>, grid, dim3(Cf::WGM * Cf::WGN * 32), smem, s,
                                     q.q[0].ksplit, q);
@@ -995,6 +996,7 @@ cudaError_t inv_from_lu(int n, T *lu, long long ld, T *U, T *L, T *out, long lon
 template <typename T>
 cudaError_t tri_inverses(int n, T *U, T *L, long long ld, T *tmp, cudaStream_t s) {
     cudaError_t e;
+    GemmTag tag("gemm:tri_inv");
     const bool lower = L != nullptr;  // L == nullptr: invert the upper triangle U only
     if ((e = launch_pdl(tri_leaf_kernel<T>, dim3((n + TRI_LEAF - 1) / TRI_LEAF, lower ? 2 : 1), dim3(TRI_LEAF), 0, s,
                         U, lower ? L : U, ld, n, 0)) != cudaSuccess)
@@ -1036,6 +1038,7 @@ cudaError_t inv_from_ul(int n, T *U, T *L, long long ld, T *tmp, T *out, long lo
     const int mode = prod_mode >= 0 ? prod_mode : (n <= 1024 ? 1 : 0);
     p.counter = (n <= 2048 && mode == 0) ? counter : nullptr;
     if (mode == 1) p.force_split = 1;
+    GemmTag tag("gemm:product");
     return gemm_launch<T>(p, 1, s);
 }
 template cudaError_t inv_from_ul<double>(int, double *, double *, long long, double *, double *, long long, const int *, int *, cudaStream_t);
@@ -1127,9 +1130,53 @@ static cudaError_t panel_step(int n, T *A, long long lda, int cb, int ce, int k0
         T *a12 = A + (long long)k0 * lda + k0 + w;
         T *a22 = A + (long long)(k0 + w) * lda + k0 + w;
         auto p = gemm_params<T>(m - w, rest, w, -1.0, a21, lda, a12, lda, 1.0, a22, lda, a22, lda);
+        GemmTag tag("gemm:lu_inner");
         if ((e = gemm_launch<T>(p, 1, s)) != cudaSuccess) return e;
     }
     return cudaSuccess;
+}
+
+// The same step with lu2's 32-column panel kernels (one CTA, or a cluster of <= 8 CTAs with a
+// DSMEM pivot exchange) for m <= LU2_PANEL_MAX_M: panel in place, then row movement + TRSM on the
+// other columns of [cb, ce) and the trailing GEMM inside [cb, ce).  Returns the width taken.
+template <typename T>
+static cudaError_t panel_step2(int n, T *A, long long lda, const CUtensorMap &tm, int cb, int ce, int k0, int *perm,
+                               int *list, T *diag, cudaStream_t s, int &w) {
+    constexpr int PW2 = Panel2W<T>::PW;
+    cudaError_t e;
+    w = min(PW2, ce - k0);
+    const int m = n - k0;
+    if ((e = lu2_panel_inplace<T>(tm, A, lda, n, k0, w, list, diag, s)) != cudaSuccess) return e;
+    const int ncols = ce - cb - w;
+    if (ncols > 0) {
+        ProfScope ps(sizeof(T) == 8 ? "lu_swap_trsm<double>" : "lu_swap_trsm<double2>", s);
+        if ((e = launch_pdl(lu_swap_trsm_kernel<T, PW2>, dim3((ncols + SWP_COLS - 1) / SWP_COLS), dim3(SWP_COLS), 0, s,
+                            A, lda, cb, ce, k0, w, (const int *)list, perm)) != cudaSuccess)
+            return e;
+    } else if (perm) {
+        // no other columns: the permutation still has to follow the panel's moves
+        if ((e = launch_pdl(lu_swap_trsm_kernel<T, PW2>, dim3(1), dim3(SWP_COLS), 0, s, A, lda, cb, ce, k0, w,
+                            (const int *)list, perm)) != cudaSuccess)
+            return e;
+    }
+    const int rest = ce - k0 - w;
+    if (rest > 0 && m - w > 0) {
+        T *a21 = A + (long long)(k0 + w) * lda + k0;
+        T *a12 = A + (long long)k0 * lda + k0 + w;
+        T *a22 = A + (long long)(k0 + w) * lda + k0 + w;
+        auto p = gemm_params<T>(m - w, rest, w, -1.0, a21, lda, a12, lda, 1.0, a22, lda, a22, lda);
+        GemmTag tag("gemm:lu_inner");
+        if ((e = gemm_launch<T>(p, 1, s)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+// new panels unless env FROB_GETRF_PANEL=old (A/B measurement aid)
+static bool getrf_new_panels() {
+    static bool v = [] {
+        const char *e = getenv("FROB_GETRF_PANEL");
+        return !(e && e[0] == 'o');
+    }();
+    return v;
 }
 
 // outer update of columns [c0, c1) by block (K0, W): U12 = Linv * A12 -> Tb, A22 -= L21 * Tb, A12 <- Tb
@@ -1139,6 +1186,7 @@ static cudaError_t outer_update(int n, T *A, long long lda, int K0, int W, int c
     cudaError_t e;
     const int nc = c1 - c0;
     if (nc <= 0) return cudaSuccess;
+    GemmTag tag("gemm:lu_outer");
     auto p = gemm_params<T>(W, nc, W, 1.0, Linv, LU_NB, A + (long long)K0 * lda + c0, lda, 0.0, nullptr, ldT,
                             Tb + c0, ldT);
     p.triA = TRI_LOWER;
@@ -1157,14 +1205,29 @@ static cudaError_t outer_update(int n, T *A, long long lda, int K0, int W, int c
 template <typename T>
 cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuStats *stats, T *work,
                   cudaStream_t s) {
-    constexpr int PW = PanelW<T>::PW;
+    constexpr int PW = PanelW<T>::PW, PW2 = Panel2W<T>::PW;
     cudaError_t e = launch_pdl(iota_kernel, dim3((n + 255) / 256), dim3(256), 0, s, perm, n);
     if (e != cudaSuccess) return e;
+    // lu2's panels stage rows with TMA and 16-byte vector stores: 16-byte aligned rows only
+    const bool np = getrf_new_panels() && ((lda * (long long)sizeof(T)) % 16 == 0) &&
+                    ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+    CUtensorMap tm;
+    if (np) {
+        const int E = (int)(sizeof(T) / 8);
+        if ((e = tma_map_rows128(&tm, A, n, (long long)n * E, lda * E, 256)) != cudaSuccess) return e;
+    }
+    // one panel step at k0 inside [cb, ce); its move list goes to the next slot of mv
+    int slot = 0;
+    auto step = [&](int cb, int ce, int k0, int &w) -> cudaError_t {
+        int *list = mv + (long long)slot * MV_INTS;
+        ++slot;
+        if (np && n - k0 <= LU2_PANEL_MAX_M) return panel_step2<T>(n, A, lda, tm, cb, ce, k0, perm, list, diag, s, w);
+        w = min(PW, ce - k0);
+        return panel_step<T, PW>(n, A, lda, cb, ce, k0, perm, list, diag, s);
+    };
     if (n < LU_TWO_LEVEL_MIN || !work) {
-        for (int k0 = 0; k0 < n; k0 += PW)
-            if ((e = panel_step<T, PW>(n, A, lda, 0, n, k0, perm, mv + (long long)(k0 / PW) * MV_INTS, diag, s)) !=
-                cudaSuccess)
-                return e;
+        for (int k0 = 0, w = 0; k0 < n; k0 += w)
+            if ((e = step(0, n, k0, w)) != cudaSuccess) return e;
     } else {
         AuxCtx &ax = aux_ctx(e);
         if (e != cudaSuccess) return e;
@@ -1177,13 +1240,12 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
         int t = 0;
         for (int K0 = 0; K0 < n; K0 += LU_NB, ++t) {
             const int W = min(LU_NB, n - K0);
-            for (int k0 = K0; k0 < K0 + W; k0 += PW)
-                if ((e = panel_step<T, PW>(n, A, lda, K0, K0 + W, k0, perm, mv + (long long)(k0 / PW) * MV_INTS,
-                                           diag, s)) != cudaSuccess)
-                    return e;
+            const int slot0 = slot;
+            for (int k0 = K0, w = 0; k0 < K0 + W; k0 += w)
+                if ((e = step(K0, K0 + W, k0, w)) != cudaSuccess) return e;
             const int cn0 = K0 + W, cn1 = min(n, K0 + 2 * W);
-            const int nl = (W + PW - 1) / PW;
-            const int *lists = mv + (long long)(K0 / PW) * MV_INTS;
+            const int nl = slot - slot0;
+            const int *lists = mv + (long long)slot0 * MV_INTS;
             T *Li = Linv[t & 1];
             if (cn0 < n) {
                 // L11^{-1} (W x W unit lower) by the triangular recursion
@@ -1193,6 +1255,7 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
                 if ((e = launch_pdl(tri_leaf_kernel<T>, dim3((W + TRI_LEAF - 1) / TRI_LEAF, 1), dim3(TRI_LEAF), 0, s,
                                     Li, Li, (long long)LU_NB, W, 1)) != cudaSuccess)
                     return e;
+                GemmTag tag("gemm:lu_Linv");
                 for (int sz = TRI_LEAF; sz < W; sz *= 2) {
                     const int full = W / (2 * sz);
                     if (full > 0 && (e = tri_level<T>(Li, Li, tmp, LU_NB, sz, 0, sz, full, s, false)) != cudaSuccess)
@@ -1209,7 +1272,7 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
             {
                 const int ncol = K0 + (n - cn1);
                 if (ncol > 0) {
-                    if ((e = launch_pdl(lu_swap_multi_kernel<T, PW>, dim3((ncol + SWM_COLS - 1) / SWM_COLS),
+                    if ((e = launch_pdl(lu_swap_multi_kernel<T, PW2>, dim3((ncol + SWM_COLS - 1) / SWM_COLS),
                                         dim3(SWM_COLS), 0, ax.st, A, lda, 0, K0, cn1, n, lists, nl)) != cudaSuccess)
                         return e;
                 }
@@ -1220,7 +1283,7 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
             // ---- caller's stream: look-ahead block [cn0, cn1)
             if (cn0 < n) {
                 if (t > 0 && (e = cudaStreamWaitEvent(s, evR[(t - 1) & 1], 0)) != cudaSuccess) return e;
-                if ((e = launch_pdl(lu_swap_multi_kernel<T, PW>, dim3((cn1 - cn0 + SWM_COLS - 1) / SWM_COLS),
+                if ((e = launch_pdl(lu_swap_multi_kernel<T, PW2>, dim3((cn1 - cn0 + SWM_COLS - 1) / SWM_COLS),
                                     dim3(SWM_COLS), 0, s, A, lda, cn0, cn1, 0, 0, lists, nl)) != cudaSuccess)
                     return e;
                 if ((e = outer_update<T>(n, A, lda, K0, W, cn0, cn1, Li, Tb[t & 1], ldT, s)) != cudaSuccess) return e;

@@ -10,6 +10,7 @@
 // written straight to its final position and the row movement list is emitted for the
 // rest of the matrix.
 #pragma once
+#include <cuda.h>
 #include "common.cuh"
 #include "gemm.cuh"
 
@@ -51,8 +52,20 @@ cudaError_t inv_from_lu(int n, T *lu, long long ld, T *U, T *L, T *out, long lon
 // Latency-oriented LU for n <= LU2_MAX_N (lu2.cu): B0 holds A on entry and is destroyed,
 // B1 is scratch (n x ld); the factors come out split: U (upper, zeros below), L (unit lower,
 // zeros above), ldo; perm[i] = original row at position i; iw = lu2_int_elems(n) ints.
-constexpr int LU2_MAX_N = 1024;
+constexpr int LU2_MAX_N = 4096;  // single CTA up to 1024 rows, then a cluster of <= 8 CTAs
 size_t lu2_int_elems(int n);
+// orders that take lu2 (LU2_MAX_N; env FROB_LU2_MAX lowers it: A/B measurement aid)
+int lu2_max_n();
+// lu2's panel width: two 128-byte row halves (32 real / 16 complex columns would spill: 8 complex)
+template <typename T> struct Panel2W { static constexpr int PW = 32, PH = 16; };
+template <> struct Panel2W<double2> { static constexpr int PW = 8, PH = 8; };
+// lu2's panel kernels used IN PLACE by the blocked getrf: rows [k0, n) x columns [k0, k0 + w) of A
+// (lda; tm = tma_map_rows128 of A with 256-row boxes) factored, rows written to their final
+// positions, the move list (MV_INTS layout) to mv, pivots to diag[k0..]; n - k0 <= LU2_PANEL_MAX_M
+constexpr int LU2_PANEL_MAX_M = 4096;
+template <typename T>
+cudaError_t lu2_panel_inplace(const CUtensorMap &tm, T *A, long long lda, int n, int k0, int w, int *mv, T *diag,
+                              cudaStream_t s);
 template <typename T>
 cudaError_t lu2_factor(int n, T *B0, T *B1, long long ld, T *U, T *L, long long ldo, int *perm, int *iw, T *diag,
                        LuStats *stats, cudaStream_t s);

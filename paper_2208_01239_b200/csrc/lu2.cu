@@ -16,6 +16,7 @@
 // (upper, zeros below) and L (unit lower, zeros above) in final row order, reading each L
 // column block through its snapshot -- the split form inv_from_ul consumes directly.
 #include <climits>
+#include <cstdlib>
 #include <cstdio>
 #include <utility>
 #include <algorithm>
@@ -29,8 +30,6 @@ constexpr int P2_WARPS = P2_T / 32;
 constexpr int P2_STG = 18;  // staging row stride in doubles (16 + 2: 16-byte aligned, conflict free)
 
 // panel width of one step: two 128-byte row halves (32 real / 16 complex columns)
-template <typename T> struct Panel2W { static constexpr int PW = 32, PH = 16; };
-template <> struct Panel2W<double2> { static constexpr int PW = 8, PH = 8; };  // one half: the two-half complex variant spills
 
 // mv2 layout (ints): [0] = number of moves, [1, 1 + MV2_MAX) dst, [1 + MV2_MAX, 1 + 2 MV2_MAX) src
 constexpr int MV2_MAX = 64;
@@ -94,7 +93,6 @@ template <typename T, int PH, int R, bool TWO>
 __global__ void __launch_bounds__(P2_T, 1)
 lu_panel2_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, long long ld, int n, int k0, int w,
                  int *__restrict__ mv2, T *__restrict__ diag) {
-    pdl_trigger();
     extern __shared__ __align__(1024) unsigned char stgb[];  // R * P2_T rows x 128 B, 128B-swizzled (TMA)
     __shared__ __align__(8) unsigned long long tbar;
     if (threadIdx.x == 0) {
@@ -102,6 +100,7 @@ lu_panel2_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, lo
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     pdl_wait();
+    pdl_trigger();  // after the wait: the BULK update launched behind this panel relies on it
     P2T(0);
     constexpr int PW = 2 * PH;                     // panel width in elements
     __shared__ unsigned long long ck[2][P2_WARPS];
@@ -424,6 +423,358 @@ lu_panel2_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, lo
 }
 
 // ---------------------------------------------------------------------------------------
+// Cluster variant of the panel for m > P2_T rows: CS = ceil(m / P2_T) CTAs (a thread-block
+// cluster), CTA r owns relative rows [r P2_T, (r+1) P2_T), one row per thread, and TMA-loads
+// only those.  Per column, after the CTA argmax, warp 0 pushes the CTA candidate (key, row
+// index, its row of the current half: 144 B) into slot r of EVERY CTA of the cluster with
+// st.async + mbarrier complete_tx; the deferred rank-1 update of the previous pivot overlaps
+// the exchange; every CTA then takes the same cluster argmax (same key order as the single-CTA
+// kernel: identical pivots) and reads the pivot row from its own shared memory.  At the half
+// transition the owners of half 0's pivot rows push their L11 and X rows the same way.  Rows
+// never move inside the panel; each CTA writes its rows to their final positions at the end;
+// rank 0 emits the move list and the pivot values.  (A column costs one DSMEM round trip,
+// ~520 cycles, more than the single-CTA kernel; in exchange each SM holds 1/CS of the panel.)
+constexpr int P2C_MAX = 8;  // portable cluster size: m <= 4096
+constexpr int P2C_PUSH_WARPS = 3;
+struct __align__(16) XSlot2 {
+    unsigned long long key;
+    int idx, pad;
+    double row[16];  // the candidate's 128-byte row half
+};
+FROB_DEV void st_async_16b(unsigned raddr, const uint4 v, unsigned rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                     raddr),
+                 "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rbar)
+                 : "memory");
+}
+
+template <typename T, int PH, bool TWO>
+__global__ void __launch_bounds__(P2_T, 1)
+lu_panel2c_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, long long ld, int n, int k0, int w,
+                  int *__restrict__ mv2, T *__restrict__ diag) {
+    extern __shared__ __align__(1024) unsigned char stgb[];  // P2_T local rows x 128 B, 128B-swizzled (TMA)
+    __shared__ __align__(8) unsigned long long tbar, hbar, xbar[2];
+    __shared__ __align__(16) XSlot2 xs[2][P2C_MAX];
+    __shared__ __align__(16) T L11s[PH][PH];  // half transition: pushed rows (128 B each)
+    __shared__ __align__(16) T U12s[PH][PH];
+    __shared__ __align__(16) T obox[2][PH][PH];  // this CTA's pivot rows of half 0: L11 | X
+    __shared__ unsigned long long ck[2][P2_WARPS];
+    __shared__ int ci[2][P2_WARPS];
+    __shared__ __align__(16) T wrow[2][P2_WARPS][PH];
+    constexpr int PW = 2 * PH;
+    __shared__ int pivrow[PW];
+    __shared__ int vac[PW];
+    __shared__ unsigned evm_s;
+    __shared__ int sdst[P2_T];
+    static_assert(PH * sizeof(T) == 128, "row halves are 128 bytes");
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    unsigned rank, CSu;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(CSu));
+    const int CS = (int)CSu;
+    const int rbeg = (int)rank * P2_T;
+    const int m = n - k0;
+    const int E = (int)(sizeof(T) / 8);
+    const bool two = TWO && w > PH;
+    constexpr unsigned XB = (unsigned)sizeof(XSlot2);
+    if (tid == 0) {
+        mbar_init(smem_u32(&tbar), 1u);
+        mbar_init(smem_u32(&hbar), 1u);
+        mbar_init(smem_u32(&xbar[0]), 1u);
+        mbar_init(smem_u32(&xbar[1]), 1u);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cluster_sync_all();  // every CTA's barriers exist before any remote complete_tx
+    if (tid == 0) {
+        mbar_arrive_expect_tx(smem_u32(&xbar[0]), (unsigned)CS * XB);
+        if (w > 1) mbar_arrive_expect_tx(smem_u32(&xbar[1]), (unsigned)CS * XB);
+        if (two) mbar_arrive_expect_tx(smem_u32(&hbar), (unsigned)(2 * PH * 128));
+    }
+    pdl_wait();
+    pdl_trigger();  // after the wait (see lu2_factor)
+#define P2CT(i) do { if (rank == 0) P2T(i); } while (0)
+#define P2CTJ(j, i) do { if ((j) == 5) P2CT(i); } while (0)
+    P2CT(0);
+    const int mr = min(P2_T, m - rbeg);  // rows of this CTA (>= 1)
+    const int nbox = (mr + 255) / 256;
+    auto tma_half = [&](int h) {
+        mbar_arrive_expect_tx(smem_u32(&tbar), (unsigned)(nbox * 256 * 128));
+        for (int b = 0; b < nbox; ++b)
+            tma_load_2d(smem_u32(stgb + b * 256 * 128), &tmap, (k0 + h * PH) * E, k0 + rbeg + 256 * b,
+                        smem_u32(&tbar));
+    };
+    auto row_from_stg = [&](int r, T (&dst)[PH]) {
+        double t[16];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const double2 v = *reinterpret_cast<const double2 *>(stgb + swz128(r, c));
+            t[2 * c] = v.x;
+            t[2 * c + 1] = v.y;
+        }
+#pragma unroll
+        for (int c = 0; c < PH; ++c) {
+            if constexpr (sizeof(T) == 8) dst[c] = t[c];
+            else dst[c] = make_double2(t[2 * c], t[2 * c + 1]);
+        }
+    };
+    auto row_to_stg = [&](int r, const T (&src)[PH]) {
+        const double *rd = reinterpret_cast<const double *>(src);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<double2 *>(stgb + swz128(r, c)) = make_double2(rd[2 * c], rd[2 * c + 1]);
+    };
+
+    if (tid == 0) tma_half(0);
+    __syncthreads();
+    mbar_wait_cta(smem_u32(&tbar), 0u);
+    const int g = rbeg + tid;  // relative row of this thread
+    T a[PH];
+    int pst = -1;
+    bool live = g < m;
+    row_from_stg(tid, a);
+    __syncthreads();  // the staging buffer is free
+    if (two && tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tma_half(1);
+    }
+
+    auto publish_first = [&]() {
+        const unsigned long long bk = live ? pkey_bits(a[0]) : 0ull;
+        const ArgMaxK wa = warp_argmax_key(bk, live ? g : INT_MAX);
+        if (lane == 0) { ck[0][warp] = wa.k; ci[0][warp] = wa.i; }
+        if (live && g == wa.i && wa.k != 0ull) st_row_smem<T, PH>(wrow[0][warp], a);
+    };
+
+    T u[PH];
+    T lp = zero_of(T());
+    bool pact = false;
+    auto run_half = [&](const int JO, const int wh) {
+#pragma unroll
+        for (int c = 0; c < PH; ++c) u[c] = zero_of(T());
+        lp = zero_of(T());
+        pact = false;
+        auto column = [&](auto Jc) {
+            constexpr int J = decltype(Jc)::value;
+            constexpr int s = J & 1;
+            const int t = JO + J;  // exchange number (JO even: buffer s = t & 1)
+            __syncthreads();
+            P2CTJ(J, 40);
+            // (a) CTA argmax, push of the CTA candidate to every CTA of the cluster (warps 0-2
+            // each take the argmax and a third of the CS x 9 16-byte chunks)
+            if (warp < P2C_PUSH_WARPS) {
+                const ArgMaxK ca = warp_argmax_key(lane < P2_WARPS ? ck[s][lane] : 0ull,
+                                                   lane < P2_WARPS ? ci[s][lane] : INT_MAX);
+                const int cw = (ca.i == INT_MAX) ? 0 : ((ca.i - rbeg) >> 5);
+                const unsigned slot = smem_u32(&xs[s][rank]);
+                const unsigned bar = smem_u32(&xbar[s]);
+                for (int task = lane + 32 * warp; task < CS * 9; task += 32 * P2C_PUSH_WARPS) {
+                    const int r = task / 9, c = task - r * 9;
+                    uint4 v;
+                    if (c == 0) v = make_uint4((unsigned)ca.k, (unsigned)(ca.k >> 32), (unsigned)ca.i, 0u);
+                    else v = *reinterpret_cast<const uint4 *>(reinterpret_cast<const unsigned char *>(wrow[s][cw]) +
+                                                              (c - 1) * 16);
+                    st_async_16b(mapa_u32(slot + c * 16, (unsigned)r), v, mapa_u32(bar, (unsigned)r));
+                }
+            }
+            P2CTJ(J, 41);
+            // (b) deferred update of pivot J-1 (columns >= J+1), overlapping the exchange
+            if (pact) {
+#pragma unroll
+                for (int c = J + 1; c < PH; ++c) a[c] = msub(a[c], lp, u[c]);
+            }
+            // (c) cluster argmax, pivot row + reciprocal
+            P2CTJ(J, 42);
+            mbar_wait_parity(smem_u32(&xbar[s]), (unsigned)((t >> 1) & 1));
+            P2CTJ(J, 43);
+            const ArgMaxK ga = warp_argmax_key(lane < CS ? xs[s][lane].key : 0ull, lane < CS ? xs[s][lane].idx : INT_MAX);
+            const int gi = ga.i;
+            const int owner = min(gi / P2_T, CS - 1);
+            ld_row_smem<T, PH>(u, reinterpret_cast<const T *>(xs[s][owner].row));
+            if (tid == 0 && t + 2 < w) mbar_arrive_expect_tx(smem_u32(&xbar[s]), (unsigned)CS * XB);
+            const T rc = rcp_spec(u[J]);
+            if (tid == 0) {
+                pivrow[JO + J] = gi;
+                if (rank == 0) diag[k0 + JO + J] = u[J];
+            }
+            P2CTJ(J, 44);
+            // (d) multiplier, eager update of column J+1
+            const bool isp = live && g == gi;
+            const bool act = live && !isp;
+            if (isp) { live = false; pst = JO + J; }
+            const T l = act ? mul(a[J], rc) : zero_of(T());
+            pact = act;
+            if (act) {
+                a[J] = l;
+                if constexpr (J + 1 < PH) a[J + 1] = msub(a[J + 1], l, u[J + 1]);
+            }
+            lp = l;
+            P2CTJ(J, 45);
+            if constexpr (J + 1 < PH) {
+                if (J + 1 < wh) {
+                    // (e) candidate of column J+1, warp argmax; (f) the warp winner publishes
+                    const unsigned long long bk = live ? pkey_bits(a[J + 1]) : 0ull;
+                    const ArgMaxK wa = warp_argmax_key(bk, live ? g : INT_MAX);
+                    if (lane == 0) { ck[s ^ 1][warp] = wa.k; ci[s ^ 1][warp] = wa.i; }
+                    if (live && g == wa.i && wa.k != 0ull) {
+                        T *dst = wrow[s ^ 1][warp];
+                        auto rowval = [&](const int c) { return (c >= J + 2) ? msub(a[c], l, u[c]) : a[c]; };
+                        if constexpr (sizeof(T) == 8) {
+#pragma unroll
+                            for (int c = 0; c < PH; c += 2)
+                                *reinterpret_cast<double2 *>(dst + c) = make_double2(rowval(c), rowval(c + 1));
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < PH; ++c) dst[c] = rowval(c);
+                        }
+                    }
+                }
+            }
+            P2CT(2 + J + (JO ? 16 : 0) * 0);
+        };
+        static_for<PH>([&](auto Jc) {
+            constexpr int Jv = decltype(Jc)::value;
+            if (Jv < wh) column(Jc);
+        });
+    };
+
+    P2CT(1);
+    publish_first();
+    run_half(0, min(w, PH));
+    __syncthreads();
+    P2CT(19);
+
+    if constexpr (TWO) if (two) {
+        // ---- half 1: gather half 0's pivot rows (L11 | X) from their owners, U12 = L11^{-1} X,
+        // rank-PH update of this CTA's rows, swap
+        mbar_wait_cta(smem_u32(&tbar), 1u);
+        if (pst >= 0) {
+            T x[PH];
+            row_from_stg(tid, x);
+            st_row_smem<T, PH>(obox[0][pst], a);
+            st_row_smem<T, PH>(obox[1][pst], x);
+        }
+        __syncthreads();
+        {
+            const unsigned hb = smem_u32(&hbar);
+            for (int task = tid; task < PH * CS * 16; task += P2_T) {
+                const int j = task / (CS * 16), rem = task - j * (CS * 16), r = rem >> 4, c = rem & 15;
+                if (pivrow[j] / P2_T != (int)rank) continue;
+                const int part = c >> 3, off = (c & 7) * 16;
+                const uint4 v = *reinterpret_cast<const uint4 *>(reinterpret_cast<const unsigned char *>(obox[part][j]) + off);
+                const unsigned dst = smem_u32(part ? &U12s[j][0] : &L11s[j][0]) + off;
+                st_async_16b(mapa_u32(dst, (unsigned)r), v, mapa_u32(hb, (unsigned)r));
+            }
+        }
+        mbar_wait_parity(smem_u32(&hbar), 0u);
+        if (tid < PH) {
+            T x[PH];
+#pragma unroll
+            for (int j = 0; j < PH; ++j) x[j] = U12s[j][tid];
+#pragma unroll
+            for (int q = 0; q < PH; ++q)
+#pragma unroll
+                for (int j = q + 1; j < PH; ++j) x[j] = msub(x[j], L11s[j][q], x[q]);
+#pragma unroll
+            for (int j = 0; j < PH; ++j) U12s[j][tid] = x[j];
+        }
+        __syncthreads();
+        if (g < m) {
+            T x[PH];
+            row_from_stg(tid, x);
+            if (pst >= 0) {
+#pragma unroll
+                for (int c = 0; c < PH; ++c) x[c] = U12s[pst][c];
+            } else {
+#pragma unroll
+                for (int j = 0; j < PH; ++j) {
+                    const T lj = a[j];
+#pragma unroll
+                    for (int c = 0; c < PH; ++c) x[c] = msub(x[c], lj, U12s[j][c]);
+                }
+            }
+            row_to_stg(tid, a);  // half 0's factored row waits in the staging buffer
+#pragma unroll
+            for (int c = 0; c < PH; ++c) a[c] = x[c];
+        }
+        __syncthreads();
+        P2CT(18);
+        publish_first();
+        run_half(PH, w - PH);
+        __syncthreads();
+    }
+    P2CT(20);
+
+    // ---- final positions (pivrow is the same in every CTA): pivot j -> j; evicted top rows
+    // (< w, not pivots) fill the rows vacated by pivots from below (>= w), in pivot order
+    if (warp == 0) {
+        const int pj = lane < w ? pivrow[lane] : -1;
+        bool rp = false;
+        if (lane < w)
+            for (int q = 0; q < w; ++q) rp |= (pivrow[q] == lane);
+        const unsigned pivmask = __ballot_sync(0xffffffffu, rp);
+        const unsigned wmask = (w >= 32) ? 0xffffffffu : ((1u << w) - 1u);
+        const unsigned evmask = wmask & ~pivmask;
+        const bool isv = lane < w && pj >= w;
+        const unsigned vb = __ballot_sync(0xffffffffu, isv);
+        if (isv) vac[__popc(vb & ((1u << lane) - 1u))] = pj;
+        if (lane == 0) evm_s = evmask;
+        __syncwarp();
+        if (rank == 0) {
+            const bool moved = lane < w && pj != lane;
+            const unsigned mb = __ballot_sync(0xffffffffu, moved);
+            const int nm = __popc(mb);
+            if (moved) {
+                const int q = __popc(mb & ((1u << lane) - 1u));
+                mv2[1 + q] = k0 + lane;
+                mv2[1 + MV2_MAX + q] = k0 + pj;
+            }
+            const bool ev = (evmask >> lane) & 1u;
+            if (ev) {
+                const int q = nm + __popc(evmask & ((1u << lane) - 1u));
+                mv2[1 + q] = k0 + vac[__popc(evmask & ((1u << lane) - 1u))];
+                mv2[1 + MV2_MAX + q] = k0 + lane;
+            }
+            if (lane == 0) mv2[0] = nm + __popc(evmask);
+        }
+    }
+    __syncthreads();
+    {
+        const unsigned evm = evm_s;
+        int dst = g;
+        if (pst >= 0) dst = pst;
+        else if (g < w) dst = vac[__popc(evm & ((1u << g) - 1u))];
+        sdst[tid] = (g < m) ? dst : -1;
+    }
+    __syncthreads();
+    // coalesced write-back of this CTA's rows, 8 threads per 128-byte row half
+    const long long ldd = ld * E;
+    double *P = reinterpret_cast<double *>(B) + (long long)k0 * ldd + (long long)k0 * E;
+    auto write_half = [&](int h) {
+        const int wd = (min(w, (h + 1) * PH) - h * PH) * E;
+#pragma unroll 4
+        for (int idx = tid; idx < mr * 8; idx += P2_T) {
+            const int r = idx >> 3, c = idx & 7;
+            if (2 * c >= wd) continue;
+            const double2 v = *reinterpret_cast<const double2 *>(stgb + swz128(r, c));
+            double *out = P + (long long)sdst[r] * ldd + h * PH * E + 2 * c;
+            if (2 * c + 1 < wd) *reinterpret_cast<double2 *>(out) = v;
+            else out[0] = v.x;
+        }
+    };
+    if constexpr (TWO) if (two) {
+        write_half(0);  // half 0's rows sit at their local positions in the staging buffer
+        __syncthreads();
+    }
+    if (g < m) row_to_stg(tid, a);
+    __syncthreads();
+    write_half(two ? 1 : 0);
+    P2CT(21);
+#undef P2CT
+#undef P2CTJ
+}
+
+// ---------------------------------------------------------------------------------------
 // Update of step k0: for rows i in [k0, n) and columns c in [k0+w, n):
 //   top rows (i < k0+w):   Bn[i][c] = U12 = L11^{-1} Bk[src_top][c]
 //   other rows:            Bn[i][c] = Bk[src(i)][c] - L21[i][:] U12[:][c]
@@ -579,6 +930,227 @@ lu_update2_kernel(const T *__restrict__ Bk, T *__restrict__ Bn, long long ld, in
     }
 }
 
+// Tensor-pipe variant of the update (the default): the same gather and TRSM, then the rank-PW
+// product on DMMA m8n8k4 fragments in the GEMM engine's register layout (8 warps as 2 x 4, warp
+// tile 32 x 16), C fragments loaded straight from the (gathered) source rows; U12 is computed
+// once per column block (first row block of tiles) and shared through Bn + a release flag.
+constexpr int U2M_WGM = 2, U2M_WGN = 4;
+template <typename T> struct U2Pad { static constexpr int P = 4; };   // row offset = 8 words mod 32
+template <> struct U2Pad<double2> { static constexpr int P = 2; };
+
+template <typename T> struct U2MinB { static constexpr int B = 2; };
+template <> struct U2MinB<double2> { static constexpr int B = 2; };
+
+template <typename T, int PW>
+FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long long ld, int n, int k0, int w,
+                            const int *__restrict__ mv2, int *__restrict__ perm, int *__restrict__ iperm,
+                            int *__restrict__ snap, int *__restrict__ u12f, int tag, int cbeg, int cend, int doperm) {
+    constexpr int SP = U2Pad<T>::P;
+    constexpr int E = 16 / (int)sizeof(T);
+    constexpr int WM = U2_TR / U2M_WGM, WN = U2_TC / U2M_WGN, MT = WM / 8, NT = WN / 8;
+    constexpr int V = AccW<T>::V;
+    static_assert(U2M_WGM * U2M_WGN * 32 == U2_T, "8 warps");
+    __shared__ int mdst[MV2_MAX], msrc[MV2_MAX];
+    __shared__ int nmv_s;
+    __shared__ __align__(16) T L11[PW][PW + SP];
+    __shared__ __align__(16) T Us[PW][U2_TC + SP];     // X, then -U12 in place
+    __shared__ __align__(16) T Ls[U2_TR][PW + SP];     // L21 rows of this tile
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm0 = (warp / U2M_WGN) * WM, wn0 = (warp % U2M_WGN) * WN;
+    const int c0 = cbeg + blockIdx.x * U2_TC;
+    const int r0 = k0 + w + blockIdx.y * U2_TR;
+    const bool tile = c0 < cend;
+    const bool rows = tile && r0 < n;
+    const int nc = min(U2_TC, cend - c0);
+    // ---- 1. requests independent of the move list
+    if (tile) {
+        for (int idx = tid; idx < PW * (PW / E); idx += U2_T) {
+            const int i = idx / (PW / E), e = (idx % (PW / E)) * E;
+            cp_async16(&L11[i][e], Bk + (long long)(k0 + i) * ld + k0 + e);
+        }
+        if (rows) {
+            for (int idx = tid; idx < U2_TR * (PW / E); idx += U2_T) {
+                const int r = idx / (PW / E), e = (idx % (PW / E)) * E;
+                if (r0 + r < n) cp_async16(&Ls[r][e], Bk + (long long)(r0 + r) * ld + k0 + e);
+            }
+        }
+    }
+    cp_async_commit();
+    double acc[MT][NT][V];
+    auto load_c = [&](int i, const T *src) {  // C fragments of row group i from a source row
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            const int cc = wn0 + j * 8 + 2 * t;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const T v = (cc + e < nc) ? src[cc + e] : zero_of(T());
+                if constexpr (sizeof(T) == 8) acc[i][j][e] = acc_re(v);
+                else { acc[i][j][e] = acc_re(v); acc[i][j][2 + e] = acc_im(v); }
+            }
+        }
+    };
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int e = 0; e < V; ++e) acc[i][j][e] = 0.0;
+    if (rows) {
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+            const int r = r0 + wm0 + i * 8 + g;
+            if (r < n) load_c(i, Bk + (long long)r * ld + c0);
+        }
+    }
+    // ---- 2. the move list
+    if (tid < MV2_MAX) {
+        const int nm = mv2[0];
+        if (tid == 0) nmv_s = nm;
+        mdst[tid] = tid < nm ? mv2[1 + tid] : -1;
+        msrc[tid] = tid < nm ? mv2[1 + MV2_MAX + tid] : -1;
+    }
+    __syncthreads();
+    const int nm = nmv_s;
+    if (doperm && blockIdx.x == 0 && blockIdx.y == 0) {
+        int pv = 0;
+        if (tid < nm) pv = perm[msrc[tid]];
+        __syncthreads();
+        if (tid < nm) {
+            perm[mdst[tid]] = pv;
+            iperm[pv] = mdst[tid];
+        }
+        __syncthreads();
+        if (snap)
+            for (int i = tid; i < n; i += U2_T) snap[i] = iperm[i];
+    }
+    if (!tile) return;
+    // ---- 3. the first row block of tiles PRODUCES U12 of its columns (gather of the pivot rows X,
+    // TRSM), stores it in Bn's top rows and raises the column block's flag; the other tiles load
+    // it from there (L2) once the flag is up, instead of each repeating the TRSM
+    const bool prod = blockIdx.y == 0;
+    if (prod) {
+        for (int idx = tid; idx < PW * (U2_TC / E); idx += U2_T) {
+            const int i = idx / (U2_TC / E), e = (idx % (U2_TC / E)) * E;
+            int src = k0 + i;
+            for (int q = 0; q < nm; ++q)
+                if (mdst[q] == k0 + i) src = msrc[q];
+            if (e < nc) cp_async16(&Us[i][e], Bk + (long long)src * ld + c0 + e);
+        }
+    }
+    cp_async_commit();
+    if (rows) {
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+            const int r = r0 + wm0 + i * 8 + g;
+            int src = r;
+            for (int q = 0; q < nm; ++q)
+                if (mdst[q] == r) src = msrc[q];
+            if (src != r && r < n) load_c(i, Bk + (long long)src * ld + c0);
+        }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    if (prod) {
+        // ---- 4. U12 = L11^{-1} X (unit lower forward substitution), one thread per column
+        if (tid < U2_TC) {
+            T x[PW];
+#pragma unroll
+            for (int i = 0; i < PW; ++i) x[i] = Us[i][tid];
+#pragma unroll
+            for (int q = 0; q < PW; ++q)
+#pragma unroll
+                for (int i = q + 1; i < PW; ++i) x[i] = msub(x[i], L11[i][q], x[q]);
+#pragma unroll
+            for (int i = 0; i < PW; ++i) Us[i][tid] = x[i];
+            if (tid < nc) {
+#pragma unroll
+                for (int i = 0; i < PW; ++i) Bn[(long long)(k0 + i) * ld + c0 + tid] = x[i];
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(u12f + blockIdx.x), "r"(tag) : "memory");
+        }
+    } else {
+        if (tid == 0) {
+            long long it = 0;
+            int v;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(u12f + blockIdx.x) : "memory");
+                if (v >= tag) break;
+                __nanosleep(32);
+                if (++it > (1LL << 26)) __trap();  // a producer that never runs: fail, do not hang
+            }
+        }
+        __syncthreads();
+        for (int idx = tid; idx < PW * (U2_TC / E); idx += U2_T) {
+            const int i = idx / (U2_TC / E), e = (idx % (U2_TC / E)) * E;
+            if (e < nc) cp_async16(&Us[i][e], Bn + (long long)(k0 + i) * ld + c0 + e);
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+    }
+    if (!rows) return;
+    // ---- 5. C += (-L21) U12 on the tensor pipe
+#pragma unroll
+    for (int kk = 0; kk < PW; kk += 4) {
+        T a[MT], b[NT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) a[i] = scal(Ls[wm0 + i * 8 + g][kk + t], -1.0);
+#pragma unroll
+        for (int j = 0; j < NT; ++j) b[j] = Us[kk + t][wn0 + j * 8 + g];
+        mma_tile<MT, NT>(acc, a, b);
+    }
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+        const int r = r0 + wm0 + i * 8 + g;
+        if (r >= n) continue;
+        T *dst = Bn + (long long)r * ld + c0;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+            const int cc = wn0 + j * 8 + 2 * t;
+            if constexpr (sizeof(T) == 8) {
+                if (cc + 1 < nc) *reinterpret_cast<double2 *>(dst + cc) = make_double2(acc[i][j][0], acc[i][j][1]);
+                else if (cc < nc) dst[cc] = acc[i][j][0];
+            } else {
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    if (cc + e < nc) dst[cc + e] = acc_val(acc[i][j], e);
+            }
+        }
+    }
+}
+
+
+// Launch modes (look-ahead pipeline of lu2_factor, see there):
+//   NEXT  (lookahead = 0): the columns of the next panel; waits for its predecessor as usual and
+//         applies the step's moves to perm / iperm (+ snapshot).
+//   BULK  (lookahead = 1): all columns right of the next panel; launched behind the NEXT panel,
+//         which it does not need, so it does NOT wait at entry (its inputs are complete: the
+//         panel it follows only released it after its own wait); the last CTA to finish waits for
+//         that panel before exiting, so the grid's completion still implies the panel's.
+template <typename T, int PW>
+__global__ void __launch_bounds__(U2_T, U2MinB<T>::B)
+lu_update2m_kernel(const T *__restrict__ Bk, T *__restrict__ Bn, long long ld, int n, int k0, int w,
+                   const int *__restrict__ mv2, int *__restrict__ perm, int *__restrict__ iperm,
+                   int *__restrict__ snap, int *__restrict__ u12f, int tag, int cbeg, int cend, int doperm,
+                   int lookahead, int *__restrict__ done_ctr) {
+    pdl_trigger();
+    if (!lookahead) pdl_wait();
+    update2m_body<T, PW>(Bk, Bn, ld, n, k0, w, mv2, perm, iperm, snap, u12f, tag, cbeg, cend, doperm);
+    if (lookahead) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const int total = (int)(gridDim.x * gridDim.y);
+            if (atomicAdd(done_ctr, 1) == total - 1) pdl_wait();
+        }
+    }
+}
+
 // Final U / L in final row order (see the file header).  snap[b * n + orig] = position of
 // original row `orig` after step b.
 template <typename T>
@@ -609,18 +1181,34 @@ __global__ void lu_assemble2_kernel(const T *__restrict__ B0, const T *__restric
     }
 }
 
-__global__ void iota2_kernel(int *p, int *q, int n) {
+__global__ void iota2_kernel(int *p, int *q, int n, int *flags, int nflags) {
     pdl_trigger();
     pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) { p[i] = i; q[i] = i; }
+    if (flags && i < nflags) flags[i] = 0;
 }
 
 // ---------------------------------------------------------------------------------------
+// tail of the int workspace: U12-ready flags (NEXT and BULK grids) + per-step finish counters
+static size_t lu2_sync_ints(int n) {
+    const size_t ncb = (size_t)(n + U2_TC - 1) / U2_TC + 1;
+    return 2 * ncb + (size_t)(n + 7) / 8 + 1;
+}
+
+int lu2_max_n() {
+    static int v = [] {
+        const char *e = getenv("FROB_LU2_MAX");
+        const int x = e ? atoi(e) : LU2_MAX_N;
+        return x < LU2_MAX_N ? x : LU2_MAX_N;
+    }();
+    return v;
+}
+
 size_t lu2_int_elems(int n) {
     const int W = 8;  // smallest panel width (complex): most steps
     const size_t steps = (size_t)(n + W - 1) / W;
-    return (size_t)n /* iperm */ + steps * MV2_INTS + steps * (size_t)n /* snapshots */;
+    return (size_t)n /* iperm */ + steps * MV2_INTS + steps * (size_t)n /* snapshots */ + lu2_sync_ints(n);
 }
 
 template <typename T, int PH, int R>
@@ -645,38 +1233,131 @@ static cudaError_t launch_panel2(const CUtensorMap &tm, T *B, long long ld, int 
                       k0, w, mv2, diag);
 }
 
+template <typename T, int PH>
+static cudaError_t launch_panel2c(const CUtensorMap &tm, T *B, long long ld, int n, int k0, int w, int *mv2, T *diag,
+                                  int CS, cudaStream_t s) {
+    constexpr bool TWO = Panel2W<T>::PW > PH;
+    const size_t smem = (size_t)P2_T * 128 + 1024;
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !attr_set[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(lu_panel2c_kernel<T, PH, TWO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_set[dev] = true;
+    }
+    double wk = 0.0;
+    for (int j = 0; j < w; ++j) wk += (double)(n - k0 - j - 1) * (1.0 + 2.0 * (w - j - 1));
+    ProfScope ps(sizeof(T) == 8 ? "lu_panel2c<double>" : "lu_panel2c<double2>", s, wk * (sizeof(T) == 8 ? 1.0 : 4.0));
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[2];
+    cfg.gridDim = dim3((unsigned)CS);
+    cfg.blockDim = dim3(P2_T);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = (unsigned)CS;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    count_launch();
+    return cudaLaunchKernelEx(&cfg, lu_panel2c_kernel<T, PH, TWO>, tm, B, ld, n, k0, w, mv2, diag);
+}
+
+template <typename T>
+cudaError_t lu2_panel_inplace(const CUtensorMap &tm, T *A, long long lda, int n, int k0, int w, int *mv, T *diag,
+                              cudaStream_t s) {
+    constexpr int PH = Panel2W<T>::PH;
+    const int m = n - k0;
+    static_assert(MV2_INTS == MV_INTS && MV2_MAX == 2 * PW_MAX, "move-list layouts agree");
+    if (m > LU2_PANEL_MAX_M || m > P2C_MAX * P2_T) return cudaErrorInvalidValue;
+    if (m > P2_T) return launch_panel2c<T, PH>(tm, A, lda, n, k0, w, mv, diag, (m + P2_T - 1) / P2_T, s);
+    return launch_panel2<T, PH, 1>(tm, A, lda, n, k0, w, mv, diag, s);
+}
+template cudaError_t lu2_panel_inplace<double>(const CUtensorMap &, double *, long long, int, int, int, int *, double *,
+                                               cudaStream_t);
+template cudaError_t lu2_panel_inplace<double2>(const CUtensorMap &, double2 *, long long, int, int, int, int *,
+                                                double2 *, cudaStream_t);
+
+// look-ahead pipeline (default) or panel -> full update per step (env FROB_LU2_LOOKAHEAD=0, A/B aid)
+static bool lu2_lookahead() {
+    static bool v = [] {
+        const char *e = getenv("FROB_LU2_LOOKAHEAD");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
+// Step k (panel P_k at k0 = k PW) is followed by
+//   NEXT_k: the update of the next panel's PW columns only (+ the step's perm / iperm / snapshot),
+//   BULK_k: the update of every column right of those, launched AFTER P_{k+1} so that it runs
+//           concurrently with it (P_{k+1} releases its dependents right after its own wait).
+// Stream order: P_0 NEXT_0 | P_1 BULK_0 NEXT_1 | P_2 BULK_1 NEXT_2 | ...  Every kernel reads
+// only data its chain of waits has completed: P_{k+1} needs NEXT_k; BULK_k needs P_k and BULK_{k-1}
+// (complete before NEXT_k, its predecessor's predecessor, finished); NEXT_{k+1} waits for BULK_k,
+// whose last CTA waits for P_{k+1}.  P_{k+1} writes columns [k0+PW, k0+2PW) of B_{k+1} and BULK_k
+// columns >= k0 + 2PW: disjoint.
 template <typename T>
 cudaError_t lu2_factor(int n, T *B0, T *B1, long long ld, T *U, T *L, long long ldo, int *perm, int *iw, T *diag,
                        LuStats *stats, cudaStream_t s) {
     constexpr int PW = Panel2W<T>::PW, PH = Panel2W<T>::PH;
     if (n > LU2_MAX_N) return cudaErrorInvalidValue;
     const int steps = (n + PW - 1) / PW;
+    const int ncb = (n + U2_TC - 1) / U2_TC + 1;
     int *iperm = iw;
     int *mvb = iw + n;
     int *snap = mvb + (size_t)steps * MV2_INTS;
+    int *sync = iw + lu2_int_elems(n) - lu2_sync_ints(n);
+    int *flagN = sync, *flagB = sync + ncb, *done = sync + 2 * ncb;
+    const int nsync = (int)lu2_sync_ints(n);
     // TMA descriptors of the two ping-pong buffers (rows x 16-double boxes, 128B swizzle)
     const int E = (int)(sizeof(T) / 8);
     CUtensorMap tm[2];
     cudaError_t e = tma_map_rows128(&tm[0], B0, n, (long long)n * E, ld * E, 256);
     if (e == cudaSuccess) e = tma_map_rows128(&tm[1], B1, n, (long long)n * E, ld * E, 256);
     if (e != cudaSuccess) return e;
-    e = launch_pdl(iota2_kernel, dim3((n + 255) / 256), dim3(256), 0, s, perm, iperm, n);
+    e = launch_pdl(iota2_kernel, dim3((max(n, nsync) + 255) / 256), dim3(256), 0, s, perm, iperm, n, sync, nsync);
     if (e != cudaSuccess) return e;
+    const bool la = lu2_lookahead();
+    const char *nm_next = sizeof(T) == 8 ? "lu_next2<double>" : "lu_next2<double2>";
+    const char *nm_bulk = sizeof(T) == 8 ? "lu_update2<double>" : "lu_update2<double2>";
+    // update of step kk over columns [cb, ce)
+    auto update = [&](int kk, int cb, int ce, bool next) -> cudaError_t {
+        const int k0 = kk * PW, w = min(PW, n - k0), m = n - k0;
+        const T *Bk = (kk & 1) ? B1 : B0;
+        T *Bn = (kk & 1) ? B0 : B1;
+        const int cols = max(0, ce - cb), rows = n - k0 - w;
+        dim3 grid(max(1, (cols + U2_TC - 1) / U2_TC), max(1, (rows + U2_TR - 1) / U2_TR));
+        if (cols == 0) grid = dim3(1, 1);
+        const double upd = ((double)(m - w) * 2.0 * w + (double)w * w) * (double)cols;  // GEMM + TRSM
+        ProfScope ps(next ? nm_next : nm_bulk, s, upd * (sizeof(T) == 8 ? 1.0 : 4.0));
+        return launch_pdl(lu_update2m_kernel<T, PW>, grid, dim3(U2_T), 0, s, Bk, Bn, ld, n, k0, w,
+                          (const int *)(mvb + (size_t)kk * MV2_INTS), perm, iperm,
+                          (next && kk + 1 < steps) ? snap + (size_t)kk * n : (int *)nullptr, next ? flagN : flagB,
+                          kk + 1, cb, ce, next ? 1 : 0, next ? 0 : 1, done + kk);
+    };
     for (int k = 0; k < steps; ++k) {
         const int k0 = k * PW, w = min(PW, n - k0), m = n - k0;
         T *Bk = (k & 1) ? B1 : B0;
-        T *Bn = (k & 1) ? B0 : B1;
         int *mv2 = mvb + (size_t)k * MV2_INTS;
-        if (m <= P2_T) e = launch_panel2<T, PH, 1>(tm[k & 1], Bk, ld, n, k0, w, mv2, diag, s);
-        else e = launch_panel2<T, PH, 2>(tm[k & 1], Bk, ld, n, k0, w, mv2, diag, s);
+        // one CTA up to P2_T rows, else a cluster of ceil(m / P2_T) CTAs (measured: a 2-CTA cluster
+        // beats one CTA with two rows per thread at 512 < m <= 1024)
+        if (m > P2_T) e = launch_panel2c<T, PH>(tm[k & 1], Bk, ld, n, k0, w, mv2, diag, (m + P2_T - 1) / P2_T, s);
+        else e = launch_panel2<T, PH, 1>(tm[k & 1], Bk, ld, n, k0, w, mv2, diag, s);
         if (e != cudaSuccess) return e;
-        const int rest = n - k0 - w;
-        dim3 grid(max(1, (rest + U2_TC - 1) / U2_TC), max(1, (rest + U2_TR - 1) / U2_TR));
-        const double upd = ((double)(m - w) * 2.0 * w + (double)w * w) * (double)rest;  // GEMM + TRSM
-        ProfScope ps(sizeof(T) == 8 ? "lu_update2<double>" : "lu_update2<double2>", s, upd * (sizeof(T) == 8 ? 1.0 : 4.0));
-        e = launch_pdl(lu_update2_kernel<T, PW>, grid, dim3(U2_T), 0, s, (const T *)Bk, Bn, ld, n, k0, w,
-                       (const int *)mv2, perm, iperm, k + 1 < steps ? snap + (size_t)k * n : (int *)nullptr);
-        if (e != cudaSuccess) return e;
+        if (!la) {
+            if ((e = update(k, k0 + w, n, true)) != cudaSuccess) return e;
+            continue;
+        }
+        if (k >= 1) {  // BULK_{k-1}: columns right of P_k's
+            const int cb = k0 + PW;
+            if (cb < n && (e = update(k - 1, cb, n, false)) != cudaSuccess) return e;
+        }
+        if ((e = update(k, k0 + w, min(n, k0 + w + PW), true)) != cudaSuccess) return e;  // NEXT_k
     }
     {
         const long long total = (long long)n * n;

@@ -74,8 +74,10 @@ def test_dgemm_exact_integers():
     assert np.array_equal(_np(fb.dgemm(_t(a), _t(b))), oracle.dgemm(a, b))
 
 
-@pytest.mark.parametrize("n", [1, 2, 5, 33, 100, 257, 1000])
+@pytest.mark.parametrize("n", [1, 2, 5, 33, 100, 257, 1000, 1536, 2100])
 def test_dgetrf_reconstruction(n):
+    # n = 1536 / 2100 (16-byte aligned rows): the blocked getrf with lu2's 32-column panel kernels
+    # (one CTA, then clusters of up to 4 CTAs), single-level and two-level (n >= 2048)
     a, _ = synth.gauss_pair(n, seed=n, shift=0.0)
     lu, perm, info = fb.dgetrf(_t(a))
     lu, perm = _np(lu), _np(perm)
@@ -142,6 +144,18 @@ def test_config2_full_size():
 def test_zinv_lu(n):
     z = synth.shifted_complex(n, seed=7 * n, shift=3.0 + math.sqrt(n))
     _check_inverse(z, _np(fb.zinv(_t(z))))
+
+
+@pytest.mark.parametrize("n", [1100, 1537, 2048])
+def test_cluster_panel_sizes(n):
+    """n > 1024: lu2 steps with more than 512 rows take the cluster panel (2..4 CTAs, DSMEM pivot
+    exchange) and the look-ahead pipeline; Frobenius and complex LU against the oracle."""
+    z = synth.shifted_complex(n, seed=31 * n, shift=math.sqrt(n) + 2.0)
+    ref, _ = oracle.zinv_gj(z)
+    x, info = fb.inv(_t(z), info=True)
+    assert info["info"] == 0
+    _check_inverse(z, _np(x), ref)
+    _check_inverse(z, _np(fb.zinv(_t(z))), ref)
 
 
 # ------------------------------------------------------------------ NEXT-1 fused first step

@@ -13,6 +13,7 @@ using namespace frob;
 unsigned long long &frob::launch_counter() { static unsigned long long c = 0; return c; }
 bool frob::prof_enabled() { return false; }
 void frob::prof_record(const char *, cudaStream_t, bool, double) {}
+thread_local const char *frob::g_gemm_tag = nullptr;
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e_), __LINE__); exit(1); } } while (0)
 
@@ -148,7 +149,7 @@ void pieces(int n) {
     CK(cudaMalloc(&B0, bytes)); CK(cudaMalloc(&B1, bytes)); CK(cudaMalloc(&diag, n * sizeof(T)));
     CK(cudaMalloc(&iw, lu2_int_elems(n) * 4)); CK(cudaMalloc(&perm, n * 4)); CK(cudaMalloc(&iperm, n * 4));
     CK(cudaMemcpy(B0, h.data(), bytes, cudaMemcpyHostToDevice));
-    iota2_kernel<<<(n + 255) / 256, 256>>>(perm, iperm, n);
+    iota2_kernel<<<(n + 255) / 256, 256>>>(perm, iperm, n, nullptr, 0);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     float ms;
     auto tm = [&](const char *nm, auto fn, int reps) {
@@ -161,12 +162,12 @@ void pieces(int n) {
     // the panel kernel re-factors the same (already factored) panel: timing only
     CUtensorMap tmap;
     CK(tma_map_rows128(&tmap, B0, n, (long long)n * (sizeof(T) / 8), ld * (sizeof(T) / 8), 256));
-    tm("panel2 (m=n) x20", [&] {
+    if (n <= 2 * P2_T) tm("panel2 (m=n) x20", [&] {
         if (n <= P2_T) launch_panel2<T, PH, 1>(tmap, B0, ld, n, 0, PW, iw, diag, 0);
-        else launch_panel2<T, PH, 2>(tmap, B0, ld, n, 0, PW, iw, diag, 0);
+        else launch_panel2c<T, PH>(tmap, B0, ld, n, 0, PW, iw, diag, (n + P2_T - 1) / P2_T, 0);
     }, 20);
 #ifdef FROB_P2_TRACE
-    {
+    if (n <= 2 * P2_T) {
         long long tr[64];
         CK(cudaDeviceSynchronize());
         CK(cudaMemcpyFromSymbol(tr, g_p2_trace, sizeof(tr)));
@@ -178,6 +179,21 @@ void pieces(int n) {
     }
 #endif
 
+    if (n > P2_T) {
+        tm("panel2c cluster (m=n) x20", [&] {
+            launch_panel2c<T, PH>(tmap, B0, ld, n, 0, PW, iw, diag, (n + P2_T - 1) / P2_T, 0);
+        }, 20);
+#ifdef FROB_P2_TRACE
+        long long tr[64];
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpyFromSymbol(tr, g_p2_trace, sizeof(tr)));
+        printf("   trace: load %lld half0 %lld trans %lld half1 %lld tail %lld | cols(half1):", tr[1] - tr[0], tr[19] - tr[1],
+               tr[18] - tr[19], tr[20] - tr[18], tr[21] - tr[20]);
+        for (int j = 1; j < PH; ++j) printf(" %lld", tr[2 + j] - tr[1 + j]);
+        printf("\n   col5: pre-bar %lld push %lld deferred %lld wait %lld argmax+row %lld mult %lld cand+pub %lld\n",
+               tr[40] - tr[6], tr[41] - tr[40], tr[42] - tr[41], tr[43] - tr[42], tr[44] - tr[43], tr[45] - tr[44], tr[7] - tr[45]);
+#endif
+    }
     const int rest = n - PW;
     dim3 grid(max(1, (rest + U2_TC - 1) / U2_TC), max(1, (rest + U2_TR - 1) / U2_TR));
     tm("update2 step 0 x20", [&] {
@@ -186,11 +202,11 @@ void pieces(int n) {
     }, 20);
     tm("panel2+update2 alternating x20", [&] {
         if (n <= P2_T) launch_panel2<T, PH, 1>(tmap, B0, ld, n, 0, PW, iw, diag, 0);
-        else launch_panel2<T, PH, 2>(tmap, B0, ld, n, 0, PW, iw, diag, 0);
+        else launch_panel2c<T, PH>(tmap, B0, ld, n, 0, PW, iw, diag, (n + P2_T - 1) / P2_T, 0);
         launch_pdl(lu_update2_kernel<T, PW>, grid, dim3(U2_T), 0, (cudaStream_t)0, (const T *)B0, B1, ld, n, 0, PW,
                    (const int *)iw, perm, iperm, (int *)nullptr);
     }, 20);
-    tm("empty-ish: iota x20", [&] { launch_pdl(iota2_kernel, dim3(1), dim3(32), 0, (cudaStream_t)0, perm, iperm, 1); }, 20);
+    tm("empty-ish: iota x20", [&] { launch_pdl(iota2_kernel, dim3(1), dim3(32), 0, (cudaStream_t)0, perm, iperm, 1, (int *)nullptr, 0); }, 20);
     CK(cudaGetLastError());
     cudaFree(B0); cudaFree(B1); cudaFree(diag); cudaFree(iw); cudaFree(perm); cudaFree(iperm);
 }
@@ -198,6 +214,7 @@ void pieces(int n) {
 int main(int argc, char **argv) {
     if (argc > 1 && argv[1][0] == 'p') {
         pieces<double>(1024); pieces<double>(512); pieces<double2>(1024);
+        pieces<double>(2048); pieces<double>(4096); pieces<double2>(4096);
         return 0;
     }
     if (argc > 1 && argv[1][0] == 't') {
@@ -215,6 +232,13 @@ int main(int argc, char **argv) {
                    tr[1] / nb, tr[2] / nb, tr[2] / n, tr[3] / nb);
         }
 #endif
+        return 0;
+    }
+    if (argc > 1 && argv[1][0] == 'c') {  // cluster panel sizes (m > 512 rows)
+        int szc[] = {513, 777, 1024, 1025, 1500, 2048, 3001, 4096};
+        run<double>(2048, 5);  // warm-up (clocks)
+        for (int n : szc) run<double>(n, 5);
+        for (int n : szc) run<double2>(n, 3);
         return 0;
     }
     if (argc > 1 && argv[1][0] == '3') {
