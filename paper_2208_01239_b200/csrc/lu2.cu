@@ -81,6 +81,141 @@ FROB_DEV void ld_row_smem(T (&u)[PW], const T *src) {
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Fused look-ahead (lu2_factor): a panel kernel of step k > 0 receives its columns NOT yet
+// updated by step k-1 and applies that update itself, instead of a separate kernel on the
+// critical path between two panels: for its rows r (positions after step k-1),
+//   a[r][c] = Bp[src(r)][c] - sum_q Lp[r][q] U12p[q][c],   c in this panel's columns,
+// src = step k-1's row moves (gather), Lp = step k-1's multipliers (Bp, its panel columns),
+// U12p = L11p^{-1} Xp from step k-1's pivot rows (every CTA solves it; the writer also stores it
+// as the U rows of step k-1 for these columns into B).  Half 0 lands in registers, half 1 in the
+// staging buffer, exactly where the TMA path would have put them.
+template <typename T, int PWT>
+struct PreSmem {
+    int mdst[MV2_MAX], msrc[MV2_MAX];
+    int nm;
+    __align__(16) T L11[PWT][PWT + 16 / (int)sizeof(T)];
+    __align__(16) T U[PWT][PWT + 16 / (int)sizeof(T)];
+};
+
+template <typename T, int PH, bool TWO>
+FROB_DEV void pre_update(const T *__restrict__ Bp, const int *__restrict__ mvp, int kp0, T *__restrict__ B,
+                         long long ld, int n, int k0, int w, int g, bool writer, int lrow, T (&a)[PH],
+                         unsigned char *stgb, unsigned char *d0s, PreSmem<T, (TWO ? 2 * PH : PH)> &sm) {
+    constexpr int PWT = TWO ? 2 * PH : PH;
+    constexpr int E = 16 / (int)sizeof(T);
+    const int tid = threadIdx.x;
+    const int m = n - k0;
+    if (tid < MV2_MAX) {
+        const int nm = mvp[0];
+        if (tid == 0) sm.nm = nm;
+        sm.mdst[tid] = tid < nm ? mvp[1 + tid] : -1;
+        sm.msrc[tid] = tid < nm ? mvp[1 + MV2_MAX + tid] : -1;
+    }
+    for (int idx = tid; idx < PWT * (PWT / E); idx += P2_T) {
+        const int i = idx / (PWT / E), e = (idx % (PWT / E)) * E;
+        cp_async16(&sm.L11[i][e], Bp + (long long)(kp0 + i) * ld + kp0 + e);
+    }
+    __syncthreads();
+    const int nm = sm.nm;
+    for (int idx = tid; idx < PWT * (PWT / E); idx += P2_T) {
+        const int i = idx / (PWT / E), e = (idx % (PWT / E)) * E;
+        int src = kp0 + i;
+        for (int q = 0; q < nm; ++q)
+            if (sm.mdst[q] == kp0 + i) src = sm.msrc[q];
+        if (e < w) cp_async16(&sm.U[i][e], Bp + (long long)src * ld + k0 + e);  // (w even or ld > n)
+    }
+    const int r = k0 + g;
+    int src = r;
+    for (int q = 0; q < nm; ++q)
+        if (sm.mdst[q] == r) src = sm.msrc[q];
+    // this row's D values (gathered) are requested before the solve, straight into shared memory
+    // (half 0 into d0s, half 1 into its staging row): no registers held across the solve
+    {
+        const T *d = Bp + (long long)src * ld + k0;
+#pragma unroll
+        for (int h = 0; h < (TWO ? 2 : 1); ++h) {
+            unsigned char *base = h ? stgb : d0s;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                unsigned char *dst = base + swz128(lrow, c);
+                if (g < m && h * PH + c * E < w) cp_async16(dst, d + h * PH + c * E);
+                else *reinterpret_cast<double2 *>(dst) = make_double2(0.0, 0.0);
+            }
+        }
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    // U12p = L11p^{-1} Xp (unit lower forward substitution), one thread per column
+    if (tid < PWT) {
+        T x[PWT];
+#pragma unroll
+        for (int i = 0; i < PWT; ++i) x[i] = sm.U[i][tid];
+#pragma unroll
+        for (int q = 0; q < PWT; ++q)
+#pragma unroll
+            for (int i = q + 1; i < PWT; ++i) x[i] = msub(x[i], sm.L11[i][q], x[q]);
+#pragma unroll
+        for (int i = 0; i < PWT; ++i) sm.U[i][tid] = x[i];
+        if (writer && tid < w) {
+#pragma unroll
+            for (int i = 0; i < PWT; ++i) B[(long long)(kp0 + i) * ld + k0 + tid] = x[i];
+        }
+    }
+    __syncthreads();
+    // this row's multipliers of the previous step (one vector load batch), then each half:
+    // x = D - L U12p over the half's columns, from and back to shared memory / registers
+    T lrow_v[PWT];
+    if (g < m) {
+        const T *lr = Bp + (long long)r * ld + kp0;
+        if constexpr (sizeof(T) == 8) {
+#pragma unroll
+            for (int q = 0; q < PWT; q += 2) {
+                const double2 v = *reinterpret_cast<const double2 *>(lr + q);
+                lrow_v[q] = v.x;
+                lrow_v[q + 1] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < PWT; ++q) lrow_v[q] = lr[q];
+        }
+    }
+    auto half = [&](unsigned char *base, int h, T (&x)[PH]) {
+        double t[16];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const double2 v = *reinterpret_cast<const double2 *>(base + swz128(lrow, c));
+            t[2 * c] = v.x;
+            t[2 * c + 1] = v.y;
+        }
+#pragma unroll
+        for (int c = 0; c < PH; ++c) {
+            if constexpr (sizeof(T) == 8) x[c] = t[c];
+            else x[c] = make_double2(t[2 * c], t[2 * c + 1]);
+        }
+        if (g < m) {
+#pragma unroll
+            for (int q = 0; q < PWT; ++q) {
+#pragma unroll
+                for (int c = 0; c < PH; ++c) x[c] = msub(x[c], lrow_v[q], sm.U[q][h * PH + c]);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < PH; ++c)
+            if (h * PH + c >= w) x[c] = zero_of(T());
+    };
+    if constexpr (TWO) {
+        T x1[PH];
+        half(stgb, 1, x1);
+        const double *xd = reinterpret_cast<const double *>(x1);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<double2 *>(stgb + swz128(lrow, c)) = make_double2(xd[2 * c], xd[2 * c + 1]);
+    }
+    half(d0s, 0, a);
+}
+
 // Panel of step k0: rows [k0, n) x columns [k0, k0 + w) of B (ld), w <= 2 * PH, factored in
 // place as two PH-column halves (PH = 16 real / 8 complex: 128-byte row halves).  Thread t owns
 // relative rows t + q * P2_T (q < R).  Half 0 is TMA-loaded and moved to registers; half 1 is
@@ -92,7 +227,8 @@ FROB_DEV void ld_row_smem(T (&u)[PW], const T *src) {
 template <typename T, int PH, int R, bool TWO>
 __global__ void __launch_bounds__(P2_T, 1)
 lu_panel2_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, long long ld, int n, int k0, int w,
-                 int *__restrict__ mv2, T *__restrict__ diag) {
+                 int *__restrict__ mv2, T *__restrict__ diag, const T *__restrict__ Bp, const int *__restrict__ mvp,
+                 int kp0) {
     extern __shared__ __align__(1024) unsigned char stgb[];  // R * P2_T rows x 128 B, 128B-swizzled (TMA)
     __shared__ __align__(8) unsigned long long tbar;
     if (threadIdx.x == 0) {
@@ -147,10 +283,6 @@ lu_panel2_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, lo
             *reinterpret_cast<double2 *>(stgb + swz128(r, c)) = make_double2(rd[2 * c], rd[2 * c + 1]);
     };
 
-    // ---- half 0: TMA load -> registers; half 1 then streams into the staging buffer
-    if (tid == 0) tma_half(0, 0u);
-    __syncthreads();
-    mbar_wait_cta(smem_u32(&tbar), 0u);
     T a[R][PH];
     int grow[R], pst[R];
     unsigned live = 0;
@@ -159,12 +291,26 @@ lu_panel2_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, lo
         grow[q] = q * P2_T + tid;
         pst[q] = -1;
         if (grow[q] < m) live |= 1u << q;
-        row_from_stg(grow[q], a[q]);
     }
-    __syncthreads();  // every thread has read its half-0 rows: the staging buffer is free
-    if (two && tid == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        tma_half(1, 1u);
+    const bool fused = R == 1 && Bp != nullptr;
+    __shared__ PreSmem<T, (TWO ? 2 * PH : PH)> psm;
+    if (fused) {
+        // ---- fused look-ahead: this panel applies the previous step's update to its columns
+        if constexpr (R == 1)
+            pre_update<T, PH, TWO>(Bp, mvp, kp0, B, ld, n, k0, w, tid, true, tid, a[0], stgb, stgb + P2_T * 128, psm);
+        __syncthreads();
+    } else {
+        // ---- half 0: TMA load -> registers; half 1 then streams into the staging buffer
+        if (tid == 0) tma_half(0, 0u);
+        __syncthreads();
+        mbar_wait_cta(smem_u32(&tbar), 0u);
+#pragma unroll
+        for (int q = 0; q < R; ++q) row_from_stg(grow[q], a[q]);
+        __syncthreads();  // every thread has read its half-0 rows: the staging buffer is free
+        if (two && tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tma_half(1, 1u);
+        }
     }
     P2T(1);
 
@@ -296,7 +442,7 @@ lu_panel2_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, lo
 
     if constexpr (TWO) if (two) {
         // ---- half 1: U12 = L11^{-1} X from half 0's pivot rows, rank-PH update, swap
-        mbar_wait_cta(smem_u32(&tbar), 1u);
+        if (!fused) mbar_wait_cta(smem_u32(&tbar), 1u);
 #pragma unroll
         for (int q = 0; q < R; ++q)
             if (pst[q] >= 0) {
@@ -451,7 +597,8 @@ FROB_DEV void st_async_16b(unsigned raddr, const uint4 v, unsigned rbar) {
 template <typename T, int PH, bool TWO>
 __global__ void __launch_bounds__(P2_T, 1)
 lu_panel2c_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, long long ld, int n, int k0, int w,
-                  int *__restrict__ mv2, T *__restrict__ diag) {
+                  int *__restrict__ mv2, T *__restrict__ diag, const T *__restrict__ Bp, const int *__restrict__ mvp,
+                  int kp0) {
     extern __shared__ __align__(1024) unsigned char stgb[];  // P2_T local rows x 128 B, 128B-swizzled (TMA)
     __shared__ __align__(8) unsigned long long tbar, hbar, xbar[2];
     __shared__ __align__(16) XSlot2 xs[2][P2C_MAX];
@@ -525,18 +672,26 @@ lu_panel2c_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, l
             *reinterpret_cast<double2 *>(stgb + swz128(r, c)) = make_double2(rd[2 * c], rd[2 * c + 1]);
     };
 
-    if (tid == 0) tma_half(0);
-    __syncthreads();
-    mbar_wait_cta(smem_u32(&tbar), 0u);
     const int g = rbeg + tid;  // relative row of this thread
     T a[PH];
     int pst = -1;
     bool live = g < m;
-    row_from_stg(tid, a);
-    __syncthreads();  // the staging buffer is free
-    if (two && tid == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        tma_half(1);
+    const bool fused = Bp != nullptr;
+    __shared__ PreSmem<T, (TWO ? 2 * PH : PH)> psm;
+    if (fused) {
+        // fused look-ahead (see pre_update); rank 0 stores the previous step's U rows
+        pre_update<T, PH, TWO>(Bp, mvp, kp0, B, ld, n, k0, w, g, rank == 0, tid, a, stgb, stgb + P2_T * 128, psm);
+        __syncthreads();
+    } else {
+        if (tid == 0) tma_half(0);
+        __syncthreads();
+        mbar_wait_cta(smem_u32(&tbar), 0u);
+        row_from_stg(tid, a);
+        __syncthreads();  // the staging buffer is free
+        if (two && tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tma_half(1);
+        }
     }
 
     auto publish_first = [&]() {
@@ -647,7 +802,7 @@ lu_panel2c_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, l
     if constexpr (TWO) if (two) {
         // ---- half 1: gather half 0's pivot rows (L11 | X) from their owners, U12 = L11^{-1} X,
         // rank-PH update of this CTA's rows, swap
-        mbar_wait_cta(smem_u32(&tbar), 1u);
+        if (!fused) mbar_wait_cta(smem_u32(&tbar), 1u);
         if (pst >= 0) {
             T x[PH];
             row_from_stg(tid, x);
@@ -1028,7 +1183,10 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
     // ---- 3. the first row block of tiles PRODUCES U12 of its columns (gather of the pivot rows X,
     // TRSM), stores it in Bn's top rows and raises the column block's flag; the other tiles load
     // it from there (L2) once the flag is up, instead of each repeating the TRSM
-    const bool prod = blockIdx.y == 0;
+    // (a grid with a single column tile -- the NEXT kernel -- lets every tile solve for itself:
+    // no hand-off on its critical path)
+    const bool solo = gridDim.x == 1;
+    const bool prod = solo || blockIdx.y == 0;
     if (prod) {
         for (int idx = tid; idx < PW * (U2_TC / E); idx += U2_T) {
             const int i = idx / (U2_TC / E), e = (idx % (U2_TC / E)) * E;
@@ -1063,13 +1221,13 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
                 for (int i = q + 1; i < PW; ++i) x[i] = msub(x[i], L11[i][q], x[q]);
 #pragma unroll
             for (int i = 0; i < PW; ++i) Us[i][tid] = x[i];
-            if (tid < nc) {
+            if (tid < nc && blockIdx.y == 0) {
 #pragma unroll
                 for (int i = 0; i < PW; ++i) Bn[(long long)(k0 + i) * ld + c0 + tid] = x[i];
             }
         }
         __syncthreads();
-        if (tid == 0) {
+        if (tid == 0 && !solo) {
             __threadfence();
             asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(u12f + blockIdx.x), "r"(tag) : "memory");
         }
@@ -1213,8 +1371,8 @@ size_t lu2_int_elems(int n) {
 
 template <typename T, int PH, int R>
 static cudaError_t launch_panel2(const CUtensorMap &tm, T *B, long long ld, int n, int k0, int w, int *mv2, T *diag,
-                                 cudaStream_t s) {
-    const size_t smem = (size_t)R * P2_T * 128 + 1024;
+                                 cudaStream_t s, const T *Bp = nullptr, const int *mvp = nullptr, int kp0 = 0) {
+    const size_t smem = (size_t)(R + 1) * P2_T * 128 + 1024;  // staging + the fused look-ahead's D0 rows
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1230,14 +1388,15 @@ static cudaError_t launch_panel2(const CUtensorMap &tm, T *B, long long ld, int 
     for (int j = 0; j < w; ++j) wk += (double)(n - k0 - j - 1) * (1.0 + 2.0 * (w - j - 1));
     ProfScope ps(sizeof(T) == 8 ? "lu_panel2<double>" : "lu_panel2<double2>", s, wk * (sizeof(T) == 8 ? 1.0 : 4.0));
     return launch_pdl(lu_panel2_kernel<T, PH, R, (Panel2W<T>::PW > PH)>, dim3(1), dim3(P2_T), smem, s, tm, B, ld, n,
-                      k0, w, mv2, diag);
+                      k0, w, mv2, diag, Bp, mvp, kp0);
 }
 
 template <typename T, int PH>
 static cudaError_t launch_panel2c(const CUtensorMap &tm, T *B, long long ld, int n, int k0, int w, int *mv2, T *diag,
-                                  int CS, cudaStream_t s) {
+                                  int CS, cudaStream_t s, const T *Bp = nullptr, const int *mvp = nullptr,
+                                  int kp0 = 0) {
     constexpr bool TWO = Panel2W<T>::PW > PH;
-    const size_t smem = (size_t)P2_T * 128 + 1024;
+    const size_t smem = (size_t)2 * P2_T * 128 + 1024;  // staging + the fused look-ahead's D0 rows
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1265,7 +1424,7 @@ static cudaError_t launch_panel2c(const CUtensorMap &tm, T *B, long long ld, int
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     count_launch();
-    return cudaLaunchKernelEx(&cfg, lu_panel2c_kernel<T, PH, TWO>, tm, B, ld, n, k0, w, mv2, diag);
+    return cudaLaunchKernelEx(&cfg, lu_panel2c_kernel<T, PH, TWO>, tm, B, ld, n, k0, w, mv2, diag, Bp, mvp, kp0);
 }
 
 template <typename T>
@@ -1283,24 +1442,31 @@ template cudaError_t lu2_panel_inplace<double>(const CUtensorMap &, double *, lo
 template cudaError_t lu2_panel_inplace<double2>(const CUtensorMap &, double2 *, long long, int, int, int, int *,
                                                 double2 *, cudaStream_t);
 
-// look-ahead pipeline (default) or panel -> full update per step (env FROB_LU2_LOOKAHEAD=0, A/B aid)
-static bool lu2_lookahead() {
-    static bool v = [] {
+// pipeline mode: 2 = fused look-ahead, 1 = separate NEXT kernels, 0 = panel -> full update per
+// step (env FROB_LU2_LOOKAHEAD overrides, A/B aid).  Measured defaults (B200, n = 1024 / 4096):
+// complex (8-column steps, 64 FMAs per row in the fused update) 2: 2.73 / 38.6 ms vs 3.00 / 44.1
+// with mode 1; real (32-column steps: 1024 FMAs per row on the panel's one or few SMs) 1:
+// 3.45 / 37.9 ms vs 3.88 / 38.9 with mode 2.
+static int lu2_lookahead(bool cplx) {
+    static int v = [] {
         const char *e = getenv("FROB_LU2_LOOKAHEAD");
-        return !(e && e[0] == '0');
+        return e ? atoi(e) : -1;
     }();
-    return v;
+    return v >= 0 ? v : (cplx ? 2 : 1);
 }
 
-// Step k (panel P_k at k0 = k PW) is followed by
-//   NEXT_k: the update of the next panel's PW columns only (+ the step's perm / iperm / snapshot),
-//   BULK_k: the update of every column right of those, launched AFTER P_{k+1} so that it runs
-//           concurrently with it (P_{k+1} releases its dependents right after its own wait).
-// Stream order: P_0 NEXT_0 | P_1 BULK_0 NEXT_1 | P_2 BULK_1 NEXT_2 | ...  Every kernel reads
-// only data its chain of waits has completed: P_{k+1} needs NEXT_k; BULK_k needs P_k and BULK_{k-1}
-// (complete before NEXT_k, its predecessor's predecessor, finished); NEXT_{k+1} waits for BULK_k,
-// whose last CTA waits for P_{k+1}.  P_{k+1} writes columns [k0+PW, k0+2PW) of B_{k+1} and BULK_k
-// columns >= k0 + 2PW: disjoint.
+// Look-ahead pipeline.  Step k (panel P_k at k0 = k PW) is followed by
+//   BULK_k: the update of every column right of the NEXT panel's, launched AFTER P_{k+1} so that
+//           it runs concurrently with it (P_{k+1} releases its dependents right after its own
+//           wait; BULK_k does not wait at entry, its last CTA waits for P_{k+1} before exiting);
+//   the update of the next panel's own PW columns is either fused into P_{k+1} (mode 2, the
+//   default: P_{k+1} reads them from B_k and applies step k's update itself, see pre_update) or a
+//   separate NEXT_k kernel between P_k and P_{k+1} (mode 1).
+// Mode 2 stream order: P_0 | P_1 BULK_0 | P_2 BULK_1 | ...  P_{k+1} waits for BULK_{k-1}, whose
+// completion implies P_k's; BULK_k is released only after that wait, so P_k and BULK_{k-1} are
+// complete when it starts.  P_{k+1} writes columns [k0+PW, k0+2PW) of B_{k+1} (and the U rows of
+// step k there), BULK_k the columns >= k0 + 2PW: disjoint.  BULK_k also applies step k's row moves
+// to perm / iperm and takes the snapshot (in step order: the BULKs are serialised).
 template <typename T>
 cudaError_t lu2_factor(int n, T *B0, T *B1, long long ld, T *U, T *L, long long ldo, int *perm, int *iw, T *diag,
                        LuStats *stats, cudaStream_t s) {
@@ -1322,11 +1488,11 @@ cudaError_t lu2_factor(int n, T *B0, T *B1, long long ld, T *U, T *L, long long 
     if (e != cudaSuccess) return e;
     e = launch_pdl(iota2_kernel, dim3((max(n, nsync) + 255) / 256), dim3(256), 0, s, perm, iperm, n, sync, nsync);
     if (e != cudaSuccess) return e;
-    const bool la = lu2_lookahead();
+    const int la = lu2_lookahead(sizeof(T) == 16);
     const char *nm_next = sizeof(T) == 8 ? "lu_next2<double>" : "lu_next2<double2>";
     const char *nm_bulk = sizeof(T) == 8 ? "lu_update2<double>" : "lu_update2<double2>";
-    // update of step kk over columns [cb, ce)
-    auto update = [&](int kk, int cb, int ce, bool next) -> cudaError_t {
+    // update of step kk over columns [cb, ce); next: waits at entry + perm/iperm/snapshot work
+    auto update = [&](int kk, int cb, int ce, bool next, bool doperm) -> cudaError_t {
         const int k0 = kk * PW, w = min(PW, n - k0), m = n - k0;
         const T *Bk = (kk & 1) ? B1 : B0;
         T *Bn = (kk & 1) ? B0 : B1;
@@ -1337,8 +1503,8 @@ cudaError_t lu2_factor(int n, T *B0, T *B1, long long ld, T *U, T *L, long long 
         ProfScope ps(next ? nm_next : nm_bulk, s, upd * (sizeof(T) == 8 ? 1.0 : 4.0));
         return launch_pdl(lu_update2m_kernel<T, PW>, grid, dim3(U2_T), 0, s, Bk, Bn, ld, n, k0, w,
                           (const int *)(mvb + (size_t)kk * MV2_INTS), perm, iperm,
-                          (next && kk + 1 < steps) ? snap + (size_t)kk * n : (int *)nullptr, next ? flagN : flagB,
-                          kk + 1, cb, ce, next ? 1 : 0, next ? 0 : 1, done + kk);
+                          (doperm && kk + 1 < steps) ? snap + (size_t)kk * n : (int *)nullptr, next ? flagN : flagB,
+                          kk + 1, cb, ce, doperm ? 1 : 0, next ? 0 : 1, done + kk);
     };
     for (int k = 0; k < steps; ++k) {
         const int k0 = k * PW, w = min(PW, n - k0), m = n - k0;
@@ -1346,19 +1512,27 @@ cudaError_t lu2_factor(int n, T *B0, T *B1, long long ld, T *U, T *L, long long 
         int *mv2 = mvb + (size_t)k * MV2_INTS;
         // one CTA up to P2_T rows, else a cluster of ceil(m / P2_T) CTAs (measured: a 2-CTA cluster
         // beats one CTA with two rows per thread at 512 < m <= 1024)
-        if (m > P2_T) e = launch_panel2c<T, PH>(tm[k & 1], Bk, ld, n, k0, w, mv2, diag, (m + P2_T - 1) / P2_T, s);
-        else e = launch_panel2<T, PH, 1>(tm[k & 1], Bk, ld, n, k0, w, mv2, diag, s);
+        // fused look-ahead: P_k reads its columns from B_{k-1} and applies step k-1's update itself
+        const bool fz = la == 2 && k > 0;
+        const T *Bp = fz ? ((k & 1) ? B0 : B1) : nullptr;
+        const int *mvp = fz ? mvb + (size_t)(k - 1) * MV2_INTS : nullptr;
+        if (m > P2_T)
+            e = launch_panel2c<T, PH>(tm[k & 1], Bk, ld, n, k0, w, mv2, diag, (m + P2_T - 1) / P2_T, s, Bp, mvp, k0 - PW);
+        else e = launch_panel2<T, PH, 1>(tm[k & 1], Bk, ld, n, k0, w, mv2, diag, s, Bp, mvp, k0 - PW);
         if (e != cudaSuccess) return e;
-        if (!la) {
-            if ((e = update(k, k0 + w, n, true)) != cudaSuccess) return e;
+        if (la == 0) {
+            if ((e = update(k, k0 + w, n, true, true)) != cudaSuccess) return e;
             continue;
         }
-        if (k >= 1) {  // BULK_{k-1}: columns right of P_k's
+        if (k >= 1) {  // BULK_{k-1}: the columns right of P_k's, concurrent with P_k
             const int cb = k0 + PW;
-            if (cb < n && (e = update(k - 1, cb, n, false)) != cudaSuccess) return e;
+            if ((la == 1 && cb < n) || la == 2)
+                if ((e = update(k - 1, min(cb, n), n, false, la == 2)) != cudaSuccess) return e;
         }
-        if ((e = update(k, k0 + w, min(n, k0 + w + PW), true)) != cudaSuccess) return e;  // NEXT_k
+        if (la == 1 && (e = update(k, k0 + w, min(n, k0 + w + PW), true, true)) != cudaSuccess) return e;  // NEXT_k
     }
+    // fused mode: the last step's row moves still go to perm / iperm
+    if (la == 2 && (e = update(steps - 1, n, n, true, true)) != cudaSuccess) return e;
     {
         const long long total = (long long)n * n;
         const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);
