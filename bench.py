@@ -482,7 +482,8 @@ def main():
             name, d = max(prof.items(), key=lambda kv: kv[1]["total_ms"])
             avg_ms = d["total_ms"] / max(1, d["launches"])
             ach_k = d["flops"] / max(1, d["launches"]) / (avg_ms * 1e-3) / 1e12
-            tensor = name.startswith("gemm")
+            # DMMA kernels: the GEMM engine and lu2's trailing updates (NEXT / BULK)
+            tensor = name.startswith("gemm") or name.startswith("lu_update2") or name.startswith("lu_next2")
             pk, pk_src = (peak, peak_src) if tensor else fp64_alu_peak()
             steps_prof = len(pw) + 1
             traffic = None
@@ -500,7 +501,10 @@ def main():
                 "launches_per_step": d["launches"] / steps_prof,
                 "share_of_step": d["total_ms"] / steps_prof / statistics.median(pw),
                 "note": ("FP64 pipe; the LU panel is a latency-bound pivot chain (one pivot search + "
-                         "rank-1 update per column), so its fraction of the FP64 peak is small by nature"
+                         "rank-1 update per column), so its fraction of the FP64 peak is small by nature; "
+                         "its launch duration includes the programmatic-dependent-launch wait for its "
+                         "predecessor (kernels overlap by design), so share_of_step can exceed the "
+                         "critical-path share"
                          if not tensor else "DMMA tensor pipe")}
             extras["kernel_profile"] = {k: {"launches_per_step": v["launches"] / steps_prof,
                                             "ms_per_step": v["total_ms"] / steps_prof,
