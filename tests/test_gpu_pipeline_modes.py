@@ -1,0 +1,63 @@
+"""GPU parity of the LU pipeline variants that are selected by environment switches (A/B aids,
+read once per process, so each runs in its own subprocess): lu2's look-ahead modes
+(FROB_LU2_LOOKAHEAD = 0 none, 1 separate NEXT kernel, 2 fused into the panel), and the blocked
+getrf with lu2's in-place panels (FROB_LU2_MAX=1024 routes n > 1024 to getrf) against the same
+oracle and bounds as tests/test_gpu_parity.py."""
+import math
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SIZES = (300, 1100)
+
+CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import synth, paper_2208_01239_b200 as fb
+out = {{}}
+for n in {sizes!r}:
+    z = synth.shifted_complex(n, seed=77 * n, shift=n ** 0.5 + 2.0)
+    zt = torch.from_numpy(z).cuda()
+    out[f"frob{{n}}"] = fb.inv(zt).cpu().numpy()
+    out[f"zinv{{n}}"] = fb.zinv(zt).cpu().numpy()
+np.savez({path!r}, **out)
+"""
+
+
+@pytest.fixture(scope="module")
+def refs():
+    r = {}
+    for n in SIZES:
+        z = synth.shifted_complex(n, seed=77 * n, shift=math.sqrt(n) + 2.0)
+        x, info = oracle.zinv_gj(z)
+        assert info == 0
+        r[n] = (z, x)
+    return r
+
+
+@pytest.mark.parametrize("env", [{"FROB_LU2_LOOKAHEAD": "0"}, {"FROB_LU2_LOOKAHEAD": "1"},
+                                 {"FROB_LU2_LOOKAHEAD": "2"}, {"FROB_LU2_MAX": "1024"}],
+                         ids=["lookahead0", "lookahead1", "lookahead2", "getrf"])
+def test_pipeline_mode(env, refs, tmp_path):
+    path = str(tmp_path / "out.npz")
+    code = CHILD.format(root=ROOT, sizes=SIZES, path=path)
+    e = dict(os.environ, **env)
+    p = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    got = np.load(path)
+    for n in SIZES:
+        z, ref = refs[n]
+        for k in ("frob", "zinv"):
+            x = got[f"{k}{n}"]
+            assert oracle.rel_fro(x, ref) <= 1e-10, (env, k, n)
+            r = np.linalg.norm(z @ x - np.eye(n))
+            assert r <= 1e-11 * n, (env, k, n, r)
