@@ -56,8 +56,14 @@ constexpr int LU2_MAX_N = 4096;  // single CTA up to 1024 rows, then a cluster o
 size_t lu2_int_elems(int n);
 // orders that take lu2 (LU2_MAX_N; env FROB_LU2_MAX lowers it: A/B measurement aid)
 int lu2_max_n();
-// lu2's panel width: two 128-byte row halves (32 real / 16 complex columns would spill: 8 complex)
-template <typename T> struct Panel2W { static constexpr int PW = 32, PH = 16; };
+// lu2's panel width: one or two 128-byte row halves (real 16 or 32 columns; complex 8 -- the
+// two-half complex variant spills).  Real 16-column steps with the fused look-ahead measured
+// 3.37 / 9.11 / 38.96 ms at n = 1024 / 2048 / 4096 against 3.33 / 9.02 / 37.22 for 32-column
+// steps with the NEXT kernel: 32 stays.
+#ifndef PANEL2_REAL_PW
+#define PANEL2_REAL_PW 32
+#endif
+template <typename T> struct Panel2W { static constexpr int PW = PANEL2_REAL_PW, PH = 16; };
 template <> struct Panel2W<double2> { static constexpr int PW = 8, PH = 8; };
 // lu2's panel kernels used IN PLACE by the blocked getrf: rows [k0, n) x columns [k0, k0 + w) of A
 // (lda; tm = tma_map_rows128 of A with 256-row boxes) factored, rows written to their final

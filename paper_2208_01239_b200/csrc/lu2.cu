@@ -1452,7 +1452,7 @@ static int lu2_lookahead(bool cplx) {
         const char *e = getenv("FROB_LU2_LOOKAHEAD");
         return e ? atoi(e) : -1;
     }();
-    return v >= 0 ? v : (cplx ? 2 : 1);
+    return v >= 0 ? v : ((cplx || Panel2W<double>::PW == Panel2W<double>::PH) ? 2 : 1);
 }
 
 // Look-ahead pipeline.  Step k (panel P_k at k0 = k PW) is followed by
