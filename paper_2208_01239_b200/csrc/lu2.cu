@@ -25,6 +25,27 @@
 
 namespace frob {
 
+// Kernel timeline tracer (build with -DFROB_TL; tools/lu2_timeline.py): per (kernel kind, step)
+// the earliest CTA start (after its dependency wait) and the latest CTA end, %globaltimer ns.
+#ifdef FROB_TL
+__device__ unsigned long long g_tl_start[5][1024], g_tl_end[5][1024];
+__device__ int g_tl_call;  // LU calls since the last reset (slot = call * 128 + step)
+FROB_DEV unsigned long long tl_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ long long g_nx_tr[2][8];
+#define NXT(i) do { if (gridDim.x == 1 && blockIdx.y <= 1 && threadIdx.x == 0 && k0 == 320) g_nx_tr[blockIdx.y][i] = clock64(); } while (0)
+#define TL_SLOT(step) ((((g_tl_call - 1) & 7) * 128 + (step)) & 1023)
+#define TL_BEGIN(kind, step) do { if (threadIdx.x == 0) atomicMin(&g_tl_start[kind][TL_SLOT(step)], tl_now()); } while (0)
+#define TL_END(kind, step) do { if (threadIdx.x == 0) atomicMax(&g_tl_end[kind][TL_SLOT(step)], tl_now()); } while (0)
+#else
+#define TL_BEGIN(kind, step) do { } while (0)
+#define TL_END(kind, step) do { } while (0)
+#define NXT(i) do { } while (0)
+#endif
+
 constexpr int P2_T = 512;
 constexpr int P2_WARPS = P2_T / 32;
 constexpr int P2_STG = 18;  // staging row stride in doubles (16 + 2: 16-byte aligned, conflict free)
@@ -237,6 +258,7 @@ lu_panel2_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, lo
     }
     pdl_wait();
     pdl_trigger();  // after the wait: the BULK update launched behind this panel relies on it
+    TL_BEGIN(0, k0 / Panel2W<T>::PW);
     P2T(0);
     constexpr int PW = 2 * PH;                     // panel width in elements
     __shared__ unsigned long long ck[2][P2_WARPS];
@@ -565,6 +587,7 @@ lu_panel2_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, lo
         if (grow[q] < m) row_to_stg(mydst[q], a[q]);
     __syncthreads();
     write_half(two ? 1 : 0, false);
+    TL_END(0, k0 / Panel2W<T>::PW);
     P2T(21);
 }
 
@@ -640,6 +663,7 @@ lu_panel2c_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, l
     }
     pdl_wait();
     pdl_trigger();  // after the wait (see lu2_factor)
+    TL_BEGIN(1, k0 / Panel2W<T>::PW);
 #define P2CT(i) do { if (rank == 0) P2T(i); } while (0)
 #define P2CTJ(j, i) do { if ((j) == 5) P2CT(i); } while (0)
     P2CT(0);
@@ -924,6 +948,7 @@ lu_panel2c_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, l
     if (g < m) row_to_stg(tid, a);
     __syncthreads();
     write_half(two ? 1 : 0);
+    TL_END(1, k0 / Panel2W<T>::PW);
     P2CT(21);
 #undef P2CT
 #undef P2CTJ
@@ -1118,6 +1143,7 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
     const bool tile = c0 < cend;
     const bool rows = tile && r0 < n;
     const int nc = min(U2_TC, cend - c0);
+    NXT(0);
     // ---- 1. requests independent of the move list
     if (tile) {
         for (int idx = tid; idx < PW * (PW / E); idx += U2_T) {
@@ -1159,6 +1185,10 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
         }
     }
     // ---- 2. the move list
+    // source rows of this tile's rows [r0, r0 + U2_TR) and of the top rows [k0, k0 + PW): identity,
+    // then the step's moves applied once (instead of a search of the move list per row)
+    __shared__ int rmap[U2_TR + PW];
+    if (tid < U2_TR + PW) rmap[tid] = (tid < U2_TR) ? r0 + tid : k0 + (tid - U2_TR);
     if (tid < MV2_MAX) {
         const int nm = mv2[0];
         if (tid == 0) nmv_s = nm;
@@ -1167,6 +1197,13 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
     }
     __syncthreads();
     const int nm = nmv_s;
+    if (tid < nm) {
+        const int d = mdst[tid];
+        if (d >= r0 && d < r0 + U2_TR) rmap[d - r0] = msrc[tid];
+        else if (d >= k0 && d < k0 + PW) rmap[U2_TR + d - k0] = msrc[tid];
+    }
+    __syncthreads();
+    NXT(1);
     if (doperm && blockIdx.x == 0 && blockIdx.y == 0) {
         int pv = 0;
         if (tid < nm) pv = perm[msrc[tid]];
@@ -1190,9 +1227,7 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
     if (prod) {
         for (int idx = tid; idx < PW * (U2_TC / E); idx += U2_T) {
             const int i = idx / (U2_TC / E), e = (idx % (U2_TC / E)) * E;
-            int src = k0 + i;
-            for (int q = 0; q < nm; ++q)
-                if (mdst[q] == k0 + i) src = msrc[q];
+            const int src = rmap[U2_TR + i];
             if (e < nc) cp_async16(&Us[i][e], Bk + (long long)src * ld + c0 + e);
         }
     }
@@ -1201,14 +1236,13 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
             const int r = r0 + wm0 + i * 8 + g;
-            int src = r;
-            for (int q = 0; q < nm; ++q)
-                if (mdst[q] == r) src = msrc[q];
+            const int src = rmap[wm0 + i * 8 + g];
             if (src != r && r < n) load_c(i, Bk + (long long)src * ld + c0);
         }
     }
     cp_async_wait<0>();
     __syncthreads();
+    NXT(2);
     if (prod) {
         // ---- 4. U12 = L11^{-1} X (unit lower forward substitution), one thread per column
         if (tid < U2_TC) {
@@ -1251,6 +1285,7 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
         cp_async_wait<0>();
         __syncthreads();
     }
+    NXT(3);
     if (!rows) return;
     // ---- 5. C += (-L21) U12 on the tensor pipe
 #pragma unroll
@@ -1280,6 +1315,7 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
             }
         }
     }
+    NXT(5);
 }
 
 
@@ -1298,7 +1334,9 @@ lu_update2m_kernel(const T *__restrict__ Bk, T *__restrict__ Bn, long long ld, i
                    int lookahead, int *__restrict__ done_ctr) {
     pdl_trigger();
     if (!lookahead) pdl_wait();
+    TL_BEGIN(lookahead ? 3 : 2, k0 / PW);
     update2m_body<T, PW>(Bk, Bn, ld, n, k0, w, mv2, perm, iperm, snap, u12f, tag, cbeg, cend, doperm);
+    TL_END(lookahead ? 3 : 2, k0 / PW);
     if (lookahead) {
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -1345,6 +1383,9 @@ __global__ void iota2_kernel(int *p, int *q, int n, int *flags, int nflags) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) { p[i] = i; q[i] = i; }
     if (flags && i < nflags) flags[i] = 0;
+#ifdef FROB_TL
+    if (flags && i == 0) atomicAdd(&g_tl_call, 1);
+#endif
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1548,4 +1589,22 @@ template cudaError_t lu2_factor<double>(int, double *, double *, long long, doub
 template cudaError_t lu2_factor<double2>(int, double2 *, double2 *, long long, double2 *, double2 *, long long,
                                          int *, int *, double2 *, LuStats *, cudaStream_t);
 
+#ifdef FROB_TL
+extern "C" int frob_tl_reset() {
+    static unsigned long long s[5][1024], z[5][1024];
+    for (auto &a : s) for (auto &v : a) v = ~0ull;
+    for (auto &a : z) for (auto &v : a) v = 0ull;
+    if (cudaMemcpyToSymbol(g_tl_start, s, sizeof(s)) != cudaSuccess) return 1;
+    const int zero = 0;
+    if (cudaMemcpyToSymbol(g_tl_call, &zero, sizeof(int)) != cudaSuccess) return 1;
+    return cudaMemcpyToSymbol(g_tl_end, z, sizeof(z)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int frob_nx_read(long long *out) {
+    return cudaMemcpyFromSymbol(out, g_nx_tr, sizeof(g_nx_tr)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int frob_tl_read(unsigned long long *start, unsigned long long *end) {
+    if (cudaMemcpyFromSymbol(start, g_tl_start, sizeof(g_tl_start)) != cudaSuccess) return 1;
+    return cudaMemcpyFromSymbol(end, g_tl_end, sizeof(g_tl_end)) == cudaSuccess ? 0 : 1;
+}
+#endif
 }  // namespace frob
