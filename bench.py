@@ -488,8 +488,11 @@ def main():
             steps_prof = len(pw) + 1
             traffic = None
             try:  # DRAM bytes per launch from this round's committed ncu --set full capture
+                # (captured at n = 1024, the config 2 default, and at n = 4096 under "<name> n=4096")
                 with open(os.path.join(ROOT, "profiles", "r01", "dram_traffic.json")) as f:
-                    tr = json.load(f).get(name)
+                    tab = json.load(f)
+                wn = getattr(wl, "n", None)
+                tr = tab.get(name) if wn == 1024 else tab.get(f"{name} n={wn}")
                 if tr and "batched" not in name:
                     traffic = tr["bytes_per_launch"]
             except Exception:
