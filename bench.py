@@ -7,7 +7,8 @@ the C ABI (frob_inv, AUTO branch).  One "step" = one full inversion (all SURVEY 
 a0-a7).  Inputs (16 MiB) are smaller than L2, so L2 is flushed (256 MiB write) between
 timed steps, outside the CUDA-event pairs.
 
-Other workloads (--config): 3 = batched 65536 x n=32 + 16384 x n=128 (one step = both
+Other workloads (--config): 1 = one n=64 matrix (the line adds a latency table: both branches,
+AUTO, complex LU and the batched kernels, warm and cold L2); 3 = batched 65536 x n=32 + 16384 x n=128 (one step = both
 sub-batches, sharded across ranks); 4 = matrix sign by Newton, n=2048 (one step = one
 full Newton solve, one instance per rank); 5 = one large matrix (--n, default 4096).
 
@@ -17,7 +18,7 @@ GEMM engine, the CPU oracle baseline (rank 0, N=1) and an end-to-end number with
 buffers.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config 2|3|4|5] [--n N]
+                  [--config 1|2|3|4|5] [--n N]
 Multi-GPU (torchrun): independent problems per rank (instances: seed + rank; batches:
 contiguous index shards), no data-path collective, "scaling": "weak"; time = max over ranks.
 """
@@ -49,7 +50,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
@@ -161,7 +162,8 @@ class SingleMatrix(Workload):
         self.flops = 10.0 * n ** 3
         self.flush = 16 * n * n * 2 < 128 * 2 ** 20
         self.n_ref = n
-        self.label = (f"config{2 if n == 1024 else 5}: single complex FP64 matrix n={n}, "
+        cfg = 1 if n == 64 else (2 if n == 1024 else 5)
+        self.label = (f"config{cfg}: single complex FP64 matrix n={n}, "
                       f"A=G1+sqrt(n)I, B=G2, Frobenius (Alg 1), AUTO branch")
 
     def step(self):
@@ -278,8 +280,8 @@ def run_reference(args, rank):
     import oracle
     import synth
     oracle.build()
-    if args.config in (2, 5):
-        n = args.n or (1024 if args.config == 2 else 4096)
+    if args.config in (1, 2, 5):
+        n = args.n or {1: 64, 2: 1024, 5: 4096}[args.config]
         z = synth.config2(n, seed=0)
         work = lambda: oracle.frob_inv(z)  # noqa: E731
         units, label = 1, f"config{args.config}: single complex FP64 matrix n={n}, Frobenius (Alg 1)"
@@ -369,8 +371,8 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     fbi.load()
 
-    if args.config in (2, 5):
-        wl = SingleMatrix(fb, torch, dev, args.n or (1024 if args.config == 2 else 4096),
+    if args.config in (1, 2, 5):
+        wl = SingleMatrix(fb, torch, dev, args.n or {1: 64, 2: 1024, 5: 4096}[args.config],
                           fdist.instance_seed(0, rank), "")
     elif args.config == 3:
         wl = Batched(fb, torch, dev, rank, ws)
@@ -431,6 +433,18 @@ def main():
         ratio = t_inv / t_mult
         r_z = t_zinv / t_inv
         lam = 1.0
+        if n <= 64:
+            # BASELINE config 1: latency of both branches, AUTO, complex LU and the
+            # batched kernels on one matrix; median of 100 after 10 warm-ups, warm and cold L2
+            lat = {}
+            zb = zr[None].contiguous()
+            cases = {"frob_auto": lambda: fb.inv(zr, out=xr), "frob_branch_a": lambda: fb.inv(zr, out=xr, branch="a"),
+                     "frob_branch_b": lambda: fb.inv(zr, out=xr, branch="b"), "zinv_lu": lambda: fb.zinv(zr, out=xr),
+                     "frob_batched_kernel": lambda: fb.inv_batched(zb), "zinv_batched_kernel": lambda: fb.zinv_batched(zb)}
+            for nm_, f_ in cases.items():
+                lat[nm_] = {"warm_l2_us": 1e3 * statistics.median(timed(f_, 100, 10, False)),
+                            "cold_l2_us": 1e3 * statistics.median(timed(f_, 100, 10, True))}
+            extras["latency_config1"] = lat
         extras["comparison_single_n"] = {
             "n": n, "frobenius_ms": t_frob, "zinv_lu_ms": t_zinv,
             "frobenius_tflops_alg": 10.0 * n ** 3 / t_frob / 1e9, "zinv_lu_tflops_alg": 8.0 * n ** 3 / t_zinv / 1e9,

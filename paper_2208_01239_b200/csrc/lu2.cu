@@ -464,7 +464,9 @@ lu_panel2_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, lo
 
     if constexpr (TWO) if (two) {
         // ---- half 1: U12 = L11^{-1} X from half 0's pivot rows, rank-PH update, swap
+        P2T(30);
         if (!fused) mbar_wait_cta(smem_u32(&tbar), 1u);
+        P2T(31);
 #pragma unroll
         for (int q = 0; q < R; ++q)
             if (pst[q] >= 0) {
@@ -489,6 +491,7 @@ lu_panel2_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, lo
             for (int j = 0; j < PH; ++j) U12s[j][tid] = x[j];
         }
         __syncthreads();
+        P2T(33);
 #pragma unroll
         for (int q = 0; q < R; ++q) {
             const int g = grow[q];
@@ -511,6 +514,7 @@ lu_panel2_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, lo
             for (int c = 0; c < PH; ++c) a[q][c] = x[c];
         }
         __syncthreads();
+        P2T(34);
         publish_first();
         run_half(PH, w - PH);
         __syncthreads();

@@ -174,6 +174,8 @@ void pieces(int n) {
         printf("   trace: load %lld | cols:", tr[1] - tr[0]);
         for (int j = 0; j < PW; ++j) printf(" %lld", tr[2 + j] - (j ? tr[1 + j] : tr[1]));
         printf(" | tail %lld | store %lld\n", tr[20] - tr[1 + PW], tr[21] - tr[20]);
+        printf("   transition: wait %lld  fill+solve %lld  update+swap %lld | half1 %lld | tail %lld\n", tr[31] - tr[30],
+               tr[33] - tr[31], tr[34] - tr[33], tr[20] - tr[34], tr[21] - tr[20]);
         printf("   col5: pre-bar %lld bar %lld argmax+row %lld l+next %lld cand+redux %lld rest %lld publish %lld\n",
                tr[40] - tr[6], tr[41] - tr[40], tr[42] - tr[41], tr[43] - tr[42], tr[44] - tr[43], tr[45] - tr[44], tr[7] - tr[45]);
     }
