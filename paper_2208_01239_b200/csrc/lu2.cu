@@ -1248,20 +1248,35 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
     __syncthreads();
     NXT(2);
     if (prod) {
-        // ---- 4. U12 = L11^{-1} X (unit lower forward substitution), one thread per column
-        if (tid < U2_TC) {
-            T x[PW];
+        // ---- 4. U12 = L11^{-1} X (unit lower forward substitution): four threads per column (rows
+        // part, part + 4, ...), x_q passed along the quad by shuffle -- a 4x shorter chain per thread
+        {
+            static_assert(U2_T == 4 * U2_TC, "four threads per column");
+            constexpr int RP = PW / 4;
+            const int c = tid >> 2, part = tid & 3;
+            T x[RP];
 #pragma unroll
-            for (int i = 0; i < PW; ++i) x[i] = Us[i][tid];
+            for (int ii = 0; ii < RP; ++ii) x[ii] = Us[part + 4 * ii][c];
 #pragma unroll
-            for (int q = 0; q < PW; ++q)
+            for (int q = 0; q < PW; ++q) {
+                T xq;
+                if constexpr (sizeof(T) == 8) {
+                    xq = __shfl_sync(0xffffffffu, x[q >> 2], (lane & ~3) | (q & 3));
+                } else {
+                    xq.x = __shfl_sync(0xffffffffu, x[q >> 2].x, (lane & ~3) | (q & 3));
+                    xq.y = __shfl_sync(0xffffffffu, x[q >> 2].y, (lane & ~3) | (q & 3));
+                }
 #pragma unroll
-                for (int i = q + 1; i < PW; ++i) x[i] = msub(x[i], L11[i][q], x[q]);
+                for (int ii = (q >> 2); ii < RP; ++ii) {
+                    const int i = part + 4 * ii;
+                    if (i > q) x[ii] = msub(x[ii], L11[i][q], xq);
+                }
+            }
 #pragma unroll
-            for (int i = 0; i < PW; ++i) Us[i][tid] = x[i];
-            if (tid < nc && blockIdx.y == 0) {
+            for (int ii = 0; ii < RP; ++ii) Us[part + 4 * ii][c] = x[ii];
+            if (c < nc && blockIdx.y == 0) {
 #pragma unroll
-                for (int i = 0; i < PW; ++i) Bn[(long long)(k0 + i) * ld + c0 + tid] = x[i];
+                for (int ii = 0; ii < RP; ++ii) Bn[(long long)(k0 + part + 4 * ii) * ld + c0 + c] = x[ii];
             }
         }
         __syncthreads();
