@@ -1128,7 +1128,8 @@ template <> struct U2MinB<double2> { static constexpr int B = 2; };
 template <typename T, int PW>
 FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long long ld, int n, int k0, int w,
                             const int *__restrict__ mv2, int *__restrict__ perm, int *__restrict__ iperm,
-                            int *__restrict__ snap, int *__restrict__ u12f, int tag, int cbeg, int cend, int doperm) {
+                            int *__restrict__ snap, int *__restrict__ u12f, int tag, int cbeg, int cend, int doperm,
+                            bool stream) {
     constexpr int SP = U2Pad<T>::P;
     constexpr int E = 16 / (int)sizeof(T);
     constexpr int WM = U2_TR / U2M_WGM, WN = U2_TC / U2M_WGN, MT = WM / 8, NT = WN / 8;
@@ -1169,7 +1170,9 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
             const int cc = wn0 + j * 8 + 2 * t;
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const T v = (cc + e < nc) ? src[cc + e] : zero_of(T());
+                // (BULK: streaming loads -- evict-first in L2, so the trailing matrix passing through
+                // does not push the concurrently running panel's code and columns out of L2)
+                const T v = (cc + e < nc) ? (stream ? __ldcs(src + cc + e) : src[cc + e]) : zero_of(T());
                 if constexpr (sizeof(T) == 8) acc[i][j][e] = acc_re(v);
                 else { acc[i][j][e] = acc_re(v); acc[i][j][2 + e] = acc_im(v); }
             }
@@ -1325,7 +1328,11 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
         for (int j = 0; j < NT; ++j) {
             const int cc = wn0 + j * 8 + 2 * t;
             if constexpr (sizeof(T) == 8) {
-                if (cc + 1 < nc) *reinterpret_cast<double2 *>(dst + cc) = make_double2(acc[i][j][0], acc[i][j][1]);
+                if (cc + 1 < nc) {
+                    const double2 v2 = make_double2(acc[i][j][0], acc[i][j][1]);
+                    if (stream) __stcs(reinterpret_cast<double2 *>(dst + cc), v2);
+                    else *reinterpret_cast<double2 *>(dst + cc) = v2;
+                }
                 else if (cc < nc) dst[cc] = acc[i][j][0];
             } else {
 #pragma unroll
@@ -1354,7 +1361,8 @@ lu_update2m_kernel(const T *__restrict__ Bk, T *__restrict__ Bn, long long ld, i
     pdl_trigger();
     if (!lookahead) pdl_wait();
     TL_BEGIN(lookahead ? 3 : 2, k0 / PW);
-    update2m_body<T, PW>(Bk, Bn, ld, n, k0, w, mv2, perm, iperm, snap, u12f, tag, cbeg, cend, doperm);
+    update2m_body<T, PW>(Bk, Bn, ld, n, k0, w, mv2, perm, iperm, snap, u12f, tag, cbeg, cend, doperm,
+                         lookahead && n > 2048);
     TL_END(lookahead ? 3 : 2, k0 / PW);
     if (lookahead) {
         __syncthreads();
