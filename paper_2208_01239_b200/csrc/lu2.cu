@@ -1122,7 +1122,9 @@ constexpr int U2M_WGM = 2, U2M_WGN = 4;
 template <typename T> struct U2Pad { static constexpr int P = 4; };   // row offset = 8 words mod 32
 template <> struct U2Pad<double2> { static constexpr int P = 2; };
 
-template <typename T> struct U2MinB { static constexpr int B = 2; };
+// CTAs per SM: real 3 (80 registers since the U12 solve went to four threads per column;
+// n = 4096 BULK step 95 -> 77 us at m = 4096), complex 2
+template <typename T> struct U2MinB { static constexpr int B = 3; };
 template <> struct U2MinB<double2> { static constexpr int B = 2; };
 
 template <typename T, int PW>
