@@ -1170,10 +1170,19 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
             const int cc = wn0 + j * 8 + 2 * t;
+            // (BULK: streaming loads -- evict-first in L2, so the trailing matrix passing through
+            // does not push the concurrently running panel's code and columns out of L2)
+            if constexpr (sizeof(T) == 8) {
+                if (cc + 1 < nc) {  // one 16-byte load (cc even, rows 16-byte aligned)
+                    const double2 *p2 = reinterpret_cast<const double2 *>(src + cc);
+                    const double2 v = stream ? __ldcs(p2) : *p2;
+                    acc[i][j][0] = v.x;
+                    acc[i][j][1] = v.y;
+                    continue;
+                }
+            }
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                // (BULK: streaming loads -- evict-first in L2, so the trailing matrix passing through
-                // does not push the concurrently running panel's code and columns out of L2)
                 const T v = (cc + e < nc) ? (stream ? __ldcs(src + cc + e) : src[cc + e]) : zero_of(T());
                 if constexpr (sizeof(T) == 8) acc[i][j][e] = acc_re(v);
                 else { acc[i][j][e] = acc_re(v); acc[i][j][2 + e] = acc_im(v); }
