@@ -838,6 +838,7 @@ lu_panel2c_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, l
             st_row_smem<T, PH>(obox[1][pst], x);
         }
         __syncthreads();
+        P2CT(22);
         {
             const unsigned hb = smem_u32(&hbar);
             for (int task = tid; task < PH * CS * 16; task += P2_T) {
@@ -849,7 +850,9 @@ lu_panel2c_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, l
                 st_async_16b(mapa_u32(dst, (unsigned)r), v, mapa_u32(hb, (unsigned)r));
             }
         }
+        P2CT(23);
         mbar_wait_parity(smem_u32(&hbar), 0u);
+        P2CT(24);
         if (tid < PH) {
             T x[PH];
 #pragma unroll
@@ -862,6 +865,7 @@ lu_panel2c_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, l
             for (int j = 0; j < PH; ++j) U12s[j][tid] = x[j];
         }
         __syncthreads();
+        P2CT(25);
         if (g < m) {
             T x[PH];
             row_from_stg(tid, x);

@@ -192,6 +192,8 @@ void pieces(int n) {
         printf("   trace: load %lld half0 %lld trans %lld half1 %lld tail %lld | cols(half1):", tr[1] - tr[0], tr[19] - tr[1],
                tr[18] - tr[19], tr[20] - tr[18], tr[21] - tr[20]);
         for (int j = 1; j < PH; ++j) printf(" %lld", tr[2 + j] - tr[1 + j]);
+        printf("\n   trans: obox %lld push %lld hwait %lld solve %lld update %lld",
+               tr[22] - tr[19], tr[23] - tr[22], tr[24] - tr[23], tr[25] - tr[24], tr[18] - tr[25]);
         printf("\n   col5: pre-bar %lld push %lld deferred %lld wait %lld argmax+row %lld mult %lld cand+pub %lld\n",
                tr[40] - tr[6], tr[41] - tr[40], tr[42] - tr[41], tr[43] - tr[42], tr[44] - tr[43], tr[45] - tr[44], tr[7] - tr[45]);
 #endif
