@@ -334,6 +334,29 @@ def cpu_baseline(args, wl):
             if time.perf_counter() - t0 > 10.0 or cnt >= 20:
                 break
         sample = f"{cnt} oracle frob_inv calls (plain C, OpenMP) on the same n={wl.n} input"
+        dt_all = time.perf_counter() - t0
+        # the complex Gauss-Jordan oracle timed separately, and one thread at n <= 1024
+        extra = {}
+        t1, c1 = time.perf_counter(), 0
+        while True:
+            oracle.zinv_gj(wl.z_np)
+            c1 += 1
+            if time.perf_counter() - t1 > 5.0 or c1 >= 20:
+                break
+        extra["zinv_gj_oracle_per_s"] = c1 / (time.perf_counter() - t1)
+        if wl.n <= 1024:
+            nt = oracle.num_threads()
+            oracle.set_threads(1)
+            t1, c1 = time.perf_counter(), 0
+            while True:
+                oracle.frob_inv(wl.z_np)
+                c1 += 1
+                if time.perf_counter() - t1 > 5.0 or c1 >= 5:
+                    break
+            extra["frob_oracle_1thread_per_s"] = c1 / (time.perf_counter() - t1)
+            oracle.set_threads(nt)
+        return {"value": cnt / dt_all, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                "sample": sample, **extra}
     elif isinstance(wl, Batched):
         zs = synth.batch(32, 4096, seed=0)
         for m in zs:

@@ -68,12 +68,19 @@ def lib():
                 getattr(L, f).restype = ctypes.c_int
             L.or_dgetri_solve.restype = None
             L.or_dgemm.restype = None
+            L.or_set_threads.argtypes = [ctypes.c_int]
+            L.or_set_threads.restype = None
             _lib = L
     return _lib
 
 
 def num_threads() -> int:
     return int(lib().or_num_threads())
+
+
+def set_threads(t: int) -> None:
+    """OpenMP thread count of the oracle's loops (timing control; results do not depend on it)."""
+    lib().or_set_threads(int(t))
 
 
 def _p(a: np.ndarray, ct=ctypes.c_double):

@@ -600,6 +600,18 @@ done:
     return info;
 }
 
+/* thread count of the OpenMP loops (measurement control only: the arithmetic of every row is
+   independent of it) */
+void or_set_threads(int t)
+{
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    if (t > 0) omp_set_num_threads(t);
+#else
+    (void)t;
+#endif
+}
+
 int or_num_threads(void)
 {
 #ifdef _OPENMP
