@@ -210,6 +210,18 @@ def test_frob_inv_rand_mu_zero_and_invalid():
 
 
 # ------------------------------------------------------------------ bitwise invariants
+@pytest.mark.parametrize("n", [513, 1500, 2048])
+def test_repeat_runs_bitwise_pipeline(n):
+    """The look-ahead pipeline (cluster panels, NEXT / BULK updates synchronised by flags and
+    programmatic launches) and the split-K GEMMs are deterministic: repeated calls agree bitwise
+    (a race in the pipeline would not)."""
+    zt = _t(synth.config2(n, seed=n))
+    for f in (fb.inv, fb.zinv):
+        ref = f(zt)
+        for _ in range(3):
+            assert torch.equal(f(zt), ref), (f.__name__, n)
+
+
 def test_bitwise_invariants():
     z = synth.shifted_complex(200, seed=3, shift=16.0)
     x = _np(fb.inv(_t(z), branch="a"))
