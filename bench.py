@@ -483,7 +483,9 @@ def main():
             # config-3 n = 32 shard, and n = 64 from the same generator (crossover evidence)
             cmp = {}
             z64 = torch.from_numpy(synth.batch(64, 16384, seed=0)).to(dev)
-            for nn, zz in ((32, wl.parts[0][1]), (64, z64)):
+            # (n = 128: the complex comparator needs a 2-CTA cluster per matrix -- a complex 128 x 128
+            # matrix fits neither one SM's registers nor its shared memory; the real ones do)
+            for nn, zz in ((32, wl.parts[0][1]), (64, z64), (128, wl.parts[1][1])):
                 tb_f = statistics.median(timed(lambda: fb.inv_batched(zz), 3, 1, False))
                 tb_z = statistics.median(timed(lambda: fb.zinv_batched(zz), 3, 1, False))
                 cnt = int(zz.shape[0])

@@ -134,6 +134,10 @@ frob_status frob_inv_batched(int n, int batch, const double *Z, long long stride
                              unsigned char *d_branch_used, void *ws, size_t ws_bytes,
                              void *stream);
 
+/* Batched complex-LU comparator (complex Gauss-Jordan with partial pivoting, |re|+|im|),
+ * 1 <= n <= 128: one CTA per matrix for n <= 64, a cluster of two CTAs (rows split, pivot
+ * candidates and pivot rows exchanged through distributed shared memory) for 64 < n <= 128.
+ * Layout, strides and d_info as frob_inv_batched. */
 size_t zinv_lu_batched_workspace_bytes(int n, int batch);
 frob_status zinv_lu_batched(int n, int batch, const double *Z, long long strideZ,
                             double *X, long long strideX, int *d_info, void *ws,

@@ -663,6 +663,168 @@ zinv_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__rest
     if (tid == 0) info[b] = inf;
 }
 
+
+// ----------------------------------------------------------------- complex GJ, 64 < n <= 128
+// A complex 128 x 128 matrix (256 KB) fits neither one SM's registers nor its shared memory, so
+// the comparator runs each matrix on a CLUSTER of two 512-thread CTAs: CTA c holds rows
+// [64c, 64c + 64) in registers (4 x 4 complex blocks per thread, as the one-CTA kernels).  Per
+// Gauss-Jordan step: candidates of column k, CTA argmax, cluster barrier, both CTAs read both
+// CTA candidates (DSMEM) and take the same pivot; the pivot row's owner writes the scaled row,
+// cluster barrier, the other CTA reads it through DSMEM; uniform exchange-form update.
+struct ZC128Smem {
+    double2 colk[2][128];
+    double2 rowp[2][128];
+    unsigned long long candk[2][16];
+    int candi[2][16];
+    unsigned long long cbk[2];
+    int cbi[2];
+    int pivrow[128];
+    int pos[128];
+    double pmag_k[128];
+};
+FROB_DEV unsigned long long ldc_u64(unsigned addr) {
+    unsigned long long v;
+    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+    return v;
+}
+FROB_DEV int ldc_s32(unsigned addr) {
+    int v;
+    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(512, 1)
+zinv_batched128c_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__restrict__ X, long long sX,
+                        int n, int *__restrict__ info) {
+    constexpr int N = 128, BR = 4, BC = 4, CT = N / BC;  // 32 column-threads x 16 row-threads
+    __shared__ ZC128Smem sm;
+    const int tid = threadIdx.x, lane = tid & 31;
+    unsigned rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const long long b = blockIdx.x >> 1;
+    const double2 *Zb = Z + b * sZ;
+    double2 *Xb = X + b * sX;
+    const int ti = tid / CT, tj = tid % CT;
+    const int rb = (int)rank * 64;        // first global row of this CTA
+    const int r0 = rb + ti * BR, c0 = tj * BC;
+    double2 a[BR][BC];
+#pragma unroll
+    for (int q = 0; q < BR; ++q)
+#pragma unroll
+        for (int c = 0; c < BC; ++c) {
+            const int i = r0 + q, j = c0 + c;
+            a[q][c] = (i < n && j < n) ? Zb[(long long)i * n + j] : make_double2(i == j ? 1.0 : 0.0, 0.0);
+        }
+    if (tid < N) sm.pos[tid] = 0;
+    __syncthreads();
+    cluster_sync_all();
+    const unsigned other = rank ^ 1u;
+    auto step = [&](const int k, auto KCc) {
+        constexpr int KC = decltype(KCc)::value;
+        const int par = k & 1;
+        const bool owner = (tj == k / BC);
+        // (1) candidates of column k among this CTA's unused rows
+        if (owner) {
+            unsigned long long bk = 0;
+            int bi = INT_MAX;
+#pragma unroll
+            for (int q = 0; q < BR; ++q) {
+                const int r = r0 + q;
+                const double2 v = a[q][KC];
+                sm.colk[par][r] = v;
+                if (r < n && !sm.pos[r]) {
+                    const unsigned long long kk = pkey_bits(v);
+                    if (kk > bk) { bk = kk; bi = r; }
+                }
+            }
+            sm.candk[par][ti] = bk;
+            sm.candi[par][ti] = bi;
+        }
+        __syncthreads();
+        if (tid < 32) {
+            const ArgMaxK m = warp_argmax_key(lane < 16 ? sm.candk[par][lane] : 0ull, lane < 16 ? sm.candi[par][lane] : INT_MAX);
+            if (lane == 0) { sm.cbk[par] = m.k; sm.cbi[par] = m.i; }
+        }
+        cluster_sync_all();
+        // (2) the cluster's pivot (max key, then the smallest row); the owner scales its row
+        unsigned long long k0 = sm.cbk[par], k1 = ldc_u64(mapa_u32(smem_u32(&sm.cbk[par]), other));
+        int i0 = sm.cbi[par], i1 = ldc_s32(mapa_u32(smem_u32(&sm.cbi[par]), other));
+        if (rank == 1) { const unsigned long long tk = k0; k0 = k1; k1 = tk; const int tt = i0; i0 = i1; i1 = tt; }
+        const int p = (k1 > k0 || (k1 == k0 && i1 < i0)) ? i1 : i0;
+        const unsigned prank = (unsigned)(p >> 6);
+        const double2 piv = (prank == rank) ? sm.colk[par][p]
+                                            : ld_cluster(mapa_u32(smem_u32(&sm.colk[par][p]), prank), double2());
+        const double2 ip = is_zero(piv) ? zero_of(double2()) : recip(piv);
+        if (tid == 0) { sm.pivrow[k] = p; sm.pmag_k[k] = pmag(piv); sm.pos[p] = 1; }
+        if (prank == rank && ti == (p - rb) / BR) {
+            const int q = (p - rb) % BR;
+#pragma unroll
+            for (int c = 0; c < BC; ++c) {
+                double2 v = a[0][c];
+#pragma unroll
+                for (int qq = 1; qq < BR; ++qq)
+                    if (q == qq) v = a[qq][c];
+                sm.rowp[par][c0 + c] = (owner && c == KC) ? ip : mul(v, ip);
+            }
+        }
+        cluster_sync_all();
+        // (3) uniform exchange-form update (the owner of column k zeroes it first; the pivot row
+        // is written last)
+        double2 rp[BC], ck[BR];
+        if (prank == rank) {
+#pragma unroll
+            for (int c = 0; c < BC; ++c) rp[c] = sm.rowp[par][c0 + c];
+        } else {
+            const unsigned base = mapa_u32(smem_u32(&sm.rowp[par][c0]), prank);
+#pragma unroll
+            for (int c = 0; c < BC; ++c) rp[c] = ld_cluster(base + c * 16u, double2());
+        }
+#pragma unroll
+        for (int q = 0; q < BR; ++q) ck[q] = sm.colk[par][r0 + q];
+        if (owner) {
+#pragma unroll
+            for (int q = 0; q < BR; ++q) a[q][KC] = zero_of(double2());
+        }
+#pragma unroll
+        for (int q = 0; q < BR; ++q)
+#pragma unroll
+            for (int c = 0; c < BC; ++c) a[q][c] = msub(a[q][c], ck[q], rp[c]);
+        if (prank == rank && ti == (p - rb) / BR) {
+#pragma unroll
+            for (int q = 0; q < BR; ++q)
+                if (r0 + q == p) {
+#pragma unroll
+                    for (int c = 0; c < BC; ++c) a[q][c] = rp[c];
+                }
+        }
+    };
+    for (int kb = 0; kb * BC < n; ++kb) {
+        bstatic_for<BC>([&](auto KCc) {
+            constexpr int KC = decltype(KCc)::value;
+            const int k = kb * BC + KC;
+            if (k < n) step(k, KCc);
+        });
+    }
+    __syncthreads();
+    double pmax, pmin;
+    sweep_finish<double2, N, 512>(sm, n, pmax, pmin);
+    const int inf = sweep_info<double2, N>(sm, n, pmax);
+    // exchange form -> inverse: X[pos[i]][pivrow[j]] = a(i, j)
+#pragma unroll
+    for (int q = 0; q < BR; ++q) {
+        const int i = r0 + q;
+        if (i >= n) continue;
+        const int orow = sm.pos[i];
+#pragma unroll
+        for (int c = 0; c < BC; ++c) {
+            const int j = c0 + c;
+            if (j < n) Xb[(long long)orow * n + sm.pivrow[j]] = a[q][c];
+        }
+    }
+    if (tid == 0 && rank == 0) info[b] = inf;
+    cluster_sync_all();  // neither CTA leaves while the other may still read its shared memory
+}
+
 template <typename K>
 static cudaError_t set_smem(K kern, size_t bytes) {
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -718,7 +880,7 @@ frob_status frob_inv_batched(int n, int batch, const double *Z, long long stride
 frob_status zinv_lu_batched(int n, int batch, const double *Z, long long strideZ, double *X,
                             long long strideX, int *d_info, void *ws, size_t ws_bytes, void *stream) {
     (void)ws; (void)ws_bytes;
-    if (n < 1 || n > 64 || batch < 0 || !d_info || strideZ < (long long)n * n || strideX < (long long)n * n)
+    if (n < 1 || n > 128 || batch < 0 || !d_info || strideZ < (long long)n * n || strideX < (long long)n * n)
         return FROB_ERR_INVALID_ARG;
     if (batch == 0) return FROB_OK;
     if (!Z || !X) return FROB_ERR_INVALID_ARG;
@@ -726,6 +888,25 @@ frob_status zinv_lu_batched(int n, int batch, const double *Z, long long strideZ
     const double2 *Zc = reinterpret_cast<const double2 *>(Z);
     double2 *Xc = reinterpret_cast<double2 *>(X);
     cudaError_t e;
+    if (n > 64) {
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute attr[1];
+        cfg.gridDim = dim3(2u * (unsigned)batch);
+        cfg.blockDim = dim3(512);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = s;
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        count_launch();
+        ProfScope ps("zinv_batched128c", s, 8.0 * n * (double)n * n * batch);
+        if (cudaLaunchKernelEx(&cfg, zinv_batched128c_kernel, Zc, strideZ, Xc, strideX, n, d_info) != cudaSuccess)
+            return FROB_ERR_CUDA;
+        return cudaGetLastError() == cudaSuccess ? FROB_OK : FROB_ERR_CUDA;
+    }
     if (n <= 32) {
         const size_t smem = sizeof(ZSmem<32>);
         if ((e = set_smem(zinv_batched_kernel<32>, smem)) != cudaSuccess) return FROB_ERR_CUDA;

@@ -230,7 +230,7 @@ def zinv(z: torch.Tensor, out: torch.Tensor | None = None):
 
 # ----------------------------------------------------------------------------- batched
 def inv_batched(z: torch.Tensor, branch: str = "auto", out: torch.Tensor | None = None):
-    """Batched Frobenius inversion, z: (batch, n, n) complex128 contiguous, n <= 64.
+    """Batched Frobenius inversion, z: (batch, n, n) complex128 contiguous, n <= 128.
     Returns (X, info int32[batch], branch_used uint8[batch])."""
     L = load()
     _need_cuda(z, "z")
@@ -246,6 +246,8 @@ def inv_batched(z: torch.Tensor, branch: str = "auto", out: torch.Tensor | None 
 
 
 def zinv_batched(z: torch.Tensor, out: torch.Tensor | None = None):
+    """Batched complex-LU comparator (complex Gauss-Jordan), n <= 128 (64 < n: a 2-CTA cluster per
+    matrix).  Returns (X, info int32[batch])."""
     L = load()
     _need_cuda(z, "z")
     assert z.dtype == torch.complex128 and z.dim() == 3 and z.is_contiguous()

@@ -287,7 +287,7 @@ def test_batched(n, branch):
         z = z.imag * 0.5 + 1j * z.real
     x, inf, bu = fb.inv_batched(_t(z), branch=branch)
     x, inf, bu = _np(x), _np(inf), _np(bu)
-    zinv_ok = n <= 64
+    zinv_ok = n <= 128
     if zinv_ok:
         xz, infz = fb.zinv_batched(_t(z))
         xz = _np(xz)
