@@ -668,36 +668,37 @@ zinv_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__rest
 // A complex 128 x 128 matrix (256 KB) fits neither one SM's registers nor its shared memory, so
 // the comparator runs each matrix on a CLUSTER of two 512-thread CTAs: CTA c holds rows
 // [64c, 64c + 64) in registers (4 x 4 complex blocks per thread, as the one-CTA kernels).  Per
-// Gauss-Jordan step: candidates of column k, CTA argmax, cluster barrier, both CTAs read both
-// CTA candidates (DSMEM) and take the same pivot; the pivot row's owner writes the scaled row,
-// cluster barrier, the other CTA reads it through DSMEM; uniform exchange-form update.
+// Gauss-Jordan step: candidates of column k, CTA argmax; each CTA pushes its candidate (key,
+// row) into both CTAs' slots with st.async + mbarrier complete_tx and both take the same pivot;
+// the pivot row's owner scales it and pushes it into the other CTA the same way (the owner goes
+// on at once, the other waits on its row barrier); uniform exchange-form update.  One-way
+// pushes only: no cluster barrier inside the sweep.
 struct ZC128Smem {
     double2 colk[2][128];
     double2 rowp[2][128];
     unsigned long long candk[2][16];
     int candi[2][16];
-    unsigned long long cbk[2];
-    int cbi[2];
+    uint4 xc[2][2];  // [parity][sender]: {key lo, key hi, row, 0}
+    unsigned long long cbar[2], rbar;
     int pivrow[128];
     int pos[128];
     double pmag_k[128];
 };
-FROB_DEV unsigned long long ldc_u64(unsigned addr) {
-    unsigned long long v;
-    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
-    return v;
+FROB_DEV void zst_async16(unsigned raddr, const uint4 v, unsigned rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                     raddr),
+                 "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rbar)
+                 : "memory");
 }
-FROB_DEV int ldc_s32(unsigned addr) {
-    int v;
-    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
-    return v;
+FROB_DEV void zmbar_expect(unsigned addr, unsigned tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(addr), "r"(tx) : "memory");
 }
 
 __global__ void __launch_bounds__(512, 1)
 zinv_batched128c_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__restrict__ X, long long sX,
                         int n, int *__restrict__ info) {
     constexpr int N = 128, BR = 4, BC = 4, CT = N / BC;  // 32 column-threads x 16 row-threads
-    __shared__ ZC128Smem sm;
+    __shared__ __align__(16) ZC128Smem sm;
     const int tid = threadIdx.x, lane = tid & 31;
     unsigned rank;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
@@ -707,6 +708,7 @@ zinv_batched128c_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__
     const int ti = tid / CT, tj = tid % CT;
     const int rb = (int)rank * 64;        // first global row of this CTA
     const int r0 = rb + ti * BR, c0 = tj * BC;
+    const unsigned other = rank ^ 1u;
     double2 a[BR][BC];
 #pragma unroll
     for (int q = 0; q < BR; ++q)
@@ -715,15 +717,27 @@ zinv_batched128c_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__
             const int i = r0 + q, j = c0 + c;
             a[q][c] = (i < n && j < n) ? Zb[(long long)i * n + j] : make_double2(i == j ? 1.0 : 0.0, 0.0);
         }
-    if (tid < N) sm.pos[tid] = 0;
+    if (tid == 0) {
+        mbar_init(smem_u32(&sm.cbar[0]), 1u);
+        mbar_init(smem_u32(&sm.cbar[1]), 1u);
+        mbar_init(smem_u32(&sm.rbar), 1u);
+        mbar_init_fence();
+    }
     __syncthreads();
-    cluster_sync_all();
-    const unsigned other = rank ^ 1u;
+    cluster_sync_all();  // both CTAs' barriers exist before any push
+    if (tid == 0) {
+        zmbar_expect(smem_u32(&sm.cbar[0]), 32u);
+        if (n > 1) zmbar_expect(smem_u32(&sm.cbar[1]), 32u);
+        zmbar_expect(smem_u32(&sm.rbar), (unsigned)(N * 16));
+    }
+    int rphase = 0;        // row-barrier phases completed (steps at which this CTA did not own the pivot)
+    unsigned used = 0;     // this thread's rows r0 .. r0+3 already pivots (no shared flags: no barrier needed)
     auto step = [&](const int k, auto KCc) {
         constexpr int KC = decltype(KCc)::value;
         const int par = k & 1;
         const bool owner = (tj == k / BC);
-        // (1) candidates of column k among this CTA's unused rows
+        // (1) candidates of column k among this CTA's unused rows; the CTA argmax is pushed into
+        // both CTAs' slots
         if (owner) {
             unsigned long long bk = 0;
             int bi = INT_MAX;
@@ -732,7 +746,7 @@ zinv_batched128c_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__
                 const int r = r0 + q;
                 const double2 v = a[q][KC];
                 sm.colk[par][r] = v;
-                if (r < n && !sm.pos[r]) {
+                if (r < n && !((used >> q) & 1u)) {
                     const unsigned long long kk = pkey_bits(v);
                     if (kk > bk) { bk = kk; bi = r; }
                 }
@@ -743,42 +757,61 @@ zinv_batched128c_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__
         __syncthreads();
         if (tid < 32) {
             const ArgMaxK m = warp_argmax_key(lane < 16 ? sm.candk[par][lane] : 0ull, lane < 16 ? sm.candi[par][lane] : INT_MAX);
-            if (lane == 0) { sm.cbk[par] = m.k; sm.cbi[par] = m.i; }
-        }
-        cluster_sync_all();
-        // (2) the cluster's pivot (max key, then the smallest row); the owner scales its row
-        unsigned long long k0 = sm.cbk[par], k1 = ldc_u64(mapa_u32(smem_u32(&sm.cbk[par]), other));
-        int i0 = sm.cbi[par], i1 = ldc_s32(mapa_u32(smem_u32(&sm.cbi[par]), other));
-        if (rank == 1) { const unsigned long long tk = k0; k0 = k1; k1 = tk; const int tt = i0; i0 = i1; i1 = tt; }
-        const int p = (k1 > k0 || (k1 == k0 && i1 < i0)) ? i1 : i0;
-        const unsigned prank = (unsigned)(p >> 6);
-        const double2 piv = (prank == rank) ? sm.colk[par][p]
-                                            : ld_cluster(mapa_u32(smem_u32(&sm.colk[par][p]), prank), double2());
-        const double2 ip = is_zero(piv) ? zero_of(double2()) : recip(piv);
-        if (tid == 0) { sm.pivrow[k] = p; sm.pmag_k[k] = pmag(piv); sm.pos[p] = 1; }
-        if (prank == rank && ti == (p - rb) / BR) {
-            const int q = (p - rb) % BR;
-#pragma unroll
-            for (int c = 0; c < BC; ++c) {
-                double2 v = a[0][c];
-#pragma unroll
-                for (int qq = 1; qq < BR; ++qq)
-                    if (q == qq) v = a[qq][c];
-                sm.rowp[par][c0 + c] = (owner && c == KC) ? ip : mul(v, ip);
+            if (lane < 2) {
+                const uint4 v = make_uint4((unsigned)m.k, (unsigned)(m.k >> 32), (unsigned)m.i, 0u);
+                const unsigned tgt = (unsigned)lane;  // lane 0 -> CTA 0, lane 1 -> CTA 1
+                zst_async16(mapa_u32(smem_u32(&sm.xc[par][rank]), tgt), v, mapa_u32(smem_u32(&sm.cbar[par]), tgt));
             }
         }
-        cluster_sync_all();
-        // (3) uniform exchange-form update (the owner of column k zeroes it first; the pivot row
+        mbar_wait_parity(smem_u32(&sm.cbar[par]), (unsigned)((k >> 1) & 1));
+        // (2) the cluster's pivot (max key, then the smallest row)
+        const uint4 x0 = sm.xc[par][0], x1 = sm.xc[par][1];
+        const unsigned long long k0 = ((unsigned long long)x0.y << 32) | x0.x, k1 = ((unsigned long long)x1.y << 32) | x1.x;
+        const int i0 = (int)x0.z, i1 = (int)x1.z;
+        const bool w1 = (k1 > k0 || (k1 == k0 && i1 < i0));
+        const int p = w1 ? i1 : i0;
+        const unsigned long long pk = w1 ? k1 : k0;
+        const unsigned prank = (unsigned)(p >> 6);
+        __syncwarp();
+        if (tid == 0) {
+            if (k + 2 < n) zmbar_expect(smem_u32(&sm.cbar[par]), 32u);
+            sm.pivrow[k] = p;
+            sm.pmag_k[k] = __longlong_as_double((long long)(pk - 1ull));  // key = bits(|re|+|im|) + 1
+        }
+        if (p >= r0 && p < r0 + BR) used |= 1u << (p - r0);
+        if (prank == rank) {
+            // (3a) the owner scales the pivot row into its own rowp and pushes it to the other CTA
+            if (ti == (p - rb) / BR) {
+                const int q = (p - rb) % BR;
+                const double2 piv = sm.colk[par][p];
+                const double2 ip = is_zero(piv) ? zero_of(double2()) : recip(piv);
+                const unsigned dst = mapa_u32(smem_u32(&sm.rowp[par][c0]), other);
+                const unsigned rb_other = mapa_u32(smem_u32(&sm.rbar), other);
+#pragma unroll
+                for (int c = 0; c < BC; ++c) {
+                    double2 v = a[0][c];
+#pragma unroll
+                    for (int qq = 1; qq < BR; ++qq)
+                        if (q == qq) v = a[qq][c];
+                    const double2 y = (owner && c == KC) ? ip : mul(v, ip);
+                    sm.rowp[par][c0 + c] = y;
+                    zst_async16(dst + c * 16u, make_uint4(__double2loint(y.x), __double2hiint(y.x), __double2loint(y.y),
+                                                         __double2hiint(y.y)), rb_other);
+                }
+            }
+            __syncthreads();
+        } else {
+            // (3b) the other CTA waits for the pushed pivot row
+            mbar_wait_parity(smem_u32(&sm.rbar), (unsigned)(rphase & 1));
+            ++rphase;
+            __syncwarp();
+            if (tid == 0) zmbar_expect(smem_u32(&sm.rbar), (unsigned)(N * 16));
+        }
+        // (4) uniform exchange-form update (the owner of column k zeroes it first; the pivot row
         // is written last)
         double2 rp[BC], ck[BR];
-        if (prank == rank) {
 #pragma unroll
-            for (int c = 0; c < BC; ++c) rp[c] = sm.rowp[par][c0 + c];
-        } else {
-            const unsigned base = mapa_u32(smem_u32(&sm.rowp[par][c0]), prank);
-#pragma unroll
-            for (int c = 0; c < BC; ++c) rp[c] = ld_cluster(base + c * 16u, double2());
-        }
+        for (int c = 0; c < BC; ++c) rp[c] = sm.rowp[par][c0 + c];
 #pragma unroll
         for (int q = 0; q < BR; ++q) ck[q] = sm.colk[par][r0 + q];
         if (owner) {
@@ -822,7 +855,7 @@ zinv_batched128c_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__
         }
     }
     if (tid == 0 && rank == 0) info[b] = inf;
-    cluster_sync_all();  // neither CTA leaves while the other may still read its shared memory
+    cluster_sync_all();  // every push has landed (all were waited for) before either CTA leaves
 }
 
 template <typename K>
