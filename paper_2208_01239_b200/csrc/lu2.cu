@@ -1210,6 +1210,11 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
     // source rows of this tile's rows [r0, r0 + U2_TR) and of the top rows [k0, k0 + PW): identity,
     // then the step's moves applied once (instead of a search of the move list per row)
     __shared__ int rmap[U2_TR + PW];
+    __shared__ int u12ready_s;
+    // (a grid with a single column tile -- the NEXT kernel -- lets every tile solve for itself:
+    // no hand-off on its critical path)
+    const bool solo = gridDim.x == 1;
+    const bool prod = solo || blockIdx.y == 0;
     if (tid < U2_TR + PW) rmap[tid] = (tid < U2_TR) ? r0 + tid : k0 + (tid - U2_TR);
     if (tid < MV2_MAX) {
         const int nm = mv2[0];
@@ -1217,8 +1222,22 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
         mdst[tid] = tid < nm ? mv2[1 + tid] : -1;
         msrc[tid] = tid < nm ? mv2[1 + MV2_MAX + tid] : -1;
     }
+    if (tid == 0 && !prod) {  // U12 of this column block already published? (one look, no spin)
+        int v;
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(u12f + blockIdx.x) : "memory");
+        u12ready_s = v >= tag;
+    }
     __syncthreads();
     const int nm = nmv_s;
+    // consumer tiles whose U12 is already out request it now, beside the move list's row map
+    const bool early = tile && !prod && u12ready_s;
+    if (early) {
+        for (int idx = tid; idx < PW * (U2_TC / E); idx += U2_T) {
+            const int i = idx / (U2_TC / E), e = (idx % (U2_TC / E)) * E;
+            if (e < nc) cp_async16(&Us[i][e], Bn + (long long)(k0 + i) * ld + c0 + e);
+        }
+        cp_async_commit();
+    }
     if (tid < nm) {
         const int d = mdst[tid];
         if (d >= r0 && d < r0 + U2_TR) rmap[d - r0] = msrc[tid];
@@ -1242,10 +1261,6 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
     // ---- 3. the first row block of tiles PRODUCES U12 of its columns (gather of the pivot rows X,
     // TRSM), stores it in Bn's top rows and raises the column block's flag; the other tiles load
     // it from there (L2) once the flag is up, instead of each repeating the TRSM
-    // (a grid with a single column tile -- the NEXT kernel -- lets every tile solve for itself:
-    // no hand-off on its critical path)
-    const bool solo = gridDim.x == 1;
-    const bool prod = solo || blockIdx.y == 0;
     if (prod) {
         for (int idx = tid; idx < PW * (U2_TC / E); idx += U2_T) {
             const int i = idx / (U2_TC / E), e = (idx % (U2_TC / E)) * E;
@@ -1302,7 +1317,7 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
             __threadfence();
             asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(u12f + blockIdx.x), "r"(tag) : "memory");
         }
-    } else {
+    } else if (!early) {
         if (tid == 0) {
             long long it = 0;
             int v;
