@@ -1068,8 +1068,9 @@ template cudaError_t inv_from_lu<double2>(int, double2 *, long long, double2 *, 
 constexpr int LU_TWO_LEVEL_MIN = 2048;
 
 struct AuxCtx {
-    cudaStream_t st = nullptr;
-    cudaEvent_t ev[4];
+    cudaStream_t st = nullptr;  // far-column updates, lowest priority
+    cudaStream_t hi = nullptr;  // the panel chain, highest priority (its CTAs are dispatched first)
+    cudaEvent_t ev[6];
     bool ok = false;
     std::mutex mu;
 };
@@ -1082,7 +1083,10 @@ static AuxCtx &aux_ctx(cudaError_t &err) {
     std::lock_guard<std::mutex> g(gmu);
     err = cudaSuccess;
     if (!c.ok) {
-        err = cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking);
+        int least = 0, greatest = 0;
+        err = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+        if (err == cudaSuccess) err = cudaStreamCreateWithPriority(&c.st, cudaStreamNonBlocking, least);
+        if (err == cudaSuccess) err = cudaStreamCreateWithPriority(&c.hi, cudaStreamNonBlocking, greatest);
         for (auto &e : c.ev)
             if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
         c.ok = (err == cudaSuccess);
@@ -1202,6 +1206,15 @@ static cudaError_t outer_update(int n, T *A, long long lda, int K0, int W, int c
                       A + (long long)K0 * lda + c0, lda, W, nc);
 }
 
+// chain / far-column stream priorities unless env FROB_LU_PRIO=0 (A/B measurement aid)
+static bool getrf_prio() {
+    static bool v = [] {
+        const char *e = getenv("FROB_LU_PRIO");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
 template <typename T>
 cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuStats *stats, T *work,
                   cudaStream_t s) {
@@ -1218,12 +1231,13 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
     }
     // one panel step at k0 inside [cb, ce); its move list goes to the next slot of mv
     int slot = 0;
+    cudaStream_t cs = s;  // the panel chain's stream
     auto step = [&](int cb, int ce, int k0, int &w) -> cudaError_t {
         int *list = mv + (long long)slot * MV_INTS;
         ++slot;
-        if (np && n - k0 <= LU2_PANEL_MAX_M) return panel_step2<T>(n, A, lda, tm, cb, ce, k0, perm, list, diag, s, w);
+        if (np && n - k0 <= LU2_PANEL_MAX_M) return panel_step2<T>(n, A, lda, tm, cb, ce, k0, perm, list, diag, cs, w);
         w = min(PW, ce - k0);
-        return panel_step<T, PW>(n, A, lda, cb, ce, k0, perm, list, diag, s);
+        return panel_step<T, PW>(n, A, lda, cb, ce, k0, perm, list, diag, cs);
     };
     if (n < LU_TWO_LEVEL_MIN || !work) {
         for (int k0 = 0, w = 0; k0 < n; k0 += w)
@@ -1237,6 +1251,15 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
         T *tmp = work + 2 * (size_t)LU_NB * LU_NB;
         T *Tb[2] = {tmp + (size_t)LU_NB * LU_NB, tmp + (size_t)LU_NB * LU_NB + (size_t)LU_NB * ldT};
         cudaEvent_t evL = ax.ev[0], evR[2] = {ax.ev[1], ax.ev[2]}, evJ = ax.ev[3];
+        // the chain (panels, L11^{-1}, look-ahead block) on a high-priority stream, the far
+        // columns on a low-priority one: the chain's CTAs take the SMs the far-column GEMM frees
+        // first instead of queueing behind its remaining tiles (env FROB_LU_PRIO=0: caller's stream)
+        const bool prio = getrf_prio();
+        if (prio) {
+            if ((e = cudaEventRecord(ax.ev[4], s)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(ax.hi, ax.ev[4], 0)) != cudaSuccess) return e;
+            cs = ax.hi;
+        }
         int t = 0;
         for (int K0 = 0; K0 < n; K0 += LU_NB, ++t) {
             const int W = min(LU_NB, n - K0);
@@ -1249,24 +1272,24 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
             T *Li = Linv[t & 1];
             if (cn0 < n) {
                 // L11^{-1} (W x W unit lower) by the triangular recursion
-                if ((e = launch_pdl(extract_unit_lower_kernel<T>, dim3(ew_grid((long long)W * W)), dim3(256), 0, s,
+                if ((e = launch_pdl(extract_unit_lower_kernel<T>, dim3(ew_grid((long long)W * W)), dim3(256), 0, cs,
                                     A + (long long)K0 * lda + K0, lda, W, Li, (long long)LU_NB)) != cudaSuccess)
                     return e;
-                if ((e = launch_pdl(tri_leaf_kernel<T>, dim3((W + TRI_LEAF - 1) / TRI_LEAF, 1), dim3(TRI_LEAF), 0, s,
+                if ((e = launch_pdl(tri_leaf_kernel<T>, dim3((W + TRI_LEAF - 1) / TRI_LEAF, 1), dim3(TRI_LEAF), 0, cs,
                                     Li, Li, (long long)LU_NB, W, 1)) != cudaSuccess)
                     return e;
                 GemmTag tag("gemm:lu_Linv");
                 for (int sz = TRI_LEAF; sz < W; sz *= 2) {
                     const int full = W / (2 * sz);
-                    if (full > 0 && (e = tri_level<T>(Li, Li, tmp, LU_NB, sz, 0, sz, full, s, false)) != cudaSuccess)
+                    if (full > 0 && (e = tri_level<T>(Li, Li, tmp, LU_NB, sz, 0, sz, full, cs, false)) != cudaSuccess)
                         return e;
                     const int o = full * 2 * sz;
-                    if (o + sz < W && (e = tri_level<T>(Li, Li, tmp, LU_NB, sz, o, W - o - sz, 1, s, false)) !=
+                    if (o + sz < W && (e = tri_level<T>(Li, Li, tmp, LU_NB, sz, o, W - o - sz, 1, cs, false)) !=
                                           cudaSuccess)
                         return e;
                 }
             }
-            if ((e = cudaEventRecord(evL, s)) != cudaSuccess) return e;
+            if ((e = cudaEventRecord(evL, cs)) != cudaSuccess) return e;
             // ---- auxiliary stream: left columns + columns beyond the look-ahead block
             if ((e = cudaStreamWaitEvent(ax.st, evL, 0)) != cudaSuccess) return e;
             {
@@ -1282,16 +1305,20 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
             if ((e = cudaEventRecord(evR[t & 1], ax.st)) != cudaSuccess) return e;
             // ---- caller's stream: look-ahead block [cn0, cn1)
             if (cn0 < n) {
-                if (t > 0 && (e = cudaStreamWaitEvent(s, evR[(t - 1) & 1], 0)) != cudaSuccess) return e;
+                if (t > 0 && (e = cudaStreamWaitEvent(cs, evR[(t - 1) & 1], 0)) != cudaSuccess) return e;
                 if ((e = launch_pdl(lu_swap_multi_kernel<T, PW2>, dim3((cn1 - cn0 + SWM_COLS - 1) / SWM_COLS),
-                                    dim3(SWM_COLS), 0, s, A, lda, cn0, cn1, 0, 0, lists, nl)) != cudaSuccess)
+                                    dim3(SWM_COLS), 0, cs, A, lda, cn0, cn1, 0, 0, lists, nl)) != cudaSuccess)
                     return e;
-                if ((e = outer_update<T>(n, A, lda, K0, W, cn0, cn1, Li, Tb[t & 1], ldT, s)) != cudaSuccess) return e;
+                if ((e = outer_update<T>(n, A, lda, K0, W, cn0, cn1, Li, Tb[t & 1], ldT, cs)) != cudaSuccess) return e;
             }
         }
         // join the auxiliary stream
         if ((e = cudaEventRecord(evJ, ax.st)) != cudaSuccess) return e;
-        if ((e = cudaStreamWaitEvent(s, evJ, 0)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(cs, evJ, 0)) != cudaSuccess) return e;
+        if (prio) {
+            if ((e = cudaEventRecord(ax.ev[5], cs)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(s, ax.ev[5], 0)) != cudaSuccess) return e;
+        }
     }
     if (stats) {
         e = launch_pdl(lu_stats_kernel<T>, dim3(1), dim3(1024), 0, s, diag, n, stats);
