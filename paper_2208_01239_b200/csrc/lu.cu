@@ -1235,7 +1235,7 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
     auto step = [&](int cb, int ce, int k0, int &w) -> cudaError_t {
         int *list = mv + (long long)slot * MV_INTS;
         ++slot;
-        if (np && n - k0 <= LU2_PANEL_MAX_M) return panel_step2<T>(n, A, lda, tm, cb, ce, k0, perm, list, diag, cs, w);
+        if (np && n - k0 <= lu2_panel_max_m()) return panel_step2<T>(n, A, lda, tm, cb, ce, k0, perm, list, diag, cs, w);
         w = min(PW, ce - k0);
         return panel_step<T, PW>(n, A, lda, cb, ce, k0, perm, list, diag, cs);
     };

@@ -67,8 +67,10 @@ template <typename T> struct Panel2W { static constexpr int PW = PANEL2_REAL_PW,
 template <> struct Panel2W<double2> { static constexpr int PW = 8, PH = 8; };
 // lu2's panel kernels used IN PLACE by the blocked getrf: rows [k0, n) x columns [k0, k0 + w) of A
 // (lda; tm = tma_map_rows128 of A with 256-row boxes) factored, rows written to their final
-// positions, the move list (MV_INTS layout) to mv, pivots to diag[k0..]; n - k0 <= LU2_PANEL_MAX_M
-constexpr int LU2_PANEL_MAX_M = 4096;
+// positions, the move list (MV_INTS layout) to mv, pivots to diag[k0..]; n - k0 <= lu2_panel_max_m()
+// (LU2_PANEL_MAX_M: a cluster of up to 16 CTAs x 512 rows; env FROB_P2C_MAX=8 lowers it to 4096)
+constexpr int LU2_PANEL_MAX_M = 8192;
+int lu2_panel_max_m();
 template <typename T>
 cudaError_t lu2_panel_inplace(const CUtensorMap &tm, T *A, long long lda, int n, int k0, int w, int *mv, T *diag,
                               cudaStream_t s);

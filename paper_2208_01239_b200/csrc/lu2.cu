@@ -607,7 +607,7 @@ lu_panel2_kernel(const __grid_constant__ CUtensorMap tmap, T *__restrict__ B, lo
 // never move inside the panel; each CTA writes its rows to their final positions at the end;
 // rank 0 emits the move list and the pivot values.  (A column costs one DSMEM round trip,
 // ~520 cycles, more than the single-CTA kernel; in exchange each SM holds 1/CS of the panel.)
-constexpr int P2C_MAX = 8;  // portable cluster size: m <= 4096
+constexpr int P2C_MAX = 16;  // non-portable cluster size (one GPC): m <= 8192
 constexpr int P2C_PUSH_WARPS = 3;
 struct __align__(16) XSlot2 {
     unsigned long long key;
@@ -1452,6 +1452,48 @@ static size_t lu2_sync_ints(int n) {
     return 2 * ncb + (size_t)(n + 7) / 8 + 1;
 }
 
+// can a cluster of cs panel CTAs (one SM each) be placed at all on this device?
+template <typename T>
+static bool panel2c_cluster_fits(int cs) {
+    constexpr int PH = Panel2W<T>::PH;
+    constexpr bool TWO = Panel2W<T>::PW > PH;
+    const size_t smem = (size_t)2 * P2_T * 128 + 1024;
+    if (cudaFuncSetAttribute(lu_panel2c_kernel<T, PH, TWO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(lu_panel2c_kernel<T, PH, TWO>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+            cudaSuccess)
+        return false;
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    cfg.gridDim = dim3((unsigned)cs);
+    cfg.blockDim = dim3(P2_T);
+    cfg.dynamicSmemBytes = smem;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, lu_panel2c_kernel<T, PH, TWO>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return nc > 0;
+}
+
+int lu2_panel_max_m() {
+    static int v = [] {
+        const char *e = getenv("FROB_P2C_MAX");
+        int cs = e ? atoi(e) : P2C_MAX;
+        cs = (cs >= 1 && cs < P2C_MAX) ? cs : P2C_MAX;
+        // clusters above the portable 8 need 16 free SMs in one GPC: keep 8 if they do not fit
+        if (cs > 8 && !(panel2c_cluster_fits<double>(cs) && panel2c_cluster_fits<double2>(cs))) cs = 8;
+        return cs * P2_T;
+    }();
+    return v;
+}
+
 int lu2_max_n() {
     static int v = [] {
         const char *e = getenv("FROB_LU2_MAX");
@@ -1501,6 +1543,8 @@ static cudaError_t launch_panel2c(const CUtensorMap &tm, T *B, long long ld, int
     if (dev < 64 && !attr_set[dev]) {
         cudaError_t e = cudaFuncSetAttribute(lu_panel2c_kernel<T, PH, TWO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
+        if (e == cudaSuccess)  // clusters of 9..16 CTAs (m > 4096, the blocked getrf's panels)
+            e = cudaFuncSetAttribute(lu_panel2c_kernel<T, PH, TWO>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         attr_set[dev] = true;
     }
@@ -1531,7 +1575,7 @@ cudaError_t lu2_panel_inplace(const CUtensorMap &tm, T *A, long long lda, int n,
     constexpr int PH = Panel2W<T>::PH;
     const int m = n - k0;
     static_assert(MV2_INTS == MV_INTS && MV2_MAX == 2 * PW_MAX, "move-list layouts agree");
-    if (m > LU2_PANEL_MAX_M || m > P2C_MAX * P2_T) return cudaErrorInvalidValue;
+    if (m > lu2_panel_max_m() || m > P2C_MAX * P2_T) return cudaErrorInvalidValue;
     if (m > P2_T) return launch_panel2c<T, PH>(tm, A, lda, n, k0, w, mv, diag, (m + P2_T - 1) / P2_T, s);
     return launch_panel2<T, PH, 1>(tm, A, lda, n, k0, w, mv, diag, s);
 }

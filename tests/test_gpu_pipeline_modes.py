@@ -61,3 +61,39 @@ def test_pipeline_mode(env, refs, tmp_path):
             assert oracle.rel_fro(x, ref) <= 1e-10, (env, k, n)
             r = np.linalg.norm(z @ x - np.eye(n))
             assert r <= 1e-11 * n, (env, k, n, r)
+
+
+P2C_CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import synth, paper_2208_01239_b200 as fb
+n = {n}
+a, _ = synth.gauss_pair(n, seed=31, shift=n ** 0.5 + 2.0)
+lu, perm, info = fb.dgetrf(torch.from_numpy(a).cuda())
+np.savez({path!r}, lu=lu.cpu().numpy(), perm=perm.cpu().numpy())
+"""
+
+
+def test_blocked_lu_wide_cluster_panels(tmp_path):
+    """The blocked getrf's panels for 4096 < m <= 8192 rows run on 9..16-CTA clusters (non-portable
+    cluster size; FROB_P2C_MAX=8 keeps them on the older 16-column cluster panel).  n = 4700: panels
+    of 4700 .. 4097 rows (10-CTA clusters, ragged last CTA).  Both must give P A = L U to rounding,
+    and the same pivots (identical argmax rule, well separated pivots for this shifted Gaussian)."""
+    n = 4700
+    got = []
+    for env in ({"FROB_P2C_MAX": "8"}, {}):
+        path = str(tmp_path / f"lu{len(got)}.npz")
+        p = subprocess.run([sys.executable, "-c", P2C_CHILD.format(root=ROOT, n=n, path=path)],
+                           env=dict(os.environ, **env), capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        got.append(np.load(path))
+    a, _ = synth.gauss_pair(n, seed=31, shift=math.sqrt(n) + 2.0)
+    for g in got:
+        lu, perm = g["lu"], g["perm"].astype(np.int64)
+        assert sorted(perm.tolist()) == list(range(n))
+        L = np.tril(lu, -1) + np.eye(n)
+        U = np.triu(lu)
+        r = np.linalg.norm(a[perm] - L @ U) / np.linalg.norm(a)
+        assert r <= 1e-14 * math.sqrt(n), r
+    assert np.array_equal(got[0]["perm"], got[1]["perm"])
+    assert np.abs(got[0]["lu"] - got[1]["lu"]).max() <= 1e-10 * np.abs(got[0]["lu"]).max()
