@@ -216,6 +216,10 @@ void pieces(int n) {
 }
 
 int main(int argc, char **argv) {
+    if (argc > 1 && argv[1][0] == 'w') {  // wide cluster panels of the blocked getrf (m > 4096: 9..16 CTAs)
+        pieces<double>(4096); pieces<double>(6000); pieces<double>(8192); pieces<double2>(8192);
+        return 0;
+    }
     if (argc > 1 && argv[1][0] == 'p') {
         pieces<double>(1024); pieces<double>(512); pieces<double2>(1024);
         pieces<double>(2048); pieces<double>(4096); pieces<double2>(4096);
