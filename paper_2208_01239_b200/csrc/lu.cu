@@ -901,7 +901,12 @@ cudaError_t extract_ul(int n, const T *lu, long long ld, T *U, T *L, cudaStream_
 template cudaError_t extract_ul<double>(int, const double *, long long, double *, double *, cudaStream_t);
 template cudaError_t extract_ul<double2>(int, const double2 *, long long, double2 *, double2 *, cudaStream_t);
 
-// blockIdx.y == 0: invert upper diagonal blocks of U in place; == 1: unit-lower blocks of L
+// blockIdx.y == 0: invert upper diagonal blocks of U in place; == 1: unit-lower blocks of L.
+// One thread per row of U^{-1} (column of L^{-1}); the recurrences are evaluated "right-looking":
+// once X[i][k] is known it is added into the accumulators of every later entry (independent
+// FMAs in registers) instead of each entry re-reading a dependent dot product, with the same
+// terms in the same order (k increasing): bit-identical to the dot-product form for real T (a
+// complex product's mul/add pairs may contract to FMAs differently: ~1e-14 relative).
 template <typename T>
 __global__ void __launch_bounds__(TRI_LEAF) tri_leaf_kernel(T *__restrict__ U, T *__restrict__ L,
                                                             long long ld, int n, int lower_only = 0) {
@@ -909,34 +914,46 @@ __global__ void __launch_bounds__(TRI_LEAF) tri_leaf_kernel(T *__restrict__ U, T
     pdl_wait();
     __shared__ T S[TRI_LEAF][TRI_LEAF + 1];
     __shared__ T X[TRI_LEAF][TRI_LEAF + 1];
+    __shared__ T R[TRI_LEAF];
     const int b0 = blockIdx.x * TRI_LEAF;
     const int sz = min(TRI_LEAF, n - b0);
     const bool upper = (blockIdx.y == 0) && !lower_only;
     T *M = upper ? U : L;
     const int tid = threadIdx.x;
-    for (int i = 0; i < sz; ++i)
-        if (tid < sz) S[i][tid] = M[(long long)(b0 + i) * ld + b0 + tid];
+    const T z = zero_of(T());
+    for (int i = 0; i < TRI_LEAF; ++i) S[i][tid] = (i < sz && tid < sz) ? M[(long long)(b0 + i) * ld + b0 + tid] : z;
     __syncthreads();
-    if (tid < sz) {
-        if (upper) {
-            // row i = tid of U^{-1}: X[i][i] = 1/u_ii; X[i][j] = -(sum_{k=i}^{j-1} X[i][k] u_kj)/u_jj
-            const int i = tid;
-            for (int j = 0; j < i; ++j) X[i][j] = zero_of(T());
-            X[i][i] = recip(S[i][i]);
-            for (int j = i + 1; j < sz; ++j) {
-                T acc = zero_of(T());
-                for (int k = i; k < j; ++k) acc = madd(acc, X[i][k], S[k][j]);
-                X[i][j] = neg(mul(acc, recip(S[j][j])));
+    R[tid] = (upper && tid < sz) ? recip(S[tid][tid]) : z;
+    __syncthreads();
+    T acc[TRI_LEAF];
+#pragma unroll
+    for (int j = 0; j < TRI_LEAF; ++j) acc[j] = z;
+    if (upper) {
+        // row i = tid of U^{-1}: X[i][i] = 1/u_ii; X[i][j] = -(sum_{k=i}^{j-1} X[i][k] u_kj)/u_jj
+        const int i = tid;
+#pragma unroll
+        for (int k = 0; k < TRI_LEAF; ++k) {
+            T xk = z;
+            if (k == i) xk = R[k];
+            else if (k > i) xk = neg(mul(acc[k], R[k]));
+            X[i][k] = xk;
+            if (k >= i) {
+#pragma unroll
+                for (int j = k + 1; j < TRI_LEAF; ++j) acc[j] = madd(acc[j], xk, S[k][j]);
             }
-        } else {
-            // column j = tid of L^{-1}: Y[j][j] = 1; Y[i][j] = -sum_{k=j}^{i-1} l_ik Y[k][j]
-            const int j = tid;
-            for (int i = 0; i < j; ++i) X[i][j] = zero_of(T());
-            X[j][j] = one_of(T());
-            for (int i = j + 1; i < sz; ++i) {
-                T acc = zero_of(T());
-                for (int k = j; k < i; ++k) acc = madd(acc, S[i][k], X[k][j]);
-                X[i][j] = neg(acc);
+        }
+    } else {
+        // column j = tid of L^{-1}: Y[j][j] = 1; Y[i][j] = -sum_{k=j}^{i-1} l_ik Y[k][j]
+        const int j = tid;
+#pragma unroll
+        for (int k = 0; k < TRI_LEAF; ++k) {
+            T yk = z;
+            if (k == j) yk = one_of(T());
+            else if (k > j) yk = neg(acc[k]);
+            X[k][j] = yk;
+            if (k >= j) {
+#pragma unroll
+                for (int i = k + 1; i < TRI_LEAF; ++i) acc[i] = madd(acc[i], S[i][k], yk);
             }
         }
     }
