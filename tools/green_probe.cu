@@ -57,7 +57,7 @@ int main(int argc, char **argv) {
     // a deep queue of short CTAs (50 KB smem: 4 per SM, ~10 us each) on the green stream, like
     // the far-column GEMM's tiles (runtime launch syntax on a driver stream)
     cudaFuncSetAttribute(smid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 50 * 1024);
-    smid_kernel<<<60000, 128, 50 * 1024, (cudaStream_t)gs>>>(d, 20000LL);
+    smid_kernel<<<60000, 128, 50 * 1024, (cudaStream_t)gs>>>(d, 200000LL);  // ~100 us each, ~10 ms in all
     CK(cudaGetLastError());
     unsigned long long *t;
     CK(cudaMalloc(&t, 2 * sizeof(unsigned long long)));
