@@ -15,10 +15,15 @@
  *     are fp64 with a leading dimension in doubles.
  *   - All matrix / workspace pointers are DEVICE pointers owned by the caller (except
  *     the *_host entry points and the host_* out-parameters, which are host memory).
- *     The library never allocates device memory and keeps no global state: calls are
+ *     The library never allocates device memory and keeps no per-call state: calls are
  *     re-entrant given distinct workspaces.
  *   - `stream` is a cudaStream_t passed as void*; NULL means the legacy default
- *     stream.  Work is enqueued asynchronously on it.  The only host synchronisations
+ *     stream.  Work is enqueued asynchronously on it.  LUs of order > 4096 (blocked
+ *     getrf) fork onto two library-owned streams per device (created on first use: the
+ *     panel chain at the highest priority, the far-column updates at the lowest) through
+ *     events and join back to `stream` before the call returns, so stream order and CUDA
+ *     graph capture are preserved; concurrent host threads serialise on that fork (one
+ *     mutex per device).  The only host synchronisations
  *     are (a) FROB_BRANCH_AUTO in frob_inv (one 32-byte device->host read of the pivot
  *     diagnostics of LU(A)), (b) a non-NULL host_info / host-side outputs, (c) the
  *     Newton drivers (one 16-byte read of delta_t per iteration), (d) *_host entries.
