@@ -1075,10 +1075,10 @@ template cudaError_t inv_from_lu<double2>(int, double2 *, long long, double2 *, 
 // =====================================================================================
 // getrf: two-level blocked right-looking LU with look-ahead
 // =====================================================================================
-// Outer blocks of LU_NB columns; inside a block, PW-column register panels with narrow
+// Outer blocks of LuNB<T>::N columns; inside a block, PW-column register panels with narrow
 // swap/TRSM/GEMM updates restricted to the block.  After a block, its row movements,
-// U12 = L11^{-1} A12 (L11^{-1} by the triangular recursion, so the TRSM is a K = LU_NB
-// GEMM) and the K = LU_NB trailing GEMM are applied: first to the NEXT block's columns on
+// U12 = L11^{-1} A12 (L11^{-1} by the triangular recursion, so the TRSM is a K = LuNB
+// GEMM) and the K = LuNB trailing GEMM are applied: first to the NEXT block's columns on
 // the caller's stream (look-ahead), and for all other columns on an internal auxiliary
 // stream, where they overlap the next block's panel chain.
 // below this order the single-level LU (full-width K = PW trailing updates) is faster
@@ -1115,8 +1115,8 @@ static long long ld8(int n) { return ((long long)n + 7) / 8 * 8; }
 
 template <typename T>
 size_t getrf_work_elems(int n) {
-    if (n <= LU_NB) return 1;
-    return 3 * (size_t)LU_NB * LU_NB + 2 * (size_t)LU_NB * ld8(n);
+    if (n <= LuNB<T>::N) return 1;
+    return 3 * (size_t)LuNB<T>::N * LuNB<T>::N + 2 * (size_t)LuNB<T>::N * ld8(n);
 }
 template size_t getrf_work_elems<double>(int);
 template size_t getrf_work_elems<double2>(int);
@@ -1134,7 +1134,7 @@ static cudaError_t panel_step(int n, T *A, long long lda, int cb, int ce, int k0
                               cudaStream_t s) {
     cudaError_t e;
     const int w = min(PW, ce - k0), m = n - k0;
-    const bool fused = (ce - cb) <= LU_NB;  // inner step of the two-level LU: swap+TRSM fused into the panel
+    const bool fused = (ce - cb) <= LuNB<T>::N;  // inner step of the two-level LU: swap+TRSM fused into the panel
     if ((e = launch_panel<T, PW>(A + (long long)k0 * lda + k0, lda, m, w, k0, list, diag, s, fused ? cb : 0,
                                  fused ? ce : 0, fused ? perm : nullptr)) != cudaSuccess)
         return e;
@@ -1208,7 +1208,7 @@ static cudaError_t outer_update(int n, T *A, long long lda, int K0, int W, int c
     const int nc = c1 - c0;
     if (nc <= 0) return cudaSuccess;
     GemmTag tag("gemm:lu_outer");
-    auto p = gemm_params<T>(W, nc, W, 1.0, Linv, LU_NB, A + (long long)K0 * lda + c0, lda, 0.0, nullptr, ldT,
+    auto p = gemm_params<T>(W, nc, W, 1.0, Linv, LuNB<T>::N, A + (long long)K0 * lda + c0, lda, 0.0, nullptr, ldT,
                             Tb + c0, ldT);
     p.triA = TRI_LOWER;
     if ((e = gemm_launch<T>(p, 1, s)) != cudaSuccess) return e;
@@ -1264,9 +1264,9 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
         if (e != cudaSuccess) return e;
         std::lock_guard<std::mutex> guard(ax.mu);
         const long long ldT = ld8(n);
-        T *Linv[2] = {work, work + (size_t)LU_NB * LU_NB};
-        T *tmp = work + 2 * (size_t)LU_NB * LU_NB;
-        T *Tb[2] = {tmp + (size_t)LU_NB * LU_NB, tmp + (size_t)LU_NB * LU_NB + (size_t)LU_NB * ldT};
+        T *Linv[2] = {work, work + (size_t)LuNB<T>::N * LuNB<T>::N};
+        T *tmp = work + 2 * (size_t)LuNB<T>::N * LuNB<T>::N;
+        T *Tb[2] = {tmp + (size_t)LuNB<T>::N * LuNB<T>::N, tmp + (size_t)LuNB<T>::N * LuNB<T>::N + (size_t)LuNB<T>::N * ldT};
         cudaEvent_t evL = ax.ev[0], evR[2] = {ax.ev[1], ax.ev[2]}, evJ = ax.ev[3];
         // the chain (panels, L11^{-1}, look-ahead block) on a high-priority stream, the far
         // columns on a low-priority one: the chain's CTAs take the SMs the far-column GEMM frees
@@ -1278,8 +1278,8 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
             cs = ax.hi;
         }
         int t = 0;
-        for (int K0 = 0; K0 < n; K0 += LU_NB, ++t) {
-            const int W = min(LU_NB, n - K0);
+        for (int K0 = 0; K0 < n; K0 += LuNB<T>::N, ++t) {
+            const int W = min(LuNB<T>::N, n - K0);
             const int slot0 = slot;
             for (int k0 = K0, w = 0; k0 < K0 + W; k0 += w)
                 if ((e = step(K0, K0 + W, k0, w)) != cudaSuccess) return e;
@@ -1290,18 +1290,18 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
             if (cn0 < n) {
                 // L11^{-1} (W x W unit lower) by the triangular recursion
                 if ((e = launch_pdl(extract_unit_lower_kernel<T>, dim3(ew_grid((long long)W * W)), dim3(256), 0, cs,
-                                    A + (long long)K0 * lda + K0, lda, W, Li, (long long)LU_NB)) != cudaSuccess)
+                                    A + (long long)K0 * lda + K0, lda, W, Li, (long long)LuNB<T>::N)) != cudaSuccess)
                     return e;
                 if ((e = launch_pdl(tri_leaf_kernel<T>, dim3((W + TRI_LEAF - 1) / TRI_LEAF, 1), dim3(TRI_LEAF), 0, cs,
-                                    Li, Li, (long long)LU_NB, W, 1)) != cudaSuccess)
+                                    Li, Li, (long long)LuNB<T>::N, W, 1)) != cudaSuccess)
                     return e;
                 GemmTag tag("gemm:lu_Linv");
                 for (int sz = TRI_LEAF; sz < W; sz *= 2) {
                     const int full = W / (2 * sz);
-                    if (full > 0 && (e = tri_level<T>(Li, Li, tmp, LU_NB, sz, 0, sz, full, cs, false)) != cudaSuccess)
+                    if (full > 0 && (e = tri_level<T>(Li, Li, tmp, LuNB<T>::N, sz, 0, sz, full, cs, false)) != cudaSuccess)
                         return e;
                     const int o = full * 2 * sz;
-                    if (o + sz < W && (e = tri_level<T>(Li, Li, tmp, LU_NB, sz, o, W - o - sz, 1, cs, false)) !=
+                    if (o + sz < W && (e = tri_level<T>(Li, Li, tmp, LuNB<T>::N, sz, o, W - o - sz, 1, cs, false)) !=
                                           cudaSuccess)
                         return e;
                 }
