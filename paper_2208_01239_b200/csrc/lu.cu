@@ -1113,10 +1113,21 @@ static AuxCtx &aux_ctx(cudaError_t &err) {
 
 static long long ld8(int n) { return ((long long)n + 7) / 8 * 8; }
 
+// the real blocked LU hands its last trailing matrix (m <= LU2_MAX_N rows) to lu2: two compact
+// m x m ping-pong buffers + lu2's ints + the sub-permutation (n = 8192 LU 26.3 -> 23.6 ms; for
+// complex matrices lu2's 8-column steps at m = 4096 are slower than the blocked steps: not used)
+template <typename T> struct GetrfTail { static constexpr bool on = sizeof(T) == 8; };
+static size_t getrf_tail_m(int n) { return (size_t)std::min(n, LU2_MAX_N); }
+template <typename T>
+static size_t getrf_tail_elems(int n) {
+    if (!GetrfTail<T>::on) return 0;
+    const size_t m = getrf_tail_m(n), ints = lu2_int_elems((int)m) + 2 * m;
+    return 2 * m * (size_t)ld8((int)m) + (ints * sizeof(int) + sizeof(T) - 1) / sizeof(T) + 64;
+}
 template <typename T>
 size_t getrf_work_elems(int n) {
     if (n <= LuNB<T>::N) return 1;
-    return 3 * (size_t)LuNB<T>::N * LuNB<T>::N + 2 * (size_t)LuNB<T>::N * ld8(n);
+    return 3 * (size_t)LuNB<T>::N * LuNB<T>::N + 2 * (size_t)LuNB<T>::N * ld8(n) + getrf_tail_elems<T>(n);
 }
 template size_t getrf_work_elems<double>(int);
 template size_t getrf_work_elems<double2>(int);
@@ -1126,6 +1137,30 @@ size_t lu_mv_ints(int n) { return ((size_t)(n + 7) / 8 + 1) * MV_INTS; }
 static int ew_grid(long long total) {
     long long nb = (total + 255) / 256;
     return (int)(nb < 148LL * 8 ? nb : 148LL * 8);
+}
+
+// rows [r0, r0 + m) of columns [c0, c0 + nc) gathered by a row permutation: dst[i][j] = A[r0 + p[i]][c0 + j]
+template <typename T>
+__global__ void gather_rows_kernel(const T *__restrict__ A, long long lda, int r0, int c0, int m, int nc,
+                                   const int *__restrict__ p, T *__restrict__ dst, long long ldd) {
+    pdl_trigger();
+    pdl_wait();
+    const long long total = (long long)m * nc;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / nc), j = (int)(idx - (long long)i * nc);
+        dst[(long long)i * ldd + j] = A[(long long)(r0 + p[i]) * lda + c0 + j];
+    }
+}
+// perm[r0 + i] = perm[r0 + p[i]] (through tmp)
+__global__ void perm_gather_kernel(int *__restrict__ perm, int r0, int m, const int *__restrict__ p,
+                                   int *__restrict__ tmp, int phase) {
+    pdl_trigger();
+    pdl_wait();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+        if (phase == 0) tmp[i] = perm[r0 + p[i]];
+        else perm[r0 + i] = tmp[i];
+    }
 }
 
 // one panel step restricted to the column range [cb, ce) (the panel lies inside it)
@@ -1223,6 +1258,15 @@ static cudaError_t outer_update(int n, T *A, long long lda, int K0, int W, int c
                       A + (long long)K0 * lda + c0, lda, W, nc);
 }
 
+// lu2 for the last trailing matrix unless env FROB_GETRF_TAIL=0 (A/B measurement aid)
+static bool getrf_tail() {
+    static bool v = [] {
+        const char *e = getenv("FROB_GETRF_TAIL");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
 // chain / far-column stream priorities unless env FROB_LU_PRIO=0 (A/B measurement aid)
 static bool getrf_prio() {
     static bool v = [] {
@@ -1278,7 +1322,12 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
             cs = ax.hi;
         }
         int t = 0;
+        int Ktail = n;  // the trailing matrix from here on goes to lu2
         for (int K0 = 0; K0 < n; K0 += LuNB<T>::N, ++t) {
+            if (GetrfTail<T>::on && K0 > 0 && n - K0 <= lu2_max_n() && getrf_tail()) {
+                Ktail = K0;
+                break;
+            }
             const int W = min(LuNB<T>::N, n - K0);
             const int slot0 = slot;
             for (int k0 = K0, w = 0; k0 < K0 + W; k0 += w)
@@ -1332,6 +1381,37 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
         // join the auxiliary stream
         if ((e = cudaEventRecord(evJ, ax.st)) != cudaSuccess) return e;
         if ((e = cudaStreamWaitEvent(cs, evJ, 0)) != cudaSuccess) return e;
+        if (Ktail < n) {
+            // ---- the trailing m x m matrix (fully updated, all earlier row moves applied to every
+            // column) factored by lu2 into compact buffers, assembled packed back in place; its
+            // row permutation then applied to the L columns on the left and to perm
+            const int m = n - Ktail;
+            const long long ldm = ld8(m);
+            T *tb = work + 3 * (size_t)LuNB<T>::N * LuNB<T>::N + 2 * (size_t)LuNB<T>::N * ld8(n);
+            tb = reinterpret_cast<T *>((reinterpret_cast<uintptr_t>(tb) + 255) & ~(uintptr_t)255);
+            T *B0 = tb, *B1 = tb + (size_t)m * ldm;
+            int *iw2 = reinterpret_cast<int *>(B1 + (size_t)m * ldm);
+            int *psub = iw2 + lu2_int_elems(m), *ptmp = psub + m;
+            T *A22 = A + (long long)Ktail * lda + Ktail;
+            if ((e = launch_pdl(copy_block_kernel<T>, dim3(ew_grid((long long)m * m)), dim3(256), 0, cs, (const T *)A22,
+                                lda, B0, ldm, m, m)) != cudaSuccess)
+                return e;
+            if ((e = lu2_factor<T>(m, B0, B1, ldm, A22, A22, lda, psub, iw2, diag + Ktail, nullptr, cs)) != cudaSuccess)
+                return e;
+            for (int c0 = 0; c0 < Ktail; c0 += m) {  // left columns in chunks of m through B1
+                const int nc = min(m, Ktail - c0);
+                if ((e = launch_pdl(gather_rows_kernel<T>, dim3(ew_grid((long long)m * nc)), dim3(256), 0, cs,
+                                    (const T *)A, lda, Ktail, c0, m, nc, (const int *)psub, B1, ldm)) != cudaSuccess)
+                    return e;
+                if ((e = launch_pdl(copy_block_kernel<T>, dim3(ew_grid((long long)m * nc)), dim3(256), 0, cs,
+                                    (const T *)B1, ldm, A + (long long)Ktail * lda + c0, lda, m, nc)) != cudaSuccess)
+                    return e;
+            }
+            for (int ph = 0; ph < 2; ++ph)
+                if ((e = launch_pdl(perm_gather_kernel, dim3((m + 255) / 256), dim3(256), 0, cs, perm, Ktail, m,
+                                    (const int *)psub, ptmp, ph)) != cudaSuccess)
+                    return e;
+        }
         if (prio) {
             if ((e = cudaEventRecord(ax.ev[5], cs)) != cudaSuccess) return e;
             if ((e = cudaStreamWaitEvent(s, ax.ev[5], 0)) != cudaSuccess) return e;

@@ -1429,8 +1429,12 @@ __global__ void lu_assemble2_kernel(const T *__restrict__ B0, const T *__restric
             const int p = snap[(long long)b * n + perm[i]];
             lval = ((b & 1) ? B1 : B0)[(long long)p * ld + c];
         }
-        U[(long long)i * ldo + c] = uval;
-        L[(long long)i * ldo + c] = lval;
+        if (U == L) {
+            U[(long long)i * ldo + c] = (c >= i) ? uval : lval;  // packed: strict L below, U on and above
+        } else {
+            U[(long long)i * ldo + c] = uval;
+            L[(long long)i * ldo + c] = lval;
+        }
     }
 }
 
