@@ -97,3 +97,27 @@ def test_blocked_lu_wide_cluster_panels(tmp_path):
         assert r <= 1e-14 * math.sqrt(n), r
     assert np.array_equal(got[0]["perm"], got[1]["perm"])
     assert np.abs(got[0]["lu"] - got[1]["lu"]).max() <= 1e-10 * np.abs(got[0]["lu"]).max()
+
+
+@pytest.mark.parametrize("n", [2048, 4352])
+def test_blocked_lu_lu2_tail(n, tmp_path):
+    """The real blocked getrf hands its last trailing matrix to lu2 (FROB_GETRF_TAIL=0: blocked to
+    the end): n = 2048 -> one 256-column block + lu2 on 1792 rows; n = 4352 -> lu2 on exactly 4096
+    rows (its maximum).  Both give P A = L U to rounding and the same pivots."""
+    got = []
+    for env in ({"FROB_GETRF_TAIL": "0"}, {}):
+        path = str(tmp_path / f"tail{len(got)}.npz")
+        p = subprocess.run([sys.executable, "-c", P2C_CHILD.format(root=ROOT, n=n, path=path)],
+                           env=dict(os.environ, **env), capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        got.append(np.load(path))
+    a, _ = synth.gauss_pair(n, seed=31, shift=math.sqrt(n) + 2.0)
+    for g in got:
+        lu, perm = g["lu"], g["perm"].astype(np.int64)
+        assert sorted(perm.tolist()) == list(range(n))
+        L = np.tril(lu, -1) + np.eye(n)
+        U = np.triu(lu)
+        r = np.linalg.norm(a[perm] - L @ U) / np.linalg.norm(a)
+        assert r <= 1e-14 * math.sqrt(n), r
+    assert np.array_equal(got[0]["perm"], got[1]["perm"])
+    assert np.abs(got[0]["lu"] - got[1]["lu"]).max() <= 1e-10 * np.abs(got[0]["lu"]).max()
