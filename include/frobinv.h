@@ -114,6 +114,18 @@ size_t frob_inv_host_workspace_bytes(int n);
 frob_status frob_inv_host(int n, const double *Z_host, double *X_host, int branch,
                           void *ws, size_t ws_bytes, void *stream, frob_info *host_info);
 
+/* `count` independent matrices with HOST buffers, pipelined: Z_host / X_host hold count
+ * dense n x n interleaved complex128 matrices back to back (count * n * n * 16 bytes each,
+ * pinned memory required for the overlap).  Matrix i + 1 is copied host->device and matrix
+ * i - 1 device->host (two library-owned copy streams per device) while matrix i is inverted on
+ * `stream` (frob_inv with `branch`), double-buffered in ws; the call synchronises `stream`
+ * before returning.  Results equal count frob_inv_host calls bit for bit.  ws must hold
+ * frob_inv_host_many_workspace_bytes(n) bytes (independent of count).  The first failing
+ * matrix's status is returned (earlier matrices are complete). */
+size_t frob_inv_host_many_workspace_bytes(int n);
+frob_status frob_inv_host_many(int n, int count, const double *Z_host, double *X_host, int branch,
+                               void *ws, size_t ws_bytes, void *stream);
+
 /* Complex-LU inversion: Alg 3 over C (the paper's comparator `X\eye(n)`,
  * P:L1057): complex LU with partial pivoting on |re|+|im|, U^{-1}, X = U^{-1} L^{-1},
  * column interchanges.  Same layout/ownership rules as frob_inv.

@@ -673,6 +673,92 @@ frob_status frob_inv_host(int n, const double *Z_host, double *X_host, int branc
     return FROB_OK;
 }
 
+size_t frob_inv_host_many_workspace_bytes(int n) {
+    return n < 1 ? 0 : align256(frob_inv_workspace_bytes(n)) + 4 * align256((size_t)n * n * 16);
+}
+
+// per-device copy streams and events of the pipelined host entry point
+struct HostPipe {
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t start, in[2], done[2], freed[2], fin;
+    bool ok = false;
+    std::mutex mu;
+};
+static HostPipe &host_pipe(cudaError_t &err) {
+    static HostPipe pipes[64];
+    static std::mutex gmu;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    HostPipe &p = pipes[dev & 63];
+    std::lock_guard<std::mutex> g(gmu);
+    err = cudaSuccess;
+    if (!p.ok) {
+        err = cudaStreamCreateWithFlags(&p.h2d, cudaStreamNonBlocking);
+        if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&p.d2h, cudaStreamNonBlocking);
+        cudaEvent_t *evs[] = {&p.start, &p.in[0], &p.in[1], &p.done[0], &p.done[1], &p.freed[0], &p.freed[1], &p.fin};
+        for (cudaEvent_t *e : evs)
+            if (err == cudaSuccess) err = cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+        p.ok = (err == cudaSuccess);
+    }
+    return p;
+}
+
+frob_status frob_inv_host_many(int n, int count, const double *Z_host, double *X_host, int branch, void *ws,
+                               size_t ws_bytes, void *stream) {
+    if (n < 1 || count < 0 || (count > 0 && (!Z_host || !X_host))) return FROB_ERR_INVALID_ARG;
+    if (count == 0) return FROB_OK;
+    if (!ws || ws_bytes < frob_inv_host_many_workspace_bytes(n)) return FROB_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t ce;
+    HostPipe &hp = host_pipe(ce);
+    FROB_CUDA(ce);
+    std::lock_guard<std::mutex> guard(hp.mu);
+    const size_t mb = (size_t)n * n * 16, md = (size_t)n * n * 2;  // bytes / doubles per matrix
+    unsigned char *b = reinterpret_cast<unsigned char *>(ws);
+    const size_t ib = align256(frob_inv_workspace_bytes(n));
+    double *Zd[2], *Xd[2];
+    for (int k = 0; k < 2; ++k) {
+        Zd[k] = reinterpret_cast<double *>(b + ib + (2 * k) * align256(mb));
+        Xd[k] = reinterpret_cast<double *>(b + ib + (2 * k + 1) * align256(mb));
+    }
+    // the copy streams start after everything already queued on `stream`
+    FROB_CUDA(cudaEventRecord(hp.start, s));
+    FROB_CUDA(cudaStreamWaitEvent(hp.h2d, hp.start, 0));
+    FROB_CUDA(cudaStreamWaitEvent(hp.d2h, hp.start, 0));
+    auto h2d = [&](int i) -> cudaError_t {
+        const int k = i & 1;
+        cudaError_t e = cudaSuccess;
+        if (i >= 2) e = cudaStreamWaitEvent(hp.h2d, hp.done[k], 0);  // inversion i - 2 has read Zd[k]
+        if (e == cudaSuccess) e = cudaMemcpyAsync(Zd[k], Z_host + (size_t)i * md, mb, cudaMemcpyHostToDevice, hp.h2d);
+        if (e == cudaSuccess) e = cudaEventRecord(hp.in[k], hp.h2d);
+        return e;
+    };
+    frob_status result = FROB_OK;
+    FROB_CUDA(h2d(0));
+    for (int i = 0; i < count; ++i) {
+        const int k = i & 1;
+        if (i + 1 < count) FROB_CUDA(h2d(i + 1));  // queued before inversion i (which may read the host)
+        FROB_CUDA(cudaStreamWaitEvent(s, hp.in[k], 0));
+        if (i >= 2) FROB_CUDA(cudaStreamWaitEvent(s, hp.freed[k], 0));  // X of i - 2 has left Xd[k]
+        const frob_status st = frob_inv_impl(n, Zd[k], n, Xd[k], n, branch, ws, ib, s, nullptr);
+        if (st != FROB_OK) {
+            result = st;
+            break;
+        }
+        FROB_CUDA(cudaEventRecord(hp.done[k], s));
+        FROB_CUDA(cudaStreamWaitEvent(hp.d2h, hp.done[k], 0));
+        FROB_CUDA(cudaMemcpyAsync(X_host + (size_t)i * md, Xd[k], mb, cudaMemcpyDeviceToHost, hp.d2h));
+        FROB_CUDA(cudaEventRecord(hp.freed[k], hp.d2h));
+    }
+    // join both copy streams back into `stream`, then wait for everything
+    FROB_CUDA(cudaEventRecord(hp.fin, hp.d2h));
+    FROB_CUDA(cudaStreamWaitEvent(s, hp.fin, 0));
+    FROB_CUDA(cudaEventRecord(hp.fin, hp.h2d));
+    FROB_CUDA(cudaStreamWaitEvent(s, hp.fin, 0));
+    FROB_CUDA(cudaStreamSynchronize(s));
+    return result;
+}
+
 size_t zinv_lu_workspace_bytes(int n) { return n < 1 ? 0 : carve_zlu(nullptr, n).bytes; }
 
 frob_status zinv_lu(int n, const double *Z, long long ldz, double *X, long long ldx, void *ws,

@@ -43,6 +43,8 @@ SIGNATURES = {
     "frob_inv_rand": (_i, [_i, _vp, _ll, _vp, _ll, _d, _vp, _sz, _vp, _FIP]),
     "frob_inv_host_workspace_bytes": (_sz, [_i]),
     "frob_inv_host": (_i, [_i, _vp, _vp, _i, _vp, _sz, _vp, _FIP]),
+    "frob_inv_host_many_workspace_bytes": (_sz, [_i]),
+    "frob_inv_host_many": (_i, [_i, _i, _vp, _vp, _i, _vp, _sz, _vp]),
     "zinv_lu_workspace_bytes": (_sz, [_i]),
     "zinv_lu": (_i, [_i, _vp, _ll, _vp, _ll, _vp, _sz, _vp, _ip]),
     "frob_inv_batched_workspace_bytes": (_sz, [_i, _i]),
@@ -211,6 +213,21 @@ def inv_host(z_host: torch.Tensor, x_host: torch.Tensor | None = None, branch: s
     ws = workspace(L.frob_inv_host_workspace_bytes(n), device)
     st = L.frob_inv_host(n, _p(z_host), _p(x_host), BRANCH[branch], _p(ws), ws.numel(), _stream(), None)
     _check("frob_inv_host", st)
+    return x_host
+
+
+def inv_host_many(z_host: torch.Tensor, x_host: torch.Tensor | None = None, branch: str = "auto",
+                  device="cuda"):
+    """count matrices (count, n, n) in pinned HOST memory, pipelined: the copies of matrices
+    i + 1 (in) and i - 1 (out) overlap the inversion of matrix i (frob_inv_host_many)."""
+    L = load()
+    assert z_host.dtype == torch.complex128 and not z_host.is_cuda and z_host.is_contiguous() and z_host.dim() == 3
+    count, n = z_host.shape[0], z_host.shape[1]
+    assert z_host.shape[2] == n
+    x_host = x_host if x_host is not None else torch.empty_like(z_host)
+    ws = workspace(L.frob_inv_host_many_workspace_bytes(n), device)
+    st = L.frob_inv_host_many(n, count, _p(z_host), _p(x_host), BRANCH[branch], _p(ws), ws.numel(), _stream())
+    _check("frob_inv_host_many", st)
     return x_host
 
 
