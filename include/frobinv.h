@@ -151,6 +151,16 @@ frob_status frob_inv_batched(int n, int batch, const double *Z, long long stride
                              unsigned char *d_branch_used, void *ws, size_t ws_bytes,
                              void *stream);
 
+/* frob_inv_batched with HOST buffers, pipelined in chunks of `chunk` matrices: the copy of
+ * chunk j + 1 in and of chunk j - 1 out (two library-owned copy streams per device) overlap the
+ * inversion of chunk j on `stream`; synchronises before returning.  Z_host / X_host: batch
+ * dense n x n complex128 matrices back to back (pinned memory required for the overlap);
+ * h_info: host int[batch] (nullable) receives d_info.  Results equal frob_inv_batched bit for
+ * bit.  ws must hold frob_inv_batched_host_workspace_bytes(n, chunk) bytes. */
+size_t frob_inv_batched_host_workspace_bytes(int n, int chunk);
+frob_status frob_inv_batched_host(int n, int batch, const double *Z_host, double *X_host, int branch,
+                                  int *h_info, int chunk, void *ws, size_t ws_bytes, void *stream);
+
 /* Batched complex-LU comparator (complex Gauss-Jordan with partial pivoting, |re|+|im|),
  * 1 <= n <= 128: one CTA per matrix for n <= 64, a cluster of two CTAs (rows split, pivot
  * candidates and pivot rows exchanged through distributed shared memory) for 64 < n <= 128.

@@ -759,6 +759,79 @@ frob_status frob_inv_host_many(int n, int count, const double *Z_host, double *X
     return result;
 }
 
+size_t frob_inv_batched_host_workspace_bytes(int n, int chunk) {
+    if (n < 1 || chunk < 1) return 0;
+    const size_t mb = align256((size_t)chunk * n * n * 16), ib = align256((size_t)chunk * sizeof(int));
+    return 4 * mb + 2 * ib + 2 * align256((size_t)chunk);
+}
+
+frob_status frob_inv_batched_host(int n, int batch, const double *Z_host, double *X_host, int branch, int *h_info,
+                                  int chunk, void *ws, size_t ws_bytes, void *stream) {
+    if (n < 1 || n > 128 || batch < 0 || chunk < 1 || (batch > 0 && (!Z_host || !X_host))) return FROB_ERR_INVALID_ARG;
+    if (batch == 0) return FROB_OK;
+    if (!ws || ws_bytes < frob_inv_batched_host_workspace_bytes(n, chunk)) return FROB_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t ce;
+    HostPipe &hp = host_pipe(ce);
+    FROB_CUDA(ce);
+    std::lock_guard<std::mutex> guard(hp.mu);
+    const size_t md = (size_t)n * n * 2;  // doubles per matrix
+    const size_t mb = align256((size_t)chunk * n * n * 16), ib = align256((size_t)chunk * sizeof(int));
+    unsigned char *b = reinterpret_cast<unsigned char *>(ws);
+    double *Zd[2], *Xd[2];
+    int *Id[2];
+    unsigned char *Bu[2];
+    for (int k = 0; k < 2; ++k) {
+        Zd[k] = reinterpret_cast<double *>(b + (2 * k) * mb);
+        Xd[k] = reinterpret_cast<double *>(b + (2 * k + 1) * mb);
+        Id[k] = reinterpret_cast<int *>(b + 4 * mb + k * ib);
+        Bu[k] = b + 4 * mb + 2 * ib + k * align256((size_t)chunk);
+    }
+    const int nch = (batch + chunk - 1) / chunk;
+    FROB_CUDA(cudaEventRecord(hp.start, s));
+    FROB_CUDA(cudaStreamWaitEvent(hp.h2d, hp.start, 0));
+    FROB_CUDA(cudaStreamWaitEvent(hp.d2h, hp.start, 0));
+    auto cnt = [&](int j) { return std::min(chunk, batch - j * chunk); };
+    auto h2d = [&](int j) -> cudaError_t {
+        const int k = j & 1;
+        cudaError_t e = cudaSuccess;
+        if (j >= 2) e = cudaStreamWaitEvent(hp.h2d, hp.done[k], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(Zd[k], Z_host + (size_t)j * chunk * md, (size_t)cnt(j) * md * 8, cudaMemcpyHostToDevice,
+                                hp.h2d);
+        if (e == cudaSuccess) e = cudaEventRecord(hp.in[k], hp.h2d);
+        return e;
+    };
+    frob_status result = FROB_OK;
+    FROB_CUDA(h2d(0));
+    for (int j = 0; j < nch; ++j) {
+        const int k = j & 1, c = cnt(j);
+        if (j + 1 < nch) FROB_CUDA(h2d(j + 1));
+        FROB_CUDA(cudaStreamWaitEvent(s, hp.in[k], 0));
+        if (j >= 2) FROB_CUDA(cudaStreamWaitEvent(s, hp.freed[k], 0));
+        const frob_status st = frob_inv_batched(n, c, Zd[k], (long long)n * n, Xd[k], (long long)n * n, branch, Id[k],
+                                                Bu[k], nullptr, 0, s);
+        if (st != FROB_OK) {
+            result = st;
+            break;
+        }
+        FROB_CUDA(cudaEventRecord(hp.done[k], s));
+        FROB_CUDA(cudaStreamWaitEvent(hp.d2h, hp.done[k], 0));
+        FROB_CUDA(cudaMemcpyAsync(X_host + (size_t)j * chunk * md, Xd[k], (size_t)c * md * 8, cudaMemcpyDeviceToHost,
+                                  hp.d2h));
+        if (h_info)
+            FROB_CUDA(cudaMemcpyAsync(h_info + (size_t)j * chunk, Id[k], (size_t)c * sizeof(int),
+                                      cudaMemcpyDeviceToHost, hp.d2h));
+        FROB_CUDA(cudaEventRecord(hp.freed[k], hp.d2h));
+    }
+    FROB_CUDA(cudaEventRecord(hp.fin, hp.d2h));
+    FROB_CUDA(cudaStreamWaitEvent(s, hp.fin, 0));
+    FROB_CUDA(cudaEventRecord(hp.fin, hp.h2d));
+    FROB_CUDA(cudaStreamWaitEvent(s, hp.fin, 0));
+    FROB_CUDA(cudaStreamSynchronize(s));
+    return result;
+}
+
 size_t zinv_lu_workspace_bytes(int n) { return n < 1 ? 0 : carve_zlu(nullptr, n).bytes; }
 
 frob_status zinv_lu(int n, const double *Z, long long ldz, double *X, long long ldx, void *ws,

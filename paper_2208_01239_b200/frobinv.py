@@ -45,6 +45,8 @@ SIGNATURES = {
     "frob_inv_host": (_i, [_i, _vp, _vp, _i, _vp, _sz, _vp, _FIP]),
     "frob_inv_host_many_workspace_bytes": (_sz, [_i]),
     "frob_inv_host_many": (_i, [_i, _i, _vp, _vp, _i, _vp, _sz, _vp]),
+    "frob_inv_batched_host_workspace_bytes": (_sz, [_i, _i]),
+    "frob_inv_batched_host": (_i, [_i, _i, _vp, _vp, _i, _vp, _i, _vp, _sz, _vp]),
     "zinv_lu_workspace_bytes": (_sz, [_i]),
     "zinv_lu": (_i, [_i, _vp, _ll, _vp, _ll, _vp, _sz, _vp, _ip]),
     "frob_inv_batched_workspace_bytes": (_sz, [_i, _i]),
@@ -229,6 +231,23 @@ def inv_host_many(z_host: torch.Tensor, x_host: torch.Tensor | None = None, bran
     st = L.frob_inv_host_many(n, count, _p(z_host), _p(x_host), BRANCH[branch], _p(ws), ws.numel(), _stream())
     _check("frob_inv_host_many", st)
     return x_host
+
+
+def inv_batched_host(z_host: torch.Tensor, x_host: torch.Tensor | None = None, branch: str = "auto",
+                     chunk: int | None = None, device="cuda"):
+    """Batched Frobenius inversion (n <= 128) with pinned HOST buffers (batch, n, n), pipelined in
+    chunks (frob_inv_batched_host).  Returns (x_host, info int32 tensor [batch])."""
+    L = load()
+    assert z_host.dtype == torch.complex128 and not z_host.is_cuda and z_host.is_contiguous() and z_host.dim() == 3
+    batch, n = z_host.shape[0], z_host.shape[1]
+    x_host = x_host if x_host is not None else torch.empty_like(z_host)
+    info = torch.empty(batch, dtype=torch.int32).pin_memory()  # pageable memory would stall the pipeline
+    chunk = chunk or max(1, min(batch, (256 << 20) // (16 * n * n)))
+    ws = workspace(L.frob_inv_batched_host_workspace_bytes(n, chunk), device)
+    st = L.frob_inv_batched_host(n, batch, _p(z_host), _p(x_host), BRANCH[branch], _p(info), chunk, _p(ws),
+                                 ws.numel(), _stream())
+    _check("frob_inv_batched_host", st)
+    return x_host, info
 
 
 def zinv(z: torch.Tensor, out: torch.Tensor | None = None):
