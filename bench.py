@@ -179,9 +179,9 @@ class SingleMatrix(Workload):
 
     def e2e_pipelined(self, k):
         """k steps through frob_inv_host_many (pinned host buffers, the copies of matrices i +- 1
-        overlapping inversion i); None when k matrices would not fit a 512 MiB pinned budget."""
+        overlapping inversion i); None when k matrices would not fit a 2 GiB pinned budget."""
         per = 16 * self.n * self.n
-        k = min(k, (512 << 20) // per)
+        k = min(k, (2 << 30) // per)
         if k < 2:
             return None
         if getattr(self, "_zk", None) is None or self._zk.shape[0] != k:
