@@ -71,6 +71,18 @@ typedef struct {
     double rho_m;      /* same for LU(M), M = X + Y X^{-1} Y                              */
 } frob_info;
 
+/* Status record written ON THE DEVICE at the end of a call's stream work (frob_inv_dev), so
+ * errors are visible without a host synchronisation inside the library: read it after the
+ * stream (e.g. cudaMemcpyAsync + sync, or a later kernel). */
+typedef struct {
+    int status;        /* frob_status of the call: FROB_OK, FROB_ERR_SINGULAR (X or M has a singular
+                          pivot, info = column), FROB_ERR_BOTH_SINGULAR, FROB_ERR_NONFINITE        */
+    int info;          /* 0 or the 1-based singular pivot column                                   */
+    int branch_used;   /* 1 = S1, 2 = S2, 0 = none                                                 */
+    int nonfinite;     /* 1 if NaN/Inf was seen in the input                                       */
+    double rho_a, rho_b, rho_m;   /* pivot ratios (NaN where the LU did not run)                   */
+} frob_dev_status;
+
 /* ---------------------------------------------------------------- single matrix */
 
 /* Bytes of device workspace frob_inv needs for order n (256-byte aligned pointer). */
@@ -82,7 +94,11 @@ size_t frob_inv_workspace_bytes(int n);
  *   X      device output, n x n complex128, leading dim ldx; must not overlap Z
  *   branch frob_branch
  *   ws     device workspace of at least frob_inv_workspace_bytes(n) bytes
- *   host_info  nullable; if non-NULL the call synchronises `stream` and fills it.
+ *   host_info  nullable; if non-NULL the call synchronises `stream`, fills it and returns the
+ *              status found on the device (singular X or M, non-finite input).  With host_info
+ *              NULL those device-side findings are NOT returned (only argument, workspace, CUDA
+ *              errors and, for AUTO, non-finite input / both parts singular are): use
+ *              frob_inv_dev to receive them asynchronously in a device status record.
  * Returns FROB_OK, or an error status (X is then unspecified). */
 frob_status frob_inv(int n, const double *Z, long long ldz, double *X, long long ldx,
                      int branch, void *ws, size_t ws_bytes, void *stream, frob_info *host_info);
@@ -93,8 +109,22 @@ frob_status frob_inv(int n, const double *Z, long long ldz, double *X, long long
  *     formed, 9 1/3 n^3 instead of 10 n^3 flops.  Same results up to rounding order.
  * Unknown bits give FROB_ERR_INVALID_ARG.  Everything else as frob_inv. */
 #define FROB_OPT_FUSED_FIRST_STEP 1
+/*   FROB_OPT_DEVICE_AUTO  (branch must be FROB_BRANCH_AUTO) reading R1 decided ON THE DEVICE: LU(A)
+ *     and LU(B) are both computed (one extra LU, 2/3 n^3 flops), a one-thread kernel picks the branch
+ *     from their pivot statistics, and the S2 factors / rotated parts move into the S1 slots by
+ *     predicated copies.  No host synchronisation at all, so the call can be captured in a CUDA
+ *     graph; results are bitwise those of the host-decided AUTO. */
+#define FROB_OPT_DEVICE_AUTO 2
 frob_status frob_inv_opts(int n, const double *Z, long long ldz, double *X, long long ldx, int branch,
                           int options, void *ws, size_t ws_bytes, void *stream, frob_info *host_info);
+
+/* frob_inv_opts with a DEVICE status record: d_status (device frob_dev_status*, nullable) receives
+ * the call's status at the end of its stream work.  The library never synchronises for forced
+ * branches or with FROB_OPT_DEVICE_AUTO (plain AUTO still reads LU(A)'s statistics on the host).
+ * The return value reports only argument / workspace / CUDA errors and the host-decided AUTO
+ * outcomes (non-finite input, both parts singular); everything else is in *d_status. */
+frob_status frob_inv_dev(int n, const double *Z, long long ldz, double *X, long long ldx, int branch,
+                         int options, frob_dev_status *d_status, void *ws, size_t ws_bytes, void *stream);
 
 /* Randomized Frobenius inversion (Alg 5): X = A - mu B, Y = mu A + B,
  * W = (X + iY)^{-1} by Alg 1 (AUTO branch rule), Z^{-1} = (W1 - mu W2) + i (mu W1 + W2).
@@ -120,11 +150,17 @@ frob_status frob_inv_host(int n, const double *Z_host, double *X_host, int branc
  * i - 1 device->host (two library-owned copy streams per device) while matrix i is inverted on
  * `stream` (frob_inv with `branch`), double-buffered in ws; the call synchronises `stream`
  * before returning.  Results equal count frob_inv_host calls bit for bit.  ws must hold
- * frob_inv_host_many_workspace_bytes(n) bytes (independent of count).  The first failing
- * matrix's status is returned (earlier matrices are complete). */
+ * frob_inv_host_many_workspace_bytes(n) bytes (independent of count).
+ *   h_status  nullable host int[count] (pinned recommended): per-matrix frob_status found on the
+ *             device (singular X or M, non-finite input, both parts singular), copied back with
+ *             each result.
+ * Returns the first failing matrix's status (device findings included; with an error that stops
+ * the loop -- AUTO both-singular / non-finite, CUDA -- later matrices are not computed and their
+ * h_status entries are FROB_ERR_INVALID_ARG).  On every return path both copy streams have been
+ * joined and `stream` synchronised, so the host buffers are no longer in use. */
 size_t frob_inv_host_many_workspace_bytes(int n);
 frob_status frob_inv_host_many(int n, int count, const double *Z_host, double *X_host, int branch,
-                               void *ws, size_t ws_bytes, void *stream);
+                               int *h_status, void *ws, size_t ws_bytes, void *stream);
 
 /* Complex-LU inversion: Alg 3 over C (the paper's comparator `X\eye(n)`,
  * P:L1057): complex LU with partial pivoting on |re|+|im|, U^{-1}, X = U^{-1} L^{-1},
@@ -201,6 +237,13 @@ frob_status frob_polar_newton(int n, const double *A, double *U, double *H, doub
 frob_status frob_dgemm(int m, int n, int k, double alpha, const double *A, long long lda,
                        const double *B, long long ldb, double beta, double *C, long long ldc,
                        void *stream);
+
+/* C = alpha * tri(T) B (T n x n triangular: uplo 1 = upper, 2 = lower, B n x m, C n x m), fp64
+ * row-major.  The GEMM engine skips the zero triangle tile by tile, so T's other strict triangle
+ * must hold zeros (as the library's triangular inverses do).  Used to measure Thm 5.1's lambda
+ * (triangular x dense costs lambda T_mult). */
+frob_status frob_dtrmm(int uplo, int n, int m, double alpha, const double *T, long long ldt, const double *B,
+                       long long ldb, double *C, long long ldc, void *stream);
 
 /* Real inversion Alg 3: Ainv = A^{-1}, fp64 n x n row-major.
  * host_info nullable (info + pivot ratio via rho_a). */

@@ -62,9 +62,14 @@ def lib():
             L.or_zhpd_inv_chol.argtypes = [ctypes.c_int, dp, dp, dp, dp]
             L.or_zinv_gj.argtypes = [ctypes.c_int, dp, dp]
             L.or_zinv_lu.argtypes = [ctypes.c_int, dp, dp, dp, dp]
+            L.or_zgetrf.argtypes = [ctypes.c_int, dp, dp, ip]
+            L.or_zgetrs.argtypes = [ctypes.c_int, dp, dp, ip, ctypes.c_int, ctypes.c_int, dp, dp]
+            L.or_zgetrs.restype = None
+            L.or_frob_inv_many.argtypes = [ctypes.c_int, ctypes.c_int, dp, dp, dp, dp, ctypes.c_int,
+                                           ctypes.c_double, ip, dp, ip]
             for f in ("or_dgetrf", "or_dtrtri_upper", "or_dinv", "or_frob_inv", "or_frob_inv_rand", "or_zinv_gj",
                       "or_dpotrf_upper", "or_hpd_frob_inv", "or_zhpd_inv_chol",
-                      "or_zinv_lu", "or_num_threads"):
+                      "or_zinv_lu", "or_num_threads", "or_zgetrf", "or_frob_inv_many"):
                 getattr(L, f).restype = ctypes.c_int
             L.or_dgetri_solve.restype = None
             L.or_dgemm.restype = None
@@ -222,6 +227,87 @@ def zinv_lu(z):
     xi = np.zeros_like(im)
     info = lib().or_zinv_lu(re.shape[0], _p(re), _p(im), _p(xr), _p(xi))
     return xr + 1j * xi, info
+
+
+def zgetrf(z):
+    """Alg 3 line 1 over C: P Z = L U.  Returns (lu_re, lu_im, ipiv, info), planar."""
+    re, im = split(z)
+    re, im = re.copy(), im.copy()
+    n = re.shape[0]
+    ipiv = np.zeros(max(n, 1), dtype=np.int32)
+    info = lib().or_zgetrf(n, _p(re), _p(im), _p(ipiv, ctypes.c_int))
+    return re, im, ipiv[:n], info
+
+
+def zgetrs(fac, r, trans: bool = False):
+    """Y = Z^{-1} R (trans=False) or Z^{-H} R (trans=True) from zgetrf's factors; R (n, k) or (n,)."""
+    lr, li, ipiv, _ = fac
+    r = np.asarray(r)
+    vec = r.ndim == 1
+    r2 = r.reshape(r.shape[0], -1)
+    yr, yi = _f64(r2.real).copy(), _f64(np.imag(r2)).copy()
+    n, k = yr.shape
+    lib().or_zgetrs(n, _p(lr), _p(li), _p(np.ascontiguousarray(ipiv, dtype=np.int32), ctypes.c_int),
+                    1 if trans else 0, k, _p(yr), _p(yi))
+    y = yr + 1j * yi
+    return y[:, 0] if vec else y
+
+
+def zsolve(z, r):
+    """Z^{-1} R by Gaussian elimination with partial pivoting (or_zgetrf + or_zgetrs)."""
+    fac = zgetrf(z)
+    if fac[3]:
+        raise np.linalg.LinAlgError(f"singular at column {fac[3]}")
+    return zgetrs(fac, r)
+
+
+def kappa2(z, fac=None, iters: int = 40, seed: int = 12345):
+    """Estimate of kappa_2(Z) = sigma_max / sigma_min (reading R10 / SURVEY G7).
+
+    sigma_max: power iteration on Z^H Z (numpy matvecs); sigma_min: inverse power iteration on
+    (Z^H Z)^{-1} = Z^{-1} Z^{-H} through zgetrs.  Both are Rayleigh-quotient estimates from
+    below, so the returned kappa is (up to convergence) a lower bound of the true one.
+    Returns (kappa, sigma_max, sigma_min)."""
+    z = np.asarray(z, dtype=np.complex128)
+    n = z.shape[0]
+    fac = fac if fac is not None else zgetrf(z)
+    rng = np.random.default_rng(seed)
+    v = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    v /= np.linalg.norm(v)
+    smax = 0.0
+    for _ in range(iters):
+        w = z @ v
+        smax = float(np.linalg.norm(w))
+        v = z.conj().T @ w
+        v /= np.linalg.norm(v)
+    u = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    u /= np.linalg.norm(u)
+    inv_smin = 0.0
+    for _ in range(iters):
+        w = zgetrs(fac, u, trans=True)           # Z^{-H} u
+        u = zgetrs(fac, w)                       # Z^{-1} Z^{-H} u
+        inv_smin = float(np.sqrt(np.linalg.norm(u)))   # ||(Z^H Z)^{-1} u|| -> 1 / sigma_min^2
+        u /= np.linalg.norm(u)
+    smin = 1.0 / inv_smin if inv_smin > 0 else 0.0
+    return (smax / smin if smin > 0 else float("inf")), smax, smin
+
+
+def frob_inv_many(zs, branch: str = "auto", tau: float = TAU_SWITCH):
+    """or_frob_inv on each matrix of zs (count, n, n), in parallel over matrices.
+
+    Returns (X (count, n, n), status int32[count], info int32[count], branch_used int32[count],
+    rho (count, 2) = (rho_A, rho_B))."""
+    zs = np.asarray(zs)
+    count, n = zs.shape[0], zs.shape[1]
+    a, b = _f64(zs.real), _f64(zs.imag)
+    xr = np.zeros_like(a)
+    xi = np.zeros_like(a)
+    out = np.zeros((count, 2), dtype=np.int32)
+    rho = np.zeros((count, 2), dtype=np.float64)
+    st = np.zeros(count, dtype=np.int32)
+    lib().or_frob_inv_many(count, n, _p(a), _p(b), _p(xr), _p(xi), BRANCH[branch], float(tau),
+                           _p(out, ctypes.c_int), _p(rho), _p(st, ctypes.c_int))
+    return xr + 1j * xi, st, out[:, 0].copy(), out[:, 1].copy(), rho
 
 
 def inverse(z, method: str = "frobenius"):

@@ -33,6 +33,10 @@
  *   or_zinv_gj       The plain definition: complex Gauss-Jordan inverse with partial
  *                    pivoting on |re|+|im| (the object Lemma 4.1, reaches exactly).
  *   or_zinv_lu       Alg 3 applied over C (the paper's comparator).
+ *   or_zgetrf        Alg 3 line 1 over C on its own; or_zgetrs solves Z Y = R or
+ *                    Z^H Y = R with its factors -- the plain definition of Z^{-1} R used for
+ *                    sketch parity at n >= 8192 (the object Lemma 4.1 reaches, applied to R).
+ *   or_frob_inv_many or_frob_inv on independent matrices (config 3 full-set parity).
  */
 #include <math.h>
 #include <stdlib.h>
@@ -598,6 +602,136 @@ int or_zinv_lu(int n, const double *zr, const double *zi, double *xr, double *xi
 done:
     free(ar); free(ai); free(wr); free(wi); free(ipiv);
     return info;
+}
+
+/* --------------------------------------------------------------- solves (sketch parity) */
+
+/* Alg 3 line 1 over C on its own: P Z = L U in place on (ar, ai) with partial
+ * pivoting on |re|+|im| (LAPACK izamax convention), ipiv[k] = row swapped with row k at
+ * step k (0-based, LAPACK order).  Right-looking, one column per step, exactly the
+ * elimination of or_zinv_lu line 1.  Returns 0 or the 1-based first exactly-zero pivot. */
+int or_zgetrf(int n, double *ar, double *ai, int *ipiv)
+{
+    int info = 0;
+    for (int k = 0; k < n; ++k) {
+        int p = k;
+        double best = cabs1(ar[(size_t)k * n + k], ai[(size_t)k * n + k]);
+        for (int i = k + 1; i < n; ++i) {
+            double v = cabs1(ar[(size_t)i * n + k], ai[(size_t)i * n + k]);
+            if (v > best) { best = v; p = i; }
+        }
+        ipiv[k] = p;
+        if (p != k) {
+            for (int j = 0; j < n; ++j) {
+                double t = ar[(size_t)k * n + j]; ar[(size_t)k * n + j] = ar[(size_t)p * n + j]; ar[(size_t)p * n + j] = t;
+                t = ai[(size_t)k * n + j]; ai[(size_t)k * n + j] = ai[(size_t)p * n + j]; ai[(size_t)p * n + j] = t;
+            }
+        }
+        double pr = ar[(size_t)k * n + k], pi = ai[(size_t)k * n + k];
+        if (pr == 0.0 && pi == 0.0) { if (!info) info = k + 1; continue; }
+        double den = pr * pr + pi * pi;
+        double ir = pr / den, ii = -pi / den;
+        #pragma omp parallel for schedule(static) if (n - k > 256)
+        for (int i = k + 1; i < n; ++i) {
+            double vr = ar[(size_t)i * n + k], vi = ai[(size_t)i * n + k];
+            double lr = vr * ir - vi * ii, li = vr * ii + vi * ir;
+            ar[(size_t)i * n + k] = lr; ai[(size_t)i * n + k] = li;
+            double *rr = ar + (size_t)i * n, *ri = ai + (size_t)i * n;
+            const double *kr = ar + (size_t)k * n, *ki = ai + (size_t)k * n;
+            for (int j = k + 1; j < n; ++j) {
+                rr[j] = rr[j] - (lr * kr[j] - li * ki[j]);
+                ri[j] = ri[j] - (lr * ki[j] + li * kr[j]);
+            }
+        }
+    }
+    return info;
+}
+
+/* Solve with the factors of or_zgetrf (P Z = L U), k right-hand sides in place on the
+ * row-major n x k arrays (br, bi):
+ *   trans = 0:  Z Y = R     -> apply the interchanges to R in order, L W = P R (forward
+ *               substitution, unit diagonal), U Y = W (back substitution);
+ *   trans = 1:  Z^H Y = R   (Z^H = U^H L^H P) -> U^H W = R (forward), L^H V = W (back,
+ *               unit diagonal), Y = P^T V (interchanges in reverse order).
+ * The plain definition of Y = Z^{-1} R (Z^{-H} R): Gaussian elimination on the augmented
+ * system.  Right-hand sides are independent (OpenMP over them). */
+void or_zgetrs(int n, const double *ar, const double *ai, const int *ipiv, int trans, int k,
+               double *br, double *bi)
+{
+    #pragma omp parallel for schedule(dynamic, 1) if (k > 1 && (long)n * n > 65536L)
+    for (int c = 0; c < k; ++c) {
+        double *yr = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+        double *yi = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+        for (int i = 0; i < n; ++i) { yr[i] = br[(size_t)i * k + c]; yi[i] = bi[(size_t)i * k + c]; }
+        if (trans == 0) {
+            for (int q = 0; q < n; ++q) {               /* P R */
+                int p = ipiv[q];
+                if (p != q) { double t = yr[q]; yr[q] = yr[p]; yr[p] = t; t = yi[q]; yi[q] = yi[p]; yi[p] = t; }
+            }
+            for (int i = 0; i < n; ++i) {               /* L W = P R */
+                double sr = yr[i], si = yi[i];
+                for (int q = 0; q < i; ++q) {
+                    double lr = ar[(size_t)i * n + q], li = ai[(size_t)i * n + q];
+                    sr = sr - (lr * yr[q] - li * yi[q]);
+                    si = si - (lr * yi[q] + li * yr[q]);
+                }
+                yr[i] = sr; yi[i] = si;
+            }
+            for (int i = n - 1; i >= 0; --i) {          /* U Y = W */
+                double sr = yr[i], si = yi[i];
+                for (int q = i + 1; q < n; ++q) {
+                    double ur = ar[(size_t)i * n + q], ui = ai[(size_t)i * n + q];
+                    sr = sr - (ur * yr[q] - ui * yi[q]);
+                    si = si - (ur * yi[q] + ui * yr[q]);
+                }
+                double dr = ar[(size_t)i * n + i], di = ai[(size_t)i * n + i];
+                double dd = dr * dr + di * di;          /* s / d = s conj(d) / |d|^2 */
+                yr[i] = (sr * dr + si * di) / dd;
+                yi[i] = (si * dr - sr * di) / dd;
+            }
+        } else {
+            for (int i = 0; i < n; ++i) {               /* U^H W = R: (U^H)[i][q] = conj(U[q][i]) */
+                double sr = yr[i], si = yi[i];
+                for (int q = 0; q < i; ++q) {
+                    double ur = ar[(size_t)q * n + i], ui = -ai[(size_t)q * n + i];
+                    sr = sr - (ur * yr[q] - ui * yi[q]);
+                    si = si - (ur * yi[q] + ui * yr[q]);
+                }
+                double dr = ar[(size_t)i * n + i], di = -ai[(size_t)i * n + i];
+                double dd = dr * dr + di * di;
+                yr[i] = (sr * dr + si * di) / dd;
+                yi[i] = (si * dr - sr * di) / dd;
+            }
+            for (int i = n - 1; i >= 0; --i) {          /* L^H V = W: (L^H)[i][q] = conj(L[q][i]) */
+                double sr = yr[i], si = yi[i];
+                for (int q = i + 1; q < n; ++q) {
+                    double lr = ar[(size_t)q * n + i], li = -ai[(size_t)q * n + i];
+                    sr = sr - (lr * yr[q] - li * yi[q]);
+                    si = si - (lr * yi[q] + li * yr[q]);
+                }
+                yr[i] = sr; yi[i] = si;
+            }
+            for (int q = n - 1; q >= 0; --q) {          /* Y = P^T V */
+                int p = ipiv[q];
+                if (p != q) { double t = yr[q]; yr[q] = yr[p]; yr[p] = t; t = yi[q]; yi[q] = yi[p]; yi[p] = t; }
+            }
+        }
+        for (int i = 0; i < n; ++i) { br[(size_t)i * k + c] = yr[i]; bi[(size_t)i * k + c] = yi[i]; }
+        free(yr); free(yi);
+    }
+}
+
+/* Alg 1 on `count` independent matrices (config 3 full-set parity): or_frob_inv per matrix,
+ * OpenMP over the matrices (each matrix's arithmetic is exactly or_frob_inv's). */
+int or_frob_inv_many(int count, int n, const double *A, const double *B, double *Xre, double *Xim,
+                     int branch, double tau_sw, int *out, double *rho, int *status)
+{
+    size_t nn = (size_t)n * n;
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int m = 0; m < count; ++m)
+        status[m] = or_frob_inv(n, A + m * nn, B + m * nn, Xre + m * nn, Xim + m * nn, branch, tau_sw,
+                                out + 2 * (size_t)m, rho + 2 * (size_t)m);
+    return 0;
 }
 
 /* thread count of the OpenMP loops (measurement control only: the arithmetic of every row is

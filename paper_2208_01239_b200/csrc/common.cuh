@@ -5,10 +5,22 @@
 #include <cstdint>
 #include <cstddef>
 #include <climits>
+#include <cstdlib>
 
 #define FROB_DEV __device__ __forceinline__
 
 namespace frob {
+
+// Tuning switches (A/B measurement aids) are read from the environment only in a tuning build
+// (-DFROB_TUNING, tools/); the shipped library always takes the measured defaults.
+inline const char *tuning_env(const char *name) {
+#ifdef FROB_TUNING
+    return std::getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
 
 // process-wide count of kernel launches issued by the library (frob_launch_count())
 unsigned long long &launch_counter();

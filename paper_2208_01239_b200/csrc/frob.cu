@@ -121,6 +121,81 @@ __global__ void copy2d_kernel(const T *__restrict__ src, long long lds, T *__res
     if (nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
 }
 
+// ---------------------------------------------------------------------- AUTO on the device
+// Reading R1 decided from the LU statistics without a host read (FROB_OPT_DEVICE_AUTO): both
+// LU(A) and LU(B) have run; flags[1] = 1 (S1), 2 (S2) or 0 (both singular).
+__global__ void auto_select_kernel(const LuStats *__restrict__ st, int *__restrict__ flags) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const LuStats a = st[0], b = st[1];
+    int use = 1;
+    if (a.info != 0 || !(a.rho <= 256.0)) {
+        const bool sa = a.info != 0, sb = b.info != 0;
+        use = (sa && sb) ? 0 : ((sa || (!sb && b.rho < a.rho)) ? 2 : 1);
+    }
+    flags[1] = use;
+}
+
+// flags[1] == 2: (A, B) <- (B, -A) in place, so the S1 code computes the S2 branch (X = B, Y = -A;
+// every step is the rotated S1 step bitwise, reading R3)
+__global__ void branch_rotate_kernel(double *__restrict__ A, double *__restrict__ B, long long ld, int n,
+                                     const int *__restrict__ flags) {
+    if (flags[1] != 2) return;
+    const long long total = (long long)n * n;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / n), j = (int)(idx - (long long)i * n);
+        const long long o = (long long)i * ld + j;
+        const double t = A[o];
+        A[o] = B[o];
+        B[o] = -t;
+    }
+}
+
+// flags[1] == 2: dst <- src (the S2 factors move into the S1 slots)
+template <typename T>
+__global__ void cond_copy_kernel(const T *__restrict__ src, T *__restrict__ dst, long long count,
+                                 const int *__restrict__ flags) {
+    if (flags[1] != 2) return;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < count;
+         idx += (long long)gridDim.x * blockDim.x)
+        dst[idx] = src[idx];
+}
+
+// Device status record of one call (frob_inv_dev / frob_inv_host_many's per-matrix status):
+// use_host = branch chosen on the host (1 | 2), or 0 = read flags[1] (device AUTO);
+// factored: bit 0 = LU(A) ran, bit 1 = LU(B) ran.
+__global__ void finalize_status_kernel(const LuStats *__restrict__ st, const int *__restrict__ flags, int use_host,
+                                       int factored, int forced_status, frob_dev_status *__restrict__ out,
+                                       int *__restrict__ status_copy) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int use = use_host ? use_host : flags[1];
+    int status = FROB_OK, info = 0;
+    if (forced_status) {
+        status = forced_status;
+    } else if (flags[0]) {
+        status = FROB_ERR_NONFINITE;
+    } else if (use == 0) {
+        status = FROB_ERR_BOTH_SINGULAR;
+        info = st[0].info;
+    } else {
+        const int ix = st[use - 1].info;
+        info = ix ? ix : st[2].info;
+        status = info ? FROB_ERR_SINGULAR : FROB_OK;
+    }
+    if (out) {
+        frob_dev_status r;
+        r.status = status;
+        r.info = info;
+        r.branch_used = (status == FROB_ERR_BOTH_SINGULAR || forced_status) ? 0 : use;
+        r.nonfinite = flags[0];
+        r.rho_a = (factored & 1) ? st[0].rho : NAN;
+        r.rho_b = (factored & 2) ? st[1].rho : NAN;
+        r.rho_m = (use && !forced_status) ? st[2].rho : NAN;
+        *out = r;
+    }
+    if (status_copy) *status_copy = status;
+}
+
 static int ew_blocks(long long total) {
     return (int)std::min<long long>((total + 255) / 256, 148LL * 8);
 }
@@ -196,10 +271,28 @@ static bool overlap(const void *a, size_t na, const void *b, size_t nb) {
 }
 
 // ---------------------------------------------------------------------- frob_inv
+// Optional outputs of one call: a device status record and/or a device int receiving the status
+// (frob_inv_host_many's per-matrix status), both written by finalize_status_kernel.
+struct StatusOut {
+    frob_dev_status *rec = nullptr;
+    int *code = nullptr;
+    bool any() const { return rec || code; }
+};
+
+static cudaError_t finalize_status(const FrobWs &w, int use_host, int factored, int forced, StatusOut so,
+                                   cudaStream_t s) {
+    if (!so.any()) return cudaSuccess;
+    count_launch();
+    finalize_status_kernel<<<1, 32, 0, s>>>(w.stats, w.flags, use_host, factored, forced, so.rec, so.code);
+    return cudaGetLastError();
+}
+
 static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *X, long long ldx,
                                  int branch, void *ws, size_t ws_bytes, cudaStream_t s,
-                                 frob_info *host_info, double mu = 0.0, bool fused = false) {
+                                 frob_info *host_info, double mu = 0.0, bool fused = false,
+                                 bool dev_auto = false, StatusOut so = StatusOut()) {
     if (n < 1 || !Z || !X || ldz < n || ldx < n || branch < 0 || branch > 2) return FROB_ERR_INVALID_ARG;
+    if (dev_auto && branch != FROB_BRANCH_AUTO) return FROB_ERR_INVALID_ARG;
     if (overlap(Z, (size_t)((n - 1) * ldz + n) * 16, X, (size_t)((n - 1) * ldx + n) * 16))
         return FROB_ERR_INVALID_ARG;
     FrobWs w = carve_frob(nullptr, n);
@@ -217,34 +310,47 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
 
     // a1: LU of the branch matrix (A unless forced B)
     int use = (branch == FROB_BRANCH_B) ? 2 : 1;
+    int factored = use;  // bit 0: LU(A) ran, bit 1: LU(B) ran
     int *perm = w.perm_x;
     double *Xlu = w.W1;
     // n <= LU2_MAX_N: latency-oriented LU (lu2.cu), factors come out split (U, L)
     const bool small = n <= lu2_max_n();
     double *Uf = w.W2, *Lf = w.W3;
-    if (small) FROB_CUDA(lu2_factor<double>(n, w.W1, w.W4, ld, w.W2, w.W3, ld, perm, w.iw, w.diag,
-                                            &w.stats[use == 1 ? 0 : 1], s));
-    else FROB_CUDA(getrf<double>(n, Xlu, ld, perm, w.mv, w.diag, &w.stats[use == 1 ? 0 : 1], w.work, s));
+    {
+        ProfScope ps("step:lu", s);
+        if (small) FROB_CUDA(lu2_factor<double>(n, w.W1, w.W4, ld, w.W2, w.W3, ld, perm, w.iw, w.diag,
+                                                &w.stats[use == 1 ? 0 : 1], s));
+        else FROB_CUDA(getrf<double>(n, Xlu, ld, perm, w.mv, w.diag, &w.stats[use == 1 ? 0 : 1], w.work, s));
+    }
+    auto lu_b = [&]() -> frob_status {
+        // LU(B) into the S2 slots (W5 / W6, W7 / perm_b), stats[1]
+        ProfScope ps("step:lu", s);
+        count_launch();
+        copy2d_kernel<double><<<ew_blocks((long long)n * n), 256, 0, s>>>(w.B, ld, w.W5, ld, n, nullptr);
+        FROB_CUDA(cudaGetLastError());
+        if (small) FROB_CUDA(lu2_factor<double>(n, w.W5, w.W4, ld, w.W6, w.W7, ld, w.perm_b, w.iw, w.diag,
+                                                &w.stats[1], s));
+        else FROB_CUDA(getrf<double>(n, w.W5, ld, w.perm_b, w.mv, w.diag, &w.stats[1], w.work, s));
+        factored |= 2;
+        return FROB_OK;
+    };
 
     LuStats hs[3];
     for (auto &h : hs) { h.rho = NAN; h.umax = 0; h.info = 0; h.nonfinite = 0; }
-    int hflags = 0;
-    if (branch == FROB_BRANCH_AUTO) {
+    int hflags[2] = {0, 0};
+    if (branch == FROB_BRANCH_AUTO && !dev_auto) {
         // a1': branch check (reading R1) -- one small device->host read
         FROB_CUDA(cudaMemcpyAsync(&hs[0], &w.stats[0], sizeof(LuStats), cudaMemcpyDeviceToHost, s));
-        FROB_CUDA(cudaMemcpyAsync(&hflags, w.flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+        FROB_CUDA(cudaMemcpyAsync(hflags, w.flags, sizeof(int), cudaMemcpyDeviceToHost, s));
         FROB_CUDA(cudaStreamSynchronize(s));
-        if (hflags) {
+        if (hflags[0]) {
             if (host_info) { host_info->info = 0; host_info->branch_used = 0; }
+            FROB_CUDA(finalize_status(w, 1, factored, FROB_ERR_NONFINITE, so, s));
             return FROB_ERR_NONFINITE;
         }
         if (hs[0].info != 0 || !(hs[0].rho <= 256.0)) {
-            count_launch();
-            copy2d_kernel<double><<<ew_blocks((long long)n * n), 256, 0, s>>>(w.B, ld, w.W5, ld, n, nullptr);
-            FROB_CUDA(cudaGetLastError());
-            if (small) FROB_CUDA(lu2_factor<double>(n, w.W5, w.W4, ld, w.W6, w.W7, ld, w.perm_b, w.iw, w.diag,
-                                                    &w.stats[1], s));
-            else FROB_CUDA(getrf<double>(n, w.W5, ld, w.perm_b, w.mv, w.diag, &w.stats[1], w.work, s));
+            const frob_status st = lu_b();
+            if (st != FROB_OK) return st;
             FROB_CUDA(cudaMemcpyAsync(&hs[1], &w.stats[1], sizeof(LuStats), cudaMemcpyDeviceToHost, s));
             FROB_CUDA(cudaStreamSynchronize(s));
             const bool sa = hs[0].info != 0, sb = hs[1].info != 0;
@@ -253,6 +359,7 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
                     host_info->info = hs[0].info; host_info->branch_used = 0;
                     host_info->rho_a = hs[0].rho; host_info->rho_b = hs[1].rho; host_info->rho_m = NAN;
                 }
+                FROB_CUDA(finalize_status(w, 1, factored, FROB_ERR_BOTH_SINGULAR, so, s));
                 return FROB_ERR_BOTH_SINGULAR;
             }
             if (sa || (!sb && hs[1].rho < hs[0].rho)) {
@@ -263,6 +370,24 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
                 Lf = w.W7;
             }
         }
+    } else if (dev_auto) {
+        // a1' on the device: LU(B) always, the decision in a one-thread kernel, the S2 factors and
+        // the rotated parts (B, -A) moved into the S1 slots by predicated kernels (no host read)
+        const frob_status st = lu_b();
+        if (st != FROB_OK) return st;
+        count_launch(small ? 5 : 4);
+        auto_select_kernel<<<1, 32, 0, s>>>(w.stats, w.flags);
+        FROB_CUDA(cudaGetLastError());
+        const long long mat = (long long)n * ld;
+        if (small) {
+            cond_copy_kernel<double><<<ew_blocks(mat), 256, 0, s>>>(w.W6, w.W2, mat, w.flags);
+            cond_copy_kernel<double><<<ew_blocks(mat), 256, 0, s>>>(w.W7, w.W3, mat, w.flags);
+        } else {
+            cond_copy_kernel<double><<<ew_blocks(mat), 256, 0, s>>>(w.W5, w.W1, mat, w.flags);
+        }
+        cond_copy_kernel<int><<<ew_blocks(n), 256, 0, s>>>(w.perm_b, w.perm_x, n, w.flags);
+        branch_rotate_kernel<<<ew_blocks((long long)n * n), 256, 0, s>>>(w.A, w.B, ld, n, w.flags);
+        FROB_CUDA(cudaGetLastError());
     }
     const double *Xm = (use == 1) ? w.A : w.B;   // X of Alg 1
     const double *Ym = (use == 1) ? w.B : w.A;   // Y of Alg 1 (S2 uses Y = -A via sgn)
@@ -271,12 +396,16 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
     double *Cb;  // C = X^{-1} Y
     if (!fused) {
         // a2: Xinv' = U^{-1} L^{-1}  (X^{-1} = Xinv' P)
-        if (small) FROB_CUDA(inv_from_ul<double>(n, Uf, Lf, ld, w.W1, w.W4, ld, nullptr, w.flags + 2, s));
-        else FROB_CUDA(inv_from_lu<double>(n, Xlu, ld, w.W2, w.W3, w.W4, ld, nullptr, w.flags + 2, s));
+        {
+            ProfScope ps("step:inv_from_lu", s);
+            if (small) FROB_CUDA(inv_from_ul<double>(n, Uf, Lf, ld, w.W1, w.W4, ld, nullptr, w.flags + 2, s));
+            else FROB_CUDA(inv_from_lu<double>(n, Xlu, ld, w.W2, w.W3, w.W4, ld, nullptr, w.flags + 2, s));
+        }
         // a3: C = X^{-1} Y = Xinv' (P Y)   [B-row gather]
         Cb = w.W2;
         auto p = gemm_params<double>(n, n, n, sgn, w.W4, ld, Ym, ld, 0.0, nullptr, ld, Cb, ld);
         p.browmap = perm;
+        GemmTag tag("gemm:frob_C");
         FROB_CUDA(gemm_launch<double>(p, 1, s));
     } else {
         // a2+a3 fused (NEXT-1): C = U^{-1} (L^{-1} (P Y)); X^{-1} is never formed
@@ -286,6 +415,7 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
             Lf = w.W3;
         }
         FROB_CUDA(tri_inverses<double>(n, Uf, Lf, ld, w.W1, s));
+        GemmTag tag("gemm:frob_C_tri");
         auto p = gemm_params<double>(n, n, n, sgn, Lf, ld, Ym, ld, 0.0, nullptr, ld, w.W4, ld);
         p.triA = TRI_LOWER;
         p.browmap = perm;
@@ -298,37 +428,60 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
     // a4: M = X + Y C
     {
         auto p = gemm_params<double>(n, n, n, sgn, Ym, ld, Cb, ld, 1.0, Xm, ld, w.W3, ld);
+        GemmTag tag("gemm:frob_M");
         FROB_CUDA(gemm_launch<double>(p, 1, s));
     }
     // a5: Re' = M^{-1} (un-permuted); scratch: the two buffers not holding C
     double *Re = (use == 1) ? w.A : w.B;  // X buffer is free now
     double *Sa = fused ? w.W2 : w.W1;
     if (small) {
-        FROB_CUDA(lu2_factor<double>(n, w.W3, Sa, ld, w.W4, w.W5, ld, w.perm_m, w.iw, w.diag, &w.stats[2], s));
+        {
+            ProfScope ps("step:lu", s);
+            FROB_CUDA(lu2_factor<double>(n, w.W3, Sa, ld, w.W4, w.W5, ld, w.perm_m, w.iw, w.diag, &w.stats[2], s));
+        }
+        ProfScope ps("step:inv_from_lu", s);
         FROB_CUDA(inv_from_ul<double>(n, w.W4, w.W5, ld, w.W3, Re, ld, nullptr, w.flags + 2, s));
     } else {
-        FROB_CUDA(getrf<double>(n, w.W3, ld, w.perm_m, w.mv, w.diag, &w.stats[2], w.work, s));
+        {
+            ProfScope ps("step:lu", s);
+            FROB_CUDA(getrf<double>(n, w.W3, ld, w.perm_m, w.mv, w.diag, &w.stats[2], w.work, s));
+        }
+        ProfScope ps("step:inv_from_lu", s);
         FROB_CUDA(inv_from_lu<double>(n, w.W3, ld, Sa, w.W4, Re, ld, nullptr, w.flags + 2, s));
     }
     // a6/a7: Im' = -C Re', fused with the column interchanges and the interleaved store
     {
         auto p = gemm_params<double>(n, n, n, -1.0, Cb, ld, Re, ld, 0.0, Re, ld, X, ldx);
         p.epi = (use == 1) ? EPI_FROB_A : EPI_FROB_B;
+        p.dbranch = dev_auto ? w.flags + 1 : nullptr;
         p.colperm = w.perm_m;
         p.mu = mu;  // Alg 5 line 5: Z^{-1} = (1 + mu i) W
+        GemmTag tag("gemm:frob_Im");
         FROB_CUDA(gemm_launch<double>(p, 1, s));
     }
+    FROB_CUDA(finalize_status(w, dev_auto ? 0 : use, factored, 0, so, s));
     if (host_info) {
         FROB_CUDA(cudaMemcpyAsync(hs, w.stats, 3 * sizeof(LuStats), cudaMemcpyDeviceToHost, s));
-        FROB_CUDA(cudaMemcpyAsync(&hflags, w.flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+        FROB_CUDA(cudaMemcpyAsync(hflags, w.flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
         FROB_CUDA(cudaStreamSynchronize(s));
+        if (dev_auto) use = hflags[1];
+        if (hflags[0]) {
+            host_info->info = 0;
+            host_info->branch_used = 0;
+            return FROB_ERR_NONFINITE;
+        }
+        host_info->rho_a = (factored & 1) ? hs[0].rho : NAN;
+        host_info->rho_b = (factored & 2) ? hs[1].rho : NAN;
+        if (use == 0) {
+            host_info->info = hs[0].info;
+            host_info->branch_used = 0;
+            host_info->rho_m = NAN;
+            return FROB_ERR_BOTH_SINGULAR;
+        }
         host_info->branch_used = use;
-        host_info->rho_a = (use == 1 || branch == FROB_BRANCH_AUTO) ? hs[0].rho : NAN;
-        host_info->rho_b = (use == 2 || (branch == FROB_BRANCH_AUTO && !std::isnan(hs[1].rho))) ? hs[1].rho : NAN;
         host_info->rho_m = hs[2].rho;
         const int ix = (use == 1) ? hs[0].info : hs[1].info;
         host_info->info = ix ? ix : hs[2].info;
-        if (hflags) return FROB_ERR_NONFINITE;
         if (host_info->info) return FROB_ERR_SINGULAR;
     }
     return FROB_OK;
@@ -647,13 +800,22 @@ frob_status frob_inv_rand(int n, const double *Z, long long ldz, double *X, long
 
 frob_status frob_inv_opts(int n, const double *Z, long long ldz, double *X, long long ldx, int branch, int options,
                           void *ws, size_t ws_bytes, void *stream, frob_info *host_info) {
-    if (options & ~FROB_OPT_FUSED_FIRST_STEP) return FROB_ERR_INVALID_ARG;
+    if (options & ~(FROB_OPT_FUSED_FIRST_STEP | FROB_OPT_DEVICE_AUTO)) return FROB_ERR_INVALID_ARG;
     return frob_inv_impl(n, Z, ldz, X, ldx, branch, ws, ws_bytes, (cudaStream_t)stream, host_info, 0.0,
-                         (options & FROB_OPT_FUSED_FIRST_STEP) != 0);
+                         (options & FROB_OPT_FUSED_FIRST_STEP) != 0, (options & FROB_OPT_DEVICE_AUTO) != 0);
+}
+
+frob_status frob_inv_dev(int n, const double *Z, long long ldz, double *X, long long ldx, int branch, int options,
+                         frob_dev_status *d_status, void *ws, size_t ws_bytes, void *stream) {
+    if (options & ~(FROB_OPT_FUSED_FIRST_STEP | FROB_OPT_DEVICE_AUTO)) return FROB_ERR_INVALID_ARG;
+    StatusOut so;
+    so.rec = d_status;
+    return frob_inv_impl(n, Z, ldz, X, ldx, branch, ws, ws_bytes, (cudaStream_t)stream, nullptr, 0.0,
+                         (options & FROB_OPT_FUSED_FIRST_STEP) != 0, (options & FROB_OPT_DEVICE_AUTO) != 0, so);
 }
 
 size_t frob_inv_host_workspace_bytes(int n) {
-    return n < 1 ? 0 : align256(frob_inv_workspace_bytes(n)) + 2 * align256((size_t)n * n * 16);
+    return n < 1 ? 0 : align256(frob_inv_workspace_bytes(n)) + 2 * align256((size_t)n * n * 16) + 256;
 }
 
 frob_status frob_inv_host(int n, const double *Z_host, double *X_host, int branch, void *ws,
@@ -665,16 +827,24 @@ frob_status frob_inv_host(int n, const double *Z_host, double *X_host, int branc
     const size_t ib = align256(frob_inv_workspace_bytes(n));
     double *Zd = reinterpret_cast<double *>(b + ib);
     double *Xd = reinterpret_cast<double *>(b + ib + align256((size_t)n * n * 16));
+    StatusOut so;
+    so.code = reinterpret_cast<int *>(b + ib + 2 * align256((size_t)n * n * 16));
     FROB_CUDA(cudaMemcpyAsync(Zd, Z_host, (size_t)n * n * 16, cudaMemcpyHostToDevice, s));
-    frob_status st = frob_inv_impl(n, Zd, n, Xd, n, branch, ws, ib, s, host_info);
+    frob_status st = frob_inv_impl(n, Zd, n, Xd, n, branch, ws, ib, s, host_info, 0.0, false, false, so);
+    int code = FROB_OK;
+    if (st == FROB_OK) {
+        FROB_CUDA(cudaMemcpyAsync(X_host, Xd, (size_t)n * n * 16, cudaMemcpyDeviceToHost, s));
+        FROB_CUDA(cudaMemcpyAsync(&code, so.code, sizeof(int), cudaMemcpyDeviceToHost, s));
+    }
+    // every path waits for the copies that read / write the caller's host buffers
+    const cudaError_t e = cudaStreamSynchronize(s);
     if (st != FROB_OK) return st;
-    FROB_CUDA(cudaMemcpyAsync(X_host, Xd, (size_t)n * n * 16, cudaMemcpyDeviceToHost, s));
-    FROB_CUDA(cudaStreamSynchronize(s));
-    return FROB_OK;
+    if (e != cudaSuccess) return cuda_fail(e);
+    return (frob_status)code;
 }
 
 size_t frob_inv_host_many_workspace_bytes(int n) {
-    return n < 1 ? 0 : align256(frob_inv_workspace_bytes(n)) + 4 * align256((size_t)n * n * 16);
+    return n < 1 ? 0 : align256(frob_inv_workspace_bytes(n)) + 4 * align256((size_t)n * n * 16) + 2 * 256;
 }
 
 // per-device copy streams and events of the pipelined host entry point
@@ -703,8 +873,25 @@ static HostPipe &host_pipe(cudaError_t &err) {
     return p;
 }
 
-frob_status frob_inv_host_many(int n, int count, const double *Z_host, double *X_host, int branch, void *ws,
-                               size_t ws_bytes, void *stream) {
+// Join both copy streams into `s` and wait for everything (every exit path of the pipelined entry
+// points: no copy into or out of the caller's host buffers is still in flight on return).
+static cudaError_t host_pipe_join(HostPipe &hp, cudaStream_t s) {
+    cudaError_t first = cudaEventRecord(hp.fin, hp.d2h);
+    if (first == cudaSuccess) first = cudaStreamWaitEvent(s, hp.fin, 0);
+    cudaError_t e = cudaEventRecord(hp.fin, hp.h2d);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, hp.fin, 0);
+    if (first == cudaSuccess) first = e;
+    e = cudaStreamSynchronize(s);
+    if (first == cudaSuccess) first = e;
+    if (first != cudaSuccess) {  // a failed join: fall back to waiting on each stream
+        cudaStreamSynchronize(hp.h2d);
+        cudaStreamSynchronize(hp.d2h);
+    }
+    return first;
+}
+
+frob_status frob_inv_host_many(int n, int count, const double *Z_host, double *X_host, int branch, int *h_status,
+                               void *ws, size_t ws_bytes, void *stream) {
     if (n < 1 || count < 0 || (count > 0 && (!Z_host || !X_host))) return FROB_ERR_INVALID_ARG;
     if (count == 0) return FROB_OK;
     if (!ws || ws_bytes < frob_inv_host_many_workspace_bytes(n)) return FROB_ERR_WORKSPACE;
@@ -713,18 +900,20 @@ frob_status frob_inv_host_many(int n, int count, const double *Z_host, double *X
     HostPipe &hp = host_pipe(ce);
     FROB_CUDA(ce);
     std::lock_guard<std::mutex> guard(hp.mu);
+    // per-matrix device status: the caller's array, else a pinned one of our own
+    int *codes = h_status;
+    if (!codes) FROB_CUDA(cudaHostAlloc(&codes, (size_t)count * sizeof(int), cudaHostAllocDefault));
+    for (int i = 0; i < count; ++i) codes[i] = FROB_ERR_INVALID_ARG;  // "not computed"
     const size_t mb = (size_t)n * n * 16, md = (size_t)n * n * 2;  // bytes / doubles per matrix
     unsigned char *b = reinterpret_cast<unsigned char *>(ws);
     const size_t ib = align256(frob_inv_workspace_bytes(n));
     double *Zd[2], *Xd[2];
+    int *Cd[2];
     for (int k = 0; k < 2; ++k) {
         Zd[k] = reinterpret_cast<double *>(b + ib + (2 * k) * align256(mb));
         Xd[k] = reinterpret_cast<double *>(b + ib + (2 * k + 1) * align256(mb));
+        Cd[k] = reinterpret_cast<int *>(b + ib + 4 * align256(mb) + k * 256);
     }
-    // the copy streams start after everything already queued on `stream`
-    FROB_CUDA(cudaEventRecord(hp.start, s));
-    FROB_CUDA(cudaStreamWaitEvent(hp.h2d, hp.start, 0));
-    FROB_CUDA(cudaStreamWaitEvent(hp.d2h, hp.start, 0));
     auto h2d = [&](int i) -> cudaError_t {
         const int k = i & 1;
         cudaError_t e = cudaSuccess;
@@ -734,28 +923,36 @@ frob_status frob_inv_host_many(int n, int count, const double *Z_host, double *X
         return e;
     };
     frob_status result = FROB_OK;
-    FROB_CUDA(h2d(0));
-    for (int i = 0; i < count; ++i) {
+    cudaError_t err = cudaEventRecord(hp.start, s);  // the copy streams start after the work queued on `stream`
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(hp.h2d, hp.start, 0);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(hp.d2h, hp.start, 0);
+    if (err == cudaSuccess) err = h2d(0);
+    for (int i = 0; i < count && err == cudaSuccess; ++i) {
         const int k = i & 1;
-        if (i + 1 < count) FROB_CUDA(h2d(i + 1));  // queued before inversion i (which may read the host)
-        FROB_CUDA(cudaStreamWaitEvent(s, hp.in[k], 0));
-        if (i >= 2) FROB_CUDA(cudaStreamWaitEvent(s, hp.freed[k], 0));  // X of i - 2 has left Xd[k]
-        const frob_status st = frob_inv_impl(n, Zd[k], n, Xd[k], n, branch, ws, ib, s, nullptr);
+        if (i + 1 < count && (err = h2d(i + 1)) != cudaSuccess) break;  // queued before inversion i
+        if ((err = cudaStreamWaitEvent(s, hp.in[k], 0)) != cudaSuccess) break;
+        if (i >= 2 && (err = cudaStreamWaitEvent(s, hp.freed[k], 0)) != cudaSuccess) break;  // X of i - 2 left Xd[k]
+        StatusOut so;
+        so.code = Cd[k];
+        const frob_status st = frob_inv_impl(n, Zd[k], n, Xd[k], n, branch, ws, ib, s, nullptr, 0.0, false, false, so);
         if (st != FROB_OK) {
             result = st;
+            codes[i] = st;
             break;
         }
-        FROB_CUDA(cudaEventRecord(hp.done[k], s));
-        FROB_CUDA(cudaStreamWaitEvent(hp.d2h, hp.done[k], 0));
-        FROB_CUDA(cudaMemcpyAsync(X_host + (size_t)i * md, Xd[k], mb, cudaMemcpyDeviceToHost, hp.d2h));
-        FROB_CUDA(cudaEventRecord(hp.freed[k], hp.d2h));
+        if ((err = cudaEventRecord(hp.done[k], s)) != cudaSuccess) break;
+        if ((err = cudaStreamWaitEvent(hp.d2h, hp.done[k], 0)) != cudaSuccess) break;
+        if ((err = cudaMemcpyAsync(X_host + (size_t)i * md, Xd[k], mb, cudaMemcpyDeviceToHost, hp.d2h)) != cudaSuccess) break;
+        if ((err = cudaMemcpyAsync(codes + i, Cd[k], sizeof(int), cudaMemcpyDeviceToHost, hp.d2h)) != cudaSuccess) break;
+        if ((err = cudaEventRecord(hp.freed[k], hp.d2h)) != cudaSuccess) break;
     }
-    // join both copy streams back into `stream`, then wait for everything
-    FROB_CUDA(cudaEventRecord(hp.fin, hp.d2h));
-    FROB_CUDA(cudaStreamWaitEvent(s, hp.fin, 0));
-    FROB_CUDA(cudaEventRecord(hp.fin, hp.h2d));
-    FROB_CUDA(cudaStreamWaitEvent(s, hp.fin, 0));
-    FROB_CUDA(cudaStreamSynchronize(s));
+    const cudaError_t ej = host_pipe_join(hp, s);
+    if (err == cudaSuccess) err = ej;
+    if (result == FROB_OK && err == cudaSuccess)
+        for (int i = 0; i < count; ++i)
+            if (codes[i] != FROB_OK) { result = (frob_status)codes[i]; break; }
+    if (!h_status) cudaFreeHost(codes);
+    if (err != cudaSuccess) return cuda_fail(err);
     return result;
 }
 
@@ -788,9 +985,6 @@ frob_status frob_inv_batched_host(int n, int batch, const double *Z_host, double
         Bu[k] = b + 4 * mb + 2 * ib + k * align256((size_t)chunk);
     }
     const int nch = (batch + chunk - 1) / chunk;
-    FROB_CUDA(cudaEventRecord(hp.start, s));
-    FROB_CUDA(cudaStreamWaitEvent(hp.h2d, hp.start, 0));
-    FROB_CUDA(cudaStreamWaitEvent(hp.d2h, hp.start, 0));
     auto cnt = [&](int j) { return std::min(chunk, batch - j * chunk); };
     auto h2d = [&](int j) -> cudaError_t {
         const int k = j & 1;
@@ -803,32 +997,34 @@ frob_status frob_inv_batched_host(int n, int batch, const double *Z_host, double
         return e;
     };
     frob_status result = FROB_OK;
-    FROB_CUDA(h2d(0));
-    for (int j = 0; j < nch; ++j) {
+    cudaError_t err = cudaEventRecord(hp.start, s);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(hp.h2d, hp.start, 0);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(hp.d2h, hp.start, 0);
+    if (err == cudaSuccess) err = h2d(0);
+    for (int j = 0; j < nch && err == cudaSuccess; ++j) {
         const int k = j & 1, c = cnt(j);
-        if (j + 1 < nch) FROB_CUDA(h2d(j + 1));
-        FROB_CUDA(cudaStreamWaitEvent(s, hp.in[k], 0));
-        if (j >= 2) FROB_CUDA(cudaStreamWaitEvent(s, hp.freed[k], 0));
+        if (j + 1 < nch && (err = h2d(j + 1)) != cudaSuccess) break;
+        if ((err = cudaStreamWaitEvent(s, hp.in[k], 0)) != cudaSuccess) break;
+        if (j >= 2 && (err = cudaStreamWaitEvent(s, hp.freed[k], 0)) != cudaSuccess) break;
         const frob_status st = frob_inv_batched(n, c, Zd[k], (long long)n * n, Xd[k], (long long)n * n, branch, Id[k],
                                                 Bu[k], nullptr, 0, s);
         if (st != FROB_OK) {
             result = st;
             break;
         }
-        FROB_CUDA(cudaEventRecord(hp.done[k], s));
-        FROB_CUDA(cudaStreamWaitEvent(hp.d2h, hp.done[k], 0));
-        FROB_CUDA(cudaMemcpyAsync(X_host + (size_t)j * chunk * md, Xd[k], (size_t)c * md * 8, cudaMemcpyDeviceToHost,
-                                  hp.d2h));
-        if (h_info)
-            FROB_CUDA(cudaMemcpyAsync(h_info + (size_t)j * chunk, Id[k], (size_t)c * sizeof(int),
-                                      cudaMemcpyDeviceToHost, hp.d2h));
-        FROB_CUDA(cudaEventRecord(hp.freed[k], hp.d2h));
+        if ((err = cudaEventRecord(hp.done[k], s)) != cudaSuccess) break;
+        if ((err = cudaStreamWaitEvent(hp.d2h, hp.done[k], 0)) != cudaSuccess) break;
+        if ((err = cudaMemcpyAsync(X_host + (size_t)j * chunk * md, Xd[k], (size_t)c * md * 8, cudaMemcpyDeviceToHost,
+                                   hp.d2h)) != cudaSuccess)
+            break;
+        if (h_info && (err = cudaMemcpyAsync(h_info + (size_t)j * chunk, Id[k], (size_t)c * sizeof(int),
+                                             cudaMemcpyDeviceToHost, hp.d2h)) != cudaSuccess)
+            break;
+        if ((err = cudaEventRecord(hp.freed[k], hp.d2h)) != cudaSuccess) break;
     }
-    FROB_CUDA(cudaEventRecord(hp.fin, hp.d2h));
-    FROB_CUDA(cudaStreamWaitEvent(s, hp.fin, 0));
-    FROB_CUDA(cudaEventRecord(hp.fin, hp.h2d));
-    FROB_CUDA(cudaStreamWaitEvent(s, hp.fin, 0));
-    FROB_CUDA(cudaStreamSynchronize(s));
+    const cudaError_t ej = host_pipe_join(hp, s);
+    if (err == cudaSuccess) err = ej;
+    if (err != cudaSuccess) return cuda_fail(err);
     return result;
 }
 
@@ -880,6 +1076,19 @@ frob_status frob_dgemm(int m, int n, int k, double alpha, const double *A, long 
     if (m < 0 || n < 0 || k < 0 || (m > 0 && n > 0 && (!C || ldc < n)) || (k > 0 && (!A || !B || lda < k || ldb < n)))
         return FROB_ERR_INVALID_ARG;
     auto p = gemm_params<double>(m, n, k, alpha, A, lda, B, ldb, beta, beta != 0.0 ? C : nullptr, ldc, C, ldc);
+    FROB_CUDA(gemm_launch<double>(p, 1, (cudaStream_t)stream));
+    return FROB_OK;
+}
+
+frob_status frob_dtrmm(int uplo, int n, int m, double alpha, const double *T, long long ldt, const double *B,
+                       long long ldb, double *C, long long ldc, void *stream) {
+    if ((uplo != TRI_UPPER && uplo != TRI_LOWER) || n < 0 || m < 0 ||
+        (n > 0 && (!T || !B || !C || ldt < n || ldb < m || ldc < m)))
+        return FROB_ERR_INVALID_ARG;
+    if (n == 0 || m == 0) return FROB_OK;
+    auto p = gemm_params<double>(n, m, n, alpha, T, ldt, B, ldb, 0.0, nullptr, ldc, C, ldc);
+    p.triA = uplo;
+    GemmTag tag("gemm:trmm");
     FROB_CUDA(gemm_launch<double>(p, 1, (cudaStream_t)stream));
     return FROB_OK;
 }

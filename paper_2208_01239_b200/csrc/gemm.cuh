@@ -41,6 +41,8 @@ struct GemmParams {
     int early_trigger;               // set by the launcher: release dependents at entry
                                      // (single-wave grids) instead of after the main loop
     double mu;                       // EPI_FROB_*: output scaled by (1 + mu i) (Alg 5 line 5)
+    const int *dbranch;              // EPI_FROB_*, nullable: branch read on the device (*dbranch == 2
+                                     // -> EPI_FROB_B, else EPI_FROB_A; AUTO decided on the device)
     int force_split;                 // request split-K even above the tile-count threshold
     int ksplit;                      // set by the launcher: > 1 = split-K over a (1, 1, ksplit)
                                      // cluster; the partials meet in distributed shared memory
@@ -387,7 +389,8 @@ FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int ro
                     if (p.epi != EPI_STORE) {
                         const double d = dv[j][e];
                         double2 *X = reinterpret_cast<double2 *>(Cp);
-                        double2 o = (p.epi == EPI_FROB_A) ? make_double2(d, v) : make_double2(v, -d);
+                        const int epi = p.dbranch ? (*p.dbranch == 2 ? EPI_FROB_B : EPI_FROB_A) : p.epi;
+                        double2 o = (epi == EPI_FROB_A) ? make_double2(d, v) : make_double2(v, -d);
                         if (p.mu != 0.0) o = make_double2(o.x - p.mu * o.y, p.mu * o.x + o.y);
                         X[(long long)row * p.ldc + oc[j][e]] = o;
                         continue;

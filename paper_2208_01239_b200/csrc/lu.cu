@@ -93,7 +93,7 @@ static cudaError_t gemm_launch_cfg(const GemmPair<T> &pp, int batch0, int batch1
     // policy (tuning aid, env FROB_PDL_GEMM): 0 = release after the main loop, 1 = early for
     // single-wave grids, 2 = always early; default 0 (measured best)
     static int policy = [] {
-        const char *v = getenv("FROB_PDL_GEMM");
+        const char *v = tuning_env("FROB_PDL_GEMM");
         return v ? atoi(v) : 0;
     }();
     const bool early = policy == 2 || (policy == 1 && ctas <= 148LL * (BIG ? 1 : 3));
@@ -1049,7 +1049,7 @@ cudaError_t inv_from_ul(int n, T *U, T *L, long long ld, T *tmp, T *out, long lo
     // otherwise; measured 236 -> 220 us real, 597 -> 529 us complex at n = 1024), n <= 2048
     // persistent longest-first CTAs, beyond a plain grid (env FROB_PRODUCT=0/1 forces one)
     static int prod_mode = [] {
-        const char *v = getenv("FROB_PRODUCT");
+        const char *v = tuning_env("FROB_PRODUCT");
         return v ? atoi(v) : -1;
     }();
     const int mode = prod_mode >= 0 ? prod_mode : (n <= 1024 ? 1 : 0);
@@ -1229,7 +1229,7 @@ static cudaError_t panel_step2(int n, T *A, long long lda, const CUtensorMap &tm
 // new panels unless env FROB_GETRF_PANEL=old (A/B measurement aid)
 static bool getrf_new_panels() {
     static bool v = [] {
-        const char *e = getenv("FROB_GETRF_PANEL");
+        const char *e = tuning_env("FROB_GETRF_PANEL");
         return !(e && e[0] == 'o');
     }();
     return v;
@@ -1261,7 +1261,7 @@ static cudaError_t outer_update(int n, T *A, long long lda, int K0, int W, int c
 // lu2 for the last trailing matrix unless env FROB_GETRF_TAIL=0 (A/B measurement aid)
 static bool getrf_tail() {
     static bool v = [] {
-        const char *e = getenv("FROB_GETRF_TAIL");
+        const char *e = tuning_env("FROB_GETRF_TAIL");
         return !(e && e[0] == '0');
     }();
     return v;
@@ -1270,7 +1270,7 @@ static bool getrf_tail() {
 // chain / far-column stream priorities unless env FROB_LU_PRIO=0 (A/B measurement aid)
 static bool getrf_prio() {
     static bool v = [] {
-        const char *e = getenv("FROB_LU_PRIO");
+        const char *e = tuning_env("FROB_LU_PRIO");
         return !(e && e[0] == '0');
     }();
     return v;

@@ -78,14 +78,6 @@ cudaError_t lu2_panel_inplace(const CUtensorMap &tm, T *A, long long lda, int n,
 template <typename T>
 cudaError_t lu2_factor(int n, T *B0, T *B1, long long ld, T *U, T *L, long long ldo, int *perm, int *iw, T *diag,
                        LuStats *stats, cudaStream_t s);
-// Persistent LU (lu3.cu) for n <= LU3_MAX_N: A (n x ld) is destroyed (it keeps the
-// L multipliers by original row), U and L come out split in final row order (ld);
-// iw = lu3_int_elems(n) ints.
-constexpr int LU3_MAX_N = 1024;
-size_t lu3_int_elems(int n);
-template <typename T>
-cudaError_t lu3_factor(int n, T *A, long long ld, T *U, T *L, int *perm, int *iw, T *diag, LuStats *stats,
-                       cudaStream_t s);
 template <typename T>
 cudaError_t lu_stats_launch(const T *diag, int n, LuStats *st, cudaStream_t s);
 // U = triu(lu) (zeros below), L = tril(lu, -1) + I (zeros above)

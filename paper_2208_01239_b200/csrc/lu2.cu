@@ -1488,7 +1488,7 @@ static bool panel2c_cluster_fits(int cs) {
 
 int lu2_panel_max_m() {
     static int v = [] {
-        const char *e = getenv("FROB_P2C_MAX");
+        const char *e = tuning_env("FROB_P2C_MAX");
         int cs = e ? atoi(e) : P2C_MAX;
         cs = (cs >= 1 && cs < P2C_MAX) ? cs : P2C_MAX;
         // clusters above the portable 8 need 16 free SMs in one GPC: keep 8 if they do not fit
@@ -1500,7 +1500,7 @@ int lu2_panel_max_m() {
 
 int lu2_max_n() {
     static int v = [] {
-        const char *e = getenv("FROB_LU2_MAX");
+        const char *e = tuning_env("FROB_LU2_MAX");
         const int x = e ? atoi(e) : LU2_MAX_N;
         return x < LU2_MAX_N ? x : LU2_MAX_N;
     }();
@@ -1595,7 +1595,7 @@ template cudaError_t lu2_panel_inplace<double2>(const CUtensorMap &, double2 *, 
 // 3.45 / 37.9 ms vs 3.88 / 38.9 with mode 2.
 static int lu2_lookahead(bool cplx) {
     static int v = [] {
-        const char *e = getenv("FROB_LU2_LOOKAHEAD");
+        const char *e = tuning_env("FROB_LU2_LOOKAHEAD");
         return e ? atoi(e) : -1;
     }();
     return v >= 0 ? v : ((cplx || Panel2W<double>::PW == Panel2W<double>::PH) ? 2 : 1);

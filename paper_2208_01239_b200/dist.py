@@ -49,3 +49,39 @@ def sum_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def instances_for_rank(total: int, rank: int, world: int) -> list[int]:
+    """Global instance indices a rank solves when `total` independent instances are spread over the
+    ranks (configs 4 / 5 with --instances: 8 instances over 1/2/4/8 GPUs -> 8/k per rank)."""
+    b, e = shard_range(total, rank, world)
+    return list(range(b, e))
+
+
+def gather_stats(stats: dict) -> list[dict]:
+    """all_gather of a small per-rank record (elapsed, units, errors, branch counts, iterations):
+    the only payload the multi-GPU path exchanges besides the timing reductions."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [dict(stats)]
+    out: list = [None] * dist.get_world_size()
+    dist.all_gather_object(out, dict(stats))
+    return out
+
+
+def summarize(times_ms: list[float], units_local: float, stats: dict, device=None) -> dict:
+    """The bench's reduction of one timed region: elapsed = MAX over ranks of the per-rank sum of
+    step times, units = SUM over ranks, value = units / elapsed (whole-job throughput), plus the
+    all-gathered per-rank records.  Shared by bench.py and the gloo tests."""
+    local_ms = float(sum(times_ms))
+    total_ms = max_over_ranks(local_ms, device)
+    units_all = sum_over_ranks(float(units_local), device)
+    rec = dict(stats)
+    rec.update({"elapsed_ms": local_ms, "units": float(units_local), "steps": len(times_ms)})
+    per_rank = gather_stats(rec)
+    for i, r in enumerate(per_rank):
+        r.setdefault("rank", i)
+    steps = max(1, len(times_ms))
+    return {"total_ms": total_ms, "units_all": units_all, "ms_per_step": total_ms / steps,
+            "value": units_all * steps / (total_ms / 1e3) if total_ms > 0 else float("nan"),
+            "per_rank": per_rank}

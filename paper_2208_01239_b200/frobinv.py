@@ -26,6 +26,20 @@ _vp, _dp, _ip = ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER
 _ll, _i, _sz, _d = ctypes.c_longlong, ctypes.c_int, ctypes.c_size_t, ctypes.c_double
 
 
+OPT_FUSED_FIRST_STEP = 1
+OPT_DEVICE_AUTO = 2
+
+
+class DevStatus(ctypes.Structure):
+    """frob_dev_status (include/frobinv.h): the device-side status record of frob_inv_dev."""
+    _fields_ = [("status", ctypes.c_int), ("info", ctypes.c_int), ("branch_used", ctypes.c_int),
+                ("nonfinite", ctypes.c_int), ("rho_a", ctypes.c_double), ("rho_b", ctypes.c_double),
+                ("rho_m", ctypes.c_double)]
+
+
+DEV_STATUS_BYTES = ctypes.sizeof(DevStatus)
+
+
 class FrobInfo(ctypes.Structure):
     _fields_ = [("info", ctypes.c_int), ("branch_used", ctypes.c_int), ("rho_a", ctypes.c_double),
                 ("rho_b", ctypes.c_double), ("rho_m", ctypes.c_double)]
@@ -44,7 +58,9 @@ SIGNATURES = {
     "frob_inv_host_workspace_bytes": (_sz, [_i]),
     "frob_inv_host": (_i, [_i, _vp, _vp, _i, _vp, _sz, _vp, _FIP]),
     "frob_inv_host_many_workspace_bytes": (_sz, [_i]),
-    "frob_inv_host_many": (_i, [_i, _i, _vp, _vp, _i, _vp, _sz, _vp]),
+    "frob_inv_host_many": (_i, [_i, _i, _vp, _vp, _i, _vp, _vp, _sz, _vp]),
+    "frob_inv_dev": (_i, [_i, _vp, _ll, _vp, _ll, _i, _i, _vp, _vp, _sz, _vp]),
+    "frob_dtrmm": (_i, [_i, _i, _i, _d, _vp, _ll, _vp, _ll, _vp, _ll, _vp]),
     "frob_inv_batched_host_workspace_bytes": (_sz, [_i, _i]),
     "frob_inv_batched_host": (_i, [_i, _i, _vp, _vp, _i, _vp, _i, _vp, _sz, _vp]),
     "zinv_lu_workspace_bytes": (_sz, [_i]),
@@ -163,22 +179,62 @@ def _check(fn, st, info=None):
 
 
 # ----------------------------------------------------------------------------- single matrix
+def _check_out(x, z, name="out"):
+    assert x.dtype == torch.complex128 and x.shape == z.shape and x.stride(1) == 1 and x.device == z.device, \
+        f"{name}: complex128 {tuple(z.shape)} with unit column stride on {z.device} required"
+
+
 def inv(z: torch.Tensor, branch: str = "auto", out: torch.Tensor | None = None, info: bool = False,
-        fused: bool = False):
+        fused: bool = False, device_auto: bool = False):
     """Z^{-1} by Frobenius inversion (Alg 1).  z: (n, n) complex128 CUDA tensor.
-    fused=True: NEXT-1 first step C = U^{-1} (L^{-1} (P Y)) (FROB_OPT_FUSED_FIRST_STEP)."""
+    fused=True: NEXT-1 first step C = U^{-1} (L^{-1} (P Y)) (FROB_OPT_FUSED_FIRST_STEP).
+    device_auto=True: the AUTO branch decided on the device (FROB_OPT_DEVICE_AUTO; no host sync)."""
     L = load()
     _need_cuda(z, "z")
     assert z.dtype == torch.complex128 and z.dim() == 2 and z.shape[0] == z.shape[1]
     z = z if z.stride(1) == 1 else z.contiguous()
     n = z.shape[0]
     x = out if out is not None else torch.empty((n, n), dtype=torch.complex128, device=z.device)
+    _check_out(x, z)
     ws = workspace(L.frob_inv_workspace_bytes(n), z.device)
     fi = FrobInfo()
-    st = L.frob_inv_opts(n, _p(z), z.stride(0), _p(x), x.stride(0), BRANCH[branch], 1 if fused else 0,
+    opts = (OPT_FUSED_FIRST_STEP if fused else 0) | (OPT_DEVICE_AUTO if device_auto else 0)
+    st = L.frob_inv_opts(n, _p(z), z.stride(0), _p(x), x.stride(0), BRANCH[branch], opts,
                          _p(ws), ws.numel(), _stream(), ctypes.byref(fi) if info else None)
     _check("frob_inv", st, fi.as_dict() if info else None)
     return (x, fi.as_dict()) if info else x
+
+
+def inv_dev(z: torch.Tensor, branch: str = "auto", out: torch.Tensor | None = None, fused: bool = False,
+            device_auto: bool = False, status: torch.Tensor | None = None):
+    """frob_inv_dev: like inv() but device-side errors land in a device status record (uint8 tensor
+    of DEV_STATUS_BYTES on z's device) instead of a host synchronisation.  Returns (X, status);
+    decode the record with dev_status(status) after the stream."""
+    L = load()
+    _need_cuda(z, "z")
+    assert z.dtype == torch.complex128 and z.dim() == 2 and z.shape[0] == z.shape[1]
+    z = z if z.stride(1) == 1 else z.contiguous()
+    n = z.shape[0]
+    x = out if out is not None else torch.empty((n, n), dtype=torch.complex128, device=z.device)
+    _check_out(x, z)
+    if status is None:
+        status = torch.zeros(DEV_STATUS_BYTES, dtype=torch.uint8, device=z.device)
+    assert status.is_cuda and status.dtype == torch.uint8 and status.numel() >= DEV_STATUS_BYTES
+    ws = workspace(L.frob_inv_workspace_bytes(n), z.device)
+    opts = (OPT_FUSED_FIRST_STEP if fused else 0) | (OPT_DEVICE_AUTO if device_auto else 0)
+    st = L.frob_inv_dev(n, _p(z), z.stride(0), _p(x), x.stride(0), BRANCH[branch], opts, _p(status), _p(ws),
+                        ws.numel(), _stream())
+    _check("frob_inv_dev", st)
+    return x, status
+
+
+def dev_status(status: torch.Tensor) -> dict:
+    """Decode a frob_dev_status record (synchronises through the device->host copy)."""
+    raw = bytes(status[:DEV_STATUS_BYTES].cpu().numpy().tobytes())
+    r = DevStatus.from_buffer_copy(raw)
+    return {"status": STATUS.get(r.status, str(r.status)), "code": r.status, "info": r.info,
+            "branch_used": r.branch_used, "nonfinite": r.nonfinite, "rho_a": r.rho_a, "rho_b": r.rho_b,
+            "rho_m": r.rho_m}
 
 
 def draw_mu(seed: int) -> float:
@@ -205,13 +261,20 @@ def inv_rand(z: torch.Tensor, mu: float | None = None, seed: int = 0, out: torch
     return (x, fi.as_dict()) if info else x
 
 
+def _check_host_out(x_host, z_host):
+    assert (x_host.shape == z_host.shape and x_host.dtype == torch.complex128 and x_host.is_contiguous()
+            and not x_host.is_cuda), "x_host: contiguous CPU complex128 of z_host's shape required"
+
+
 def inv_host(z_host: torch.Tensor, x_host: torch.Tensor | None = None, branch: str = "auto",
              device="cuda"):
     """End-to-end call with HOST buffers (pinned recommended): H2D, invert, D2H."""
     L = load()
     assert z_host.dtype == torch.complex128 and not z_host.is_cuda and z_host.is_contiguous()
     n = z_host.shape[0]
-    x_host = x_host if x_host is not None else torch.empty_like(z_host)
+    assert z_host.dim() == 2 and z_host.shape[0] == z_host.shape[1]
+    x_host = x_host if x_host is not None else torch.empty_like(z_host).pin_memory()
+    _check_host_out(x_host, z_host)
     ws = workspace(L.frob_inv_host_workspace_bytes(n), device)
     st = L.frob_inv_host(n, _p(z_host), _p(x_host), BRANCH[branch], _p(ws), ws.numel(), _stream(), None)
     _check("frob_inv_host", st)
@@ -219,16 +282,25 @@ def inv_host(z_host: torch.Tensor, x_host: torch.Tensor | None = None, branch: s
 
 
 def inv_host_many(z_host: torch.Tensor, x_host: torch.Tensor | None = None, branch: str = "auto",
-                  device="cuda"):
+                  device="cuda", status: bool = False):
     """count matrices (count, n, n) in pinned HOST memory, pipelined: the copies of matrices
-    i + 1 (in) and i - 1 (out) overlap the inversion of matrix i (frob_inv_host_many)."""
+    i + 1 (in) and i - 1 (out) overlap the inversion of matrix i (frob_inv_host_many).
+    status=True: return (x_host, per-matrix status int32[count]) and do not raise on a failing
+    matrix (its status code says which)."""
     L = load()
     assert z_host.dtype == torch.complex128 and not z_host.is_cuda and z_host.is_contiguous() and z_host.dim() == 3
     count, n = z_host.shape[0], z_host.shape[1]
     assert z_host.shape[2] == n
-    x_host = x_host if x_host is not None else torch.empty_like(z_host)
+    x_host = x_host if x_host is not None else torch.empty_like(z_host).pin_memory()
+    _check_host_out(x_host, z_host)
+    codes = torch.empty(count, dtype=torch.int32).pin_memory()
     ws = workspace(L.frob_inv_host_many_workspace_bytes(n), device)
-    st = L.frob_inv_host_many(n, count, _p(z_host), _p(x_host), BRANCH[branch], _p(ws), ws.numel(), _stream())
+    st = L.frob_inv_host_many(n, count, _p(z_host), _p(x_host), BRANCH[branch], _p(codes), _p(ws), ws.numel(),
+                              _stream())
+    if status:
+        if st not in STATUS or st in (4, 6, 7):
+            _check("frob_inv_host_many", st)
+        return x_host, codes
     _check("frob_inv_host_many", st)
     return x_host
 
@@ -240,7 +312,9 @@ def inv_batched_host(z_host: torch.Tensor, x_host: torch.Tensor | None = None, b
     L = load()
     assert z_host.dtype == torch.complex128 and not z_host.is_cuda and z_host.is_contiguous() and z_host.dim() == 3
     batch, n = z_host.shape[0], z_host.shape[1]
-    x_host = x_host if x_host is not None else torch.empty_like(z_host)
+    assert z_host.shape[2] == n
+    x_host = x_host if x_host is not None else torch.empty_like(z_host).pin_memory()
+    _check_host_out(x_host, z_host)
     info = torch.empty(batch, dtype=torch.int32).pin_memory()  # pageable memory would stall the pipeline
     chunk = chunk or max(1, min(batch, (256 << 20) // (16 * n * n)))
     ws = workspace(L.frob_inv_batched_host_workspace_bytes(n, chunk), device)
@@ -410,6 +484,20 @@ def dgemm(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor | None = None, alpha
     st = L.frob_dgemm(m, n, k, alpha, _p(a), a.stride(0), _p(b), b.stride(0), beta, _p(c), c.stride(0),
                       _stream())
     _check("frob_dgemm", st)
+    return c
+
+
+def dtrmm(t: torch.Tensor, b: torch.Tensor, uplo: str = "lower", alpha: float = 1.0,
+          c: torch.Tensor | None = None):
+    """C = alpha tri(T) B on the GEMM engine (T's other strict triangle must be zero)."""
+    L = load()
+    _need_cuda(t, "t")
+    n, m = b.shape
+    assert t.shape == (n, n) and t.dtype == b.dtype == torch.float64
+    c = c if c is not None else torch.empty((n, m), dtype=torch.float64, device=b.device)
+    st = L.frob_dtrmm(1 if uplo == "upper" else 2, n, m, alpha, _p(t), t.stride(0), _p(b), b.stride(0), _p(c),
+                      c.stride(0), _stream())
+    _check("frob_dtrmm", st)
     return c
 
 

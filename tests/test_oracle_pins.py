@@ -459,3 +459,103 @@ def test_hpd_rejects_indefinite():
     _, st, col = oracle.hpd_frob_inv(z)
     assert st == 1 and col == 1
     assert oracle.zhpd_inv_chol(z)[1] == 1
+
+
+# ------------------------------------------------------------------ solves used by sketch parity
+def test_zgetrf_lapack_pivots_and_reconstruction():
+    """or_zgetrf vs LAPACK zgetrf (scipy): same izamax (|re|+|im|) pivots, same factors to
+    rounding, and P Z = L U."""
+    import scipy.linalg as sl
+    rng = np.random.default_rng(11)
+    for n in (1, 2, 7, 64, 301):
+        z = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+        lr, li, ipiv, info = oracle.zgetrf(z)
+        assert info == 0
+        lu, piv = sl.lu_factor(z)
+        assert np.array_equal(ipiv, piv)
+        f = lr + 1j * li
+        assert np.abs(f - lu).max() <= 1e-13 * n * np.abs(lu).max()
+        lo = np.tril(f, -1) + np.eye(n)
+        up = np.triu(f)
+        pz = z.copy()
+        for k in range(n):
+            pz[[k, ipiv[k]]] = pz[[ipiv[k], k]]
+        assert np.abs(lo @ up - pz).max() <= 1e-13 * n * np.abs(z).max()
+
+
+def test_zgetrf_zero_pivot():
+    z = np.array([[0, 0], [0, 1j]], dtype=np.complex128)
+    assert oracle.zgetrf(z)[3] == 1
+
+
+def test_zgetrs_closed_forms():
+    """Diagonal: Y = R / d elementwise (one complex division per entry, exact up to the
+    division's rounding); a permutation times a diagonal of powers of two (and i): exact."""
+    rng = np.random.default_rng(3)
+    n, k = 9, 4
+    d = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    r = rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k))
+    y = oracle.zgetrs(oracle.zgetrf(np.diag(d)), r)
+    assert np.abs(y - r / d[:, None]).max() <= 4 * U * np.abs(r / d[:, None]).max()
+    perm = rng.permutation(n)
+    scal = (2.0 ** rng.integers(-3, 4, size=n)) * np.array([1, 1j, -1, -1j])[rng.integers(0, 4, size=n)]
+    p = np.zeros((n, n), dtype=np.complex128)
+    p[np.arange(n), perm] = scal
+    # P Y = R  =>  Y[perm[i]] = R[i] / scal[i]
+    y = oracle.zgetrs(oracle.zgetrf(p), r)
+    ref = np.empty_like(r)
+    ref[perm] = r / scal[:, None]
+    assert np.array_equal(y, ref)
+    yh = oracle.zgetrs(oracle.zgetrf(p), r, trans=True)
+    assert np.array_equal(yh, np.linalg.solve(p.conj().T, r))  # exact: powers of two, permutation
+
+
+def test_zgetrs_vs_gauss_jordan_and_residuals():
+    """Y = Z^{-1} R agrees with the (independently pinned) Gauss-Jordan inverse times R, and both
+    Z Y = R and Z^H Y' = R hold to rounding; also the exact rational inverse on an integer Z."""
+    rng = np.random.default_rng(5)
+    n, k = 120, 7
+    z = synth.shifted_complex(n, 7, 0, 3.0 * math.sqrt(n))
+    r = rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k))
+    fac = oracle.zgetrf(z)
+    y = oracle.zgetrs(fac, r)
+    x, _ = oracle.zinv_gj(z)
+    assert np.linalg.norm(y - x @ r) <= 1e-12 * np.linalg.norm(y)
+    assert np.linalg.norm(z @ y - r) <= 1e-12 * np.linalg.norm(r)
+    yh = oracle.zgetrs(fac, r, trans=True)
+    assert np.linalg.norm(z.conj().T @ yh - r) <= 1e-12 * np.linalg.norm(r)
+    assert np.linalg.norm(yh - x.conj().T @ r) <= 1e-12 * np.linalg.norm(yh)
+    case = _gold("exact_inverses.json")["cases"][-1]
+    ze = np.array(case["re"], float) + 1j * np.array(case["im"], float)
+    ref = _dec(case["inv"])
+    ye = oracle.zsolve(ze, np.eye(ze.shape[0]))
+    kap = np.linalg.cond(ze)
+    assert np.abs(ye - ref).max() <= 50 * ze.shape[0] * U * kap * max(1.0, kap) * np.abs(ref).max()
+
+
+def test_kappa2_estimate_closed_forms():
+    """kappa_2 of Q diag(s) W^H (Q, W unitary) is s_max / s_min; of a diagonal, max|d|/min|d|."""
+    rng = np.random.default_rng(9)
+    n = 80
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    w, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    s = np.linspace(1.0, 2.0, n)
+    s[0], s[-1] = 0.01, 50.0      # isolated extremes: power iterations converge fast
+    z = (q * s[None, :]) @ w.conj().T
+    kap, smax, smin = oracle.kappa2(z)
+    assert abs(smax - 50.0) <= 1e-6 * 50.0 and abs(smin - 0.01) <= 1e-6 * 0.01
+    assert abs(kap - 5000.0) <= 1e-5 * 5000.0
+    d = np.array([3.0, -0.5j, 2 + 2j, 7.0])
+    assert abs(oracle.kappa2(np.diag(d))[0] - 14.0) <= 1e-9
+
+
+def test_frob_inv_many_matches_single_calls_bitwise():
+    zs = synth.batch(16, 12, seed=4)
+    zs[3] = 0.0
+    zs[3].imag = np.eye(16)             # A = 0: branch B
+    x, st, info, bu, rho = oracle.frob_inv_many(zs)
+    for i in range(zs.shape[0]):
+        xi, sti, inf = oracle.frob_inv(zs[i])
+        assert st[i] == sti and info[i] == inf["info"] and bu[i] == inf["branch_used"]
+        assert np.array_equal(x[i], xi)
+    assert bu[3] == 2

@@ -4,7 +4,7 @@
 #include "../paper_2208_01239_b200/csrc/lu.cu"
 #include "../paper_2208_01239_b200/csrc/tma.cu"
 #include "../paper_2208_01239_b200/csrc/lu2.cu"
-#include "../paper_2208_01239_b200/csrc/lu3.cu"
+#include "lu3_experiment.cu"
 #include <vector>
 #include <random>
 #include <cmath>

@@ -1,4 +1,4 @@
-// lu3.cu -- persistent LU with partial pivoting (Alg 3 line 1) for the inversion
+// lu3_experiment.cu -- EXPERIMENT (not built into libfrobinv.so; kept for tools/lu2_probe.cu): persistent LU with partial pivoting (Alg 3 line 1) for the inversion
 // path, orders n <= LU3_MAX_N (1024), real (PW = 16) and complex (PW = 8).
 //
 // ONE cooperative launch per factorisation (one 1024-thread CTA per SM, all co-resident).
@@ -25,11 +25,20 @@
 #include <utility>
 #include <algorithm>
 #include <cooperative_groups.h>
-#include "lu.cuh"
+#include "../paper_2208_01239_b200/csrc/lu.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace frob {
+
+// Persistent LU (this file; experiment, not built into the library) for n <= LU3_MAX_N: A (n x ld) is destroyed (it keeps the
+// L multipliers by original row), U and L come out split in final row order (ld);
+// iw = lu3_int_elems(n) ints.
+constexpr int LU3_MAX_N = 1024;
+size_t lu3_int_elems(int n);
+template <typename T>
+cudaError_t lu3_factor(int n, T *A, long long ld, T *U, T *L, int *perm, int *iw, T *diag, LuStats *stats,
+                       cudaStream_t s);
 
 constexpr int LU3_T = 1024;      // threads per CTA (panel: one row per thread)
 constexpr int LU3_W = LU3_T / 32;
