@@ -24,8 +24,8 @@
  *     events and join back to `stream` before the call returns, so stream order and CUDA
  *     graph capture are preserved; concurrent host threads serialise on that fork (one
  *     mutex per device).  The only host synchronisations
- *     are (a) FROB_BRANCH_AUTO in frob_inv (one 32-byte device->host read of the pivot
- *     diagnostics of LU(A)), (b) a non-NULL host_info / host-side outputs, (c) the
+ *     are (a) FROB_BRANCH_AUTO in frob_inv (one small device->host read of LU(A)'s
+ *     diagnostics and the norms of A and A^{-1}; a second one if B is inverted too), (b) a non-NULL host_info / host-side outputs, (c) the
  *     Newton drivers (one 16-byte read of delta_t per iteration), (d) *_host entries.
  *   - Outputs must not alias inputs (X != Z, S != Z, ...): FROB_ERR_INVALID_ARG.
  *   - Singular pivots: a pivot u_kk of an LU is "singular" when
@@ -55,8 +55,9 @@ typedef enum {
 } frob_status;
 
 typedef enum {
-    FROB_BRANCH_AUTO = 0, /* S1 unless LU(A) is singular or its pivot ratio exceeds 256; then the
-                             branch whose LU has the smaller pivot ratio (reading R1)   */
+    FROB_BRANCH_AUTO = 0, /* S1 unless A is singular or kappa_inf(A) = ||A||_inf ||A^{-1}||_inf of the
+                             computed inverse exceeds 1e6; then also B is inverted and the part with
+                             the smaller kappa_inf is used (reading R1', Thm 5.2)      */
     FROB_BRANCH_A = 1,    /* S1: X = A, Y = B (Alg 1 line 2)                                      */
     FROB_BRANCH_B = 2     /* S2: X = B, Y = A (Alg 1 line 4)                                      */
 } frob_branch;
@@ -69,6 +70,10 @@ typedef struct {
     double rho_a;      /* max|u_ii|/min|u_ii| of LU(A) (NaN if A was not factored)       */
     double rho_b;      /* same for LU(B)                                                 */
     double rho_m;      /* same for LU(M), M = X + Y X^{-1} Y                              */
+    double kappa_a;    /* kappa_inf(A) = ||A||_inf ||A^{-1}||_inf from the computed inverse (AUTO
+                          rule R1'; NEXT-1: the bound ||A||_inf ||U^{-1}||_inf ||L^{-1}||_inf);
+                          NaN if A was not inverted                                     */
+    double kappa_b;    /* same for B                                                     */
 } frob_info;
 
 /* Status record written ON THE DEVICE at the end of a call's stream work (frob_inv_dev), so
@@ -81,6 +86,7 @@ typedef struct {
     int branch_used;   /* 1 = S1, 2 = S2, 0 = none                                                 */
     int nonfinite;     /* 1 if NaN/Inf was seen in the input                                       */
     double rho_a, rho_b, rho_m;   /* pivot ratios (NaN where the LU did not run)                   */
+    double kappa_a, kappa_b;      /* kappa_inf of the parts as in frob_info                        */
 } frob_dev_status;
 
 /* ---------------------------------------------------------------- single matrix */
@@ -109,11 +115,12 @@ frob_status frob_inv(int n, const double *Z, long long ldz, double *X, long long
  *     formed, 9 1/3 n^3 instead of 10 n^3 flops.  Same results up to rounding order.
  * Unknown bits give FROB_ERR_INVALID_ARG.  Everything else as frob_inv. */
 #define FROB_OPT_FUSED_FIRST_STEP 1
-/*   FROB_OPT_DEVICE_AUTO  (branch must be FROB_BRANCH_AUTO) reading R1 decided ON THE DEVICE: LU(A)
- *     and LU(B) are both computed (one extra LU, 2/3 n^3 flops), a one-thread kernel picks the branch
- *     from their pivot statistics, and the S2 factors / rotated parts move into the S1 slots by
- *     predicated copies.  No host synchronisation at all, so the call can be captured in a CUDA
- *     graph; results are bitwise those of the host-decided AUTO. */
+/*   FROB_OPT_DEVICE_AUTO  (branch must be FROB_BRANCH_AUTO, not with FROB_OPT_FUSED_FIRST_STEP)
+ *     reading R1' decided ON THE DEVICE: A and B are both factored and inverted (one extra real
+ *     inversion, 2 n^3 flops), a one-thread kernel picks the branch from their kappa_inf, and B's
+ *     inverse / permutation and the rotated parts move into the S1 slots by predicated copies.
+ *     No host synchronisation at all, so the call can be captured in a CUDA graph; results are
+ *     bitwise those of the host-decided AUTO. */
 #define FROB_OPT_DEVICE_AUTO 2
 frob_status frob_inv_opts(int n, const double *Z, long long ldz, double *X, long long ldx, int branch,
                           int options, void *ws, size_t ws_bytes, void *stream, frob_info *host_info);
@@ -259,11 +266,11 @@ frob_status frob_dgetrf(int n, double *A, long long lda, int *perm, void *ws, si
                         void *stream, frob_info *host_info);
 
 /* Hermitian positive definite inversion (paper Section 6).
- * frob_hpd_inv: Alg 6 "first variant of Frobenius inversion" (P:L705-728) -- for HPD Z = A + iB
+ * frob_hpd_inv: Alg 6 "first variant of Frobenius inversion" (P:L717-747) -- for HPD Z = A + iB
  *   (Lemma 6.1: A symmetric positive definite, B skew, Z in S1): Cholesky A = U^T U,
  *   K1 = U^{-T} B, K2 = U^{-1} K1, K4 = A - K1^T K1 = V^T V, K6 = V^{-1} V^{-T}, K7 = K2 K6,
- *   Z^{-1} = K6 - i K7 (Cholesky blocked right-looking, Alg 10 P:L786-800).
- * zhpd_inv_chol: Alg 8 over C (P:L748-760), the comparator: Z = U^H U, X = U^{-1} U^{-H}.
+ *   Z^{-1} = K6 - i K7 (Cholesky blocked right-looking, Alg 10 P:L823-842).
+ * zhpd_inv_chol: Alg 8 over C (P:L785-800), the comparator: Z = U^H U, X = U^{-1} U^{-H}.
  *   Z, X: device n x n complex128 (ldz, ldx complex elements), Z is not checked for being
  *   Hermitian (only its upper triangle is read by the Cholesky factorisations).
  *   host_info: nullable; if non-NULL the call synchronises and stores 0 or the 1-based column
@@ -271,6 +278,13 @@ frob_status frob_dgetrf(int n, double *A, long long lda, int *perm, void *ws, si
 size_t frob_hpd_inv_workspace_bytes(int n);
 frob_status frob_hpd_inv(int n, const double *Z, long long ldz, double *X, long long ldx, void *ws,
                          size_t ws_bytes, void *stream, int *host_info);
+/* frob_dpoinv: real symmetric positive definite inversion, Alg 8 over R: A = U^T U
+ *   (blocked Cholesky, upper triangle of A read), K = U^{-1}, X = K K^T.  Its time is Thm 6.2's
+ *   T_pinv (defined on Alg 9, which has the same flop count).  A, X: device n x n
+ *   fp64 row-major (lda, ldx doubles); host_info as frob_hpd_inv. */
+size_t frob_dpoinv_workspace_bytes(int n);
+frob_status frob_dpoinv(int n, const double *A, long long lda, double *X, long long ldx, void *ws,
+                        size_t ws_bytes, void *stream, int *host_info);
 size_t zhpd_inv_chol_workspace_bytes(int n);
 frob_status zhpd_inv_chol(int n, const double *Z, long long ldz, double *X, long long ldx, void *ws,
                           size_t ws_bytes, void *stream, int *host_info);

@@ -15,6 +15,7 @@ exact rational brute force, invariants and the paper's printed special cases.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 import threading
@@ -28,7 +29,7 @@ _lock = threading.Lock()
 _lib = None
 
 BRANCH = {"auto": 0, "a": 1, "b": 2}
-TAU_SWITCH = 256.0  # DESIGN.md reading R1
+KAPPA_SWITCH = 1.0e6  # DESIGN.md reading R1': AUTO switch test on kappa_inf(A) = ||A||_inf ||A^-1||_inf
 
 
 def build(force: bool = False) -> str:
@@ -150,7 +151,7 @@ def split(z):
     return _f64(z.real), _f64(z.imag)
 
 
-def frob_inv(z, branch: str = "auto", tau: float = TAU_SWITCH):
+def frob_inv(z, branch: str = "auto", kappa_sw: float = KAPPA_SWITCH):
     """Alg 1.  Returns (X complex128, status, info dict).
 
     status: 0 ok, 1 singular (info['info'] = 1-based column), 2 both parts singular.
@@ -160,15 +161,15 @@ def frob_inv(z, branch: str = "auto", tau: float = TAU_SWITCH):
     xr = np.zeros_like(a)
     xi = np.zeros_like(a)
     out = np.zeros(2, dtype=np.int32)
-    rho = np.zeros(2, dtype=np.float64)
-    st = lib().or_frob_inv(n, _p(a), _p(b), _p(xr), _p(xi), BRANCH[branch], float(tau),
+    rho = np.zeros(4, dtype=np.float64)
+    st = lib().or_frob_inv(n, _p(a), _p(b), _p(xr), _p(xi), BRANCH[branch], float(kappa_sw),
                            _p(out, ctypes.c_int), _p(rho))
     x = xr + 1j * xi
-    return x, st, {"info": int(out[0]), "branch_used": int(out[1]),
-                   "rho_a": float(rho[0]), "rho_b": float(rho[1])}
+    return x, st, {"info": int(out[0]), "branch_used": int(out[1]), "rho_a": float(rho[0]), "rho_b": float(rho[1]),
+                   "kappa_a": float(rho[2]), "kappa_b": float(rho[3])}
 
 
-def frob_inv_rand(z, mu: float, tau: float = TAU_SWITCH):
+def frob_inv_rand(z, mu: float, kappa_sw: float = KAPPA_SWITCH):
     """Alg 5 with the random mu given: Z^{-1} = (1 + mu i) (Z (1 + mu i))^{-1}.
 
     Returns (X complex128, status, info dict) as frob_inv (status of the inner Alg 1 call).
@@ -178,15 +179,15 @@ def frob_inv_rand(z, mu: float, tau: float = TAU_SWITCH):
     xr = np.zeros_like(a)
     xi = np.zeros_like(a)
     out = np.zeros(2, dtype=np.int32)
-    rho = np.zeros(2, dtype=np.float64)
-    st = lib().or_frob_inv_rand(n, _p(a), _p(b), float(mu), _p(xr), _p(xi), float(tau),
+    rho = np.zeros(4, dtype=np.float64)
+    st = lib().or_frob_inv_rand(n, _p(a), _p(b), float(mu), _p(xr), _p(xi), float(kappa_sw),
                                 _p(out, ctypes.c_int), _p(rho))
-    return xr + 1j * xi, st, {"info": int(out[0]), "branch_used": int(out[1]),
-                              "rho_a": float(rho[0]), "rho_b": float(rho[1])}
+    return xr + 1j * xi, st, {"info": int(out[0]), "branch_used": int(out[1]), "rho_a": float(rho[0]),
+                              "rho_b": float(rho[1]), "kappa_a": float(rho[2]), "kappa_b": float(rho[3])}
 
 
 def dpotrf_upper(a):
-    """Alg 10 (P:L786-800): A = U^T U, U upper.  Returns (U, info)."""
+    """Alg 10 (P:L823-842): A = U^T U, U upper.  Returns (U, info)."""
     a = _f64(a)
     u = np.zeros_like(a)
     info = lib().or_dpotrf_upper(a.shape[0], _p(a), _p(u))
@@ -194,7 +195,7 @@ def dpotrf_upper(a):
 
 
 def hpd_frob_inv(z):
-    """Alg 6 (P:L705-728) for Hermitian positive definite Z.  Returns (X, status, col)."""
+    """Alg 6 (P:L717-747) for Hermitian positive definite Z.  Returns (X, status, col)."""
     a, b = split(z)
     xr = np.zeros_like(a)
     xi = np.zeros_like(a)
@@ -204,7 +205,7 @@ def hpd_frob_inv(z):
 
 
 def zhpd_inv_chol(z):
-    """Alg 8 over C (P:L748-760): complex Cholesky inversion X = U^{-1} U^{-H}.  Returns (X, info)."""
+    """Alg 8 over C (P:L785-800): complex Cholesky inversion X = U^{-1} U^{-H}.  Returns (X, info)."""
     re, im = split(z)
     xr = np.zeros_like(re)
     xi = np.zeros_like(im)
@@ -261,51 +262,48 @@ def zsolve(z, r):
     return zgetrs(fac, r)
 
 
-def kappa2(z, fac=None, iters: int = 40, seed: int = 12345):
+def kappa2(z, fac=None, iters: int = 30, block: int = 16, seed: int = 12345):
     """Estimate of kappa_2(Z) = sigma_max / sigma_min (reading R10 / SURVEY G7).
 
-    sigma_max: power iteration on Z^H Z (numpy matvecs); sigma_min: inverse power iteration on
-    (Z^H Z)^{-1} = Z^{-1} Z^{-H} through zgetrs.  Both are Rayleigh-quotient estimates from
-    below, so the returned kappa is (up to convergence) a lower bound of the true one.
-    Returns (kappa, sigma_max, sigma_min)."""
+    Block subspace iteration with Rayleigh-Ritz (block size `block`): sigma_max^2 = largest
+    eigenvalue of Z^H Z (numpy matvecs), 1 / sigma_min^2 = largest eigenvalue of
+    (Z^H Z)^{-1} = Z^{-1} Z^{-H} (applied through zgetrs).  A block converges at the rate of the
+    ratio to the (block+1)-th singular value, so the clustered small singular values of random
+    matrices do not stall it.  Ritz values approach from below: the returned kappa is (up to
+    convergence) a lower bound of the true one.  Returns (kappa, sigma_max, sigma_min)."""
     z = np.asarray(z, dtype=np.complex128)
     n = z.shape[0]
+    k = max(1, min(block, n))
     fac = fac if fac is not None else zgetrf(z)
     rng = np.random.default_rng(seed)
-    v = rng.standard_normal(n) + 1j * rng.standard_normal(n)
-    v /= np.linalg.norm(v)
-    smax = 0.0
-    for _ in range(iters):
-        w = z @ v
-        smax = float(np.linalg.norm(w))
-        v = z.conj().T @ w
-        v /= np.linalg.norm(v)
-    u = rng.standard_normal(n) + 1j * rng.standard_normal(n)
-    u /= np.linalg.norm(u)
-    inv_smin = 0.0
-    for _ in range(iters):
-        w = zgetrs(fac, u, trans=True)           # Z^{-H} u
-        u = zgetrs(fac, w)                       # Z^{-1} Z^{-H} u
-        inv_smin = float(np.sqrt(np.linalg.norm(u)))   # ||(Z^H Z)^{-1} u|| -> 1 / sigma_min^2
-        u /= np.linalg.norm(u)
-    smin = 1.0 / inv_smin if inv_smin > 0 else 0.0
+
+    def top_eig(apply):
+        q, _ = np.linalg.qr(rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k)))
+        for _ in range(iters):
+            q, _ = np.linalg.qr(apply(q))
+        t = q.conj().T @ apply(q)
+        return float(np.linalg.eigvalsh(0.5 * (t + t.conj().T)).max())
+
+    smax = math.sqrt(top_eig(lambda v: z.conj().T @ (z @ v)))
+    lam = top_eig(lambda v: zgetrs(fac, zgetrs(fac, v, trans=True)))
+    smin = 1.0 / math.sqrt(lam) if lam > 0 else 0.0
     return (smax / smin if smin > 0 else float("inf")), smax, smin
 
 
-def frob_inv_many(zs, branch: str = "auto", tau: float = TAU_SWITCH):
+def frob_inv_many(zs, branch: str = "auto", kappa_sw: float = KAPPA_SWITCH):
     """or_frob_inv on each matrix of zs (count, n, n), in parallel over matrices.
 
     Returns (X (count, n, n), status int32[count], info int32[count], branch_used int32[count],
-    rho (count, 2) = (rho_A, rho_B))."""
+    rho (count, 4) = (rho_A, rho_B, kappa_inf(A), kappa_inf(B)))."""
     zs = np.asarray(zs)
     count, n = zs.shape[0], zs.shape[1]
     a, b = _f64(zs.real), _f64(zs.imag)
     xr = np.zeros_like(a)
     xi = np.zeros_like(a)
     out = np.zeros((count, 2), dtype=np.int32)
-    rho = np.zeros((count, 2), dtype=np.float64)
+    rho = np.zeros((count, 4), dtype=np.float64)
     st = np.zeros(count, dtype=np.int32)
-    lib().or_frob_inv_many(count, n, _p(a), _p(b), _p(xr), _p(xi), BRANCH[branch], float(tau),
+    lib().or_frob_inv_many(count, n, _p(a), _p(b), _p(xr), _p(xi), BRANCH[branch], float(kappa_sw),
                            _p(out, ctypes.c_int), _p(rho), _p(st, ctypes.c_int))
     return xr + 1j * xi, st, out[:, 0].copy(), out[:, 1].copy(), rho
 

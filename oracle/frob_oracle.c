@@ -23,13 +23,13 @@
  *                    interchanges that undo P (A = P^T L U  =>  A^{-1} = U^{-1} L^{-1} P).
  *   or_dinv          Alg 3 = the real inversion inv_{n,R} used twice by Alg 1.
  *   or_dgemm         m_{n,R}: C = A B, plain triple loop, k ascending.
- *   or_dpotrf_upper  Alg 10 Cholesky (P:L786-800); or_hpd_frob_inv Alg 6 (P:L705-728);
- *   or_zhpd_inv_chol Alg 8 complex Cholesky inversion (P:L748-760)
+ *   or_dpotrf_upper  Alg 10 Cholesky (P:L823-842); or_hpd_frob_inv Alg 6 (P:L717-747);
+ *   or_zhpd_inv_chol Alg 8 complex Cholesky inversion (P:L785-800)
  *   or_frob_inv_rand Alg 5 randomized Frobenius inversion, mu given
  *   or_frob_inv      Alg 1 "Frobenius inversion I" with tau = 1 (f = x^2+1,
  *                    P:L123): S1 branch returns J - iK, S2 branch returns K - iJ.  The
  *                    numerical branch choice (the paper's S1/S2 are algebraic)
- *                    follows DESIGN.md reading R1.
+ *                    follows DESIGN.md reading R1' (kappa_inf of the part, Thm 5.2).
  *   or_zinv_gj       The plain definition: complex Gauss-Jordan inverse with partial
  *                    pivoting on |re|+|im| (the object Lemma 4.1, reaches exactly).
  *   or_zinv_lu       Alg 3 applied over C (the paper's comparator).
@@ -207,70 +207,83 @@ void or_dgemm(int m, int n, int k, const double *a, const double *b, double *c)
     }
 }
 
-/* Factor X only to obtain (rho, singular column): used by the AUTO branch rule. */
-static void lu_probe(int n, const double *x, double *rho, int *sc)
+/* ||A||_inf = max_i sum_j |a_ij| (j ascending) */
+static double norm_inf(int n, const double *a)
 {
-    double *lu = (double *)malloc(sizeof(double) * (size_t)n * n);
-    int *ipiv = (int *)malloc(sizeof(int) * (size_t)(n > 0 ? n : 1));
-    memcpy(lu, x, sizeof(double) * (size_t)n * n);
-    or_dgetrf(n, lu, ipiv);
-    pivot_diag(n, lu, max_abs((size_t)n * n, x), rho, sc);
-    free(lu); free(ipiv);
+    double m = 0.0;
+    for (int i = 0; i < n; ++i) {
+        double r = 0.0;
+        for (int j = 0; j < n; ++j) r = r + fabs(a[(size_t)i * n + j]);
+        if (r > m) m = r;
+    }
+    return m;
 }
 
 /* Alg 1 with tau = 1.
- *   branch: 0 = AUTO (R1), 1 = S1 (X=A, Y=B), 2 = S2 (X=B, Y=A).
- *   tau_sw: AUTO switch threshold on the pivot ratio rho_A.
+ *   branch: 0 = AUTO (reading R1'), 1 = S1 (X=A, Y=B), 2 = S2 (X=B, Y=A).
+ *   kappa_sw: AUTO switch threshold on kappa_inf(X) = ||X||_inf ||X^{-1}||_inf.
+ * AUTO (R1'): invert A (line "compute X^{-1}" with X = A); keep S1 unless A is singular (R2) or
+ * kappa_inf(A) > kappa_sw -- the leading term of the Thm 5.2 bound is
+ * |X^{-1}| |L_X| |U_X| |X^{-1}| |Y| |J|, i.e. the error grows with the conditioning of X; then
+ * also invert B and keep the branch whose part has the smaller kappa_inf (the computed inverse
+ * of the chosen part is used as "X^{-1}").
  * Returns 0 ok, 1 singular (out[0] = 1-based column), 2 both parts singular.
- * out[0]=info, out[1]=branch used (1|2); rho[0]=rho_A, rho[1]=rho_B (NaN if not factored). */
+ * out[0]=info, out[1]=branch used (1|2); rho[0..3] = rho_A, rho_B (pivot ratios), kappa_inf(A),
+ * kappa_inf(B) (NaN where that part was not factored / inverted). */
 int or_frob_inv(int n, const double *A, const double *B, double *Xre, double *Xim,
-                int branch, double tau_sw, int *out, double *rho)
+                int branch, double kappa_sw, int *out, double *rho)
 {
-    double rho_a = NAN, rho_b = NAN;
-    int sc_a = 0, sc_b = 0;
-    int use = branch;
-    if (branch == 0) {
-        lu_probe(n, A, &rho_a, &sc_a);
-        if (sc_a || rho_a > tau_sw) {
-            lu_probe(n, B, &rho_b, &sc_b);
-            if (sc_a && sc_b) { out[0] = 0; out[1] = 0; rho[0] = rho_a; rho[1] = rho_b; return 2; }
-            if (sc_a) use = 2;
-            else if (sc_b) use = 1;
-            else use = (rho_b < rho_a) ? 2 : 1;
-        } else {
-            use = 1;
-        }
-    }
-    rho[0] = rho_a; rho[1] = rho_b;
-    out[1] = use;
-    const double *X = (use == 1) ? A : B;   /* line 2 / line 4 of Alg 1 */
-    const double *Y = (use == 1) ? B : A;
     size_t nn = (size_t)n * n;
     double *Xinv = (double *)malloc(sizeof(double) * nn);
+    double *Xinv2 = (double *)malloc(sizeof(double) * nn);
     double *F = (double *)malloc(sizeof(double) * nn);
     double *G = (double *)malloc(sizeof(double) * nn);
     double *J = (double *)malloc(sizeof(double) * nn);
     double *K = (double *)malloc(sizeof(double) * nn);
-    double rx;
-    int info = or_dinv(n, X, Xinv, &rx);          /* compute X^{-1}                 */
-    if (use == 1 && branch != 0) rho[0] = rx;
-    if (use == 2 && branch != 0) rho[1] = rx;
-    if (info) { out[0] = info; goto done; }
-    or_dgemm(n, n, n, Xinv, Y, F);                 /* compute X^{-1} Y               */
-    or_dgemm(n, n, n, Y, F, G);                    /* compute Y X^{-1} Y             */
-    for (size_t i = 0; i < nn; ++i) G[i] = X[i] + G[i]; /* tau1 X + tau2 Y X^{-1} Y    */
-    info = or_dinv(n, G, J, NULL);                 /* J = (tau1 X + tau2 Y X^-1 Y)^-1 */
-    if (info) { out[0] = info; goto done; }
-    or_dgemm(n, n, n, F, J, K);                    /* K = X^{-1} Y J                 */
-    if (use == 1) {                                /* return J - iK                  */
-        for (size_t i = 0; i < nn; ++i) { Xre[i] = J[i]; Xim[i] = -K[i]; }
-    } else {                                       /* return K - iJ                  */
-        for (size_t i = 0; i < nn; ++i) { Xre[i] = K[i]; Xim[i] = -J[i]; }
+    int use = branch, info = 0;
+    rho[0] = rho[1] = rho[2] = rho[3] = NAN;
+    if (branch == 0) {
+        int ia = or_dinv(n, A, Xinv, &rho[0]);          /* compute X^{-1}, X = A            */
+        double ka = ia ? INFINITY : norm_inf(n, A) * norm_inf(n, Xinv);
+        rho[2] = ka;
+        use = 1;
+        if (ia || !(ka <= kappa_sw)) {
+            int ib = or_dinv(n, B, Xinv2, &rho[1]);     /* compute X^{-1}, X = B            */
+            double kb = ib ? INFINITY : norm_inf(n, B) * norm_inf(n, Xinv2);
+            rho[3] = kb;
+            if (ia && ib) { out[0] = ia; out[1] = 0; info = -1; goto done; }
+            if (ia || (!ib && kb < ka)) {
+                double *t = Xinv; Xinv = Xinv2; Xinv2 = t;
+                use = 2;
+            }
+        }
+    } else {
+        double rx;
+        info = or_dinv(n, use == 1 ? A : B, Xinv, &rx);  /* compute X^{-1}                 */
+        rho[use == 1 ? 0 : 1] = rx;
+        if (info) { out[0] = info; out[1] = use; goto done; }
+        rho[use == 1 ? 2 : 3] = norm_inf(n, use == 1 ? A : B) * norm_inf(n, Xinv);
     }
-    out[0] = 0;
+    out[1] = use;
+    {
+        const double *X = (use == 1) ? A : B;   /* line 2 / line 4 of Alg 1 */
+        const double *Y = (use == 1) ? B : A;
+        or_dgemm(n, n, n, Xinv, Y, F);                 /* compute X^{-1} Y               */
+        or_dgemm(n, n, n, Y, F, G);                    /* compute Y X^{-1} Y             */
+        for (size_t i = 0; i < nn; ++i) G[i] = X[i] + G[i]; /* tau1 X + tau2 Y X^{-1} Y    */
+        info = or_dinv(n, G, J, NULL);                 /* J = (tau1 X + tau2 Y X^-1 Y)^-1 */
+        if (info) { out[0] = info; goto done; }
+        or_dgemm(n, n, n, F, J, K);                    /* K = X^{-1} Y J                 */
+        if (use == 1) {                                /* return J - iK                  */
+            for (size_t i = 0; i < nn; ++i) { Xre[i] = J[i]; Xim[i] = -K[i]; }
+        } else {                                       /* return K - iJ                  */
+            for (size_t i = 0; i < nn; ++i) { Xre[i] = K[i]; Xim[i] = -J[i]; }
+        }
+        out[0] = 0;
+    }
 done:
-    free(Xinv); free(F); free(G); free(J); free(K);
-    return info ? 1 : 0;
+    free(Xinv); free(Xinv2); free(F); free(G); free(J); free(K);
+    return info < 0 ? 2 : (info ? 1 : 0);
 }
 
 /* Alg 5 "randomized Frobenius inversion", mu supplied by the caller (line 1 draws
@@ -281,7 +294,7 @@ done:
  *   line 5: Z^{-1} = (W1 - mu W2) + i (mu W1 + W2)
  * Returns the status of the inner Alg 1 call (out / rho as there). */
 int or_frob_inv_rand(int n, const double *A, const double *B, double mu, double *Xre, double *Xim,
-                     double tau_sw, int *out, double *rho)
+                     double kappa_sw, int *out, double *rho)
 {
     size_t nn = (size_t)n * n;
     double *X = (double *)malloc(sizeof(double) * nn);
@@ -292,7 +305,7 @@ int or_frob_inv_rand(int n, const double *A, const double *B, double mu, double 
         X[i] = A[i] - mu * B[i];
         Y[i] = mu * A[i] + B[i];
     }
-    int st = or_frob_inv(n, X, Y, W1, W2, 0, tau_sw, out, rho);   /* lines 3-4 */
+    int st = or_frob_inv(n, X, Y, W1, W2, 0, kappa_sw, out, rho);   /* lines 3-4 */
     if (st == 0) {
         for (size_t i = 0; i < nn; ++i) {       /* line 5 */
             Xre[i] = W1[i] - mu * W2[i];
@@ -305,7 +318,7 @@ int or_frob_inv_rand(int n, const double *A, const double *B, double mu, double 
 
 /* --------------------------------------------------------------- HPD (Section 6) */
 
-/* Alg 10 "Cholesky decomposition" (P:L786-800), real case, column by column:
+/* Alg 10 "Cholesky decomposition" (P:L823-842), real case, column by column:
  *   Z[1:k-1,k] = (Z[1:k-1,1:k-1]^T)^{-1} Z[1:k-1,k]        (forward substitution)
  *   Z[k,k]     = sqrt(Z[k,k] - Z[1:k-1,k]^T Z[1:k-1,k])
  * on the upper triangle of a; u (n x n) receives U with A = U^T U (zeros below).
@@ -354,7 +367,7 @@ static void transpose(int n, const double *a, double *t)
         for (int j = 0; j < n; ++j) t[(size_t)j * n + i] = a[(size_t)i * n + j];
 }
 
-/* Alg 6 "first variant of Frobenius inversion" (P:L705-728) for HPD Z = A + iB (Lemma 6.1:
+/* Alg 6 "first variant of Frobenius inversion" (P:L717-747) for HPD Z = A + iB (Lemma 6.1:
  * Z is in S1, so X = A, Y = B):
  *   l.6  X = U^T U            l.7  K1 = (U^T)^{-1} Y      l.8  K2 = U^{-1} K1
  *   l.9  K3 = K1^T K1         l.10 K4 = X - K3            l.11 K4 = V^T V
@@ -387,7 +400,7 @@ done:
     return st;
 }
 
-/* Alg 8 "first matrix inversion via Cholesky decomposition" (P:L748-760) over C:
+/* Alg 8 "first matrix inversion via Cholesky decomposition" (P:L785-800) over C:
  * Z = U^H U (Alg 10 with conjugates), K = U^{-1}, X = K K^H.  Returns 0 or the 1-based
  * column of a non-positive pivot. */
 int or_zhpd_inv_chol(int n, const double *zr, const double *zi, double *xr, double *xi)
@@ -724,13 +737,13 @@ void or_zgetrs(int n, const double *ar, const double *ai, const int *ipiv, int t
 /* Alg 1 on `count` independent matrices (config 3 full-set parity): or_frob_inv per matrix,
  * OpenMP over the matrices (each matrix's arithmetic is exactly or_frob_inv's). */
 int or_frob_inv_many(int count, int n, const double *A, const double *B, double *Xre, double *Xim,
-                     int branch, double tau_sw, int *out, double *rho, int *status)
+                     int branch, double kappa_sw, int *out, double *rho, int *status)
 {
     size_t nn = (size_t)n * n;
     #pragma omp parallel for schedule(dynamic, 1)
     for (int m = 0; m < count; ++m)
-        status[m] = or_frob_inv(n, A + m * nn, B + m * nn, Xre + m * nn, Xim + m * nn, branch, tau_sw,
-                                out + 2 * (size_t)m, rho + 2 * (size_t)m);
+        status[m] = or_frob_inv(n, A + m * nn, B + m * nn, Xre + m * nn, Xim + m * nn, branch, kappa_sw,
+                                out + 2 * (size_t)m, rho + 4 * (size_t)m);
     return 0;
 }
 

@@ -6,8 +6,8 @@
 //   X^{-1} by a register-resident Gauss-Jordan sweep with partial pivoting
 //       (each thread owns a 4x4 block; no row swaps: the pivot order is recorded and
 //        undone when the inverse is written back -- "exchange" form of GJ)
-//   branch check (reading R1) on the sweep pivots (= the U diagonal of LU with
-//       partial pivoting); lazy: B is swept only when A fails
+//   branch check (reading R1'): kappa_inf(A) = ||A||_inf ||A^{-1}||_inf from the computed
+//       inverse; lazy: B is swept only when A is singular or kappa_inf(A) > KAPPA_SWITCH
 //   C = X^{-1} Y,  M = X + Y C,  Re = M^{-1} (sweep),  Im = -C Re
 //       the three GEMMs run on the FP64 tensor cores (DMMA m8n8k4) from shared memory
 //   store X interleaved (branch S1: Re - i(-Im) ... see the epilogue)
@@ -397,6 +397,55 @@ FROB_DEV void cta_mma_foreach(const double (&acc)[WT<N>::MT][WT<N>::NT][2], F f,
             for (int e = 0; e < 2; ++e) f(wm0 + i * 8 + g, wn0 + j * 8 + 2 * t + e, acc[i][j][e]);
 }
 
+// ----------------------------------------------------------------- AUTO rule R1' helpers
+// block-wide maximum (all threads call; scratch >= 32 doubles; returns the max to every thread)
+FROB_DEV double block_max(double v, double *scratch, int nthreads) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) scratch[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double m = 0.0;
+    for (int i = 0; i < (nthreads + 31) / 32; ++i) m = fmax(m, scratch[i]);
+    __syncthreads();
+    return m;
+}
+
+// ||M||_inf of the leading n x n part through an accessor (row sums in fixed order)
+template <typename F>
+FROB_DEV double mat_norm_inf(int n, F f, double *scratch, int nthreads) {
+    double m = 0.0;
+    for (int r = threadIdx.x; r < n; r += nthreads) {
+        double sum = 0.0;
+        for (int c = 0; c < n; ++c) sum += fabs(f(r, c));
+        m = fmax(m, sum);
+    }
+    return block_max(m, scratch, nthreads);
+}
+
+// ||X^{-1}||_inf of the inverse a Gauss-Jordan sweep left in the register blocks: the blocks hold
+// a row and column permutation of it (padding rows >= n: identity, padding columns: zero), which
+// leaves the maximum absolute row sum unchanged.  red: >= N * CT + 32 doubles.
+template <int N, int BR, int BC>
+FROB_DEV double reg_norm_inf(const double (&a)[BR][BC], int n, double *red) {
+    using G = Geo<N, BR, BC>;
+    const int tid = threadIdx.x, ti = tid / G::CT, tj = tid % G::CT;
+#pragma unroll
+    for (int q = 0; q < BR; ++q) {
+        double sum = 0.0;
+#pragma unroll
+        for (int c = 0; c < BC; ++c) sum += fabs(a[q][c]);
+        red[(ti * BR + q) * G::CT + tj] = sum;
+    }
+    __syncthreads();
+    double m = 0.0;
+    for (int r = tid; r < n; r += G::THREADS) {
+        double sum = 0.0;
+        for (int c = 0; c < G::CT; ++c) sum += red[r * G::CT + c];
+        m = fmax(m, sum);
+    }
+    return block_max(m, red + N * G::CT, G::THREADS);
+}
+
 // ----------------------------------------------------------------- Frobenius kernel
 // n <= 32: one-barrier sweep (measured 6% faster); n <= 64: two-barrier sweep (the one-barrier
 // variant's candidate-row publishing costs more than the barrier it saves, 7.0 vs 10.0 ms)
@@ -414,6 +463,7 @@ template <int N>
 struct FrobSmem {
     double buf[3][N * BCfg<N>::S];
     typename FrobSweep<N>::SH sw;
+    double red[N * Geo<N>::CT + 32];   // R1' norm reductions
 };
 
 template <int N>
@@ -447,16 +497,19 @@ frob_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__rest
     int inf_x = sweep_info<double, N>(sm.sw, n, pmax);
     sweep_store<double, N, 4, 4>(a, sm.sw, Ws, C::S);
     if (branch == FROB_BRANCH_AUTO) {
-        const double rho_a = (pmin > 0.0) ? pmax / pmin : INFINITY;
-        if (inf_x != 0 || !(rho_a <= 256.0)) {
-            // lazy switch: sweep B too and keep the branch with the smaller pivot ratio
+        // reading R1': kappa_inf(A) from the computed inverse; above KAPPA_SWITCH (or A singular)
+        // sweep B too and keep the part with the smaller kappa_inf
+        const double na = mat_norm_inf(n, [&](int i, int j) { return As[i * C::S + j]; }, sm.red, C::THREADS);
+        const double ka = inf_x ? INFINITY : na * reg_norm_inf<N, 4, 4>(a, n, sm.red);
+        if (inf_x != 0 || !(ka <= KAPPA_SWITCH)) {
             __syncthreads();
             load_blocks<double, N>(a, Bs, n);
             double qmax, qmin;
             frob_sweep<N>(a, n, sm.sw, qmax, qmin);
             const int inf_b = sweep_info<double, N>(sm.sw, n, qmax);
-            const double rho_b = (qmin > 0.0) ? qmax / qmin : INFINITY;
-            if (inf_b == 0 && (inf_x != 0 || rho_b < rho_a)) {
+            const double nb = mat_norm_inf(n, [&](int i, int j) { return Bs[i * C::S + j]; }, sm.red, C::THREADS);
+            const double kb = inf_b ? INFINITY : nb * reg_norm_inf<N, 4, 4>(a, n, sm.red);
+            if (inf_b == 0 && (inf_x != 0 || kb < ka)) {
                 use = 2;
                 inf_x = 0;
                 __syncthreads();
@@ -515,6 +568,7 @@ constexpr int T128 = (128 / R128) * (128 / B128);
 struct Frob128Smem {
     double S[128 * 132];
     SweepShared<double, 128> sw;
+    double red[128 * (128 / B128) + 32];   // R1' norm reductions
 };
 
 // Steps a3..a7 for a fixed branch (USE = 1: X = A, Y = B; USE = 2: X = B, Y = -A), so the
@@ -595,15 +649,18 @@ frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
         inf_x = sweep_info<double, N>(sm.sw, n, pmax);
         sweep_store<double, N, R128, B128>(a, sm.sw, S, SS);
         if (branch == FROB_BRANCH_AUTO) {
-            const double rho_a = (pmin > 0.0) ? pmax / pmin : INFINITY;
-            if (inf_x != 0 || !(rho_a <= 256.0)) {
+            // reading R1' (see frob_batched_kernel)
+            const double na = mat_norm_inf(n, [&](int i, int j) { return Zb[i * n + j].x; }, sm.red, T128);
+            const double ka = inf_x ? INFINITY : na * reg_norm_inf<N, R128, B128>(a, n, sm.red);
+            if (inf_x != 0 || !(ka <= KAPPA_SWITCH)) {
                 __syncthreads();
                 load_blocks_f<double, N, R128, B128>(a, n, [&](int i, int j) { return Zb[i * n + j].y; });
                 double qmax, qmin;
                 gj_sweep<double, N, R128, B128>(a, n, sm.sw, qmax, qmin);
                 const int inf_b = sweep_info<double, N>(sm.sw, n, qmax);
-                const double rho_b = (qmin > 0.0) ? qmax / qmin : INFINITY;
-                if (inf_b == 0 && (inf_x != 0 || rho_b < rho_a)) {
+                const double nb = mat_norm_inf(n, [&](int i, int j) { return Zb[i * n + j].y; }, sm.red, T128);
+                const double kb = inf_b ? INFINITY : nb * reg_norm_inf<N, R128, B128>(a, n, sm.red);
+                if (inf_b == 0 && (inf_x != 0 || kb < ka)) {
                     use = 2;
                     inf_x = 0;
                     __syncthreads();

@@ -22,6 +22,11 @@ inline const char *tuning_env(const char *name) {
 #endif
 }
 
+// AUTO branch rule (reading R1'): S1 is kept while kappa_inf(A) = ||A||_inf ||A^-1||_inf
+// <= KAPPA_SWITCH (the conditioning of X drives the leading term of Thm 5.2's bound);
+// above it (or with A singular) both parts are inverted and the smaller kappa_inf wins.
+constexpr double KAPPA_SWITCH = 1.0e6;
+
 // process-wide count of kernel launches issued by the library (frob_launch_count())
 unsigned long long &launch_counter();
 inline void count_launch(unsigned long long k = 1) { __atomic_fetch_add(&launch_counter(), k, __ATOMIC_RELAXED); }

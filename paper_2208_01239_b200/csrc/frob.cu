@@ -121,16 +121,49 @@ __global__ void copy2d_kernel(const T *__restrict__ src, long long lds, T *__res
     if (nonfinite && __syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite, 1);
 }
 
-// ---------------------------------------------------------------------- AUTO on the device
-// Reading R1 decided from the LU statistics without a host read (FROB_OPT_DEVICE_AUTO): both
-// LU(A) and LU(B) have run; flags[1] = 1 (S1), 2 (S2) or 0 (both singular).
-__global__ void auto_select_kernel(const LuStats *__restrict__ st, int *__restrict__ flags) {
+// ---------------------------------------------------------------------- AUTO rule R1'
+// ||M||_inf = max_i sum_j |M[i][j]| of an n x n row-major matrix: one warp per row (lanes stride
+// the columns, fixed-order shuffle sum), the maximum over rows by atomicMax on the bit patterns
+// of the non-negative sums (order-independent, so the result is deterministic).  *out must be 0.
+__global__ void __launch_bounds__(256) norm_inf_kernel(const double *__restrict__ M, long long ld, int n,
+                                                       unsigned long long *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int warps = (gridDim.x * blockDim.x) >> 5;
+    double best = 0.0;
+    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+        const double *row = M + (long long)i * ld;
+        double s = 0.0;
+        for (int j = lane; j < n; j += 32) s += fabs(row[j]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        best = fmax(best, s);   // NaN rows are dropped here; non-finite input is flagged at ingest
+    }
+    if (lane == 0 && best > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(best));
+}
+
+// kappa_inf of a part from its norm slots (s0 = ||X||, s1, s2 = norms whose product bounds / equals
+// ||X^{-1}||: s2 = NULL for the exact ||X^{-1}||), infinity when the LU flagged it singular
+FROB_DEV double kappa_of(const unsigned long long *nrm, int i0, int i1, int i2, int singular) {
+    if (singular) return INFINITY;
+    double k = __longlong_as_double((long long)nrm[i0]) * __longlong_as_double((long long)nrm[i1]);
+    if (i2 >= 0) k *= __longlong_as_double((long long)nrm[i2]);
+    return k;
+}
+
+// norm slots in the workspace (u64 bit patterns of non-negative doubles)
+enum { NRM_A = 0, NRM_AINV = 1, NRM_AL = 2, NRM_B = 3, NRM_BINV = 4, NRM_BL = 5, NRM_SLOTS = 8 };
+
+// Reading R1' decided on the device (FROB_OPT_DEVICE_AUTO): both parts factored and inverted;
+// flags[1] = 1 (S1), 2 (S2) or 0 (both singular)
+__global__ void auto_select_kernel(const LuStats *__restrict__ st, const unsigned long long *__restrict__ nrm,
+                                   int *__restrict__ flags) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const LuStats a = st[0], b = st[1];
+    const bool sa = st[0].info != 0, sb = st[1].info != 0;
+    const double ka = kappa_of(nrm, NRM_A, NRM_AINV, -1, sa);
     int use = 1;
-    if (a.info != 0 || !(a.rho <= 256.0)) {
-        const bool sa = a.info != 0, sb = b.info != 0;
-        use = (sa && sb) ? 0 : ((sa || (!sb && b.rho < a.rho)) ? 2 : 1);
+    if (sa || !(ka <= KAPPA_SWITCH)) {
+        const double kb = kappa_of(nrm, NRM_B, NRM_BINV, -1, sb);
+        use = (sa && sb) ? 0 : ((sa || (!sb && kb < ka)) ? 2 : 1);
     }
     flags[1] = use;
 }
@@ -151,7 +184,7 @@ __global__ void branch_rotate_kernel(double *__restrict__ A, double *__restrict_
     }
 }
 
-// flags[1] == 2: dst <- src (the S2 factors move into the S1 slots)
+// flags[1] == 2: dst <- src (the S2 inverse / permutation move into the S1 slots)
 template <typename T>
 __global__ void cond_copy_kernel(const T *__restrict__ src, T *__restrict__ dst, long long count,
                                  const int *__restrict__ flags) {
@@ -163,9 +196,10 @@ __global__ void cond_copy_kernel(const T *__restrict__ src, T *__restrict__ dst,
 
 // Device status record of one call (frob_inv_dev / frob_inv_host_many's per-matrix status):
 // use_host = branch chosen on the host (1 | 2), or 0 = read flags[1] (device AUTO);
-// factored: bit 0 = LU(A) ran, bit 1 = LU(B) ran.
-__global__ void finalize_status_kernel(const LuStats *__restrict__ st, const int *__restrict__ flags, int use_host,
-                                       int factored, int forced_status, frob_dev_status *__restrict__ out,
+// factored: bit 0 = LU(A) ran, bit 1 = LU(B) ran; kfused: kappa from ||U^-1|| ||L^-1|| (NEXT-1).
+__global__ void finalize_status_kernel(const LuStats *__restrict__ st, const int *__restrict__ flags,
+                                       const unsigned long long *__restrict__ nrm, int use_host, int factored,
+                                       int kfused, int forced_status, frob_dev_status *__restrict__ out,
                                        int *__restrict__ status_copy) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const int use = use_host ? use_host : flags[1];
@@ -191,6 +225,8 @@ __global__ void finalize_status_kernel(const LuStats *__restrict__ st, const int
         r.rho_a = (factored & 1) ? st[0].rho : NAN;
         r.rho_b = (factored & 2) ? st[1].rho : NAN;
         r.rho_m = (use && !forced_status) ? st[2].rho : NAN;
+        r.kappa_a = (factored & 1) ? kappa_of(nrm, NRM_A, NRM_AINV, kfused ? NRM_AL : -1, st[0].info) : NAN;
+        r.kappa_b = (factored & 2) ? kappa_of(nrm, NRM_B, NRM_BINV, kfused ? NRM_BL : -1, st[1].info) : NAN;
         *out = r;
     }
     if (status_copy) *status_copy = status;
@@ -206,7 +242,8 @@ struct FrobWs {
     double *diag, *work;
     int *perm_x, *perm_b, *perm_m, *mv, *iw;
     LuStats *stats;   // [0] A, [1] B, [2] M
-    int *flags;       // [0] nonfinite
+    int *flags;       // [0] nonfinite, [1] device-AUTO branch, [2] GEMM tile counter
+    unsigned long long *nrm;  // NRM_* slots (inside the flags block: one memset clears both)
     size_t bytes;
 };
 
@@ -232,7 +269,8 @@ static FrobWs carve_frob(void *ws, int n) {
     w.mv = c.take<int>(lu_mv_ints(n));
     w.iw = small ? c.take<int>(lu2_int_elems(n)) : nullptr;
     w.stats = c.take<LuStats>(3);
-    w.flags = c.take<int>(4);
+    w.flags = c.take<int>(64);  // 256 bytes: flags[0..31] + NRM_SLOTS u64 norm slots
+    w.nrm = w.flags ? reinterpret_cast<unsigned long long *>(w.flags + 32) : nullptr;
     w.bytes = c.off;
     return w;
 }
@@ -279,12 +317,26 @@ struct StatusOut {
     bool any() const { return rec || code; }
 };
 
-static cudaError_t finalize_status(const FrobWs &w, int use_host, int factored, int forced, StatusOut so,
-                                   cudaStream_t s) {
+static cudaError_t finalize_status(const FrobWs &w, int use_host, int factored, bool kfused, int forced,
+                                   StatusOut so, cudaStream_t s) {
     if (!so.any()) return cudaSuccess;
     count_launch();
-    finalize_status_kernel<<<1, 32, 0, s>>>(w.stats, w.flags, use_host, factored, forced, so.rec, so.code);
+    finalize_status_kernel<<<1, 32, 0, s>>>(w.stats, w.flags, w.nrm, use_host, factored, kfused ? 1 : 0, forced,
+                                            so.rec, so.code);
     return cudaGetLastError();
+}
+
+static cudaError_t norm_inf(const double *M, long long ld, int n, unsigned long long *slot, cudaStream_t s) {
+    count_launch();
+    const int blocks = (int)std::min<long long>(((long long)n * 32 + 255) / 256, 148LL * 4);
+    norm_inf_kernel<<<blocks, 256, 0, s>>>(M, ld, n, slot);
+    return cudaGetLastError();
+}
+
+static double nrm_val(unsigned long long v) {
+    double d;
+    std::memcpy(&d, &v, sizeof(d));
+    return d;
 }
 
 static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *X, long long ldx,
@@ -292,102 +344,171 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
                                  frob_info *host_info, double mu = 0.0, bool fused = false,
                                  bool dev_auto = false, StatusOut so = StatusOut()) {
     if (n < 1 || !Z || !X || ldz < n || ldx < n || branch < 0 || branch > 2) return FROB_ERR_INVALID_ARG;
-    if (dev_auto && branch != FROB_BRANCH_AUTO) return FROB_ERR_INVALID_ARG;
+    if (dev_auto && (branch != FROB_BRANCH_AUTO || fused)) return FROB_ERR_INVALID_ARG;
     if (overlap(Z, (size_t)((n - 1) * ldz + n) * 16, X, (size_t)((n - 1) * ldx + n) * 16))
         return FROB_ERR_INVALID_ARG;
     FrobWs w = carve_frob(nullptr, n);
     if (!ws || ws_bytes < w.bytes) return FROB_ERR_WORKSPACE;
     w = carve_frob(ws, n);
     const long long ld = ld_of(n);
+    const long long mat = (long long)n * ld;
     const double2 *Zc = reinterpret_cast<const double2 *>(Z);
+    const bool small = n <= lu2_max_n();  // latency-oriented LU (lu2.cu), factors come out split (U, L)
+    const bool autob = branch == FROB_BRANCH_AUTO;
 
-    FROB_CUDA(cudaMemsetAsync(w.flags, 0, 4 * sizeof(int), s));
-    // a0: ingest
+    FROB_CUDA(cudaMemsetAsync(w.flags, 0, 64 * sizeof(int), s));
+    // a0: ingest (W1 = copy of the first branch matrix for its LU)
     count_launch();
-    split_kernel<<<ew_blocks((long long)n * n), 256, 0, s>>>(Zc, ldz, n, w.A, w.B, w.W1,
+    // (the literal path factors B from W5, NEXT-1 every part from W1)
+    split_kernel<<<ew_blocks((long long)n * n), 256, 0, s>>>(Zc, ldz, n, w.A, w.B,
+                                                             (!fused && branch == FROB_BRANCH_B) ? w.W5 : w.W1,
                                                              branch == FROB_BRANCH_B ? 2 : 1, ld, w.flags, mu);
     FROB_CUDA(cudaGetLastError());
 
-    // a1: LU of the branch matrix (A unless forced B)
     int use = (branch == FROB_BRANCH_B) ? 2 : 1;
-    int factored = use;  // bit 0: LU(A) ran, bit 1: LU(B) ran
-    int *perm = w.perm_x;
-    double *Xlu = w.W1;
-    // n <= LU2_MAX_N: latency-oriented LU (lu2.cu), factors come out split (U, L)
-    const bool small = n <= lu2_max_n();
-    double *Uf = w.W2, *Lf = w.W3;
-    {
-        ProfScope ps("step:lu", s);
-        if (small) FROB_CUDA(lu2_factor<double>(n, w.W1, w.W4, ld, w.W2, w.W3, ld, perm, w.iw, w.diag,
-                                                &w.stats[use == 1 ? 0 : 1], s));
-        else FROB_CUDA(getrf<double>(n, Xlu, ld, perm, w.mv, w.diag, &w.stats[use == 1 ? 0 : 1], w.work, s));
-    }
-    auto lu_b = [&]() -> frob_status {
-        // LU(B) into the S2 slots (W5 / W6, W7 / perm_b), stats[1]
-        ProfScope ps("step:lu", s);
-        count_launch();
-        copy2d_kernel<double><<<ew_blocks((long long)n * n), 256, 0, s>>>(w.B, ld, w.W5, ld, n, nullptr);
-        FROB_CUDA(cudaGetLastError());
-        if (small) FROB_CUDA(lu2_factor<double>(n, w.W5, w.W4, ld, w.W6, w.W7, ld, w.perm_b, w.iw, w.diag,
-                                                &w.stats[1], s));
-        else FROB_CUDA(getrf<double>(n, w.W5, ld, w.perm_b, w.mv, w.diag, &w.stats[1], w.work, s));
-        factored |= 2;
+    int factored = 0;                 // bit 0: LU(A) ran, bit 1: LU(B) ran
+    int *perm = w.perm_x;             // perm of the chosen part's LU
+    double *Xinv = w.W4;              // a2 output: Xinv' = U^{-1} L^{-1} (X^{-1} = Xinv' P)
+    double *Uf = w.W2, *Lf = w.W3;    // NEXT-1: U^{-1}, L^{-1} of the chosen part
+
+    // a1 + a2 for part u (1 = A, 2 = B) of the literal path: LU, then Xinv' into `out`.
+    //   u = 1: LU input W1 (written by split), lu2 ping-pong W4 -> (W2, W3) | getrf in place W1;
+    //          inverse into W4 (scratch W1 | W2, W3)
+    //   u = 2: LU input W5 (copy of B), lu2 ping-pong W1 -> (W6, W7) | getrf in place W5;
+    //          inverse into W1 (scratch W5 | W2, W3)
+    auto lit_part = [&](int u, bool copy_in) -> frob_status {
+        double *in = (u == 1) ? w.W1 : w.W5;
+        int *pm = (u == 1) ? w.perm_x : w.perm_b;
+        if (copy_in) {
+            count_launch();
+            copy2d_kernel<double><<<ew_blocks((long long)n * n), 256, 0, s>>>(u == 1 ? w.A : w.B, ld, in, ld, n,
+                                                                              nullptr);
+            FROB_CUDA(cudaGetLastError());
+        }
+        {
+            ProfScope ps("step:lu", s);
+            if (small) FROB_CUDA(lu2_factor<double>(n, in, u == 1 ? w.W4 : w.W1, ld, u == 1 ? w.W2 : w.W6,
+                                                    u == 1 ? w.W3 : w.W7, ld, pm, w.iw, w.diag, &w.stats[u - 1], s));
+            else FROB_CUDA(getrf<double>(n, in, ld, pm, w.mv, w.diag, &w.stats[u - 1], w.work, s));
+        }
+        factored |= u;
+        ProfScope ps("step:inv_from_lu", s);
+        if (small) {
+            if (u == 1) FROB_CUDA(inv_from_ul<double>(n, w.W2, w.W3, ld, w.W1, w.W4, ld, nullptr, w.flags + 2, s));
+            else FROB_CUDA(inv_from_ul<double>(n, w.W6, w.W7, ld, w.W5, w.W1, ld, nullptr, w.flags + 2, s));
+        } else {
+            FROB_CUDA(inv_from_lu<double>(n, in, ld, w.W2, w.W3, u == 1 ? w.W4 : w.W1, ld, nullptr, w.flags + 2, s));
+        }
         return FROB_OK;
     };
+    // NEXT-1 a1 + triangular inverses of part u into (W2, W3), perm_x (the same slots for both
+    // parts: a switch recomputes)
+    auto fused_part = [&](int u, bool copy_in) -> frob_status {
+        if (copy_in) {
+            count_launch();
+            copy2d_kernel<double><<<ew_blocks((long long)n * n), 256, 0, s>>>(u == 1 ? w.A : w.B, ld, w.W1, ld, n,
+                                                                              nullptr);
+            FROB_CUDA(cudaGetLastError());
+        }
+        {
+            ProfScope ps("step:lu", s);
+            if (small) FROB_CUDA(lu2_factor<double>(n, w.W1, w.W4, ld, w.W2, w.W3, ld, w.perm_x, w.iw, w.diag,
+                                                    &w.stats[u - 1], s));
+            else {
+                FROB_CUDA(getrf<double>(n, w.W1, ld, w.perm_x, w.mv, w.diag, &w.stats[u - 1], w.work, s));
+                FROB_CUDA(extract_ul<double>(n, w.W1, ld, w.W2, w.W3, s));
+            }
+        }
+        factored |= u;
+        FROB_CUDA(tri_inverses<double>(n, w.W2, w.W3, ld, w.W1, s));
+        return FROB_OK;
+    };
+    // norms of part u for kappa_inf (R1'): ||X|| and ||Xinv'|| (literal) or ||U^-1||, ||L^-1|| (NEXT-1)
+    auto part_norms = [&](int u, const double *xinv) -> frob_status {
+        const int o = (u == 1) ? 0 : 3;
+        FROB_CUDA(norm_inf(u == 1 ? w.A : w.B, ld, n, w.nrm + NRM_A + o, s));
+        if (!fused) {
+            FROB_CUDA(norm_inf(xinv, ld, n, w.nrm + NRM_AINV + o, s));
+        } else {
+            FROB_CUDA(norm_inf(w.W2, ld, n, w.nrm + NRM_AINV + o, s));
+            FROB_CUDA(norm_inf(w.W3, ld, n, w.nrm + NRM_AL + o, s));
+        }
+        return FROB_OK;
+    };
+    auto part = [&](int u, bool copy_in) { return fused ? fused_part(u, copy_in) : lit_part(u, copy_in); };
+#define FROB_ST(x) do { const frob_status _s = (x); if (_s != FROB_OK) return _s; } while (0)
 
+    FROB_ST(part(use, false));
+    if (use == 2 && !fused) {  // forced S2: B's inverse and permutation
+        perm = w.perm_b;
+        Xinv = w.W1;
+    }
     LuStats hs[3];
     for (auto &h : hs) { h.rho = NAN; h.umax = 0; h.info = 0; h.nonfinite = 0; }
     int hflags[2] = {0, 0};
-    if (branch == FROB_BRANCH_AUTO && !dev_auto) {
-        // a1': branch check (reading R1) -- one small device->host read
+    unsigned long long hn[NRM_SLOTS] = {0};
+    double kap[2] = {NAN, NAN};
+    auto kappa_host = [&](int u) {
+        const int o = (u == 1) ? 0 : 3;
+        if (hs[u - 1].info) return (double)INFINITY;
+        double k = nrm_val(hn[NRM_A + o]) * nrm_val(hn[NRM_AINV + o]);
+        if (fused) k *= nrm_val(hn[NRM_AL + o]);
+        return k;
+    };
+    if (autob && !dev_auto) {
+        // a1' (reading R1'): kappa_inf(A) from the computed inverse (or NEXT-1's triangular inverses),
+        // one small device->host read
+        FROB_ST(part_norms(1, w.W4));
         FROB_CUDA(cudaMemcpyAsync(&hs[0], &w.stats[0], sizeof(LuStats), cudaMemcpyDeviceToHost, s));
         FROB_CUDA(cudaMemcpyAsync(hflags, w.flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+        FROB_CUDA(cudaMemcpyAsync(hn, w.nrm, sizeof(hn), cudaMemcpyDeviceToHost, s));
         FROB_CUDA(cudaStreamSynchronize(s));
         if (hflags[0]) {
             if (host_info) { host_info->info = 0; host_info->branch_used = 0; }
-            FROB_CUDA(finalize_status(w, 1, factored, FROB_ERR_NONFINITE, so, s));
+            FROB_CUDA(finalize_status(w, 1, factored, fused, FROB_ERR_NONFINITE, so, s));
             return FROB_ERR_NONFINITE;
         }
-        if (hs[0].info != 0 || !(hs[0].rho <= 256.0)) {
-            const frob_status st = lu_b();
-            if (st != FROB_OK) return st;
+        kap[0] = kappa_host(1);
+        if (hs[0].info != 0 || !(kap[0] <= KAPPA_SWITCH)) {
+            FROB_ST(part(2, true));
+            FROB_ST(part_norms(2, w.W1));
             FROB_CUDA(cudaMemcpyAsync(&hs[1], &w.stats[1], sizeof(LuStats), cudaMemcpyDeviceToHost, s));
+            FROB_CUDA(cudaMemcpyAsync(hn, w.nrm, sizeof(hn), cudaMemcpyDeviceToHost, s));
             FROB_CUDA(cudaStreamSynchronize(s));
+            kap[1] = kappa_host(2);
             const bool sa = hs[0].info != 0, sb = hs[1].info != 0;
             if (sa && sb) {
                 if (host_info) {
                     host_info->info = hs[0].info; host_info->branch_used = 0;
                     host_info->rho_a = hs[0].rho; host_info->rho_b = hs[1].rho; host_info->rho_m = NAN;
+                    host_info->kappa_a = kap[0]; host_info->kappa_b = kap[1];
                 }
-                FROB_CUDA(finalize_status(w, 1, factored, FROB_ERR_BOTH_SINGULAR, so, s));
+                FROB_CUDA(finalize_status(w, 1, factored, fused, FROB_ERR_BOTH_SINGULAR, so, s));
                 return FROB_ERR_BOTH_SINGULAR;
             }
-            if (sa || (!sb && hs[1].rho < hs[0].rho)) {
+            if (sa || (!sb && kap[1] < kap[0])) {
                 use = 2;
                 perm = w.perm_b;
-                Xlu = w.W5;
-                Uf = w.W6;
-                Lf = w.W7;
+                Xinv = w.W1;
+            } else if (fused) {
+                FROB_ST(part(1, true));  // NEXT-1 keeps one set of slots: back to A
             }
         }
     } else if (dev_auto) {
-        // a1' on the device: LU(B) always, the decision in a one-thread kernel, the S2 factors and
-        // the rotated parts (B, -A) moved into the S1 slots by predicated kernels (no host read)
-        const frob_status st = lu_b();
-        if (st != FROB_OK) return st;
-        count_launch(small ? 5 : 4);
-        auto_select_kernel<<<1, 32, 0, s>>>(w.stats, w.flags);
-        FROB_CUDA(cudaGetLastError());
-        const long long mat = (long long)n * ld;
-        if (small) {
-            cond_copy_kernel<double><<<ew_blocks(mat), 256, 0, s>>>(w.W6, w.W2, mat, w.flags);
-            cond_copy_kernel<double><<<ew_blocks(mat), 256, 0, s>>>(w.W7, w.W3, mat, w.flags);
-        } else {
-            cond_copy_kernel<double><<<ew_blocks(mat), 256, 0, s>>>(w.W5, w.W1, mat, w.flags);
-        }
+        // a1' on the device: both parts factored and inverted, the decision in a one-thread kernel,
+        // B's inverse / permutation and the rotated parts (B, -A) moved into the S1 slots by
+        // predicated kernels (no host read)
+        FROB_ST(part_norms(1, w.W4));
+        FROB_ST(part(2, true));
+        FROB_ST(part_norms(2, w.W1));
+        count_launch(4);
+        auto_select_kernel<<<1, 32, 0, s>>>(w.stats, w.nrm, w.flags);
+        cond_copy_kernel<double><<<ew_blocks(mat), 256, 0, s>>>(w.W1, w.W4, mat, w.flags);
         cond_copy_kernel<int><<<ew_blocks(n), 256, 0, s>>>(w.perm_b, w.perm_x, n, w.flags);
         branch_rotate_kernel<<<ew_blocks((long long)n * n), 256, 0, s>>>(w.A, w.B, ld, n, w.flags);
         FROB_CUDA(cudaGetLastError());
+    } else if (so.any() || host_info) {
+        FROB_ST(part_norms(use, Xinv));  // kappa of the forced part (reported only)
     }
     const double *Xm = (use == 1) ? w.A : w.B;   // X of Alg 1
     const double *Ym = (use == 1) ? w.B : w.A;   // Y of Alg 1 (S2 uses Y = -A via sgn)
@@ -395,30 +516,18 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
 
     double *Cb;  // C = X^{-1} Y
     if (!fused) {
-        // a2: Xinv' = U^{-1} L^{-1}  (X^{-1} = Xinv' P)
-        {
-            ProfScope ps("step:inv_from_lu", s);
-            if (small) FROB_CUDA(inv_from_ul<double>(n, Uf, Lf, ld, w.W1, w.W4, ld, nullptr, w.flags + 2, s));
-            else FROB_CUDA(inv_from_lu<double>(n, Xlu, ld, w.W2, w.W3, w.W4, ld, nullptr, w.flags + 2, s));
-        }
         // a3: C = X^{-1} Y = Xinv' (P Y)   [B-row gather]
         Cb = w.W2;
-        auto p = gemm_params<double>(n, n, n, sgn, w.W4, ld, Ym, ld, 0.0, nullptr, ld, Cb, ld);
+        auto p = gemm_params<double>(n, n, n, sgn, Xinv, ld, Ym, ld, 0.0, nullptr, ld, Cb, ld);
         p.browmap = perm;
         GemmTag tag("gemm:frob_C");
         FROB_CUDA(gemm_launch<double>(p, 1, s));
     } else {
         // a2+a3 fused (NEXT-1): C = U^{-1} (L^{-1} (P Y)); X^{-1} is never formed
-        if (!small) {
-            FROB_CUDA(extract_ul<double>(n, Xlu, ld, w.W2, w.W3, s));
-            Uf = w.W2;
-            Lf = w.W3;
-        }
-        FROB_CUDA(tri_inverses<double>(n, Uf, Lf, ld, w.W1, s));
         GemmTag tag("gemm:frob_C_tri");
         auto p = gemm_params<double>(n, n, n, sgn, Lf, ld, Ym, ld, 0.0, nullptr, ld, w.W4, ld);
         p.triA = TRI_LOWER;
-        p.browmap = perm;
+        p.browmap = w.perm_x;
         FROB_CUDA(gemm_launch<double>(p, 1, s));
         Cb = w.W1;
         auto q = gemm_params<double>(n, n, n, 1.0, Uf, ld, w.W4, ld, 0.0, nullptr, ld, Cb, ld);
@@ -459,10 +568,11 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
         GemmTag tag("gemm:frob_Im");
         FROB_CUDA(gemm_launch<double>(p, 1, s));
     }
-    FROB_CUDA(finalize_status(w, dev_auto ? 0 : use, factored, 0, so, s));
+    FROB_CUDA(finalize_status(w, dev_auto ? 0 : use, factored, fused, 0, so, s));
     if (host_info) {
         FROB_CUDA(cudaMemcpyAsync(hs, w.stats, 3 * sizeof(LuStats), cudaMemcpyDeviceToHost, s));
         FROB_CUDA(cudaMemcpyAsync(hflags, w.flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+        FROB_CUDA(cudaMemcpyAsync(hn, w.nrm, sizeof(hn), cudaMemcpyDeviceToHost, s));
         FROB_CUDA(cudaStreamSynchronize(s));
         if (dev_auto) use = hflags[1];
         if (hflags[0]) {
@@ -472,6 +582,8 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
         }
         host_info->rho_a = (factored & 1) ? hs[0].rho : NAN;
         host_info->rho_b = (factored & 2) ? hs[1].rho : NAN;
+        host_info->kappa_a = (factored & 1) ? kappa_host(1) : NAN;
+        host_info->kappa_b = (factored & 2) ? kappa_host(2) : NAN;
         if (use == 0) {
             host_info->info = hs[0].info;
             host_info->branch_used = 0;
@@ -485,6 +597,7 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
         if (host_info->info) return FROB_ERR_SINGULAR;
     }
     return FROB_OK;
+#undef FROB_ST
 }
 
 // ---------------------------------------------------------------------- zinv_lu
@@ -1124,6 +1237,8 @@ frob_status frob_dinv(int n, const double *A, long long lda, double *Ainv, long 
         host_info->rho_a = hs.rho;
         host_info->rho_b = NAN;
         host_info->rho_m = NAN;
+        host_info->kappa_a = NAN;
+        host_info->kappa_b = NAN;
         if (hs.info) return FROB_ERR_SINGULAR;
     }
     return FROB_OK;
@@ -1159,6 +1274,8 @@ frob_status frob_dgetrf(int n, double *A, long long lda, int *perm, void *ws, si
         host_info->rho_a = hs.rho;
         host_info->rho_b = NAN;
         host_info->rho_m = NAN;
+        host_info->kappa_a = NAN;
+        host_info->kappa_b = NAN;
         if (hs.info) return FROB_ERR_SINGULAR;
     }
     return FROB_OK;

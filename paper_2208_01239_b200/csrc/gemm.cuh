@@ -36,6 +36,8 @@ struct GemmParams {
     const int *browmap;              // nullable: row k of B is B[browmap[k]]
     const int *colperm;              // nullable: output column j goes to colperm[j]
     int triA, triB, epi;
+    int triC;                        // TRI_UPPER: tiles strictly below the diagonal are skipped (their
+                                     // output is not needed: symmetric trailing updates, SYRK-style)
     int *counter;                    // non-null: persistent CTAs take tiles from this counter,
                                      // longest k-range first (square triangular products)
     int early_trigger;               // set by the launcher: release dependents at entry
@@ -421,6 +423,7 @@ gemm_kernel(GemmPair<T> pp) {
     const GemmParams<T> &p = (z < pp.zsplit) ? pp.q[0] : pp.q[1];
     const long long bz = (z < pp.zsplit) ? z : z - pp.zsplit;
     if (SPLIT || !p.counter) {
+        if (p.triC == TRI_UPPER && (int)(blockIdx.y * Cf::BM) >= (int)(blockIdx.x + 1) * Cf::BN) return;
         gemm_tile<T, VEC, BIG, SPLIT>(p, bz, blockIdx.y * Cf::BM, blockIdx.x * Cf::BN, As, Bs);
         return;
     }

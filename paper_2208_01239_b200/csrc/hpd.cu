@@ -1,14 +1,17 @@
 // hpd.cu -- Hermitian positive definite inversion (paper Section 6):
-//   frob_hpd_inv   Alg 6 "first variant of Frobenius inversion" (P:L705-728): two real
+//   frob_hpd_inv   Alg 6 "first variant of Frobenius inversion" (P:L717-747): two real
 //                  Cholesky factorisations, triangular inverses and five real GEMMs
-//   zhpd_inv_chol  Alg 8 "first matrix inversion via Cholesky" over C (P:L748-760), the
+//   zhpd_inv_chol  Alg 8 "first matrix inversion via Cholesky" over C (P:L785-800), the
 //                  comparator: complex Cholesky, U^{-1}, X = U^{-1} U^{-H}
-// Cholesky (Alg 10, P:L786-800, upper form A = U^H U) is blocked right-looking with
+//   frob_dpoinv    Alg 8 over R: the real SPD inversion whose time is Thm 6.2's T_pinv (P:L845,
+//                  defined on Alg 9, which has the same flop count)
+// Cholesky (Alg 10, P:L823-842, upper form A = U^H U) is blocked right-looking with
 // CHOL_NB-row block rows:
 //   chol_diag_kernel  one CTA factors the diagonal block in shared memory (column by column,
 //                     sqrt + row scaling + rank-1 update) and also writes W^H = (U_kk^{-1})^H
 //   panel             U_k,right = W^H A_k,right   (GEMM engine, triangular A operand)
-//   trailing          A_right -= (U_k,right)^H U_k,right  (conjugate transpose + GEMM, beta = 1)
+//   trailing          A_right -= (U_k,right)^H U_k,right  (conjugate transpose + GEMM, beta = 1;
+//                     tiles strictly below the diagonal skipped: only the upper triangle is read)
 // The GEMM engine takes no transposed operands, so every ^T / ^H is an explicit transpose.
 #include <algorithm>
 #include <climits>
@@ -168,6 +171,7 @@ static cudaError_t potrf_upper(int n, T *A, long long ld, T *work, int *info, cu
         if ((e = transpose<T>(Ak, ld, tb, CHOL_NB, nb, m, true, s)) != cudaSuccess) return e;
         T *Ar = A + (long long)(k0 + nb) * ld + k0 + nb;
         auto q = gemm_params<T>(m, m, nb, -1.0, tb, CHOL_NB, Ak, ld, 1.0, Ar, ld, Ar, ld);
+        q.triC = TRI_UPPER;  // only the upper triangle of the trailing matrix is ever read (SYRK)
         if ((e = gemm_launch<T>(q, 1, s)) != cudaSuccess) return e;
     }
     count_launch();
@@ -202,6 +206,15 @@ __global__ void zcopy_kernel(const double2 *__restrict__ Z, long long ldz, int n
     }
 }
 __global__ void set_int_kernel(int *p, int v) { *p = v; }
+__global__ void copy_real_kernel(const double *__restrict__ A, long long lda, int n, double *__restrict__ U,
+                                 long long ld) {
+    const long long total = (long long)n * n;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / n), j = (int)(idx - (long long)i * n);
+        U[(long long)i * ld + j] = A[(long long)i * lda + j];
+    }
+}
 
 size_t hpd_ws_bytes(int n) {
     const long long ld = ld_hpd(n);
@@ -289,6 +302,49 @@ frob_status frob_hpd_inv(int n, const double *Z, long long ldz, double *X, long 
     }
     return FROB_OK;
 #undef HPD_CK
+}
+
+size_t frob_dpoinv_workspace_bytes(int n) {
+    if (n < 1) return 0;
+    const long long ld = ld_hpd(n);
+    return 3 * al256((size_t)n * ld * 8) + al256((size_t)(CHOL_NB * CHOL_NB + (size_t)n * CHOL_NB) * 8) + 256;
+}
+
+frob_status frob_dpoinv(int n, const double *A, long long lda, double *X, long long ldx, void *ws, size_t ws_bytes,
+                        void *stream, int *host_info) {
+    if (n < 1 || !A || !X || lda < n || ldx < n) return FROB_ERR_INVALID_ARG;
+    if (!ws || ws_bytes < frob_dpoinv_workspace_bytes(n)) return FROB_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    const long long ld = ld_hpd(n);
+    unsigned char *b = reinterpret_cast<unsigned char *>(ws);
+    const size_t mb = al256((size_t)n * ld * 8);
+    double *U = (double *)b, *Kt = (double *)(b + mb), *T = (double *)(b + 2 * mb);
+    double *work = (double *)(b + 3 * mb);
+    int *info = (int *)(b + 3 * mb + al256((size_t)(CHOL_NB * CHOL_NB + (size_t)n * CHOL_NB) * 8));
+    cudaError_t e;
+#define DP_CK(x) do { if ((e = (x)) != cudaSuccess) return FROB_ERR_CUDA; } while (0)
+    count_launch(2);
+    set_int_kernel<<<1, 1, 0, s>>>(info, INT_MAX);
+    copy_real_kernel<<<grid_for((long long)n * n), 256, 0, s>>>(A, lda, n, U, ld);
+    DP_CK(cudaGetLastError());
+    DP_CK(potrf_upper<double>(n, U, ld, work, info, s));      // A = U^T U       (Alg 8 line 1)
+    DP_CK(tri_inverses<double>(n, U, nullptr, ld, T, s));      // K = U^{-1}      (line 2)
+    DP_CK(transpose<double>(U, ld, Kt, ld, n, n, false, s));   // K^T
+    {
+        auto p = gemm_params<double>(n, n, n, 1.0, U, ld, Kt, ld, 0.0, nullptr, ld, X, ldx);
+        p.triA = TRI_UPPER;
+        p.triB = TRI_LOWER;
+        DP_CK(gemm_launch<double>(p, 1, s));                   // X = K K^T       (line 3)
+    }
+    if (host_info) {
+        int h = 0;
+        DP_CK(cudaMemcpyAsync(&h, info, sizeof(int), cudaMemcpyDeviceToHost, s));
+        DP_CK(cudaStreamSynchronize(s));
+        *host_info = (h == INT_MAX) ? 0 : h;
+        if (h != INT_MAX) return FROB_ERR_SINGULAR;
+    }
+    return FROB_OK;
+#undef DP_CK
 }
 
 frob_status zhpd_inv_chol(int n, const double *Z, long long ldz, double *X, long long ldx, void *ws, size_t ws_bytes,

@@ -105,7 +105,7 @@ GemmParams<T> gemm_params(int M, int N, int K, double alpha, const T *A, long lo
     p.A = A; p.lda = lda; p.B = B; p.ldb = ldb;
     p.C = C; p.ldc = ldc; p.D = D; p.ldd = ldd;
     p.alpha = alpha; p.beta = beta;
-    p.triA = TRI_NONE; p.triB = TRI_NONE; p.epi = EPI_STORE;
+    p.triA = TRI_NONE; p.triB = TRI_NONE; p.triC = TRI_NONE; p.epi = EPI_STORE;
     return p;
 }
 

@@ -34,7 +34,7 @@ class DevStatus(ctypes.Structure):
     """frob_dev_status (include/frobinv.h): the device-side status record of frob_inv_dev."""
     _fields_ = [("status", ctypes.c_int), ("info", ctypes.c_int), ("branch_used", ctypes.c_int),
                 ("nonfinite", ctypes.c_int), ("rho_a", ctypes.c_double), ("rho_b", ctypes.c_double),
-                ("rho_m", ctypes.c_double)]
+                ("rho_m", ctypes.c_double), ("kappa_a", ctypes.c_double), ("kappa_b", ctypes.c_double)]
 
 
 DEV_STATUS_BYTES = ctypes.sizeof(DevStatus)
@@ -42,11 +42,12 @@ DEV_STATUS_BYTES = ctypes.sizeof(DevStatus)
 
 class FrobInfo(ctypes.Structure):
     _fields_ = [("info", ctypes.c_int), ("branch_used", ctypes.c_int), ("rho_a", ctypes.c_double),
-                ("rho_b", ctypes.c_double), ("rho_m", ctypes.c_double)]
+                ("rho_b", ctypes.c_double), ("rho_m", ctypes.c_double), ("kappa_a", ctypes.c_double),
+                ("kappa_b", ctypes.c_double)]
 
     def as_dict(self):
         return {"info": self.info, "branch_used": self.branch_used, "rho_a": self.rho_a,
-                "rho_b": self.rho_b, "rho_m": self.rho_m}
+                "rho_b": self.rho_b, "rho_m": self.rho_m, "kappa_a": self.kappa_a, "kappa_b": self.kappa_b}
 
 
 _FIP = ctypes.POINTER(FrobInfo)
@@ -75,6 +76,8 @@ SIGNATURES = {
     "frob_hpd_inv_workspace_bytes": (_sz, [_i]),
     "frob_hpd_inv": (_i, [_i, _vp, _ll, _vp, _ll, _vp, _sz, _vp, _ip]),
     "zhpd_inv_chol_workspace_bytes": (_sz, [_i]),
+    "frob_dpoinv_workspace_bytes": (_sz, [_i]),
+    "frob_dpoinv": (_i, [_i, _vp, _ll, _vp, _ll, _vp, _sz, _vp, _ip]),
     "zhpd_inv_chol": (_i, [_i, _vp, _ll, _vp, _ll, _vp, _sz, _vp, _ip]),
     "frob_sylvester_workspace_bytes": (_sz, [_i, _i, _i]),
     "frob_sylvester": (_i, [_i, _i, _vp, _vp, _vp, _vp, _d, _i, _i, _vp, _sz, _vp, _ip, _dp]),
@@ -234,7 +237,7 @@ def dev_status(status: torch.Tensor) -> dict:
     r = DevStatus.from_buffer_copy(raw)
     return {"status": STATUS.get(r.status, str(r.status)), "code": r.status, "info": r.info,
             "branch_used": r.branch_used, "nonfinite": r.nonfinite, "rho_a": r.rho_a, "rho_b": r.rho_b,
-            "rho_m": r.rho_m}
+            "rho_m": r.rho_m, "kappa_a": r.kappa_a, "kappa_b": r.kappa_b}
 
 
 def draw_mu(seed: int) -> float:
@@ -425,13 +428,28 @@ def _hpd_call(fn, wsfn, z, out, check):
 
 
 def hpd_inv(z: torch.Tensor, out: torch.Tensor | None = None, check: bool = True):
-    """HPD inversion by the Cholesky-based Frobenius variant (Alg 6, P:L705-728)."""
+    """HPD inversion by the Cholesky-based Frobenius variant (Alg 6, P:L717-747)."""
     return _hpd_call("frob_hpd_inv", "frob_hpd_inv_workspace_bytes", z, out, check)
 
 
 def zhpd_inv(z: torch.Tensor, out: torch.Tensor | None = None, check: bool = True):
-    """HPD inversion by complex Cholesky (Alg 8 over C, P:L748-760), the comparator."""
+    """HPD inversion by complex Cholesky (Alg 8 over C, P:L785-800), the comparator."""
     return _hpd_call("zhpd_inv_chol", "zhpd_inv_chol_workspace_bytes", z, out, check)
+
+
+def dpoinv(a: torch.Tensor, out: torch.Tensor | None = None, check: bool = True):
+    """Real SPD inversion (Alg 8 over R): Thm 6.2's T_pinv operation.  a: (n, n) float64 CUDA."""
+    L = load()
+    _need_cuda(a, "a")
+    assert a.dtype == torch.float64 and a.dim() == 2 and a.shape[0] == a.shape[1] and a.stride(1) == 1
+    n = a.shape[0]
+    x = out if out is not None else torch.empty((n, n), dtype=torch.float64, device=a.device)
+    ws = workspace(L.frob_dpoinv_workspace_bytes(n), a.device)
+    info = ctypes.c_int(0)
+    st = L.frob_dpoinv(n, _p(a), a.stride(0), _p(x), x.stride(0), _p(ws), ws.numel(), _stream(),
+                       ctypes.byref(info) if check else None)
+    _check("frob_dpoinv", st, {"info": info.value} if check else None)
+    return x
 
 
 def sylvester(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, tol: float = 1e-12, max_iter: int = 50,

@@ -12,7 +12,8 @@ config 3 from torch.linalg.svdvals (cuSOLVER, an independent library; it only pi
 - config 5, n = 8192 / 16384: sketch parity -- X_gpu R against X_oracle R, R the
   +-1 matrix synth.rademacher(n, 64), X_oracle R stored by tests/golden/make_sketch.py, which calls
   only oracle/ and synth/ (Gaussian elimination on the augmented system);
-- per-column residuals ||Z x_j - e_j|| <= 1e-11 sqrt(n) (x kappa factor) in fp64 on the host;
+- the residual ||Z X - I||_F <= 1e-11 n (x kappa factor) with torch's complex GEMM, and sampled
+  columns ||Z x_j - e_j|| in fp64 on the host (their RMS x sqrt(n) estimates the same residual);
 - config 3: EVERY matrix (65536 x n=32, 16384 x n=128) against the oracle's Alg 1
   (oracle.frob_inv_many, the same AUTO rule R1), and the branch each side took.
 The GPU calls are the bench's launch configuration (frob_inv AUTO / frob_inv_batched AUTO).
@@ -45,17 +46,25 @@ def _sketch_meta():
         return json.load(f)
 
 
-def _col_residuals(z, x_dev, n, kf, seed):
+def _residuals(z, zt, x_dev, n, kf, seed):
+    """The north-star residual ||Z X - I||_F <= 1e-11 n (x kappa factor), with an independent library
+    GEMM (torch complex128), plus sampled columns ||Z x_j - e_j|| in fp64 on the host: their RMS
+    times sqrt(n) estimates the same Frobenius residual (checked with a 1.5x sampling allowance)."""
+    eye = torch.eye(n, dtype=torch.complex128, device=DEV)
+    res = float(torch.linalg.norm(zt @ x_dev - eye))
+    del eye
+    assert res <= 1e-11 * n * kf, (n, res, 1e-11 * n * kf)
     rng = np.random.default_rng(seed)
     cols = rng.choice(n, size=8, replace=False)
     xs = x_dev[:, torch.from_numpy(cols).to(DEV)].cpu().numpy()
-    worst = 0.0
+    rs = []
     for k, j in enumerate(cols):
         r = z @ xs[:, k]
         r[j] -= 1.0
-        worst = max(worst, float(np.linalg.norm(r)))
-    assert worst <= 1e-11 * math.sqrt(n) * kf, (n, worst)
-    return worst
+        rs.append(float(np.linalg.norm(r)))
+    est = math.sqrt(n * np.mean(np.square(rs)))
+    assert est <= 1.5 * 1e-11 * n * kf, (n, est, rs)
+    return res, max(rs)
 
 
 @pytest.mark.parametrize("n", [2048, 4096])
@@ -69,15 +78,12 @@ def test_config5_elementwise_vs_oracle(n):
     meta = _sketch_meta()
     kappa = meta[str(n)]["kappa2_est"] if str(n) in meta else float(np.linalg.cond(z))
     kf = _kfac(kappa)
-    eye = torch.eye(n, dtype=torch.complex128, device=DEV)
     for name, f in (("frob", lambda: fb.inv(zt)), ("frob_fused", lambda: fb.inv(zt, fused=True)),
                     ("zinv_lu", lambda: fb.zinv(zt))):
         x = f()
         rel = oracle.rel_fro(x.cpu().numpy(), ref)
         assert rel <= 1e-10 * kf, (name, rel, kappa)
-        res = float(torch.linalg.norm(zt @ x - eye))
-        assert res <= 1e-11 * n * kf, (name, res)
-        _col_residuals(z, x, n, kf, seed=n)
+        _residuals(z, zt, x, n, kf, seed=n)
 
 
 @pytest.mark.parametrize("n", [8192, 16384])
@@ -100,7 +106,7 @@ def test_config5_sketch_parity(n):
         y = x @ r  # independent library GEMM (torch complex128)
         rel = float(torch.linalg.norm(y - yo) / torch.linalg.norm(yo))
         assert rel <= 1e-10 * kf, (name, n, rel, kappa)
-        _col_residuals(z, x, n, kf, seed=n + 1)
+        _residuals(z, zt, x, n, kf, seed=n + 1)
         del x, y
         torch.cuda.empty_cache()
 
@@ -125,8 +131,8 @@ def _config3_part(n, total, chunk):
         rel = num / den
         bound = 1e-10 * np.maximum(1.0, kap[s:e] / 1e4)
         same = bu[s:e] == buo
-        # branch decision: identical except where rho_A sits within rounding of the switch point
-        near = np.abs(rho[:, 0] / oracle.TAU_SWITCH - 1.0) < 1e-6
+        # branch decision: identical except where kappa_inf(A) sits within rounding of the switch point
+        near = (np.abs(rho[:, 2] / oracle.KAPPA_SWITCH - 1.0) < 1e-6) | (np.abs(rho[:, 3] / rho[:, 2] - 1.0) < 1e-6)
         bad_branch = np.nonzero(~same & ~near)[0]
         assert bad_branch.size == 0, (n, s + bad_branch[:8], rho[bad_branch[:8]])
         for i in np.nonzero(~same)[0]:      # rounding-level ties: judge against the definition

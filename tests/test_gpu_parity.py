@@ -255,7 +255,7 @@ def test_auto_switches_and_both_singular():
     b = rng.standard_normal((n, n)) + 6 * np.eye(n)
     z = a + 1j * b
     x, info = fb.inv(_t(z), info=True)
-    assert info["branch_used"] == 2 and info["rho_a"] > 256
+    assert info["branch_used"] == 2 and info["kappa_a"] > 1e6 and info["kappa_b"] < info["kappa_a"]
     _check_inverse(z, _np(x), rel=1e-8)
     with pytest.raises(fb.FrobError) as e:
         fb.inv(_t(synth.dft_unitary(16)))
@@ -439,3 +439,20 @@ def test_hpd_not_positive_definite():
         with pytest.raises(fb.FrobError) as e:
             f(_t(z))
         assert e.value.name == "singular"
+
+
+@pytest.mark.parametrize("n", [1, 63, 64, 65, 200, 1000, 2100])
+def test_dpoinv_vs_oracle(n):
+    """Real SPD inversion (Alg 8 over R, T_pinv of Thm 6.2) vs the oracle's real inverse; the
+    Cholesky's symmetric trailing update skips the tiles below the diagonal."""
+    rng = np.random.default_rng(n)
+    g = rng.standard_normal((n, n)) / math.sqrt(n)
+    a = g @ g.T + 0.5 * np.eye(n)
+    ref, info, _ = oracle.dinv(a)
+    assert info == 0
+    x = _np(fb.dpoinv(_t(a)))
+    assert oracle.rel_fro(x, ref) <= 1e-12 * max(1.0, np.linalg.cond(a))
+    a[3, 3] = -1.0
+    with pytest.raises(fb.FrobError) as e:
+        fb.dpoinv(_t(a))
+    assert e.value.name == "singular"

@@ -162,3 +162,24 @@ def test_dtrmm_lower_upper():
             c = fb.dtrmm(_t(tri), _t(b), uplo=uplo).cpu().numpy()
             ref = oracle.dgemm(tri, b)
             assert np.abs(c - ref).max() <= 1e-13 * n * np.abs(ref).max()
+
+
+def test_auto_rule_kappa_switch_matches_oracle():
+    """Reading R1': config-3 matrix 7639 (pivot ratio 230, kappa_inf(A) ~ 7.6e6) switches to S2 in the
+    single-matrix path (lu2), the batched kernel and the oracle alike, and is accurate there;
+    the reported kappa_inf values agree with the oracle's."""
+    z = synth.batch(128, 1, seed=0, start=7639)[0]
+    ref, _ = oracle.zinv_gj(z)
+    xo, st, io = oracle.frob_inv(z)
+    assert st == 0 and io["branch_used"] == 2
+    x, info = fb.inv(_t(z), info=True)
+    assert info["branch_used"] == 2
+    assert abs(info["kappa_a"] / io["kappa_a"] - 1) < 1e-9 and abs(info["kappa_b"] / io["kappa_b"] - 1) < 1e-9
+    assert oracle.rel_fro(x.cpu().numpy(), ref) <= 1e-11
+    xb, inf, bu = fb.inv_batched(_t(z[None]))
+    assert int(bu[0]) == 2 and int(inf[0]) == 0
+    assert oracle.rel_fro(xb[0].cpu().numpy(), ref) <= 1e-11
+    xd, idv = fb.inv(_t(z), device_auto=True, info=True)
+    assert idv["branch_used"] == 2 and torch.equal(xd, x)
+    xf, ifu = fb.inv(_t(z), fused=True, info=True)
+    assert ifu["branch_used"] == 2 and oracle.rel_fro(xf.cpu().numpy(), ref) <= 1e-11

@@ -307,15 +307,45 @@ def test_frob_vs_definition_config_style(n):
 
 
 def test_auto_switch_on_bad_a():
-    """A nearly singular (rho_A huge) -> AUTO takes branch B (R1)."""
+    """A nearly singular (kappa_inf(A) huge) -> AUTO takes branch B (R1')."""
     n = 12
     rng = np.random.default_rng(5)
     a = rng.standard_normal((n, n))
     a[:, 0] = a[:, 1] * (1 + 1e-9)
     b = rng.standard_normal((n, n)) + 4 * np.eye(n)
     x, st, info = oracle.frob_inv(a + 1j * b, "auto")
-    assert st == 0 and info["branch_used"] == 2 and info["rho_a"] > oracle.TAU_SWITCH
+    assert st == 0 and info["branch_used"] == 2 and info["kappa_a"] > oracle.KAPPA_SWITCH
+    assert info["kappa_b"] < info["kappa_a"]
     assert oracle.rel_fro(x, np.linalg.inv(a + 1j * b)) <= 1e-9
+
+
+def test_auto_rule_kappa_inf_exact_and_switch_point():
+    """R1': kappa_inf(X) = ||X||_inf ||X^{-1}||_inf of the part (checked against numpy's inverse);
+    AUTO keeps S1 at or below the threshold and compares both parts above it."""
+    z = synth.shifted_complex(40, seed=3, shift=9.0)
+    x, st, info = oracle.frob_inv(z)
+    ka = np.abs(z.real).sum(1).max() * np.abs(np.linalg.inv(z.real)).sum(1).max()
+    assert st == 0 and info["branch_used"] == 1 and abs(info["kappa_a"] - ka) <= 1e-12 * ka
+    assert np.isnan(info["kappa_b"])                      # B untouched below the threshold
+    x2, st2, info2 = oracle.frob_inv(z, kappa_sw=0.5 * ka)  # force the comparison
+    kb = np.abs(z.imag).sum(1).max() * np.abs(np.linalg.inv(z.imag)).sum(1).max()
+    assert abs(info2["kappa_b"] - kb) <= 1e-12 * kb
+    assert info2["branch_used"] == (2 if kb < ka else 1)
+    xb, _, _ = oracle.frob_inv(z, "b")
+    assert np.array_equal(x2, xb if kb < ka else x)
+
+
+def test_auto_rule_fixes_ill_conditioned_a_with_small_pivot_ratio():
+    """Config-3 matrix 7639 (n = 128, seed 0 + index): LU(A)'s pivot ratio is only 230 (the round-1
+    rule kept S1) but kappa_2(A) = 5.9e5, kappa_2(M) = 3.9e7 and S1's result is 2.2e-10 off the
+    definition; R1' switches to S2 (kappa_inf(B) ~ 1e4), which is accurate."""
+    z = synth.batch(128, 1, seed=0, start=7639)[0]
+    ref, _ = oracle.zinv_gj(z)
+    x, st, info = oracle.frob_inv(z)
+    assert st == 0 and info["branch_used"] == 2 and info["kappa_a"] > oracle.KAPPA_SWITCH
+    assert oracle.rel_fro(x, ref) <= 1e-11
+    xa, _, _ = oracle.frob_inv(z, "a")
+    assert oracle.rel_fro(xa, ref) > 1e-10
 
 
 def test_paper_accuracy_generator_residuals():
