@@ -142,13 +142,14 @@ def _role_counts(fn):
 @pytest.mark.parametrize("n", [64, 1024, 4100])
 def test_operation_count_inv_twice_m_thrice(n):
     """Alg 1 computes 'inv twice and m thrice': 2 LU + 2 inverse-from-LU and exactly the
-    three GEMMs C = X^{-1} Y, M = X + Y C, Im = -C Re; AUTO adds LU(B) only when it switches."""
+    three GEMMs C = X^{-1} Y, M = X + Y C, Im = -C Re; AUTO (reading R1') adds the inversion of B
+    (LU + inverse) only when kappa_inf(A) calls for the comparison."""
     zt = _t(synth.config2(n, seed=1))
     c = _role_counts(lambda: fb.inv(zt))
     assert c == {"step:lu": 2, "step:inv_from_lu": 2, "gemm:frob_C": 1, "gemm:frob_M": 1, "gemm:frob_Im": 1}, c
     zb = _t(_bad_a(n))
     c = _role_counts(lambda: fb.inv(zb))
-    assert c == {"step:lu": 3, "step:inv_from_lu": 2, "gemm:frob_C": 1, "gemm:frob_M": 1, "gemm:frob_Im": 1}, c
+    assert c == {"step:lu": 3, "step:inv_from_lu": 3, "gemm:frob_C": 1, "gemm:frob_M": 1, "gemm:frob_Im": 1}, c
     c = _role_counts(lambda: fb.inv(zt, branch="b"))
     assert c["step:lu"] == 2 and c["step:inv_from_lu"] == 2
 
