@@ -62,8 +62,14 @@ struct GemmPair {
 // BIG = 1: 128 x 128 tiles (8 warps of 64 x 32), one CTA per SM, fewer shared loads per DMMA --
 // large problems (>= 2 waves of tiles).
 template <typename T, int BIG = 0> struct GemmCfg;
+#ifndef FROB_GEMM_BK      // A/B build knobs (tools/build_variant.sh); the library uses the defaults
+#define FROB_GEMM_BK 16
+#endif
+#ifndef FROB_GEMM_STAGES
+#define FROB_GEMM_STAGES 3
+#endif
 template <> struct GemmCfg<double, 0> {
-    static constexpr int BM = 64, BN = 64, BK = 16, WGM = 2, WGN = 2, STAGES = 3;
+    static constexpr int BM = 64, BN = 64, BK = FROB_GEMM_BK, WGM = 2, WGN = 2, STAGES = FROB_GEMM_STAGES;
     static constexpr int PADA = 4, PADB = 4;
 };
 template <> struct GemmCfg<double, 1> {
@@ -423,8 +429,19 @@ gemm_kernel(GemmPair<T> pp) {
     const GemmParams<T> &p = (z < pp.zsplit) ? pp.q[0] : pp.q[1];
     const long long bz = (z < pp.zsplit) ? z : z - pp.zsplit;
     if (SPLIT || !p.counter) {
-        if (p.triC == TRI_UPPER && (int)(blockIdx.y * Cf::BM) >= (int)(blockIdx.x + 1) * Cf::BN) return;
-        gemm_tile<T, VEC, BIG, SPLIT>(p, bz, blockIdx.y * Cf::BM, blockIdx.x * Cf::BN, As, Bs);
+        // grouped tile order: consecutive CTAs walk GROUP_M tile rows column by column, so the ~444
+        // resident CTAs cover a ~16 x 28 block of tiles and share their A and B k-slabs in L2
+        // (row-major order made the resident wave span all tile columns: every B panel was re-read
+        // from DRAM once per tile row -- 557 GB per 16384^3 GEMM, ncu)
+        constexpr int GROUP_M = 16;
+        const int tn = gridDim.x, tm = gridDim.y;
+        const int lin = blockIdx.y * tn + blockIdx.x;
+        const int first = (lin / (GROUP_M * tn)) * GROUP_M;
+        const int gm = min(tm - first, GROUP_M);
+        const int rem = lin - first * tn;
+        const int ty = first + rem % gm, tx = rem / gm;
+        if (p.triC == TRI_UPPER && ty * Cf::BM >= (tx + 1) * Cf::BN) return;
+        gemm_tile<T, VEC, BIG, SPLIT>(p, bz, ty * Cf::BM, tx * Cf::BN, As, Bs);
         return;
     }
     // persistent: tiles in order of max(I, J) = 0, 1, ... (longest k-range first for

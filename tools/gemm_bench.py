@@ -4,8 +4,16 @@ import sys
 import torch
 sys.path.insert(0, ".")
 import paper_2208_01239_b200 as fb
+from paper_2208_01239_b200 import frobinv as fbi
 
-for n in (1024, 2048, 4096, 8192):
+# --lib PATH: an A/B variant of the library (tools/build_variant.sh)
+args = sys.argv[1:]
+if args and args[0] == "--lib":
+    fbi.load(args[1])
+    args = args[2:]
+sys.argv = [sys.argv[0]] + args
+
+for n in ([int(v) for v in sys.argv[1:]] or [1024, 2048, 4096, 8192]):
     a = torch.randn(n, n, dtype=torch.float64, device="cuda")
     b = torch.randn(n, n, dtype=torch.float64, device="cuda")
     c = torch.empty_like(a)
