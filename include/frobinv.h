@@ -71,7 +71,7 @@ typedef struct {
     double rho_b;      /* same for LU(B)                                                 */
     double rho_m;      /* same for LU(M), M = X + Y X^{-1} Y                              */
     double kappa_a;    /* kappa_inf(A) = ||A||_inf ||A^{-1}||_inf from the computed inverse (AUTO
-                          rule R1'; NEXT-1: the bound ||A||_inf ||U^{-1}||_inf ||L^{-1}||_inf);
+                          rule R1'; NEXT-1: ||A||_inf times the Hager-Higham estimate of ||A^{-1}||_inf);
                           NaN if A was not inverted                                     */
     double kappa_b;    /* same for B                                                     */
 } frob_info;

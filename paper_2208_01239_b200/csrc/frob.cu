@@ -10,6 +10,7 @@
 #include <mutex>
 #include <string>
 #include <vector>
+#include <algorithm>
 #include "lu.cuh"
 #include "../../include/frobinv.h"
 
@@ -240,6 +241,7 @@ static int ew_blocks(long long total) {
 struct FrobWs {
     double *A, *B, *W1, *W2, *W3, *W4, *W5, *W6, *W7;  // W6, W7: n <= LU2_MAX_N only
     double *diag, *work;
+    double *vec;      // 3 n-vectors: NEXT-1's estimate of ||X^{-1}||_inf (Hager-Higham)
     int *perm_x, *perm_b, *perm_m, *mv, *iw;
     LuStats *stats;   // [0] A, [1] B, [2] M
     int *flags;       // [0] nonfinite, [1] device-AUTO branch, [2] GEMM tile counter
@@ -263,6 +265,7 @@ static FrobWs carve_frob(void *ws, int n) {
     w.W7 = small ? c.take<double>((size_t)n * ld) : nullptr;
     w.diag = c.take<double>((size_t)n);
     w.work = c.take<double>(getrf_work_elems<double>(n));
+    w.vec = c.take<double>(3 * (size_t)ld_of(n));
     w.perm_x = c.take<int>((size_t)n);
     w.perm_b = c.take<int>((size_t)n);
     w.perm_m = c.take<int>((size_t)n);
@@ -337,6 +340,86 @@ static double nrm_val(unsigned long long v) {
     double d;
     std::memcpy(&d, &v, sizeof(d));
     return d;
+}
+
+// ||X^{-1}||_inf for NEXT-1, which never forms X^{-1} (R1'): the Hager-Higham estimate (LAPACK
+// dlacon's iteration, at most 5 steps) of ||B||_1 for B = X^{-T} = P^T L^{-T} U^{-T}, from the
+// explicit triangular inverses Ui = U^{-1}, Li = L^{-1} and perm ((P Y)[i] = Y[perm[i]]).  Products on
+// the GEMM engine: B x = P^T ((x^T Ui) Li)^T as row-vector products, B^T v = X^{-1} v = Ui (Li (P v)).
+// A lower bound of the exact norm (it is exact for most matrices); synchronises per step.
+static frob_status inv_norm_estimate(int n, const double *Ui, const double *Li, long long ld, const int *perm,
+                                     double *vec, cudaStream_t s, double *out) {
+    const long long lv = ld_of(n);
+    double *v0 = vec, *v1 = vec + lv, *v2 = vec + 2 * lv;
+    std::vector<int> hp(n);
+    std::vector<double> x(n, 1.0 / n), y(n), t(n), z(n);
+    FROB_CUDA(cudaMemcpyAsync(hp.data(), perm, n * sizeof(int), cudaMemcpyDeviceToHost, s));
+    auto rowprod = [&](const double *in, const double *M, int tri, double *o) -> frob_status {  // o = in^T M
+        auto p = gemm_params<double>(1, n, n, 1.0, in, n, M, ld, 0.0, nullptr, n, o, n);
+        p.triB = tri;
+        GemmTag tag("gemm:inv_norm_est");
+        FROB_CUDA(gemm_launch<double>(p, 1, s));
+        return FROB_OK;
+    };
+    auto colprod = [&](const double *M, int tri, const double *in, double *o) -> frob_status {  // o = M in
+        auto p = gemm_params<double>(n, 1, n, 1.0, M, ld, in, 1, 0.0, nullptr, 1, o, 1);
+        p.triA = tri;
+        GemmTag tag("gemm:inv_norm_est");
+        FROB_CUDA(gemm_launch<double>(p, 1, s));
+        return FROB_OK;
+    };
+    auto apply_B = [&](const std::vector<double> &in, std::vector<double> &o) -> frob_status {  // o = X^{-T} in
+        FROB_CUDA(cudaMemcpyAsync(v0, in.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
+        frob_status st = rowprod(v0, Ui, TRI_UPPER, v1);
+        if (st != FROB_OK) return st;
+        if ((st = rowprod(v1, Li, TRI_LOWER, v2)) != FROB_OK) return st;
+        FROB_CUDA(cudaMemcpyAsync(t.data(), v2, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        FROB_CUDA(cudaStreamSynchronize(s));
+        for (int i = 0; i < n; ++i) o[hp[i]] = t[i];  // P^T
+        return FROB_OK;
+    };
+    auto apply_BT = [&](const std::vector<double> &in, std::vector<double> &o) -> frob_status {  // o = X^{-1} in
+        for (int i = 0; i < n; ++i) t[i] = in[hp[i]];  // P in
+        FROB_CUDA(cudaMemcpyAsync(v0, t.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
+        frob_status st = colprod(Li, TRI_LOWER, v0, v1);
+        if (st != FROB_OK) return st;
+        if ((st = colprod(Ui, TRI_UPPER, v1, v2)) != FROB_OK) return st;
+        FROB_CUDA(cudaMemcpyAsync(o.data(), v2, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        FROB_CUDA(cudaStreamSynchronize(s));
+        return FROB_OK;
+    };
+    double est = 0.0;
+    int jlast = -1;
+    for (int it = 0; it < 5; ++it) {
+        frob_status st = apply_B(x, y);
+        if (st != FROB_OK) return st;
+        double e1 = 0.0;
+        for (int i = 0; i < n; ++i) e1 += std::fabs(y[i]);
+        if (it > 0 && e1 <= est) break;  // no increase: converged
+        est = e1;
+        std::vector<double> xi(n);
+        for (int i = 0; i < n; ++i) xi[i] = (y[i] >= 0.0) ? 1.0 : -1.0;
+        if ((st = apply_BT(xi, z)) != FROB_OK) return st;
+        int j = 0;
+        double zx = 0.0;
+        for (int i = 0; i < n; ++i) {
+            if (std::fabs(z[i]) > std::fabs(z[j])) j = i;
+            zx += z[i] * x[i];
+        }
+        if (std::fabs(z[j]) <= zx || j == jlast) break;
+        jlast = j;
+        std::fill(x.begin(), x.end(), 0.0);
+        x[j] = 1.0;
+    }
+    // Higham's safeguard vector: x_i = (-1)^i (1 + i / (n - 1))
+    std::vector<double> xa(n);
+    for (int i = 0; i < n; ++i) xa[i] = ((i & 1) ? -1.0 : 1.0) * (1.0 + (n > 1 ? (double)i / (n - 1) : 0.0));
+    frob_status st = apply_B(xa, y);
+    if (st != FROB_OK) return st;
+    double ea = 0.0;
+    for (int i = 0; i < n; ++i) ea += std::fabs(y[i]);
+    *out = std::max(est, 2.0 * ea / (3.0 * n));
+    return FROB_OK;
 }
 
 static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *X, long long ldx,
@@ -430,8 +513,15 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
         if (!fused) {
             FROB_CUDA(norm_inf(xinv, ld, n, w.nrm + NRM_AINV + o, s));
         } else {
-            FROB_CUDA(norm_inf(w.W2, ld, n, w.nrm + NRM_AINV + o, s));
-            FROB_CUDA(norm_inf(w.W3, ld, n, w.nrm + NRM_AL + o, s));
+            // NEXT-1: the Hager-Higham estimate of ||X^{-1}||_inf from U^{-1}, L^{-1} (host loop),
+            // written into the same slot (bit pattern of a non-negative double)
+            double e = 0.0;
+            const frob_status st = inv_norm_estimate(n, w.W2, w.W3, ld, w.perm_x, w.vec, s, &e);
+            if (st != FROB_OK) return st;
+            unsigned long long bits;
+            std::memcpy(&bits, &e, sizeof(bits));
+            FROB_CUDA(cudaMemcpyAsync(w.nrm + NRM_AINV + o, &bits, sizeof(bits), cudaMemcpyHostToDevice, s));
+            FROB_CUDA(cudaStreamSynchronize(s));  // `bits` lives on this stack frame
         }
         return FROB_OK;
     };
@@ -451,9 +541,7 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
     auto kappa_host = [&](int u) {
         const int o = (u == 1) ? 0 : 3;
         if (hs[u - 1].info) return (double)INFINITY;
-        double k = nrm_val(hn[NRM_A + o]) * nrm_val(hn[NRM_AINV + o]);
-        if (fused) k *= nrm_val(hn[NRM_AL + o]);
-        return k;
+        return nrm_val(hn[NRM_A + o]) * nrm_val(hn[NRM_AINV + o]);
     };
     if (autob && !dev_auto) {
         // a1' (reading R1'): kappa_inf(A) from the computed inverse (or NEXT-1's triangular inverses),
@@ -465,7 +553,7 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
         FROB_CUDA(cudaStreamSynchronize(s));
         if (hflags[0]) {
             if (host_info) { host_info->info = 0; host_info->branch_used = 0; }
-            FROB_CUDA(finalize_status(w, 1, factored, fused, FROB_ERR_NONFINITE, so, s));
+            FROB_CUDA(finalize_status(w, 1, factored, false, FROB_ERR_NONFINITE, so, s));
             return FROB_ERR_NONFINITE;
         }
         kap[0] = kappa_host(1);
@@ -483,7 +571,7 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
                     host_info->rho_a = hs[0].rho; host_info->rho_b = hs[1].rho; host_info->rho_m = NAN;
                     host_info->kappa_a = kap[0]; host_info->kappa_b = kap[1];
                 }
-                FROB_CUDA(finalize_status(w, 1, factored, fused, FROB_ERR_BOTH_SINGULAR, so, s));
+                FROB_CUDA(finalize_status(w, 1, factored, false, FROB_ERR_BOTH_SINGULAR, so, s));
                 return FROB_ERR_BOTH_SINGULAR;
             }
             if (sa || (!sb && kap[1] < kap[0])) {
@@ -568,7 +656,7 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
         GemmTag tag("gemm:frob_Im");
         FROB_CUDA(gemm_launch<double>(p, 1, s));
     }
-    FROB_CUDA(finalize_status(w, dev_auto ? 0 : use, factored, fused, 0, so, s));
+    FROB_CUDA(finalize_status(w, dev_auto ? 0 : use, factored, false, 0, so, s));
     if (host_info) {
         FROB_CUDA(cudaMemcpyAsync(hs, w.stats, 3 * sizeof(LuStats), cudaMemcpyDeviceToHost, s));
         FROB_CUDA(cudaMemcpyAsync(hflags, w.flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
