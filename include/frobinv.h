@@ -146,7 +146,10 @@ frob_status frob_inv_rand(int n, const double *Z, long long ldz, double *X, long
 
 /* Same computation with HOST input/output buffers (pinned memory recommended): copies
  * Z host->device, runs frob_inv, copies X device->host, synchronises.  Z_host/X_host
- * are dense (ld = n).  ws must hold frob_inv_host_workspace_bytes(n) bytes. */
+ * are dense (ld = n).  ws must hold frob_inv_host_workspace_bytes(n) bytes.  For n >= 8192 the
+ * final GEMM runs in 8 row blocks and each block's device->host copy (a library-owned copy stream)
+ * overlaps the next block (results bitwise those of frob_inv).  The status found on the device
+ * (singular X or M, non-finite input) is always returned. */
 size_t frob_inv_host_workspace_bytes(int n);
 frob_status frob_inv_host(int n, const double *Z_host, double *X_host, int branch,
                           void *ws, size_t ws_bytes, void *stream, frob_info *host_info);

@@ -221,9 +221,9 @@ static double norm_inf(int n, const double *a)
 
 /* Alg 1 with tau = 1.
  *   branch: 0 = AUTO (reading R1'), 1 = S1 (X=A, Y=B), 2 = S2 (X=B, Y=A).
- *   kappa_sw: AUTO switch threshold on kappa_inf(X) = ||X||_inf ||X^{-1}||_inf.
+ *   kappa_sw: AUTO switch threshold on kappa_inf(X) / sqrt(n), kappa_inf(X) = ||X||_inf ||X^{-1}||_inf.
  * AUTO (R1'): invert A (line "compute X^{-1}" with X = A); keep S1 unless A is singular (R2) or
- * kappa_inf(A) > kappa_sw -- the leading term of the Thm 5.2 bound is
+ * kappa_inf(A) / sqrt(n) > kappa_sw (an O(1)-accurate stand-in for kappa_2(A) of a dense matrix) -- the leading term of the Thm 5.2 bound is
  * |X^{-1}| |L_X| |U_X| |X^{-1}| |Y| |J|, i.e. the error grows with the conditioning of X; then
  * also invert B and keep the branch whose part has the smaller kappa_inf (the computed inverse
  * of the chosen part is used as "X^{-1}").
@@ -247,7 +247,7 @@ int or_frob_inv(int n, const double *A, const double *B, double *Xre, double *Xi
         double ka = ia ? INFINITY : norm_inf(n, A) * norm_inf(n, Xinv);
         rho[2] = ka;
         use = 1;
-        if (ia || !(ka <= kappa_sw)) {
+        if (ia || !(ka <= kappa_sw * sqrt((double)n))) {
             int ib = or_dinv(n, B, Xinv2, &rho[1]);     /* compute X^{-1}, X = B            */
             double kb = ib ? INFINITY : norm_inf(n, B) * norm_inf(n, Xinv2);
             rho[3] = kb;

@@ -7,7 +7,7 @@
 //       (each thread owns a 4x4 block; no row swaps: the pivot order is recorded and
 //        undone when the inverse is written back -- "exchange" form of GJ)
 //   branch check (reading R1'): kappa_inf(A) = ||A||_inf ||A^{-1}||_inf from the computed
-//       inverse; lazy: B is swept only when A is singular or kappa_inf(A) > KAPPA_SWITCH
+//       inverse; lazy: B is swept only when A is singular or kappa_inf(A) > kappa_switch(n)
 //   C = X^{-1} Y,  M = X + Y C,  Re = M^{-1} (sweep),  Im = -C Re
 //       the three GEMMs run on the FP64 tensor cores (DMMA m8n8k4) from shared memory
 //   store X interleaved (branch S1: Re - i(-Im) ... see the epilogue)
@@ -497,11 +497,11 @@ frob_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__rest
     int inf_x = sweep_info<double, N>(sm.sw, n, pmax);
     sweep_store<double, N, 4, 4>(a, sm.sw, Ws, C::S);
     if (branch == FROB_BRANCH_AUTO) {
-        // reading R1': kappa_inf(A) from the computed inverse; above KAPPA_SWITCH (or A singular)
+        // reading R1': kappa_inf(A) from the computed inverse; above kappa_switch(n) (or A singular)
         // sweep B too and keep the part with the smaller kappa_inf
         const double na = mat_norm_inf(n, [&](int i, int j) { return As[i * C::S + j]; }, sm.red, C::THREADS);
         const double ka = inf_x ? INFINITY : na * reg_norm_inf<N, 4, 4>(a, n, sm.red);
-        if (inf_x != 0 || !(ka <= KAPPA_SWITCH)) {
+        if (inf_x != 0 || !(ka <= kappa_switch(n))) {
             __syncthreads();
             load_blocks<double, N>(a, Bs, n);
             double qmax, qmin;
@@ -652,7 +652,7 @@ frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
             // reading R1' (see frob_batched_kernel)
             const double na = mat_norm_inf(n, [&](int i, int j) { return Zb[i * n + j].x; }, sm.red, T128);
             const double ka = inf_x ? INFINITY : na * reg_norm_inf<N, R128, B128>(a, n, sm.red);
-            if (inf_x != 0 || !(ka <= KAPPA_SWITCH)) {
+            if (inf_x != 0 || !(ka <= kappa_switch(n))) {
                 __syncthreads();
                 load_blocks_f<double, N, R128, B128>(a, n, [&](int i, int j) { return Zb[i * n + j].y; });
                 double qmax, qmin;

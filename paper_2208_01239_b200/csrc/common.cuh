@@ -6,8 +6,10 @@
 #include <cstddef>
 #include <climits>
 #include <cstdlib>
+#include <cmath>
 
 #define FROB_DEV __device__ __forceinline__
+#define FROB_DEV_HOST_INLINE __host__ __device__ inline
 
 namespace frob {
 
@@ -22,10 +24,13 @@ inline const char *tuning_env(const char *name) {
 #endif
 }
 
-// AUTO branch rule (reading R1'): S1 is kept while kappa_inf(A) = ||A||_inf ||A^-1||_inf
-// <= KAPPA_SWITCH (the conditioning of X drives the leading term of Thm 5.2's bound);
-// above it (or with A singular) both parts are inverted and the smaller kappa_inf wins.
-constexpr double KAPPA_SWITCH = 1.0e6;
+// AUTO branch rule (reading R1'): S1 is kept while kappa_inf(A) / sqrt(n) <= KAPPA_SWITCH,
+// kappa_inf(A) = ||A||_inf ||A^-1||_inf of the computed inverse (the conditioning of X drives the
+// leading term of Thm 5.2's bound; kappa_inf / sqrt(n) tracks kappa_2 of dense matrices
+// up to an O(1) factor); above it (or with A singular) both parts are inverted and the smaller
+// kappa_inf wins.
+constexpr double KAPPA_SWITCH = 8.8e4;
+FROB_DEV_HOST_INLINE double kappa_switch(int n) { return KAPPA_SWITCH * sqrt((double)n); }
 
 // process-wide count of kernel launches issued by the library (frob_launch_count())
 unsigned long long &launch_counter();

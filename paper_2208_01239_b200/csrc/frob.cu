@@ -157,12 +157,12 @@ enum { NRM_A = 0, NRM_AINV = 1, NRM_AL = 2, NRM_B = 3, NRM_BINV = 4, NRM_BL = 5,
 // Reading R1' decided on the device (FROB_OPT_DEVICE_AUTO): both parts factored and inverted;
 // flags[1] = 1 (S1), 2 (S2) or 0 (both singular)
 __global__ void auto_select_kernel(const LuStats *__restrict__ st, const unsigned long long *__restrict__ nrm,
-                                   int *__restrict__ flags) {
+                                   int n, int *__restrict__ flags) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const bool sa = st[0].info != 0, sb = st[1].info != 0;
     const double ka = kappa_of(nrm, NRM_A, NRM_AINV, -1, sa);
     int use = 1;
-    if (sa || !(ka <= KAPPA_SWITCH)) {
+    if (sa || !(ka <= kappa_switch(n))) {
         const double kb = kappa_of(nrm, NRM_B, NRM_BINV, -1, sb);
         use = (sa && sb) ? 0 : ((sa || (!sb && kb < ka)) ? 2 : 1);
     }
@@ -319,6 +319,12 @@ struct StatusOut {
     int *code = nullptr;
     bool any() const { return rec || code; }
 };
+// Optional row-block split of the final GEMM (a6): chunk c (rows [c rows_per, ...)) records ev[c]
+// on the stream when stored, so a caller can copy it out while the next chunk is computed.
+struct OutChunks {
+    int k = 1;
+    cudaEvent_t *ev = nullptr;
+};
 
 static cudaError_t finalize_status(const FrobWs &w, int use_host, int factored, bool kfused, int forced,
                                    StatusOut so, cudaStream_t s) {
@@ -425,7 +431,7 @@ static frob_status inv_norm_estimate(int n, const double *Ui, const double *Li, 
 static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *X, long long ldx,
                                  int branch, void *ws, size_t ws_bytes, cudaStream_t s,
                                  frob_info *host_info, double mu = 0.0, bool fused = false,
-                                 bool dev_auto = false, StatusOut so = StatusOut()) {
+                                 bool dev_auto = false, StatusOut so = StatusOut(), OutChunks oc = OutChunks()) {
     if (n < 1 || !Z || !X || ldz < n || ldx < n || branch < 0 || branch > 2) return FROB_ERR_INVALID_ARG;
     if (dev_auto && (branch != FROB_BRANCH_AUTO || fused)) return FROB_ERR_INVALID_ARG;
     if (overlap(Z, (size_t)((n - 1) * ldz + n) * 16, X, (size_t)((n - 1) * ldx + n) * 16))
@@ -557,7 +563,7 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
             return FROB_ERR_NONFINITE;
         }
         kap[0] = kappa_host(1);
-        if (hs[0].info != 0 || !(kap[0] <= KAPPA_SWITCH)) {
+        if (hs[0].info != 0 || !(kap[0] <= kappa_switch(n))) {
             FROB_ST(part(2, true));
             FROB_ST(part_norms(2, w.W1));
             FROB_CUDA(cudaMemcpyAsync(&hs[1], &w.stats[1], sizeof(LuStats), cudaMemcpyDeviceToHost, s));
@@ -590,7 +596,7 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
         FROB_ST(part(2, true));
         FROB_ST(part_norms(2, w.W1));
         count_launch(4);
-        auto_select_kernel<<<1, 32, 0, s>>>(w.stats, w.nrm, w.flags);
+        auto_select_kernel<<<1, 32, 0, s>>>(w.stats, w.nrm, n, w.flags);
         cond_copy_kernel<double><<<ew_blocks(mat), 256, 0, s>>>(w.W1, w.W4, mat, w.flags);
         cond_copy_kernel<int><<<ew_blocks(n), 256, 0, s>>>(w.perm_b, w.perm_x, n, w.flags);
         branch_rotate_kernel<<<ew_blocks((long long)n * n), 256, 0, s>>>(w.A, w.B, ld, n, w.flags);
@@ -648,13 +654,19 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
     }
     // a6/a7: Im' = -C Re', fused with the column interchanges and the interleaved store
     {
-        auto p = gemm_params<double>(n, n, n, -1.0, Cb, ld, Re, ld, 0.0, Re, ld, X, ldx);
-        p.epi = (use == 1) ? EPI_FROB_A : EPI_FROB_B;
-        p.dbranch = dev_auto ? w.flags + 1 : nullptr;
-        p.colperm = w.perm_m;
-        p.mu = mu;  // Alg 5 line 5: Z^{-1} = (1 + mu i) W
-        GemmTag tag("gemm:frob_Im");
-        FROB_CUDA(gemm_launch<double>(p, 1, s));
+        const int per = (oc.k > 1) ? (int)(((long long)n + oc.k - 1) / oc.k + 63) / 64 * 64 : n;
+        for (int r0 = 0, c = 0; r0 < n; r0 += per, ++c) {
+            const int rc = std::min(per, n - r0);
+            auto p = gemm_params<double>(rc, n, n, -1.0, Cb + (long long)r0 * ld, ld, Re, ld, 0.0,
+                                         Re + (long long)r0 * ld, ld, X + 2 * (long long)r0 * ldx, ldx);
+            p.epi = (use == 1) ? EPI_FROB_A : EPI_FROB_B;
+            p.dbranch = dev_auto ? w.flags + 1 : nullptr;
+            p.colperm = w.perm_m;
+            p.mu = mu;  // Alg 5 line 5: Z^{-1} = (1 + mu i) W
+            GemmTag tag("gemm:frob_Im");
+            FROB_CUDA(gemm_launch<double>(p, 1, s));
+            if (oc.ev && c < oc.k) FROB_CUDA(cudaEventRecord(oc.ev[c], s));
+        }
     }
     FROB_CUDA(finalize_status(w, dev_auto ? 0 : use, factored, false, 0, so, s));
     if (host_info) {
@@ -1019,39 +1031,15 @@ size_t frob_inv_host_workspace_bytes(int n) {
     return n < 1 ? 0 : align256(frob_inv_workspace_bytes(n)) + 2 * align256((size_t)n * n * 16) + 256;
 }
 
-frob_status frob_inv_host(int n, const double *Z_host, double *X_host, int branch, void *ws,
-                          size_t ws_bytes, void *stream, frob_info *host_info) {
-    if (n < 1 || !Z_host || !X_host) return FROB_ERR_INVALID_ARG;
-    if (!ws || ws_bytes < frob_inv_host_workspace_bytes(n)) return FROB_ERR_WORKSPACE;
-    cudaStream_t s = (cudaStream_t)stream;
-    unsigned char *b = reinterpret_cast<unsigned char *>(ws);
-    const size_t ib = align256(frob_inv_workspace_bytes(n));
-    double *Zd = reinterpret_cast<double *>(b + ib);
-    double *Xd = reinterpret_cast<double *>(b + ib + align256((size_t)n * n * 16));
-    StatusOut so;
-    so.code = reinterpret_cast<int *>(b + ib + 2 * align256((size_t)n * n * 16));
-    FROB_CUDA(cudaMemcpyAsync(Zd, Z_host, (size_t)n * n * 16, cudaMemcpyHostToDevice, s));
-    frob_status st = frob_inv_impl(n, Zd, n, Xd, n, branch, ws, ib, s, host_info, 0.0, false, false, so);
-    int code = FROB_OK;
-    if (st == FROB_OK) {
-        FROB_CUDA(cudaMemcpyAsync(X_host, Xd, (size_t)n * n * 16, cudaMemcpyDeviceToHost, s));
-        FROB_CUDA(cudaMemcpyAsync(&code, so.code, sizeof(int), cudaMemcpyDeviceToHost, s));
-    }
-    // every path waits for the copies that read / write the caller's host buffers
-    const cudaError_t e = cudaStreamSynchronize(s);
-    if (st != FROB_OK) return st;
-    if (e != cudaSuccess) return cuda_fail(e);
-    return (frob_status)code;
-}
-
 size_t frob_inv_host_many_workspace_bytes(int n) {
     return n < 1 ? 0 : align256(frob_inv_workspace_bytes(n)) + 4 * align256((size_t)n * n * 16) + 2 * 256;
 }
 
 // per-device copy streams and events of the pipelined host entry point
+constexpr int HOST_CHUNKS = 8;
 struct HostPipe {
     cudaStream_t h2d = nullptr, d2h = nullptr;
-    cudaEvent_t start, in[2], done[2], freed[2], fin;
+    cudaEvent_t start, in[2], done[2], freed[2], fin, chunk[HOST_CHUNKS];
     bool ok = false;
     std::mutex mu;
 };
@@ -1069,6 +1057,8 @@ static HostPipe &host_pipe(cudaError_t &err) {
         cudaEvent_t *evs[] = {&p.start, &p.in[0], &p.in[1], &p.done[0], &p.done[1], &p.freed[0], &p.freed[1], &p.fin};
         for (cudaEvent_t *e : evs)
             if (err == cudaSuccess) err = cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+        for (cudaEvent_t &e : p.chunk)
+            if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
         p.ok = (err == cudaSuccess);
     }
     return p;
@@ -1089,6 +1079,61 @@ static cudaError_t host_pipe_join(HostPipe &hp, cudaStream_t s) {
         cudaStreamSynchronize(hp.d2h);
     }
     return first;
+}
+
+frob_status frob_inv_host(int n, const double *Z_host, double *X_host, int branch, void *ws,
+                          size_t ws_bytes, void *stream, frob_info *host_info) {
+    if (n < 1 || !Z_host || !X_host) return FROB_ERR_INVALID_ARG;
+    if (!ws || ws_bytes < frob_inv_host_workspace_bytes(n)) return FROB_ERR_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned char *b = reinterpret_cast<unsigned char *>(ws);
+    const size_t ib = align256(frob_inv_workspace_bytes(n));
+    double *Zd = reinterpret_cast<double *>(b + ib);
+    double *Xd = reinterpret_cast<double *>(b + ib + align256((size_t)n * n * 16));
+    StatusOut so;
+    so.code = reinterpret_cast<int *>(b + ib + 2 * align256((size_t)n * n * 16));
+    // n >= 8192: the final GEMM runs in HOST_CHUNKS row blocks (>= 1024 rows: still several waves of
+    // tiles, no split-K, so every element is computed exactly as in one launch) and each block is
+    // copied out on a library-owned copy stream while the next one is computed
+    const int K = (n >= 8192) ? HOST_CHUNKS : 1;
+    cudaError_t ce = cudaSuccess;
+    HostPipe &hp = host_pipe(ce);
+    FROB_CUDA(ce);
+    std::unique_lock<std::mutex> guard(hp.mu, std::defer_lock);
+    OutChunks oc;
+    if (K > 1) {
+        guard.lock();
+        oc.k = K;
+        oc.ev = hp.chunk;
+    }
+    FROB_CUDA(cudaMemcpyAsync(Zd, Z_host, (size_t)n * n * 16, cudaMemcpyHostToDevice, s));
+    frob_status st = frob_inv_impl(n, Zd, n, Xd, n, branch, ws, ib, s, host_info, 0.0, false, false, so, oc);
+    int code = FROB_OK;
+    cudaError_t err = cudaSuccess;
+    if (st == FROB_OK && K > 1) {
+        err = cudaEventRecord(hp.start, s);
+        if (err == cudaSuccess) err = cudaStreamWaitEvent(hp.d2h, hp.start, 0);  // d2h after earlier work
+        const int per = (int)(((long long)n + K - 1) / K + 63) / 64 * 64;
+        for (int r0 = 0, c = 0; r0 < n && err == cudaSuccess; r0 += per, ++c) {
+            const int rc = std::min(per, n - r0);
+            err = cudaStreamWaitEvent(hp.d2h, hp.chunk[c], 0);
+            if (err == cudaSuccess)
+                err = cudaMemcpyAsync(X_host + 2 * (size_t)r0 * n, Xd + 2 * (size_t)r0 * n, (size_t)rc * n * 16,
+                                      cudaMemcpyDeviceToHost, hp.d2h);
+        }
+        if (err == cudaSuccess) err = cudaMemcpyAsync(&code, so.code, sizeof(int), cudaMemcpyDeviceToHost, s);
+        const cudaError_t ej = host_pipe_join(hp, s);
+        if (err == cudaSuccess) err = ej;
+    } else if (st == FROB_OK) {
+        err = cudaMemcpyAsync(X_host, Xd, (size_t)n * n * 16, cudaMemcpyDeviceToHost, s);
+        if (err == cudaSuccess) err = cudaMemcpyAsync(&code, so.code, sizeof(int), cudaMemcpyDeviceToHost, s);
+    }
+    // every path waits for the copies that read / write the caller's host buffers
+    const cudaError_t e = cudaStreamSynchronize(s);
+    if (st != FROB_OK) return st;
+    if (err != cudaSuccess) return cuda_fail(err);
+    if (e != cudaSuccess) return cuda_fail(e);
+    return (frob_status)code;
 }
 
 frob_status frob_inv_host_many(int n, int count, const double *Z_host, double *X_host, int branch, int *h_status,

@@ -31,7 +31,10 @@ constexpr int MV_INTS = 1 + 4 * PW_MAX;
 
 // Outer block width of the two-level LU (real 256: K = 256 outer GEMMs, n = 8192 LU 27.6 ->
 // 26.3 ms; complex 128, where 256 measured slower)
-template <typename T> struct LuNB { static constexpr int N = sizeof(T) == 8 ? 256 : 128; };
+#ifndef FROB_LUNB_D  // A/B build knob (tools/build_variant.sh): outer block of the blocked real LU
+#define FROB_LUNB_D 256
+#endif
+template <typename T> struct LuNB { static constexpr int N = sizeof(T) == 8 ? FROB_LUNB_D : 128; };
 // ints needed for the per-panel row-movement lists (mv) of an order-n LU
 size_t lu_mv_ints(int n);
 // elements of T workspace for the outer update (L11^{-1} x2, recursion scratch, U12 x2)

@@ -132,7 +132,7 @@ def _config3_part(n, total, chunk):
         bound = 1e-10 * np.maximum(1.0, kap[s:e] / 1e4)
         same = bu[s:e] == buo
         # branch decision: identical except where kappa_inf(A) sits within rounding of the switch point
-        near = (np.abs(rho[:, 2] / oracle.KAPPA_SWITCH - 1.0) < 1e-6) | (np.abs(rho[:, 3] / rho[:, 2] - 1.0) < 1e-6)
+        near = (np.abs(rho[:, 2] / (oracle.KAPPA_SWITCH * math.sqrt(n)) - 1.0) < 1e-6) | (np.abs(rho[:, 3] / rho[:, 2] - 1.0) < 1e-6)
         bad_branch = np.nonzero(~same & ~near)[0]
         assert bad_branch.size == 0, (n, s + bad_branch[:8], rho[bad_branch[:8]])
         for i in np.nonzero(~same)[0]:      # rounding-level ties: judge against the definition

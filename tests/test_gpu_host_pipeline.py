@@ -28,3 +28,14 @@ def test_host_many_matches_inv_host():
     xs = fb.inv_host_many(zs)
     for i in range(3):
         assert torch.equal(xs[i], fb.inv_host(zs[i].contiguous().pin_memory()))
+
+
+def test_inv_host_chunked_output_bitwise():
+    """n >= 8192: frob_inv_host copies X out in 8 row blocks while the final GEMM continues; the result
+    equals the device-resident frob_inv bit for bit."""
+    import paper_2208_01239_b200 as fb
+    n = 8192
+    zh = torch.from_numpy(synth.config2(n, seed=3)).pin_memory()
+    xh = fb.inv_host(zh)
+    ref = fb.inv(zh.cuda()).cpu()
+    assert torch.equal(xh, ref)

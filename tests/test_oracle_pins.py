@@ -314,7 +314,7 @@ def test_auto_switch_on_bad_a():
     a[:, 0] = a[:, 1] * (1 + 1e-9)
     b = rng.standard_normal((n, n)) + 4 * np.eye(n)
     x, st, info = oracle.frob_inv(a + 1j * b, "auto")
-    assert st == 0 and info["branch_used"] == 2 and info["kappa_a"] > oracle.KAPPA_SWITCH
+    assert st == 0 and info["branch_used"] == 2 and info["kappa_a"] > oracle.KAPPA_SWITCH * math.sqrt(n)
     assert info["kappa_b"] < info["kappa_a"]
     assert oracle.rel_fro(x, np.linalg.inv(a + 1j * b)) <= 1e-9
 
@@ -327,7 +327,7 @@ def test_auto_rule_kappa_inf_exact_and_switch_point():
     ka = np.abs(z.real).sum(1).max() * np.abs(np.linalg.inv(z.real)).sum(1).max()
     assert st == 0 and info["branch_used"] == 1 and abs(info["kappa_a"] - ka) <= 1e-12 * ka
     assert np.isnan(info["kappa_b"])                      # B untouched below the threshold
-    x2, st2, info2 = oracle.frob_inv(z, kappa_sw=0.5 * ka)  # force the comparison
+    x2, st2, info2 = oracle.frob_inv(z, kappa_sw=0.5 * ka / math.sqrt(40))  # force the comparison
     kb = np.abs(z.imag).sum(1).max() * np.abs(np.linalg.inv(z.imag)).sum(1).max()
     assert abs(info2["kappa_b"] - kb) <= 1e-12 * kb
     assert info2["branch_used"] == (2 if kb < ka else 1)
@@ -342,7 +342,7 @@ def test_auto_rule_fixes_ill_conditioned_a_with_small_pivot_ratio():
     z = synth.batch(128, 1, seed=0, start=7639)[0]
     ref, _ = oracle.zinv_gj(z)
     x, st, info = oracle.frob_inv(z)
-    assert st == 0 and info["branch_used"] == 2 and info["kappa_a"] > oracle.KAPPA_SWITCH
+    assert st == 0 and info["branch_used"] == 2 and info["kappa_a"] > oracle.KAPPA_SWITCH * math.sqrt(128)
     assert oracle.rel_fro(x, ref) <= 1e-11
     xa, _, _ = oracle.frob_inv(z, "a")
     assert oracle.rel_fro(xa, ref) > 1e-10
