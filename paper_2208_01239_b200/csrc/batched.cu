@@ -424,26 +424,24 @@ FROB_DEV double mat_norm_inf(int n, F f, double *scratch, int nthreads) {
 
 // ||X^{-1}||_inf of the inverse a Gauss-Jordan sweep left in the register blocks: the blocks hold
 // a row and column permutation of it (padding rows >= n: identity, padding columns: zero), which
-// leaves the maximum absolute row sum unchanged.  red: >= N * CT + 32 doubles.
+// leaves the maximum absolute row sum unchanged.  The CT threads of a block-row are consecutive
+// lanes of one warp, so each row sum is a shuffle reduction; scratch: >= 32 doubles.
 template <int N, int BR, int BC>
-FROB_DEV double reg_norm_inf(const double (&a)[BR][BC], int n, double *red) {
+FROB_DEV double reg_norm_inf(const double (&a)[BR][BC], int n, double *scratch) {
     using G = Geo<N, BR, BC>;
-    const int tid = threadIdx.x, ti = tid / G::CT, tj = tid % G::CT;
+    static_assert((G::CT & (G::CT - 1)) == 0 && G::CT <= 32, "block-rows must be lane groups");
+    const int tid = threadIdx.x, r0 = (tid / G::CT) * BR;
+    double m = 0.0;
 #pragma unroll
     for (int q = 0; q < BR; ++q) {
         double sum = 0.0;
 #pragma unroll
         for (int c = 0; c < BC; ++c) sum += fabs(a[q][c]);
-        red[(ti * BR + q) * G::CT + tj] = sum;
+#pragma unroll
+        for (int o = 1; o < G::CT; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (r0 + q < n) m = fmax(m, sum);
     }
-    __syncthreads();
-    double m = 0.0;
-    for (int r = tid; r < n; r += G::THREADS) {
-        double sum = 0.0;
-        for (int c = 0; c < G::CT; ++c) sum += red[r * G::CT + c];
-        m = fmax(m, sum);
-    }
-    return block_max(m, red + N * G::CT, G::THREADS);
+    return block_max(m, scratch, G::THREADS);
 }
 
 // ----------------------------------------------------------------- Frobenius kernel
@@ -463,7 +461,6 @@ template <int N>
 struct FrobSmem {
     double buf[3][N * BCfg<N>::S];
     typename FrobSweep<N>::SH sw;
-    double red[N * Geo<N>::CT + 32];   // R1' norm reductions
 };
 
 template <int N>
@@ -499,16 +496,16 @@ frob_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__rest
     if (branch == FROB_BRANCH_AUTO) {
         // reading R1': kappa_inf(A) from the computed inverse; above kappa_switch(n) (or A singular)
         // sweep B too and keep the part with the smaller kappa_inf
-        const double na = mat_norm_inf(n, [&](int i, int j) { return As[i * C::S + j]; }, sm.red, C::THREADS);
-        const double ka = inf_x ? INFINITY : na * reg_norm_inf<N, 4, 4>(a, n, sm.red);
+        const double na = mat_norm_inf(n, [&](int i, int j) { return As[i * C::S + j]; }, sm.sw.pmag_k, C::THREADS);
+        const double ka = inf_x ? INFINITY : na * reg_norm_inf<N, 4, 4>(a, n, sm.sw.pmag_k);
         if (inf_x != 0 || !(ka <= kappa_switch(n))) {
             __syncthreads();
             load_blocks<double, N>(a, Bs, n);
             double qmax, qmin;
             frob_sweep<N>(a, n, sm.sw, qmax, qmin);
             const int inf_b = sweep_info<double, N>(sm.sw, n, qmax);
-            const double nb = mat_norm_inf(n, [&](int i, int j) { return Bs[i * C::S + j]; }, sm.red, C::THREADS);
-            const double kb = inf_b ? INFINITY : nb * reg_norm_inf<N, 4, 4>(a, n, sm.red);
+            const double nb = mat_norm_inf(n, [&](int i, int j) { return Bs[i * C::S + j]; }, sm.sw.pmag_k, C::THREADS);
+            const double kb = inf_b ? INFINITY : nb * reg_norm_inf<N, 4, 4>(a, n, sm.sw.pmag_k);
             if (inf_b == 0 && (inf_x != 0 || kb < ka)) {
                 use = 2;
                 inf_x = 0;
@@ -568,7 +565,6 @@ constexpr int T128 = (128 / R128) * (128 / B128);
 struct Frob128Smem {
     double S[128 * 132];
     SweepShared<double, 128> sw;
-    double red[128 * (128 / B128) + 32];   // R1' norm reductions
 };
 
 // Steps a3..a7 for a fixed branch (USE = 1: X = A, Y = B; USE = 2: X = B, Y = -A), so the
@@ -650,16 +646,16 @@ frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
         sweep_store<double, N, R128, B128>(a, sm.sw, S, SS);
         if (branch == FROB_BRANCH_AUTO) {
             // reading R1' (see frob_batched_kernel)
-            const double na = mat_norm_inf(n, [&](int i, int j) { return Zb[i * n + j].x; }, sm.red, T128);
-            const double ka = inf_x ? INFINITY : na * reg_norm_inf<N, R128, B128>(a, n, sm.red);
+            const double na = mat_norm_inf(n, [&](int i, int j) { return Zb[i * n + j].x; }, sm.sw.pmag_k, T128);
+            const double ka = inf_x ? INFINITY : na * reg_norm_inf<N, R128, B128>(a, n, sm.sw.pmag_k);
             if (inf_x != 0 || !(ka <= kappa_switch(n))) {
                 __syncthreads();
                 load_blocks_f<double, N, R128, B128>(a, n, [&](int i, int j) { return Zb[i * n + j].y; });
                 double qmax, qmin;
                 gj_sweep<double, N, R128, B128>(a, n, sm.sw, qmax, qmin);
                 const int inf_b = sweep_info<double, N>(sm.sw, n, qmax);
-                const double nb = mat_norm_inf(n, [&](int i, int j) { return Zb[i * n + j].y; }, sm.red, T128);
-                const double kb = inf_b ? INFINITY : nb * reg_norm_inf<N, R128, B128>(a, n, sm.red);
+                const double nb = mat_norm_inf(n, [&](int i, int j) { return Zb[i * n + j].y; }, sm.sw.pmag_k, T128);
+                const double kb = inf_b ? INFINITY : nb * reg_norm_inf<N, R128, B128>(a, n, sm.sw.pmag_k);
                 if (inf_b == 0 && (inf_x != 0 || kb < ka)) {
                     use = 2;
                     inf_x = 0;

@@ -1111,8 +1111,7 @@ frob_status frob_inv_host(int n, const double *Z_host, double *X_host, int branc
     int code = FROB_OK;
     cudaError_t err = cudaSuccess;
     if (st == FROB_OK && K > 1) {
-        err = cudaEventRecord(hp.start, s);
-        if (err == cudaSuccess) err = cudaStreamWaitEvent(hp.d2h, hp.start, 0);  // d2h after earlier work
+        // (each copy waits only for its chunk's event, recorded on `stream` after that chunk's GEMM)
         const int per = (int)(((long long)n + K - 1) / K + 63) / 64 * 64;
         for (int r0 = 0, c = 0; r0 < n && err == cudaSuccess; r0 += per, ++c) {
             const int rc = std::min(per, n - r0);
