@@ -110,9 +110,9 @@ frob_status frob_inv(int n, const double *Z, long long ldz, double *X, long long
                      int branch, void *ws, size_t ws_bytes, void *stream, frob_info *host_info);
 
 /* frob_inv with options (bit mask):
- *   FROB_OPT_FUSED_FIRST_STEP  NEXT-1 (Thm 5.1 proof): C = X^{-1} Y is computed as
- *     U^{-1} (L^{-1} (P Y)) from the triangular inverses of LU(X) -- X^{-1} itself is never
- *     formed, 9 1/3 n^3 instead of 10 n^3 flops.  Same results up to rounding order.
+ *   FROB_OPT_FUSED_FIRST_STEP  NEXT-1 (Thm 5.1 proof): C = X^{-1} Y is computed by
+ *     solving L G = P Y and U C = G (blocked substitution with the LU factors) -- X^{-1} itself is
+ *     never formed, 8 2/3 n^3 instead of 10 n^3 flops.  Same results up to rounding order.
  * Unknown bits give FROB_ERR_INVALID_ARG.  Everything else as frob_inv. */
 #define FROB_OPT_FUSED_FIRST_STEP 1
 /*   FROB_OPT_DEVICE_AUTO  (branch must be FROB_BRANCH_AUTO, not with FROB_OPT_FUSED_FIRST_STEP)

@@ -348,37 +348,100 @@ static double nrm_val(unsigned long long v) {
     return d;
 }
 
+// ---------------------------------------------------------------------- NEXT-1 triangular solves
+// The paper's fused first step (Thm 5.1 proof) solves with the LU factors instead of
+// forming X^{-1}: L G = P Y, U C = G.  Blocked substitution on the GEMM engine: the NB x NB diagonal
+// blocks of L and U are inverted in place once (tri_inverses on each block; their strict off-block
+// parts stay the factors), then block row k: X_k = T_kk^{-1} W_k (triangular-operand GEMM) and the
+// not-yet-solved block rows W -= T_{.,k} X_k (K = NB GEMM).  n^3 flops per solve with n right-hand
+// sides, so the fused step costs 2/3 n^3 (LU) + 2 n^3 = the paper's T_inv + lambda T_mult.
+#ifndef FROB_TRSM_NB  // A/B build knob (tools/build_variant.sh)
+#define FROB_TRSM_NB 512
+#endif
+constexpr int TRSM_NB = FROB_TRSM_NB;
+
+static cudaError_t block_diag_invert(int n, double *U, double *L, long long ld, double *tmp, cudaStream_t s) {
+    for (int r0 = 0; r0 < n; r0 += TRSM_NB) {
+        const int rk = std::min(TRSM_NB, n - r0);
+        const cudaError_t e = tri_inverses<double>(rk, U + (long long)r0 * ld + r0, L ? L + (long long)r0 * ld + r0 : nullptr,
+                                                   ld, tmp, s);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+// Solve T X = W (T n x n triangular, its TRSM_NB diagonal blocks inverted by block_diag_invert; W n x m,
+// destroyed; X n x m).  lower: forward substitution by block rows, else backward.
+static cudaError_t trsm_blocked(int n, int m, const double *T, long long ldt, bool lower, double *W, long long ldw,
+                                double *X, long long ldx, cudaStream_t s) {
+    const int nb = (n + TRSM_NB - 1) / TRSM_NB;
+    cudaError_t e;
+    for (int step = 0; step < nb; ++step) {
+        const int kb = lower ? step : nb - 1 - step;
+        const int r0 = kb * TRSM_NB, rk = std::min(TRSM_NB, n - r0);
+        auto p = gemm_params<double>(rk, m, rk, 1.0, T + (long long)r0 * ldt + r0, ldt, W + (long long)r0 * ldw, ldw,
+                                     0.0, nullptr, ldx, X + (long long)r0 * ldx, ldx);
+        p.triA = lower ? TRI_LOWER : TRI_UPPER;
+        if ((e = gemm_launch<double>(p, 1, s)) != cudaSuccess) return e;
+        const int u0 = lower ? r0 + rk : 0, ur = lower ? n - r0 - rk : r0;  // rows still to solve
+        if (ur > 0) {
+            auto q = gemm_params<double>(ur, m, rk, -1.0, T + (long long)u0 * ldt + r0, ldt, X + (long long)r0 * ldx,
+                                         ldx, 1.0, W + (long long)u0 * ldw, ldw, W + (long long)u0 * ldw, ldw);
+            if ((e = gemm_launch<double>(q, 1, s)) != cudaSuccess) return e;
+        }
+    }
+    return cudaSuccess;
+}
+
+// dst (n x n, ldd) = src^T
+__global__ void __launch_bounds__(256) transpose_d_kernel(const double *__restrict__ src, long long lds,
+                                                          double *__restrict__ dst, long long ldd, int n) {
+    __shared__ double tile[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int tiles = (n + 31) / 32;
+    for (int t = blockIdx.x; t < tiles * tiles; t += gridDim.x) {
+        const int bi = t / tiles, bj = t % tiles;
+        __syncthreads();
+        for (int r = ty; r < 32; r += 8) {
+            const int i = bi * 32 + r, j = bj * 32 + tx;
+            if (i < n && j < n) tile[r][tx] = src[(long long)i * lds + j];
+        }
+        __syncthreads();
+        for (int r = ty; r < 32; r += 8) {
+            const int i = bj * 32 + r, j = bi * 32 + tx;
+            if (i < n && j < n) dst[(long long)i * ldd + j] = tile[tx][r];
+        }
+    }
+}
+
+// out[i][j] = sgn * Y[perm[i]][j]  (P Y, with the S2 sign)
+__global__ void gather_rows_signed_kernel(const double *__restrict__ Y, long long ld, const int *__restrict__ perm,
+                                          double sgn, int n, double *__restrict__ out) {
+    const long long total = (long long)n * n;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / n), j = (int)(idx - (long long)i * n);
+        out[(long long)i * ld + j] = sgn * Y[(long long)perm[i] * ld + j];
+    }
+}
+
 // ||X^{-1}||_inf for NEXT-1, which never forms X^{-1} (R1'): the Hager-Higham estimate (LAPACK
-// dlacon's iteration, at most 5 steps) of ||B||_1 for B = X^{-T} = P^T L^{-T} U^{-T}, from the
-// explicit triangular inverses Ui = U^{-1}, Li = L^{-1} and perm ((P Y)[i] = Y[perm[i]]).  Products on
-// the GEMM engine: B x = P^T ((x^T Ui) Li)^T as row-vector products, B^T v = X^{-1} v = Ui (Li (P v)).
-// A lower bound of the exact norm (it is exact for most matrices); synchronises per step.
-static frob_status inv_norm_estimate(int n, const double *Ui, const double *Li, long long ld, const int *perm,
-                                     double *vec, cudaStream_t s, double *out) {
+// dlacon's iteration, at most 5 steps) of ||B||_1 for B = X^{-T} = P^T L^{-T} U^{-T}, by blocked
+// solves with the factors (U, L: diagonal blocks inverted) and their transposes (Ut = U^T lower,
+// Lt = L^T upper); perm: (P Y)[i] = Y[perm[i]].  A lower bound of the exact norm (exact for most
+// matrices); synchronises per step.
+static frob_status inv_norm_estimate(int n, const double *U, const double *L, const double *Ut, const double *Lt,
+                                     long long ld, const int *perm, double *vec, cudaStream_t s, double *out) {
     const long long lv = ld_of(n);
     double *v0 = vec, *v1 = vec + lv, *v2 = vec + 2 * lv;
     std::vector<int> hp(n);
     std::vector<double> x(n, 1.0 / n), y(n), t(n), z(n);
     FROB_CUDA(cudaMemcpyAsync(hp.data(), perm, n * sizeof(int), cudaMemcpyDeviceToHost, s));
-    auto rowprod = [&](const double *in, const double *M, int tri, double *o) -> frob_status {  // o = in^T M
-        auto p = gemm_params<double>(1, n, n, 1.0, in, n, M, ld, 0.0, nullptr, n, o, n);
-        p.triB = tri;
-        GemmTag tag("gemm:inv_norm_est");
-        FROB_CUDA(gemm_launch<double>(p, 1, s));
-        return FROB_OK;
-    };
-    auto colprod = [&](const double *M, int tri, const double *in, double *o) -> frob_status {  // o = M in
-        auto p = gemm_params<double>(n, 1, n, 1.0, M, ld, in, 1, 0.0, nullptr, 1, o, 1);
-        p.triA = tri;
-        GemmTag tag("gemm:inv_norm_est");
-        FROB_CUDA(gemm_launch<double>(p, 1, s));
-        return FROB_OK;
-    };
+    GemmTag tag("gemm:inv_norm_est");
     auto apply_B = [&](const std::vector<double> &in, std::vector<double> &o) -> frob_status {  // o = X^{-T} in
         FROB_CUDA(cudaMemcpyAsync(v0, in.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
-        frob_status st = rowprod(v0, Ui, TRI_UPPER, v1);
-        if (st != FROB_OK) return st;
-        if ((st = rowprod(v1, Li, TRI_LOWER, v2)) != FROB_OK) return st;
+        FROB_CUDA(trsm_blocked(n, 1, Ut, ld, true, v0, 1, v1, 1, s));    // U^T w = in
+        FROB_CUDA(trsm_blocked(n, 1, Lt, ld, false, v1, 1, v2, 1, s));   // L^T v = w
         FROB_CUDA(cudaMemcpyAsync(t.data(), v2, n * sizeof(double), cudaMemcpyDeviceToHost, s));
         FROB_CUDA(cudaStreamSynchronize(s));
         for (int i = 0; i < n; ++i) o[hp[i]] = t[i];  // P^T
@@ -387,9 +450,8 @@ static frob_status inv_norm_estimate(int n, const double *Ui, const double *Li, 
     auto apply_BT = [&](const std::vector<double> &in, std::vector<double> &o) -> frob_status {  // o = X^{-1} in
         for (int i = 0; i < n; ++i) t[i] = in[hp[i]];  // P in
         FROB_CUDA(cudaMemcpyAsync(v0, t.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
-        frob_status st = colprod(Li, TRI_LOWER, v0, v1);
-        if (st != FROB_OK) return st;
-        if ((st = colprod(Ui, TRI_UPPER, v1, v2)) != FROB_OK) return st;
+        FROB_CUDA(trsm_blocked(n, 1, L, ld, true, v0, 1, v1, 1, s));
+        FROB_CUDA(trsm_blocked(n, 1, U, ld, false, v1, 1, v2, 1, s));
         FROB_CUDA(cudaMemcpyAsync(o.data(), v2, n * sizeof(double), cudaMemcpyDeviceToHost, s));
         FROB_CUDA(cudaStreamSynchronize(s));
         return FROB_OK;
@@ -509,7 +571,7 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
             }
         }
         factored |= u;
-        FROB_CUDA(tri_inverses<double>(n, w.W2, w.W3, ld, w.W1, s));
+        FROB_CUDA(block_diag_invert(n, w.W2, w.W3, ld, w.W1, s));
         return FROB_OK;
     };
     // norms of part u for kappa_inf (R1'): ||X|| and ||Xinv'|| (literal) or ||U^-1||, ||L^-1|| (NEXT-1)
@@ -522,7 +584,12 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
             // NEXT-1: the Hager-Higham estimate of ||X^{-1}||_inf from U^{-1}, L^{-1} (host loop),
             // written into the same slot (bit pattern of a non-negative double)
             double e = 0.0;
-            const frob_status st = inv_norm_estimate(n, w.W2, w.W3, ld, w.perm_x, w.vec, s, &e);
+            count_launch(2);
+            const int tb = (int)std::min<long long>((long long)((n + 31) / 32) * ((n + 31) / 32), 148LL * 8);
+            transpose_d_kernel<<<tb, 256, 0, s>>>(w.W2, ld, w.W4, ld, n);  // U^T (lower)
+            transpose_d_kernel<<<tb, 256, 0, s>>>(w.W3, ld, w.W5, ld, n);  // L^T (upper)
+            FROB_CUDA(cudaGetLastError());
+            const frob_status st = inv_norm_estimate(n, w.W2, w.W3, w.W4, w.W5, ld, w.perm_x, w.vec, s, &e);
             if (st != FROB_OK) return st;
             unsigned long long bits;
             std::memcpy(&bits, &e, sizeof(bits));
@@ -617,16 +684,15 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
         GemmTag tag("gemm:frob_C");
         FROB_CUDA(gemm_launch<double>(p, 1, s));
     } else {
-        // a2+a3 fused (NEXT-1): C = U^{-1} (L^{-1} (P Y)); X^{-1} is never formed
-        GemmTag tag("gemm:frob_C_tri");
-        auto p = gemm_params<double>(n, n, n, sgn, Lf, ld, Ym, ld, 0.0, nullptr, ld, w.W4, ld);
-        p.triA = TRI_LOWER;
-        p.browmap = w.perm_x;
-        FROB_CUDA(gemm_launch<double>(p, 1, s));
+        // a2+a3 fused (NEXT-1): L G = P Y, U C = G by blocked substitution; X^{-1} is
+        // never formed (W4 = sgn P Y, G -> W5, C -> W1)
+        count_launch();
+        gather_rows_signed_kernel<<<ew_blocks((long long)n * n), 256, 0, s>>>(Ym, ld, w.perm_x, sgn, n, w.W4);
+        FROB_CUDA(cudaGetLastError());
+        GemmTag tag("gemm:frob_trsm");
+        FROB_CUDA(trsm_blocked(n, n, Lf, ld, true, w.W4, ld, w.W5, ld, s));
         Cb = w.W1;
-        auto q = gemm_params<double>(n, n, n, 1.0, Uf, ld, w.W4, ld, 0.0, nullptr, ld, Cb, ld);
-        q.triA = TRI_UPPER;
-        FROB_CUDA(gemm_launch<double>(q, 1, s));
+        FROB_CUDA(trsm_blocked(n, n, Uf, ld, false, w.W5, ld, Cb, ld, s));
     }
     // a4: M = X + Y C
     {

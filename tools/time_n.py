@@ -1,4 +1,4 @@
-"""Median time of frob_inv / zinv at size n (no profiler, CUDA events). Usage: python tools/time_n.py N [frob|zinv] [reps]"""
+"""Median time of frob_inv / NEXT-1 / zinv at size n (no profiler, CUDA events). Usage: python tools/time_n.py N [frob|fused|zinv] [reps]"""
 import sys, os, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -6,10 +6,11 @@ import synth
 import paper_2208_01239_b200 as fb
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 which = sys.argv[2] if len(sys.argv) > 2 else "frob"
-reps = int(sys.argv[3]) if len(sys.argv) > 3 else 10
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else (10 if n <= 8192 else 3)
 z = torch.from_numpy(synth.config2(n)).cuda()
 x = torch.empty_like(z)
-fn = (lambda: fb.inv(z, out=x)) if which == "frob" else (lambda: fb.zinv(z, out=x))
+fn = {"frob": lambda: fb.inv(z, out=x), "fused": lambda: fb.inv(z, out=x, fused=True),
+      "zinv": lambda: fb.zinv(z, out=x)}[which]
 for _ in range(3):
     fn()
 torch.cuda.synchronize()
