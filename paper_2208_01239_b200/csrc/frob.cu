@@ -353,10 +353,11 @@ static double nrm_val(unsigned long long v) {
 // forming X^{-1}: L G = P Y, U C = G.  Blocked substitution on the GEMM engine: the NB x NB diagonal
 // blocks of L and U are inverted in place once (tri_inverses on each block; their strict off-block
 // parts stay the factors), then block row k: X_k = T_kk^{-1} W_k (triangular-operand GEMM) and the
-// not-yet-solved block rows W -= T_{.,k} X_k (K = NB GEMM).  n^3 flops per solve with n right-hand
+// not-yet-solved block rows W -= T_{.,k} X_k (K = NB GEMM).  NB = 2048 (A/B at n = 2048 ... 16384:
+// 256 / 512 / 1024 / 2048 / 4096 -> 1368 / 1308 / 1284 / 1278 / 1279 ms at n = 16384).  n^3 flops per solve with n right-hand
 // sides, so the fused step costs 2/3 n^3 (LU) + 2 n^3 = the paper's T_inv + lambda T_mult.
 #ifndef FROB_TRSM_NB  // A/B build knob (tools/build_variant.sh)
-#define FROB_TRSM_NB 512
+#define FROB_TRSM_NB 2048
 #endif
 constexpr int TRSM_NB = FROB_TRSM_NB;
 

@@ -282,6 +282,19 @@ FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int ro
         }
     };
 
+    auto compute_stage = [&](int kt) {
+        const T *as = As + (kt % STAGES) * BM * SA;
+        const T *bs = Bs + (kt % STAGES) * BK * SB;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            T a[MT], b[NT];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) a[i] = as[(wm0 + i * 8 + g) * SA + kk + t];
+#pragma unroll
+            for (int j = 0; j < NT; ++j) b[j] = bs[(kk + t) * SB + wn0 + j * 8 + g];
+            mma_tile<MT, NT>(acc, a, b);
+        }
+    };
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
         if (s < nk) load_stage(s, s);
@@ -295,17 +308,7 @@ FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int ro
             if (nx < nk) load_stage(nx % STAGES, nx);
             cp_async_commit();
         }
-        const T *as = As + (kt % STAGES) * BM * SA;
-        const T *bs = Bs + (kt % STAGES) * BK * SB;
-#pragma unroll
-        for (int kk = 0; kk < BK; kk += 4) {
-            T a[MT], b[NT];
-#pragma unroll
-            for (int i = 0; i < MT; ++i) a[i] = as[(wm0 + i * 8 + g) * SA + kk + t];
-#pragma unroll
-            for (int j = 0; j < NT; ++j) b[j] = bs[(kk + t) * SB + wn0 + j * 8 + g];
-            mma_tile<MT, NT>(acc, a, b);
-        }
+        compute_stage(kt);
     }
     cp_async_wait<0>();
     if (!p.counter && !p.early_trigger) pdl_trigger();
