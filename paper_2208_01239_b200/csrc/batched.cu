@@ -21,6 +21,9 @@
 
 namespace frob {
 
+FROB_DEV double fast_recip(double x) { return frcp(x); }
+FROB_DEV double2 fast_recip(double2 x) { return recip(x); }
+
 // Register-block geometry: N x N matrix, each thread owns a BR x BC block.
 template <int N, int BR = 4, int BC = 4>
 struct Geo {
@@ -142,9 +145,11 @@ FROB_DEV void gj_sweep(T (&a)[BR][BC], int n, SweepShared<T, N> &sh, double &pma
                                           lane < G::RT ? sh.candi[par][lane] : INT_MAX);
         const int p = m.i;
         const T piv = sh.colk[par][p];
-        const T ip = is_zero(piv) ? zero_of(T()) : recip(piv);
         if (tid == 0) { sh.pivrow[k] = p; sh.pmag_k[k] = pmag(piv); sh.pos[p] = 1; }
         if (ti == p / BR) {
+            // 1/piv only where it is used: the pivot row's block-row scales the row for everyone
+            // (a correctly rounded division is a multi-instruction sequence with a slow-path branch)
+            const T ip = is_zero(piv) ? zero_of(T()) : recip(piv);
             const int q = p % BR;
 #pragma unroll
             for (int c = 0; c < BC; ++c) {
@@ -242,7 +247,9 @@ FROB_DEV void gj_sweep_1bar(T (&a)[BR][BC], int n, SweepShared1<T, N> &sh, doubl
         const int p = m.i;
         const int tip = p / BR;
         const T piv = sh.slot[par][tip][k];
-        const T ip = is_zero(piv) ? zero_of(T()) : recip(piv);
+        // every thread scales its own copy of the pivot row: the branch-free reciprocal for real
+        // pivots (MUFU + two Newton steps, ~1 ulp) instead of the correctly rounded division
+        const T ip = is_zero(piv) ? zero_of(T()) : fast_recip(piv);
         if (tid == 0) { sh.pivrow[k] = p; sh.pmag_k[k] = pmag(piv); }
         if (tip == ti) used |= 1u << (p - r0);
         // exchange-form update, uniform over the block: the owner of column k first zeroes it
