@@ -184,3 +184,18 @@ def test_auto_rule_kappa_switch_matches_oracle():
     assert idv["branch_used"] == 2 and torch.equal(xd, x)
     xf, ifu = fb.inv(_t(z), fused=True, info=True)
     assert ifu["branch_used"] == 2 and oracle.rel_fro(xf.cpu().numpy(), ref) <= 1e-11
+
+
+@pytest.mark.parametrize("n", [100, 1100, 4200])
+def test_fused_kappa_estimate_vs_exact(n):
+    """NEXT-1's AUTO rule uses the Hager-Higham estimate of ||A^-1||_inf (blocked substitution with the
+    LU factors and their transposes); it is a lower bound of the exact kappa_inf the literal path
+    computes from X^{-1}, and for these inputs it is exact to rounding."""
+    z = synth.config2(n, seed=n + 5)
+    zt = _t(z)
+    _, il = fb.inv(zt, info=True)
+    _, ifu = fb.inv(zt, fused=True, info=True)
+    assert il["branch_used"] == ifu["branch_used"] == 1
+    kl, kf = il["kappa_a"], ifu["kappa_a"]
+    assert kf <= kl * (1 + 1e-9) and kf >= kl / 3.0, (kl, kf)
+    assert abs(kf / kl - 1.0) < 1e-6, (kl, kf)
