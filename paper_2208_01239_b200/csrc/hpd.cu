@@ -28,11 +28,19 @@ FROB_DEV double2 conj_of(double2 v) { return make_double2(v.x, -v.y); }
 FROB_DEV double re_part(double v) { return v; }
 FROB_DEV double re_part(double2 v) { return v.x; }
 FROB_DEV double2 from_real(double v, double2) { return make_double2(v, 0.0); }
+FROB_DEV double shfl_xor4(double v, int o) { return __shfl_xor_sync(0xffffffffu, v, o); }
+FROB_DEV double2 shfl_xor4(double2 v, int o) {
+    return make_double2(__shfl_xor_sync(0xffffffffu, v.x, o), __shfl_xor_sync(0xffffffffu, v.y, o));
+}
 FROB_DEV double from_real(double v, double) { return v; }
 
 // Factor the diagonal block (k0, k0) in place (upper; zeros below inside the block) and write
 // W^H = (U_kk^{-1})^H (lower triangular, CHOL_NB x CHOL_NB, ld CHOL_NB) to wh.  info: first
 // 1-based column with a non-positive pivot (atomicMin; INT_MAX = none).
+// 256 threads as 16 x 16: two barriers per column (every thread derives the pivot and its reciprocal
+// from S[j][j] itself; the scaled row j, then the trailing upper triangle in 2-D strides, no index
+// divisions); U_kk^{-1} by row-wise back substitution with 4 threads per column (shuffle-summed
+// partial dot products, one barrier per row) from the reciprocals kept during the factorisation.
 template <typename T>
 __global__ void __launch_bounds__(256) chol_diag_kernel(T *__restrict__ A, long long ld, int n, int k0,
                                                         T *__restrict__ wh, int *__restrict__ info) {
@@ -40,59 +48,58 @@ __global__ void __launch_bounds__(256) chol_diag_kernel(T *__restrict__ A, long 
     typedef T Row[CHOL_NB + 1];
     Row *S = reinterpret_cast<Row *>(chol_smem);          // the block, then U_kk
     Row *W = S + CHOL_NB;                                  // U_kk^{-1}
-    __shared__ double piv_s;
-    const int tid = threadIdx.x;
+    __shared__ double pdiag[CHOL_NB], rdiag[CHOL_NB];      // u_jj and 1 / u_jj
+    const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
     const int nb = min(CHOL_NB, n - k0);
-    for (int idx = tid; idx < CHOL_NB * CHOL_NB; idx += blockDim.x) {
-        const int i = idx / CHOL_NB, j = idx % CHOL_NB;
-        S[i][j] = (i < nb && j < nb) ? A[(long long)(k0 + i) * ld + k0 + j]
-                                     : ((i == j) ? one_of(T()) : zero_of(T()));
-    }
+    for (int i = ty; i < CHOL_NB; i += 16)
+        for (int j = tx; j < CHOL_NB; j += 16)
+            S[i][j] = (i < nb && j < nb) ? A[(long long)(k0 + i) * ld + k0 + j]
+                                         : ((i == j) ? one_of(T()) : zero_of(T()));
     __syncthreads();
     for (int j = 0; j < nb; ++j) {
-        if (tid == 0) {
-            const double d = re_part(S[j][j]);
-            if (!(d > 0.0)) atomicMin(info, k0 + j + 1);
-            piv_s = sqrt(d);  // NaN for a failed pivot: the result is flagged through info
-        }
-        __syncthreads();
-        const double p = piv_s;
+        const double d = re_part(S[j][j]);
+        const double p = sqrt(d);  // NaN for a failed pivot: the result is flagged through info
         const double ip = 1.0 / p;
-        // row j of U: U[j][c] = S[j][c] / p (c > j), U[j][j] = p
-        for (int c = j + 1 + tid; c < nb; c += blockDim.x) S[j][c] = scal(S[j][c], ip);
-        if (tid == 0) S[j][j] = from_real(p, T());
+        if (tid == 0) {
+            if (!(d > 0.0)) atomicMin(info, k0 + j + 1);
+            pdiag[j] = p;
+            rdiag[j] = ip;
+        }
+        // row j of U: U[j][c] = S[j][c] / p (c > j); U[j][j] = p is written at the end
+        for (int c = j + 1 + tid; c < nb; c += 256) S[j][c] = scal(S[j][c], ip);
         __syncthreads();
         // trailing upper part: S[r][c] -= conj(U[j][r]) U[j][c], j < r <= c
-        const int m = nb - j - 1;
-        for (int idx = tid; idx < m * m; idx += blockDim.x) {
-            const int r = j + 1 + idx / m, c = j + 1 + idx % m;
-            if (c >= r) S[r][c] = msub(S[r][c], conj_of(S[j][r]), S[j][c]);
+        for (int r = j + 1 + ty; r < nb; r += 16) {
+            const T ur = conj_of(S[j][r]);
+            for (int c = r + tx; c < nb; c += 16) S[r][c] = msub(S[r][c], ur, S[j][c]);
         }
         __syncthreads();
     }
-    for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
-        const int i = idx / nb, j = idx % nb;
-        A[(long long)(k0 + i) * ld + k0 + j] = (j >= i) ? S[i][j] : zero_of(T());
-    }
-    // W = U_kk^{-1}: column c by back substitution (U W = I), then W^H
-    if (tid < nb) {
-        const int c = tid;
+    for (int i = ty; i < nb; i += 16)
+        for (int j = tx; j < nb; j += 16)
+            A[(long long)(k0 + i) * ld + k0 + j] = (j > i) ? S[i][j] : ((j == i) ? from_real(pdiag[i], T()) : zero_of(T()));
+    // W = U_kk^{-1} (upper): rows from the bottom, W[i][c] = (delta_ic - sum_{i<q<=c} U[i][q] W[q][c]) / u_ii,
+    // column c on the 4 consecutive lanes 4c .. 4c + 3 (a quarter of the q range each)
+    {
+        const int c = tid >> 2, l = tid & 3;
         for (int i = CHOL_NB - 1; i >= 0; --i) {
-            T acc = (i == c) ? one_of(T()) : zero_of(T());
-            if (i <= c && i < nb) {
-                for (int q = i + 1; q <= c; ++q) acc = msub(acc, S[i][q], W[q][c]);
-                acc = scal(acc, 1.0 / re_part(S[i][i]));
-            } else {
-                acc = zero_of(T());
+            T acc = zero_of(T());
+            if (i < nb && c < nb && c > i)
+                for (int q = i + 1 + l; q <= c; q += 4) acc = msub(acc, S[i][q], W[q][c]);
+            acc = add(acc, shfl_xor4(acc, 1));
+            acc = add(acc, shfl_xor4(acc, 2));
+            if (l == 0) {
+                T v = zero_of(T());
+                if (i < nb && c < nb && c >= i) v = scal(add(acc, (c == i) ? one_of(T()) : zero_of(T())), rdiag[i]);
+                else if (i >= nb && c == i) v = one_of(T());
+                W[i][c] = v;
             }
-            W[i][c] = acc;
+            __syncthreads();
         }
     }
-    __syncthreads();
-    for (int idx = tid; idx < CHOL_NB * CHOL_NB; idx += blockDim.x) {
-        const int i = idx / CHOL_NB, j = idx % CHOL_NB;
-        wh[idx] = (i < nb && j < nb) ? conj_of(W[j][i]) : zero_of(T());
-    }
+    for (int i = ty; i < CHOL_NB; i += 16)
+        for (int j = tx; j < CHOL_NB; j += 16)
+            wh[i * CHOL_NB + j] = (i < nb && j < nb) ? conj_of(W[j][i]) : zero_of(T());
 }
 
 // dst (cols x rows, ldd) = src (rows x cols, lds)^T (conjugated if conj)
