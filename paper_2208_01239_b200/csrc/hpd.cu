@@ -15,6 +15,7 @@
 // The GEMM engine takes no transposed operands, so every ^T / ^H is an explicit transpose.
 #include <algorithm>
 #include <climits>
+#include <utility>
 #include <cstdio>
 #include "lu.cuh"
 #include "../../include/frobinv.h"
@@ -28,78 +29,137 @@ FROB_DEV double2 conj_of(double2 v) { return make_double2(v.x, -v.y); }
 FROB_DEV double re_part(double v) { return v; }
 FROB_DEV double re_part(double2 v) { return v.x; }
 FROB_DEV double2 from_real(double v, double2) { return make_double2(v, 0.0); }
-FROB_DEV double shfl_xor4(double v, int o) { return __shfl_xor_sync(0xffffffffu, v, o); }
-FROB_DEV double2 shfl_xor4(double2 v, int o) {
-    return make_double2(__shfl_xor_sync(0xffffffffu, v.x, o), __shfl_xor_sync(0xffffffffu, v.y, o));
+FROB_DEV double shfl_mask(double v, int src, unsigned mask) { return __shfl_sync(mask, v, src); }
+FROB_DEV double2 shfl_mask(double2 v, int src, unsigned mask) {
+    return make_double2(__shfl_sync(mask, v.x, src), __shfl_sync(mask, v.y, src));
+}
+template <typename F, int... J>
+FROB_DEV void bstatic_for_h_impl(F &&f, std::integer_sequence<int, J...>) {
+    (f(std::integral_constant<int, J>{}), ...);
+}
+template <int K, typename F>
+FROB_DEV void bstatic_for_h(F &&f) {
+    bstatic_for_h_impl(f, std::make_integer_sequence<int, K>{});
 }
 FROB_DEV double from_real(double v, double) { return v; }
 
 // Factor the diagonal block (k0, k0) in place (upper; zeros below inside the block) and write
 // W^H = (U_kk^{-1})^H (lower triangular, CHOL_NB x CHOL_NB, ld CHOL_NB) to wh.  info: first
 // 1-based column with a non-positive pivot (atomicMin; INT_MAX = none).
-// 256 threads as 16 x 16: two barriers per column (every thread derives the pivot and its reciprocal
-// from S[j][j] itself; the scaled row j, then the trailing upper triangle in 2-D strides, no index
-// divisions); U_kk^{-1} by row-wise back substitution with 4 threads per column (shuffle-summed
-// partial dot products, one barrier per row) from the reciprocals kept during the factorisation.
+// The 64 x 64 block lives in REGISTERS: 256 threads as 16 x 16, thread (ti, tj) owns rows 4 ti ..,
+// columns 4 tj .. (the column index inside a 4-block is static: the steps are unrolled by 4).
+// Cholesky step j: the 16 threads of row j's block-row (one half-warp) take u_jj from the diagonal
+// owner by a shuffle, scale their part of row j and publish it (double-buffered); ONE barrier; every
+// thread applies the rank-1 update conj(U[j][r]) U[j][c] to its upper-triangle entries.  Then
+// U_kk^{-1} in place by the exchange (Gauss-Jordan) sweep without pivoting -- u_jj is unchanged by
+// earlier steps of an upper-triangular sweep, so 1 / u_jj comes from the factorisation -- again
+// one barrier per step (column j and the scaled row j published together).
 template <typename T>
 __global__ void __launch_bounds__(256) chol_diag_kernel(T *__restrict__ A, long long ld, int n, int k0,
                                                         T *__restrict__ wh, int *__restrict__ info) {
-    extern __shared__ __align__(16) unsigned char chol_smem[];
-    typedef T Row[CHOL_NB + 1];
-    Row *S = reinterpret_cast<Row *>(chol_smem);          // the block, then U_kk
-    Row *W = S + CHOL_NB;                                  // U_kk^{-1}
-    __shared__ double pdiag[CHOL_NB], rdiag[CHOL_NB];      // u_jj and 1 / u_jj
-    const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+    __shared__ T rowb[2][CHOL_NB], colb[2][CHOL_NB];
+    __shared__ double rdiag[CHOL_NB];
+    const int tid = threadIdx.x, ti = tid >> 4, tj = tid & 15, r0 = ti * 4, c0 = tj * 4;
+    const int half = (tid & 31) & 16;
+    const unsigned hmask = 0xffffu << half;
     const int nb = min(CHOL_NB, n - k0);
-    for (int i = ty; i < CHOL_NB; i += 16)
-        for (int j = tx; j < CHOL_NB; j += 16)
-            S[i][j] = (i < nb && j < nb) ? A[(long long)(k0 + i) * ld + k0 + j]
-                                         : ((i == j) ? one_of(T()) : zero_of(T()));
-    __syncthreads();
-    for (int j = 0; j < nb; ++j) {
-        const double d = re_part(S[j][j]);
-        const double p = sqrt(d);  // NaN for a failed pivot: the result is flagged through info
-        const double ip = 1.0 / p;
-        if (tid == 0) {
-            if (!(d > 0.0)) atomicMin(info, k0 + j + 1);
-            pdiag[j] = p;
-            rdiag[j] = ip;
+    T a[4][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int i = r0 + q, j = c0 + c;
+            a[q][c] = (i < nb && j < nb) ? A[(long long)(k0 + i) * ld + k0 + j] : ((i == j) ? one_of(T()) : zero_of(T()));
         }
-        // row j of U: U[j][c] = S[j][c] / p (c > j); U[j][j] = p is written at the end
-        for (int c = j + 1 + tid; c < nb; c += 256) S[j][c] = scal(S[j][c], ip);
-        __syncthreads();
-        // trailing upper part: S[r][c] -= conj(U[j][r]) U[j][c], j < r <= c
-        for (int r = j + 1 + ty; r < nb; r += 16) {
-            const T ur = conj_of(S[j][r]);
-            for (int c = r + tx; c < nb; c += 16) S[r][c] = msub(S[r][c], ur, S[j][c]);
-        }
-        __syncthreads();
-    }
-    for (int i = ty; i < nb; i += 16)
-        for (int j = tx; j < nb; j += 16)
-            A[(long long)(k0 + i) * ld + k0 + j] = (j > i) ? S[i][j] : ((j == i) ? from_real(pdiag[i], T()) : zero_of(T()));
-    // W = U_kk^{-1} (upper): rows from the bottom, W[i][c] = (delta_ic - sum_{i<q<=c} U[i][q] W[q][c]) / u_ii,
-    // column c on the 4 consecutive lanes 4c .. 4c + 3 (a quarter of the q range each)
-    {
-        const int c = tid >> 2, l = tid & 3;
-        for (int i = CHOL_NB - 1; i >= 0; --i) {
-            T acc = zero_of(T());
-            if (i < nb && c < nb && c > i)
-                for (int q = i + 1 + l; q <= c; q += 4) acc = msub(acc, S[i][q], W[q][c]);
-            acc = add(acc, shfl_xor4(acc, 1));
-            acc = add(acc, shfl_xor4(acc, 2));
-            if (l == 0) {
-                T v = zero_of(T());
-                if (i < nb && c < nb && c >= i) v = scal(add(acc, (c == i) ? one_of(T()) : zero_of(T())), rdiag[i]);
-                else if (i >= nb && c == i) v = one_of(T());
-                W[i][c] = v;
+    // ---- factorisation
+    for (int jb = 0; jb * 4 < nb; ++jb) {
+        bstatic_for_h<4>([&](auto JQc) {
+            constexpr int jq = decltype(JQc)::value;
+            const int j = jb * 4 + jq;
+            if (j >= nb) return;
+            const int par = j & 1;
+            if (ti == jb) {
+                const double d = re_part(shfl_mask(a[jq][jq], half + jb, hmask));  // a[jq][jq] of thread (jb, jb)
+                const double p = sqrt(d);  // NaN for a failed pivot: flagged through info
+                const double ip = 1.0 / p;
+                if (tj == jb) {
+                    rdiag[j] = ip;
+                    if (!(d > 0.0)) atomicMin(info, k0 + j + 1);
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int col = c0 + c;
+                    const T u = (col > j) ? scal(a[jq][c], ip) : ((col == j) ? from_real(p, T()) : zero_of(T()));
+                    a[jq][c] = u;
+                    rowb[par][col] = u;
+                }
             }
             __syncthreads();
-        }
+            T ur[4], uc[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) ur[q] = conj_of(rowb[par][r0 + q]);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) uc[c] = rowb[par][c0 + c];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (r0 + q > j && c0 + c >= r0 + q) a[q][c] = msub(a[q][c], ur[q], uc[c]);
+        });
     }
-    for (int i = ty; i < CHOL_NB; i += 16)
-        for (int j = tx; j < CHOL_NB; j += 16)
-            wh[i * CHOL_NB + j] = (i < nb && j < nb) ? conj_of(W[j][i]) : zero_of(T());
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int i = r0 + q, j = c0 + c;
+            if (j < i) a[q][c] = zero_of(T());   // U: zeros below the diagonal
+            if (i < nb && j < nb) A[(long long)(k0 + i) * ld + k0 + j] = a[q][c];
+        }
+    __syncthreads();  // rdiag complete
+    // ---- U_kk^{-1} in place: exchange step with pivot (j, j), j = 0 .. nb-1
+    for (int jb = 0; jb * 4 < nb; ++jb) {
+        bstatic_for_h<4>([&](auto JQc) {
+            constexpr int jq = decltype(JQc)::value;
+            const int j = jb * 4 + jq;
+            if (j >= nb) return;
+            const int par = j & 1;
+            const double ip = rdiag[j];
+            if (tj == jb) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) colb[par][r0 + q] = a[q][jq];
+            }
+            if (ti == jb) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) rowb[par][c0 + c] = (c0 + c == j) ? from_real(ip, T()) : scal(a[jq][c], ip);
+            }
+            __syncthreads();
+            T ck[4], rp[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) ck[q] = colb[par][r0 + q];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) rp[c] = rowb[par][c0 + c];
+            if (tj == jb) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) a[q][jq] = zero_of(T());
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) a[q][c] = msub(a[q][c], ck[q], rp[c]);
+            if (ti == jb) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) a[jq][c] = rp[c];
+            }
+        });
+    }
+    // W^H: wh[i][j] = conj(W[j][i])  (W = U_kk^{-1}: upper; padding zero)
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int i = r0 + q, j = c0 + c;
+            wh[j * CHOL_NB + i] = (i < nb && j < nb && j >= i) ? conj_of(a[q][c]) : zero_of(T());
+        }
 }
 
 // dst (cols x rows, ldd) = src (rows x cols, lds)^T (conjugated if conj)
@@ -159,16 +219,8 @@ static cudaError_t potrf_upper(int n, T *A, long long ld, T *work, int *info, cu
     T *tb = work + CHOL_NB * CHOL_NB;  // (n - k0 - nb) x CHOL_NB transposed panel
     for (int k0 = 0; k0 < n; k0 += CHOL_NB) {
         const int nb = std::min(CHOL_NB, n - k0), m = n - k0 - nb;
-        const size_t smem = 2 * (size_t)CHOL_NB * (CHOL_NB + 1) * sizeof(T);
-        static bool attr = false;
-        if (!attr) {
-            if ((e = cudaFuncSetAttribute(chol_diag_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
-                cudaSuccess)
-                return e;
-            attr = true;
-        }
         count_launch();
-        chol_diag_kernel<T><<<1, 256, smem, s>>>(A, ld, n, k0, wh, info);
+        chol_diag_kernel<T><<<1, 256, 0, s>>>(A, ld, n, k0, wh, info);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if (m <= 0) break;
         T *Ak = A + (long long)k0 * ld + k0 + nb;  // block row k, right part (nb x m)
