@@ -456,3 +456,49 @@ def test_dpoinv_vs_oracle(n):
     with pytest.raises(fb.FrobError) as e:
         fb.dpoinv(_t(a))
     assert e.value.name == "singular"
+
+
+# ------------------------------------------------------------------ the paper's own generators
+@pytest.mark.parametrize("n", [64, 512, 1024])
+def test_paper_speed_generator_uniform(n):
+    """E1's inputs: A, B with iid U(0,1) entries (no diagonal shift: kappa grows with n),
+    AUTO Frobenius, NEXT-1 and complex LU against the oracle's Gauss-Jordan inverse; the bound is
+    kappa-scaled (R10)."""
+    rng = np.random.default_rng(1055 + n)
+    z = rng.uniform(0.0, 1.0, (n, n)) + 1j * rng.uniform(0.0, 1.0, (n, n))
+    ref, info = oracle.zinv_gj(z)
+    assert info == 0
+    kf = max(1.0, np.linalg.cond(z) / 1e4)
+    zt = _t(z)
+    for name, x in (("auto", fb.inv(zt)), ("fused", fb.inv(zt, fused=True)), ("zinv", fb.zinv(zt))):
+        rel = oracle.rel_fro(_np(x), ref)
+        assert rel <= 1e-10 * kf, (name, rel, kf)
+        assert _resid(z, _np(x)) <= 1e-11 * n * kf
+
+
+@pytest.mark.parametrize("n", [64, 256, 1024])
+def test_paper_accuracy_generator_hadamard(n):
+    """E2's inputs: A, B = H D H^T / ||.||_F with kappa = 10 (synth.hadamard_kappa),
+    the paper's left / right residuals of GPU Frobenius vs GPU complex LU: both at
+    rounding level, as the paper reports ("difference is so small")."""
+    z = synth.hadamard_kappa(n, 10.0, seed=1) + 1j * synth.hadamard_kappa(n, 10.0, seed=2)
+    ref, _ = oracle.zinv_gj(z)
+    zt = _t(z)
+    xf, xz = _np(fb.inv(zt)), _np(fb.zinv(zt))
+    assert oracle.rel_fro(xf, ref) <= 1e-12 and oracle.rel_fro(xz, ref) <= 1e-12
+    lf, rf = oracle.res_lr(z, xf)
+    lz, rz = oracle.res_lr(z, xz)
+    assert max(lf, rf, lz, rz) <= 1e-13 * n
+
+
+@pytest.mark.parametrize("n", [300, 1030])
+def test_alg5_both_singular_structured_large(n):
+    """Alg 5 on a unitary Z = DFT/sqrt(n) at larger n (real and imaginary parts singular): Z^{-1} = Z^H;
+    AUTO Alg 1 reports both parts singular."""
+    z = synth.dft_unitary(n)
+    zt = _t(z)
+    with pytest.raises(fb.FrobError) as e:
+        fb.inv(zt)
+    assert e.value.name == "both_singular"
+    x = _np(fb.inv_rand(zt, seed=7))
+    assert oracle.rel_fro(x, z.conj().T) <= 1e-11
