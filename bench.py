@@ -205,11 +205,11 @@ class SingleMatrix(Workload):
 
     def e2e_pipelined(self, k):
         """k steps through frob_inv_host_many (pinned host buffers, the copies of matrices i +- 1
-        overlapping inversion i; k DISTINCT matrices, seeds 1000 + i); None when k matrices would
-        not fit a 2 GiB pinned budget."""
+        overlapping inversion i; k DISTINCT matrices, seeds 1000 + i); None when fewer than two
+        matrices (inputs and outputs) fit a 24 GiB pinned budget."""
         import synth
         per = 16 * self.n * self.n
-        k = min(k, (2 << 30) // per)
+        k = min(k, (24 << 30) // (2 * per))
         if k < 2:
             return None
         if getattr(self, "_zk", None) is None or self._zk.shape[0] != k:
