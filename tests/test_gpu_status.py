@@ -190,7 +190,8 @@ def test_auto_rule_kappa_switch_matches_oracle():
 def test_fused_kappa_estimate_vs_exact(n):
     """NEXT-1's AUTO rule uses the Hager-Higham estimate of ||A^-1||_inf (blocked substitution with the
     LU factors and their transposes); it is a lower bound of the exact kappa_inf the literal path
-    computes from X^{-1}, and for these inputs it is exact to rounding."""
+    computes from X^{-1}, within the estimator's usual factor (here 0.76 at n = 100, exact to
+    rounding at n = 1100 and 4200)."""
     z = synth.config2(n, seed=n + 5)
     zt = _t(z)
     _, il = fb.inv(zt, info=True)
@@ -198,4 +199,5 @@ def test_fused_kappa_estimate_vs_exact(n):
     assert il["branch_used"] == ifu["branch_used"] == 1
     kl, kf = il["kappa_a"], ifu["kappa_a"]
     assert kf <= kl * (1 + 1e-9) and kf >= kl / 3.0, (kl, kf)
-    assert abs(kf / kl - 1.0) < 1e-6, (kl, kf)
+    if n >= 1000:
+        assert abs(kf / kl - 1.0) < 1e-6, (kl, kf)
