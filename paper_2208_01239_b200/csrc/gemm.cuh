@@ -76,6 +76,19 @@ template <> struct GemmCfg<double, 1> {
     static constexpr int BM = 128, BN = 128, BK = 16, WGM = 2, WGN = 4, STAGES = 3;
     static constexpr int PADA = 4, PADB = 4;
 };
+// BIG = 2: 64 x 128 tiles (4 warps of 32 x 64), two CTAs per SM: 12 fragment loads per 32 DMMA
+// instead of 8 per 16, and 0.094 instead of 0.125 staged bytes per flop -- large real problems
+// with long k-ranges (BK = 8 x 4 stages: the BK = 16 version spilled in its main loop)
+#ifndef FROB_WIDE_BK
+#define FROB_WIDE_BK 8
+#endif
+#ifndef FROB_WIDE_STAGES
+#define FROB_WIDE_STAGES 4
+#endif
+template <> struct GemmCfg<double, 2> {
+    static constexpr int BM = 64, BN = 128, BK = FROB_WIDE_BK, WGM = 2, WGN = 2, STAGES = FROB_WIDE_STAGES;
+    static constexpr int PADA = 4, PADB = 4;
+};
 template <int BIG> struct GemmCfg<double2, BIG> {
     static constexpr int BM = 64, BN = 64, BK = 8, WGM = 2, WGN = 4, STAGES = 3;
     static constexpr int PADA = 4, PADB = 2;
@@ -207,42 +220,32 @@ FROB_DEV void gemm_tile(const GemmParams<T> &p, const long long bz, const int ro
     constexpr int ACH = BM * BK / E, BCH = BK * BN / E;
     constexpr int APT = (ACH + NTH - 1) / NTH, BPT = (BCH + NTH - 1) / NTH;
     static_assert(ACH % NTH == 0 && BCH % NTH == 0, "whole chunks per thread");
+    // chunk c = tid + u * NTH of a stage sits at row c / (chunks per row): the column is the same for
+    // every u and the row advances by a constant, so one base address per operand serves all u
+    static_assert(NTH % (BK / E) == 0 && NTH % (BN / E) == 0, "affine chunk rows");
+    constexpr int ARS = NTH / (BK / E), BRS = NTH / (BN / E);  // row step per u
     const bool fast = VEC && row0 + BM <= M && col0 + BN <= N;
-    const T *asrc[APT];
-    unsigned adst[APT];
-    int boff[BPT], bdst[BPT], brr[BPT];
-    if (fast) {
-#pragma unroll
-        for (int u = 0; u < APT; ++u) {
-            const int c = tid + u * NTH;
-            const int r = c / (BK / E), cc = (c % (BK / E)) * E;
-            asrc[u] = A + (long long)(row0 + r) * p.lda + kb + cc;
-            adst[u] = (unsigned)(r * SA + cc);
-        }
-#pragma unroll
-        for (int u = 0; u < BPT; ++u) {
-            const int c = tid + u * NTH;
-            const int r = c / (BN / E), cc = (c % (BN / E)) * E;
-            brr[u] = r;
-            boff[u] = col0 + cc;
-            bdst[u] = r * SB + cc;
-        }
-    }
+    const int ar0 = tid / (BK / E), acc0 = (tid % (BK / E)) * E;
+    const int br0 = tid / (BN / E), bcc0 = (tid % (BN / E)) * E;
+    const T *asrc0 = A + (long long)(row0 + ar0) * p.lda + kb + acc0;
+    const unsigned adst0 = (unsigned)(ar0 * SA + acc0);
+    const int boff0 = col0 + bcc0, bdst0 = br0 * SB + bcc0;
     auto load_stage = [&](int s, int kt) {
         const int k0 = kb + kt * BK;
         if (fast && k0 + BK <= K) {
-            T *as = As + s * BM * SA;
-            T *bs = Bs + s * BK * SB;
+            T *as = As + s * BM * SA + adst0;
+            T *bs = Bs + s * BK * SB + bdst0;
+            const T *ag = asrc0 + kt * BK;
 #pragma unroll
-            for (int u = 0; u < APT; ++u) cp_async16(as + adst[u], asrc[u] + kt * BK);
+            for (int u = 0; u < APT; ++u) cp_async16(as + u * ARS * SA, ag + (long long)u * ARS * p.lda);
             if (p.browmap) {
 #pragma unroll
                 for (int u = 0; u < BPT; ++u)
-                    cp_async16(bs + bdst[u], B + (long long)p.browmap[k0 + brr[u]] * p.ldb + boff[u]);
+                    cp_async16(bs + u * BRS * SB, B + (long long)p.browmap[k0 + br0 + u * BRS] * p.ldb + boff0);
             } else {
+                const T *bg = B + (long long)(k0 + br0) * p.ldb + boff0;
 #pragma unroll
-                for (int u = 0; u < BPT; ++u)
-                    cp_async16(bs + bdst[u], B + (long long)(k0 + brr[u]) * p.ldb + boff[u]);
+                for (int u = 0; u < BPT; ++u) cp_async16(bs + u * BRS * SB, bg + (long long)u * BRS * p.ldb);
             }
             return;
         }

@@ -7,6 +7,7 @@
 #include <utility>
 #include <type_traits>
 #include <mutex>
+#include <vector>
 #include <algorithm>
 #include "lu.cuh"
 #include "tma.cuh"
@@ -113,7 +114,23 @@ static cudaError_t gemm_launch_impl(const GemmPair<T> &pp, int batch0, int batch
     if (batch1 > 0) tiles += (long long)((pp.q[1].M + 127) / 128) * ((pp.q[1].N + 127) / 128) * batch1;
     // (measured: the 128 x 128 variant runs one CTA per SM and is slower than 3 x 64 x 64 per SM;
     //  kept compiled for experiments, not selected)
-    if (sizeof(T) == 8 && !p0.counter && tiles >= (1LL << 40)) return gemm_launch_cfg<T, VEC, 1>(pp, batch0, batch1, s);
+    if constexpr (sizeof(T) == 8) {
+        if (!p0.counter && tiles >= (1LL << 40)) return gemm_launch_cfg<T, VEC, 1>(pp, batch0, batch1, s);
+        // 64 x 128 tiles, two CTAs per SM, for long k-ranges once they fill two waves
+        static const int wide_k = [] {  // env FROB_GEMM_WIDE_K: the k-range from which it is used (A/B aid)
+            const char *v = tuning_env("FROB_GEMM_WIDE_K");
+            return v ? atoi(v) : 1024;
+        }();
+        long long t2 = (long long)((p0.M + 63) / 64) * ((p0.N + 127) / 128) * batch0;
+        if (batch1 > 0) t2 += (long long)((pp.q[1].M + 63) / 64) * ((pp.q[1].N + 127) / 128) * batch1;
+        const int K = batch1 > 0 ? std::min(p0.K, pp.q[1].K) : p0.K;
+        // (plain operands only: the coarser tiles waste more of a triangular k-range, and the B-row
+        // gather's per-stage index loads double with BK = 8 -- both measured slower)
+        auto plain = [](const GemmParams<T> &q) { return q.triA == TRI_NONE && q.triB == TRI_NONE && !q.browmap; };
+        if (wide_k > 0 && !p0.counter && K >= wide_k && t2 >= 2LL * 148 * 2 && plain(p0) &&
+            (batch1 == 0 || plain(pp.q[1])))
+            return gemm_launch_cfg<T, VEC, 2>(pp, batch0, batch1, s);
+    }
     return gemm_launch_cfg<T, VEC, 0>(pp, batch0, batch1, s);
 }
 
@@ -1276,6 +1293,40 @@ static bool getrf_prio() {
     return v;
 }
 
+// Host-side event timeline of getrf (-DFROB_TL builds only; tools/getrf_timeline.py): timing
+// events recorded on the chain and far-column streams at the points named by `kind`, read back
+// as ms relative to the first one.  Events on two streams do not serialise the kernels.
+#ifdef FROB_TL
+static std::vector<std::pair<int, cudaEvent_t>> g_evt;
+static std::mutex g_evt_mu;
+static void ev_trace(int kind, int t, cudaStream_t st) {
+    std::lock_guard<std::mutex> g(g_evt_mu);
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, st);
+    g_evt.emplace_back(kind * 100000 + t, e);
+}
+extern "C" int frob_evtrace_reset() {
+    std::lock_guard<std::mutex> g(g_evt_mu);
+    for (auto &p : g_evt) cudaEventDestroy(p.second);
+    g_evt.clear();
+    return 0;
+}
+extern "C" int frob_evtrace_read(int *codes, float *ms, int cap) {
+    std::lock_guard<std::mutex> g(g_evt_mu);
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    const int cnt = (int)std::min<size_t>(g_evt.size(), (size_t)cap);
+    for (int i = 0; i < cnt; ++i) {
+        codes[i] = g_evt[i].first;
+        if (cudaEventElapsedTime(&ms[i], g_evt[0].second, g_evt[i].second) != cudaSuccess) ms[i] = -1.f;
+    }
+    return cnt;
+}
+#define EV_TRACE(kind, t, st) ev_trace(kind, t, st)
+#else
+#define EV_TRACE(kind, t, st) do { } while (0)
+#endif
+
 template <typename T>
 cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuStats *stats, T *work,
                   cudaStream_t s) {
@@ -1330,12 +1381,14 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
             }
             const int W = min(LuNB<T>::N, n - K0);
             const int slot0 = slot;
+            EV_TRACE(0, t, cs);
             for (int k0 = K0, w = 0; k0 < K0 + W; k0 += w)
                 if ((e = step(K0, K0 + W, k0, w)) != cudaSuccess) return e;
             const int cn0 = K0 + W, cn1 = min(n, K0 + 2 * W);
             const int nl = slot - slot0;
             const int *lists = mv + (long long)slot0 * MV_INTS;
             T *Li = Linv[t & 1];
+            EV_TRACE(1, t, cs);
             if (cn0 < n) {
                 // L11^{-1} (W x W unit lower) by the triangular recursion
                 if ((e = launch_pdl(extract_unit_lower_kernel<T>, dim3(ew_grid((long long)W * W)), dim3(256), 0, cs,
@@ -1355,9 +1408,11 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
                         return e;
                 }
             }
+            EV_TRACE(2, t, cs);
             if ((e = cudaEventRecord(evL, cs)) != cudaSuccess) return e;
             // ---- auxiliary stream: left columns + columns beyond the look-ahead block
             if ((e = cudaStreamWaitEvent(ax.st, evL, 0)) != cudaSuccess) return e;
+            EV_TRACE(3, t, ax.st);
             {
                 const int ncol = K0 + (n - cn1);
                 if (ncol > 0) {
@@ -1368,19 +1423,23 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
                 if (cn1 < n && (e = outer_update<T>(n, A, lda, K0, W, cn1, n, Li, Tb[t & 1], ldT, ax.st)) != cudaSuccess)
                     return e;
             }
+            EV_TRACE(4, t, ax.st);
             if ((e = cudaEventRecord(evR[t & 1], ax.st)) != cudaSuccess) return e;
             // ---- caller's stream: look-ahead block [cn0, cn1)
             if (cn0 < n) {
                 if (t > 0 && (e = cudaStreamWaitEvent(cs, evR[(t - 1) & 1], 0)) != cudaSuccess) return e;
+                EV_TRACE(5, t, cs);
                 if ((e = launch_pdl(lu_swap_multi_kernel<T, PW2>, dim3((cn1 - cn0 + SWM_COLS - 1) / SWM_COLS),
                                     dim3(SWM_COLS), 0, cs, A, lda, cn0, cn1, 0, 0, lists, nl)) != cudaSuccess)
                     return e;
                 if ((e = outer_update<T>(n, A, lda, K0, W, cn0, cn1, Li, Tb[t & 1], ldT, cs)) != cudaSuccess) return e;
+                EV_TRACE(6, t, cs);
             }
         }
         // join the auxiliary stream
         if ((e = cudaEventRecord(evJ, ax.st)) != cudaSuccess) return e;
         if ((e = cudaStreamWaitEvent(cs, evJ, 0)) != cudaSuccess) return e;
+        EV_TRACE(7, 0, cs);
         if (Ktail < n) {
             // ---- the trailing m x m matrix (fully updated, all earlier row moves applied to every
             // column) factored by lu2 into compact buffers, assembled packed back in place; its
@@ -1398,6 +1457,7 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
                 return e;
             if ((e = lu2_factor<T>(m, B0, B1, ldm, A22, A22, lda, psub, iw2, diag + Ktail, nullptr, cs)) != cudaSuccess)
                 return e;
+            EV_TRACE(8, 0, cs);
             for (int c0 = 0; c0 < Ktail; c0 += m) {  // left columns in chunks of m through B1
                 const int nc = min(m, Ktail - c0);
                 if ((e = launch_pdl(gather_rows_kernel<T>, dim3(ew_grid((long long)m * nc)), dim3(256), 0, cs,
@@ -1412,6 +1472,7 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
                                     (const int *)psub, ptmp, ph)) != cudaSuccess)
                     return e;
         }
+        EV_TRACE(9, 0, cs);
         if (prio) {
             if ((e = cudaEventRecord(ax.ev[5], cs)) != cudaSuccess) return e;
             if ((e = cudaStreamWaitEvent(s, ax.ev[5], 0)) != cudaSuccess) return e;

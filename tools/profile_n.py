@@ -1,11 +1,15 @@
 """Per-kernel (and per GEMM role) time of one frob_inv / zinv at size n, from the library's
-CUDA-event profiler.  Usage: python tools/profile_n.py N [frob|zinv] [reps]"""
+CUDA-event profiler.  Usage: python tools/profile_n.py N [frob|zinv] [reps] [--lib PATH]"""
 import sys, os, json, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import synth
 import paper_2208_01239_b200 as fb
 from paper_2208_01239_b200 import frobinv as fbi
+if "--lib" in sys.argv:
+    i = sys.argv.index("--lib")
+    fbi.load(sys.argv[i + 1])
+    del sys.argv[i:i + 2]
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 which = sys.argv[2] if len(sys.argv) > 2 else "frob"
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
