@@ -543,17 +543,23 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
                                                                               nullptr);
             FROB_CUDA(cudaGetLastError());
         }
+        // EarlyInv scratch: a buffer idle from the LU's start to the end of the inverse (W5 before
+        // part 2 copies B there; W2 holds only part 1's spent factors then)
+        EarlyInv ei;
+        ei.h = small ? early_inv_h(n) : 0;
+        ei.vbuf = (u == 1) ? w.W5 : w.W2;
         {
             ProfScope ps("step:lu", s);
             if (small) FROB_CUDA(lu2_factor<double>(n, in, u == 1 ? w.W4 : w.W1, ld, u == 1 ? w.W2 : w.W6,
-                                                    u == 1 ? w.W3 : w.W7, ld, pm, w.iw, w.diag, &w.stats[u - 1], s));
+                                                    u == 1 ? w.W3 : w.W7, ld, pm, w.iw, w.diag, &w.stats[u - 1], s,
+                                                    &ei));
             else FROB_CUDA(getrf<double>(n, in, ld, pm, w.mv, w.diag, &w.stats[u - 1], w.work, s));
         }
         factored |= u;
         ProfScope ps("step:inv_from_lu", s);
         if (small) {
-            if (u == 1) FROB_CUDA(inv_from_ul<double>(n, w.W2, w.W3, ld, w.W1, w.W4, ld, nullptr, w.flags + 2, s));
-            else FROB_CUDA(inv_from_ul<double>(n, w.W6, w.W7, ld, w.W5, w.W1, ld, nullptr, w.flags + 2, s));
+            if (u == 1) FROB_CUDA(inv_from_ul<double>(n, w.W2, w.W3, ld, w.W1, w.W4, ld, nullptr, w.flags + 2, s, &ei));
+            else FROB_CUDA(inv_from_ul<double>(n, w.W6, w.W7, ld, w.W5, w.W1, ld, nullptr, w.flags + 2, s, &ei));
         } else {
             FROB_CUDA(inv_from_lu<double>(n, in, ld, w.W2, w.W3, u == 1 ? w.W4 : w.W1, ld, nullptr, w.flags + 2, s));
         }
@@ -714,12 +720,16 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
     double *Re = (use == 1) ? w.A : w.B;  // X buffer is free now
     double *Sa = fused ? w.W2 : w.W1;
     if (small) {
+        EarlyInv ei;  // scratch: Re (X's buffer, idle until the product writes it)
+        ei.h = early_inv_h(n);
+        ei.vbuf = Re;
         {
             ProfScope ps("step:lu", s);
-            FROB_CUDA(lu2_factor<double>(n, w.W3, Sa, ld, w.W4, w.W5, ld, w.perm_m, w.iw, w.diag, &w.stats[2], s));
+            FROB_CUDA(lu2_factor<double>(n, w.W3, Sa, ld, w.W4, w.W5, ld, w.perm_m, w.iw, w.diag, &w.stats[2], s,
+                                         &ei));
         }
         ProfScope ps("step:inv_from_lu", s);
-        FROB_CUDA(inv_from_ul<double>(n, w.W4, w.W5, ld, w.W3, Re, ld, nullptr, w.flags + 2, s));
+        FROB_CUDA(inv_from_ul<double>(n, w.W4, w.W5, ld, w.W3, Re, ld, nullptr, w.flags + 2, s, &ei));
     } else {
         {
             ProfScope ps("step:lu", s);

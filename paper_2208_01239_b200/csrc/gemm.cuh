@@ -445,7 +445,11 @@ gemm_kernel(GemmPair<T> pp) {
         const int first = (lin / (GROUP_M * tn)) * GROUP_M;
         const int gm = min(tm - first, GROUP_M);
         const int rem = lin - first * tn;
-        const int ty = first + rem % gm, tx = rem / gm;
+        int ty = first + rem % gm, tx = rem / gm;
+        // longest triangular k-ranges first (the tail wave then holds short tiles): n = 4096 / 8192
+        // Frobenius 32.84 -> 32.67 / 190.2 -> 189.5 ms
+        if (p.triB == TRI_UPPER) tx = tn - 1 - tx;
+        if (p.triA == TRI_LOWER) ty = tm - 1 - ty;
         if (p.triC == TRI_UPPER && ty * Cf::BM >= (tx + 1) * Cf::BN) return;
         gemm_tile<T, VEC, BIG, SPLIT>(p, bz, ty * Cf::BM, tx * Cf::BN, As, Bs);
         return;

@@ -8,6 +8,7 @@
 #include <type_traits>
 #include <mutex>
 #include <vector>
+#include <string>
 #include <algorithm>
 #include "lu.cuh"
 #include "tma.cuh"
@@ -985,6 +986,14 @@ static cudaError_t tri_level(T *U, T *L, T *tmp, long long ld, int s, int o, int
                              cudaStream_t st, bool do_upper = true, bool do_lower = true) {
     const long long stride = 2LL * s * (ld + 1);
     cudaError_t e;
+#ifdef FROB_TUNING  // per-level profiler tags (tools/profile_n.py), tuning builds only
+    static const char *lvl[] = {"gemm:tri_inv_s32", "gemm:tri_inv_s64", "gemm:tri_inv_s128", "gemm:tri_inv_s256",
+                                "gemm:tri_inv_s512", "gemm:tri_inv_s1024", "gemm:tri_inv_s2048", "gemm:tri_inv_s4096",
+                                "gemm:tri_inv_s8192"};
+    int li = 0;
+    while ((32 << li) < s && li < 8) ++li;
+    GemmTag ltag(g_gemm_tag && std::string(g_gemm_tag) == "gemm:tri_inv" ? lvl[li] : g_gemm_tag);
+#endif
     // step 1 -- upper: W = U12 * inv(U22);  lower: W = L21 * inv(L11)   (one launch)
     auto pu = gemm_params<T>(s, s2, s2, 1.0, U + (long long)o * ld + o + s, ld,
                              U + (long long)(o + s) * ld + o + s, ld, 0.0, nullptr, ld,
@@ -1050,11 +1059,58 @@ cudaError_t tri_inverses(int n, T *U, T *L, long long ld, T *tmp, cudaStream_t s
 template cudaError_t tri_inverses<double>(int, double *, double *, long long, double *, cudaStream_t);
 template cudaError_t tri_inverses<double2>(int, double2 *, double2 *, long long, double2 *, cudaStream_t);
 
+// out[i][c] = Wp[pos_h[perm[h + i]] - h][c]: EarlyInv's W' rows in the final order (i < n - h, c < h)
+template <typename T>
+__global__ void gather_w_kernel(const T *__restrict__ Wp, long long ld, const int *__restrict__ perm,
+                                const int *__restrict__ pos_h, int n, int h, T *__restrict__ out, long long ldo) {
+    const long long total = (long long)(n - h) * h;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / h), c = (int)(idx % h);
+        out[(long long)i * ldo + c] = Wp[(long long)(pos_h[perm[h + i]] - h) * ld + c];
+    }
+}
+
 template <typename T>
 cudaError_t inv_from_ul(int n, T *U, T *L, long long ld, T *tmp, T *out, long long ldo, const int *colperm,
-                        int *counter, cudaStream_t s) {
+                        int *counter, cudaStream_t s, EarlyInv *early) {
     cudaError_t e;
-    if ((e = tri_inverses<T>(n, U, L, ld, tmp, s)) != cudaSuccess) return e;
+    if (early && early->h > 0 && early->done) {
+        // U11^{-1}, L11^{-1} and V = U11^{-1} U12 came from lu2_factor's auxiliary stream (EarlyInv)
+        const int h = early->h, r = n - h;
+        EV_TRACE(20, 0, s);
+        e = cudaStreamWaitEvent(s, early->done, 0);
+        cudaEventDestroy(early->done);  // released once the recorded work completes
+        early->done = nullptr;
+        if (e != cudaSuccess) return e;
+        T *U22 = U + (long long)h * ld + h, *L22 = L + (long long)h * ld + h;
+        EV_TRACE(21, 0, s);
+        if ((e = tri_inverses<T>(r, U22, L22, ld, tmp + (long long)h * ld + h, s)) != cudaSuccess) return e;
+        EV_TRACE(22, 0, s);
+        GemmTag tag("gemm:tri_inv");
+        const T *V = reinterpret_cast<const T *>(early->vbuf) + h;
+        // W = L21 L11^{-1} in the final row order: W'[pos_h(perm[i]) - h] (into tmp rows [h, n), columns [0, h))
+        {
+            const long long total = (long long)r * h;
+            count_launch();
+            gather_w_kernel<T><<<(int)std::min<long long>((total + 255) / 256, 148LL * 8), 256, 0, s>>>(
+                reinterpret_cast<const T *>(early->vbuf) + (long long)h * ld + h, ld, early->perm, early->pos_h, n, h,
+                tmp + (long long)h * ld, ld);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
+        // U12 <- -V U22^{-1}  and  L21 <- -L22^{-1} W: one launch
+        auto pu = gemm_params<T>(h, r, r, -1.0, V, ld, U22, ld, 0.0, nullptr, ld, U + h, ld);
+        pu.triB = TRI_UPPER;
+        auto ql = gemm_params<T>(r, h, r, -1.0, L22, ld, tmp + (long long)h * ld, ld, 0.0, nullptr, ld,
+                                 L + (long long)h * ld, ld);
+        ql.triA = TRI_LOWER;
+        if ((e = gemm_launch2<T>(ql, 1, pu, 1, s)) != cudaSuccess) return e;
+        EV_TRACE(23, 0, s);
+    } else {
+        EV_TRACE(20, 1, s);
+        if ((e = tri_inverses<T>(n, U, L, ld, tmp, s)) != cudaSuccess) return e;
+        EV_TRACE(23, 1, s);
+    }
     // X = U^{-1} L^{-1}: (upper) x (lower) -> k from max(row0, col0)
     auto p = gemm_params<T>(n, n, n, 1.0, U, ld, L, ld, 0.0, nullptr, ld, out, ldo);
     p.triA = TRI_UPPER;
@@ -1073,10 +1129,12 @@ cudaError_t inv_from_ul(int n, T *U, T *L, long long ld, T *tmp, T *out, long lo
     p.counter = (n <= 2048 && mode == 0) ? counter : nullptr;
     if (mode == 1) p.force_split = 1;
     GemmTag tag("gemm:product");
-    return gemm_launch<T>(p, 1, s);
+    e = gemm_launch<T>(p, 1, s);
+    EV_TRACE(24, 0, s);
+    return e;
 }
-template cudaError_t inv_from_ul<double>(int, double *, double *, long long, double *, double *, long long, const int *, int *, cudaStream_t);
-template cudaError_t inv_from_ul<double2>(int, double2 *, double2 *, long long, double2 *, double2 *, long long, const int *, int *, cudaStream_t);
+template cudaError_t inv_from_ul<double>(int, double *, double *, long long, double *, double *, long long, const int *, int *, cudaStream_t, EarlyInv *);
+template cudaError_t inv_from_ul<double2>(int, double2 *, double2 *, long long, double2 *, double2 *, long long, const int *, int *, cudaStream_t, EarlyInv *);
 
 template <typename T>
 cudaError_t lu_stats_launch(const T *diag, int n, LuStats *st, cudaStream_t s) {
@@ -1252,54 +1310,13 @@ static bool getrf_new_panels() {
     return v;
 }
 
-// outer update of columns [c0, c1) by block (K0, W): U12 = Linv * A12 -> Tb, A22 -= L21 * Tb, A12 <- Tb
-template <typename T>
-static cudaError_t outer_update(int n, T *A, long long lda, int K0, int W, int c0, int c1, const T *Linv, T *Tb,
-                                long long ldT, cudaStream_t s) {
-    cudaError_t e;
-    const int nc = c1 - c0;
-    if (nc <= 0) return cudaSuccess;
-    GemmTag tag("gemm:lu_outer");
-    auto p = gemm_params<T>(W, nc, W, 1.0, Linv, LuNB<T>::N, A + (long long)K0 * lda + c0, lda, 0.0, nullptr, ldT,
-                            Tb + c0, ldT);
-    p.triA = TRI_LOWER;
-    if ((e = gemm_launch<T>(p, 1, s)) != cudaSuccess) return e;
-    const int mr = n - K0 - W;
-    if (mr > 0) {
-        T *c = A + (long long)(K0 + W) * lda + c0;
-        auto q = gemm_params<T>(mr, nc, W, -1.0, A + (long long)(K0 + W) * lda + K0, lda, Tb + c0, ldT, 1.0, c, lda,
-                                c, lda);
-        if ((e = gemm_launch<T>(q, 1, s)) != cudaSuccess) return e;
-    }
-    return launch_pdl(copy_block_kernel<T>, dim3(ew_grid((long long)W * nc)), dim3(256), 0, s, Tb + c0, ldT,
-                      A + (long long)K0 * lda + c0, lda, W, nc);
-}
-
-// lu2 for the last trailing matrix unless env FROB_GETRF_TAIL=0 (A/B measurement aid)
-static bool getrf_tail() {
-    static bool v = [] {
-        const char *e = tuning_env("FROB_GETRF_TAIL");
-        return !(e && e[0] == '0');
-    }();
-    return v;
-}
-
-// chain / far-column stream priorities unless env FROB_LU_PRIO=0 (A/B measurement aid)
-static bool getrf_prio() {
-    static bool v = [] {
-        const char *e = tuning_env("FROB_LU_PRIO");
-        return !(e && e[0] == '0');
-    }();
-    return v;
-}
-
 // Host-side event timeline of getrf (-DFROB_TL builds only; tools/getrf_timeline.py): timing
 // events recorded on the chain and far-column streams at the points named by `kind`, read back
 // as ms relative to the first one.  Events on two streams do not serialise the kernels.
 #ifdef FROB_TL
 static std::vector<std::pair<int, cudaEvent_t>> g_evt;
 static std::mutex g_evt_mu;
-static void ev_trace(int kind, int t, cudaStream_t st) {
+void ev_trace(int kind, int t, cudaStream_t st) {
     std::lock_guard<std::mutex> g(g_evt_mu);
     cudaEvent_t e;
     if (cudaEventCreate(&e) != cudaSuccess) return;
@@ -1322,10 +1339,51 @@ extern "C" int frob_evtrace_read(int *codes, float *ms, int cap) {
     }
     return cnt;
 }
-#define EV_TRACE(kind, t, st) ev_trace(kind, t, st)
-#else
-#define EV_TRACE(kind, t, st) do { } while (0)
 #endif
+
+// outer update of columns [c0, c1) by block (K0, W): U12 = Linv * A12 -> Tb, A22 -= L21 * Tb, A12 <- Tb
+template <typename T>
+static cudaError_t outer_update(int n, T *A, long long lda, int K0, int W, int c0, int c1, const T *Linv, T *Tb,
+                                long long ldT, cudaStream_t s) {
+    cudaError_t e;
+    const int nc = c1 - c0;
+    if (nc <= 0) return cudaSuccess;
+    GemmTag tag("gemm:lu_outer");
+    auto p = gemm_params<T>(W, nc, W, 1.0, Linv, LuNB<T>::N, A + (long long)K0 * lda + c0, lda, 0.0, nullptr, ldT,
+                            Tb + c0, ldT);
+    p.triA = TRI_LOWER;
+    if ((e = gemm_launch<T>(p, 1, s)) != cudaSuccess) return e;
+    EV_TRACE(10, K0 / LuNB<T>::N + (c1 == n ? 0 : 50000), s);
+    const int mr = n - K0 - W;
+    if (mr > 0) {
+        T *c = A + (long long)(K0 + W) * lda + c0;
+        auto q = gemm_params<T>(mr, nc, W, -1.0, A + (long long)(K0 + W) * lda + K0, lda, Tb + c0, ldT, 1.0, c, lda,
+                                c, lda);
+        if ((e = gemm_launch<T>(q, 1, s)) != cudaSuccess) return e;
+    }
+    EV_TRACE(11, K0 / LuNB<T>::N + (c1 == n ? 0 : 50000), s);
+    return launch_pdl(copy_block_kernel<T>, dim3(ew_grid((long long)W * nc)), dim3(256), 0, s, Tb + c0, ldT,
+                      A + (long long)K0 * lda + c0, lda, W, nc);
+}
+
+// lu2 for the last trailing matrix unless env FROB_GETRF_TAIL=0 (A/B measurement aid)
+static bool getrf_tail() {
+    static bool v = [] {
+        const char *e = tuning_env("FROB_GETRF_TAIL");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
+// chain / far-column stream priorities unless env FROB_LU_PRIO=0 (A/B measurement aid)
+static bool getrf_prio() {
+    static bool v = [] {
+        const char *e = tuning_env("FROB_LU_PRIO");
+        return !(e && e[0] == '0');
+    }();
+    return v;
+}
+
 
 template <typename T>
 cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuStats *stats, T *work,

@@ -78,9 +78,30 @@ int lu2_panel_max_m();
 template <typename T>
 cudaError_t lu2_panel_inplace(const CUtensorMap &tm, T *A, long long lda, int n, int k0, int w, int *mv, T *diag,
                               cudaStream_t s);
+// Early triangular inverses (real lu2): the first h rows of U and the block L11 are final once lu2's
+// step h / PW has been applied, while the rest of the LU -- its chain-bound tail, which leaves most
+// SMs idle -- is still running.  lu2_factor then assembles them on a low-priority auxiliary stream,
+// inverts U11 and L11 in place (tri_inverses) and forms V = U11^{-1} U12 into rows [0, h), columns
+// [h, n) of vbuf (its top-left h x h block is that recursion's scratch); inv_from_ul waits for that
+// work and finishes with the order-(n - h) blocks and the top-level products
+//   U^{-1} = [U11^{-1}, -V U22^{-1}; 0, U22^{-1}],  L^{-1} = [L11^{-1}, 0; -L22^{-1} W, L22^{-1}],  W = L21 L11^{-1}.
+// vbuf: n x ldo doubles, untouched by anything else from lu2_factor's start until inv_from_ul returns.
+// L21 is not final at that point (later pivots move its rows), but its rows are only permuted:
+// W' = L21' L11^{-1} is formed early on the rows in their order after step h / PW - 1 (vbuf rows
+// [h, n): L21' in columns [0, h), W' in columns [h, 2h)) and gathered into the final order at the end
+// (W[i] = W'[pos_h(perm[h + i]) - h], pos_h = that step's row-position snapshot).
+struct EarlyInv {
+    int h = 0;                    // 0: not used
+    double *vbuf = nullptr;
+    cudaEvent_t done = nullptr;   // recorded on the auxiliary stream after V and W'
+    const int *pos_h = nullptr;   // set by lu2_factor: original row -> position after step h / PW - 1
+    const int *perm = nullptr;    // set by lu2_factor: the final permutation (valid after the LU)
+};
+// h for an order-n lu2 factorisation (0 below the size where it pays; env FROB_EARLY=0: off, A/B aid)
+int early_inv_h(int n);
 template <typename T>
 cudaError_t lu2_factor(int n, T *B0, T *B1, long long ld, T *U, T *L, long long ldo, int *perm, int *iw, T *diag,
-                       LuStats *stats, cudaStream_t s);
+                       LuStats *stats, cudaStream_t s, EarlyInv *early = nullptr);
 template <typename T>
 cudaError_t lu_stats_launch(const T *diag, int n, LuStats *st, cudaStream_t s);
 // U = triu(lu) (zeros below), L = tril(lu, -1) + I (zeros above)
@@ -92,7 +113,15 @@ cudaError_t tri_inverses(int n, T *U, T *L, long long ld, T *tmp, cudaStream_t s
 // Xinv = U^{-1} L^{-1} from split factors (U, L destroyed; scratch n x ld)
 template <typename T>
 cudaError_t inv_from_ul(int n, T *U, T *L, long long ld, T *scratch, T *out, long long ldo, const int *colperm,
-                        int *counter, cudaStream_t s);
+                        int *counter, cudaStream_t s, EarlyInv *early = nullptr);
+
+// host-side event timeline (-DFROB_TL builds: tools/getrf_timeline.py, tools/early_timeline.py)
+#ifdef FROB_TL
+void ev_trace(int kind, int t, cudaStream_t st);
+#define EV_TRACE(kind, t, st) ev_trace(kind, t, st)
+#else
+#define EV_TRACE(kind, t, st) do { } while (0)
+#endif
 
 template <typename T>
 cudaError_t gemm_launch(const GemmParams<T> &p, int batch, cudaStream_t s);

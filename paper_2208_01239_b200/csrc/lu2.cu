@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <utility>
 #include <algorithm>
+#include <mutex>
 #include "lu.cuh"
 #include "tma.cuh"
 
@@ -1406,16 +1407,17 @@ lu_update2m_kernel(const T *__restrict__ Bk, T *__restrict__ Bn, long long ld, i
 
 // Final U / L in final row order (see the file header).  snap[b * n + orig] = position of
 // original row `orig` after step b.
+// Rows [r0, r1) only (EarlyInv assembles the first h rows ahead of the rest).
 template <typename T>
 __global__ void lu_assemble2_kernel(const T *__restrict__ B0, const T *__restrict__ B1, long long ld, int n, int W,
                                     const int *__restrict__ perm, const int *__restrict__ snap, T *__restrict__ U,
-                                    T *__restrict__ L, long long ldo) {
+                                    T *__restrict__ L, long long ldo, int r0, int r1) {
     pdl_trigger();
     pdl_wait();
-    const long long total = (long long)n * n;
+    const long long total = (long long)(r1 - r0) * n;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
-        const int i = (int)(idx / n), c = (int)(idx - (long long)i * n);
+        const int i = r0 + (int)(idx / n), c = (int)(idx % n);
         const int k = i / W, b = c / W;
         const T *Bk = (k & 1) ? B1 : B0;
         T uval = zero_of(T()), lval = zero_of(T());
@@ -1588,6 +1590,121 @@ template cudaError_t lu2_panel_inplace<double>(const CUtensorMap &, double *, lo
 template cudaError_t lu2_panel_inplace<double2>(const CUtensorMap &, double2 *, long long, int, int, int, int *,
                                                 double2 *, cudaStream_t);
 
+// ---------------------------------------------------------------------------------------
+// EarlyInv (see lu.cuh): a lowest-priority auxiliary stream per device
+int early_inv_h(int n) {
+    static int mode = [] {
+        const char *e = tuning_env("FROB_EARLY");
+        return e ? atoi(e) : -1;
+    }();
+    const int min_n = mode > 1 ? mode : 1024;
+    if (mode == 0 || n < min_n || n > LU2_MAX_N) return 0;
+    constexpr int PW = Panel2W<double>::PW;
+    return (n / 2) / PW * PW;
+}
+
+// per-device streams: hi = 0 the lowest priority (EarlyInv work), 1 the highest (the LU's chain
+// while EarlyInv work runs beside it: its panels take the SMs the auxiliary GEMMs free first)
+static cudaError_t early_stream(int hi, cudaStream_t *out) {
+    static std::mutex mu;
+    static cudaStream_t st[2][64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> g(mu);
+    if (!st[hi][dev]) {
+        int least = 0, greatest = 0;
+        if ((e = cudaDeviceGetStreamPriorityRange(&least, &greatest)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithPriority(&st[hi][dev], cudaStreamNonBlocking, hi ? greatest : least)) !=
+            cudaSuccess)
+            return e;
+    }
+    *out = st[hi][dev];
+    return cudaSuccess;
+}
+static cudaError_t early_aux_stream(cudaStream_t *out) { return early_stream(0, out); }
+// dst waits for everything enqueued on src so far
+static cudaError_t stream_join(cudaStream_t dst, cudaStream_t src) {
+    cudaEvent_t ev;
+    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+    e = cudaEventRecord(ev, src);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(dst, ev, 0);
+    cudaEventDestroy(ev);
+    return e;
+}
+
+// inv[pos[o]] = o: position -> original row after the snapshot's step
+__global__ void invert_perm_kernel(const int *__restrict__ pos, int n, int *__restrict__ inv) {
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o < n) inv[pos[o]] = o;
+}
+// L21' rows [h, n), columns [0, h) in their order after step h / PW - 1 (at[j] = original row at
+// position j then): column block b's multipliers sit in B_b at the original row's position after step b
+__global__ void gather_l21_kernel(const double *__restrict__ B0, const double *__restrict__ B1, long long ld, int n,
+                                  int h, int W, const int *__restrict__ at, const int *__restrict__ snap,
+                                  double *__restrict__ out, long long ldo) {
+    const long long total = (long long)(n - h) * h;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int j = h + (int)(idx / h), c = (int)(idx % h), b = c / W;
+        const int p = snap[(long long)b * n + at[j]];
+        out[(long long)j * ldo + c] = ((b & 1) ? B1 : B0)[(long long)p * ld + c];
+    }
+}
+
+// the EarlyInv work of lu2_factor: fork from s after step h / PW - 1 is complete
+static cudaError_t early_inv_launch(int n, const double *B0, const double *B1, long long ld, double *U, double *L,
+                                    long long ldo, const int *perm, const int *snap, int *at, EarlyInv &ei,
+                                    cudaStream_t s) {
+    constexpr int PW = Panel2W<double>::PW;
+    const int h = ei.h;
+    cudaStream_t aux;
+    cudaError_t e = early_aux_stream(&aux);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&ei.done, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = stream_join(aux, s)) != cudaSuccess) return e;
+    EV_TRACE(30, 0, aux);
+    {
+        const long long total = (long long)h * n;
+        const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);
+        count_launch();
+        lu_assemble2_kernel<double><<<blocks, 256, 0, aux>>>(B0, B1, ld, n, PW, perm, snap, U, L, ldo, 0, h);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    EV_TRACE(31, 0, aux);
+    if ((e = tri_inverses<double>(h, U, L, ldo, ei.vbuf, aux)) != cudaSuccess) return e;
+    EV_TRACE(32, 0, aux);
+    {
+        GemmTag tag("gemm:tri_inv");
+        auto p = gemm_params<double>(h, n - h, h, 1.0, U, ldo, U + h, ldo, 0.0, nullptr, ldo, ei.vbuf + h, ldo);
+        p.triA = TRI_UPPER;
+        if ((e = gemm_launch<double>(p, 1, aux)) != cudaSuccess) return e;
+    }
+    EV_TRACE(33, 0, aux);
+    // W' = L21' L11^{-1} (rows in their order after step hstep - 1)
+    const int *pos_h = snap + (long long)(h / PW - 1) * n;
+    count_launch(2);
+    invert_perm_kernel<<<(n + 255) / 256, 256, 0, aux>>>(pos_h, n, at);
+    {
+        const long long total = (long long)(n - h) * h;
+        const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);
+        gather_l21_kernel<<<blocks, 256, 0, aux>>>(B0, B1, ld, n, h, PW, at, snap, ei.vbuf, ldo);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    {
+        GemmTag tag("gemm:tri_inv");
+        auto p = gemm_params<double>(n - h, h, h, 1.0, ei.vbuf + (long long)h * ldo, ldo, L, ldo, 0.0, nullptr, ldo,
+                                     ei.vbuf + (long long)h * ldo + h, ldo);
+        p.triB = TRI_LOWER;
+        if ((e = gemm_launch<double>(p, 1, aux)) != cudaSuccess) return e;
+    }
+    ei.pos_h = pos_h;
+    ei.perm = perm;
+    return cudaEventRecord(ei.done, aux);
+}
+
 // pipeline mode: 2 = fused look-ahead, 1 = separate NEXT kernels, 0 = panel -> full update per
 // step (env FROB_LU2_LOOKAHEAD overrides, A/B aid).  Measured defaults (B200, n = 1024 / 4096):
 // complex (8-column steps, 64 FMAs per row in the fused update) 2: 2.73 / 38.6 ms vs 3.00 / 44.1
@@ -1614,10 +1731,37 @@ static int lu2_lookahead(bool cplx) {
 // step k there), BULK_k the columns >= k0 + 2PW: disjoint.  BULK_k also applies step k's row moves
 // to perm / iperm and takes the snapshot (in step order: the BULKs are serialised).
 template <typename T>
+static cudaError_t lu2_factor_on(int n, T *B0, T *B1, long long ld, T *U, T *L, long long ldo, int *perm, int *iw,
+                                 T *diag, LuStats *stats, cudaStream_t s, EarlyInv *early, bool ew);
+
+template <typename T>
 cudaError_t lu2_factor(int n, T *B0, T *B1, long long ld, T *U, T *L, long long ldo, int *perm, int *iw, T *diag,
-                       LuStats *stats, cudaStream_t s) {
-    constexpr int PW = Panel2W<T>::PW, PH = Panel2W<T>::PH;
+                       LuStats *stats, cudaStream_t s, EarlyInv *early) {
+    constexpr int PW = Panel2W<T>::PW;
     if (n > LU2_MAX_N) return cudaErrorInvalidValue;
+    // EarlyInv (real only): forked once step hstep - 1 is complete, i.e. behind BULK_{hstep-1}
+    const bool ew = sizeof(T) == 8 && early && early->h > 0 && early->h < n && early->h % PW == 0 && early->vbuf;
+    if (early && !ew) early->h = 0;
+    static const int hi_mode = [] {
+        const char *v = tuning_env("FROB_EARLY_HI");
+        return v ? atoi(v) : 1;
+    }();
+    if (!ew || !hi_mode) return lu2_factor_on<T>(n, B0, B1, ld, U, L, ldo, perm, iw, diag, stats, s, early, ew);
+    // the factorisation itself on the highest-priority stream, joined back into s
+    cudaStream_t hs;
+    cudaError_t e = early_stream(1, &hs);
+    if (e == cudaSuccess) e = stream_join(hs, s);
+    if (e == cudaSuccess) e = lu2_factor_on<T>(n, B0, B1, ld, U, L, ldo, perm, iw, diag, stats, hs, early, ew);
+    const cudaError_t j = stream_join(s, hs);
+    return e != cudaSuccess ? e : j;
+}
+
+template <typename T>
+static cudaError_t lu2_factor_on(int n, T *B0, T *B1, long long ld, T *U, T *L, long long ldo, int *perm, int *iw,
+                                 T *diag, LuStats *stats, cudaStream_t s, EarlyInv *early, bool ew) {
+    constexpr int PW = Panel2W<T>::PW, PH = Panel2W<T>::PH;
+    const int hstep = ew ? early->h / PW : -1;
+    EV_TRACE(34, 0, s);
     const int steps = (n + PW - 1) / PW;
     const int ncb = (n + U2_TC - 1) / U2_TC + 1;
     int *iperm = iw;
@@ -1675,6 +1819,14 @@ cudaError_t lu2_factor(int n, T *B0, T *B1, long long ld, T *U, T *L, long long 
             if ((la == 1 && cb < n) || la == 2)
                 if ((e = update(k - 1, min(cb, n), n, false, la == 2)) != cudaSuccess) return e;
         }
+        if constexpr (sizeof(T) == 8) {
+            if (k == hstep) EV_TRACE(36, 0, s);
+            // (real steps use n / 32 of the n / 8 snapshot slots lu2_int_elems sizes for complex: the
+            // position -> row map of EarlyInv lives behind them)
+            if (k == hstep && (e = early_inv_launch(n, B0, B1, ld, U, L, ldo, perm, snap, snap + (size_t)steps * n,
+                                                    *early, s)) != cudaSuccess)
+                return e;
+        }
         if (la == 1 && (e = update(k, k0 + w, min(n, k0 + w + PW), true, true)) != cudaSuccess) return e;  // NEXT_k
     }
     // fused mode: the last step's row moves still go to perm / iperm
@@ -1683,16 +1835,17 @@ cudaError_t lu2_factor(int n, T *B0, T *B1, long long ld, T *U, T *L, long long 
         const long long total = (long long)n * n;
         const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 8);
         e = launch_pdl(lu_assemble2_kernel<T>, dim3(blocks), dim3(256), 0, s, (const T *)B0, (const T *)B1, ld, n,
-                       PW, (const int *)perm, (const int *)snap, U, L, ldo);
+                       PW, (const int *)perm, (const int *)snap, U, L, ldo, ew ? early->h : 0, n);
         if (e != cudaSuccess) return e;
     }
     if (stats) e = lu_stats_launch<T>(diag, n, stats, s);
+    EV_TRACE(35, 0, s);
     return e;
 }
 template cudaError_t lu2_factor<double>(int, double *, double *, long long, double *, double *, long long, int *,
-                                        int *, double *, LuStats *, cudaStream_t);
+                                        int *, double *, LuStats *, cudaStream_t, EarlyInv *);
 template cudaError_t lu2_factor<double2>(int, double2 *, double2 *, long long, double2 *, double2 *, long long,
-                                         int *, int *, double2 *, LuStats *, cudaStream_t);
+                                         int *, int *, double2 *, LuStats *, cudaStream_t, EarlyInv *);
 
 #ifdef FROB_TL
 extern "C" int frob_tl_reset() {
