@@ -1111,6 +1111,32 @@ cudaError_t inv_from_ul(int n, T *U, T *L, long long ld, T *tmp, T *out, long lo
         if ((e = tri_inverses<T>(n, U, L, ld, tmp, s)) != cudaSuccess) return e;
         EV_TRACE(23, 1, s);
     }
+    if (early && early->h > 0 && early->pos_h) {
+        // X = U^{-1} L^{-1} by blocks, P11 = U11^{-1} L11^{-1} formed early (EarlyInv, vbuf's top-left):
+        //   X11 = U12' L21' + P11,  X12 = U12' L22',  X21 = U22' L21',  X22 = U22' L22'
+        const int h = early->h, r = n - h;
+        const T *P11 = reinterpret_cast<const T *>(early->vbuf);
+        const T *U12 = U + h, *U22 = U + (long long)h * ld + h, *L21 = L + (long long)h * ld,
+                *L22 = L + (long long)h * ld + h;
+        T *o21 = out + (long long)h * ldo;
+        auto blk = [&](int M, int N, int K, const T *A, const T *B, const T *D, T *Cb, int col0, int ta, int tb) {
+            auto q = gemm_params<T>(M, N, K, 1.0, A, ld, B, ld, D ? 1.0 : 0.0, D, ld, colperm ? Cb : Cb + col0, ldo);
+            q.colperm = colperm ? colperm + col0 : nullptr;
+            q.triA = ta;
+            q.triB = tb;
+            return q;
+        };
+        GemmTag tag("gemm:product");
+        const auto x11 = blk(h, h, r, U12, L21, P11, out, 0, TRI_NONE, TRI_NONE);
+        const auto x22 = blk(r, r, r, U22, L22, nullptr, o21, h, TRI_UPPER, TRI_LOWER);
+        if ((e = gemm_launch2<T>(x11, 1, x22, 1, s)) != cudaSuccess) return e;
+        const auto x12 = blk(h, r, r, U12, L22, nullptr, out, h, TRI_NONE, TRI_LOWER);
+        const auto x21 = blk(r, h, r, U22, L21, nullptr, o21, 0, TRI_UPPER, TRI_NONE);
+        e = gemm_launch2<T>(x12, 1, x21, 1, s);
+        early->pos_h = nullptr;
+        EV_TRACE(24, 0, s);
+        return e;
+    }
     // X = U^{-1} L^{-1}: (upper) x (lower) -> k from max(row0, col0)
     auto p = gemm_params<T>(n, n, n, 1.0, U, ld, L, ld, 0.0, nullptr, ld, out, ldo);
     p.triA = TRI_UPPER;

@@ -1152,7 +1152,10 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
     const int wm0 = (warp / U2M_WGN) * WM, wn0 = (warp % U2M_WGN) * WN;
     const int c0 = cbeg + blockIdx.x * U2_TC;
     const int r0 = k0 + w + blockIdx.y * U2_TR;
-    const bool tile = c0 < cend;
+    // doperm == 2: the grid's extra last row of CTAs does the perm / iperm / snapshot work alone (off
+    // the tiles' critical path: it cost the (0, 0) tile ~6k cycles of NEXT's ~10k)
+    const bool pcta = doperm == 2 && blockIdx.y == gridDim.y - 1;
+    const bool tile = c0 < cend && !pcta;
     const bool rows = tile && r0 < n;
     const int nc = min(U2_TC, cend - c0);
     NXT(0);
@@ -1246,7 +1249,7 @@ FROB_DEV void update2m_body(const T *__restrict__ Bk, T *__restrict__ Bn, long l
     }
     __syncthreads();
     NXT(1);
-    if (doperm && blockIdx.x == 0 && blockIdx.y == 0) {
+    if (doperm && (doperm == 2 ? (pcta && blockIdx.x == 0) : (blockIdx.x == 0 && blockIdx.y == 0))) {
         int pv = 0;
         if (tid < nm) pv = perm[msrc[tid]];
         __syncthreads();
@@ -1597,10 +1600,15 @@ int early_inv_h(int n) {
         const char *e = tuning_env("FROB_EARLY");
         return e ? atoi(e) : -1;
     }();
-    const int min_n = mode > 1 ? mode : 1024;
+    static int frac = [] {  // h as a percentage of n (env FROB_EARLY_FRAC, A/B aid)
+        const char *e = tuning_env("FROB_EARLY_FRAC");
+        return e ? atoi(e) : 50;
+    }();
+    const int min_n = mode > 1 ? mode : 2048;  // (n = 1024: 3.16 ms with it, 3.10 without)
     if (mode == 0 || n < min_n || n > LU2_MAX_N) return 0;
     constexpr int PW = Panel2W<double>::PW;
-    return (n / 2) / PW * PW;
+    const int h = (int)((long long)n * frac / 100) / PW * PW;
+    return (h > 0 && 2 * h <= n) ? h : 0;
 }
 
 // per-device streams: hi = 0 the lowest priority (EarlyInv work), 1 the highest (the LU's chain
@@ -1654,6 +1662,16 @@ __global__ void gather_l21_kernel(const double *__restrict__ B0, const double *_
     }
 }
 
+// split-K for the EarlyInv GEMMs: shorter CTA lifetimes beside the chain, whose cluster panels wait
+// for whole SMs (n = 4096 Frobenius 31.42 -> 31.19 ms; env FROB_EARLY_SPLIT=0: off, A/B aid)
+static int early_split() {
+    static int v = [] {
+        const char *e = tuning_env("FROB_EARLY_SPLIT");
+        return e ? atoi(e) : 1;
+    }();
+    return v;
+}
+
 // the EarlyInv work of lu2_factor: fork from s after step h / PW - 1 is complete
 static cudaError_t early_inv_launch(int n, const double *B0, const double *B1, long long ld, double *U, double *L,
                                     long long ldo, const int *perm, const int *snap, int *at, EarlyInv &ei,
@@ -1680,11 +1698,12 @@ static cudaError_t early_inv_launch(int n, const double *B0, const double *B1, l
         GemmTag tag("gemm:tri_inv");
         auto p = gemm_params<double>(h, n - h, h, 1.0, U, ldo, U + h, ldo, 0.0, nullptr, ldo, ei.vbuf + h, ldo);
         p.triA = TRI_UPPER;
+        p.force_split = early_split();
         if ((e = gemm_launch<double>(p, 1, aux)) != cudaSuccess) return e;
     }
     EV_TRACE(33, 0, aux);
     // W' = L21' L11^{-1} (rows in their order after step hstep - 1)
-    const int *pos_h = snap + (long long)(h / PW - 1) * n;
+    const int *pos_h = snap + (long long)(h / PW - 1) * n;  // (snapshots of earlier steps stay valid)
     count_launch(2);
     invert_perm_kernel<<<(n + 255) / 256, 256, 0, aux>>>(pos_h, n, at);
     {
@@ -1698,6 +1717,17 @@ static cudaError_t early_inv_launch(int n, const double *B0, const double *B1, l
         auto p = gemm_params<double>(n - h, h, h, 1.0, ei.vbuf + (long long)h * ldo, ldo, L, ldo, 0.0, nullptr, ldo,
                                      ei.vbuf + (long long)h * ldo + h, ldo);
         p.triB = TRI_LOWER;
+        p.force_split = early_split();
+        if ((e = gemm_launch<double>(p, 1, aux)) != cudaSuccess) return e;
+    }
+    // P11 = U11^{-1} L11^{-1}: the top-left block of the product's first term (vbuf's top-left block,
+    // free again after the recursion)
+    {
+        GemmTag tag("gemm:product");
+        auto p = gemm_params<double>(h, h, h, 1.0, U, ldo, L, ldo, 0.0, nullptr, ldo, ei.vbuf, ldo);
+        p.triA = TRI_UPPER;
+        p.triB = TRI_LOWER;
+        p.force_split = early_split();
         if ((e = gemm_launch<double>(p, 1, aux)) != cudaSuccess) return e;
     }
     ei.pos_h = pos_h;
@@ -1760,7 +1790,15 @@ template <typename T>
 static cudaError_t lu2_factor_on(int n, T *B0, T *B1, long long ld, T *U, T *L, long long ldo, int *perm, int *iw,
                                  T *diag, LuStats *stats, cudaStream_t s, EarlyInv *early, bool ew) {
     constexpr int PW = Panel2W<T>::PW, PH = Panel2W<T>::PH;
-    const int hstep = ew ? early->h / PW : -1;
+    // fork step: 3/4 of the steps (the h rows are final from step h / PW; forking later leaves the
+    // auxiliary GEMMs fewer of the chain's steps to slow: n = 4096 Frobenius 31.18 / 30.98 / 30.83 /
+    // 31.05 ms at 50 / 70 / 75 / 80%; env FROB_EARLY_FORK: percent, A/B aid)
+    static const int fork_pct = [] {
+        const char *v = tuning_env("FROB_EARLY_FORK");
+        return v ? atoi(v) : 75;
+    }();
+    const int nsteps = (n + PW - 1) / PW;
+    const int hstep = ew ? std::min(nsteps - 1, std::max(early->h / PW, (int)((long long)nsteps * fork_pct / 100))) : -1;
     EV_TRACE(34, 0, s);
     const int steps = (n + PW - 1) / PW;
     const int ncb = (n + U2_TC - 1) / U2_TC + 1;
@@ -1789,12 +1827,15 @@ static cudaError_t lu2_factor_on(int n, T *B0, T *B1, long long ld, T *U, T *L, 
         const int cols = max(0, ce - cb), rows = n - k0 - w;
         dim3 grid(max(1, (cols + U2_TC - 1) / U2_TC), max(1, (rows + U2_TR - 1) / U2_TR));
         if (cols == 0) grid = dim3(1, 1);
+        // NEXT: one more row of CTAs for the perm / iperm / snapshot work (doperm = 2)
+        const int dp = doperm ? (next ? 2 : 1) : 0;
+        if (dp == 2) grid.y += 1;
         const double upd = ((double)(m - w) * 2.0 * w + (double)w * w) * (double)cols;  // GEMM + TRSM
         ProfScope ps(next ? nm_next : nm_bulk, s, upd * (sizeof(T) == 8 ? 1.0 : 4.0));
         return launch_pdl(lu_update2m_kernel<T, PW>, grid, dim3(U2_T), 0, s, Bk, Bn, ld, n, k0, w,
                           (const int *)(mvb + (size_t)kk * MV2_INTS), perm, iperm,
                           (doperm && kk + 1 < steps) ? snap + (size_t)kk * n : (int *)nullptr, next ? flagN : flagB,
-                          kk + 1, cb, ce, doperm ? 1 : 0, next ? 0 : 1, done + kk);
+                          kk + 1, cb, ce, dp, next ? 0 : 1, done + kk);
     };
     for (int k = 0; k < steps; ++k) {
         const int k0 = k * PW, w = min(PW, n - k0), m = n - k0;
