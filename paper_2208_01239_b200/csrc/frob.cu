@@ -548,12 +548,17 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
         EarlyInv ei;
         ei.h = small ? early_inv_h(n) : 0;
         ei.vbuf = (u == 1) ? w.W5 : w.W2;
+        if (!small && getrf_early_ok(n) && u == 1) {  // getrf's EarlyInv: the split factors go to W2, W3
+            ei.vbuf = w.W5;  // (part 2 has no idle matrix: A's inverse in W4 may still be the one kept)
+            ei.U = w.W2;
+            ei.L = w.W3;
+        }
         {
             ProfScope ps("step:lu", s);
             if (small) FROB_CUDA(lu2_factor<double>(n, in, u == 1 ? w.W4 : w.W1, ld, u == 1 ? w.W2 : w.W6,
                                                     u == 1 ? w.W3 : w.W7, ld, pm, w.iw, w.diag, &w.stats[u - 1], s,
                                                     &ei));
-            else FROB_CUDA(getrf<double>(n, in, ld, pm, w.mv, w.diag, &w.stats[u - 1], w.work, s));
+            else FROB_CUDA(getrf<double>(n, in, ld, pm, w.mv, w.diag, &w.stats[u - 1], w.work, s, &ei));
         }
         factored |= u;
         ProfScope ps("step:inv_from_lu", s);
@@ -561,7 +566,8 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
             if (u == 1) FROB_CUDA(inv_from_ul<double>(n, w.W2, w.W3, ld, w.W1, w.W4, ld, nullptr, w.flags + 2, s, &ei));
             else FROB_CUDA(inv_from_ul<double>(n, w.W6, w.W7, ld, w.W5, w.W1, ld, nullptr, w.flags + 2, s, &ei));
         } else {
-            FROB_CUDA(inv_from_lu<double>(n, in, ld, w.W2, w.W3, u == 1 ? w.W4 : w.W1, ld, nullptr, w.flags + 2, s));
+            FROB_CUDA(inv_from_lu<double>(n, in, ld, w.W2, w.W3, u == 1 ? w.W4 : w.W1, ld, nullptr, w.flags + 2, s,
+                                          &ei));
         }
         return FROB_OK;
     };
@@ -731,12 +737,18 @@ static frob_status frob_inv_impl(int n, const double *Z, long long ldz, double *
         ProfScope ps("step:inv_from_lu", s);
         FROB_CUDA(inv_from_ul<double>(n, w.W4, w.W5, ld, w.W3, Re, ld, nullptr, w.flags + 2, s, &ei));
     } else {
+        EarlyInv ei;  // getrf's EarlyInv (4096 < n <= 8192): scratch Re, split factors Sa / W4
+        if (getrf_early_ok(n)) {
+            ei.vbuf = Re;
+            ei.U = Sa;
+            ei.L = w.W4;
+        }
         {
             ProfScope ps("step:lu", s);
-            FROB_CUDA(getrf<double>(n, w.W3, ld, w.perm_m, w.mv, w.diag, &w.stats[2], w.work, s));
+            FROB_CUDA(getrf<double>(n, w.W3, ld, w.perm_m, w.mv, w.diag, &w.stats[2], w.work, s, &ei));
         }
         ProfScope ps("step:inv_from_lu", s);
-        FROB_CUDA(inv_from_lu<double>(n, w.W3, ld, Sa, w.W4, Re, ld, nullptr, w.flags + 2, s));
+        FROB_CUDA(inv_from_lu<double>(n, w.W3, ld, Sa, w.W4, Re, ld, nullptr, w.flags + 2, s, &ei));
     }
     // a6/a7: Im' = -C Re', fused with the column interchanges and the interleaved store
     {
@@ -824,6 +836,7 @@ static frob_status zinv_lu_impl(int n, const double *Z, long long ldz, double *X
 // ---------------------------------------------------------------------- real inverse
 struct DinvWs {
     double *W, *U, *L, *W2, *diag, *work;  // W2: n <= LU2_MAX_N only
+    double *V;                             // EarlyInv scratch (early_inv_h(n) > 0 only)
     int *perm, *mv, *iw;
     LuStats *stats;
     int *flags;
@@ -838,6 +851,7 @@ static DinvWs carve_dinv(void *ws, int n) {
     w.L = c.take<double>((size_t)n * ld);
     const bool small = n <= lu2_max_n();
     w.W2 = small ? c.take<double>((size_t)n * ld) : nullptr;
+    w.V = (small && early_inv_h(n) > 0) ? c.take<double>((size_t)n * ld) : nullptr;
     w.diag = c.take<double>((size_t)n);
     w.work = c.take<double>(getrf_work_elems<double>(n));
     w.perm = c.take<int>((size_t)n);
@@ -1440,8 +1454,11 @@ frob_status frob_dinv(int n, const double *A, long long lda, double *Ainv, long 
     copy2d_kernel<double><<<ew_blocks((long long)n * n), 256, 0, s>>>(A, lda, w.W, ld, n, nullptr);
     FROB_CUDA(cudaGetLastError());
     if (n <= lu2_max_n()) {
-        FROB_CUDA(lu2_factor<double>(n, w.W, w.W2, ld, w.U, w.L, ld, w.perm, w.iw, w.diag, w.stats, s));
-        FROB_CUDA(inv_from_ul<double>(n, w.U, w.L, ld, w.W, Ainv, ldainv, w.perm, w.flags, s));
+        EarlyInv ei;  // the same inversion as frob_inv's (T_inv of the threshold analysis)
+        ei.h = w.V ? early_inv_h(n) : 0;
+        ei.vbuf = w.V;
+        FROB_CUDA(lu2_factor<double>(n, w.W, w.W2, ld, w.U, w.L, ld, w.perm, w.iw, w.diag, w.stats, s, &ei));
+        FROB_CUDA(inv_from_ul<double>(n, w.U, w.L, ld, w.W, Ainv, ldainv, w.perm, w.flags, s, &ei));
     } else {
         FROB_CUDA(getrf<double>(n, w.W, ld, w.perm, w.mv, w.diag, w.stats, w.work, s));
         FROB_CUDA(inv_from_lu<double>(n, w.W, ld, w.U, w.L, Ainv, ldainv, w.perm, w.flags, s));

@@ -896,11 +896,11 @@ constexpr int TRI_LEAF = 32;
 // U = triu(lu) (zeros below), L = tril(lu, -1) + I (zeros above)
 template <typename T>
 __global__ void extract_ul_kernel(const T *__restrict__ lu, long long ld, int n, T *__restrict__ U,
-                                  T *__restrict__ L) {
-    const long long total = (long long)n * n;
+                                  T *__restrict__ L, int r0, int r1) {  // rows [r0, r1)
+    const long long total = (long long)(r1 - r0) * n;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
-        const int i = (int)(idx / n), j = (int)(idx - (long long)i * n);
+        const int i = r0 + (int)(idx / n), j = (int)(idx % n);
         const T v = lu[(long long)i * ld + j];
         const T z = zero_of(T());
         U[(long long)i * ld + j] = (j >= i) ? v : z;
@@ -913,7 +913,7 @@ cudaError_t extract_ul(int n, const T *lu, long long ld, T *U, T *L, cudaStream_
     const long long total = (long long)n * n;
     const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
     count_launch();
-    extract_ul_kernel<T><<<blocks, 256, 0, s>>>(lu, ld, n, U, L);
+    extract_ul_kernel<T><<<blocks, 256, 0, s>>>(lu, ld, n, U, L, 0, n);
     return cudaGetLastError();
 }
 template cudaError_t extract_ul<double>(int, const double *, long long, double *, double *, cudaStream_t);
@@ -1023,16 +1023,18 @@ static cudaError_t tri_level(T *U, T *L, T *tmp, long long ld, int s, int o, int
 
 template <typename T>
 cudaError_t inv_from_lu(int n, T *lu, long long ld, T *U, T *L, T *out, long long ldo,
-                        const int *colperm, int *counter, cudaStream_t s) {
+                        const int *colperm, int *counter, cudaStream_t s, EarlyInv *early) {
     cudaError_t e;
+    // (EarlyInv from getrf: the first h rows of U and L are in place already)
+    const int r0 = (early && early->ready) ? early->h : 0;
     {
-        long long total = (long long)n * n;
+        long long total = (long long)(n - r0) * n;
         long long nb = (total + 255) / 256; int blocks = (int)(nb < 148LL * 16 ? nb : 148LL * 16);
         count_launch();
-        extract_ul_kernel<T><<<blocks, 256, 0, s>>>(lu, ld, n, U, L);
+        extract_ul_kernel<T><<<blocks, 256, 0, s>>>(lu, ld, n, U, L, r0, n);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
-    return inv_from_ul<T>(n, U, L, ld, lu, out, ldo, colperm, counter, s);  // the LU factors are scratch now
+    return inv_from_ul<T>(n, U, L, ld, lu, out, ldo, colperm, counter, s, early);  // the LU factors are scratch now
 }
 
 // U <- U^{-1}, L <- L^{-1} in place (32 x 32 diagonal inverses + log-depth recursion)
@@ -1060,14 +1062,17 @@ template cudaError_t tri_inverses<double>(int, double *, double *, long long, do
 template cudaError_t tri_inverses<double2>(int, double2 *, double2 *, long long, double2 *, cudaStream_t);
 
 // out[i][c] = Wp[pos_h[perm[h + i]] - h][c]: EarlyInv's W' rows in the final order (i < n - h, c < h)
+// (getrf's EarlyInv: out[i][c] = Wp[wmap[i]][c])
 template <typename T>
 __global__ void gather_w_kernel(const T *__restrict__ Wp, long long ld, const int *__restrict__ perm,
-                                const int *__restrict__ pos_h, int n, int h, T *__restrict__ out, long long ldo) {
+                                const int *__restrict__ pos_h, const int *__restrict__ wmap, int n, int h,
+                                T *__restrict__ out, long long ldo) {
     const long long total = (long long)(n - h) * h;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
         const int i = (int)(idx / h), c = (int)(idx % h);
-        out[(long long)i * ldo + c] = Wp[(long long)(pos_h[perm[h + i]] - h) * ld + c];
+        const int src = wmap ? wmap[i] : pos_h[perm[h + i]] - h;
+        out[(long long)i * ldo + c] = Wp[(long long)src * ld + c];
     }
 }
 
@@ -1094,8 +1099,8 @@ cudaError_t inv_from_ul(int n, T *U, T *L, long long ld, T *tmp, T *out, long lo
             const long long total = (long long)r * h;
             count_launch();
             gather_w_kernel<T><<<(int)std::min<long long>((total + 255) / 256, 148LL * 8), 256, 0, s>>>(
-                reinterpret_cast<const T *>(early->vbuf) + (long long)h * ld + h, ld, early->perm, early->pos_h, n, h,
-                tmp + (long long)h * ld, ld);
+                reinterpret_cast<const T *>(early->vbuf) + (long long)h * ld + h, ld, early->perm, early->pos_h,
+                early->wmap, n, h, tmp + (long long)h * ld, ld);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
         }
         // U12 <- -V U22^{-1}  and  L21 <- -L22^{-1} W: one launch
@@ -1111,7 +1116,7 @@ cudaError_t inv_from_ul(int n, T *U, T *L, long long ld, T *tmp, T *out, long lo
         if ((e = tri_inverses<T>(n, U, L, ld, tmp, s)) != cudaSuccess) return e;
         EV_TRACE(23, 1, s);
     }
-    if (early && early->h > 0 && early->pos_h) {
+    if (early && early->ready && early->h > 0) {
         // X = U^{-1} L^{-1} by blocks, P11 = U11^{-1} L11^{-1} formed early (EarlyInv, vbuf's top-left):
         //   X11 = U12' L21' + P11,  X12 = U12' L22',  X21 = U22' L21',  X22 = U22' L22'
         const int h = early->h, r = n - h;
@@ -1133,7 +1138,7 @@ cudaError_t inv_from_ul(int n, T *U, T *L, long long ld, T *tmp, T *out, long lo
         const auto x12 = blk(h, r, r, U12, L22, nullptr, out, h, TRI_NONE, TRI_LOWER);
         const auto x21 = blk(r, h, r, U22, L21, nullptr, o21, 0, TRI_UPPER, TRI_NONE);
         e = gemm_launch2<T>(x12, 1, x21, 1, s);
-        early->pos_h = nullptr;
+        early->ready = false;
         EV_TRACE(24, 0, s);
         return e;
     }
@@ -1169,8 +1174,8 @@ cudaError_t lu_stats_launch(const T *diag, int n, LuStats *st, cudaStream_t s) {
 template cudaError_t lu_stats_launch<double>(const double *, int, LuStats *, cudaStream_t);
 template cudaError_t lu_stats_launch<double2>(const double2 *, int, LuStats *, cudaStream_t);
 
-template cudaError_t inv_from_lu<double>(int, double *, long long, double *, double *, double *, long long, const int *, int *, cudaStream_t);
-template cudaError_t inv_from_lu<double2>(int, double2 *, long long, double2 *, double2 *, double2 *, long long, const int *, int *, cudaStream_t);
+template cudaError_t inv_from_lu<double>(int, double *, long long, double *, double *, double *, long long, const int *, int *, cudaStream_t, EarlyInv *);
+template cudaError_t inv_from_lu<double2>(int, double2 *, long long, double2 *, double2 *, double2 *, long long, const int *, int *, cudaStream_t, EarlyInv *);
 
 
 // =====================================================================================
@@ -1413,7 +1418,7 @@ static bool getrf_prio() {
 
 template <typename T>
 cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuStats *stats, T *work,
-                  cudaStream_t s) {
+                  cudaStream_t s, EarlyInv *early) {
     constexpr int PW = PanelW<T>::PW, PW2 = Panel2W<T>::PW;
     cudaError_t e = launch_pdl(iota_kernel, dim3((n + 255) / 256), dim3(256), 0, s, perm, n);
     if (e != cudaSuccess) return e;
@@ -1524,6 +1529,17 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
         if ((e = cudaEventRecord(evJ, ax.st)) != cudaSuccess) return e;
         if ((e = cudaStreamWaitEvent(cs, evJ, 0)) != cudaSuccess) return e;
         EV_TRACE(7, 0, cs);
+        // EarlyInv (real, Ktail <= n / 2): U's first Ktail rows and L11 are final now; the tail's
+        // left-column permutation below must not overwrite L21 before the auxiliary stream copied it
+        cudaEvent_t l21_done = nullptr;
+        if constexpr (sizeof(T) == 8) {
+            if (early && early->vbuf && early->U && early->L && Ktail < n && Ktail > 0 && 2 * Ktail <= n) {
+                if ((e = getrf_early_launch(n, A, lda, Ktail, *early, cs, &l21_done)) != cudaSuccess) return e;
+            } else if (early) {
+                early->h = 0;
+                early->ready = false;
+            }
+        }
         if (Ktail < n) {
             // ---- the trailing m x m matrix (fully updated, all earlier row moves applied to every
             // column) factored by lu2 into compact buffers, assembled packed back in place; its
@@ -1535,6 +1551,9 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
             T *B0 = tb, *B1 = tb + (size_t)m * ldm;
             int *iw2 = reinterpret_cast<int *>(B1 + (size_t)m * ldm);
             int *psub = iw2 + lu2_int_elems(m), *ptmp = psub + m;
+            if constexpr (sizeof(T) == 8) {
+                if (early && early->ready) early->wmap = psub;  // W[i] = W'[psub[i]] once the tail is done
+            }
             T *A22 = A + (long long)Ktail * lda + Ktail;
             if ((e = launch_pdl(copy_block_kernel<T>, dim3(ew_grid((long long)m * m)), dim3(256), 0, cs, (const T *)A22,
                                 lda, B0, ldm, m, m)) != cudaSuccess)
@@ -1542,6 +1561,11 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
             if ((e = lu2_factor<T>(m, B0, B1, ldm, A22, A22, lda, psub, iw2, diag + Ktail, nullptr, cs)) != cudaSuccess)
                 return e;
             EV_TRACE(8, 0, cs);
+            if (l21_done) {
+                e = cudaStreamWaitEvent(cs, l21_done, 0);
+                cudaEventDestroy(l21_done);
+                if (e != cudaSuccess) return e;
+            }
             for (int c0 = 0; c0 < Ktail; c0 += m) {  // left columns in chunks of m through B1
                 const int nc = min(m, Ktail - c0);
                 if ((e = launch_pdl(gather_rows_kernel<T>, dim3(ew_grid((long long)m * nc)), dim3(256), 0, cs,
@@ -1567,8 +1591,9 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
     }
     return e;
 }
-template cudaError_t getrf<double>(int, double *, long long, int *, int *, double *, LuStats *, double *, cudaStream_t);
+template cudaError_t getrf<double>(int, double *, long long, int *, int *, double *, LuStats *, double *, cudaStream_t,
+                                   EarlyInv *);
 template cudaError_t getrf<double2>(int, double2 *, long long, int *, int *, double2 *, LuStats *, double2 *,
-                                    cudaStream_t);
+                                    cudaStream_t, EarlyInv *);
 
 }  // namespace frob

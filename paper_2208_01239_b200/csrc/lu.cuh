@@ -24,6 +24,32 @@ struct LuStats {
     int nonfinite;   // 1 if any pivot is NaN/Inf
 };
 
+// Early triangular inverses (real lu2): the first h rows of U and the block L11 are final once lu2's
+// step h / PW has been applied, while the rest of the LU -- its chain-bound tail, which leaves most
+// SMs idle -- is still running.  lu2_factor then assembles them on a low-priority auxiliary stream,
+// inverts U11 and L11 in place (tri_inverses) and forms V = U11^{-1} U12 into rows [0, h), columns
+// [h, n) of vbuf (its top-left h x h block is that recursion's scratch); inv_from_ul waits for that
+// work and finishes with the order-(n - h) blocks and the top-level products
+//   U^{-1} = [U11^{-1}, -V U22^{-1}; 0, U22^{-1}],  L^{-1} = [L11^{-1}, 0; -L22^{-1} W, L22^{-1}],  W = L21 L11^{-1}.
+// vbuf: n x ldo doubles, untouched by anything else from lu2_factor's start until inv_from_ul returns.
+// L21 is not final at that point (later pivots move its rows), but its rows are only permuted:
+// W' = L21' L11^{-1} is formed early on the rows in their order after step h / PW - 1 (vbuf rows
+// [h, n): L21' in columns [0, h), W' in columns [h, 2h)) and gathered into the final order at the end
+// (W[i] = W'[pos_h(perm[h + i]) - h], pos_h = that step's row-position snapshot).
+// The blocked LU (getrf, 4096 < n <= 8192) does the same during its lu2 tail: when the blocked part
+// has reached h = Ktail (<= n / 2), U's first h rows and L11 are final and L21 only awaits the tail's
+// row permutation psub (W[i] = W'[psub[i]]); U and L are then the inverse's split buffers.
+struct EarlyInv {
+    int h = 0;                    // lu2: the split row (0: not used); getrf sets it
+    double *vbuf = nullptr;
+    double *U = nullptr, *L = nullptr;  // getrf only: where the inverse's split factors go
+    cudaEvent_t done = nullptr;   // recorded on the auxiliary stream after V, W' and P11
+    const int *pos_h = nullptr;   // lu2: original row -> position after step h / PW - 1
+    const int *perm = nullptr;    // lu2: the final permutation (valid after the LU)
+    const int *wmap = nullptr;    // getrf: W[i] = W'[wmap[i]] (the tail's psub, valid after the LU)
+    bool ready = false;           // the early blocks were launched (the product takes the block path)
+};
+
 // Row movement produced by one panel: rows src[q] -> dst[q] (global indices), q < cnt.
 // Layout in an int buffer: [cnt, dst[0..2PWMAX), src[0..2PWMAX)].
 constexpr int PW_MAX = 32;
@@ -43,7 +69,13 @@ size_t getrf_work_elems(int n);
 
 template <typename T>
 cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuStats *stats, T *work,
-                  cudaStream_t s);
+                  cudaStream_t s, EarlyInv *early = nullptr);
+// getrf takes EarlyInv for 4096 < n <= 8192 (env FROB_EARLY=0: off, A/B aid)
+bool getrf_early_ok(int n);
+// getrf's EarlyInv work (lu2.cu): forked from s at the tail (A's first h rows final); l21_done is
+// recorded once L21 has been copied out (the tail's left-column permutation must wait for it)
+cudaError_t getrf_early_launch(int n, const double *A, long long lda, int h, EarlyInv &ei, cudaStream_t s,
+                               cudaEvent_t *l21_done);
 
 // From an LU in `lu` (ld): Xinv = U^{-1} L^{-1} (un-permuted: A^{-1} = Xinv P).
 // Work buffers U, L (n x ld each) are overwritten; `lu` may be used as the
@@ -51,7 +83,7 @@ cudaError_t getrf(int n, T *A, long long lda, int *perm, int *mv, T *diag, LuSta
 // counter: device int scratch for the persistent product scheduler (nullable = static grid)
 template <typename T>
 cudaError_t inv_from_lu(int n, T *lu, long long ld, T *U, T *L, T *out, long long ldo,
-                        const int *colperm, int *counter, cudaStream_t s);
+                        const int *colperm, int *counter, cudaStream_t s, EarlyInv *early = nullptr);
 
 // Latency-oriented LU for n <= LU2_MAX_N (lu2.cu): B0 holds A on entry and is destroyed,
 // B1 is scratch (n x ld); the factors come out split: U (upper, zeros below), L (unit lower,
@@ -78,25 +110,6 @@ int lu2_panel_max_m();
 template <typename T>
 cudaError_t lu2_panel_inplace(const CUtensorMap &tm, T *A, long long lda, int n, int k0, int w, int *mv, T *diag,
                               cudaStream_t s);
-// Early triangular inverses (real lu2): the first h rows of U and the block L11 are final once lu2's
-// step h / PW has been applied, while the rest of the LU -- its chain-bound tail, which leaves most
-// SMs idle -- is still running.  lu2_factor then assembles them on a low-priority auxiliary stream,
-// inverts U11 and L11 in place (tri_inverses) and forms V = U11^{-1} U12 into rows [0, h), columns
-// [h, n) of vbuf (its top-left h x h block is that recursion's scratch); inv_from_ul waits for that
-// work and finishes with the order-(n - h) blocks and the top-level products
-//   U^{-1} = [U11^{-1}, -V U22^{-1}; 0, U22^{-1}],  L^{-1} = [L11^{-1}, 0; -L22^{-1} W, L22^{-1}],  W = L21 L11^{-1}.
-// vbuf: n x ldo doubles, untouched by anything else from lu2_factor's start until inv_from_ul returns.
-// L21 is not final at that point (later pivots move its rows), but its rows are only permuted:
-// W' = L21' L11^{-1} is formed early on the rows in their order after step h / PW - 1 (vbuf rows
-// [h, n): L21' in columns [0, h), W' in columns [h, 2h)) and gathered into the final order at the end
-// (W[i] = W'[pos_h(perm[h + i]) - h], pos_h = that step's row-position snapshot).
-struct EarlyInv {
-    int h = 0;                    // 0: not used
-    double *vbuf = nullptr;
-    cudaEvent_t done = nullptr;   // recorded on the auxiliary stream after V and W'
-    const int *pos_h = nullptr;   // set by lu2_factor: original row -> position after step h / PW - 1
-    const int *perm = nullptr;    // set by lu2_factor: the final permutation (valid after the LU)
-};
 // h for an order-n lu2 factorisation (0 below the size where it pays; env FROB_EARLY=0: off, A/B aid)
 int early_inv_h(int n);
 template <typename T>

@@ -1595,6 +1595,14 @@ template cudaError_t lu2_panel_inplace<double2>(const CUtensorMap &, double2 *, 
 
 // ---------------------------------------------------------------------------------------
 // EarlyInv (see lu.cuh): a lowest-priority auxiliary stream per device
+static long long ld_of_ws(int n) { return ((long long)n + 7) / 8 * 8; }  // the callers' workspace ld
+bool getrf_early_ok(int n) {
+    static int mode = [] {
+        const char *e = tuning_env("FROB_EARLY");
+        return e ? atoi(e) : -1;
+    }();
+    return mode != 0 && n > LU2_MAX_N && n <= 2 * LU2_MAX_N;
+}
 int early_inv_h(int n) {
     static int mode = [] {
         const char *e = tuning_env("FROB_EARLY");
@@ -1732,6 +1740,80 @@ static cudaError_t early_inv_launch(int n, const double *B0, const double *B1, l
     }
     ei.pos_h = pos_h;
     ei.perm = perm;
+    ei.wmap = nullptr;
+    ei.ready = true;
+    return cudaEventRecord(ei.done, aux);
+}
+
+// getrf's EarlyInv (see lu.cuh): A's first h rows hold U's rows and L11 (packed), rows [h, n) of its
+// first h columns the multipliers L21 in their order before the tail's permutation
+__global__ void early_extract_kernel(const double *__restrict__ A, long long lda, int n, int h,
+                                     double *__restrict__ U, double *__restrict__ L, long long ld,
+                                     double *__restrict__ l21, long long ldv) {
+    const long long top = (long long)h * n, total = top + (long long)(n - h) * h;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        if (idx < top) {
+            const int i = (int)(idx / n), j = (int)(idx % n);
+            const double v = A[(long long)i * lda + j];
+            U[(long long)i * ld + j] = (j >= i) ? v : 0.0;
+            L[(long long)i * ld + j] = (j < i) ? v : ((j == i) ? 1.0 : 0.0);
+        } else {
+            const long long q = idx - top;
+            const int i = h + (int)(q / h), j = (int)(q % h);
+            l21[(long long)i * ldv + j] = A[(long long)i * lda + j];
+        }
+    }
+}
+
+cudaError_t getrf_early_launch(int n, const double *A, long long lda, int h, EarlyInv &ei, cudaStream_t s,
+                               cudaEvent_t *l21_done) {
+    cudaStream_t aux;
+    cudaError_t e = early_aux_stream(&aux);
+    if (e != cudaSuccess) return e;
+    const long long ld = ld_of_ws(n);
+    ei.h = h;
+    if ((e = cudaEventCreateWithFlags(&ei.done, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(l21_done, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = stream_join(aux, s)) != cudaSuccess) return e;
+    EV_TRACE(30, 1, aux);
+    {
+        const long long total = (long long)h * n + (long long)(n - h) * h;
+        count_launch();
+        early_extract_kernel<<<(int)std::min<long long>((total + 255) / 256, 148LL * 8), 256, 0, aux>>>(
+            A, lda, n, h, ei.U, ei.L, ld, ei.vbuf, ld);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(*l21_done, aux)) != cudaSuccess) return e;
+    }
+    EV_TRACE(31, 1, aux);
+    if ((e = tri_inverses<double>(h, ei.U, ei.L, ld, ei.vbuf, aux)) != cudaSuccess) return e;
+    EV_TRACE(32, 1, aux);
+    GemmTag tag("gemm:tri_inv");
+    {   // V = U11^{-1} U12
+        auto p = gemm_params<double>(h, n - h, h, 1.0, ei.U, ld, ei.U + h, ld, 0.0, nullptr, ld, ei.vbuf + h, ld);
+        p.triA = TRI_UPPER;
+        p.force_split = early_split();
+        if ((e = gemm_launch<double>(p, 1, aux)) != cudaSuccess) return e;
+    }
+    {   // W' = L21' L11^{-1}
+        auto p = gemm_params<double>(n - h, h, h, 1.0, ei.vbuf + (long long)h * ld, ld, ei.L, ld, 0.0, nullptr, ld,
+                                     ei.vbuf + (long long)h * ld + h, ld);
+        p.triB = TRI_LOWER;
+        p.force_split = early_split();
+        if ((e = gemm_launch<double>(p, 1, aux)) != cudaSuccess) return e;
+    }
+    {   // P11 = U11^{-1} L11^{-1}
+        GemmTag ptag("gemm:product");
+        auto p = gemm_params<double>(h, h, h, 1.0, ei.U, ld, ei.L, ld, 0.0, nullptr, ld, ei.vbuf, ld);
+        p.triA = TRI_UPPER;
+        p.triB = TRI_LOWER;
+        p.force_split = early_split();
+        if ((e = gemm_launch<double>(p, 1, aux)) != cudaSuccess) return e;
+    }
+    EV_TRACE(33, 1, aux);
+    ei.pos_h = nullptr;
+    ei.perm = nullptr;
+    ei.ready = true;
     return cudaEventRecord(ei.done, aux);
 }
 
