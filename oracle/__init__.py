@@ -29,7 +29,7 @@ _lock = threading.Lock()
 _lib = None
 
 BRANCH = {"auto": 0, "a": 1, "b": 2}
-KAPPA_SWITCH = 8.8e4  # DESIGN.md reading R1': AUTO switch test on kappa_inf(A) / sqrt(n), kappa_inf = ||A||_inf ||A^-1||_inf
+KAPPA_SWITCH = 2.5e4  # DESIGN.md reading R1': AUTO switch test on kappa_inf(A) / sqrt(n), kappa_inf = ||A||_inf ||A^-1||_inf
 
 
 def build(force: bool = False) -> str:

@@ -568,6 +568,17 @@ frob_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__rest
 // 512 threads, 4 x 8 register blocks (32 FMAs per thread per sweep step): fewer per-step
 // bookkeeping instructions than 1024 x (4 x 4), more warps to hide latency than 256 x (8 x 8)
 constexpr int R128 = 4, B128 = 8;
+// phase clock stamps of sampled CTAs (probe builds with -DFROB_B128_TL: tools/batched128_phases.py)
+#ifdef FROB_B128_TL
+__device__ long long g_b128_tl[16][8];
+#define B128_TL(i) do { __syncthreads(); if (threadIdx.x == 0 && (blockIdx.x & 1023) == 0) \
+    g_b128_tl[(blockIdx.x >> 10) & 15][i] = clock64(); } while (0)
+extern "C" int frob_b128_tl_read(long long *h) {
+    return (int)cudaMemcpyFromSymbol(h, g_b128_tl, sizeof(g_b128_tl));
+}
+#else
+#define B128_TL(i) do { } while (0)
+#endif
 constexpr int T128 = (128 / R128) * (128 / B128);
 struct Frob128Smem {
     double S[128 * 132];
@@ -586,6 +597,7 @@ FROB_DEV void frob128_rest(const double2 *__restrict__ Zb, double2 *__restrict__
     };
     auto Xv = [&](int i, int j) { return (USE == 1) ? Zb[i * n + j].x : Zb[i * n + j].y; };
     double acc[WT<N>::MT][WT<N>::NT][2];
+    B128_TL(2);
     // a3: C = X^{-1} Y -> Cg   (two 64-row halves to bound register use)
     for (int h = 0; h < 2; ++h) {
         cta_mma_f<N>([&](int r, int k) { return S[r * SS + k]; }, Yv, acc, 64 * h);
@@ -594,6 +606,7 @@ FROB_DEV void frob128_rest(const double2 *__restrict__ Zb, double2 *__restrict__
         }, 64 * h);
     }
     __syncthreads();
+    B128_TL(3);
     // a4: M = X + Y C -> S
     for (int h = 0; h < 2; ++h) {
         cta_mma_f<N>(Yv, [&](int k, int c) { return (k < n && c < n) ? Cg[k * n + c] : 0.0; }, acc, 64 * h);
@@ -601,6 +614,7 @@ FROB_DEV void frob128_rest(const double2 *__restrict__ Zb, double2 *__restrict__
                            64 * h);
     }
     __syncthreads();
+    B128_TL(4);
     // a5: Re = M^{-1} -> S
     {
         double a[R128][B128];
@@ -611,6 +625,7 @@ FROB_DEV void frob128_rest(const double2 *__restrict__ Zb, double2 *__restrict__
         sweep_store<double, N, R128, B128>(a, sw, S, SS);
     }
     __syncthreads();
+    B128_TL(5);
     // a6/a7: Im = -C Re, interleaved store (after every warp has finished reading its C rows)
     auto out = [&](int i, int j, double v) {
         if (i < n && j < n) {
@@ -624,6 +639,7 @@ FROB_DEV void frob128_rest(const double2 *__restrict__ Zb, double2 *__restrict__
         __syncthreads();
         cta_mma_foreach<N>(acc, out, 64 * h);
     }
+    B128_TL(6);
 }
 
 __global__ void __launch_bounds__(T128, 1)
@@ -643,14 +659,17 @@ frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
 
     int use = (branch == FROB_BRANCH_B) ? 2 : 1;
     int inf_x;
+    B128_TL(0);
     {
         double a[R128][B128];
         double pmax, pmin;
         if (use == 1) load_blocks_f<double, N, R128, B128>(a, n, [&](int i, int j) { return Zb[i * n + j].x; });
         else load_blocks_f<double, N, R128, B128>(a, n, [&](int i, int j) { return Zb[i * n + j].y; });
+        B128_TL(7);
         gj_sweep<double, N, R128, B128>(a, n, sm.sw, pmax, pmin);
         inf_x = sweep_info<double, N>(sm.sw, n, pmax);
         sweep_store<double, N, R128, B128>(a, sm.sw, S, SS);
+        B128_TL(1);
         if (branch == FROB_BRANCH_AUTO) {
             // reading R1' (see frob_batched_kernel)
             const double na = mat_norm_inf(n, [&](int i, int j) { return Zb[i * n + j].x; }, sm.sw.pmag_k, T128);

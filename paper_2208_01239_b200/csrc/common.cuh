@@ -28,8 +28,9 @@ inline const char *tuning_env(const char *name) {
 // kappa_inf(A) = ||A||_inf ||A^-1||_inf of the computed inverse (the conditioning of X drives the
 // leading term of Thm 5.2's bound; kappa_inf / sqrt(n) tracks kappa_2 of dense matrices
 // up to an O(1) factor); above it (or with A singular) both parts are inverted and the smaller
-// kappa_inf wins.
-constexpr double KAPPA_SWITCH = 8.8e4;
+// kappa_inf wins.  2.5e4: S1's error is at most ~2.6 u kappa_inf(A) (R1'), so the switch
+// keeps it <= 1e-10 up to n = 128 by that calibration, not by the luck of one kernel's rounding.
+constexpr double KAPPA_SWITCH = 2.5e4;
 FROB_DEV_HOST_INLINE double kappa_switch(int n) { return KAPPA_SWITCH * sqrt((double)n); }
 
 // process-wide count of kernel launches issued by the library (frob_launch_count())

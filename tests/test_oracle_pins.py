@@ -589,3 +589,20 @@ def test_frob_inv_many_matches_single_calls_bitwise():
         assert st[i] == sti and info[i] == inf["info"] and bu[i] == inf["branch_used"]
         assert np.array_equal(x[i], xi)
     assert bu[3] == 2
+
+
+def test_auto_rule_threshold_from_the_error_calibration():
+    """R1' threshold 2.5e4 (kappa_inf(A) / sqrt(n)): S1's error is up to ~2.6 u kappa_inf(A), so every
+    part kept must have kappa_inf(A) <= 1e-10 / (2.6 u) = 3.5e5 at n = 128.  Config-3 matrix 487
+    (kappa_2(Z) = 678, kappa_inf(A) = 6.2e5) sits between the old (8.8e4 sqrt(n) = 1.0e6) and the new
+    switch point: AUTO now takes S2, which is accurate; S1 carries u kappa_inf(A)-sized error."""
+    n = 128
+    z = synth.batch(n, 1, seed=0, start=487)[0]
+    ref, _ = oracle.zinv_gj(z)
+    x, st, info = oracle.frob_inv(z)
+    assert 1e-10 / (2.6 * 2.0 ** -53) > oracle.KAPPA_SWITCH * math.sqrt(n)
+    assert st == 0 and info["branch_used"] == 2
+    assert oracle.KAPPA_SWITCH * math.sqrt(n) < info["kappa_a"] < 8.8e4 * math.sqrt(n)
+    assert oracle.rel_fro(x, ref) <= 1e-12
+    xa, _, _ = oracle.frob_inv(z, "a")
+    assert oracle.rel_fro(xa, ref) > 1e-12
