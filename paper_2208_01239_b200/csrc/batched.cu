@@ -562,12 +562,10 @@ frob_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__rest
 }
 
 // ----------------------------------------------------------------- Frobenius, 64 < n <= 128
-// 512 threads, 4x8 register blocks for the sweeps; one 135 KB shared buffer (X^{-1}, then
-// M, then Re); C = X^{-1} Y lives in the first half of the OUTPUT matrix (planar n x n
-// doubles) until the final epilogue overwrites it with the interleaved result.
-// 512 threads, 4 x 8 register blocks (32 FMAs per thread per sweep step): fewer per-step
-// bookkeeping instructions than 1024 x (4 x 4), more warps to hide latency than 256 x (8 x 8)
-constexpr int R128 = 4, B128 = 8;
+// 512 threads.  The two inversions by the blocked, warp-specialised Gauss-Jordan sweep below
+// (gj128_sweep); the three GEMMs by DMMA from shared / L1-resident operands (cta_mma_f).  One
+// 135 KB shared buffer (X^{-1}, then M, then Re); C = X^{-1} Y lives in the second half of the
+// OUTPUT matrix (planar n x n doubles) until the final epilogue overwrites it with the result.
 // phase clock stamps of sampled CTAs (probe builds with -DFROB_B128_TL: tools/batched128_phases.py)
 #ifdef FROB_B128_TL
 __device__ long long g_b128_tl[16][8];
@@ -579,70 +577,374 @@ extern "C" int frob_b128_tl_read(long long *h) {
 #else
 #define B128_TL(i) do { } while (0)
 #endif
-constexpr int T128 = (128 / R128) * (128 / B128);
+
+// ----------------------------------------------------------------- blocked Gauss-Jordan, N = 128
+// The exchange-form sweep (same pivots as gj_sweep: partial pivoting, first maximum; result
+// scattered as inverse[pos[i]][pivrow[j]] = element (i, j)) in 8-column panels.  The matrix lives
+// in the DMMA accumulators of the 16 warps (each a 32 x 32 block of 8 x 8 tiles).  One warp (the
+// panel warp) factors panel b in LU form in its registers (its own tiles parked in shared memory
+// meanwhile): pivot search by REDUX, pivot row through shared memory, no block barrier; with M =
+// A_RK = L11 U11 (rows R = the panel's pivot rows in order) and A_IK = L21 U11, sweeping the panel
+// acts on every other column block J as
+//     A_IJ -= L21 W,   A_RJ = V,   W = L11^-1 A_RJ,   V = U11^-1 W   (forward / back substitution)
+//     A_IK = -L21 L11^-1,   A_RK = U11^-1 L11^-1.
+// The other columns take the substitution form (rank-8 DMMA with the multipliers) -- NOT the product
+// of the swept panel with the old pivot rows: that form rounds ~20x worse on ill-conditioned parts
+// (tools/gj_block_accuracy.py), this one as well as the unblocked sweep.  The owners of the
+// next panel's columns update them first and hand them over (look-ahead).
+constexpr int G8_W = 8;                  // panel width
+constexpr int G8_T = 512;                // 16 warps
+constexpr int G8_PW = 15;                // the panel warp (tile rows 96.., tile columns 96..)
+constexpr int G8_PS = 10;                // panel buffer row stride (doubles; 16-byte rows)
+constexpr int G8_TS = 132;               // T / W / V buffer row stride
+constexpr int G8_BAR_U = 1, G8_BAR_PANEL = 2, G8_BAR_FACT = 3;  // named barriers (0 = __syncthreads)
+struct G8Shared {
+    double pb[2][128 * G8_PS];   // panel b: handed to the panel warp, then its LU form (multipliers / U rows)
+    double pf[2][128 * G8_PS];   // panel b swept (A_IK, A_RK above)
+    double tb[2][G8_W * G8_TS];  // T = the pivot rows (old), then W
+    double tv[G8_W * G8_TS];     // V (written after, read before a U barrier: one buffer)
+    double park[32 * 32];        // the panel warp's own tiles while it factors a panel; norm row sums
+    double lu[G8_W * G8_W];      // the panel's pivot rows (L11 strictly below, U11 on / above the diagonal)
+    double rpiv[G8_W];           // 1 / u_cc
+    double uinv[G8_W * G8_W];    // U11^-1
+    double linv[G8_W * G8_W];    // L11^-1 (unit lower)
+    int prow[2][G8_W];
+    signed char rowslot[2][128];  // panel slot of a pivot row, -1 otherwise
+};
 struct Frob128Smem {
     double S[128 * 132];
     SweepShared<double, 128> sw;
+    G8Shared gs;
 };
 
-// Steps a3..a7 for a fixed branch (USE = 1: X = A, Y = B; USE = 2: X = B, Y = -A), so the
-// sign of Y is a compile-time property of the operand accessors.
-template <int USE>
-FROB_DEV void frob128_rest(const double2 *__restrict__ Zb, double2 *__restrict__ Xb, int n, double *S, double *Cg,
-                           SweepShared<double, 128> &sw, int &inf_m) {
-    constexpr int N = 128, SS = 132;
-    auto Yv = [&](int i, int j) {
-        if (i >= n || j >= n) return 0.0;
-        return (USE == 1) ? Zb[i * n + j].y : -Zb[i * n + j].x;
-    };
-    auto Xv = [&](int i, int j) { return (USE == 1) ? Zb[i * n + j].x : Zb[i * n + j].y; };
-    double acc[WT<N>::MT][WT<N>::NT][2];
-    B128_TL(2);
-    // a3: C = X^{-1} Y -> Cg   (two 64-row halves to bound register use)
-    for (int h = 0; h < 2; ++h) {
-        cta_mma_f<N>([&](int r, int k) { return S[r * SS + k]; }, Yv, acc, 64 * h);
-        cta_mma_foreach<N>(acc, [&](int i, int j, double v) {
-            if (i < n && j < n) Cg[i * n + j] = v;
-        }, 64 * h);
-    }
-    __syncthreads();
-    B128_TL(3);
-    // a4: M = X + Y C -> S
-    for (int h = 0; h < 2; ++h) {
-        cta_mma_f<N>(Yv, [&](int k, int c) { return (k < n && c < n) ? Cg[k * n + c] : 0.0; }, acc, 64 * h);
-        cta_mma_foreach<N>(acc, [&](int i, int j, double v) { S[i * SS + j] = (i < n && j < n) ? Xv(i, j) + v : 0.0; },
-                           64 * h);
-    }
-    __syncthreads();
-    B128_TL(4);
-    // a5: Re = M^{-1} -> S
-    {
-        double a[R128][B128];
-        double pmax, pmin;
-        load_blocks_f<double, N, R128, B128>(a, n, [&](int i, int j) { return S[i * SS + j]; });
-        gj_sweep<double, N, R128, B128>(a, n, sw, pmax, pmin);
-        inf_m = sweep_info<double, N>(sw, n, pmax);
-        sweep_store<double, N, R128, B128>(a, sw, S, SS);
-    }
-    __syncthreads();
-    B128_TL(5);
-    // a6/a7: Im = -C Re, interleaved store (after every warp has finished reading its C rows)
-    auto out = [&](int i, int j, double v) {
-        if (i < n && j < n) {
-            const double re = S[i * SS + j];
-            Xb[i * n + j] = (USE == 1) ? make_double2(re, -v) : make_double2(-v, -re);
-        }
-    };
-    for (int h = 0; h < 2; ++h) {
-        cta_mma_f<N>([&](int r, int k) { return (r < n && k < n) ? Cg[r * n + k] : 0.0; },
-                     [&](int k, int c) { return S[k * SS + c]; }, acc, 64 * h);
-        __syncthreads();
-        cta_mma_foreach<N>(acc, out, 64 * h);
-    }
-    B128_TL(6);
+FROB_DEV void nbar_sync(int id, int cnt) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
+FROB_DEV void nbar_arrive(int id, int cnt) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
+
+// accumulator element (i, j, e) of warp w: row 32 (w >> 2) + 8 i + g, column 32 (w & 3) + 8 j + 2 t + e
+template <typename F>
+FROB_DEV void gj128_load(double (&a)[4][4][2], int n, F f) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r0 = 32 * (warp >> 2) + (lane >> 2), c0 = 32 * (warp & 3) + 2 * (lane & 3);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int r = r0 + 8 * i, c = c0 + 8 * j + e;
+                a[i][j][e] = (r < n && c < n) ? f(r, c) : (r == c ? 1.0 : 0.0);
+            }
 }
 
-__global__ void __launch_bounds__(T128, 1)
+FROB_DEV void gj128_store(const double (&a)[4][4][2], const SweepShared<double, 128> &sh, double *M, int ldm) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r0 = 32 * (warp >> 2) + (lane >> 2), c0 = 32 * (warp & 3) + 2 * (lane & 3);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int orow = sh.pos[r0 + 8 * i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) M[orow * ldm + sh.pivrow[c0 + 8 * j + e]] = a[i][j][e];
+    }
+}
+
+// max absolute row sum of the sweep result (rows < n); scratch >= 32 doubles
+FROB_DEV double gj128_norm_inf(const double (&a)[4][4][2], int n, double *part, double *scratch) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r0 = 32 * (warp >> 2) + (lane >> 2);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        double sum = 0.0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sum += fabs(a[i][j][0]) + fabs(a[i][j][1]);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+        sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+        if ((lane & 3) == 0) part[(warp & 3) * 128 + r0 + 8 * i] = sum;
+    }
+    __syncthreads();
+    double m = 0.0;
+    const int r = threadIdx.x;
+    if (r < n) m = ((part[r] + part[128 + r]) + part[256 + r]) + part[384 + r];
+    return block_max(m, scratch, G8_T);
+}
+
+// The panel warp's LU factorisation of panel b: lane l holds rows l + 32 q (q < 4), panel column c
+// in p[q][c >> 1][c & 1]; umask = my rows already used as pivots (earlier panels' pivot rows are
+// ordinary rows here, as in the exchange form).  Per column the owner lane of the pivot row
+// publishes it through shared memory; the chain is branch-free.  Beside it, lanes 0..7 build the
+// rows of U11^-1 and lanes 8..15 the columns of L11^-1, one column / row per step.
+FROB_DEV void g8_panel(double (&p)[4][4][2], int b, int n, unsigned &umask, SweepShared<double, 128> &sh,
+                       G8Shared &gs) {
+    const int lane = threadIdx.x & 31, par = b & 1;
+    double *pb = gs.pb[par];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const double2 v = *reinterpret_cast<const double2 *>(&pb[(lane + 32 * q) * G8_PS + 2 * h]);
+            p[q][h][0] = v.x;
+            p[q][h][1] = v.y;
+        }
+    if (b >= 2 && lane < G8_W) gs.rowslot[par][gs.prow[par][lane]] = -1;
+    unsigned pmask = 0;                 // my rows pivoted in this panel (they hold U rows from then on)
+    const bool urole = lane < G8_W;     // lanes 0..7: row `lane` of U11^-1; 8..15: column lane-8 of L11^-1
+    const int ti = lane & (G8_W - 1);
+    double tr[G8_W];
+#pragma unroll
+    for (int j = 0; j < G8_W; ++j) tr[j] = 0.0;
+    bstatic_for<G8_W>([&](auto cc) {
+        constexpr int c = decltype(cc)::value;
+        const int k = b * G8_W + c;
+        // candidates, branch-free: key 0 = not eligible; first max (rows l + 32 q grow with q)
+        unsigned long long kq[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int r = lane + 32 * q;
+            const bool el = !((umask >> q) & 1u) && ((r < n) == (k < n));
+            kq[q] = el ? pkey_bits(p[q][c >> 1][c & 1]) : 0ull;
+        }
+        const bool s01 = kq[1] > kq[0], s23 = kq[3] > kq[2];
+        const unsigned long long k01 = s01 ? kq[1] : kq[0], k23 = s23 ? kq[3] : kq[2];
+        const bool s = k23 > k01;
+        const unsigned long long bk = s ? k23 : k01;
+        const int qb = s ? (s23 ? 3 : 2) : (s01 ? 1 : 0);
+        const unsigned hi = (unsigned)(bk >> 32), lo32 = (unsigned)bk;
+        const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo32 : 0u);
+        const int pr = (int)__reduce_min_sync(0xffffffffu, (bk != 0ull && hi == mh && lo32 == ml)
+                                                                 ? (unsigned)(lane + 32 * qb) : 0xffffffffu);
+        const int qp = pr >> 5;
+        const bool me = (lane == (pr & 31));
+        double vq = p[0][c >> 1][c & 1];
+        vq = (qp == 1) ? p[1][c >> 1][c & 1] : vq;
+        vq = (qp == 2) ? p[2][c >> 1][c & 1] : vq;
+        vq = (qp == 3) ? p[3][c >> 1][c & 1] : vq;
+        const double piv = __shfl_sync(0xffffffffu, vq, pr & 31);
+        // the pivot row (multipliers in columns < c, U in columns >= c) -> shared, by its owner
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (me && qp == q) {
+#pragma unroll
+                for (int h = 0; h < G8_W / 2; ++h)
+                    *reinterpret_cast<double2 *>(&gs.lu[c * G8_W + 2 * h]) = make_double2(p[q][h][0], p[q][h][1]);
+            }
+        const unsigned bit = me ? (1u << qp) : 0u;
+        pmask |= bit;
+        umask |= bit;
+        const double ip = (piv == 0.0) ? 0.0 : frcp(piv);
+        if (lane == 0) {
+            gs.rpiv[c] = ip;
+            sh.pivrow[k] = pr;
+            sh.pmag_k[k] = fabs(piv);
+            gs.prow[par][c] = pr;
+            gs.rowslot[par][pr] = (signed char)c;
+        }
+        __syncwarp();
+        double u[G8_W];
+#pragma unroll
+        for (int c2 = c + 1; c2 < G8_W; ++c2) u[c2] = gs.lu[c * G8_W + c2];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const bool up = !((pmask >> q) & 1u);
+            const double m = p[q][c >> 1][c & 1] * ip;
+            const double mm = up ? m : 0.0;
+            p[q][c >> 1][c & 1] = up ? m : p[q][c >> 1][c & 1];
+#pragma unroll
+            for (int c2 = c + 1; c2 < G8_W; ++c2) p[q][c2 >> 1][c2 & 1] = fma(-mm, u[c2], p[q][c2 >> 1][c2 & 1]);
+        }
+        // U11^-1 (Uinv U = I, column c: Uinv[i][c] = -(sum_{k<c} Uinv[i][k] U[k][c]) / u_cc) and
+        // L11^-1 (L Linv = I, row c: Linv[c][j] = delta_cj - sum_{i<c} L[c][i] Linv[i][j])
+        {
+            double acc = 0.0;
+#pragma unroll
+            for (int i = 0; i < c; ++i) acc = fma(tr[i], urole ? gs.lu[i * G8_W + c] : gs.lu[c * G8_W + i], acc);
+            tr[c] = urole ? ((ti == c) ? ip : (ti < c ? -acc * ip : 0.0)) : ((ti == c ? 1.0 : 0.0) - acc);
+        }
+    });
+    if (lane < 2 * G8_W) {
+#pragma unroll
+        for (int j = 0; j < G8_W; ++j) {
+            if (urole) gs.uinv[ti * G8_W + j] = tr[j];
+            else gs.linv[j * G8_W + ti] = tr[j];
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+            *reinterpret_cast<double2 *>(&pb[(lane + 32 * q) * G8_PS + 2 * h]) = make_double2(p[q][h][0], p[q][h][1]);
+    __syncwarp();
+}
+
+// rows 8 w .. 8 w + 7 of the swept panel (warp w, after the hand-off): X L11^-1 with X = -(multipliers)
+// for a non-pivot row and X = row c of U11^-1 for pivot row p_c  (two DMMA)
+FROB_DEV void g8_form_panel(G8Shared &gs, int par, int warp, int lane) {
+    const int g = lane >> 2, t = lane & 3, r = 8 * warp + g;
+    const double *pb = gs.pb[par];
+    const int sl = gs.rowslot[par][r];
+    const double a0 = (sl >= 0) ? gs.uinv[sl * G8_W + t] : -pb[r * G8_PS + t];
+    const double a1 = (sl >= 0) ? gs.uinv[sl * G8_W + 4 + t] : -pb[r * G8_PS + 4 + t];
+    double d0 = 0.0, d1 = 0.0;
+    dmma(d0, d1, a0, gs.linv[t * G8_W + g]);
+    dmma(d0, d1, a1, gs.linv[(4 + t) * G8_W + g]);
+    *reinterpret_cast<double2 *>(&gs.pf[par][r * G8_PS + 2 * t]) = make_double2(d0, d1);
+}
+
+FROB_DEV void gj128_sweep(double (&a)[4][4][2], int n, SweepShared<double, 128> &sh, G8Shared &gs, double &pmax,
+                          double &pmin) {
+    constexpr int NP = 128 / G8_W;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform for the compiler
+    const int g = lane >> 2, t = lane & 3;
+    const int wc = warp & 3, r0 = 32 * (warp >> 2) + g;
+    const bool pw = (warp == G8_PW);
+    unsigned umask = 0;
+    for (int i = tid; i < 2 * 128; i += G8_T) (&gs.rowslot[0][0])[i] = -1;
+    __syncthreads();
+    // threads meeting at the panel-b hand-over: its four owner warps (+ the panel warp)
+    auto panel_cnt = [](int b) { return ((b >> 2) == (G8_PW & 3)) ? 128 : 160; };
+    auto hand_over = [&](int b, int jb) {  // my tiles of column block jb (panel b) -> panel buffer
+        double *pb = gs.pb[b & 1];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j == jb) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    *reinterpret_cast<double2 *>(&pb[(r0 + 8 * i) * G8_PS + 2 * t]) = make_double2(a[i][j][0], a[i][j][1]);
+            }
+        if (!pw) nbar_arrive(G8_BAR_PANEL, panel_cnt(b));
+    };
+    auto run_panel = [&](int b) {  // panel warp: park my tiles, factor panel b, signal, restore
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) gs.park[(i * 8 + j * 2 + e) * 32 + lane] = a[i][j][e];
+        nbar_sync(G8_BAR_PANEL, panel_cnt(b));
+        g8_panel(a, b, n, umask, sh, gs);
+        nbar_arrive(G8_BAR_FACT, G8_T);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) a[i][j][e] = gs.park[(i * 8 + j * 2 + e) * 32 + lane];
+    };
+    if (wc == 0) hand_over(0, 0);
+    if (pw) run_panel(0);
+    for (int b = 0; b < NP; ++b) {
+        const int par = b & 1, jb = b & 3;
+        const bool bown = (wc == (b >> 2));
+        const int b1 = b + 1, j1 = b1 & 3;
+        const bool nown = (b1 < NP) && (wc == (b1 >> 2));
+        if (!pw) nbar_sync(G8_BAR_FACT, G8_T);
+        const double *pb = gs.pb[par];
+        double *tb = gs.tb[par];
+        double *tv = gs.tv;
+        g8_form_panel(gs, par, warp, lane);
+        // T: my part of the panel's pivot rows, before the update
+        int slot[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            slot[i] = gs.rowslot[par][r0 + 8 * i];
+            if (slot[i] >= 0) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    *reinterpret_cast<double2 *>(&tb[slot[i] * G8_TS + 32 * wc + 8 * j + 2 * t]) =
+                        make_double2(a[i][j][0], a[i][j][1]);
+            }
+        }
+        nbar_sync(G8_BAR_U, G8_T);
+        // W = L11^-1 T (forward), V = U11^-1 W (back substitution): one column per thread of warps 0..3
+        if (tid < 128) {
+            double w[G8_W], v[G8_W];
+#pragma unroll
+            for (int c = 0; c < G8_W; ++c) {
+                double s = tb[c * G8_TS + tid];
+#pragma unroll
+                for (int i = 0; i < c; ++i) s = fma(-gs.lu[c * G8_W + i], w[i], s);
+                w[c] = s;
+            }
+#pragma unroll
+            for (int c = G8_W - 1; c >= 0; --c) {
+                double s = w[c];
+#pragma unroll
+                for (int i = c + 1; i < G8_W; ++i) s = fma(-gs.lu[c * G8_W + i], v[i], s);
+                v[c] = s * gs.rpiv[c];
+            }
+#pragma unroll
+            for (int c = 0; c < G8_W; ++c) {
+                tb[c * G8_TS + tid] = w[c];
+                tv[c * G8_TS + tid] = v[c];
+            }
+        }
+        nbar_sync(G8_BAR_U, G8_T);
+        // A fragments: -(multipliers) for the rows outside the panel's pivots, 0 for those
+        double pa[4][2];
+        auto load_pa = [&]() {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const bool pv = gs.rowslot[par][r0 + 8 * i] >= 0;
+                pa[i][0] = pv ? 0.0 : -pb[(r0 + 8 * i) * G8_PS + t];
+                pa[i][1] = pv ? 0.0 : -pb[(r0 + 8 * i) * G8_PS + 4 + t];
+            }
+        };
+        auto upd = [&](auto jj) {
+            constexpr int j = decltype(jj)::value;
+            const double t0 = tb[t * G8_TS + 32 * wc + 8 * j + g];
+            const double t1 = tb[(4 + t) * G8_TS + 32 * wc + 8 * j + g];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                dmma(a[i][j][0], a[i][j][1], pa[i][0], t0);
+                dmma(a[i][j][0], a[i][j][1], pa[i][1], t1);
+                if (slot[i] >= 0) {
+                    const double2 v = *reinterpret_cast<const double2 *>(&tv[slot[i] * G8_TS + 32 * wc + 8 * j + 2 * t]);
+                    a[i][j][0] = v.x;
+                    a[i][j][1] = v.y;
+                }
+            }
+        };
+        load_pa();
+        if (nown) {  // the next panel's columns first
+            bstatic_for<4>([&](auto jj) {
+                if (decltype(jj)::value == j1) upd(jj);
+            });
+            hand_over(b1, j1);
+        }
+        if (pw && b1 < NP) {
+            run_panel(b1);
+            load_pa();
+        }
+        bstatic_for<4>([&](auto jj) {
+            constexpr int j = decltype(jj)::value;
+            if (!(bown && j == jb) && !(nown && j == j1)) upd(jj);
+        });
+        if (bown) {
+            const double *pf = gs.pf[par];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (j == jb) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const double2 v = *reinterpret_cast<const double2 *>(&pf[(r0 + 8 * i) * G8_PS + 2 * t]);
+                        a[i][j][0] = v.x;
+                        a[i][j][1] = v.y;
+                    }
+                }
+        }
+    }
+    __syncthreads();
+    sweep_finish<double, 128, G8_T>(sh, n, pmax, pmin);
+}
+
+// Planar operand views of the interleaved input: part 0 = Re Z = A, part 1 = Im Z = B.
+FROB_DEV double zpart(const double *Zd, int n, int part, int i, int j) { return Zd[2 * (i * n + j) + part]; }
+
+// One copy of each step in the kernel (the part in use, its sign and the output layout are runtime
+// values): the unrolled sweep and GEMM bodies are large.
+__global__ void __launch_bounds__(G8_T, 1)
 frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__restrict__ X, long long sX, int n,
                        int branch, int *__restrict__ info, unsigned char *__restrict__ bused) {
     constexpr int N = 128, SS = 132;
@@ -651,52 +953,103 @@ frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
     double *S = sm.S;
     const int tid = threadIdx.x;
     const long long b = blockIdx.x;
-    const double2 *Zb = Z + b * sZ;
+    const double *Zd = reinterpret_cast<const double *>(Z + b * sZ);
     double2 *Xb = X + b * sX;
     // scratch: planar C (n x n) in the SECOND half of the output matrix, so the final
     // epilogue for rows < 64 (bytes [0, 1024 n)) never clobbers C rows >= 64 (n >= 64)
     double *Cg = reinterpret_cast<double *>(Xb) + (long long)n * n;
 
     int use = (branch == FROB_BRANCH_B) ? 2 : 1;
-    int inf_x;
+    int inf_x = 0, inf_m = 0;
+    double ka = 0.0;
     B128_TL(0);
-    {
-        double a[R128][B128];
+    // pass 0: X^{-1} of the part in use; pass 1 (AUTO, reading R1'): the other part; pass 2: M^{-1}
+    for (int pass = 0;;) {
+        double a[4][4][2];
         double pmax, pmin;
-        if (use == 1) load_blocks_f<double, N, R128, B128>(a, n, [&](int i, int j) { return Zb[i * n + j].x; });
-        else load_blocks_f<double, N, R128, B128>(a, n, [&](int i, int j) { return Zb[i * n + j].y; });
-        B128_TL(7);
-        gj_sweep<double, N, R128, B128>(a, n, sm.sw, pmax, pmin);
-        inf_x = sweep_info<double, N>(sm.sw, n, pmax);
-        sweep_store<double, N, R128, B128>(a, sm.sw, S, SS);
-        B128_TL(1);
-        if (branch == FROB_BRANCH_AUTO) {
-            // reading R1' (see frob_batched_kernel)
-            const double na = mat_norm_inf(n, [&](int i, int j) { return Zb[i * n + j].x; }, sm.sw.pmag_k, T128);
-            const double ka = inf_x ? INFINITY : na * reg_norm_inf<N, R128, B128>(a, n, sm.sw.pmag_k);
-            if (inf_x != 0 || !(ka <= kappa_switch(n))) {
-                __syncthreads();
-                load_blocks_f<double, N, R128, B128>(a, n, [&](int i, int j) { return Zb[i * n + j].y; });
-                double qmax, qmin;
-                gj_sweep<double, N, R128, B128>(a, n, sm.sw, qmax, qmin);
-                const int inf_b = sweep_info<double, N>(sm.sw, n, qmax);
-                const double nb = mat_norm_inf(n, [&](int i, int j) { return Zb[i * n + j].y; }, sm.sw.pmag_k, T128);
-                const double kb = inf_b ? INFINITY : nb * reg_norm_inf<N, R128, B128>(a, n, sm.sw.pmag_k);
-                if (inf_b == 0 && (inf_x != 0 || kb < ka)) {
-                    use = 2;
-                    inf_x = 0;
+        const int xpart = (pass == 0) ? use - 1 : 2 - use;  // the part swept in passes 0 / 1
+        if (pass < 2) gj128_load(a, n, [&](int i, int j) { return zpart(Zd, n, xpart, i, j); });
+        else gj128_load(a, n, [&](int i, int j) { return S[i * SS + j]; });
+        gj128_sweep(a, n, sm.sw, sm.gs, pmax, pmin);
+        const int inf = sweep_info<double, N>(sm.sw, n, pmax);
+        if (pass == 2) {
+            inf_m = inf;
+            gj128_store(a, sm.sw, S, SS);
+            break;
+        }
+        if (pass == 0) {
+            inf_x = inf;
+            gj128_store(a, sm.sw, S, SS);
+            B128_TL(1);
+            if (branch == FROB_BRANCH_AUTO) {
+                const double na = mat_norm_inf(n, [&](int i, int j) { return zpart(Zd, n, 0, i, j); }, sm.sw.pmag_k, G8_T);
+                ka = inf_x ? INFINITY : na * gj128_norm_inf(a, n, sm.gs.park, sm.sw.pmag_k);
+                if (inf_x != 0 || !(ka <= kappa_switch(n))) {
                     __syncthreads();
-                    sweep_store<double, N, R128, B128>(a, sm.sw, S, SS);
-                } else if (inf_b != 0 && inf_x != 0) {
-                    inf_x = -1;
+                    pass = 1;
+                    continue;
                 }
             }
+        } else {
+            const int inf_b = inf;
+            const double nb = mat_norm_inf(n, [&](int i, int j) { return zpart(Zd, n, 1, i, j); }, sm.sw.pmag_k, G8_T);
+            const double kb = inf_b ? INFINITY : nb * gj128_norm_inf(a, n, sm.gs.park, sm.sw.pmag_k);
+            if (inf_b == 0 && (inf_x != 0 || kb < ka)) {
+                use = 2;
+                inf_x = 0;
+                __syncthreads();
+                gj128_store(a, sm.sw, S, SS);
+            } else if (inf_b != 0 && inf_x != 0) {
+                inf_x = -1;
+            }
         }
+        __syncthreads();
+        // X = part use-1, Y = sgn * part 2-use (S2: Y = -A)
+        const int xp = use - 1, yp = 2 - use;
+        const double sgn = (use == 1) ? 1.0 : -1.0;
+        auto Yv = [&](int i, int j) { return (i < n && j < n) ? sgn * zpart(Zd, n, yp, i, j) : 0.0; };
+        double acc[WT<N>::MT][WT<N>::NT][2];
+        B128_TL(2);
+        // a3: C = X^{-1} Y -> Cg   (two 64-row halves to bound register use)
+        for (int h = 0; h < 2; ++h) {
+            cta_mma_f<N>([&](int r, int k) { return S[r * SS + k]; }, Yv, acc, 64 * h);
+            cta_mma_foreach<N>(acc, [&](int i, int j, double v) {
+                if (i < n && j < n) Cg[i * n + j] = v;
+            }, 64 * h);
+        }
+        __syncthreads();
+        B128_TL(3);
+        // a4: M = X + Y C -> S
+        for (int h = 0; h < 2; ++h) {
+            cta_mma_f<N>(Yv, [&](int k, int c) { return (k < n && c < n) ? Cg[k * n + c] : 0.0; }, acc, 64 * h);
+            cta_mma_foreach<N>(acc, [&](int i, int j, double v) {
+                S[i * SS + j] = (i < n && j < n) ? zpart(Zd, n, xp, i, j) + v : 0.0;
+            }, 64 * h);
+        }
+        __syncthreads();
+        B128_TL(4);
+        pass = 2;
     }
     __syncthreads();
-    int inf_m = 0;
-    if (use == 1) frob128_rest<1>(Zb, Xb, n, S, Cg, sm.sw, inf_m);
-    else frob128_rest<2>(Zb, Xb, n, S, Cg, sm.sw, inf_m);
+    B128_TL(5);
+    // a6/a7: Im = -C Re, interleaved store (after every warp has finished reading its C rows)
+    {
+        double acc[WT<N>::MT][WT<N>::NT][2];
+        const bool s1 = (use == 1);
+        auto out = [&](int i, int j, double v) {
+            if (i < n && j < n) {
+                const double re = S[i * SS + j];
+                Xb[i * n + j] = s1 ? make_double2(re, -v) : make_double2(-v, -re);
+            }
+        };
+        for (int h = 0; h < 2; ++h) {
+            cta_mma_f<N>([&](int r, int k) { return (r < n && k < n) ? Cg[r * n + k] : 0.0; },
+                         [&](int k, int c) { return S[k * SS + c]; }, acc, 64 * h);
+            __syncthreads();
+            cta_mma_foreach<N>(acc, out, 64 * h);
+        }
+    }
+    B128_TL(6);
     if (tid == 0) {
         info[b] = (inf_x < 0) ? 1 : (inf_x ? inf_x : inf_m);
         if (bused) bused[b] = (inf_x < 0) ? 0 : (unsigned char)use;
@@ -983,7 +1336,7 @@ frob_status frob_inv_batched(int n, int batch, const double *Z, long long stride
         if ((e = set_smem(frob_batched128_kernel, smem)) != cudaSuccess) return FROB_ERR_CUDA;
         count_launch();
         ProfScope ps("frob_batched128", s, 10.0 * n * (double)n * n * batch);
-        frob_batched128_kernel<<<batch, T128, smem, s>>>(Zc, strideZ, Xc, strideX, n, branch, d_info,
+        frob_batched128_kernel<<<batch, G8_T, smem, s>>>(Zc, strideZ, Xc, strideX, n, branch, d_info,
                                                          d_branch_used);
     }
     return cudaGetLastError() == cudaSuccess ? FROB_OK : FROB_ERR_CUDA;
