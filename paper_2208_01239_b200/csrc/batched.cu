@@ -600,7 +600,6 @@ constexpr int G8_TS = 132;               // T / W / V buffer row stride
 constexpr int G8_BAR_U = 1, G8_BAR_PANEL = 2, G8_BAR_FACT = 3;  // named barriers (0 = __syncthreads)
 struct G8Shared {
     double pb[2][128 * G8_PS];   // panel b: handed to the panel warp, then its LU form (multipliers / U rows)
-    double pf[2][128 * G8_PS];   // panel b swept (A_IK, A_RK above)
     double tb[2][G8_W * G8_TS];  // T = the pivot rows (old), then W
     double tv[G8_W * G8_TS];     // V (written after, read before a U barrier: one buffer)
     double park[32 * 32];        // the panel warp's own tiles while it factors a panel; norm row sums
@@ -672,8 +671,7 @@ FROB_DEV double gj128_norm_inf(const double (&a)[4][4][2], int n, double *part, 
 // The panel warp's LU factorisation of panel b: lane l holds rows l + 32 q (q < 4), panel column c
 // in p[q][c >> 1][c & 1]; umask = my rows already used as pivots (earlier panels' pivot rows are
 // ordinary rows here, as in the exchange form).  Per column the owner lane of the pivot row
-// publishes it through shared memory; the chain is branch-free.  Beside it, lanes 0..7 build the
-// rows of U11^-1 and lanes 8..15 the columns of L11^-1, one column / row per step.
+// publishes it through shared memory; the chain is branch-free.
 FROB_DEV void g8_panel(double (&p)[4][4][2], int b, int n, unsigned &umask, SweepShared<double, 128> &sh,
                        G8Shared &gs) {
     const int lane = threadIdx.x & 31, par = b & 1;
@@ -688,11 +686,6 @@ FROB_DEV void g8_panel(double (&p)[4][4][2], int b, int n, unsigned &umask, Swee
         }
     if (b >= 2 && lane < G8_W) gs.rowslot[par][gs.prow[par][lane]] = -1;
     unsigned pmask = 0;                 // my rows pivoted in this panel (they hold U rows from then on)
-    const bool urole = lane < G8_W;     // lanes 0..7: row `lane` of U11^-1; 8..15: column lane-8 of L11^-1
-    const int ti = lane & (G8_W - 1);
-    double tr[G8_W];
-#pragma unroll
-    for (int j = 0; j < G8_W; ++j) tr[j] = 0.0;
     bstatic_for<G8_W>([&](auto cc) {
         constexpr int c = decltype(cc)::value;
         const int k = b * G8_W + c;
@@ -753,22 +746,7 @@ FROB_DEV void g8_panel(double (&p)[4][4][2], int b, int n, unsigned &umask, Swee
 #pragma unroll
             for (int c2 = c + 1; c2 < G8_W; ++c2) p[q][c2 >> 1][c2 & 1] = fma(-mm, u[c2], p[q][c2 >> 1][c2 & 1]);
         }
-        // U11^-1 (Uinv U = I, column c: Uinv[i][c] = -(sum_{k<c} Uinv[i][k] U[k][c]) / u_cc) and
-        // L11^-1 (L Linv = I, row c: Linv[c][j] = delta_cj - sum_{i<c} L[c][i] Linv[i][j])
-        {
-            double acc = 0.0;
-#pragma unroll
-            for (int i = 0; i < c; ++i) acc = fma(tr[i], urole ? gs.lu[i * G8_W + c] : gs.lu[c * G8_W + i], acc);
-            tr[c] = urole ? ((ti == c) ? ip : (ti < c ? -acc * ip : 0.0)) : ((ti == c ? 1.0 : 0.0) - acc);
-        }
     });
-    if (lane < 2 * G8_W) {
-#pragma unroll
-        for (int j = 0; j < G8_W; ++j) {
-            if (urole) gs.uinv[ti * G8_W + j] = tr[j];
-            else gs.linv[j * G8_W + ti] = tr[j];
-        }
-    }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
@@ -777,18 +755,26 @@ FROB_DEV void g8_panel(double (&p)[4][4][2], int b, int n, unsigned &umask, Swee
     __syncwarp();
 }
 
-// rows 8 w .. 8 w + 7 of the swept panel (warp w, after the hand-off): X L11^-1 with X = -(multipliers)
-// for a non-pivot row and X = row c of U11^-1 for pivot row p_c  (two DMMA)
-FROB_DEV void g8_form_panel(G8Shared &gs, int par, int warp, int lane) {
-    const int g = lane >> 2, t = lane & 3, r = 8 * warp + g;
-    const double *pb = gs.pb[par];
-    const int sl = gs.rowslot[par][r];
-    const double a0 = (sl >= 0) ? gs.uinv[sl * G8_W + t] : -pb[r * G8_PS + t];
-    const double a1 = (sl >= 0) ? gs.uinv[sl * G8_W + 4 + t] : -pb[r * G8_PS + 4 + t];
-    double d0 = 0.0, d1 = 0.0;
-    dmma(d0, d1, a0, gs.linv[t * G8_W + g]);
-    dmma(d0, d1, a1, gs.linv[(4 + t) * G8_W + g]);
-    *reinterpret_cast<double2 *>(&gs.pf[par][r * G8_PS + 2 * t]) = make_double2(d0, d1);
+// U11^-1 (Uinv U = I, column by column: Uinv[i][c] = -(sum_{k<c} Uinv[i][k] U[k][c]) / u_cc) by
+// threads 0..7 (row i = thread) and L11^-1 (L Linv = I, row by row: Linv[c][j] = delta_cj -
+// sum_{i<c} L[c][i] Linv[i][j]) by threads 8..15 (column j = thread - 8), from the LU-form pivot rows
+FROB_DEV void g8_tri_inverses(G8Shared &gs, int ti) {
+    const bool urole = ti < G8_W;
+    const int r = ti & (G8_W - 1);
+    double tr[G8_W];
+#pragma unroll
+    for (int c = 0; c < G8_W; ++c) {
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < c; ++i) acc = fma(tr[i], urole ? gs.lu[i * G8_W + c] : gs.lu[c * G8_W + i], acc);
+        const double ip = gs.rpiv[c];
+        tr[c] = urole ? ((r == c) ? ip : (r < c ? -acc * ip : 0.0)) : ((r == c ? 1.0 : 0.0) - acc);
+    }
+#pragma unroll
+    for (int j = 0; j < G8_W; ++j) {
+        if (urole) gs.uinv[r * G8_W + j] = tr[j];
+        else gs.linv[j * G8_W + r] = tr[j];
+    }
 }
 
 FROB_DEV void gj128_sweep(double (&a)[4][4][2], int n, SweepShared<double, 128> &sh, G8Shared &gs, double &pmax,
@@ -843,7 +829,6 @@ FROB_DEV void gj128_sweep(double (&a)[4][4][2], int n, SweepShared<double, 128> 
         const double *pb = gs.pb[par];
         double *tb = gs.tb[par];
         double *tv = gs.tv;
-        g8_form_panel(gs, par, warp, lane);
         // T: my part of the panel's pivot rows, before the update
         int slot[4];
 #pragma unroll
@@ -857,7 +842,9 @@ FROB_DEV void gj128_sweep(double (&a)[4][4][2], int n, SweepShared<double, 128> 
             }
         }
         nbar_sync(G8_BAR_U, G8_T);
-        // W = L11^-1 T (forward), V = U11^-1 W (back substitution): one column per thread of warps 0..3
+        // W = L11^-1 T (forward), V = U11^-1 W (back substitution): one column per thread of warps
+        // 0..3; meanwhile 16 threads of warp 4 form U11^-1 and L11^-1
+        if (tid >= 128 && tid < 128 + 2 * G8_W) g8_tri_inverses(gs, tid - 128);
         if (tid < 128) {
             double w[G8_W], v[G8_W];
 #pragma unroll
@@ -922,15 +909,22 @@ FROB_DEV void gj128_sweep(double (&a)[4][4][2], int n, SweepShared<double, 128> 
             if (!(bown && j == jb) && !(nown && j == j1)) upd(jj);
         });
         if (bown) {
-            const double *pf = gs.pf[par];
+            // my rows of the swept panel, straight into the accumulators: X L11^-1 with X = -(multipliers)
+            // for a non-pivot row and X = row c of U11^-1 for pivot row p_c (two DMMA per tile)
+            const double l0 = gs.linv[t * G8_W + g], l1 = gs.linv[(4 + t) * G8_W + g];
+            const int ra = 32 * (warp >> 2);
 #pragma unroll
             for (int j = 0; j < 4; ++j)
                 if (j == jb) {
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        const double2 v = *reinterpret_cast<const double2 *>(&pf[(r0 + 8 * i) * G8_PS + 2 * t]);
-                        a[i][j][0] = v.x;
-                        a[i][j][1] = v.y;
+                        const int r = ra + 8 * i + g;  // the A-fragment row of this lane
+                        const int sl = gs.rowslot[par][r];
+                        const double x0 = (sl >= 0) ? gs.uinv[sl * G8_W + t] : -pb[r * G8_PS + t];
+                        const double x1 = (sl >= 0) ? gs.uinv[sl * G8_W + 4 + t] : -pb[r * G8_PS + 4 + t];
+                        a[i][j][0] = a[i][j][1] = 0.0;
+                        dmma(a[i][j][0], a[i][j][1], x0, l0);
+                        dmma(a[i][j][0], a[i][j][1], x1, l1);
                     }
                 }
         }
