@@ -1002,24 +1002,29 @@ frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
         const int xp = use - 1, yp = 2 - use;
         const double sgn = (use == 1) ? 1.0 : -1.0;
         auto Yv = [&](int i, int j) { return (i < n && j < n) ? sgn * zpart(Zd, n, yp, i, j) : 0.0; };
-        double acc[WT<N>::MT][WT<N>::NT][2];
+        double acc0[WT<N>::MT][WT<N>::NT][2], acc1[WT<N>::MT][WT<N>::NT][2];
         B128_TL(2);
-        // a3: C = X^{-1} Y -> Cg   (two 64-row halves to bound register use)
-        for (int h = 0; h < 2; ++h) {
-            cta_mma_f<N>([&](int r, int k) { return S[r * SS + k]; }, Yv, acc, 64 * h);
-            cta_mma_foreach<N>(acc, [&](int i, int j, double v) {
-                if (i < n && j < n) Cg[i * n + j] = v;
-            }, 64 * h);
-        }
+        // a3: C = X^{-1} Y (both 64-row halves in registers), then C -> S (X^{-1} is done) and -> Cg
+        cta_mma_f<N>([&](int r, int k) { return S[r * SS + k]; }, Yv, acc0, 0);
+        cta_mma_f<N>([&](int r, int k) { return S[r * SS + k]; }, Yv, acc1, 64);
+        __syncthreads();
+        auto put_c = [&](int i, int j, double v) {
+            S[i * SS + j] = v;  // zero in the padding (Y is)
+            if (i < n && j < n) Cg[i * n + j] = v;
+        };
+        cta_mma_foreach<N>(acc0, put_c, 0);
+        cta_mma_foreach<N>(acc1, put_c, 64);
         __syncthreads();
         B128_TL(3);
-        // a4: M = X + Y C -> S
-        for (int h = 0; h < 2; ++h) {
-            cta_mma_f<N>(Yv, [&](int k, int c) { return (k < n && c < n) ? Cg[k * n + c] : 0.0; }, acc, 64 * h);
-            cta_mma_foreach<N>(acc, [&](int i, int j, double v) {
-                S[i * SS + j] = (i < n && j < n) ? zpart(Zd, n, xp, i, j) + v : 0.0;
-            }, 64 * h);
-        }
+        // a4: M = X + Y C with C from shared memory -> S
+        cta_mma_f<N>(Yv, [&](int k, int c) { return S[k * SS + c]; }, acc0, 0);
+        cta_mma_f<N>(Yv, [&](int k, int c) { return S[k * SS + c]; }, acc1, 64);
+        __syncthreads();
+        auto put_m = [&](int i, int j, double v) {
+            S[i * SS + j] = (i < n && j < n) ? zpart(Zd, n, xp, i, j) + v : 0.0;
+        };
+        cta_mma_foreach<N>(acc0, put_m, 0);
+        cta_mma_foreach<N>(acc1, put_m, 64);
         __syncthreads();
         B128_TL(4);
         pass = 2;
