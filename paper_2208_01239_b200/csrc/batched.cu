@@ -21,6 +21,12 @@
 
 namespace frob {
 
+// DMMA without `volatile`: the compiler may interleave independent tiles (the f64 mma's latency is long)
+FROB_DEV void dmma_s(double &c0, double &c1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+        : "+d"(c0), "+d"(c1)
+        : "d"(a), "d"(b));
+}
 FROB_DEV double fast_recip(double x) { return frcp(x); }
 FROB_DEV double2 fast_recip(double2 x) { return recip(x); }
 
@@ -362,7 +368,7 @@ FROB_DEV void cta_mma_f(FA fa, FB fb, double (&acc)[WT<N>::MT][WT<N>::NT][2], in
 #pragma unroll
         for (int i = 0; i < W::MT; ++i)
 #pragma unroll
-            for (int j = 0; j < W::NT; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+            for (int j = 0; j < W::NT; ++j) dmma_s(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
 }
 
@@ -574,8 +580,13 @@ __device__ long long g_b128_tl[16][8];
 extern "C" int frob_b128_tl_read(long long *h) {
     return (int)cudaMemcpyFromSymbol(h, g_b128_tl, sizeof(g_b128_tl));
 }
+// per-panel timeline of block 0's last sweep (plain stores, nothing waits on them)
+__device__ long long g_g8tl[16][6];
+#define G8_TL(b, slot) do { if ((threadIdx.x & 31) == 0 && blockIdx.x == 0) g_g8tl[(b) & 15][slot] = clock64(); } while (0)
+extern "C" int frob_g8_tl_read(long long *h) { return (int)cudaMemcpyFromSymbol(h, g_g8tl, sizeof(g_g8tl)); }
 #else
 #define B128_TL(i) do { } while (0)
+#define G8_TL(b, slot) do { } while (0)
 #endif
 
 // ----------------------------------------------------------------- blocked Gauss-Jordan, N = 128
@@ -601,12 +612,13 @@ constexpr int G8_BAR_U = 1, G8_BAR_PANEL = 2, G8_BAR_FACT = 3;  // named barrier
 struct G8Shared {
     double pb[2][128 * G8_PS];   // panel b: handed to the panel warp, then its LU form (multipliers / U rows)
     double tb[2][G8_W * G8_TS];  // T = the pivot rows (old), then W
-    double tv[G8_W * G8_TS];     // V (written after, read before a U barrier: one buffer)
+    double tw[G8_W * G8_TS];     // W (written after, read before a U barrier: one buffer)
+    double tv[G8_W * G8_TS];     // V
     double park[32 * 32];        // the panel warp's own tiles while it factors a panel; norm row sums
     double lu[G8_W * G8_W];      // the panel's pivot rows (L11 strictly below, U11 on / above the diagonal)
     double rpiv[G8_W];           // 1 / u_cc
-    double uinv[G8_W * G8_W];    // U11^-1
-    double linv[G8_W * G8_W];    // L11^-1 (unit lower)
+    double uinv[2][G8_W * G8_W]; // U11^-1 (by panel parity: the last owners of panel b read it while
+    double linv[2][G8_W * G8_W]; // L11^-1    panel b+1's are formed)
     int prow[2][G8_W];
     signed char rowslot[2][128];  // panel slot of a pivot row, -1 otherwise
 };
@@ -758,7 +770,7 @@ FROB_DEV void g8_panel(double (&p)[4][4][2], int b, int n, unsigned &umask, Swee
 // U11^-1 (Uinv U = I, column by column: Uinv[i][c] = -(sum_{k<c} Uinv[i][k] U[k][c]) / u_cc) by
 // threads 0..7 (row i = thread) and L11^-1 (L Linv = I, row by row: Linv[c][j] = delta_cj -
 // sum_{i<c} L[c][i] Linv[i][j]) by threads 8..15 (column j = thread - 8), from the LU-form pivot rows
-FROB_DEV void g8_tri_inverses(G8Shared &gs, int ti) {
+FROB_DEV void g8_tri_inverses(G8Shared &gs, int ti, int par) {
     const bool urole = ti < G8_W;
     const int r = ti & (G8_W - 1);
     double tr[G8_W];
@@ -772,8 +784,8 @@ FROB_DEV void g8_tri_inverses(G8Shared &gs, int ti) {
     }
 #pragma unroll
     for (int j = 0; j < G8_W; ++j) {
-        if (urole) gs.uinv[r * G8_W + j] = tr[j];
-        else gs.linv[j * G8_W + r] = tr[j];
+        if (urole) gs.uinv[par][r * G8_W + j] = tr[j];
+        else gs.linv[par][j * G8_W + r] = tr[j];
     }
 }
 
@@ -809,8 +821,10 @@ FROB_DEV void gj128_sweep(double (&a)[4][4][2], int n, SweepShared<double, 128> 
 #pragma unroll
                 for (int e = 0; e < 2; ++e) gs.park[(i * 8 + j * 2 + e) * 32 + lane] = a[i][j][e];
         nbar_sync(G8_BAR_PANEL, panel_cnt(b));
+        G8_TL(b, 0);
         g8_panel(a, b, n, umask, sh, gs);
         nbar_arrive(G8_BAR_FACT, G8_T);
+        G8_TL(b, 1);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -826,6 +840,7 @@ FROB_DEV void gj128_sweep(double (&a)[4][4][2], int n, SweepShared<double, 128> 
         const int b1 = b + 1, j1 = b1 & 3;
         const bool nown = (b1 < NP) && (wc == (b1 >> 2));
         if (!pw) nbar_sync(G8_BAR_FACT, G8_T);
+        if (warp == 0) G8_TL(b, 2);
         const double *pb = gs.pb[par];
         double *tb = gs.tb[par];
         double *tv = gs.tv;
@@ -841,33 +856,41 @@ FROB_DEV void gj128_sweep(double (&a)[4][4][2], int n, SweepShared<double, 128> 
                         make_double2(a[i][j][0], a[i][j][1]);
             }
         }
+        // meanwhile 16 threads of warp 4 form U11^-1 and L11^-1
+        if (tid >= 128 && tid < 128 + 2 * G8_W) g8_tri_inverses(gs, tid - 128, par);
+        if (warp == 4) G8_TL(b, 5);
         nbar_sync(G8_BAR_U, G8_T);
-        // W = L11^-1 T (forward), V = U11^-1 W (back substitution): one column per thread of warps
-        // 0..3; meanwhile 16 threads of warp 4 form U11^-1 and L11^-1
-        if (tid >= 128 && tid < 128 + 2 * G8_W) g8_tri_inverses(gs, tid - 128);
-        if (tid < 128) {
-            double w[G8_W], v[G8_W];
+        if (warp == 0) G8_TL(b, 3);
+        // W = L11^-1 T and V = U11^-1 W (2 + 2 DMMA per 8-column tile) by warps 0..3, one 32-column band each
+        if (warp < 4) {
+            double *tw = gs.tw;
+            const double l0 = gs.linv[par][g * G8_W + t], l1 = gs.linv[par][g * G8_W + 4 + t];
+            const double u0 = gs.uinv[par][g * G8_W + t], u1 = gs.uinv[par][g * G8_W + 4 + t];
+            double d[4][2];
 #pragma unroll
-            for (int c = 0; c < G8_W; ++c) {
-                double s = tb[c * G8_TS + tid];
-#pragma unroll
-                for (int i = 0; i < c; ++i) s = fma(-gs.lu[c * G8_W + i], w[i], s);
-                w[c] = s;
+            for (int j = 0; j < 4; ++j) {
+                d[j][0] = d[j][1] = 0.0;
+                dmma_s(d[j][0], d[j][1], l0, tb[t * G8_TS + 32 * wc + 8 * j + g]);
             }
 #pragma unroll
-            for (int c = G8_W - 1; c >= 0; --c) {
-                double s = w[c];
+            for (int j = 0; j < 4; ++j) dmma_s(d[j][0], d[j][1], l1, tb[(4 + t) * G8_TS + 32 * wc + 8 * j + g]);
 #pragma unroll
-                for (int i = c + 1; i < G8_W; ++i) s = fma(-gs.lu[c * G8_W + i], v[i], s);
-                v[c] = s * gs.rpiv[c];
+            for (int j = 0; j < 4; ++j)
+                *reinterpret_cast<double2 *>(&tw[g * G8_TS + 32 * wc + 8 * j + 2 * t]) = make_double2(d[j][0], d[j][1]);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                d[j][0] = d[j][1] = 0.0;
+                dmma_s(d[j][0], d[j][1], u0, tw[t * G8_TS + 32 * wc + 8 * j + g]);
             }
 #pragma unroll
-            for (int c = 0; c < G8_W; ++c) {
-                tb[c * G8_TS + tid] = w[c];
-                tv[c * G8_TS + tid] = v[c];
-            }
+            for (int j = 0; j < 4; ++j) dmma_s(d[j][0], d[j][1], u1, tw[(4 + t) * G8_TS + 32 * wc + 8 * j + g]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                *reinterpret_cast<double2 *>(&tv[g * G8_TS + 32 * wc + 8 * j + 2 * t]) = make_double2(d[j][0], d[j][1]);
         }
         nbar_sync(G8_BAR_U, G8_T);
+        if (warp == 0) G8_TL(b, 4);
         // A fragments: -(multipliers) for the rows outside the panel's pivots, 0 for those
         double pa[4][2];
         auto load_pa = [&]() {
@@ -880,12 +903,14 @@ FROB_DEV void gj128_sweep(double (&a)[4][4][2], int n, SweepShared<double, 128> 
         };
         auto upd = [&](auto jj) {
             constexpr int j = decltype(jj)::value;
-            const double t0 = tb[t * G8_TS + 32 * wc + 8 * j + g];
-            const double t1 = tb[(4 + t) * G8_TS + 32 * wc + 8 * j + g];
+            const double t0 = gs.tw[t * G8_TS + 32 * wc + 8 * j + g];
+            const double t1 = gs.tw[(4 + t) * G8_TS + 32 * wc + 8 * j + g];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dmma_s(a[i][j][0], a[i][j][1], pa[i][0], t0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dmma_s(a[i][j][0], a[i][j][1], pa[i][1], t1);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                dmma(a[i][j][0], a[i][j][1], pa[i][0], t0);
-                dmma(a[i][j][0], a[i][j][1], pa[i][1], t1);
                 if (slot[i] >= 0) {
                     const double2 v = *reinterpret_cast<const double2 *>(&tv[slot[i] * G8_TS + 32 * wc + 8 * j + 2 * t]);
                     a[i][j][0] = v.x;
@@ -900,10 +925,6 @@ FROB_DEV void gj128_sweep(double (&a)[4][4][2], int n, SweepShared<double, 128> 
             });
             hand_over(b1, j1);
         }
-        if (pw && b1 < NP) {
-            run_panel(b1);
-            load_pa();
-        }
         bstatic_for<4>([&](auto jj) {
             constexpr int j = decltype(jj)::value;
             if (!(bown && j == jb) && !(nown && j == j1)) upd(jj);
@@ -911,7 +932,7 @@ FROB_DEV void gj128_sweep(double (&a)[4][4][2], int n, SweepShared<double, 128> 
         if (bown) {
             // my rows of the swept panel, straight into the accumulators: X L11^-1 with X = -(multipliers)
             // for a non-pivot row and X = row c of U11^-1 for pivot row p_c (two DMMA per tile)
-            const double l0 = gs.linv[t * G8_W + g], l1 = gs.linv[(4 + t) * G8_W + g];
+            const double l0 = gs.linv[par][t * G8_W + g], l1 = gs.linv[par][(4 + t) * G8_W + g];
             const int ra = 32 * (warp >> 2);
 #pragma unroll
             for (int j = 0; j < 4; ++j)
@@ -920,14 +941,15 @@ FROB_DEV void gj128_sweep(double (&a)[4][4][2], int n, SweepShared<double, 128> 
                     for (int i = 0; i < 4; ++i) {
                         const int r = ra + 8 * i + g;  // the A-fragment row of this lane
                         const int sl = gs.rowslot[par][r];
-                        const double x0 = (sl >= 0) ? gs.uinv[sl * G8_W + t] : -pb[r * G8_PS + t];
-                        const double x1 = (sl >= 0) ? gs.uinv[sl * G8_W + 4 + t] : -pb[r * G8_PS + 4 + t];
+                        const double x0 = (sl >= 0) ? gs.uinv[par][sl * G8_W + t] : -pb[r * G8_PS + t];
+                        const double x1 = (sl >= 0) ? gs.uinv[par][sl * G8_W + 4 + t] : -pb[r * G8_PS + 4 + t];
                         a[i][j][0] = a[i][j][1] = 0.0;
-                        dmma(a[i][j][0], a[i][j][1], x0, l0);
-                        dmma(a[i][j][0], a[i][j][1], x1, l1);
+                        dmma_s(a[i][j][0], a[i][j][1], x0, l0);
+                        dmma_s(a[i][j][0], a[i][j][1], x1, l1);
                     }
                 }
         }
+        if (pw && b1 < NP) run_panel(b1);  // after my whole update b (its registers hold the panel meanwhile)
     }
     __syncthreads();
     sweep_finish<double, 128, G8_T>(sh, n, pmax, pmin);
