@@ -1,0 +1,14 @@
+import sys, torch
+sys.path.insert(0, ".")
+import paper_2208_01239_b200 as fb, synth
+lib = sys.argv[1]
+if lib != "default":
+    fb.frobinv.load(lib)
+z = torch.from_numpy(synth.batch(128, 4096, seed=0)).cuda().repeat(4, 1, 1).contiguous()
+for _ in range(2): fb.inv_batched(z)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(5): fb.inv_batched(z)
+e1.record(); torch.cuda.synchronize()
+print(lib, "%.2f ms" % (e0.elapsed_time(e1) / 5))
