@@ -567,6 +567,73 @@ frob_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__rest
     }
 }
 
+// ----------------------------------------------------------------- in-CTA GEMM, N = 128, staged operand
+// acc0 / acc1 (rows 0..63 / 64..127, the WT<128> warp tiling) = A B over K = 128.  The operand read
+// from L2 (A if STAGE_A, else B) goes through 16-wide k-slabs in shared memory (two buffers; the next
+// slab's four elements per thread are loaded into registers while the current slab is consumed);
+// the other one comes through `fo` (shared memory).  Replaces fragment loads straight from L2.
+constexpr int SLAB_K = 16, SLAB_AS = 20, SLAB_BS = 132;  // k per slab, A-slab / B-slab row strides
+constexpr int SLAB_DOUBLES = 2 * 128 * SLAB_AS;          // >= 2 * SLAB_K * SLAB_BS
+template <bool STAGE_A, typename FG, typename FO>
+FROB_DEV void cta_mma2_staged(FG fg, FO fo, double *slab, double (&acc0)[WT<128>::MT][WT<128>::NT][2],
+                              double (&acc1)[WT<128>::MT][WT<128>::NT][2]) {
+    using W = WT<128>;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm0 = (warp / W::WGN) * (W::MT * 8), wn0 = (warp % W::WGN) * (W::NT * 8);
+    constexpr int BUF = STAGE_A ? 128 * SLAB_AS : SLAB_K * SLAB_BS;
+#pragma unroll
+    for (int i = 0; i < W::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < W::NT; ++j) acc0[i][j][0] = acc0[i][j][1] = acc1[i][j][0] = acc1[i][j][1] = 0.0;
+    double v[4];
+    auto fetch = [&](int k0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = tid + 512 * q;
+            v[q] = STAGE_A ? fg(e >> 4, k0 + (e & 15)) : fg(k0 + (e >> 7), e & 127);
+        }
+    };
+    auto put = [&](double *buf) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = tid + 512 * q;
+            if (STAGE_A) buf[(e >> 4) * SLAB_AS + (e & 15)] = v[q];
+            else buf[(e >> 7) * SLAB_BS + (e & 127)] = v[q];
+        }
+    };
+    fetch(0);
+    put(slab);
+    __syncthreads();
+    for (int s = 0; s < 128 / SLAB_K; ++s) {
+        const double *cur = slab + (s & 1) * BUF;
+        if (s + 1 < 128 / SLAB_K) fetch((s + 1) * SLAB_K);
+#pragma unroll
+        for (int kk = 0; kk < SLAB_K; kk += 4) {
+            const int kg = s * SLAB_K + kk;
+            double a0[W::MT], a1[W::MT], b[W::NT];
+#pragma unroll
+            for (int i = 0; i < W::MT; ++i) {
+                const int r = wm0 + i * 8 + g;
+                a0[i] = STAGE_A ? cur[r * SLAB_AS + kk + t] : fo(r, kg + t);
+                a1[i] = STAGE_A ? cur[(64 + r) * SLAB_AS + kk + t] : fo(64 + r, kg + t);
+            }
+#pragma unroll
+            for (int j = 0; j < W::NT; ++j)
+                b[j] = STAGE_A ? fo(kg + t, wn0 + j * 8 + g) : cur[(kk + t) * SLAB_BS + wn0 + j * 8 + g];
+#pragma unroll
+            for (int i = 0; i < W::MT; ++i)
+#pragma unroll
+                for (int j = 0; j < W::NT; ++j) {
+                    dmma_s(acc0[i][j][0], acc0[i][j][1], a0[i], b[j]);
+                    dmma_s(acc1[i][j][0], acc1[i][j][1], a1[i], b[j]);
+                }
+        }
+        if (s + 1 < 128 / SLAB_K) put(slab + ((s + 1) & 1) * BUF);
+        __syncthreads();
+    }
+}
+
 // ----------------------------------------------------------------- Frobenius, 64 < n <= 128
 // 512 threads.  The two inversions by the blocked, warp-specialised Gauss-Jordan sweep below
 // (gj128_sweep); the three GEMMs by DMMA from shared / L1-resident operands (cta_mma_f).  One
@@ -625,7 +692,10 @@ struct G8Shared {
 struct Frob128Smem {
     double S[128 * 132];
     SweepShared<double, 128> sw;
-    G8Shared gs;
+    union {
+        G8Shared gs;                  // the sweeps
+        double slab[SLAB_DOUBLES];    // the GEMMs' staged operand
+    };
 };
 
 FROB_DEV void nbar_sync(int id, int cnt) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory"); }
@@ -1026,9 +1096,8 @@ frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
         auto Yv = [&](int i, int j) { return (i < n && j < n) ? sgn * zpart(Zd, n, yp, i, j) : 0.0; };
         double acc0[WT<N>::MT][WT<N>::NT][2], acc1[WT<N>::MT][WT<N>::NT][2];
         B128_TL(2);
-        // a3: C = X^{-1} Y (both 64-row halves in registers), then C -> S (X^{-1} is done) and -> Cg
-        cta_mma_f<N>([&](int r, int k) { return S[r * SS + k]; }, Yv, acc0, 0);
-        cta_mma_f<N>([&](int r, int k) { return S[r * SS + k]; }, Yv, acc1, 64);
+        // a3: C = X^{-1} Y (both 64-row halves in registers, Y staged), then C -> S (X^{-1} is done) and -> Cg
+        cta_mma2_staged<false>(Yv, [&](int r, int k) { return S[r * SS + k]; }, sm.slab, acc0, acc1);
         __syncthreads();
         auto put_c = [&](int i, int j, double v) {
             S[i * SS + j] = v;  // zero in the padding (Y is)
@@ -1038,9 +1107,8 @@ frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
         cta_mma_foreach<N>(acc1, put_c, 64);
         __syncthreads();
         B128_TL(3);
-        // a4: M = X + Y C with C from shared memory -> S
-        cta_mma_f<N>(Yv, [&](int k, int c) { return S[k * SS + c]; }, acc0, 0);
-        cta_mma_f<N>(Yv, [&](int k, int c) { return S[k * SS + c]; }, acc1, 64);
+        // a4: M = X + Y C with C from shared memory (Y staged) -> S
+        cta_mma2_staged<true>(Yv, [&](int k, int c) { return S[k * SS + c]; }, sm.slab, acc0, acc1);
         __syncthreads();
         auto put_m = [&](int i, int j, double v) {
             S[i * SS + j] = (i < n && j < n) ? zpart(Zd, n, xp, i, j) + v : 0.0;
@@ -1053,9 +1121,9 @@ frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
     }
     __syncthreads();
     B128_TL(5);
-    // a6/a7: Im = -C Re, interleaved store (after every warp has finished reading its C rows)
+    // a6/a7: Im = -C Re (C staged from the output buffer), interleaved store once every warp has read C
     {
-        double acc[WT<N>::MT][WT<N>::NT][2];
+        double acc0[WT<N>::MT][WT<N>::NT][2], acc1[WT<N>::MT][WT<N>::NT][2];
         const bool s1 = (use == 1);
         auto out = [&](int i, int j, double v) {
             if (i < n && j < n) {
@@ -1063,12 +1131,10 @@ frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
                 Xb[i * n + j] = s1 ? make_double2(re, -v) : make_double2(-v, -re);
             }
         };
-        for (int h = 0; h < 2; ++h) {
-            cta_mma_f<N>([&](int r, int k) { return (r < n && k < n) ? Cg[r * n + k] : 0.0; },
-                         [&](int k, int c) { return S[k * SS + c]; }, acc, 64 * h);
-            __syncthreads();
-            cta_mma_foreach<N>(acc, out, 64 * h);
-        }
+        cta_mma2_staged<true>([&](int r, int k) { return (r < n && k < n) ? Cg[r * n + k] : 0.0; },
+                              [&](int k, int c) { return S[k * SS + c]; }, sm.slab, acc0, acc1);
+        cta_mma_foreach<N>(acc0, out, 0);
+        cta_mma_foreach<N>(acc1, out, 64);
     }
     B128_TL(6);
     if (tid == 0) {
