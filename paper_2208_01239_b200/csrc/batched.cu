@@ -567,6 +567,228 @@ frob_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__rest
     }
 }
 
+// ----------------------------------------------------------------- Frobenius, n <= 32: one warp per matrix
+// Lane i holds row i of the matrix being inverted, so the pivot search of a column is a warp REDUX
+// (no block barrier) and the pivot row is the pivot lane's own registers (it scales the row and
+// publishes it through shared memory; no select trees).  The three GEMMs are 32 x 32 x 32 DMMA
+// products from shared memory.  Per warp: Y (sign applied) and W (X^{-1}, then C, then M, then Re)
+// in shared memory; C also in the second half of the output matrix for a6.
+#ifndef FROB_W32_WARPS
+#define FROB_W32_WARPS 4
+#endif
+constexpr int W32_WARPS = FROB_W32_WARPS;  // matrices per CTA (A/B build knob)
+constexpr int W32_S = 36;     // shared row stride (doubles)
+struct W32Smem {
+    double Y[32 * W32_S];
+    double W[32 * W32_S];
+    double rp[2][32];         // the scaled pivot row (by step parity)
+    int pivrow[32], pos[32];
+    double pmag[32];
+};
+
+// exchange-form Gauss-Jordan sweep on the rows in registers (lane = row), partial pivoting, first
+// maximum; on return row i holds inverse[pos[i]][pivrow[j]] = a[j].  Returns the LAPACK-style info
+// (reading R2) and the max abs row sum of the inverse (for R1').
+FROB_DEV int w32_sweep(double (&a)[32], int n, W32Smem &sm, double &nrm_inv) {
+    const int lane = threadIdx.x & 31;
+    bool used = false;
+    bstatic_for<32>([&](auto kk) {
+        constexpr int k = decltype(kk)::value;
+        const bool el = !used && ((lane < n) == (k < n));
+        const unsigned long long key = el ? pkey_bits(a[k]) : 0ull;
+        const unsigned hi = (unsigned)(key >> 32), lo32 = (unsigned)key;
+        const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo32 : 0u);
+        const int p = (int)__reduce_min_sync(0xffffffffu, (key != 0ull && hi == mh && lo32 == ml) ? (unsigned)lane : 0xffffffffu);
+        double *rp = sm.rp[k & 1];
+        if (lane == p) {
+            const double piv = a[k];
+            const double ip = (piv == 0.0) ? 0.0 : frcp(piv);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) a[j] = (j == k) ? ip : a[j] * ip;
+#pragma unroll
+            for (int h = 0; h < 16; ++h) *reinterpret_cast<double2 *>(&rp[2 * h]) = make_double2(a[2 * h], a[2 * h + 1]);
+            used = true;
+            sm.pivrow[k] = p;
+            sm.pmag[k] = fabs(piv);
+        }
+        __syncwarp();
+        if (lane != p) {
+            const double ck = a[k];
+            a[k] = 0.0;
+#pragma unroll
+            for (int h = 0; h < 16; ++h) {
+                const double2 r = *reinterpret_cast<const double2 *>(&rp[2 * h]);
+                a[2 * h] = fma(-ck, r.x, a[2 * h]);
+                a[2 * h + 1] = fma(-ck, r.y, a[2 * h + 1]);
+            }
+        }
+    });
+    __syncwarp();
+    sm.pos[sm.pivrow[lane]] = lane;
+    double rs = 0.0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) rs += fabs(a[j]);
+    double m = (lane < n) ? rs : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    nrm_inv = m;
+    // reading R2: first pivot column with |u_kk| < 100 n u max|u_ii| (or exactly 0)
+    double pm = (lane < n) ? sm.pmag[lane] : 0.0;
+    double pmax = pm;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pmax = fmax(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+    const double thr = 100.0 * n * 1.1102230246251565e-16 * pmax;
+    const bool bad = (lane < n) && (!(pm >= thr) || pm == 0.0);
+    const unsigned bm = __ballot_sync(0xffffffffu, bad);
+    __syncwarp();
+    return bm ? __ffs(bm) : 0;
+}
+
+// the sweep result (scrambled rows) -> M as the plain inverse
+FROB_DEV void w32_store(const double (&a)[32], const W32Smem &sm, double *M) {
+    const int lane = threadIdx.x & 31;
+    const int orow = sm.pos[lane];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) M[orow * W32_S + sm.pivrow[j]] = a[j];
+}
+
+// acc (16 tiles of 8 x 8: tile (i, j) rows 8 i + g, columns 8 j + 2 t + e) = A B over K = 32,
+// fragments through accessors
+template <typename FA, typename FB>
+FROB_DEV void w32_mma(FA fa, FB fb, double (&acc)[4][4][2]) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 2
+    for (int kk = 0; kk < 32; kk += 4) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) av[i] = fa(8 * i + g, kk + t);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bv[j] = fb(kk + t, 8 * j + g);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma_s(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+    }
+}
+
+template <typename F>
+FROB_DEV void w32_foreach(const double (&acc)[4][4][2], F f) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) f(8 * i + g, 8 * j + 2 * t + e, acc[i][j][e]);
+}
+
+__global__ void __launch_bounds__(32 * W32_WARPS)
+frob_batched32w_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__restrict__ X, long long sX, int n,
+                       int batch, int branch, int *__restrict__ info, unsigned char *__restrict__ bused) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int wid = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
+    const long long b = (long long)blockIdx.x * W32_WARPS + wid;
+    if (b >= batch) return;  // whole warps only (no block barrier in this kernel)
+    W32Smem &sm = reinterpret_cast<W32Smem *>(smem_raw)[wid];
+    const double *Zd = reinterpret_cast<const double *>(Z + b * sZ);
+    double2 *Xb = X + b * sX;
+    double *Cg = reinterpret_cast<double *>(Xb) + (long long)n * n;  // planar C scratch (second half)
+    auto part = [&](int p, int i, int j) { return (i < n && j < n) ? Zd[2 * (i * n + j) + p] : 0.0; };
+
+    int use = (branch == FROB_BRANCH_B) ? 2 : 1;
+    double a[32];
+    // row `lane` of X (identity padding) -> registers; row `lane` of Y (raw) -> shared
+    auto load_rows = [&](int xp) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            double2 z = make_double2(0.0, 0.0);
+            if (lane < n && j < n) z = reinterpret_cast<const double2 *>(Zd)[lane * n + j];
+            const double xv = xp == 0 ? z.x : z.y, yv = xp == 0 ? z.y : z.x;
+            a[j] = (lane < n && j < n) ? xv : (lane == j ? 1.0 : 0.0);
+            sm.Y[lane * W32_S + j] = yv;
+        }
+    };
+    auto row_norm = [&]() {  // ||X||_inf of the part in registers (rows < n)
+        double rs = 0.0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) rs += fabs(a[j]);
+        double m = (lane < n) ? rs : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        return m;
+    };
+    load_rows(use - 1);
+    double nx = row_norm(), ni;
+    int inf_x = w32_sweep(a, n, sm, ni);
+    w32_store(a, sm, sm.W);
+    if (branch == FROB_BRANCH_AUTO) {
+        // reading R1' (see frob_batched_kernel)
+        const double ka = inf_x ? INFINITY : nx * ni;
+        if (inf_x != 0 || !(ka <= kappa_switch(n))) {
+            // B into the registers (its rows), A kept aside in case B is not better
+#pragma unroll
+            for (int j = 0; j < 32; ++j) a[j] = (lane < n && j < n) ? sm.Y[lane * W32_S + j] : (lane == j ? 1.0 : 0.0);
+            const double nb = row_norm();
+            double nib;
+            const int inf_b = w32_sweep(a, n, sm, nib);
+            const double kb = inf_b ? INFINITY : nb * nib;
+            if (inf_b == 0 && (inf_x != 0 || kb < ka)) {
+                use = 2;
+                inf_x = 0;
+                w32_store(a, sm, sm.W);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) sm.Y[lane * W32_S + j] = part(0, lane, j);  // Y = (-)A
+            } else if (inf_b != 0 && inf_x != 0) {
+                inf_x = -1;  // both singular
+            }
+        }
+    }
+    __syncwarp();
+    const double sgn = (use == 1) ? 1.0 : -1.0;  // Y of Alg 1 (S2: Y = -A)
+    const int xp = use - 1;
+    double acc[4][4][2];
+    // a3: C = X^{-1} (sgn Y) -> W (X^{-1} is then done) and -> Cg
+    w32_mma([&](int r, int k) { return sm.W[r * W32_S + k]; }, [&](int k, int c) { return sm.Y[k * W32_S + c]; }, acc);
+    __syncwarp();
+    w32_foreach(acc, [&](int i, int j, double v) {
+        sm.W[i * W32_S + j] = sgn * v;
+        if (i < n && j < n) Cg[i * n + j] = sgn * v;
+    });
+    __syncwarp();
+    // a4: M = X + (sgn Y) C -> W
+    w32_mma([&](int r, int k) { return sm.Y[r * W32_S + k]; }, [&](int k, int c) { return sm.W[k * W32_S + c]; }, acc);
+    __syncwarp();
+    w32_foreach(acc, [&](int i, int j, double v) { sm.W[i * W32_S + j] = (i < n && j < n) ? fma(sgn, v, part(xp, i, j)) : 0.0; });
+    __syncwarp();
+    // a5: Re = M^{-1} -> W
+#pragma unroll
+    for (int j = 0; j < 32; ++j) a[j] = (lane < n && j < n) ? sm.W[lane * W32_S + j] : (lane == j ? 1.0 : 0.0);
+    double nm;
+    const int inf_m = w32_sweep(a, n, sm, nm);
+    w32_store(a, sm, sm.W);
+    __syncwarp();
+    // a6/a7: Im = -C Re, interleaved store
+    w32_mma([&](int r, int k) { return (r < n && k < n) ? Cg[r * n + k] : 0.0; },
+            [&](int k, int c) { return sm.W[k * W32_S + c]; }, acc);
+    __syncwarp();
+    w32_foreach(acc, [&](int i, int j, double v) {
+        if (i < n && j < n) {
+            const double re = sm.W[i * W32_S + j];
+            Xb[i * n + j] = (use == 1) ? make_double2(re, -v) : make_double2(-v, -re);
+        }
+    });
+    if (lane == 0) {
+        info[b] = (inf_x < 0) ? 1 : (inf_x ? inf_x : inf_m);
+        if (bused) bused[b] = (inf_x < 0) ? 0 : (unsigned char)use;
+    }
+}
+
 // ----------------------------------------------------------------- in-CTA GEMM, N = 128, staged operand
 // acc0 / acc1 (rows 0..63 / 64..127, the WT<128> warp tiling) = A B over K = 128.  The operand read
 // from L2 (A if STAGE_A, else B) goes through 16-wide k-slabs in shared memory (two buffers; the next
@@ -1405,12 +1627,12 @@ frob_status frob_inv_batched(int n, int batch, const double *Z, long long stride
     double2 *Xc = reinterpret_cast<double2 *>(X);
     cudaError_t e;
     if (n <= 32) {
-        const size_t smem = sizeof(FrobSmem<32>);
-        if ((e = set_smem(frob_batched_kernel<32>, smem)) != cudaSuccess) return FROB_ERR_CUDA;
+        const size_t smem = sizeof(W32Smem) * W32_WARPS;
+        if ((e = set_smem(frob_batched32w_kernel, smem)) != cudaSuccess) return FROB_ERR_CUDA;
         count_launch();
-        ProfScope ps("frob_batched<32>", s, 10.0 * n * (double)n * n * batch);
-        frob_batched_kernel<32><<<batch, BCfg<32>::THREADS, smem, s>>>(Zc, strideZ, Xc, strideX, n, branch,
-                                                                       d_info, d_branch_used);
+        ProfScope ps("frob_batched32w", s, 10.0 * n * (double)n * n * batch);
+        frob_batched32w_kernel<<<(batch + W32_WARPS - 1) / W32_WARPS, 32 * W32_WARPS, smem, s>>>(
+            Zc, strideZ, Xc, strideX, n, batch, branch, d_info, d_branch_used);
     } else if (n <= 64) {
         const size_t smem = sizeof(FrobSmem<64>);
         if ((e = set_smem(frob_batched_kernel<64>, smem)) != cudaSuccess) return FROB_ERR_CUDA;
