@@ -571,15 +571,15 @@ frob_batched_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__rest
 // Lane i holds row i of the matrix being inverted, so the pivot search of a column is a warp REDUX
 // (no block barrier) and the pivot row is the pivot lane's own registers (it scales the row and
 // publishes it through shared memory; no select trees).  The three GEMMs are 32 x 32 x 32 DMMA
-// products from shared memory.  Per warp: Y (sign applied) and W (X^{-1}, then C, then M, then Re)
-// in shared memory; C also in the second half of the output matrix for a6.
+// products.  Per warp only W (X^{-1}, then C, then M, then Re) lives in shared memory; the parts A, B
+// are read from L1 / L2 where a step needs them and C also goes to the second half of the output
+// matrix for a6 -- 10 KB of shared memory and <= 128 registers per warp, 16 warps per SM.
 #ifndef FROB_W32_WARPS
 #define FROB_W32_WARPS 4
 #endif
 constexpr int W32_WARPS = FROB_W32_WARPS;  // matrices per CTA (A/B build knob)
 constexpr int W32_S = 36;     // shared row stride (doubles)
 struct W32Smem {
-    double Y[32 * W32_S];
     double W[32 * W32_S];
     double rp[2][32];         // the scaled pivot row (by step parity)
     int pivrow[32], pos[32];
@@ -687,7 +687,7 @@ FROB_DEV void w32_foreach(const double (&acc)[4][4][2], F f) {
             for (int e = 0; e < 2; ++e) f(8 * i + g, 8 * j + 2 * t + e, acc[i][j][e]);
 }
 
-__global__ void __launch_bounds__(32 * W32_WARPS)
+__global__ void __launch_bounds__(32 * W32_WARPS, 16 / W32_WARPS)
 frob_batched32w_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__restrict__ X, long long sX, int n,
                        int batch, int branch, int *__restrict__ info, unsigned char *__restrict__ bused) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -703,16 +703,10 @@ frob_batched32w_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
 
     int use = (branch == FROB_BRANCH_B) ? 2 : 1;
     double a[32];
-    // row `lane` of X (identity padding) -> registers; row `lane` of Y (raw) -> shared
+    // row `lane` of part xp (identity padding) -> registers
     auto load_rows = [&](int xp) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            double2 z = make_double2(0.0, 0.0);
-            if (lane < n && j < n) z = reinterpret_cast<const double2 *>(Zd)[lane * n + j];
-            const double xv = xp == 0 ? z.x : z.y, yv = xp == 0 ? z.y : z.x;
-            a[j] = (lane < n && j < n) ? xv : (lane == j ? 1.0 : 0.0);
-            sm.Y[lane * W32_S + j] = yv;
-        }
+        for (int j = 0; j < 32; ++j) a[j] = (lane < n && j < n) ? Zd[2 * (lane * n + j) + xp] : (lane == j ? 1.0 : 0.0);
     };
     auto row_norm = [&]() {  // ||X||_inf of the part in registers (rows < n)
         double rs = 0.0;
@@ -731,9 +725,8 @@ frob_batched32w_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
         // reading R1' (see frob_batched_kernel)
         const double ka = inf_x ? INFINITY : nx * ni;
         if (inf_x != 0 || !(ka <= kappa_switch(n))) {
-            // B into the registers (its rows), A kept aside in case B is not better
-#pragma unroll
-            for (int j = 0; j < 32; ++j) a[j] = (lane < n && j < n) ? sm.Y[lane * W32_S + j] : (lane == j ? 1.0 : 0.0);
+            // B into the registers (its rows); A's inverse stays in W in case B is not better
+            load_rows(1);
             const double nb = row_norm();
             double nib;
             const int inf_b = w32_sweep(a, n, sm, nib);
@@ -742,8 +735,6 @@ frob_batched32w_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
                 use = 2;
                 inf_x = 0;
                 w32_store(a, sm, sm.W);
-#pragma unroll
-                for (int j = 0; j < 32; ++j) sm.Y[lane * W32_S + j] = part(0, lane, j);  // Y = (-)A
             } else if (inf_b != 0 && inf_x != 0) {
                 inf_x = -1;  // both singular
             }
@@ -751,10 +742,11 @@ frob_batched32w_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
     }
     __syncwarp();
     const double sgn = (use == 1) ? 1.0 : -1.0;  // Y of Alg 1 (S2: Y = -A)
-    const int xp = use - 1;
+    const int xp = use - 1, yp = 2 - use;
+    auto Yv = [&](int i, int j) { return part(yp, i, j); };  // raw Y; the sign goes on C
     double acc[4][4][2];
     // a3: C = X^{-1} (sgn Y) -> W (X^{-1} is then done) and -> Cg
-    w32_mma([&](int r, int k) { return sm.W[r * W32_S + k]; }, [&](int k, int c) { return sm.Y[k * W32_S + c]; }, acc);
+    w32_mma([&](int r, int k) { return sm.W[r * W32_S + k]; }, Yv, acc);
     __syncwarp();
     w32_foreach(acc, [&](int i, int j, double v) {
         sm.W[i * W32_S + j] = sgn * v;
@@ -762,7 +754,7 @@ frob_batched32w_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
     });
     __syncwarp();
     // a4: M = X + (sgn Y) C -> W
-    w32_mma([&](int r, int k) { return sm.Y[r * W32_S + k]; }, [&](int k, int c) { return sm.W[k * W32_S + c]; }, acc);
+    w32_mma(Yv, [&](int k, int c) { return sm.W[k * W32_S + c]; }, acc);
     __syncwarp();
     w32_foreach(acc, [&](int i, int j, double v) { sm.W[i * W32_S + j] = (i < n && j < n) ? fma(sgn, v, part(xp, i, j)) : 0.0; });
     __syncwarp();
