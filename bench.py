@@ -725,6 +725,20 @@ def run_extras(args, wl, fb, fbi, torch, dev, rank, timed, peak, peak_src, units
             "algorithmic": ("2 n^3 flop per launch (each of C = X^-1 Y, M = X + Y C, Im = -C Re is one n x n x n "
                             "GEMM launch)" if name.startswith("gemm_kernel<double> Frob") else
                             "the library's per-launch algorithmic flop count (DESIGN.md section 6)")}
+        if name.startswith("lu_panel2"):
+            # a pivot chain: report cycles per column against a latency floor built from the measured
+            # primitive latencies (3 x REDUX chain 72, dependent LDS 38,
+            # __syncthreads 36, DSMEM st.async + mbarrier round trip 519, DFMA 11, reciprocal 4 x DFMA)
+            cluster = name.startswith("lu_panel2c")
+            floor = 72 + (519 if cluster else 36) + 38 + 72 + 38 + 44 + 11
+            cyc = avg_ms * 1e-3 * 1.965e9 / 32  # one launch = one 32-column step, cycles at the 1965 MHz clock
+            extras["roofline"]["chain"] = {
+                "cycles_per_column": cyc, "floor_cycles_per_column": floor, "frac": floor / cyc,
+                "floor_basis": ("per column: warp argmax (3 dependent REDUX), " +
+                                ("DSMEM candidate push + mbarrier round trip" if cluster else "__syncthreads") +
+                                ", block argmax over the warp candidates (LDS + 3 REDUX), pivot-row read (LDS), "
+                                "reciprocal (4 dependent DFMA), next column's update (DFMA); measured primitive "
+                                "latencies, tools/lat_probe.cu / tools/dsmem_probe.cu")}
         extras["kernel_profile"] = {k: {"launches_per_step": v["launches"] / steps_prof,
                                         "ms_per_step": v["total_ms"] / steps_prof,
                                         "tflops": v["flops"] / (v["total_ms"] * 1e-3) / 1e12 if v["total_ms"] else None}
