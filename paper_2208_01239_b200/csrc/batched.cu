@@ -781,6 +781,82 @@ frob_batched32w_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
     }
 }
 
+// Complex comparator, n <= 32, in the same row-per-lane warp design (a like-for-like n = 32 comparison):
+// complex Gauss-Jordan (exchange form, partial pivoting on |re|+|im|, first maximum), lane i = row i.
+struct Z32Smem {
+    double2 rp[2][32];
+    int pivrow[32], pos[32];
+    double pmag[32];
+};
+#ifndef FROB_Z32_MINB
+#define FROB_Z32_MINB 3  // 3 CTAs per SM (168 registers, some spilling): 3.54 vs 3.89 ms at 1 (A/B: tools/abz32.py)
+#endif
+__global__ void __launch_bounds__(32 * W32_WARPS, FROB_Z32_MINB)
+zinv_batched32w_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__restrict__ X, long long sX, int n,
+                       int batch, int *__restrict__ info) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int wid = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
+    const long long b = (long long)blockIdx.x * W32_WARPS + wid;
+    if (b >= batch) return;
+    Z32Smem &sm = reinterpret_cast<Z32Smem *>(smem_raw)[wid];
+    const double2 *Zb = Z + b * sZ;
+    double2 *Xb = X + b * sX;
+    double2 a[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+        a[j] = (lane < n && j < n) ? Zb[lane * n + j] : make_double2(lane == j ? 1.0 : 0.0, 0.0);
+    bool used = false;
+    bstatic_for<32>([&](auto kk) {
+        constexpr int k = decltype(kk)::value;
+        const bool el = !used && ((lane < n) == (k < n));
+        const unsigned long long key = el ? pkey_bits(a[k]) : 0ull;
+        const unsigned hi = (unsigned)(key >> 32), lo32 = (unsigned)key;
+        const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo32 : 0u);
+        const int p = (int)__reduce_min_sync(0xffffffffu, (key != 0ull && hi == mh && lo32 == ml) ? (unsigned)lane : 0xffffffffu);
+        double2 *rp = sm.rp[k & 1];
+        if (lane == p) {
+            const double2 piv = a[k];
+            const double2 ip = is_zero(piv) ? make_double2(0.0, 0.0) : fast_recip(piv);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                a[j] = (j == k) ? ip : mul(a[j], ip);
+                rp[j] = a[j];
+            }
+            used = true;
+            sm.pivrow[k] = p;
+            sm.pmag[k] = pmag(piv);
+        }
+        __syncwarp();
+        if (lane != p) {
+            const double2 ck = a[k];
+            a[k] = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) a[j] = msub(a[j], ck, rp[j]);
+        }
+    });
+    __syncwarp();
+    sm.pos[sm.pivrow[lane]] = lane;
+    __syncwarp();
+    // reading R2 (as sweep_info): first pivot column with |u_kk| < 100 n u max|u_ii| (or exactly 0)
+    const double pm = (lane < n) ? sm.pmag[lane] : 0.0;
+    double pmax = pm;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pmax = fmax(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+    const double thr = 100.0 * n * 1.1102230246251565e-16 * pmax;
+    const unsigned bm = __ballot_sync(0xffffffffu, (lane < n) && (!(pm >= thr) || pm == 0.0));
+    const int orow = sm.pos[lane];
+    if (orow < n) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const int c = sm.pivrow[j];
+            if (c < n) Xb[orow * n + c] = a[j];
+        }
+    }
+    if (lane == 0) info[b] = bm ? __ffs(bm) : 0;
+}
+
 // ----------------------------------------------------------------- in-CTA GEMM, N = 128, staged operand
 // acc0 / acc1 (rows 0..63 / 64..127, the WT<128> warp tiling) = A B over K = 128.  The operand read
 // from L2 (A if STAGE_A, else B) goes through 16-wide k-slabs in shared memory (two buffers; the next
@@ -1674,11 +1750,12 @@ frob_status zinv_lu_batched(int n, int batch, const double *Z, long long strideZ
         return cudaGetLastError() == cudaSuccess ? FROB_OK : FROB_ERR_CUDA;
     }
     if (n <= 32) {
-        const size_t smem = sizeof(ZSmem<32>);
-        if ((e = set_smem(zinv_batched_kernel<32>, smem)) != cudaSuccess) return FROB_ERR_CUDA;
+        const size_t smem = sizeof(Z32Smem) * W32_WARPS;
+        if ((e = set_smem(zinv_batched32w_kernel, smem)) != cudaSuccess) return FROB_ERR_CUDA;
         count_launch();
-        ProfScope ps("zinv_batched<32>", s, 8.0 * n * (double)n * n * batch);
-        zinv_batched_kernel<32><<<batch, BCfg<32>::THREADS, smem, s>>>(Zc, strideZ, Xc, strideX, n, d_info);
+        ProfScope ps("zinv_batched32w", s, 8.0 * n * (double)n * n * batch);
+        zinv_batched32w_kernel<<<(batch + W32_WARPS - 1) / W32_WARPS, 32 * W32_WARPS, smem, s>>>(
+            Zc, strideZ, Xc, strideX, n, batch, d_info);
     } else {
         const size_t smem = sizeof(ZSmem<64>);
         if ((e = set_smem(zinv_batched_kernel<64>, smem)) != cudaSuccess) return FROB_ERR_CUDA;
