@@ -1285,6 +1285,17 @@ FROB_DEV void gj128_sweep(double (&a)[4][4][2], int n, SweepShared<double, 128> 
             });
             hand_over(b1, j1);
         }
+        // The panel warp factors panel b + 1 BEFORE the rest of its update b (off the chain: the
+        // others wait at FACT for that factor only).  Safe: W / V (tw, tv) of panel b are rewritten
+        // only after the first U barrier of b + 1, which the panel warp reaches after this update;
+        // pb / rowslot / linv / uinv of panel b (parity b & 1) only in panel b + 2.  The factor uses
+        // the accumulators as scratch (parked meanwhile), so pa and slot are read again afterwards.
+        if (pw && b1 < NP) {
+            run_panel(b1);
+            load_pa();
+#pragma unroll
+            for (int i = 0; i < 4; ++i) slot[i] = gs.rowslot[par][r0 + 8 * i];
+        }
         bstatic_for<4>([&](auto jj) {
             constexpr int j = decltype(jj)::value;
             if (!(bown && j == jb) && !(nown && j == j1)) upd(jj);
@@ -1309,7 +1320,6 @@ FROB_DEV void gj128_sweep(double (&a)[4][4][2], int n, SweepShared<double, 128> 
                     }
                 }
         }
-        if (pw && b1 < NP) run_panel(b1);  // after my whole update b (its registers hold the panel meanwhile)
     }
     __syncthreads();
     sweep_finish<double, 128, G8_T>(sh, n, pmax, pmin);
@@ -1346,6 +1356,9 @@ frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
         const int xpart = (pass == 0) ? use - 1 : 2 - use;  // the part swept in passes 0 / 1
         if (pass < 2) gj128_load(a, n, [&](int i, int j) { return zpart(Zd, n, xpart, i, j); });
         else gj128_load(a, n, [&](int i, int j) { return S[i * SS + j]; });
+        // ||part||_inf for the AUTO rule from the registers just loaded (park / pmag_k are free until
+        // the sweep): a few barriers instead of a serial, uncoalesced row-sum pass over global memory
+        const double nrm_part = (branch == FROB_BRANCH_AUTO && pass < 2) ? gj128_norm_inf(a, n, sm.gs.park, sm.sw.pmag_k) : 0.0;
         gj128_sweep(a, n, sm.sw, sm.gs, pmax, pmin);
         const int inf = sweep_info<double, N>(sm.sw, n, pmax);
         if (pass == 2) {
@@ -1358,8 +1371,7 @@ frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
             gj128_store(a, sm.sw, S, SS);
             B128_TL(1);
             if (branch == FROB_BRANCH_AUTO) {
-                const double na = mat_norm_inf(n, [&](int i, int j) { return zpart(Zd, n, 0, i, j); }, sm.sw.pmag_k, G8_T);
-                ka = inf_x ? INFINITY : na * gj128_norm_inf(a, n, sm.gs.park, sm.sw.pmag_k);
+                ka = inf_x ? INFINITY : nrm_part * gj128_norm_inf(a, n, sm.gs.park, sm.sw.pmag_k);
                 if (inf_x != 0 || !(ka <= kappa_switch(n))) {
                     __syncthreads();
                     pass = 1;
@@ -1368,8 +1380,7 @@ frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
             }
         } else {
             const int inf_b = inf;
-            const double nb = mat_norm_inf(n, [&](int i, int j) { return zpart(Zd, n, 1, i, j); }, sm.sw.pmag_k, G8_T);
-            const double kb = inf_b ? INFINITY : nb * gj128_norm_inf(a, n, sm.gs.park, sm.sw.pmag_k);
+            const double kb = inf_b ? INFINITY : nrm_part * gj128_norm_inf(a, n, sm.gs.park, sm.sw.pmag_k);
             if (inf_b == 0 && (inf_x != 0 || kb < ka)) {
                 use = 2;
                 inf_x = 0;
@@ -1382,8 +1393,11 @@ frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
         __syncthreads();
         // X = part use-1, Y = sgn * part 2-use (S2: Y = -A)
         const int xp = use - 1, yp = 2 - use;
-        const double sgn = (use == 1) ? 1.0 : -1.0;
-        auto Yv = [&](int i, int j) { return (i < n && j < n) ? sgn * zpart(Zd, n, yp, i, j) : 0.0; };
+        // sgn * v as a sign-bit flip (integer pipe, not the FP64 pipe the DMMAs issue to); same bits
+        const unsigned long long sbit = (use == 1) ? 0ull : 0x8000000000000000ull;
+        auto Yv = [&](int i, int j) {
+            return (i < n && j < n) ? __longlong_as_double(__double_as_longlong(zpart(Zd, n, yp, i, j)) ^ sbit) : 0.0;
+        };
         double acc0[WT<N>::MT][WT<N>::NT][2], acc1[WT<N>::MT][WT<N>::NT][2];
         B128_TL(2);
         // a3: C = X^{-1} Y (both 64-row halves in registers, Y staged), then C -> S (X^{-1} is done) and -> Cg
