@@ -864,18 +864,27 @@ zinv_batched32w_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
 // the other one comes through `fo` (shared memory).  Replaces fragment loads straight from L2.
 constexpr int SLAB_K = 16, SLAB_AS = 20, SLAB_BS = 132;  // k per slab, A-slab / B-slab row strides
 constexpr int SLAB_DOUBLES = 2 * 128 * SLAB_AS;          // >= 2 * SLAB_K * SLAB_BS
-template <bool STAGE_A, typename FG, typename FO>
+struct ZeroInit {
+    FROB_DEV double operator()(int, int) const { return 0.0; }
+};
+template <bool STAGE_A, typename FG, typename FO, typename FI = ZeroInit>
 FROB_DEV void cta_mma2_staged(FG fg, FO fo, double *slab, double (&acc0)[WT<128>::MT][WT<128>::NT][2],
-                              double (&acc1)[WT<128>::MT][WT<128>::NT][2]) {
+                              double (&acc1)[WT<128>::MT][WT<128>::NT][2], FI fi = FI()) {
     using W = WT<128>;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int wm0 = (warp / W::WGN) * (W::MT * 8), wn0 = (warp % W::WGN) * (W::NT * 8);
     constexpr int BUF = STAGE_A ? 128 * SLAB_AS : SLAB_K * SLAB_BS;
+    // accumulator (row, col) of element (i, j, e): (wm0 + 8 i + g [+ 64], wn0 + 8 j + 2 t + e)
 #pragma unroll
     for (int i = 0; i < W::MT; ++i)
 #pragma unroll
-        for (int j = 0; j < W::NT; ++j) acc0[i][j][0] = acc0[i][j][1] = acc1[i][j][0] = acc1[i][j][1] = 0.0;
+        for (int j = 0; j < W::NT; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                acc0[i][j][e] = fi(wm0 + i * 8 + g, wn0 + j * 8 + 2 * t + e);
+                acc1[i][j][e] = fi(64 + wm0 + i * 8 + g, wn0 + j * 8 + 2 * t + e);
+            }
     double v[4];
     auto fetch = [&](int k0) {
 #pragma unroll
@@ -1412,11 +1421,11 @@ frob_batched128_kernel(const double2 *__restrict__ Z, long long sZ, double2 *__r
         __syncthreads();
         B128_TL(3);
         // a4: M = X + Y C with C from shared memory (Y staged) -> S
-        cta_mma2_staged<true>(Yv, [&](int k, int c) { return S[k * SS + c]; }, sm.slab, acc0, acc1);
+        // (the accumulators start from X: its reads overlap the first slab's instead of the epilogue)
+        cta_mma2_staged<true>(Yv, [&](int k, int c) { return S[k * SS + c]; }, sm.slab, acc0, acc1,
+                              [&](int i, int j) { return (i < n && j < n) ? zpart(Zd, n, xp, i, j) : 0.0; });
         __syncthreads();
-        auto put_m = [&](int i, int j, double v) {
-            S[i * SS + j] = (i < n && j < n) ? zpart(Zd, n, xp, i, j) + v : 0.0;
-        };
+        auto put_m = [&](int i, int j, double v) { S[i * SS + j] = v; };  // 0 in the padding (X, Y are)
         cta_mma_foreach<N>(acc0, put_m, 0);
         cta_mma_foreach<N>(acc1, put_m, 64);
         __syncthreads();
